@@ -1,0 +1,368 @@
+"""Benchmark of the randomized block matmul hot path (arXiv 2105.04940) on B200.
+
+Default workload (BASELINE.json configs[1], "cfg2"): M 500x20000, N 20000x500
+fp64, N(0,1) x lognormal(0,1.5) per column/row, K=50 unequal blocks; one step =
+the configuration's sweep c in {10,20,40} blocks (W = 4000/8000/16000 columns)
+x {OPL, ONC, ONMCNR two-step with c0=500}: nine approximate products, each
+norm pass -> probabilities/sizes -> sampling -> gather/rescale -> C.D.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload cfg1|cfg2|cfg3]
+
+value  = approx-product time per step (ms), device-timed with CUDA events,
+         inputs resident in HBM, L2 flushed (256 MB write) before every step.
+e2e    = the same step through the public API with the inputs copied from
+         pinned host memory and the nine C.D results read back, every step.
+--impl reference times the CPU port of the reference (oracle/, kind "port")
+on the host cores for the same workload.
+Under torchrun each rank runs an independent replica (the sweep does not
+shard; "replicas only"); value is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import workloads  # noqa: E402
+
+METRIC = "approx-product time, norm-pass HBM GB/s, GEMM TC util; rel. Frobenius err"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3"])
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- workloads
+
+def workload_spec(name):
+    """(cfg index, data builder, list of (c_blocks, W, method, c0))."""
+    if name == "cfg1":
+        return 1, workloads.cfg1, [(20, 2000, m, 0) for m in ("OPL", "ONC", "UU")]
+    if name == "cfg2":
+        return 2, workloads.cfg2, [(cb, W, m, 500) for cb, W in zip((10, 20, 40), (4000, 8000, 16000))
+                                   for m in ("OPL", "ONC", "ONMCNR")]
+    if name == "cfg3":
+        return 3, workloads.cfg3, [(200, 20000, "ONU", 5000)]
+    raise ValueError(name)
+
+
+def algorithmic(m, n, p, runs):
+    norm_bytes = 8 * (m * n + n * p)
+    gemm_flops = [2.0 * m * p * W for _, W, _, _ in runs]
+    return norm_bytes, gemm_flops
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    def __init__(self, index=0):
+        self.samples, self.proc, self.index = [], None, index
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- reference arm
+
+def cpu_step(M, N, sizes, runs, cfg):
+    from oracle import blockmm_oracle as O
+    t0 = time.perf_counter()
+    for cb, W, meth, c0 in runs:
+        O.approx_product(M, N, sizes, W, meth, workloads.sample_rng(cfg, cb), c0=c0)
+    return (time.perf_counter() - t0) * 1e3
+
+
+def cpu_cores():
+    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS"):
+        if os.environ.get(var):
+            return int(os.environ[var])
+    return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg, build, runs = workload_spec(args.workload)
+    M, N, sizes = build()
+    for _ in range(args.warmup):
+        cpu_step(M, N, sizes, runs, cfg)
+    times = [cpu_step(M, N, sizes, runs, cfg) for _ in range(args.steps)]
+    v = float(np.mean(times))
+    sample = f"{args.workload}: full step ({len(runs)} approx products), mean of {args.steps}"
+    line = {
+        "metric": METRIC, "value": v, "unit": "ms/step", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8(d))",
+        "config": {"workload": args.workload, "runs": [f"{m}@W={W}" for _, W, m, _ in runs]},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": "ms/step", "cores": cpu_cores(), "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+
+def measure_dgemm_peak(torch):
+    """cuBLAS float64 GEMM 8192^3 (best of 5): the measured FP64 tensor ceiling."""
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    torch.matmul(a, b)
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2105_04940_b200 as bm
+    from paper_2105_04940_b200 import _lib
+    from paper_2105_04940_b200.pipeline import SketchPipeline, seeds_from_rngs
+
+    cfg, build, runs = workload_spec(args.workload)
+    M_h, N_h, sizes = build()
+    m, n = M_h.shape
+    p = N_h.shape[1]
+    K = len(sizes)
+    Md = torch.as_tensor(M_h, device="cuda")
+    Nd = torch.as_tensor(N_h, device="cuda")
+    pipes = [SketchPipeline(m, n, p, sizes, W, meth, c0=c0) for _, W, meth, c0 in runs]
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(Mx, Nx, gemm_events=None):
+        outs = []
+        for (cb, W, meth, c0), pipe in zip(runs, pipes):
+            rng = workloads.sample_rng(cfg, cb)
+            seeds = seeds_from_rngs(meth, [rng], K)
+            if gemm_events is not None:
+                pipe.gemm_events = gemm_events
+            outs.append(pipe.run(Mx, Nx, seeds))
+        return outs
+
+    # correctness of the bench configuration itself (untimed)
+    for pipe_out, pipe in zip(step(Md, Nd), pipes):
+        pipe.check()
+    for _ in range(args.warmup):
+        step(Md, Nd)
+    torch.cuda.synchronize()
+
+    # ---- device-timed steps (inputs resident, L2 flushed before each step)
+    n_launch0 = _lib.launches()
+    times = []
+    gemm_ev = []
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(Md, Nd, gemm_ev)
+            e1.record(stream)
+            times.append((e0, e1))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = (_lib.launches() - n_launch0) // args.steps
+    ms = [a.elapsed_time(b) for a, b in times]
+    ms_step = float(np.mean(ms))
+    if world > 1:
+        t = torch.tensor([ms_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+
+    # ---- e2e through the public API with host buffers (pinned) every step
+    M_pin = torch.from_numpy(M_h).pin_memory()
+    N_pin = torch.from_numpy(N_h).pin_memory()
+    Mx = torch.empty_like(Md)
+    Nx = torch.empty_like(Nd)
+    outs_h = [torch.empty((m, p), dtype=torch.float64).pin_memory() for _ in runs]
+    e2e = []
+    for it in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Mx.copy_(M_pin, non_blocking=True)
+        Nx.copy_(N_pin, non_blocking=True)
+        outs = step(Mx, Nx)
+        for o, h in zip(outs, outs_h):
+            h.copy_(o, non_blocking=True)
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            e2e.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = float(np.mean(e2e))
+    h2d = M_h.nbytes + N_h.nbytes
+    d2h = len(runs) * m * p * 8
+
+    # ---- roofline of the dominant kernels, timed live (events around their launches)
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peak.get("hbm_gbs", 6650.0))
+    norm_bytes, gemm_flops = algorithmic(m, n, p, runs)
+    kt = kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush)
+    dgemm_peak = measure_dgemm_peak(torch)
+    gemm_ms = kt["gemm_ms"]
+    gemm_achieved = sum(gemm_flops) / (sum(gemm_ms) * 1e-3) / 1e12
+    norms_achieved = norm_bytes / (kt["norms_ms"] * 1e-3) / 1e9
+
+    # errors of the W=16000 ONC product vs the exact product (verification, untimed)
+    from paper_2105_04940_b200.analysis import sq_diff
+    exact = bm.multiply_exact(Md, Nd)
+    idx = [i for i, r in enumerate(runs) if r[2] == "ONC"][-1]
+    CD = pipes[idx].run(Md, Nd, seeds_from_rngs("ONC", [workloads.sample_rng(cfg, runs[idx][0])], K))
+    err_sq, ref_sq = sq_diff(exact, CD)
+    fro_m = np.linalg.norm(M_h)
+    fro_n = np.linalg.norm(N_h)
+
+    line = {
+        "metric": METRIC, "value": ms_step, "unit": "ms/step", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8(d))",
+        "config": {"workload": args.workload, "m": m, "n": n, "p": p, "K": K,
+                   "runs": [f"{meth}@W={W}" for _, W, meth, _ in runs], "l2": "flushed (256 MB write) before each step",
+                   "parallelism": f"replicas x{world}"},
+        "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "kernel": "gemm_f64_kernel (C.D, DMMA)", "achieved": gemm_achieved,
+                     "peak": dgemm_peak, "unit": "TFLOP/s", "frac": gemm_achieved / dgemm_peak,
+                     "peak_source": "cuBLAS dgemm 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
+                     "traffic": None},
+        "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norms_achieved,
+                           "peak": hbm_peak, "unit": "GB/s", "frac": norms_achieved / hbm_peak,
+                           "algorithmic_bytes": norm_bytes},
+        "kernel_ms": {k: v for k, v in kt.items() if k != "gemm_ms"} | {"gemm_ms": gemm_ms},
+        "rel_err_baseline_metric": float(np.sqrt(err_sq) / (fro_m * fro_n)),
+        "rel_err_reference_metric": float(np.sqrt(err_sq / ref_sq)),
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        line["cpu_baseline"] = cpu_baseline(M_h, N_h, sizes, runs, cfg, args)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
+    """Per-kernel device times with CUDA events on the launching stream."""
+    from paper_2105_04940_b200 import _lib
+    from paper_2105_04940_b200.pipeline import seeds_from_rngs
+    st = _lib.stream_ptr()
+    lib = _lib.load()
+    out = {"gemm_ms": []}
+    m, n = Md.shape
+    p = Nd.shape[1]
+    # norm pass alone (L2 flushed first)
+    pipe = pipes[0]
+    reps = []
+    for _ in range(5):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.bmm_norms(0, Md.data_ptr(), m, n, n, 0, Nd.data_ptr(), p, p, 0, 1, 0, pipe.colsq.data_ptr(),
+                      pipe.rowsq.data_ptr(), st)
+        e1.record()
+        torch.cuda.synchronize()
+        reps.append(e0.elapsed_time(e1))
+    out["norms_ms"] = float(np.median(reps))
+    # the sampled GEMM of each run (C, D already gathered by the last step)
+    for (cb, W, meth, c0), pipe in zip(runs, pipes):
+        reps = []
+        for _ in range(5):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            lib.bmm_gemm_f64(pipe.C.data_ptr(), W, m * W, pipe.D.data_ptr(), p, W * p, m, p, W, 1,
+                             pipe.CD.data_ptr(), p, m * p, pipe.ws_gemm.data_ptr(), pipe.ws_gemm.numel(), st)
+            e1.record()
+            torch.cuda.synchronize()
+            reps.append(e0.elapsed_time(e1))
+        out["gemm_ms"].append(float(np.median(reps)))
+    return out
+
+
+def cpu_baseline(M, N, sizes, runs, cfg, args):
+    t = cpu_step(M, N, sizes, runs, cfg)
+    return {"value": t, "unit": "ms/step", "cores": cpu_cores(), "kind": "port",
+            "sample": f"{args.workload}: one full step ({len(runs)} approx products) with oracle/blockmm_oracle.py "
+                      f"(NumPy + OpenBLAS, {cpu_cores()} BLAS threads)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,224 @@
+/*
+ * blockmm_b200.h -- C ABI of the B200-native randomized block matrix
+ * multiplication hot path (arXiv 2105.04940).
+ *
+ * The reference (/root/reference/pkg/src/blockmm) is pure Python/NumPy and has
+ * no FFI layer; its drop-in boundary is the Python API re-exported from
+ * pkg/src/blockmm/__init__.py:10-99.  Each entry point below replaces the
+ * NumPy/BLAS computation inside one reference function (cited per entry);
+ * the Python package paper_2105_04940_b200 binds them with ctypes and keeps
+ * the reference's names, arguments, return types and ValueError behaviour.
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer unless named host_*;
+ *   - matrices are row-major with an explicit leading dimension (elements);
+ *   - batched entry points take `batch` problems of identical shape, problem
+ *     b starting at base + b * stride (elements);
+ *   - `stream` is a cudaStream_t passed as void*; all work is enqueued on it
+ *     and nothing synchronises the host unless stated;
+ *   - returns BMM_OK (0) or a negative BMM_E_* code; bmm_last_error() gives a
+ *     thread-local message for the last failure.
+ *   - per-problem validation outcomes that the reference reports as
+ *     ValueError/AssertionError are written to a device `status` array (see
+ *     BMM_ST_*), because they depend on device-computed values.
+ */
+#ifndef BLOCKMM_B200_H
+#define BLOCKMM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element types */
+#define BMM_F64 0
+#define BMM_F32 1
+
+/* return codes */
+#define BMM_OK 0
+#define BMM_E_ARG (-1)
+#define BMM_E_CUDA (-2)
+#define BMM_E_UNSUPPORTED (-3)
+
+/* per-problem device status codes (reference error it stands for) */
+#define BMM_ST_OK 0
+#define BMM_ST_ZERO_SCORE 1        /* plan.py:390-391,410-411,453-454 "all blocks have zero score" */
+#define BMM_ST_CAUCHY_SCHWARZ 2    /* plan.py:119-120 BlockScores check                             */
+#define BMM_ST_RADICAND 3          /* plan.py:358-360 radicand negative beyond slack               */
+#define BMM_ST_ALL_ZERO_WEIGHT 4   /* plan.py:267-268 "all weights are zero"                        */
+#define BMM_ST_BAD_WEIGHT 5        /* plan.py:265-266 weights must be finite and >= 0              */
+#define BMM_ST_CAP_BELOW_FLOOR 6   /* plan.py:285-286                                               */
+#define BMM_ST_BELOW_FLOORS 7      /* plan.py:287-288 (diag = number of floors)                     */
+#define BMM_ST_ABOVE_CAPS 8        /* plan.py:289-290 (diag = total caps)                           */
+#define BMM_ST_NO_CONVERGE 9       /* plan.py:306,321,347 AssertionError                            */
+#define BMM_ST_NOT_PLACED 10       /* plan.py:342 AssertionError                                    */
+#define BMM_ST_EMPTY_SUPPORT 11    /* estimators.py:39-40                                           */
+
+/* budget rules for bmm_budgets (plan.py allocators) */
+#define BMM_RULE_EXPLICIT 0   /* integerize(weights, c, caps, floor)          plan.py:242-347 */
+#define BMM_RULE_ONC 1        /* allocate_by_score_sums: w = s                plan.py:403-413 */
+#define BMM_RULE_OPL 2        /* allocate_optimal: w = sqrt(max(s^2-g^2,0))   plan.py:383-400 */
+#define BMM_RULE_TWO_STEP 3   /* allocate_two_step: w = sqrt(|s^2-pilot^2|)   plan.py:465-470 */
+#define BMM_RULE_UU 4         /* allocate_uniform: w = 1, floor all           plan.py:416-421 */
+#define BMM_RULE_PILOT 5      /* two-step pilot: c draws per block with p0 != 0 (s > 0, or every
+                                 block when s is NULL)        plan.py:447,457-460 */
+
+/* ---------------------------------------------------------------- library */
+int bmm_version(void);
+const char* bmm_last_error(void);
+/* number of kernels this library has launched since load (evidence counter) */
+int64_t bmm_launch_count(void);
+
+/* ---------------------------------------------------------------- K1 norms
+ * colsq[b, i] = sum_h M[b][h, i]^2, accumulated sequentially over h in float64
+ * (numpy's order for np.linalg.norm(M, axis=0) on a C-ordered matrix,
+ * matrix.py:107-109).  With accumulate != 0 the chain continues from the
+ * values already in colsq (exact row-slab chunking).
+ * rowsq[b, i] = numpy-pairwise sum over f of N[b][i, f]^2 in float64
+ * (np.linalg.norm(N, axis=1), matrix.py:112-114).
+ * Either side may be skipped by passing a NULL matrix pointer.
+ * float32 inputs are upcast element-wise (exact squares), which equals the
+ * reference run on the float64-upcast matrices.                            */
+int bmm_norms(int dtype,
+              const void* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
+              const void* N, int64_t p, int64_t ldn, int64_t strideN,
+              int64_t batch, int accumulate,
+              double* colsq, double* rowsq, void* stream);
+
+/* ---------------------------------------------------------------- K2 plan
+ * Per block k (offsets[0..K], shared by all problems):
+ *   sc[i]   = sqrt(colsq[i]) * sqrt(rowsq[i])                     plan.py:165-167
+ *   probs   = optimal_probabilities: sc/pw(sc) then p/pw(p),
+ *             all-zero vector for a zero-score block              plan.py:192-206
+ *   s[k]    = sc[o] + pw(sc[o+1:e])  (np.add.reduceat)            plan.py:170-173
+ *   fnorm[k]= ||M^k||_F * ||N_k||_F (SSM block weights)            plan.py:483-492
+ * probs / s / fnorm may be NULL to skip.  colsq/rowsq stride = n, s/fnorm
+ * stride = K, probs stride = n.                                           */
+int bmm_block_probs(const double* colsq, const double* rowsq, int64_t n,
+                    const int64_t* offsets, int64_t K, int64_t batch,
+                    double* probs, double* s, double* fnorm, void* stream);
+
+/* SSM block probabilities q = f / pw(f) (plan.py:493-496); status gets
+ * BMM_ST_ZERO_SCORE when pw(f) == 0.                                        */
+int bmm_normalize(const double* f, int64_t K, int64_t batch, double* q,
+                  int32_t* status, void* stream);
+
+/* Integer budgets (plan.py:242-347 integerize, with the weights/caps/floors
+ * of the allocator named by `rule`).
+ *   s      : score sums (K per problem; unused for UU / EXPLICIT)
+ *   aux    : squared norms g_k^2 (OPL) / pilot^2 (TWO_STEP), as the segmented
+ *            square-sum GEMM returns them (the kernel takes sqrt and squares
+ *            again, the reference's rounding path); weights (EXPLICIT)
+ *   sizes  : block sizes n_k (K, shared)
+ *   caps   : EXPLICIT only, optional explicit caps (K per problem) or NULL
+ *   floors : EXPLICIT only, optional uint8 floor mask (K per problem) or NULL
+ *   c      : budget per problem (batch entries)
+ *   cap    : allocator `cap` flag
+ *   budgets: out, int64 K per problem;  col_off: out, K+1 per problem (may be NULL)
+ *   status, diag: out, one per problem;  notes: out, 1 if the weights fell
+ *            back to the score sums (plan.py:394-398, 467-469)
+ *   ws     : workspace of bmm_budgets_workspace(K) bytes per problem        */
+int64_t bmm_budgets_workspace(int64_t K);
+int bmm_budgets(int rule, const double* s, const double* aux, const int64_t* sizes,
+                const int64_t* caps, const uint8_t* floors,
+                int64_t K, int64_t batch, const int64_t* c, int cap,
+                int64_t* budgets, int64_t* col_off, int32_t* status, int64_t* diag,
+                int32_t* notes, void* ws, void* stream);
+
+/* ---------------------------------------------------------------- K3 sampler
+ * Per-block inverse-CDF tables: cum = np.cumsum(p) (sequential) and the last
+ * index with p > 0 (estimators.py:37-38).  len = offsets[K] per problem.     */
+int bmm_block_cdf(const double* probs, const int64_t* offsets, int64_t K, int64_t batch,
+                  int64_t n, double* cum, int64_t* last_support, void* stream);
+
+/* numpy SeedSequence -> PCG64 seeding of child streams:
+ *   child j of problem b is SeedSequence(entropy, spawn_key = key + (first_child[b]+j,))
+ * words[b, 0..n_words) holds the uint32 assembled entropy *before* the child
+ * index (run entropy zero-padded to >= 4 words, then the parent spawn key
+ * words).  states[b, j] = {state_hi, state_lo, inc_hi, inc_lo}.
+ * Replaces rng.spawn(K) at estimators.py:141,207 and plan.py:456.            */
+int bmm_seed_streams(const uint32_t* words, int64_t n_words, const int64_t* first_child,
+                     int64_t count, int64_t batch, uint64_t* states, void* stream);
+
+/* Draw budgets[k] indices per block from child stream k (estimators.py:34-44,
+ * 77-78): u = (next64 >> 11) * 2^-53, idx = min(upper_bound(cum, u), last),
+ * scale = 1/sqrt(c_k * p[idx]).  Outputs are indexed by the global sketch
+ * column t = col_off[k] + draw:  column[t] = offsets[k] + idx (global inner
+ * index), prob[t] = p[idx], scale[t].  W = col_off[K] per problem; outputs
+ * have stride w_stride.  `states` has one stream per block (stride K).
+ * The SSM baseline (estimators.py:242-243) is the same call with one block
+ * spanning the K block probabilities and the caller's own PCG64 state.    */
+int bmm_sample(const double* probs, const double* cum, const int64_t* last_support,
+               const int64_t* offsets, int64_t K, int64_t batch, int64_t n,
+               const int64_t* budgets, const int64_t* col_off, int64_t w_stride,
+               const uint64_t* states, int64_t* column, double* prob, double* scale,
+               void* stream);
+
+/* ---------------------------------------------------------------- K4 gather
+ * C[h, t] = M[h, column[t]] * scale[t]        (m x W, ldc)     estimators.py:79
+ * D[t, f] = N[column[t], f] * scale[t]        (W x p, ldd)     estimators.py:80
+ * The product is formed in float64 and rounded once to out_dtype: with
+ * float64 output this is bit-identical to NumPy on float64 (or upcast float32)
+ * inputs.
+ * Either side may be skipped with a NULL output.                            */
+int bmm_gather(int dtype, int out_dtype,
+               const void* M, int64_t ldm, int64_t strideM,
+               const void* N, int64_t ldn, int64_t strideN,
+               int64_t m, int64_t p, const int64_t* column, const double* scale,
+               int64_t W, int64_t w_stride, int64_t batch,
+               void* C, int64_t ldc, int64_t strideC,
+               void* D, int64_t ldd, int64_t strideD, void* stream);
+
+/* SSM whole-block gather (estimators.py:244-249): draw t copies block
+ * blocks[t] scaled by scale[t]; the sketch columns of draw t start at
+ * sk_off[t] (prefix of the drawn widths).                                   */
+int bmm_gather_blocks(int dtype,
+                      const void* M, int64_t ldm, const void* N, int64_t ldn,
+                      int64_t m, int64_t p, const int64_t* offsets,
+                      const int64_t* blocks, const double* scale, const int64_t* sk_off,
+                      int64_t draws, int64_t W,
+                      void* C, int64_t ldc, void* D, int64_t ldd, void* stream);
+
+/* ---------------------------------------------------------------- K5/K8 GEMM fp64
+ * out[b] = A[b] (m x k, lda) @ B[b] (k x nc, ldb), float64 on the DMMA
+ * tensor pipe (mma.sync m8n8k4 f64), split-K with a fixed-order reduction
+ * (deterministic).  Used for C @ D (estimators.py:175,253) and the exact
+ * product M @ N (matrix.py:98-104).  ws: bmm_gemm_f64_workspace bytes.    */
+int64_t bmm_gemm_f64_workspace(int64_t m, int64_t nc, int64_t k, int64_t batch);
+int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA,
+                 const double* B, int64_t ldb, int64_t strideB,
+                 int64_t m, int64_t nc, int64_t k, int64_t batch,
+                 double* out, int64_t ldo, int64_t strideO,
+                 void* ws, int64_t ws_bytes, void* stream);
+
+/* Segmented square-sum GEMM: gsq[b, j] = || A[:, seg_j] @ B[seg_j, :] ||_F^2
+ * for segments seg_j = [seg[j], seg[j+1]) of the inner dimension.
+ * OPL block product norms g_k^2 (plan.py:183-188) with seg = offsets, and
+ * two-step pilot norms ||C0 D0||_F^2 (plan.py:457-464) with seg = pilot
+ * sketch offsets.  Deterministic (per-tile partials reduced in order).    */
+int64_t bmm_segsq_f64_workspace(int64_t m, int64_t nc, int64_t nseg, int64_t batch);
+int bmm_segsq_f64(const double* A, int64_t lda, int64_t strideA,
+                  const double* B, int64_t ldb, int64_t strideB,
+                  int64_t m, int64_t nc, const int64_t* seg, int64_t nseg, int64_t seg_stride,
+                  int64_t batch, double* gsq, void* ws, int64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- K9 error
+ * err[b] = { sum (X - Y)^2, sum X^2 } over m x nc (X = exact MN, Y = C D),
+ * float64 accumulation, deterministic two-level reduction.  X, Y may be
+ * float64 (dtype F64) or float32 (dtype F32).  analysis.py:318-325.        */
+int64_t bmm_sqdiff_workspace(int64_t m, int64_t nc, int64_t batch);
+int bmm_sqdiff(int dtype, const void* X, int64_t ldx, int64_t strideX,
+               const void* Y, int64_t ldy, int64_t strideY,
+               int64_t m, int64_t nc, int64_t batch, double* err,
+               void* ws, int64_t ws_bytes, void* stream);
+
+/* sum of a float64 vector segment in numpy pairwise order: out[b] = 0 + pw(x[b, 0:len])
+ * (used for ||M||_F^2 = pw(colsq), ||N||_F^2 = pw(rowsq)).                */
+int bmm_pairwise_sum(const double* x, int64_t len, int64_t stride, int64_t batch,
+                     double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLOCKMM_B200_H */

@@ -1,0 +1,442 @@
+// K5 / K7 / K8 / K9 -- float64 contractions on the DMMA tensor pipe.
+//
+// sm_100a has no tcgen05 float64 kind, so float64 GEMMs use the warp-level
+// DMMA path (mma.sync.m8n8k4.f64 -> DMMA.8x8x4).  CTA tile 64x64x16, four
+// warps of 32x32, a 4-stage cp.async ring, padded shared-memory rows so the
+// A/B fragment loads are bank-conflict free per half-warp.
+//
+// Reference call sites replaced:
+//   C @ D                     estimators.py:175, 253
+//   M @ N (exact product)     matrix.py:98-104
+//   ||M^k @ N_k||_F^2         plan.py:183-188   (segmented square-sum mode)
+//   ||C0 @ D0||_F^2 (pilot)   plan.py:463-464   (segmented square-sum mode)
+//   ||exact - approx||_F^2    analysis.py:318-325 (bmm_sqdiff)
+// Split-K partials and per-tile square-sums are reduced in a fixed order, so
+// every result is run-to-run deterministic.
+#include "common.cuh"
+
+namespace bmm {
+
+constexpr int GB_M = 64, GB_N = 64, GB_K = 16, G_STAGES = 4, G_THREADS = 128;
+constexpr int A_STR = GB_K + 4;   // doubles per A smem row
+constexpr int B_STR = GB_N + 4;   // doubles per B smem row
+constexpr int A_TILE = GB_M * A_STR;
+constexpr int B_TILE = GB_K * B_STR;
+constexpr int G_SMEM_BYTES = G_STAGES * (A_TILE + B_TILE) * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+struct TileArgs {
+  const double* A; int64_t lda;
+  const double* B; int64_t ldb;
+  int64_t m, nc;      // rows of A, columns of B
+  int64_t m0, n0;     // tile origin
+};
+
+// Stage one BK slice [k0, k0+BK) of the A and B tiles; columns at or beyond kend are zero.
+template <bool V16>
+__device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64_t kend, double* as, double* bs) {
+  const int tid = threadIdx.x;
+  if constexpr (V16) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = tid + G_THREADS * q;
+      const int row = c >> 3, kc = (c & 7) * 2;
+      const int64_t gr = ta.m0 + row, gk = k0 + kc;
+      int64_t nv = kend - gk;
+      nv = nv < 0 ? 0 : (nv > 2 ? 2 : nv);
+      if (gr >= ta.m) nv = 0;
+      const double* src = nv ? ta.A + gr * ta.lda + gk : ta.A;
+      cp_async16(smem_u32(as + row * A_STR + kc), src, (int)(nv * 8));
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = tid + G_THREADS * q;
+      const int row = c >> 5, nc2 = (c & 31) * 2;
+      const int64_t gk = k0 + row, gn = ta.n0 + nc2;
+      int64_t nv = ta.nc - gn;
+      nv = nv < 0 ? 0 : (nv > 2 ? 2 : nv);
+      if (gk >= kend) nv = 0;
+      const double* src = nv ? ta.B + gk * ta.ldb + gn : ta.B;
+      cp_async16(smem_u32(bs + row * B_STR + nc2), src, (int)(nv * 8));
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = tid + G_THREADS * q;
+      const int row = c >> 4, kk = c & 15;
+      const int64_t gr = ta.m0 + row, gk = k0 + kk;
+      const bool ok = gr < ta.m && gk < kend;
+      cp_async8(smem_u32(as + row * A_STR + kk), ok ? ta.A + gr * ta.lda + gk : ta.A, ok ? 8 : 0);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = tid + G_THREADS * q;
+      const int row = c >> 6, nn = c & 63;
+      const int64_t gk = k0 + row, gn = ta.n0 + nn;
+      const bool ok = gk < kend && gn < ta.nc;
+      cp_async8(smem_u32(bs + row * B_STR + nn), ok ? ta.B + gk * ta.ldb + gn : ta.B, ok ? 8 : 0);
+    }
+  }
+}
+
+// acc += A[m0:+64, kbeg:kend] @ B[kbeg:kend, n0:+64]
+template <bool V16>
+__device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64_t kend, double* smem,
+                                         double (&acc)[4][4][2]) {
+  double* As = smem;
+  double* Bs = smem + G_STAGES * A_TILE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t ktiles = (kend - kbeg + GB_K - 1) / GB_K;
+#pragma unroll
+  for (int s = 0; s < G_STAGES - 1; ++s) {
+    if (s < ktiles) load_stage<V16>(ta, kbeg + s * GB_K, kend, As + s * A_TILE, Bs + s * B_TILE);
+    cp_async_commit();
+  }
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<G_STAGES - 2>();
+    __syncthreads();
+    const int64_t nt = kt + G_STAGES - 1;
+    if (nt < ktiles) {
+      const int ns = (int)(nt % G_STAGES);
+      load_stage<V16>(ta, kbeg + nt * GB_K, kend, As + ns * A_TILE, Bs + ns * B_TILE);
+    }
+    cp_async_commit();
+    const int cs = (int)(kt % G_STAGES);
+    const double* as = As + cs * A_TILE + (wm * 32 + g) * A_STR + t;
+    const double* bs = Bs + cs * B_TILE + t * B_STR + wn * 32 + g;
+#pragma unroll
+    for (int kk = 0; kk < GB_K; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = as[mi * 8 * A_STR + kk];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = bs[kk * B_STR + ni * 8];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+template <bool V16>
+__global__ void __launch_bounds__(G_THREADS) gemm_f64_kernel(const double* __restrict__ A, int64_t lda,
+                                                             int64_t strideA, const double* __restrict__ B,
+                                                             int64_t ldb, int64_t strideB, int64_t m, int64_t nc,
+                                                             int64_t k, int64_t splits, int64_t kchunk,
+                                                             double* __restrict__ out, int64_t ldo,
+                                                             int64_t strideO, double* __restrict__ part) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t z = blockIdx.z;
+  const int64_t b = z / splits, sp = z - b * splits;
+  TileArgs ta{A + b * strideA, lda, B + b * strideB, ldb, m, nc, (int64_t)blockIdx.y * GB_M,
+              (int64_t)blockIdx.x * GB_N};
+  const int64_t kbeg = sp * kchunk;
+  const int64_t kend = min(k, kbeg + kchunk);
+  double acc[4][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  if (kbeg < kend) mainloop<V16>(ta, kbeg, kend, smem, acc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  double* dst;
+  int64_t ld;
+  if (splits == 1) { dst = out + b * strideO; ld = ldo; }
+  else { dst = part + z * m * nc; ld = nc; }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int64_t r = ta.m0 + wm * 32 + mi * 8 + g;
+    if (r >= m) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int64_t c0 = ta.n0 + wn * 32 + ni * 8 + 2 * t;
+      if (c0 < nc) dst[r * ld + c0] = acc[mi][ni][0];
+      if (c0 + 1 < nc) dst[r * ld + c0 + 1] = acc[mi][ni][1];
+    }
+  }
+}
+
+__global__ void splitk_reduce_kernel(const double* __restrict__ part, int64_t splits, int64_t m, int64_t nc,
+                                     int64_t batch, double* __restrict__ out, int64_t ldo, int64_t strideO) {
+  const int64_t per = m * nc;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < per * batch;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g / per, e = g - b * per;
+    const double* p = part + b * splits * per + e;
+    double acc = p[0];
+    for (int64_t s = 1; s < splits; ++s) acc = __dadd_rn(acc, p[s * per]);
+    const int64_t r = e / nc, c = e - r * nc;
+    out[b * strideO + r * ldo + c] = acc;
+  }
+}
+
+// ---- segmented square sums
+__global__ void __launch_bounds__(G_THREADS) segsq_f64_kernel(const double* __restrict__ A, int64_t lda,
+                                                              int64_t strideA, const double* __restrict__ B,
+                                                              int64_t ldb, int64_t strideB, int64_t m,
+                                                              int64_t nc, const int64_t* __restrict__ seg,
+                                                              int64_t nseg, int64_t seg_stride,
+                                                              int64_t chunks, double* __restrict__ part) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double red[G_THREADS / 32];
+  const int64_t z = blockIdx.z;
+  const int64_t b = z / chunks, ch = z - b * chunks;
+  const int64_t per = (nseg + chunks - 1) / chunks;
+  const int64_t j0 = ch * per, j1 = min(nseg, j0 + per);
+  TileArgs ta{A + b * strideA, lda, B + b * strideB, ldb, m, nc, (int64_t)blockIdx.y * GB_M,
+              (int64_t)blockIdx.x * GB_N};
+  const int64_t tiles = (int64_t)gridDim.x * gridDim.y;
+  const int64_t tile = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  for (int64_t j = j0; j < j1; ++j) {
+    const int64_t kbeg = seg[b * seg_stride + j], kend = seg[b * seg_stride + j + 1];
+    double acc[4][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    if (kbeg < kend) mainloop<false>(ta, kbeg, kend, smem, acc);
+    double sq = 0.0;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        sq = fma(acc[mi][ni][0], acc[mi][ni][0], sq);
+        sq = fma(acc[mi][ni][1], acc[mi][ni][1], sq);
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = red[0];
+      for (int w = 1; w < G_THREADS / 32; ++w) tot += red[w];
+      part[(b * nseg + j) * tiles + tile] = tot;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void segsq_reduce_kernel(const double* __restrict__ part, int64_t tiles, int64_t total,
+                                    double* __restrict__ gsq) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const double* p = part + g * tiles;
+    double acc = 0.0;
+    for (int64_t i = 0; i < tiles; ++i) acc += p[i];
+    gsq[g] = acc;
+  }
+}
+
+// ---- squared difference / squared norm (error evaluation)
+constexpr int SQ_THREADS = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(SQ_THREADS) sqdiff_kernel(const T* __restrict__ X, int64_t ldx, int64_t strideX,
+                                                            const T* __restrict__ Y, int64_t ldy, int64_t strideY,
+                                                            int64_t m, int64_t nc, int64_t parts,
+                                                            double* __restrict__ part) {
+  __shared__ double red[2][SQ_THREADS / 32];
+  const int64_t b = blockIdx.y, c = blockIdx.x;
+  const int64_t total = m * nc;
+  const int64_t chunk = (total + parts - 1) / parts;
+  const int64_t e0 = c * chunk, e1 = min(total, e0 + chunk);
+  const T* xb = X + b * strideX;
+  const T* yb = Y ? Y + b * strideY : nullptr;
+  double se = 0.0, sr = 0.0;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += SQ_THREADS) {
+    const int64_t r = e / nc, col = e - r * nc;
+    const double x = (double)xb[r * ldx + col];
+    const double y = yb ? (double)yb[r * ldy + col] : 0.0;
+    const double d = x - y;
+    se = fma(d, d, se);
+    sr = fma(x, x, sr);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    se += __shfl_xor_sync(0xffffffffu, se, o);
+    sr += __shfl_xor_sync(0xffffffffu, sr, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = se; red[1][threadIdx.x >> 5] = sr; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, r = 0.0;
+    for (int w = 0; w < SQ_THREADS / 32; ++w) { a += red[0][w]; r += red[1][w]; }
+    part[(b * parts + c) * 2] = a;
+    part[(b * parts + c) * 2 + 1] = r;
+  }
+}
+
+__global__ void sqdiff_final_kernel(const double* __restrict__ part, int64_t parts, int64_t batch,
+                                    double* __restrict__ err) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    double a = 0.0, r = 0.0;
+    for (int64_t c = 0; c < parts; ++c) { a += part[(b * parts + c) * 2]; r += part[(b * parts + c) * 2 + 1]; }
+    err[2 * b] = a;
+    err[2 * b + 1] = r;
+  }
+}
+
+inline int64_t sq_parts(int64_t m, int64_t nc, int64_t batch) {
+  int64_t parts = ceil_div(m * nc, 4096);
+  int64_t target = ceil_div(148 * 8, batch);
+  if (parts > target) parts = target;
+  if (parts > 1024) parts = 1024;
+  if (parts < 1) parts = 1;
+  return parts;
+}
+
+struct SplitPlan {
+  int64_t splits, kchunk;
+};
+
+inline SplitPlan plan_split(int64_t m, int64_t nc, int64_t k, int64_t batch) {
+  const int64_t tiles = ceil_div(m, GB_M) * ceil_div(nc, GB_N) * batch;
+  int64_t splits = ceil_div(2 * 148, tiles);
+  const int64_t max_splits = ceil_div(k, 4 * GB_K);  // at least 64 of k per split
+  if (splits > max_splits) splits = max_splits;
+  if (splits < 1) splits = 1;
+  if (batch * splits > 65535) splits = 65535 / batch;
+  int64_t kchunk = ceil_div(ceil_div(k, splits), GB_K) * GB_K;
+  splits = ceil_div(k, kchunk);
+  if (splits < 1) splits = 1;
+  return {splits, kchunk};
+}
+
+inline int64_t segsq_chunks(int64_t m, int64_t nc, int64_t nseg, int64_t batch) {
+  const int64_t tiles = ceil_div(m, GB_M) * ceil_div(nc, GB_N) * batch;
+  int64_t ch = ceil_div(2 * 148, tiles);
+  if (ch > nseg) ch = nseg;
+  if (ch < 1) ch = 1;
+  if (batch * ch > 65535) ch = 65535 / batch;
+  return ch;
+}
+
+}  // namespace bmm
+
+using namespace bmm;
+
+extern "C" int64_t bmm_gemm_f64_workspace(int64_t m, int64_t nc, int64_t k, int64_t batch) {
+  SplitPlan sp = plan_split(m, nc, k, batch);
+  return sp.splits > 1 ? sp.splits * batch * m * nc * 8 : 0;
+}
+
+extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                            int64_t strideB, int64_t m, int64_t nc, int64_t k, int64_t batch, double* out,
+                            int64_t ldo, int64_t strideO, void* ws, int64_t ws_bytes, void* stream) {
+  BMM_REQUIRE(m >= 0 && nc >= 0 && k >= 0 && batch >= 1, BMM_E_ARG, "bmm_gemm_f64: bad shape");
+  if (m == 0 || nc == 0) return BMM_OK;
+  cudaStream_t st = as_stream(stream);
+  if (k == 0) {
+    for (int64_t b = 0; b < batch; ++b)
+      if (cudaMemset2DAsync(out + b * strideO, ldo * 8, 0, nc * 8, m, st) != cudaSuccess) {
+        set_error("bmm_gemm_f64: memset failed");
+        return BMM_E_CUDA;
+      }
+    return BMM_OK;
+  }
+  SplitPlan sp = plan_split(m, nc, k, batch);
+  const int64_t need = sp.splits > 1 ? sp.splits * batch * m * nc * 8 : 0;
+  BMM_REQUIRE(ws_bytes >= need && (need == 0 || ws != nullptr), BMM_E_ARG,
+              "bmm_gemm_f64: workspace too small (%lld < %lld)", (long long)ws_bytes, (long long)need);
+  BMM_REQUIRE(ceil_div(m, GB_M) <= 65535, BMM_E_UNSUPPORTED, "bmm_gemm_f64: m too large");
+  const bool v16 = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
+                   lda % 2 == 0 && ldb % 2 == 0 && strideA % 2 == 0 && strideB % 2 == 0;
+  dim3 grid((unsigned)ceil_div(nc, GB_N), (unsigned)ceil_div(m, GB_M), (unsigned)(batch * sp.splits));
+  if (v16) {
+    cudaFuncSetAttribute(gemm_f64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES);
+    gemm_f64_kernel<true><<<grid, G_THREADS, G_SMEM_BYTES, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k,
+                                                                sp.splits, sp.kchunk, out, ldo, strideO,
+                                                                (double*)ws);
+  } else {
+    cudaFuncSetAttribute(gemm_f64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES);
+    gemm_f64_kernel<false><<<grid, G_THREADS, G_SMEM_BYTES, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k,
+                                                                 sp.splits, sp.kchunk, out, ldo, strideO,
+                                                                 (double*)ws);
+  }
+  BMM_CHECK_LAUNCH("gemm_f64_kernel");
+  if (sp.splits > 1) {
+    splitk_reduce_kernel<<<grid_for(m * nc * batch, 256), 256, 0, st>>>((const double*)ws, sp.splits, m, nc,
+                                                                        batch, out, ldo, strideO);
+    BMM_CHECK_LAUNCH("splitk_reduce_kernel");
+  }
+  return BMM_OK;
+}
+
+extern "C" int64_t bmm_segsq_f64_workspace(int64_t m, int64_t nc, int64_t nseg, int64_t batch) {
+  return ceil_div(m, GB_M) * ceil_div(nc, GB_N) * nseg * batch * 8;
+}
+
+extern "C" int bmm_segsq_f64(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                             int64_t strideB, int64_t m, int64_t nc, const int64_t* seg, int64_t nseg,
+                             int64_t seg_stride, int64_t batch, double* gsq, void* ws, int64_t ws_bytes,
+                             void* stream) {
+  BMM_REQUIRE(m >= 1 && nc >= 1 && nseg >= 1 && batch >= 1, BMM_E_ARG, "bmm_segsq_f64: bad shape");
+  const int64_t tiles = ceil_div(m, GB_M) * ceil_div(nc, GB_N);
+  const int64_t need = tiles * nseg * batch * 8;
+  BMM_REQUIRE(ws_bytes >= need && ws != nullptr, BMM_E_ARG, "bmm_segsq_f64: workspace too small");
+  BMM_REQUIRE(ceil_div(m, GB_M) <= 65535, BMM_E_UNSUPPORTED, "bmm_segsq_f64: m too large");
+  cudaStream_t st = as_stream(stream);
+  const int64_t chunks = segsq_chunks(m, nc, nseg, batch);
+  dim3 grid((unsigned)ceil_div(nc, GB_N), (unsigned)ceil_div(m, GB_M), (unsigned)(batch * chunks));
+  cudaFuncSetAttribute(segsq_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES);
+  segsq_f64_kernel<<<grid, G_THREADS, G_SMEM_BYTES, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg,
+                                                          seg_stride, chunks, (double*)ws);
+  BMM_CHECK_LAUNCH("segsq_f64_kernel");
+  segsq_reduce_kernel<<<grid_for(nseg * batch, 128), 128, 0, st>>>((const double*)ws, tiles, nseg * batch, gsq);
+  BMM_CHECK_LAUNCH("segsq_reduce_kernel");
+  return BMM_OK;
+}
+
+extern "C" int64_t bmm_sqdiff_workspace(int64_t m, int64_t nc, int64_t batch) {
+  return sq_parts(m, nc, batch) * batch * 2 * 8;
+}
+
+extern "C" int bmm_sqdiff(int dtype, const void* X, int64_t ldx, int64_t strideX, const void* Y, int64_t ldy,
+                          int64_t strideY, int64_t m, int64_t nc, int64_t batch, double* err, void* ws,
+                          int64_t ws_bytes, void* stream) {
+  BMM_REQUIRE(m >= 1 && nc >= 1 && batch >= 1 && batch <= 65535, BMM_E_ARG, "bmm_sqdiff: bad shape");
+  const int64_t parts = sq_parts(m, nc, batch);
+  BMM_REQUIRE(ws_bytes >= parts * batch * 16 && ws != nullptr, BMM_E_ARG, "bmm_sqdiff: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  dim3 grid((unsigned)parts, (unsigned)batch);
+  if (dtype == BMM_F64)
+    sqdiff_kernel<double><<<grid, SQ_THREADS, 0, st>>>((const double*)X, ldx, strideX, (const double*)Y, ldy,
+                                                       strideY, m, nc, parts, (double*)ws);
+  else if (dtype == BMM_F32)
+    sqdiff_kernel<float><<<grid, SQ_THREADS, 0, st>>>((const float*)X, ldx, strideX, (const float*)Y, ldy,
+                                                      strideY, m, nc, parts, (double*)ws);
+  else {
+    set_error("bmm_sqdiff: unknown dtype %d", dtype);
+    return BMM_E_ARG;
+  }
+  BMM_CHECK_LAUNCH("sqdiff_kernel");
+  sqdiff_final_kernel<<<grid_for(batch, 64), 64, 0, st>>>((const double*)ws, parts, batch, err);
+  BMM_CHECK_LAUNCH("sqdiff_final_kernel");
+  return BMM_OK;
+}

@@ -1,0 +1,274 @@
+// K3 sampler and K4 gather.
+//
+// Reference: _draw_indices (estimators.py:34-44), sketch_columns (55-81),
+// estimate_product (125-175), estimate_product_block_sampling (221-253).
+//
+// One warp per block: lane L serves draws L, L+32, ... of the block's child
+// stream; lane L jumps its PCG64 state L+1 steps ahead, then 32 steps per
+// draw, so the warp consumes exactly the uniform sequence rng.random(c_k)
+// would produce.  The CDF is the sequential np.cumsum of the block
+// probabilities; the draw is upper_bound (searchsorted side="right") clamped
+// onto the last positive-probability index.
+#include "common.cuh"
+#include "rng.cuh"
+
+namespace bmm {
+
+__global__ void block_cdf_kernel(const double* __restrict__ probs, const int64_t* __restrict__ offsets,
+                                 int64_t K, int64_t batch, int64_t n, double* __restrict__ cum,
+                                 int64_t* __restrict__ last) {
+  const int64_t total = K * batch;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g / K, k = g - b * K;
+    const int64_t o = offsets[k], e = offsets[k + 1];
+    const double* p = probs + b * n;
+    double* cb = cum + b * n;
+    double acc = 0.0;
+    int64_t lst = -1;
+    for (int64_t i = o; i < e; ++i) {
+      const double v = p[i];
+      acc = (i == o) ? v : __dadd_rn(acc, v);
+      cb[i] = acc;
+      if (v > 0.0) lst = i - o;
+    }
+    last[g] = lst;
+  }
+}
+
+__global__ void seed_streams_kernel(const uint32_t* __restrict__ words, int64_t nw,
+                                    const int64_t* __restrict__ first_child, int64_t count,
+                                    int64_t batch, uint64_t* __restrict__ states) {
+  const int64_t total = count * batch;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g / count, j = g - b * count;
+    U128 st, inc;
+    seed_pcg64(words + b * nw, nw, (uint64_t)(first_child[b] + j), st, inc);
+    uint64_t* o = states + 4 * g;
+    o[0] = st.hi;
+    o[1] = st.lo;
+    o[2] = inc.hi;
+    o[3] = inc.lo;
+  }
+}
+
+__global__ void __launch_bounds__(256) sample_kernel(
+    const double* __restrict__ probs, const double* __restrict__ cum,
+    const int64_t* __restrict__ last, const int64_t* __restrict__ offsets, int64_t K, int64_t batch,
+    int64_t n, const int64_t* __restrict__ budgets, const int64_t* __restrict__ col_off,
+    int64_t w_stride, const uint64_t* __restrict__ states, int64_t* __restrict__ column,
+    double* __restrict__ prob, double* __restrict__ scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps_total = K * batch;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < warps_total;
+       g += (int64_t)gridDim.x * wpb) {
+    const int64_t b = g / K, k = g - b * K;
+    const int64_t ck = budgets[g];
+    if (ck <= 0) continue;
+    const int64_t o = offsets[k], len = offsets[k + 1] - o;
+    const double* cb = cum + b * n + o;
+    const double* pb = probs + b * n + o;
+    const int64_t lst = last[g];
+    const uint64_t* sp = states + 4 * g;
+    U128 st{sp[0], sp[1]}, inc{sp[2], sp[3]};
+    U128 m1, p1, m32, p32;
+    pcg_jump((uint64_t)lane + 1, inc, m1, p1);
+    pcg_jump(32, inc, m32, p32);
+    st = add128(mul128(m1, st), p1);
+    const double dck = (double)ck;
+    const int64_t t0 = col_off[b * (K + 1) + k];
+    for (int64_t j = lane; j < ck; j += 32) {
+      const double u = u53(pcg_output(st));
+      // first index with cum > u
+      int64_t lo = 0, hi = len;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (cb[mid] > u) hi = mid; else lo = mid + 1;
+      }
+      const int64_t idx = lo < lst ? lo : lst;
+      const double pr = pb[idx];
+      const double sc = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dck, pr)));
+      const int64_t t = b * w_stride + t0 + j;
+      column[t] = o + idx;
+      prob[t] = pr;
+      scale[t] = sc;
+      st = add128(mul128(m32, st), p32);
+    }
+  }
+}
+
+// ---- K4 gather
+
+__device__ __forceinline__ double load_as_double(const double* p) { return __ldg(p); }
+__device__ __forceinline__ double load_as_double(const float* p) { return (double)__ldg(p); }
+__device__ __forceinline__ void store_val(double* p, double v) { *p = v; }
+__device__ __forceinline__ void store_val(float* p, double v) { *p = (float)v; }
+
+// C[h, t] = M[h, column[t]] * scale[t]
+template <typename T, typename TO>
+__global__ void __launch_bounds__(256) gather_c_kernel(const T* __restrict__ M, int64_t ldm, int64_t strideM,
+                                                       int64_t m, const int64_t* __restrict__ column,
+                                                       const double* __restrict__ scale, int64_t W,
+                                                       int64_t w_stride, int64_t batch, TO* __restrict__ C,
+                                                       int64_t ldc, int64_t strideC) {
+  const int64_t per_b = m * W;
+  const int64_t total = per_b * batch;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g / per_b, r = g - b * per_b;
+    const int64_t h = r / W, t = r - h * W;
+    const int64_t col = column[b * w_stride + t];
+    const double s = scale[b * w_stride + t];
+    store_val(C + b * strideC + h * ldc + t, __dmul_rn(load_as_double(M + b * strideM + h * ldm + col), s));
+  }
+}
+
+// D[t, f] = N[column[t], f] * scale[t]
+template <typename T, typename TO>
+__global__ void __launch_bounds__(256) gather_d_kernel(const T* __restrict__ N, int64_t ldn, int64_t strideN,
+                                                       int64_t p, const int64_t* __restrict__ column,
+                                                       const double* __restrict__ scale, int64_t W,
+                                                       int64_t w_stride, int64_t batch, TO* __restrict__ D,
+                                                       int64_t ldd, int64_t strideD) {
+  const int64_t per_b = W * p;
+  const int64_t total = per_b * batch;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g / per_b, r = g - b * per_b;
+    const int64_t t = r / p, f = r - t * p;
+    const int64_t row = column[b * w_stride + t];
+    const double s = scale[b * w_stride + t];
+    store_val(D + b * strideD + t * ldd + f, __dmul_rn(load_as_double(N + b * strideN + row * ldn + f), s));
+  }
+}
+
+// SSM: sketch column j belongs to draw t with sk_off[t] <= j < sk_off[t+1]
+template <typename T>
+__global__ void gather_blocks_kernel(const T* __restrict__ M, int64_t ldm, const T* __restrict__ N,
+                                     int64_t ldn, int64_t m, int64_t p,
+                                     const int64_t* __restrict__ offsets,
+                                     const int64_t* __restrict__ blocks,
+                                     const double* __restrict__ scale,
+                                     const int64_t* __restrict__ sk_off, int64_t draws, int64_t W,
+                                     T* __restrict__ C, int64_t ldc, T* __restrict__ D, int64_t ldd) {
+  const int64_t totC = C ? m * W : 0;
+  const int64_t totD = D ? W * p : 0;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < totC + totD;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j, h = 0, f = 0;
+    if (g < totC) { h = g / W; j = g - h * W; }
+    else { const int64_t r = g - totC; j = r / p; f = r - j * p; }
+    int64_t lo = 0, hi = draws;  // last t with sk_off[t] <= j
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (sk_off[mid] <= j) lo = mid; else hi = mid;
+    }
+    const int64_t t = lo;
+    const int64_t src = offsets[blocks[t]] + (j - sk_off[t]);
+    const double s = scale[t];
+    if (g < totC) store_val(C + h * ldc + j, __dmul_rn(s, load_as_double(M + h * ldm + src)));
+    else store_val(D + j * ldd + f, __dmul_rn(s, load_as_double(N + src * ldn + f)));
+  }
+}
+
+template <typename T, typename TO>
+int launch_gather(const T* M, int64_t ldm, int64_t strideM, const T* N, int64_t ldn, int64_t strideN,
+                  int64_t m, int64_t p, const int64_t* column, const double* scale, int64_t W,
+                  int64_t w_stride, int64_t batch, TO* C, int64_t ldc, int64_t strideC, TO* D,
+                  int64_t ldd, int64_t strideD, cudaStream_t st) {
+  if (C != nullptr && m > 0) {
+    gather_c_kernel<T, TO><<<grid_for(m * W * batch, 256), 256, 0, st>>>(M, ldm, strideM, m, column, scale, W,
+                                                                     w_stride, batch, C, ldc, strideC);
+    BMM_CHECK_LAUNCH("gather_c_kernel");
+  }
+  if (D != nullptr && p > 0) {
+    gather_d_kernel<T, TO><<<grid_for(W * p * batch, 256), 256, 0, st>>>(N, ldn, strideN, p, column, scale, W,
+                                                                     w_stride, batch, D, ldd, strideD);
+    BMM_CHECK_LAUNCH("gather_d_kernel");
+  }
+  return BMM_OK;
+}
+
+}  // namespace bmm
+
+using namespace bmm;
+
+extern "C" int bmm_block_cdf(const double* probs, const int64_t* offsets, int64_t K, int64_t batch,
+                             int64_t n, double* cum, int64_t* last_support, void* stream) {
+  BMM_REQUIRE(K >= 1 && batch >= 1, BMM_E_ARG, "bmm_block_cdf: bad shape");
+  block_cdf_kernel<<<grid_for(K * batch, 128, 16, 16), 128, 0, as_stream(stream)>>>(probs, offsets, K, batch,
+                                                                                   n, cum, last_support);
+  BMM_CHECK_LAUNCH("block_cdf_kernel");
+  return BMM_OK;
+}
+
+extern "C" int bmm_seed_streams(const uint32_t* words, int64_t n_words, const int64_t* first_child,
+                                int64_t count, int64_t batch, uint64_t* states, void* stream) {
+  BMM_REQUIRE(n_words >= 4 && count >= 0 && batch >= 1, BMM_E_ARG,
+              "bmm_seed_streams: need >= 4 entropy words (padded run entropy)");
+  if (count == 0) return BMM_OK;
+  seed_streams_kernel<<<grid_for(count * batch, 128), 128, 0, as_stream(stream)>>>(words, n_words, first_child,
+                                                                                  count, batch, states);
+  BMM_CHECK_LAUNCH("seed_streams_kernel");
+  return BMM_OK;
+}
+
+extern "C" int bmm_sample(const double* probs, const double* cum, const int64_t* last_support,
+                          const int64_t* offsets, int64_t K, int64_t batch, int64_t n,
+                          const int64_t* budgets, const int64_t* col_off, int64_t w_stride,
+                          const uint64_t* states, int64_t* column, double* prob, double* scale,
+                          void* stream) {
+  BMM_REQUIRE(K >= 1 && batch >= 1, BMM_E_ARG, "bmm_sample: bad shape");
+  const int64_t warps = K * batch;
+  sample_kernel<<<grid_for(warps * 32, 256, 8, 16), 256, 0, as_stream(stream)>>>(
+      probs, cum, last_support, offsets, K, batch, n, budgets, col_off, w_stride, states, column, prob,
+      scale);
+  BMM_CHECK_LAUNCH("sample_kernel");
+  return BMM_OK;
+}
+
+extern "C" int bmm_gather(int dtype, int out_dtype, const void* M, int64_t ldm, int64_t strideM,
+                          const void* N, int64_t ldn, int64_t strideN, int64_t m, int64_t p,
+                          const int64_t* column, const double* scale, int64_t W, int64_t w_stride,
+                          int64_t batch, void* C, int64_t ldc, int64_t strideC, void* D, int64_t ldd,
+                          int64_t strideD, void* stream) {
+  BMM_REQUIRE(W >= 0 && batch >= 1, BMM_E_ARG, "bmm_gather: bad shape");
+  if (W == 0) return BMM_OK;
+  cudaStream_t st = as_stream(stream);
+#define BMM_GATHER_CASE(TI, TO)                                                                       \
+  return launch_gather<TI, TO>((const TI*)M, ldm, strideM, (const TI*)N, ldn, strideN, m, p, column, \
+                               scale, W, w_stride, batch, (TO*)C, ldc, strideC, (TO*)D, ldd, strideD, st)
+  if (dtype == BMM_F64 && out_dtype == BMM_F64) BMM_GATHER_CASE(double, double);
+  if (dtype == BMM_F32 && out_dtype == BMM_F64) BMM_GATHER_CASE(float, double);
+  if (dtype == BMM_F32 && out_dtype == BMM_F32) BMM_GATHER_CASE(float, float);
+  if (dtype == BMM_F64 && out_dtype == BMM_F32) BMM_GATHER_CASE(double, float);
+#undef BMM_GATHER_CASE
+  set_error("bmm_gather: unknown dtype %d/%d", dtype, out_dtype);
+  return BMM_E_ARG;
+}
+
+extern "C" int bmm_gather_blocks(int dtype, const void* M, int64_t ldm, const void* N, int64_t ldn,
+                                 int64_t m, int64_t p, const int64_t* offsets, const int64_t* blocks,
+                                 const double* scale, const int64_t* sk_off, int64_t draws, int64_t W,
+                                 void* C, int64_t ldc, void* D, int64_t ldd, void* stream) {
+  BMM_REQUIRE(draws >= 1 && W >= 1, BMM_E_ARG, "bmm_gather_blocks: bad shape");
+  cudaStream_t st = as_stream(stream);
+  const int64_t work = (C ? m * W : 0) + (D ? W * p : 0);
+  if (work == 0) return BMM_OK;
+  if (dtype == BMM_F64) {
+    gather_blocks_kernel<double><<<grid_for(work, 256), 256, 0, st>>>(
+        (const double*)M, ldm, (const double*)N, ldn, m, p, offsets, blocks, scale, sk_off, draws, W,
+        (double*)C, ldc, (double*)D, ldd);
+  } else if (dtype == BMM_F32) {
+    gather_blocks_kernel<float><<<grid_for(work, 256), 256, 0, st>>>(
+        (const float*)M, ldm, (const float*)N, ldn, m, p, offsets, blocks, scale, sk_off, draws, W,
+        (float*)C, ldc, (float*)D, ldd);
+  } else {
+    set_error("bmm_gather_blocks: unknown dtype %d", dtype);
+    return BMM_E_ARG;
+  }
+  BMM_CHECK_LAUNCH("gather_blocks_kernel");
+  return BMM_OK;
+}

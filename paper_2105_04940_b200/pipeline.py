@@ -1,0 +1,291 @@
+"""Device-resident approximate-product pipeline (the batched fast path).
+
+One object holds every buffer for a fixed (shape, partition, method, budget,
+batch), so a call is a fixed sequence of kernel launches on the current
+stream with no allocation and no host synchronisation:
+
+  K1 bmm_norms -> K2 bmm_block_probs -> [OPL: bmm_segsq_f64 of M^k N_k]
+  [two-step: pilot budgets -> CDF -> child seeds -> draws -> gather -> segsq]
+  -> bmm_budgets -> bmm_block_cdf -> bmm_seed_streams -> bmm_sample
+  -> bmm_gather -> bmm_gemm_f64  (C @ D)
+
+It computes exactly what the reference composition computes
+(allocate_* + estimate_product, estimate_product_two_step,
+estimate_product_block_sampling; pkg/src/blockmm/plan.py:383-480,
+estimators.py:125-253) and is bit-compatible with the per-call API in this
+package (same kernels, same streams).  Device status codes (the reference's
+ValueError/AssertionError cases) are read only by ``check()``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import rng as _rng
+from .plan import raise_status
+
+METHODS = ("OPL", "ONC", "UU", "ONU", "ONMCNR", "SSM")
+
+
+@dataclass
+class StreamSeeds:
+    """Entropy words and first child index per problem for one spawn(K)."""
+
+    words: np.ndarray        # (batch, n_words) uint32
+    first: np.ndarray        # (batch,) int64
+
+
+@dataclass
+class CallSeeds:
+    main: Optional[StreamSeeds] = None
+    pilot: Optional[StreamSeeds] = None
+    states: Optional[np.ndarray] = None   # SSM: (batch, 4) uint64 caller stream states
+
+
+def seeds_from_rngs(method: str, rngs: list, K: int, draws: int = 0) -> CallSeeds:
+    """Apply the reference's generator side effects for one call per problem
+    and return the device seeds.  rngs: one numpy Generator per problem."""
+
+    def stack(parts):
+        ws = [w for w, _ in parts]
+        if len({len(w) for w in ws}) != 1:
+            raise ValueError("all problems' generators must have entropy/key words of equal length")
+        return StreamSeeds(np.stack(ws).astype(np.uint32), np.array([f for _, f in parts], dtype=np.int64))
+
+    if method == "SSM":
+        st = np.stack([_rng.stream_state(r) for r in rngs])
+        for r in rngs:
+            _rng.consume(r, draws)
+        return CallSeeds(states=st)
+    if method in ("ONU", "ONMCNR"):
+        pil, mai = [], []
+        for r in rngs:
+            pr, mr = r.spawn(2)                       # estimators.py:207
+            pil.append(_rng.spawn_words(pr, K))       # plan.py:456
+            mai.append(_rng.spawn_words(mr, K))       # estimators.py:141
+        return CallSeeds(main=stack(mai), pilot=stack(pil))
+    return CallSeeds(main=stack([_rng.spawn_words(r, K) for r in rngs]))
+
+
+class SketchPipeline:
+    """Preallocated device pipeline for `batch` problems of shape
+    M (m x n), N (n x p) sharing one block partition."""
+
+    def __init__(self, m: int, n: int, p: int, sizes, c: int, method: str, *, batch: int = 1,
+                 dtype=torch.float64, c0: int = 0, cap: bool = True, draws: int = 0):
+        if method not in METHODS:
+            raise ValueError(f"unknown method {method!r}")
+        dev = _lib.device()
+        self.m, self.n, self.p, self.B = int(m), int(n), int(p), int(batch)
+        self.sizes = tuple(int(s) for s in sizes)
+        if sum(self.sizes) != self.n:
+            raise ValueError("partition does not cover n")
+        self.K = len(self.sizes)
+        self.method, self.c, self.c0, self.cap = method, int(c), int(c0), bool(cap)
+        self.dtype = dtype
+        self.lib = _lib.load()
+        K, B, n_ = self.K, self.B, self.n
+        f64 = dict(dtype=torch.float64, device=dev)
+        i64 = dict(dtype=torch.int64, device=dev)
+        off = np.zeros(K + 1, dtype=np.int64)
+        np.cumsum(self.sizes, out=off[1:])
+        self.offsets = torch.as_tensor(off, device=dev)
+        self.sizes_d = torch.as_tensor(np.asarray(self.sizes, dtype=np.int64), device=dev)
+        self.colsq = torch.empty(B * n_, **f64)
+        self.rowsq = torch.empty(B * n_, **f64)
+        self.probs = torch.empty(B * n_, **f64)
+        self.s = torch.empty(B * K, **f64)
+        self.cum = torch.empty(B * n_, **f64)
+        self.last = torch.empty(B * K, **i64)
+        self.budgets = torch.empty(B * K, **i64)
+        self.col_off = torch.empty(B * (K + 1), **i64)
+        self.status = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.diag = torch.zeros(B, **i64)
+        self.notes = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.states = torch.empty(B * K * 4, **i64)
+        self.c_arr = torch.full((B,), self.c, **i64)
+        self.ws_budget = torch.empty(max(256, self.lib.bmm_budgets_workspace(K) * B), dtype=torch.uint8, device=dev)
+        if method == "SSM":
+            self.draws = int(draws)
+            if len(set(self.sizes)) != 1:
+                raise ValueError("batched SSM needs equal blocks (fixed sketch width)")
+            self.W = self.draws * self.sizes[0]
+            self.fnorm = torch.empty(B * K, **f64)
+            self.q = torch.empty(B * K, **f64)
+            self.qcum = torch.empty(B * K, **f64)
+            self.qlast = torch.empty(B, **i64)
+            self.qoff = torch.as_tensor(np.array([0, K], dtype=np.int64), device=dev)
+            self.q_bud = torch.full((B,), self.draws, **i64)
+            self.q_coloff = torch.as_tensor(np.tile(np.array([0, self.draws], dtype=np.int64), B), device=dev)
+            self.sk_off = torch.as_tensor(np.arange(self.draws + 1, dtype=np.int64) * self.sizes[0], device=dev)
+            self.ssm_states = torch.empty(B * 4, **i64)
+            self.blk = torch.empty(B * self.draws, **i64)
+            self.blk_prob = torch.empty(B * self.draws, **f64)
+            self.blk_scale = torch.empty(B * self.draws, **f64)
+        else:
+            self.W = self.c
+        W = self.W
+        self.column = torch.zeros(B * W, **i64)  # zero-init: failed plans gather column 0, never garbage
+        self.prob = torch.empty(B * W, **f64)
+        self.scale = torch.empty(B * W, **f64)
+        self.C = torch.empty(B * self.m * W, **f64)
+        self.D = torch.empty(B * W * self.p, **f64)
+        self.CD = torch.empty(B * self.m * self.p, **f64)
+        self.ws_gemm = torch.empty(max(256, self.lib.bmm_gemm_f64_workspace(self.m, self.p, W, B)),
+                                   dtype=torch.uint8, device=dev)
+        if method == "OPL":
+            self.gsq = torch.empty(B * K, **f64)
+            self.ws_seg = torch.empty(max(256, self.lib.bmm_segsq_f64_workspace(self.m, self.p, K, B)),
+                                      dtype=torch.uint8, device=dev)
+        if method in ("ONU", "ONMCNR"):
+            self.pc = self.c0 // K
+            if self.pc < 1:
+                raise ValueError(f"c0={self.c0} gives no pilot draws for K={K} blocks")
+            W0 = K * self.pc
+            self.W0 = W0
+            self.p_bud = torch.empty(B * K, **i64)
+            self.p_coloff = torch.empty(B * (K + 1), **i64)
+            self.p_c = torch.full((B,), self.pc, **i64)
+            self.p_states = torch.empty(B * K * 4, **i64)
+            self.p_column = torch.zeros(B * W0, **i64)
+            self.p_prob = torch.zeros(B * W0, **f64)
+            self.p_scale = torch.zeros(B * W0, **f64)
+            self.C0 = torch.empty(B * self.m * W0, **f64)
+            self.D0 = torch.empty(B * W0 * self.p, **f64)
+            self.pilot_sq = torch.empty(B * K, **f64)
+            self.ws_seg = torch.empty(max(256, self.lib.bmm_segsq_f64_workspace(self.m, self.p, K, B)),
+                                      dtype=torch.uint8, device=dev)
+            if method == "ONU":
+                u = np.concatenate([np.full(nk, 1.0 / nk) for nk in self.sizes])
+                self.p0 = torch.as_tensor(np.tile(u, B), device=dev)
+            self.p0cum = torch.empty(B * n_, **f64)
+            self.p0last = torch.empty(B * K, **i64)
+        self._words = None
+
+    # ------------------------------------------------------------------ steps
+    def _c(self, name, *args):
+        rc = getattr(self.lib, name)(*args)
+        if rc < 0:
+            raise RuntimeError(f"{name} failed ({rc}): {self.lib.bmm_last_error().decode()}")
+
+    def _seed(self, seeds: StreamSeeds, states: torch.Tensor, st):
+        dev = states.device
+        words = torch.as_tensor(np.ascontiguousarray(seeds.words).view(np.int32), device=dev)
+        first = torch.as_tensor(seeds.first, device=dev)
+        self._keep = (words, first)  # keep alive until the launch has consumed them
+        self._c("bmm_seed_streams", words.data_ptr(), seeds.words.shape[1], first.data_ptr(), self.K, self.B,
+                states.data_ptr(), st)
+
+    def run(self, M: torch.Tensor, N: torch.Tensor, seeds: CallSeeds) -> torch.Tensor:
+        """Approximate products of the batch; returns CD as (B, m, p) (or (m, p))."""
+        B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W
+        dt = _lib.matrix_dtype(M)
+        st = _lib.stream_ptr()
+        sM, sN = m * n, n * p
+        ldm, ldn = M.stride(-2), N.stride(-2)
+        P = lambda t: t.data_ptr()  # noqa: E731
+        self._c("bmm_norms", dt, P(M), m, n, ldm, sM, P(N), p, ldn, sN, B, 0, P(self.colsq), P(self.rowsq), st)
+        if self.method == "SSM":
+            return self._run_ssm(M, N, seeds, dt, st)
+        need_probs = True
+        self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B,
+                P(self.probs) if need_probs else None, P(self.s), None, st)
+        rule = {"ONC": _lib.RULE_ONC, "OPL": _lib.RULE_OPL, "UU": _lib.RULE_UU,
+                "ONU": _lib.RULE_TWO_STEP, "ONMCNR": _lib.RULE_TWO_STEP}[self.method]
+        aux = None
+        if self.method == "OPL":
+            A, Bm = self._f64(M, N)
+            self._c("bmm_segsq_f64", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p, P(self.offsets), K,
+                    0, B, P(self.gsq), P(self.ws_seg), self.ws_seg.numel(), st)
+            aux = self.gsq
+        if self.method in ("ONU", "ONMCNR"):
+            p0 = self.p0 if self.method == "ONU" else self.probs
+            s_for_pilot = None if self.method == "ONU" else self.s
+            self._c("bmm_budgets", _lib.RULE_PILOT, P(s_for_pilot) if s_for_pilot is not None else None, None,
+                    None, None, None, K, B, P(self.p_c), 1, P(self.p_bud), P(self.p_coloff), None, None, None,
+                    P(self.ws_budget), st)
+            self._c("bmm_block_cdf", P(p0), P(self.offsets), K, B, n, P(self.p0cum), P(self.p0last), st)
+            self._seed(seeds.pilot, self.p_states, st)
+            self._c("bmm_sample", P(p0), P(self.p0cum), P(self.p0last), P(self.offsets), K, B, n, P(self.p_bud),
+                    P(self.p_coloff), self.W0, P(self.p_states), P(self.p_column), P(self.p_prob),
+                    P(self.p_scale), st)
+            self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.p_column),
+                    P(self.p_scale), self.W0, self.W0, B, P(self.C0), self.W0, m * self.W0, P(self.D0), p,
+                    self.W0 * p, st)
+            self._c("bmm_segsq_f64", P(self.C0), self.W0, m * self.W0, P(self.D0), p, self.W0 * p, m, p,
+                    P(self.p_coloff), K, K + 1, B, P(self.pilot_sq), P(self.ws_seg), self.ws_seg.numel(), st)
+            aux = self.pilot_sq
+        self._c("bmm_budgets", rule, P(self.s) if rule != _lib.RULE_UU else None, P(aux) if aux is not None else None,
+                P(self.sizes_d), None, None, K, B, P(self.c_arr), int(self.cap), P(self.budgets), P(self.col_off),
+                P(self.status), P(self.diag), P(self.notes), P(self.ws_budget), st)
+        probs = self.probs
+        if self.method == "UU":
+            if not hasattr(self, "_uprobs"):
+                u = np.concatenate([np.full(nk, 1.0 / nk) for nk in self.sizes])
+                self._uprobs = torch.as_tensor(np.tile(u, B), device=M.device)
+            probs = self._uprobs
+        self._c("bmm_block_cdf", P(probs), P(self.offsets), K, B, n, P(self.cum), P(self.last), st)
+        self._seed(seeds.main, self.states, st)
+        self._c("bmm_sample", P(probs), P(self.cum), P(self.last), P(self.offsets), K, B, n, P(self.budgets),
+                P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
+        self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column), P(self.scale),
+                W, W, B, P(self.C), W, m * W, P(self.D), p, W * p, st)
+        self._c("bmm_gemm_f64", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, B, P(self.CD), p, m * p,
+                P(self.ws_gemm), self.ws_gemm.numel(), st)
+        return self.CD.view(B, m, p) if B > 1 else self.CD.view(m, p)
+
+    def _run_ssm(self, M, N, seeds, dt, st):
+        B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W
+        P = lambda t: t.data_ptr()  # noqa: E731
+        self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B, None, None,
+                P(self.fnorm), st)
+        self._c("bmm_normalize", P(self.fnorm), K, B, P(self.q), P(self.status), st)
+        self._c("bmm_block_cdf", P(self.q), P(self.qoff), 1, B, K, P(self.qcum), P(self.qlast), st)
+        states = torch.as_tensor(np.ascontiguousarray(seeds.states).view(np.int64).ravel(), device=M.device)
+        self._keep = states
+        self._c("bmm_sample", P(self.q), P(self.qcum), P(self.qlast), P(self.qoff), 1, B, K, P(self.q_bud),
+                P(self.q_coloff), self.draws, P(states), P(self.blk), P(self.blk_prob), P(self.blk_scale), st)
+        if B != 1:
+            raise NotImplementedError("batched SSM gather")
+        A, Bm = self._f64(M, N)
+        self._c("bmm_gather_blocks", _lib.BMM_F64, P(A), A.stride(-2), P(Bm), Bm.stride(-2), m, p, P(self.offsets),
+                P(self.blk), P(self.blk_scale), P(self.sk_off), self.draws, W, P(self.C), W, P(self.D), p, st)
+        self._c("bmm_gemm_f64", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, B, P(self.CD), p, m * p,
+                P(self.ws_gemm), self.ws_gemm.numel(), st)
+        return self.CD.view(m, p)
+
+    def _f64(self, M, N):
+        if M.dtype == torch.float64:
+            return M, N
+        if getattr(self, "_up", None) is None or self._up[0].shape != M.shape:
+            self._up = (torch.empty(M.shape, dtype=torch.float64, device=M.device),
+                        torch.empty(N.shape, dtype=torch.float64, device=N.device))
+        self._up[0].copy_(M)
+        self._up[1].copy_(N)
+        return self._up
+
+    def check(self) -> None:
+        """Raise the reference's exception for the first failing problem (syncs)."""
+        st = self.status.cpu().numpy()
+        bad = np.flatnonzero(st != 0)
+        if bad.size:
+            b = int(bad[0])
+            raise_status(int(st[b]), int(self.diag[b].item()), self.c)
+
+    # audit views
+    def budgets_host(self) -> np.ndarray:
+        return self.budgets.view(self.B, self.K).cpu().numpy()
+
+    def columns_host(self) -> np.ndarray:
+        if self.method == "SSM":
+            return self.blk.view(self.B, self.draws).cpu().numpy()
+        return self.column.view(self.B, self.W).cpu().numpy()
+
+    def scales_host(self) -> np.ndarray:
+        if self.method == "SSM":
+            return self.blk_scale.view(self.B, self.draws).cpu().numpy()
+        return self.scale.view(self.B, self.W).cpu().numpy()

@@ -1,0 +1,420 @@
+"""Sampling plans -- the reference's ``blockmm.plan`` hot-path surface
+(pkg/src/blockmm/plan.py) with every numeric step on the B200:
+
+* one K1 norm pass feeds probabilities, score sums and budgets (the reference
+  recomputes the norms two or three times per allocator, plan.py:165-173);
+* K2 (bmm_block_probs) gives the per-block probabilities and score sums in
+  NumPy's exact summation order, so they are bit-identical;
+* the block-product norms g_k of the optimal allocator come from the DMMA
+  segmented square-sum GEMM (plan.py:183-188);
+* integer budgets come from the device largest-remainder kernel
+  (bmm_budgets, plan.py:242-347), bit-identical budgets for identical inputs.
+The host only validates arguments, reads back results and builds the same
+frozen records the reference returns.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import rng as _rng
+from .matrix import BlockPartition, device_norms_sq
+
+METHOD_TAGS = ("OPL", "ONC", "ONU", "ONMCNR", "UU", "SSM")
+PROB_SUM_TOL = 1e-12
+RADICAND_SLACK = 1e-9
+
+
+def _check_instance(M, N, part: BlockPartition) -> None:
+    """plan.py:41-46."""
+    if M.ndim != 2 or N.ndim != 2:
+        raise ValueError("factors must be 2-D")
+    if M.shape[1] != N.shape[0]:
+        raise ValueError(f"inner dimensions differ: {M.shape} x {N.shape}")
+    part.check_length(M.shape[1], "inner dimension")
+
+
+@dataclass(frozen=True, eq=False)
+class BlockProbabilities:
+    """Per-block probability vectors (plan.py:49-99): each sums to 1 within
+    PROB_SUM_TOL, or is all zero for a flagged zero-score block."""
+
+    per_block: tuple
+    rule: str = "explicit"
+
+    def __post_init__(self):
+        checked = []
+        for k, vec in enumerate(self.per_block):
+            v = np.ascontiguousarray(vec, dtype=np.float64)
+            if v.ndim != 1 or v.size == 0:
+                raise ValueError(f"block {k}: probabilities must be a nonempty vector")
+            if not np.isfinite(v).all() or (v < 0).any():
+                raise ValueError(f"block {k}: probabilities must be finite and >= 0")
+            tot = v.sum()
+            if tot != 0.0 and abs(tot - 1.0) > PROB_SUM_TOL:
+                raise ValueError(f"block {k}: probabilities sum to {tot!r}, not 1")
+            checked.append(v)
+        object.__setattr__(self, "per_block", tuple(checked))
+
+    def __len__(self) -> int:
+        return len(self.per_block)
+
+    def __getitem__(self, k: int) -> np.ndarray:
+        return self.per_block[k]
+
+    @property
+    def num_blocks(self) -> int:
+        return len(self.per_block)
+
+    @property
+    def zero_blocks(self) -> tuple:
+        return tuple(k for k, v in enumerate(self.per_block) if v.sum() == 0.0)
+
+    def check_partition(self, part: BlockPartition) -> None:
+        if len(self.per_block) != part.num_blocks:
+            raise ValueError(f"probabilities cover {len(self.per_block)} blocks, "
+                             f"partition has {part.num_blocks}")
+        for k, (v, nk) in enumerate(zip(self.per_block, part.sizes)):
+            if v.size != nk:
+                raise ValueError(f"block {k}: {v.size} probabilities for {nk} columns")
+
+    def flat(self) -> np.ndarray:
+        """All blocks concatenated in partition order (the device layout)."""
+        return np.concatenate(self.per_block) if self.per_block else np.zeros(0)
+
+
+@dataclass(frozen=True, eq=False)
+class BlockScores:
+    """Score sums s_k and block-product norms g_k (plan.py:102-122)."""
+
+    score_sums: np.ndarray
+    product_norms: np.ndarray
+    exact: bool = True
+
+    def __post_init__(self):
+        s = np.asarray(self.score_sums, dtype=np.float64)
+        g = np.asarray(self.product_norms, dtype=np.float64)
+        if s.ndim != 1 or s.shape != g.shape:
+            raise ValueError("score_sums and product_norms must be matching vectors")
+        if (s < 0).any() or (g < 0).any():
+            raise ValueError("scores must be nonnegative")
+        if self.exact and (g > s * (1 + RADICAND_SLACK) + 1e-300).any():
+            raise ValueError("exact product norm exceeds score sum (Cauchy-Schwarz violated)")
+        object.__setattr__(self, "score_sums", s)
+        object.__setattr__(self, "product_norms", g)
+
+
+@dataclass(frozen=True, eq=False)
+class SamplingPlan:
+    """Partition + probabilities + integer budgets (plan.py:125-162)."""
+
+    partition: BlockPartition
+    probs: BlockProbabilities
+    budgets: np.ndarray
+    method: str = ""
+    notes: tuple = ()
+    pilot_norms: Optional[np.ndarray] = None
+
+    def __post_init__(self):
+        b = np.asarray(self.budgets)
+        if b.dtype.kind not in "iu" and not np.array_equal(b, np.round(b)):
+            raise ValueError("budgets must be integers")
+        b = b.astype(np.int64)
+        if b.ndim != 1 or b.size != self.partition.num_blocks:
+            raise ValueError("budgets must be one integer per block")
+        if (b < 0).any():
+            raise ValueError("budgets must be >= 0")
+        self.probs.check_partition(self.partition)
+        zero = set(self.probs.zero_blocks)
+        for k in range(self.partition.num_blocks):
+            if (b[k] == 0) != (k in zero):
+                raise ValueError(f"block {k}: zero budget and zero-probability flag must coincide")
+        object.__setattr__(self, "budgets", b)
+        if self.pilot_norms is not None:
+            pn = np.asarray(self.pilot_norms, dtype=np.float64)
+            if pn.shape != (self.partition.num_blocks,):
+                raise ValueError("pilot_norms must be one value per block")
+            object.__setattr__(self, "pilot_norms", pn)
+
+    @property
+    def total(self) -> int:
+        return int(self.budgets.sum())
+
+
+# ---------------------------------------------------------------- device core
+
+class DeviceInstance:
+    """Device copies of (M, N) plus the products of one K1 norm pass.
+
+    Every plan / estimator entry point builds one of these, so a single norm
+    pass feeds probabilities, score sums and budgets."""
+
+    def __init__(self, M, N, part: BlockPartition):
+        _check_instance(M, N, part)
+        self.M = _lib.float_matrix(M)
+        self.N = _lib.float_matrix(N)
+        if self.N.dtype != self.M.dtype:
+            self.N = self.N.to(torch.float64)
+            self.M = self.M.to(torch.float64)
+        self.part = part
+        self.K = part.num_blocks
+        self.n = int(self.M.shape[1])
+        self.offsets = _lib.i64(part.offsets)
+        self.sizes = _lib.i64(part.sizes)
+        self._norms = None
+
+    @property
+    def norms(self):
+        if self._norms is None:
+            self._norms = device_norms_sq(self.M, self.N)
+        return self._norms
+
+    def block_stats(self, probs=True, s=True, fnorm=False):
+        colsq, rowsq = self.norms
+        dev = colsq.device
+        pr = torch.empty(self.n, dtype=torch.float64, device=dev) if probs else None
+        sk = torch.empty(self.K, dtype=torch.float64, device=dev) if s else None
+        fk = torch.empty(self.K, dtype=torch.float64, device=dev) if fnorm else None
+        _lib.call("bmm_block_probs", _lib.ptr(colsq), _lib.ptr(rowsq), self.n, _lib.ptr(self.offsets),
+                  self.K, 1, _lib.ptr(pr), _lib.ptr(sk), _lib.ptr(fk), _lib.stream_ptr())
+        return pr, sk, fk
+
+    def block_product_sq(self) -> torch.Tensor:
+        """g_k^2 = ||M^k N_k||_F^2 for every block (DMMA segmented square sums)."""
+        return segsq(self.M, self.N, self.offsets, self.K)
+
+
+def segsq(A: torch.Tensor, B: torch.Tensor, seg: torch.Tensor, nseg: int) -> torch.Tensor:
+    if A.dtype != torch.float64:
+        A = A.to(torch.float64)
+    if B.dtype != torch.float64:
+        B = B.to(torch.float64)
+    m, p = A.shape[0], B.shape[1]
+    out = torch.empty(nseg, dtype=torch.float64, device=A.device)
+    wsb = _lib.load().bmm_segsq_f64_workspace(m, p, nseg, 1)
+    ws = _lib.workspace(wsb)
+    _lib.call("bmm_segsq_f64", _lib.ptr(A), A.stride(0), 0, _lib.ptr(B), B.stride(0), 0, m, p,
+              _lib.ptr(seg), nseg, 0, 1, _lib.ptr(out), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    return out
+
+
+def split_blocks(flat: np.ndarray, part: BlockPartition) -> tuple:
+    off = part.offsets
+    return tuple(flat[off[k]:off[k + 1]].copy() for k in range(part.num_blocks))
+
+
+def raise_status(st: int, diag: int, c: int) -> None:
+    """Map a device status code to the reference's exception."""
+    if st == _lib.ST_OK:
+        return
+    msgs = {
+        _lib.ST_ZERO_SCORE: "all blocks have zero score: nothing to sample",
+        _lib.ST_CAUCHY_SCHWARZ: "exact product norm exceeds score sum (Cauchy-Schwarz violated)",
+        _lib.ST_RADICAND: "radicand negative beyond rounding slack",
+        _lib.ST_ALL_ZERO_WEIGHT: "all weights are zero",
+        _lib.ST_BAD_WEIGHT: "weights must be finite and >= 0",
+        _lib.ST_CAP_BELOW_FLOOR: "some cap lies below the required floor of 1",
+        _lib.ST_BELOW_FLOORS: f"budget c={c} is below the {diag} required floors",
+        _lib.ST_ABOVE_CAPS: f"budget c={c} exceeds the total caps {diag}",
+        _lib.ST_EMPTY_SUPPORT: "probability vector has empty support",
+    }
+    if st == _lib.ST_NO_CONVERGE:
+        raise AssertionError("apportionment did not converge")
+    if st == _lib.ST_NOT_PLACED:
+        raise AssertionError("apportionment failed to place the full budget")
+    raise ValueError(msgs.get(st, f"device status {st}"))
+
+
+def device_budgets(rule: int, K: int, c: int, *, s=None, aux=None, sizes=None, caps=None,
+                   floors=None, cap=True):
+    """Run bmm_budgets for one problem; returns (budgets int64 ndarray, notes flag)."""
+    dev = _lib.device()
+    budgets = torch.empty(K, dtype=torch.int64, device=dev)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    diag = torch.empty(1, dtype=torch.int64, device=dev)
+    notes = torch.empty(1, dtype=torch.int32, device=dev)
+    ws = _lib.workspace(_lib.load().bmm_budgets_workspace(K))
+    cd = _lib.i64([c])
+    _lib.call("bmm_budgets", rule, _lib.ptr(s), _lib.ptr(aux), _lib.ptr(sizes), _lib.ptr(caps),
+              _lib.ptr(floors), K, 1, _lib.ptr(cd), int(bool(cap)), _lib.ptr(budgets), None,
+              _lib.ptr(status), _lib.ptr(diag), _lib.ptr(notes), _lib.ptr(ws), _lib.stream_ptr())
+    st, dg, nt = int(status.item()), int(diag.item()), int(notes.item())
+    raise_status(st, dg, c)
+    return _lib.host(budgets), nt
+
+
+# ---------------------------------------------------------------- public API
+
+def score_sums(M, N, part: BlockPartition):
+    """s_k = sum over block k of ||M col|| * ||N row|| (plan.py:170-173)."""
+    inst = DeviceInstance(M, N, part)
+    _, s, _ = inst.block_stats(probs=False, s=True)
+    return _lib.host(s) if _lib.want_numpy(M, N) else s
+
+
+def block_scores(M, N, part: BlockPartition) -> BlockScores:
+    """Score sums and exact block-product norms (plan.py:176-189)."""
+    inst = DeviceInstance(M, N, part)
+    _, s, _ = inst.block_stats(probs=False, s=True)
+    g = torch.sqrt(inst.block_product_sq())
+    return BlockScores(_lib.host(s), _lib.host(g), exact=True)
+
+
+def optimal_probabilities(M, N, part: BlockPartition) -> BlockProbabilities:
+    """p_i proportional to ||M col i|| * ||N row i|| per block (plan.py:192-206)."""
+    inst = DeviceInstance(M, N, part)
+    pr, _, _ = inst.block_stats(probs=True, s=False)
+    return BlockProbabilities(split_blocks(_lib.host(pr), part), rule="optimal")
+
+
+def uniform_probabilities(part: BlockPartition) -> BlockProbabilities:
+    """1/n_k within every block (plan.py:209-212)."""
+    return BlockProbabilities(tuple(np.full(nk, 1.0 / nk) for nk in part.sizes), rule="uniform")
+
+
+def integerize(weights, c: int, caps=None, floor=None) -> np.ndarray:
+    """Largest-remainder split of c into integer block counts with floors and
+    caps (plan.py:242-347), on device (bmm_budgets, rule EXPLICIT)."""
+    w = np.asarray(weights, dtype=np.float64)
+    if w.ndim != 1 or w.size == 0:
+        raise ValueError("weights must be a nonempty vector")
+    if not np.isfinite(w).all() or (w < 0).any():
+        raise ValueError("weights must be finite and >= 0")
+    if not (w > 0).any():
+        raise ValueError("all weights are zero")
+    c = int(c)
+    if c < 0:
+        raise ValueError("budget must be >= 0")
+    K = w.size
+    fl = None
+    if floor is not None:
+        fl = np.asarray(floor, dtype=bool)
+        if fl.shape != (K,):
+            raise ValueError("floor mask must have one entry per block")
+    cp = None
+    if caps is not None:
+        cp = np.asarray(caps, dtype=np.int64)
+        if cp.shape != (K,):
+            raise ValueError("caps must have one entry per block")
+    dev = _lib.device()
+    wd = _lib.f64(w)
+    capd = _lib.i64(cp) if cp is not None else None
+    fld = torch.as_tensor(fl.astype(np.uint8), device=dev) if fl is not None else None
+    budgets, _ = device_budgets(_lib.RULE_EXPLICIT, K, c, aux=wd, caps=capd, floors=fld)
+    return budgets
+
+
+def optimal_size_weights(M, N, part: BlockPartition) -> np.ndarray:
+    """sqrt(s_k^2 - g_k^2) with exact g_k (plan.py:350-361)."""
+    sc = block_scores(M, N, part)
+    # K-length bookkeeping on the device-computed s and g
+    rad = sc.score_sums ** 2 - sc.product_norms ** 2
+    bad = rad < -RADICAND_SLACK * sc.score_sums ** 2
+    if bad.any():
+        raise ValueError(f"radicand negative beyond rounding slack in blocks {np.where(bad)[0]}")
+    return np.sqrt(np.maximum(rad, 0.0))
+
+
+def real_optimal_budgets(M, N, part: BlockPartition, c: int) -> np.ndarray:
+    """c * w_k / sum(w) before integerization (plan.py:364-370)."""
+    w = optimal_size_weights(M, N, part)
+    tot = w.sum()
+    if tot == 0.0:
+        raise ValueError("all optimal size weights are zero")
+    return c * w / tot
+
+
+_FALLBACK_NOTES = {
+    "OPL": ("optimal size weights all zero; fell back to score-sum sizes",),
+    "TWO": ("pilot size weights all zero; fell back to score-sum sizes",),
+}
+
+
+def allocate_optimal(M, N, part: BlockPartition, c: int, cap: bool = True) -> SamplingPlan:
+    """Variance-minimising plan, tag OPL (plan.py:383-400; Eq. 3.9)."""
+    inst = DeviceInstance(M, N, part)
+    pr, s, _ = inst.block_stats(probs=True, s=True)
+    gsq = inst.block_product_sq()
+    budgets, note = device_budgets(_lib.RULE_OPL, inst.K, int(c), s=s, aux=gsq, sizes=inst.sizes, cap=cap)
+    probs = BlockProbabilities(split_blocks(_lib.host(pr), part), rule="optimal")
+    return SamplingPlan(part, probs, budgets, method="OPL", notes=_FALLBACK_NOTES["OPL"] if note else ())
+
+
+def allocate_by_score_sums(M, N, part: BlockPartition, c: int, cap: bool = True) -> SamplingPlan:
+    """Score-sum sizes, tag ONC (plan.py:403-413; Eq. 4.2)."""
+    inst = DeviceInstance(M, N, part)
+    pr, s, _ = inst.block_stats(probs=True, s=True)
+    budgets, _ = device_budgets(_lib.RULE_ONC, inst.K, int(c), s=s, sizes=inst.sizes, cap=cap)
+    probs = BlockProbabilities(split_blocks(_lib.host(pr), part), rule="optimal")
+    return SamplingPlan(part, probs, budgets, method="ONC")
+
+
+def allocate_uniform(part: BlockPartition, c: int, cap: bool = True) -> SamplingPlan:
+    """Uniform probabilities and c/K sizes, tag UU (plan.py:416-421)."""
+    budgets, _ = device_budgets(_lib.RULE_UU, part.num_blocks, int(c), sizes=_lib.i64(part.sizes), cap=cap)
+    return SamplingPlan(part, uniform_probabilities(part), budgets, method="UU")
+
+
+def allocate_two_step(M, N, part: BlockPartition, c: int, c0: int, p0: BlockProbabilities,
+                      rng: np.random.Generator, cap: bool = True,
+                      method: Optional[str] = None) -> SamplingPlan:
+    """Pilot-then-allocate plan, tags ONU/ONMCNR (plan.py:424-480; Alg. 3).
+
+    floor(c0/K) pilot draws per block on child streams rng.spawn(K); the pilot
+    norms ||C0 D0||_F come from the DMMA segmented square-sum GEMM."""
+    from .estimators import sample_blocks, gather_sketch  # estimators builds on plans
+
+    _check_instance(M, N, part)
+    p0.check_partition(part)
+    K = part.num_blocks
+    pilot_count = int(c0) // K
+    if pilot_count < 1:
+        raise ValueError(f"c0={c0} gives no pilot draws for K={K} blocks")
+    inst = DeviceInstance(M, N, part)
+    _, s, _ = inst.block_stats(probs=False, s=True)
+    s_host = _lib.host(s)
+    if s_host.sum() == 0.0:
+        raise ValueError("all blocks have zero score: nothing to sample")
+    live = np.array([v.sum() != 0.0 for v in p0.per_block])
+    for k in np.flatnonzero(live):  # sketch_columns validation (estimators.py:75-76)
+        if abs(p0[k].sum() - 1.0) > 1e-9:
+            raise ValueError("probabilities must be >= 0 and sum to 1")
+    words, first = _rng.spawn_words(rng, K)
+    pilot_budgets = np.where(live, pilot_count, 0).astype(np.int64)
+    col, prob, scale, col_off = sample_blocks(inst, p0.flat(), pilot_budgets, words, first)
+    W0 = int(col_off[-1].item()) if K else 0
+    if W0 > 0:
+        C0, D0 = gather_sketch(inst, col, scale, W0, dtype=torch.float64)
+        pilot_sq = segsq(C0, D0, col_off, K)
+    else:
+        pilot_sq = torch.zeros(K, dtype=torch.float64, device=s.device)
+    budgets, note = device_budgets(_lib.RULE_TWO_STEP, K, int(c), s=s, aux=pilot_sq, sizes=inst.sizes,
+                                   cap=cap)
+    pilot = torch.sqrt(pilot_sq)
+    if method is None:
+        method = "ONU" if p0.rule == "uniform" else "ONMCNR"
+    pr, _, _ = inst.block_stats(probs=True, s=False)
+    probs = BlockProbabilities(split_blocks(_lib.host(pr), part), rule="optimal")
+    return SamplingPlan(part, probs, budgets, method=method,
+                        notes=_FALLBACK_NOTES["TWO"] if note else (), pilot_norms=_lib.host(pilot))
+
+
+def block_norm_probabilities(M, N, part: BlockPartition):
+    """Whole-block probabilities q_k ∝ ||M^k||_F ||N_k||_F, tag SSM (plan.py:483-496)."""
+    inst = DeviceInstance(M, N, part)
+    q, st = inst_block_q(inst)
+    if st != _lib.ST_OK:
+        raise ValueError("all blocks have zero norm: nothing to sample")
+    return _lib.host(q) if _lib.want_numpy(M, N) else q
+
+
+def inst_block_q(inst: DeviceInstance):
+    _, _, f = inst.block_stats(probs=False, s=False, fnorm=True)
+    q = torch.empty(inst.K, dtype=torch.float64, device=f.device)
+    status = torch.empty(1, dtype=torch.int32, device=f.device)
+    _lib.call("bmm_normalize", _lib.ptr(f), inst.K, 1, _lib.ptr(q), _lib.ptr(status), _lib.stream_ptr())
+    return q, int(status.item())

@@ -1,0 +1,88 @@
+"""Host-side logic of the product package that runs without a GPU: generator
+side effects, argument validation and record types."""
+import numpy as np
+import pytest
+
+from oracle import numpy_rng as R
+from paper_2105_04940_b200 import rng as hrng
+from paper_2105_04940_b200.matrix import BlockPartition
+from paper_2105_04940_b200.plan import BlockProbabilities, SamplingPlan, raise_status
+from paper_2105_04940_b200 import _lib
+
+
+@pytest.mark.parametrize("seed", [5, 2**70 + 3, [1, 2, 3]])
+def test_spawn_words_match_numpy_children(seed):
+    rng = np.random.default_rng(seed)
+    rng.spawn(2)
+    ref = np.random.default_rng(seed)
+    ref.spawn(2)
+    kids = ref.spawn(5)
+    words, first = hrng.spawn_words(rng, 5)
+    assert first == 2
+    for j, kid in enumerate(kids):
+        assert R.pool_from_assembled(list(map(int, words)) + [first + j]) == list(kid.bit_generator.seed_seq.pool)
+    # side effect: the parent's counter advanced exactly like rng.spawn(5)
+    assert rng.bit_generator.seed_seq.n_children_spawned == 7
+    assert rng.spawn(1)[0].random() == ref.spawn(1)[0].random()
+
+
+def test_spawn_words_nested_key():
+    rng = np.random.default_rng(11)
+    child = rng.spawn(2)[1]  # key (1,)
+    words, first = hrng.spawn_words(child, 3)
+    kid = np.random.default_rng(11).spawn(2)[1].spawn(3)[2]
+    assert R.pool_from_assembled(list(map(int, words)) + [first + 2]) == list(kid.bit_generator.seed_seq.pool)
+
+
+def test_consume_matches_random():
+    a = np.random.default_rng(3)
+    b = np.random.default_rng(3)
+    a.integers(0, 2**32, dtype=np.uint32)  # leaves a buffered 32-bit half
+    b.integers(0, 2**32, dtype=np.uint32)
+    hrng.consume(a, 7)
+    b.random(7)
+    assert a.bit_generator.state == b.bit_generator.state
+    st = hrng.stream_state(a)
+    s = b.bit_generator.state["state"]
+    assert (int(st[0]) << 64 | int(st[1])) == s["state"] and (int(st[2]) << 64 | int(st[3])) == s["inc"]
+
+
+def test_non_pcg64_generator_rejected():
+    with pytest.raises(ValueError):
+        hrng.spawn_words(np.random.Generator(np.random.Philox(1)), 2)
+
+
+def test_partition_and_plan_validation():
+    part = BlockPartition((3, 5))
+    assert part.offsets.tolist() == [0, 3, 8] and part.total == 8
+    assert part.block_slice(1) == slice(3, 8)
+    with pytest.raises(IndexError):
+        part.block_slice(2)
+    with pytest.raises(ValueError):
+        BlockPartition(())
+    with pytest.raises(ValueError):
+        BlockPartition.equal(10, 3)
+    probs = BlockProbabilities((np.full(3, 1 / 3), np.zeros(5)))
+    assert probs.zero_blocks == (1,)
+    SamplingPlan(part, probs, np.array([2, 0]))
+    with pytest.raises(ValueError):
+        SamplingPlan(part, probs, np.array([2, 1]))
+    with pytest.raises(ValueError):
+        BlockProbabilities((np.array([0.5, 0.4]),))
+
+
+def test_status_mapping():
+    raise_status(_lib.ST_OK, 0, 5)
+    with pytest.raises(ValueError, match="below the 100 required floors"):
+        raise_status(_lib.ST_BELOW_FLOORS, 100, 20)
+    with pytest.raises(AssertionError):
+        raise_status(_lib.ST_NOT_PLACED, 0, 1)
+
+
+def test_product_path_fails_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2105_04940_b200 as bm
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        bm.column_norms(np.ones((2, 2)))
