@@ -199,19 +199,19 @@ def run_ours(args):
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
-    def step(Mx, Nx, gemm_events=None):
+    def step(Mx, Nx):
         outs = []
         for (cb, W, meth, c0), pipe in zip(runs, pipes):
             rng = workloads.sample_rng(cfg, cb)
             seeds = seeds_from_rngs(meth, [rng], K)
-            if gemm_events is not None:
-                pipe.gemm_events = gemm_events
             outs.append(pipe.run(Mx, Nx, seeds))
         return outs
 
-    # correctness of the bench configuration itself (untimed)
+    # correctness of the bench configuration itself (untimed), then graph capture
     for pipe_out, pipe in zip(step(Md, Nd), pipes):
         pipe.check()
+    for pipe in pipes:
+        pipe.capture(Md, Nd)
     for _ in range(args.warmup):
         step(Md, Nd)
     torch.cuda.synchronize()
@@ -219,7 +219,6 @@ def run_ours(args):
     # ---- device-timed steps (inputs resident, L2 flushed before each step)
     n_launch0 = _lib.launches()
     times = []
-    gemm_ev = []
     with ClockSampler(local) as clocks:
         if world > 1:
             dist.barrier()
@@ -228,7 +227,7 @@ def run_ours(args):
             flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step(Md, Nd, gemm_ev)
+            step(Md, Nd)
             e1.record(stream)
             times.append((e0, e1))
         torch.cuda.synchronize()
@@ -245,8 +244,7 @@ def run_ours(args):
     # ---- e2e through the public API with host buffers (pinned) every step
     M_pin = torch.from_numpy(M_h).pin_memory()
     N_pin = torch.from_numpy(N_h).pin_memory()
-    Mx = torch.empty_like(Md)
-    Nx = torch.empty_like(Nd)
+    Mx, Nx = Md, Nd  # the captured graphs read these buffers
     outs_h = [torch.empty((m, p), dtype=torch.float64).pin_memory() for _ in runs]
     e2e = []
     for it in range(args.warmup + args.steps):

@@ -369,12 +369,14 @@ extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const
                    lda % 2 == 0 && ldb % 2 == 0 && strideA % 2 == 0 && strideB % 2 == 0;
   dim3 grid((unsigned)ceil_div(nc, GB_N), (unsigned)ceil_div(m, GB_M), (unsigned)(batch * sp.splits));
   if (v16) {
-    cudaFuncSetAttribute(gemm_f64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES);
+    static bool attr_t = false;
+    if (!attr_t) { cudaFuncSetAttribute(gemm_f64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES); attr_t = true; }
     gemm_f64_kernel<true><<<grid, G_THREADS, G_SMEM_BYTES, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k,
                                                                 sp.splits, sp.kchunk, out, ldo, strideO,
                                                                 (double*)ws);
   } else {
-    cudaFuncSetAttribute(gemm_f64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES);
+    static bool attr_f = false;
+    if (!attr_f) { cudaFuncSetAttribute(gemm_f64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES); attr_f = true; }
     gemm_f64_kernel<false><<<grid, G_THREADS, G_SMEM_BYTES, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k,
                                                                  sp.splits, sp.kchunk, out, ldo, strideO,
                                                                  (double*)ws);
@@ -404,7 +406,8 @@ extern "C" int bmm_segsq_f64(const double* A, int64_t lda, int64_t strideA, cons
   cudaStream_t st = as_stream(stream);
   const int64_t chunks = segsq_chunks(m, nc, nseg, batch);
   dim3 grid((unsigned)ceil_div(nc, GB_N), (unsigned)ceil_div(m, GB_M), (unsigned)(batch * chunks));
-  cudaFuncSetAttribute(segsq_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES);
+  static bool attr_s = false;
+  if (!attr_s) { cudaFuncSetAttribute(segsq_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES); attr_s = true; }
   segsq_f64_kernel<<<grid, G_THREADS, G_SMEM_BYTES, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg,
                                                           seg_stride, chunks, (double*)ws);
   BMM_CHECK_LAUNCH("segsq_f64_kernel");

@@ -164,7 +164,10 @@ class SketchPipeline:
                 self.p0 = torch.as_tensor(np.tile(u, B), device=dev)
             self.p0cum = torch.empty(B * n_, **f64)
             self.p0last = torch.empty(B * K, **i64)
-        self._words = None
+        if method == "UU":
+            u = np.concatenate([np.full(nk, 1.0 / nk) for nk in self.sizes])
+            self._uprobs = torch.as_tensor(np.tile(u, B), device=dev)
+        self.graph = None
 
     # ------------------------------------------------------------------ steps
     def _c(self, name, *args):
@@ -172,16 +175,74 @@ class SketchPipeline:
         if rc < 0:
             raise RuntimeError(f"{name} failed ({rc}): {self.lib.bmm_last_error().decode()}")
 
-    def _seed(self, seeds: StreamSeeds, states: torch.Tensor, st):
-        dev = states.device
-        words = torch.as_tensor(np.ascontiguousarray(seeds.words).view(np.int32), device=dev)
-        first = torch.as_tensor(seeds.first, device=dev)
-        self._keep = (words, first)  # keep alive until the launch has consumed them
-        self._c("bmm_seed_streams", words.data_ptr(), seeds.words.shape[1], first.data_ptr(), self.K, self.B,
+    def _seed(self, which: str, states: torch.Tensor, st):
+        words, first = self._seedbuf[which]
+        self._c("bmm_seed_streams", words.data_ptr(), words.shape[1], first.data_ptr(), self.K, self.B,
                 states.data_ptr(), st)
+
+    # ---- per-call seed material: pinned staging -> async copy into fixed device buffers
+    def set_seeds(self, seeds: CallSeeds) -> None:
+        """Stage this call's seeds (host numpy) into the device buffers the
+        launch sequence reads; async, double-buffered pinned staging."""
+        items = {}
+        if seeds.main is not None:
+            items["main"] = seeds.main
+        if seeds.pilot is not None:
+            items["pilot"] = seeds.pilot
+        if seeds.states is not None:
+            items["states"] = seeds.states
+        if not hasattr(self, "_seedbuf"):
+            self._seedbuf, self._stage, self._stage_ev, self._slot = {}, [{}, {}], [None, None], 0
+        self._slot ^= 1
+        ev = self._stage_ev[self._slot]
+        if ev is not None:
+            ev.synchronize()
+        stage = self._stage[self._slot]
+        dev = self.colsq.device
+        for key, val in items.items():
+            arrs = ((np.ascontiguousarray(val.words).view(np.int32), np.ascontiguousarray(val.first, dtype=np.int64))
+                    if key != "states" else (np.ascontiguousarray(val).view(np.int64).reshape(self.B, 4),))
+            if key not in self._seedbuf:
+                self._seedbuf[key] = tuple(torch.empty(a.shape, dtype=torch.from_numpy(a).dtype, device=dev)
+                                           for a in arrs)
+            if key not in stage:
+                stage[key] = tuple(torch.empty(a.shape, dtype=torch.from_numpy(a).dtype).pin_memory() for a in arrs)
+            for dst, pin, a in zip(self._seedbuf[key], stage[key], arrs):
+                if tuple(dst.shape) != a.shape:
+                    raise ValueError("seed material changed shape; build a new pipeline")
+                pin.numpy()[...] = a
+                dst.copy_(pin, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._stage_ev[self._slot] = ev
+
+    def capture(self, M: torch.Tensor, N: torch.Tensor) -> None:
+        """Record the launch sequence for these input buffers as a CUDA graph."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.launch(M, N)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch(M, N)
+        self.graph, self._graph_ptrs = g, (M.data_ptr(), N.data_ptr())
 
     def run(self, M: torch.Tensor, N: torch.Tensor, seeds: CallSeeds) -> torch.Tensor:
         """Approximate products of the batch; returns CD as (B, m, p) (or (m, p))."""
+        self.set_seeds(seeds)
+        if getattr(self, "graph", None) is not None and self._graph_ptrs == (M.data_ptr(), N.data_ptr()):
+            self.graph.replay()
+            return self._result()
+        return self.launch(M, N)
+
+    def _result(self):
+        if self.method == "SSM":
+            return self.CD.view(self.m, self.p)
+        return self.CD.view(self.B, self.m, self.p) if self.B > 1 else self.CD.view(self.m, self.p)
+
+    def launch(self, M: torch.Tensor, N: torch.Tensor) -> torch.Tensor:
+        """Enqueue the whole pipeline on the current stream (graph-capturable)."""
         B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W
         dt = _lib.matrix_dtype(M)
         st = _lib.stream_ptr()
@@ -190,7 +251,7 @@ class SketchPipeline:
         P = lambda t: t.data_ptr()  # noqa: E731
         self._c("bmm_norms", dt, P(M), m, n, ldm, sM, P(N), p, ldn, sN, B, 0, P(self.colsq), P(self.rowsq), st)
         if self.method == "SSM":
-            return self._run_ssm(M, N, seeds, dt, st)
+            return self._run_ssm(M, N, dt, st)
         need_probs = True
         self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B,
                 P(self.probs) if need_probs else None, P(self.s), None, st)
@@ -209,7 +270,7 @@ class SketchPipeline:
                     None, None, None, K, B, P(self.p_c), 1, P(self.p_bud), P(self.p_coloff), None, None, None,
                     P(self.ws_budget), st)
             self._c("bmm_block_cdf", P(p0), P(self.offsets), K, B, n, P(self.p0cum), P(self.p0last), st)
-            self._seed(seeds.pilot, self.p_states, st)
+            self._seed("pilot", self.p_states, st)
             self._c("bmm_sample", P(p0), P(self.p0cum), P(self.p0last), P(self.offsets), K, B, n, P(self.p_bud),
                     P(self.p_coloff), self.W0, P(self.p_states), P(self.p_column), P(self.p_prob),
                     P(self.p_scale), st)
@@ -222,14 +283,9 @@ class SketchPipeline:
         self._c("bmm_budgets", rule, P(self.s) if rule != _lib.RULE_UU else None, P(aux) if aux is not None else None,
                 P(self.sizes_d), None, None, K, B, P(self.c_arr), int(self.cap), P(self.budgets), P(self.col_off),
                 P(self.status), P(self.diag), P(self.notes), P(self.ws_budget), st)
-        probs = self.probs
-        if self.method == "UU":
-            if not hasattr(self, "_uprobs"):
-                u = np.concatenate([np.full(nk, 1.0 / nk) for nk in self.sizes])
-                self._uprobs = torch.as_tensor(np.tile(u, B), device=M.device)
-            probs = self._uprobs
+        probs = self._uprobs if self.method == "UU" else self.probs
         self._c("bmm_block_cdf", P(probs), P(self.offsets), K, B, n, P(self.cum), P(self.last), st)
-        self._seed(seeds.main, self.states, st)
+        self._seed("main", self.states, st)
         self._c("bmm_sample", P(probs), P(self.cum), P(self.last), P(self.offsets), K, B, n, P(self.budgets),
                 P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
         self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column), P(self.scale),
@@ -238,15 +294,14 @@ class SketchPipeline:
                 P(self.ws_gemm), self.ws_gemm.numel(), st)
         return self.CD.view(B, m, p) if B > 1 else self.CD.view(m, p)
 
-    def _run_ssm(self, M, N, seeds, dt, st):
+    def _run_ssm(self, M, N, dt, st):
         B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W
         P = lambda t: t.data_ptr()  # noqa: E731
         self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B, None, None,
                 P(self.fnorm), st)
         self._c("bmm_normalize", P(self.fnorm), K, B, P(self.q), P(self.status), st)
         self._c("bmm_block_cdf", P(self.q), P(self.qoff), 1, B, K, P(self.qcum), P(self.qlast), st)
-        states = torch.as_tensor(np.ascontiguousarray(seeds.states).view(np.int64).ravel(), device=M.device)
-        self._keep = states
+        (states,) = self._seedbuf["states"]
         self._c("bmm_sample", P(self.q), P(self.qcum), P(self.qlast), P(self.qoff), 1, B, K, P(self.q_bud),
                 P(self.q_coloff), self.draws, P(states), P(self.blk), P(self.blk_prob), P(self.blk_scale), st)
         if B != 1:

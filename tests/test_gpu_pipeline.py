@@ -1,0 +1,85 @@
+"""The device-resident pipeline (paper_2105_04940_b200.pipeline) is bit-identical
+to the per-call API and to the oracle, eagerly, under CUDA-graph replay and
+batched over problems."""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import blockmm_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+bm = pytest.importorskip("paper_2105_04940_b200")
+from paper_2105_04940_b200.pipeline import SketchPipeline, seeds_from_rngs  # noqa: E402
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b))
+
+
+@pytest.mark.parametrize("method", ["OPL", "ONC", "UU", "ONU", "ONMCNR"])
+@pytest.mark.parametrize("graph", [False, True])
+def test_pipeline_matches_oracle(method, graph):
+    M, N, sizes = workloads.cfg2(n=4000, m=60, p=50, K=12)
+    c, c0 = 300, 120
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    pipe = SketchPipeline(60, 4000, 50, sizes, c, method, c0=c0)
+    if graph:
+        pipe.run(Md, Nd, seeds_from_rngs(method, [np.random.default_rng(1)], len(sizes)))
+        pipe.capture(Md, Nd)
+    for seed in (5, 6):
+        rng = np.random.default_rng(seed)
+        CD = pipe.run(Md, Nd, seeds_from_rngs(method, [rng], len(sizes))).cpu().numpy()
+        pipe.check()
+        ref = O.approx_product(M, N, sizes, c, method, np.random.default_rng(seed), c0=c0)
+        assert np.array_equal(pipe.budgets_host()[0], ref["budgets"]), method
+        assert np.array_equal(pipe.columns_host()[0], ref["columns"]), method
+        assert np.array_equal(pipe.scales_host()[0], ref["scale"]), method
+        assert rel(CD, ref["CD"]) < 1e-12
+
+
+def test_pipeline_ssm_matches_oracle():
+    M, N, sizes = workloads.cfg1(scale=10)
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    pipe = SketchPipeline(M.shape[0], M.shape[1], N.shape[1], sizes, 0, "SSM", draws=4)
+    rng_a, rng_b = np.random.default_rng(3), np.random.default_rng(3)
+    CD = pipe.run(Md, Nd, seeds_from_rngs("SSM", [rng_a], len(sizes), draws=4)).cpu().numpy()
+    ref = O.ssm_product(M, N, sizes, 4, rng_b)
+    assert np.array_equal(pipe.columns_host()[0], ref["blocks"])
+    np.testing.assert_allclose(pipe.scales_host()[0], ref["scale"], rtol=1e-13)
+    assert rel(CD, ref["CD"]) < 1e-12
+    assert rng_a.bit_generator.state == rng_b.bit_generator.state
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_pipeline_batched_matches_per_problem(dtype):
+    B, m, n, p, K = 5, 32, 1024, 24, 16
+    Ms, Ns = [], []
+    for b in range(B):
+        g = np.random.default_rng(100 + b)
+        Ms.append((g.standard_normal((m, n)) * g.lognormal(0, 1, n)).astype(dtype))
+        Ns.append((g.standard_normal((n, p)) * g.lognormal(0, 1, (n, 1))).astype(dtype))
+    Md = torch.as_tensor(np.stack(Ms), device="cuda")
+    Nd = torch.as_tensor(np.stack(Ns), device="cuda")
+    sizes = (n // K,) * K
+    c = 256
+    for method in ("ONC", "OPL"):
+        pipe = SketchPipeline(m, n, p, sizes, c, method, batch=B)
+        rngs = [workloads.sample_rng(5, b) for b in range(B)]
+        CD = pipe.run(Md, Nd, seeds_from_rngs(method, rngs, K)).cpu().numpy()
+        pipe.check()
+        for b in range(B):
+            ref = O.approx_product(Ms[b].astype(np.float64), Ns[b].astype(np.float64), sizes, c, method,
+                                   workloads.sample_rng(5, b))
+            assert np.array_equal(pipe.budgets_host()[b], ref["budgets"]), (method, b)
+            assert np.array_equal(pipe.columns_host()[b], ref["columns"]), (method, b)
+            assert rel(CD[b], ref["CD"]) < 1e-12
+
+
+def test_pipeline_reports_reference_errors():
+    M, N, sizes = workloads.cfg1(scale=10)
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    pipe = SketchPipeline(M.shape[0], M.shape[1], N.shape[1], sizes, 5, "ONC")  # 5 < K floors
+    pipe.run(Md, Nd, seeds_from_rngs("ONC", [np.random.default_rng(0)], len(sizes)))
+    with pytest.raises(ValueError, match="required floors"):
+        pipe.check()
