@@ -233,7 +233,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    launches = (_lib.launches() - n_launch0) // args.steps
+    # eager launches (none when every pipeline replays its CUDA graph) + graph-contained kernels
+    launches = (_lib.launches() - n_launch0) // args.steps + sum(p.graph_launches for p in pipes)
     ms = [a.elapsed_time(b) for a, b in times]
     ms_step = float(np.mean(ms))
     if world > 1:

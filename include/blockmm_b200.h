@@ -93,11 +93,13 @@ int bmm_norms(int dtype,
  *             all-zero vector for a zero-score block              plan.py:192-206
  *   s[k]    = sc[o] + pw(sc[o+1:e])  (np.add.reduceat)            plan.py:170-173
  *   fnorm[k]= ||M^k||_F * ||N_k||_F (SSM block weights)            plan.py:483-492
- * probs / s / fnorm may be NULL to skip.  colsq/rowsq stride = n, s/fnorm
- * stride = K, probs stride = n.                                           */
+ *   cum/last: optional fused inverse-CDF tables of probs (see bmm_block_cdf)
+ * probs / s / fnorm / cum may be NULL to skip.  colsq/rowsq/probs/cum stride
+ * = n, s/fnorm/last stride = K.  One warp per block.                       */
 int bmm_block_probs(const double* colsq, const double* rowsq, int64_t n,
                     const int64_t* offsets, int64_t K, int64_t batch,
-                    double* probs, double* s, double* fnorm, void* stream);
+                    double* probs, double* s, double* fnorm,
+                    double* cum, int64_t* last_support, void* stream);
 
 /* SSM block probabilities q = f / pw(f) (plan.py:493-496); status gets
  * BMM_ST_ZERO_SCORE when pw(f) == 0.                                        */
@@ -147,10 +149,12 @@ int bmm_seed_streams(const uint32_t* words, int64_t n_words, const int64_t* firs
  * column t = col_off[k] + draw:  column[t] = offsets[k] + idx (global inner
  * index), prob[t] = p[idx], scale[t].  W = col_off[K] per problem; outputs
  * have stride w_stride.  `states` has one stream per block (stride K).
+ * max_len >= the largest block size: the block's CDF is staged in shared
+ * memory for the binary searches when it fits.
  * The SSM baseline (estimators.py:242-243) is the same call with one block
  * spanning the K block probabilities and the caller's own PCG64 state.    */
 int bmm_sample(const double* probs, const double* cum, const int64_t* last_support,
-               const int64_t* offsets, int64_t K, int64_t batch, int64_t n,
+               const int64_t* offsets, int64_t K, int64_t batch, int64_t n, int64_t max_len,
                const int64_t* budgets, const int64_t* col_off, int64_t w_stride,
                const uint64_t* states, int64_t* column, double* prob, double* scale,
                void* stream);

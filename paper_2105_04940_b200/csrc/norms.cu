@@ -106,6 +106,27 @@ __global__ void __launch_bounds__(128) rowsq_kernel(const T* __restrict__ N, int
   }
 }
 
+// Few, wide rows: one warp per row (warp_pw_sum), so a row's loads are all in
+// flight at once; same tree, same bits as rowsq_kernel.
+constexpr int kRowWarps = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(32 * kRowWarps) rowsq_warp_kernel(const T* __restrict__ N, int64_t n,
+                                                                    int64_t p, int64_t ldn, int64_t strideN,
+                                                                    int64_t batch, double* __restrict__ rowsq) {
+  __shared__ WarpPwScratch scratch[kRowWarps];
+  WarpPwScratch* scr = &scratch[threadIdx.x >> 5];
+  const int64_t total = n * batch;
+  for (int64_t g = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5); g < total;
+       g += (int64_t)gridDim.x * kRowWarps) {
+    const int64_t b = g / n, i = g - b * n;
+    const T* row = N + b * strideN + i * ldn;
+    SrcSq<T> src{row, false};
+    const double v = __dadd_rn(0.0, warp_pw_sum(src, 0, p, scr));
+    if ((threadIdx.x & 31) == 0) rowsq[g] = v;
+  }
+}
+
 template <typename T>
 int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM, const T* N,
                  int64_t p, int64_t ldn, int64_t strideN, int64_t batch, int accumulate,
@@ -131,9 +152,15 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
   }
   if (N != nullptr) {
     BMM_REQUIRE(rowsq != nullptr, BMM_E_ARG, "bmm_norms: rowsq is NULL");
-    rowsq_kernel<T><<<grid_for(n * batch, 128, 16, 64), 128, 0, st>>>(N, n, p, ldn, strideN, batch,
-                                                                         rowsq);
-    BMM_CHECK_LAUNCH("rowsq_kernel");
+    const int64_t rows = n * batch;
+    if (rows < 148LL * 512 && p > 128) {
+      const int64_t blocks = std::min<int64_t>(ceil_div(rows, kRowWarps), 148LL * 8 * 64);
+      rowsq_warp_kernel<T><<<(unsigned)blocks, 32 * kRowWarps, 0, st>>>(N, n, p, ldn, strideN, batch, rowsq);
+      BMM_CHECK_LAUNCH("rowsq_warp_kernel");
+    } else {
+      rowsq_kernel<T><<<grid_for(rows, 128, 16, 64), 128, 0, st>>>(N, n, p, ldn, strideN, batch, rowsq);
+      BMM_CHECK_LAUNCH("rowsq_kernel");
+    }
   }
   return BMM_OK;
 }

@@ -44,11 +44,13 @@ __device__ __forceinline__ double pw_leaf(const Src& src, int64_t s, int64_t len
   return res;
 }
 
-// numpy pairwise sum of src(start .. start+n).  Iterative post-order walk of
-// the split tree (depth <= log2(n/64) + 1, so 40 frames cover any int64 n).
-template <class Src>
-__device__ double pw_sum(const Src& src, int64_t start, int64_t n) {
-  if (n <= 128) return pw_leaf(src, start, n);
+// Post-order walk of NumPy's pairwise split tree over [start, start+n),
+// calling leaf(s, len) for the <=128-element leaves left to right and
+// combining left + right exactly as the recursion does (depth <=
+// log2(n/64) + 1, so 40 frames cover any int64 n).
+template <class LeafFn>
+__device__ double pw_tree(int64_t start, int64_t n, LeafFn&& leaf) {
+  if (n <= 128) return leaf(start, n);
   int64_t fs[40], fl[40];
   double fleft[40];
   int fstage[40];
@@ -66,7 +68,7 @@ __device__ double pw_sum(const Src& src, int64_t start, int64_t n) {
       fl[sp] = n2;
       continue;
     }
-    double ret = pw_leaf(src, fs[sp], len);
+    double ret = leaf(fs[sp], len);
     // unwind: combine with finished left siblings, or descend into a right child
     for (;;) {
       if (sp == 0) return ret;
@@ -86,6 +88,132 @@ __device__ double pw_sum(const Src& src, int64_t start, int64_t n) {
       ret = __dadd_rn(fleft[sp], ret);
     }
   }
+}
+
+// numpy pairwise sum of src(start .. start+n), one thread.
+template <class Src>
+__device__ double pw_sum(const Src& src, int64_t start, int64_t n) {
+  return pw_tree(start, n, [&](int64_t s, int64_t len) { return pw_leaf(src, s, len); });
+}
+
+// np.cumsum of p[0..len) into cum (strictly sequential float64 chain,
+// cum[0] = p[0]) by one warp: lanes load 32 values at a time, every lane runs
+// the same 32-step chain over the shuffled values and keeps its own prefix,
+// so loads and stores are coalesced while the adds stay in NumPy's order.
+// Returns (to every lane) the last index with p > 0, or -1.
+__device__ __forceinline__ int64_t warp_cumsum(const double* __restrict__ p, double* __restrict__ cum,
+                                               int64_t len) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  int64_t last = -1;
+  for (int64_t base = 0; base < len; base += 32) {
+    const int64_t i = base + lane;
+    const double x = (i < len) ? p[i] : 0.0;
+    const unsigned pos = __ballot_sync(0xffffffffu, x > 0.0);
+    if (pos) last = base + 31 - __clz(pos);
+    double mine = 0.0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const double v = __shfl_sync(0xffffffffu, x, q);
+      acc = __dadd_rn(acc, v);  // 0 + p[0] == p[0]: probabilities are never -0
+      if (lane == q) mine = acc;
+    }
+    if (i < len) cum[i] = mine;
+  }
+  return last;
+}
+
+// ---- warp-cooperative version --------------------------------------------
+// The same tree, with leaves evaluated in parallel: lane group g = lane/8
+// takes leaf 4q+g, lane j = lane%8 runs accumulator r_j (elements j, j+8, ...),
+// the 8 accumulators combine through an xor butterfly (commutative adds, so
+// every lane ends with ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))), lane j=0 adds
+// the tail, and lane 0 walks the tree over the stored leaf values.
+// scratch: per-warp shared memory for kWarpLeaves leaves.
+constexpr int kWarpLeaves = 128;
+
+struct WarpPwScratch {
+  double val[kWarpLeaves];
+  int64_t start[kWarpLeaves];
+  int32_t len[kWarpLeaves];
+};
+
+template <class Src>
+__device__ __forceinline__ double warp_leaf8(const Src& src, int64_t s, int64_t len, int j) {
+  // accumulator j of a leaf with len >= 8
+  double r = src(s + j);
+  const int64_t body = len - (len % 8);
+#pragma unroll 4
+  for (int64_t i = 8; i < body; i += 8) r = __dadd_rn(r, src(s + i + j));
+  return r;
+}
+
+__device__ __forceinline__ double group8_reduce(double r) {
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+  return r;
+}
+
+// All 32 lanes must call; every lane receives the sum.
+template <class Src>
+__device__ double warp_pw_sum(const Src& src, int64_t start, int64_t n, WarpPwScratch* scr) {
+  const int lane = threadIdx.x & 31;
+  const int j = lane & 7, grp = lane >> 3;
+  if (n < 8) {
+    double r = 0.0;
+    if (lane == 0)
+      for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, src(start + i));
+    return __shfl_sync(0xffffffffu, r, 0);
+  }
+  if (n <= 128) {
+    double r = (grp == 0) ? warp_leaf8(src, start, n, j) : 0.0;
+    r = group8_reduce(r);
+    if (lane == 0)
+      for (int64_t i = n - (n % 8); i < n; ++i) r = __dadd_rn(r, src(start + i));
+    return __shfl_sync(0xffffffffu, r, 0);
+  }
+  // enumerate leaves (lane 0) in left-to-right order
+  int count = 0;
+  if (lane == 0) {
+    pw_tree(start, n, [&](int64_t s, int64_t len) {
+      if (count < kWarpLeaves) { scr->start[count] = s; scr->len[count] = (int32_t)len; }
+      ++count;
+      return 0.0;
+    });
+  }
+  count = __shfl_sync(0xffffffffu, count, 0);
+  __syncwarp();
+  if (count > kWarpLeaves) {  // very long range: single-lane walk
+    double r = 0.0;
+    if (lane == 0) r = pw_sum(src, start, n);
+    return __shfl_sync(0xffffffffu, r, 0);
+  }
+  for (int base = 0; base < count; base += 4) {
+    const int q = base + grp;
+    const bool on = q < count;
+    int64_t s = 0, len = 0;
+    double r = 0.0;
+    if (on) {
+      s = scr->start[q];
+      len = scr->len[q];
+      r = warp_leaf8(src, s, len, j);
+    }
+    r = group8_reduce(r);
+    if (on && j == 0) {
+      for (int64_t i = len - (len % 8); i < len; ++i) r = __dadd_rn(r, src(s + i));
+      scr->val[q] = r;
+    }
+  }
+  __syncwarp();
+  double res = 0.0;
+  if (lane == 0) {
+    int idx = 0;
+    res = pw_tree(start, n, [&](int64_t, int64_t) { return scr->val[idx++]; });
+  }
+  res = __shfl_sync(0xffffffffu, res, 0);
+  __syncwarp();
+  return res;
 }
 
 // ---- element sources -------------------------------------------------------

@@ -23,14 +23,23 @@ struct SrcScore {
   }
 };
 
-__global__ void __launch_bounds__(128) block_probs_kernel(const double* __restrict__ colsq,
-                                                          const double* __restrict__ rowsq, int64_t n,
-                                                          const int64_t* __restrict__ offsets, int64_t K,
-                                                          int64_t batch, double* probs, double* s,
-                                                          double* fnorm) {
+constexpr int kProbWarps = 4;
+
+// One warp per (problem, block).  Elementwise steps are lane-parallel
+// (coalesced); the NumPy sums are warp_pw_sum; the optional CDF is the
+// sequential np.cumsum on lane 0 (estimators.py:37-38) so the sampler can
+// start from it directly.
+__global__ void __launch_bounds__(32 * kProbWarps) block_probs_kernel(
+    const double* __restrict__ colsq, const double* __restrict__ rowsq, int64_t n,
+    const int64_t* __restrict__ offsets, int64_t K, int64_t batch, double* __restrict__ probs,
+    double* __restrict__ s, double* __restrict__ fnorm, double* __restrict__ cum,
+    int64_t* __restrict__ last) {
+  __shared__ WarpPwScratch scratch[kProbWarps];
+  WarpPwScratch* scr = &scratch[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
   const int64_t total = K * batch;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t g = blockIdx.x * (int64_t)kProbWarps + (threadIdx.x >> 5); g < total;
+       g += (int64_t)gridDim.x * kProbWarps) {
     const int64_t b = g / K, k = g - b * K;
     const int64_t o = offsets[k], nk = offsets[k + 1] - o;
     const double* cs = colsq + b * n;
@@ -38,26 +47,41 @@ __global__ void __launch_bounds__(128) block_probs_kernel(const double* __restri
     SrcScore sc{cs, rs};
     if (probs != nullptr) {
       double* pb = probs + b * n;
+      // stage sc into the output vector, then normalise in place
+      for (int64_t i = lane; i < nk; i += 32) pb[o + i] = sc(o + i);
+      __syncwarp();
+      const SrcF64 sp{pb};
       // total = sk.sum(); p = sk / total; p / p.sum()      plan.py:199-205
-      const double tot = __dadd_rn(0.0, pw_sum(sc, o, nk));
-      if (tot == 0.0) {
-        for (int64_t i = 0; i < nk; ++i) pb[o + i] = 0.0;
-      } else {
-        for (int64_t i = 0; i < nk; ++i) pb[o + i] = __ddiv_rn(sc(o + i), tot);
-        const double tot2 = __dadd_rn(0.0, pw_sum(SrcF64{pb}, o, nk));
-        for (int64_t i = 0; i < nk; ++i) pb[o + i] = __ddiv_rn(pb[o + i], tot2);
+      const double tot = __dadd_rn(0.0, warp_pw_sum(sp, o, nk, scr));
+      if (s != nullptr) {
+        // np.add.reduceat: first element, then the pairwise sum of the rest   plan.py:173
+        const double rest = warp_pw_sum(sp, o + 1, nk - 1, scr);
+        if (lane == 0) s[g] = __dadd_rn(pb[o], rest);
       }
-    }
-    if (s != nullptr) {
-      // np.add.reduceat: first element, then the pairwise sum of the rest   plan.py:173
-      s[b * K + k] = __dadd_rn(sc(o), pw_sum(sc, o + 1, nk - 1));
+      __syncwarp();
+      if (tot == 0.0) {
+        for (int64_t i = lane; i < nk; i += 32) pb[o + i] = 0.0;
+      } else {
+        for (int64_t i = lane; i < nk; i += 32) pb[o + i] = __ddiv_rn(pb[o + i], tot);
+        __syncwarp();
+        const double tot2 = __dadd_rn(0.0, warp_pw_sum(sp, o, nk, scr));
+        for (int64_t i = lane; i < nk; i += 32) pb[o + i] = __ddiv_rn(pb[o + i], tot2);
+      }
+      __syncwarp();
+      if (cum != nullptr) {
+        const int64_t lst = warp_cumsum(pb + o, cum + b * n + o, nk);
+        if (lane == 0) last[g] = lst;
+      }
+    } else if (s != nullptr) {
+      const double rest = warp_pw_sum(sc, o + 1, nk - 1, scr);
+      if (lane == 0) s[g] = __dadd_rn(sc(o), rest);
     }
     if (fnorm != nullptr) {
       // ||M^k||_F * ||N_k||_F (plan.py:489).  The reference takes each factor
       // from a BLAS ddot, whose order is not reproducible; tolerance-level.
-      const double fm = __dsqrt_rn(__dadd_rn(0.0, pw_sum(SrcF64{cs}, o, nk)));
-      const double fn = __dsqrt_rn(__dadd_rn(0.0, pw_sum(SrcF64{rs}, o, nk)));
-      fnorm[b * K + k] = __dmul_rn(fm, fn);
+      const double fm = __dsqrt_rn(__dadd_rn(0.0, warp_pw_sum(SrcF64{cs}, o, nk, scr)));
+      const double fn = __dsqrt_rn(__dadd_rn(0.0, warp_pw_sum(SrcF64{rs}, o, nk, scr)));
+      if (lane == 0) fnorm[g] = __dmul_rn(fm, fn);
     }
   }
 }
@@ -481,10 +505,15 @@ using namespace bmm;
 
 extern "C" int bmm_block_probs(const double* colsq, const double* rowsq, int64_t n,
                                const int64_t* offsets, int64_t K, int64_t batch, double* probs,
-                               double* s, double* fnorm, void* stream) {
+                               double* s, double* fnorm, double* cum, int64_t* last_support,
+                               void* stream) {
   BMM_REQUIRE(K >= 1 && batch >= 1 && n >= 1, BMM_E_ARG, "bmm_block_probs: bad shape");
-  block_probs_kernel<<<grid_for(K * batch, 128, 16, 16), 128, 0, as_stream(stream)>>>(
-      colsq, rowsq, n, offsets, K, batch, probs, s, fnorm);
+  BMM_REQUIRE(cum == nullptr || (probs != nullptr && last_support != nullptr), BMM_E_ARG,
+              "bmm_block_probs: cum needs probs and last_support");
+  const int64_t warps = K * batch;
+  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(warps, kProbWarps), 148LL * 16 * 64);
+  block_probs_kernel<<<grid, 32 * kProbWarps, 0, as_stream(stream)>>>(colsq, rowsq, n, offsets, K, batch,
+                                                                      probs, s, fnorm, cum, last_support);
   BMM_CHECK_LAUNCH("block_probs_kernel");
   return BMM_OK;
 }

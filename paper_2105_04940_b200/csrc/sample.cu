@@ -11,28 +11,24 @@
 // onto the last positive-probability index.
 #include "common.cuh"
 #include "rng.cuh"
+#include "pairwise.cuh"
 
 namespace bmm {
 
-__global__ void block_cdf_kernel(const double* __restrict__ probs, const int64_t* __restrict__ offsets,
-                                 int64_t K, int64_t batch, int64_t n, double* __restrict__ cum,
-                                 int64_t* __restrict__ last) {
+constexpr int kCdfWarps = 4;
+
+// One warp per block: sequential np.cumsum (warp_cumsum) and the last index
+// with p > 0.
+__global__ void __launch_bounds__(32 * kCdfWarps) block_cdf_kernel(
+    const double* __restrict__ probs, const int64_t* __restrict__ offsets, int64_t K, int64_t batch, int64_t n,
+    double* __restrict__ cum, int64_t* __restrict__ last) {
   const int64_t total = K * batch;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t g = blockIdx.x * (int64_t)kCdfWarps + (threadIdx.x >> 5); g < total;
+       g += (int64_t)gridDim.x * kCdfWarps) {
     const int64_t b = g / K, k = g - b * K;
-    const int64_t o = offsets[k], e = offsets[k + 1];
-    const double* p = probs + b * n;
-    double* cb = cum + b * n;
-    double acc = 0.0;
-    int64_t lst = -1;
-    for (int64_t i = o; i < e; ++i) {
-      const double v = p[i];
-      acc = (i == o) ? v : __dadd_rn(acc, v);
-      cb[i] = acc;
-      if (v > 0.0) lst = i - o;
-    }
-    last[g] = lst;
+    const int64_t o = offsets[k], len = offsets[k + 1] - o;
+    const int64_t lst = warp_cumsum(probs + b * n + o, cum + b * n + o, len);
+    if ((threadIdx.x & 31) == 0) last[g] = lst;
   }
 }
 
@@ -53,23 +49,36 @@ __global__ void seed_streams_kernel(const uint32_t* __restrict__ words, int64_t 
   }
 }
 
-__global__ void __launch_bounds__(256) sample_kernel(
+constexpr int kSampleWarps = 4;
+
+// One warp per block.  SMEM: the block's CDF is staged in shared memory
+// (max_len doubles per warp) so the binary searches stay on chip.
+template <bool SMEM>
+__global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
     const double* __restrict__ probs, const double* __restrict__ cum,
     const int64_t* __restrict__ last, const int64_t* __restrict__ offsets, int64_t K, int64_t batch,
     int64_t n, const int64_t* __restrict__ budgets, const int64_t* __restrict__ col_off,
     int64_t w_stride, const uint64_t* __restrict__ states, int64_t* __restrict__ column,
-    double* __restrict__ prob, double* __restrict__ scale) {
+    double* __restrict__ prob, double* __restrict__ scale, int64_t max_len, int wpb) {
+  extern __shared__ double scum_all[];
   const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  if (w >= wpb) return;
+  double* scum = scum_all + (SMEM ? w * max_len : 0);
   const int64_t warps_total = K * batch;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < warps_total;
-       g += (int64_t)gridDim.x * wpb) {
+  for (int64_t g = blockIdx.x * (int64_t)wpb + w; g < warps_total; g += (int64_t)gridDim.x * wpb) {
     const int64_t b = g / K, k = g - b * K;
     const int64_t ck = budgets[g];
     if (ck <= 0) continue;
     const int64_t o = offsets[k], len = offsets[k + 1] - o;
     const double* cb = cum + b * n + o;
     const double* pb = probs + b * n + o;
+    if (SMEM) {
+      __syncwarp();
+      for (int64_t i = lane; i < len; i += 32) scum[i] = cb[i];
+      __syncwarp();
+      cb = scum;
+    }
     const int64_t lst = last[g];
     const uint64_t* sp = states + 4 * g;
     U128 st{sp[0], sp[1]}, inc{sp[2], sp[3]};
@@ -81,7 +90,7 @@ __global__ void __launch_bounds__(256) sample_kernel(
     const int64_t t0 = col_off[b * (K + 1) + k];
     for (int64_t j = lane; j < ck; j += 32) {
       const double u = u53(pcg_output(st));
-      // first index with cum > u
+      // first index with cum > u  (searchsorted side="right")
       int64_t lo = 0, hi = len;
       while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
@@ -198,8 +207,9 @@ using namespace bmm;
 extern "C" int bmm_block_cdf(const double* probs, const int64_t* offsets, int64_t K, int64_t batch,
                              int64_t n, double* cum, int64_t* last_support, void* stream) {
   BMM_REQUIRE(K >= 1 && batch >= 1, BMM_E_ARG, "bmm_block_cdf: bad shape");
-  block_cdf_kernel<<<grid_for(K * batch, 128, 16, 16), 128, 0, as_stream(stream)>>>(probs, offsets, K, batch,
-                                                                                   n, cum, last_support);
+  const int64_t blocks = std::min<int64_t>(ceil_div(K * batch, kCdfWarps), 148LL * 16 * 64);
+  block_cdf_kernel<<<(unsigned)blocks, 32 * kCdfWarps, 0, as_stream(stream)>>>(probs, offsets, K, batch, n, cum,
+                                                                              last_support);
   BMM_CHECK_LAUNCH("block_cdf_kernel");
   return BMM_OK;
 }
@@ -216,15 +226,34 @@ extern "C" int bmm_seed_streams(const uint32_t* words, int64_t n_words, const in
 }
 
 extern "C" int bmm_sample(const double* probs, const double* cum, const int64_t* last_support,
-                          const int64_t* offsets, int64_t K, int64_t batch, int64_t n,
+                          const int64_t* offsets, int64_t K, int64_t batch, int64_t n, int64_t max_len,
                           const int64_t* budgets, const int64_t* col_off, int64_t w_stride,
                           const uint64_t* states, int64_t* column, double* prob, double* scale,
                           void* stream) {
-  BMM_REQUIRE(K >= 1 && batch >= 1, BMM_E_ARG, "bmm_sample: bad shape");
+  BMM_REQUIRE(K >= 1 && batch >= 1 && max_len >= 1, BMM_E_ARG, "bmm_sample: bad shape");
   const int64_t warps = K * batch;
-  sample_kernel<<<grid_for(warps * 32, 256, 8, 16), 256, 0, as_stream(stream)>>>(
-      probs, cum, last_support, offsets, K, batch, n, budgets, col_off, w_stride, states, column, prob,
-      scale);
+  cudaStream_t st = as_stream(stream);
+  const int64_t per_warp = max_len * 8;
+  int wpb = kSampleWarps;
+  bool smem = true;
+  if (per_warp * kSampleWarps > 96 * 1024) wpb = 1;
+  if (per_warp > 200 * 1024) smem = false;
+  const int64_t blocks = std::min<int64_t>(ceil_div(warps, wpb), 148LL * 16 * 64);
+  if (smem) {
+    const int bytes = (int)(per_warp * wpb);
+    static int attr = 0;
+    if (bytes > 48 * 1024 && bytes > attr) {
+      cudaFuncSetAttribute(sample_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = 200 * 1024;
+    }
+    sample_kernel<true><<<(unsigned)blocks, 32 * kSampleWarps, bytes, st>>>(
+        probs, cum, last_support, offsets, K, batch, n, budgets, col_off, w_stride, states, column, prob, scale,
+        max_len, wpb);
+  } else {
+    sample_kernel<false><<<(unsigned)blocks, 32 * kSampleWarps, 0, st>>>(
+        probs, cum, last_support, offsets, K, batch, n, budgets, col_off, w_stride, states, column, prob, scale,
+        max_len, wpb);
+  }
   BMM_CHECK_LAUNCH("sample_kernel");
   return BMM_OK;
 }

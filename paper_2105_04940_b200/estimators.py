@@ -127,7 +127,8 @@ def sample_blocks(inst: DeviceInstance, probs, budgets: np.ndarray, words: np.nd
     column = torch.empty(max(W, 1), dtype=torch.int64, device=dev)
     prob = torch.empty(max(W, 1), dtype=torch.float64, device=dev)
     scale = torch.empty(max(W, 1), dtype=torch.float64, device=dev)
-    _lib.call("bmm_sample", _lib.ptr(pr), _lib.ptr(cum), _lib.ptr(last), _lib.ptr(inst.offsets), K, 1, n,
+    max_len = int(getattr(inst, "max_len", n))
+    _lib.call("bmm_sample", _lib.ptr(pr), _lib.ptr(cum), _lib.ptr(last), _lib.ptr(inst.offsets), K, 1, n, max_len,
               _lib.ptr(bud_d), _lib.ptr(col_off), W, _lib.ptr(states), _lib.ptr(column), _lib.ptr(prob),
               _lib.ptr(scale), _lib.stream_ptr())
     return column[:W], prob[:W], scale[:W], col_off
@@ -268,4 +269,5 @@ class _BlockLevel:
     def __init__(self, K: int):
         self.K = 1
         self.n = K
+        self.max_len = K
         self.offsets = _lib.i64([0, K])

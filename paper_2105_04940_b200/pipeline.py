@@ -85,6 +85,7 @@ class SketchPipeline:
         if sum(self.sizes) != self.n:
             raise ValueError("partition does not cover n")
         self.K = len(self.sizes)
+        self.max_len = max(self.sizes)
         self.method, self.c, self.c0, self.cap = method, int(c), int(c0), bool(cap)
         self.dtype = dtype
         self.lib = _lib.load()
@@ -224,8 +225,10 @@ class SketchPipeline:
             self.launch(M, N)
         torch.cuda.current_stream().wait_stream(side)
         g = torch.cuda.CUDAGraph()
+        n0 = _lib.launches()
         with torch.cuda.graph(g):
             self.launch(M, N)
+        self.graph_launches = _lib.launches() - n0  # our kernels per replay
         self.graph, self._graph_ptrs = g, (M.data_ptr(), N.data_ptr())
 
     def run(self, M: torch.Tensor, N: torch.Tensor, seeds: CallSeeds) -> torch.Tensor:
@@ -252,9 +255,9 @@ class SketchPipeline:
         self._c("bmm_norms", dt, P(M), m, n, ldm, sM, P(N), p, ldn, sN, B, 0, P(self.colsq), P(self.rowsq), st)
         if self.method == "SSM":
             return self._run_ssm(M, N, dt, st)
-        need_probs = True
+        # probabilities, score sums and (fused) the main CDF of the optimal probabilities
         self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B,
-                P(self.probs) if need_probs else None, P(self.s), None, st)
+                P(self.probs), P(self.s), None, P(self.cum), P(self.last), st)
         rule = {"ONC": _lib.RULE_ONC, "OPL": _lib.RULE_OPL, "UU": _lib.RULE_UU,
                 "ONU": _lib.RULE_TWO_STEP, "ONMCNR": _lib.RULE_TWO_STEP}[self.method]
         aux = None
@@ -269,9 +272,13 @@ class SketchPipeline:
             self._c("bmm_budgets", _lib.RULE_PILOT, P(s_for_pilot) if s_for_pilot is not None else None, None,
                     None, None, None, K, B, P(self.p_c), 1, P(self.p_bud), P(self.p_coloff), None, None, None,
                     P(self.ws_budget), st)
-            self._c("bmm_block_cdf", P(p0), P(self.offsets), K, B, n, P(self.p0cum), P(self.p0last), st)
+            if self.method == "ONU":
+                self._c("bmm_block_cdf", P(p0), P(self.offsets), K, B, n, P(self.p0cum), P(self.p0last), st)
+                p0cum, p0last = self.p0cum, self.p0last
+            else:  # ONMCNR pilots with the optimal probabilities: their CDF is already built
+                p0cum, p0last = self.cum, self.last
             self._seed("pilot", self.p_states, st)
-            self._c("bmm_sample", P(p0), P(self.p0cum), P(self.p0last), P(self.offsets), K, B, n, P(self.p_bud),
+            self._c("bmm_sample", P(p0), P(p0cum), P(p0last), P(self.offsets), K, B, n, self.max_len, P(self.p_bud),
                     P(self.p_coloff), self.W0, P(self.p_states), P(self.p_column), P(self.p_prob),
                     P(self.p_scale), st)
             self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.p_column),
@@ -284,9 +291,11 @@ class SketchPipeline:
                 P(self.sizes_d), None, None, K, B, P(self.c_arr), int(self.cap), P(self.budgets), P(self.col_off),
                 P(self.status), P(self.diag), P(self.notes), P(self.ws_budget), st)
         probs = self._uprobs if self.method == "UU" else self.probs
-        self._c("bmm_block_cdf", P(probs), P(self.offsets), K, B, n, P(self.cum), P(self.last), st)
+        if self.method == "UU":
+            self._c("bmm_block_cdf", P(probs), P(self.offsets), K, B, n, P(self.cum), P(self.last), st)
         self._seed("main", self.states, st)
-        self._c("bmm_sample", P(probs), P(self.cum), P(self.last), P(self.offsets), K, B, n, P(self.budgets),
+        self._c("bmm_sample", P(probs), P(self.cum), P(self.last), P(self.offsets), K, B, n, self.max_len,
+                P(self.budgets),
                 P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
         self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column), P(self.scale),
                 W, W, B, P(self.C), W, m * W, P(self.D), p, W * p, st)
@@ -298,11 +307,11 @@ class SketchPipeline:
         B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W
         P = lambda t: t.data_ptr()  # noqa: E731
         self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B, None, None,
-                P(self.fnorm), st)
+                P(self.fnorm), None, None, st)
         self._c("bmm_normalize", P(self.fnorm), K, B, P(self.q), P(self.status), st)
         self._c("bmm_block_cdf", P(self.q), P(self.qoff), 1, B, K, P(self.qcum), P(self.qlast), st)
         (states,) = self._seedbuf["states"]
-        self._c("bmm_sample", P(self.q), P(self.qcum), P(self.qlast), P(self.qoff), 1, B, K, P(self.q_bud),
+        self._c("bmm_sample", P(self.q), P(self.qcum), P(self.qlast), P(self.qoff), 1, B, K, K, P(self.q_bud),
                 P(self.q_coloff), self.draws, P(states), P(self.blk), P(self.blk_prob), P(self.blk_scale), st)
         if B != 1:
             raise NotImplementedError("batched SSM gather")
