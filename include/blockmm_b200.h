@@ -217,6 +217,25 @@ int bmm_sqdiff(int dtype, const void* X, int64_t ldx, int64_t strideX,
                int64_t m, int64_t nc, int64_t batch, double* err,
                void* ws, int64_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------- K4/K6 float32 path
+ * Split gather for 3xTF32: x = M[h, column[t]] * scale[t] (formed in float64,
+ * as the reference does on upcast inputs), hi = tf32_rna(x), lo = x - hi:
+ *   a_hi/a_lo [(b*m + h) * W + t]   (A = C, K-major)
+ *   b_hi/b_lo [(b*p + f) * W + t]   (B = D^T, K-major)                       */
+int bmm_gather_tf32x3(int dtype, const void* M, int64_t ldm, int64_t strideM,
+                      const void* N, int64_t ldn, int64_t strideN,
+                      int64_t m, int64_t p, const int64_t* column, const double* scale,
+                      int64_t W, int64_t w_stride, int64_t batch,
+                      float* a_hi, float* a_lo, float* b_hi, float* b_lo, void* stream);
+
+/* out[b] (m x nc, float32) = A[b] (m x k) @ B[b]^T with A = a_hi + a_lo,
+ * B = b_hi + b_lo as written by bmm_gather_tf32x3: tcgen05.mma kind::tf32,
+ * hi.hi + hi.lo + lo.hi accumulated in TMEM (float32), TMA SWIZZLE_128B
+ * operand tiles (estimators.py:175 for the float32 configs).  k % 4 == 0.   */
+int bmm_gemm_tf32x3(const float* a_hi, const float* a_lo, const float* b_hi, const float* b_lo,
+                    int64_t m, int64_t nc, int64_t k, int64_t batch,
+                    float* out, int64_t ldo, int64_t strideO, void* stream);
+
 /* sum of a float64 vector segment in numpy pairwise order: out[b] = 0 + pw(x[b, 0:len])
  * (used for ||M||_F^2 = pw(colsq), ||N||_F^2 = pw(rowsq)).                */
 int bmm_pairwise_sum(const double* x, int64_t len, int64_t stride, int64_t batch,

@@ -1,0 +1,359 @@
+// K6 -- float32 sampled contraction on the 5th-generation tensor cores.
+//
+// C (m x W) @ D (W x p) for float32 inputs (configs 4 and 5), where the
+// reference computes in float64 (estimators.py:143-144,175).  1xTF32 misses
+// the 1e-5 tolerance at W = 32768, so each operand is split once,
+// x = hi + lo with hi = tf32_rna(x) and lo = x - hi (float32), and the tile
+// accumulates hi.hi + hi.lo + lo.hi ("3xTF32") into one float32 TMEM
+// accumulator.
+//
+//   * bmm_gather_tf32x3: the K4 gather writes the split operands K-major:
+//       A_hi/A_lo[b*m + h, t] = split(M[h, column[t]] * scale[t])
+//       B_hi/B_lo[b*p + f, t] = split(N[column[t], f] * scale[t])   (D^T)
+//   * bmm_gemm_tf32x3: one CTA per 128x128 output tile; warp 0 drives TMA
+//     (SWIZZLE_128B, 32 x 128 float boxes) into a 3-stage mbarrier ring, one
+//     thread of warp 1 issues tcgen05.mma.kind::tf32 (M=128, N=128, K=8) into
+//     a 128-column TMEM accumulator and frees stages with tcgen05.commit,
+//     and all four warps drain TMEM with tcgen05.ld.32x32b for the epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace bmm {
+
+constexpr int T_BM = 128, T_BN = 128, T_BK = 32, T_STAGES = 3, T_THREADS = 128;
+constexpr int T_TILE_BYTES = T_BM * T_BK * 4;                // 16 KB: one operand tile
+constexpr int T_STAGE_BYTES = 4 * T_TILE_BYTES;              // A_hi, A_lo, B_hi, B_lo
+constexpr int T_SMEM_BYTES = T_STAGES * T_STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)1 << 16;                          // leading byte offset (16 B, unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                          // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;                          // layout: SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: F32 accumulate, TF32 A/B, both K-major, M=128, N=128.
+constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(T_BN >> 3) << 17) |
+                                ((uint32_t)(T_BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(kIdescTf32), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(T_THREADS, 1) gemm_tf32x3_kernel(
+    const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+    const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo, int64_t m, int64_t nc,
+    int64_t k, float* __restrict__ out, int64_t ldo, int64_t strideO) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_STAGES * T_STAGE_BYTES);
+  uint64_t* empty = full + T_STAGES;
+  uint64_t* tmem_full = empty + T_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = blockIdx.z;
+  const int a_row0 = (int)(b * m + (int64_t)blockIdx.y * T_BM);
+  const int b_row0 = (int)(b * nc + (int64_t)blockIdx.x * T_BN);
+  const int ktiles = (int)((k + T_BK - 1) / T_BK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < T_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_alo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_bhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_blo)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(T_BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int s = kt % T_STAGES;
+      if (kt >= T_STAGES) mbar_wait(&empty[s], ((kt / T_STAGES) - 1) & 1);
+      uint8_t* st = smem + s * T_STAGE_BYTES;
+      mbar_expect_tx(&full[s], T_STAGE_BYTES);
+      const int kc = kt * T_BK;
+      tma_load_2d(st + 0 * T_TILE_BYTES, &tm_ahi, &full[s], kc, a_row0);
+      tma_load_2d(st + 1 * T_TILE_BYTES, &tm_alo, &full[s], kc, a_row0);
+      tma_load_2d(st + 2 * T_TILE_BYTES, &tm_bhi, &full[s], kc, b_row0);
+      tma_load_2d(st + 3 * T_TILE_BYTES, &tm_blo, &full[s], kc, b_row0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int s = kt % T_STAGES;
+      mbar_wait(&full[s], (kt / T_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t base = su32(smem + s * T_STAGE_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < T_BK / 8; ++kk) {
+        const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the 128 B swizzle row
+        const uint64_t ahi = umma_desc_sw128(base + 0 * T_TILE_BYTES + off);
+        const uint64_t alo = umma_desc_sw128(base + 1 * T_TILE_BYTES + off);
+        const uint64_t bhi = umma_desc_sw128(base + 2 * T_TILE_BYTES + off);
+        const uint64_t blo = umma_desc_sw128(base + 3 * T_TILE_BYTES + off);
+        // small cross terms first, then the leading product
+        umma_tf32(tmem, alo, bhi, (kt | kk) != 0);
+        umma_tf32(tmem, ahi, blo, 1);
+        umma_tf32(tmem, ahi, bhi, 1);
+      }
+      umma_commit(&empty[s]);  // stage s free once these MMAs have read it
+    }
+    umma_commit(tmem_full);
+  }
+  __syncwarp();
+
+  // ---- epilogue: TMEM -> registers -> global (each warp owns 32 accumulator lanes)
+  mbar_wait(tmem_full, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const int64_t row = (int64_t)blockIdx.y * T_BM + warp * 32 + lane;
+  float* orow = out + b * strideO + row * ldo;
+  const int64_t col0 = (int64_t)blockIdx.x * T_BN;
+#pragma unroll 1
+  for (int c = 0; c < T_BN; c += 32) {
+    uint32_t v[32];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+          "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    if (row < m) {
+      const int64_t cb = col0 + c;
+      if (cb + 32 <= nc && (ldo % 4) == 0 && ((reinterpret_cast<uintptr_t>(orow + cb) & 15) == 0)) {
+        float4* o4 = reinterpret_cast<float4*>(orow + cb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          o4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                              __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (cb + j < nc) orow[cb + j] = __uint_as_float(v[j]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(T_BN));
+  }
+}
+
+// ---- split gather (K4 for the float32 path)
+
+__device__ __forceinline__ void split_tf32(double x, float& hi, float& lo) {
+  const float xf = (float)x;
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(xf));
+  hi = __uint_as_float(h);
+  lo = (float)(x - (double)hi);
+}
+
+template <typename T>
+__device__ __forceinline__ double ld_d(const T* p) { return (double)__ldg(p); }
+
+// A_hi/A_lo[b*m + h, t] = split(M[b][h, column[t]] * scale[t])
+template <typename T>
+__global__ void __launch_bounds__(256) gather_a_split_kernel(const T* __restrict__ M, int64_t ldm, int64_t strideM,
+                                                             int64_t m, const int64_t* __restrict__ column,
+                                                             const double* __restrict__ scale, int64_t W,
+                                                             int64_t w_stride, int64_t batch, float* __restrict__ ahi,
+                                                             float* __restrict__ alo) {
+  const int64_t per_b = m * W;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < per_b * batch;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g / per_b, r = g - b * per_b;
+    const int64_t h = r / W, t = r - h * W;
+    const double x = __dmul_rn(ld_d(M + b * strideM + h * ldm + column[b * w_stride + t]), scale[b * w_stride + t]);
+    float hi, lo;
+    split_tf32(x, hi, lo);
+    ahi[g] = hi;
+    alo[g] = lo;
+  }
+}
+
+// B_hi/B_lo[b*p + f, t] = split(N[b][column[t], f] * scale[t]) through a 32x32 smem transpose.
+template <typename T>
+__global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restrict__ N, int64_t ldn, int64_t strideN,
+                                                              int64_t p, const int64_t* __restrict__ column,
+                                                              const double* __restrict__ scale, int64_t W,
+                                                              int64_t w_stride, float* __restrict__ bhi,
+                                                              float* __restrict__ blo) {
+  __shared__ float sh[32][33], sl[32][33];
+  const int64_t b = blockIdx.z;
+  const int64_t t0 = (int64_t)blockIdx.x * 32, f0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t t = t0 + i, f = f0 + tx;
+    float hi = 0.f, lo = 0.f;
+    if (t < W && f < p) {
+      const double x = __dmul_rn(ld_d(N + b * strideN + column[b * w_stride + t] * ldn + f), scale[b * w_stride + t]);
+      split_tf32(x, hi, lo);
+    }
+    sh[i][tx] = hi;
+    sl[i][tx] = lo;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t f = f0 + i, t = t0 + tx;
+    if (f < p && t < W) {
+      const int64_t o = (b * p + f) * W + t;
+      bhi[o] = sh[tx][i];
+      blo[o] = sl[tx][i];
+    }
+  }
+}
+
+// ---- host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols) {
+  auto enc = get_encode();
+  BMM_REQUIRE(enc != nullptr, BMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {(cuuint32_t)T_BK, (cuuint32_t)T_BM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BMM_REQUIRE(r == CUDA_SUCCESS, BMM_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return BMM_OK;
+}
+
+}  // namespace bmm
+
+using namespace bmm;
+
+extern "C" int bmm_gather_tf32x3(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N, int64_t ldn,
+                                 int64_t strideN, int64_t m, int64_t p, const int64_t* column, const double* scale,
+                                 int64_t W, int64_t w_stride, int64_t batch, float* a_hi, float* a_lo, float* b_hi,
+                                 float* b_lo, void* stream) {
+  BMM_REQUIRE(m >= 1 && p >= 1 && W >= 1 && batch >= 1, BMM_E_ARG, "bmm_gather_tf32x3: bad shape");
+  BMM_REQUIRE(batch <= 65535 && ceil_div(p, 32) <= 65535, BMM_E_UNSUPPORTED, "bmm_gather_tf32x3: grid too large");
+  cudaStream_t st = as_stream(stream);
+  dim3 tgrid((unsigned)ceil_div(W, 32), (unsigned)ceil_div(p, 32), (unsigned)batch);
+  if (dtype == BMM_F32) {
+    gather_a_split_kernel<float><<<grid_for(m * W * batch, 256), 256, 0, st>>>(
+        (const float*)M, ldm, strideM, m, column, scale, W, w_stride, batch, a_hi, a_lo);
+    BMM_CHECK_LAUNCH("gather_a_split_kernel");
+    gather_bt_split_kernel<float><<<tgrid, 256, 0, st>>>((const float*)N, ldn, strideN, p, column, scale, W,
+                                                         w_stride, b_hi, b_lo);
+  } else if (dtype == BMM_F64) {
+    gather_a_split_kernel<double><<<grid_for(m * W * batch, 256), 256, 0, st>>>(
+        (const double*)M, ldm, strideM, m, column, scale, W, w_stride, batch, a_hi, a_lo);
+    BMM_CHECK_LAUNCH("gather_a_split_kernel");
+    gather_bt_split_kernel<double><<<tgrid, 256, 0, st>>>((const double*)N, ldn, strideN, p, column, scale, W,
+                                                          w_stride, b_hi, b_lo);
+  } else {
+    set_error("bmm_gather_tf32x3: unknown dtype %d", dtype);
+    return BMM_E_ARG;
+  }
+  BMM_CHECK_LAUNCH("gather_bt_split_kernel");
+  return BMM_OK;
+}
+
+extern "C" int bmm_gemm_tf32x3(const float* a_hi, const float* a_lo, const float* b_hi, const float* b_lo,
+                               int64_t m, int64_t nc, int64_t k, int64_t batch, float* out, int64_t ldo,
+                               int64_t strideO, void* stream) {
+  BMM_REQUIRE(m >= 1 && nc >= 1 && k >= 1 && batch >= 1, BMM_E_ARG, "bmm_gemm_tf32x3: bad shape");
+  BMM_REQUIRE(k % 4 == 0, BMM_E_UNSUPPORTED, "bmm_gemm_tf32x3: k must be a multiple of 4 (16-byte TMA rows)");
+  BMM_REQUIRE(batch * m < (1LL << 31) && batch * nc < (1LL << 31) && batch <= 65535, BMM_E_UNSUPPORTED,
+              "bmm_gemm_tf32x3: problem too large for 32-bit TMA coordinates");
+  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+  int rc;
+  if ((rc = make_map(&ma_hi, a_hi, batch * m, k)) != BMM_OK) return rc;
+  if ((rc = make_map(&ma_lo, a_lo, batch * m, k)) != BMM_OK) return rc;
+  if ((rc = make_map(&mb_hi, b_hi, batch * nc, k)) != BMM_OK) return rc;
+  if ((rc = make_map(&mb_lo, b_lo, batch * nc, k)) != BMM_OK) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM_BYTES);
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div(nc, T_BN), (unsigned)ceil_div(m, T_BM), (unsigned)batch);
+  gemm_tf32x3_kernel<<<grid, T_THREADS, T_SMEM_BYTES, as_stream(stream)>>>(ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out,
+                                                                         ldo, strideO);
+  BMM_CHECK_LAUNCH("gemm_tf32x3_kernel");
+  return BMM_OK;
+}
