@@ -22,7 +22,7 @@
 
 namespace bmm {
 
-constexpr int T_BM = 128, T_BN = 128, T_BK = 32, T_STAGES = 3, T_THREADS = 128;
+constexpr int T_BM = 128, T_BN = 128, T_BK = 32, T_STAGES = 3;
 constexpr int T_TILE_BYTES = T_BM * T_BK * 4;                // 16 KB: one operand tile
 constexpr int T_STAGE_BYTES = 4 * T_TILE_BYTES;              // A_hi, A_lo, B_hi, B_lo
 constexpr int T_SMEM_BYTES = T_STAGES * T_STAGE_BYTES + 1024 + 256;
@@ -88,7 +88,36 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
-__global__ void __launch_bounds__(T_THREADS, 1) gemm_tf32x3_kernel(
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+        "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+        "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+
+// Warp roles: 0 = TMA producer, 1 = MMA issuer, 2..5 = accumulator drain /
+// epilogue (warp w reads TMEM lanes 32*(w%4) .. +31, the quarter it may access).
+//
+// Chunked accumulation: the tensor core's float32 accumulate truncates, so
+// its error grows linearly with K (measured ~6e-9 per K element).  Every
+// T_CHUNK stages the MMA issuer switches between two TMEM accumulators
+// (accumulate=0 at the chunk start) and the drain warps add the finished
+// chunk into round-to-nearest float32 registers; the error then stays at one
+// chunk's worth (~1e-6) for any W.
+constexpr int T_CHUNK = 4;           // stages per accumulation chunk (128 K elements)
+constexpr int T_WARPS = 6;
+
+__global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_tf32x3_kernel(
     const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
     const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo, int64_t m, int64_t nc,
     int64_t k, float* __restrict__ out, int64_t ldo, int64_t strideO) {
@@ -96,21 +125,26 @@ __global__ void __launch_bounds__(T_THREADS, 1) gemm_tf32x3_kernel(
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_STAGES * T_STAGE_BYTES);
   uint64_t* empty = full + T_STAGES;
-  uint64_t* tmem_full = empty + T_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty + T_STAGES;   // [2]
+  uint64_t* acc_empty = acc_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = blockIdx.z;
   const int a_row0 = (int)(b * m + (int64_t)blockIdx.y * T_BM);
   const int b_row0 = (int)(b * nc + (int64_t)blockIdx.x * T_BN);
   const int ktiles = (int)((k + T_BK - 1) / T_BK);
+  const int nchunks = (ktiles + T_CHUNK - 1) / T_CHUNK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < T_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&acc_full[q], 1);
+      mbar_init(&acc_empty[q], 4);  // one arrive per drain warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_alo)) : "memory");
@@ -119,7 +153,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) gemm_tf32x3_kernel(
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
-                 "r"(T_BN));
+                 "r"(2 * T_BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -127,84 +161,92 @@ __global__ void __launch_bounds__(T_THREADS, 1) gemm_tf32x3_kernel(
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer
-    for (int kt = 0; kt < ktiles; ++kt) {
-      const int s = kt % T_STAGES;
-      if (kt >= T_STAGES) mbar_wait(&empty[s], ((kt / T_STAGES) - 1) & 1);
-      uint8_t* st = smem + s * T_STAGE_BYTES;
-      mbar_expect_tx(&full[s], T_STAGE_BYTES);
-      const int kc = kt * T_BK;
-      tma_load_2d(st + 0 * T_TILE_BYTES, &tm_ahi, &full[s], kc, a_row0);
-      tma_load_2d(st + 1 * T_TILE_BYTES, &tm_alo, &full[s], kc, a_row0);
-      tma_load_2d(st + 2 * T_TILE_BYTES, &tm_bhi, &full[s], kc, b_row0);
-      tma_load_2d(st + 3 * T_TILE_BYTES, &tm_blo, &full[s], kc, b_row0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer
-    for (int kt = 0; kt < ktiles; ++kt) {
-      const int s = kt % T_STAGES;
-      mbar_wait(&full[s], (kt / T_STAGES) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t base = su32(smem + s * T_STAGE_BYTES);
-#pragma unroll
-      for (int kk = 0; kk < T_BK / 8; ++kk) {
-        const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the 128 B swizzle row
-        const uint64_t ahi = umma_desc_sw128(base + 0 * T_TILE_BYTES + off);
-        const uint64_t alo = umma_desc_sw128(base + 1 * T_TILE_BYTES + off);
-        const uint64_t bhi = umma_desc_sw128(base + 2 * T_TILE_BYTES + off);
-        const uint64_t blo = umma_desc_sw128(base + 3 * T_TILE_BYTES + off);
-        // small cross terms first, then the leading product
-        umma_tf32(tmem, alo, bhi, (kt | kk) != 0);
-        umma_tf32(tmem, ahi, blo, 1);
-        umma_tf32(tmem, ahi, bhi, 1);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % T_STAGES;
+        if (kt >= T_STAGES) mbar_wait(&empty[s], ((kt / T_STAGES) - 1) & 1);
+        uint8_t* st = smem + s * T_STAGE_BYTES;
+        mbar_expect_tx(&full[s], T_STAGE_BYTES);
+        const int kc = kt * T_BK;
+        tma_load_2d(st + 0 * T_TILE_BYTES, &tm_ahi, &full[s], kc, a_row0);
+        tma_load_2d(st + 1 * T_TILE_BYTES, &tm_alo, &full[s], kc, a_row0);
+        tma_load_2d(st + 2 * T_TILE_BYTES, &tm_bhi, &full[s], kc, b_row0);
+        tma_load_2d(st + 3 * T_TILE_BYTES, &tm_blo, &full[s], kc, b_row0);
       }
-      umma_commit(&empty[s]);  // stage s free once these MMAs have read it
     }
-    umma_commit(tmem_full);
-  }
-  __syncwarp();
-
-  // ---- epilogue: TMEM -> registers -> global (each warp owns 32 accumulator lanes)
-  mbar_wait(tmem_full, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const int64_t row = (int64_t)blockIdx.y * T_BM + warp * 32 + lane;
-  float* orow = out + b * strideO + row * ldo;
-  const int64_t col0 = (int64_t)blockIdx.x * T_BN;
-#pragma unroll 1
-  for (int c = 0; c < T_BN; c += 32) {
-    uint32_t v[32];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
-          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
-          "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-    if (row < m) {
-      const int64_t cb = col0 + c;
-      if (cb + 32 <= nc && (ldo % 4) == 0 && ((reinterpret_cast<uintptr_t>(orow + cb) & 15) == 0)) {
-        float4* o4 = reinterpret_cast<float4*>(orow + cb);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % T_STAGES;
+        const int chunk = kt / T_CHUNK, q = chunk & 1;
+        const bool first = (kt % T_CHUNK) == 0;
+        if (first && chunk >= 2) mbar_wait(&acc_empty[q], ((chunk >> 1) - 1) & 1);
+        mbar_wait(&full[s], (kt / T_STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t base = su32(smem + s * T_STAGE_BYTES);
+        const uint32_t acc = tmem + (uint32_t)(q * T_BN);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          o4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                              __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        for (int kk = 0; kk < T_BK / 8; ++kk) {
+          const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the 128 B swizzle row
+          const uint64_t ahi = umma_desc_sw128(base + 0 * T_TILE_BYTES + off);
+          const uint64_t alo = umma_desc_sw128(base + 1 * T_TILE_BYTES + off);
+          const uint64_t bhi = umma_desc_sw128(base + 2 * T_TILE_BYTES + off);
+          const uint64_t blo = umma_desc_sw128(base + 3 * T_TILE_BYTES + off);
+          // small cross terms first, then the leading product
+          umma_tf32(acc, alo, bhi, !(first && kk == 0));
+          umma_tf32(acc, ahi, blo, 1);
+          umma_tf32(acc, ahi, bhi, 1);
+        }
+        umma_commit(&empty[s]);  // stage s free once these MMAs have read it
+        if ((kt % T_CHUNK) == T_CHUNK - 1 || kt == ktiles - 1) umma_commit(&acc_full[q]);
+      }
+    }
+  } else {
+    // ---- drain: add each finished chunk into float32 registers, then store
+    const int quarter = warp & 3;
+    float sum[T_BN];
+#pragma unroll
+    for (int c = 0; c < T_BN; ++c) sum[c] = 0.f;
+    for (int chunk = 0; chunk < nchunks; ++chunk) {
+      const int q = chunk & 1;
+      mbar_wait(&acc_full[q], (chunk >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < T_BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(q * T_BN + c), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum[c + j] += __uint_as_float(v[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[q]);
+    }
+    const int64_t row = (int64_t)blockIdx.y * T_BM + quarter * 32 + lane;
+    if (row < m) {
+      float* orow = out + b * strideO + row * ldo;
+      const int64_t col0 = (int64_t)blockIdx.x * T_BN;
+      const bool vec = (col0 + T_BN <= nc) && (ldo % 4) == 0 && ((reinterpret_cast<uintptr_t>(orow + col0) & 15) == 0);
+      if (vec) {
+        float4* o4 = reinterpret_cast<float4*>(orow + col0);
+#pragma unroll
+        for (int j = 0; j < T_BN / 4; ++j)
+          o4[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (cb + j < nc) orow[cb + j] = __uint_as_float(v[j]);
+        for (int j = 0; j < T_BN; ++j)
+          if (col0 + j < nc) orow[col0 + j] = sum[j];
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(T_BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * T_BN));
   }
 }
 
@@ -352,7 +394,7 @@ extern "C" int bmm_gemm_tf32x3(const float* a_hi, const float* a_lo, const float
     attr = true;
   }
   dim3 grid((unsigned)ceil_div(nc, T_BN), (unsigned)ceil_div(m, T_BM), (unsigned)batch);
-  gemm_tf32x3_kernel<<<grid, T_THREADS, T_SMEM_BYTES, as_stream(stream)>>>(ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out,
+  gemm_tf32x3_kernel<<<grid, 32 * T_WARPS, T_SMEM_BYTES, as_stream(stream)>>>(ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out,
                                                                          ldo, strideO);
   BMM_CHECK_LAUNCH("gemm_tf32x3_kernel");
   return BMM_OK;

@@ -133,11 +133,21 @@ class SketchPipeline:
         self.column = torch.zeros(B * W, **i64)  # zero-init: failed plans gather column 0, never garbage
         self.prob = torch.empty(B * W, **f64)
         self.scale = torch.empty(B * W, **f64)
-        self.C = torch.empty(B * self.m * W, **f64)
-        self.D = torch.empty(B * W * self.p, **f64)
-        self.CD = torch.empty(B * self.m * self.p, **f64)
-        self.ws_gemm = torch.empty(max(256, self.lib.bmm_gemm_f64_workspace(self.m, self.p, W, B)),
-                                   dtype=torch.uint8, device=dev)
+        # float32 inputs take the tcgen05 3xTF32 path (TMA rows need W % 4 == 0)
+        self.tf32 = (dtype == torch.float32 and method != "SSM" and W % 4 == 0)
+        if self.tf32:
+            f32 = dict(dtype=torch.float32, device=dev)
+            self.a_hi = torch.empty(B * self.m * W, **f32)
+            self.a_lo = torch.empty(B * self.m * W, **f32)
+            self.b_hi = torch.empty(B * self.p * W, **f32)
+            self.b_lo = torch.empty(B * self.p * W, **f32)
+            self.CD = torch.empty(B * self.m * self.p, **f32)
+        else:
+            self.C = torch.empty(B * self.m * W, **f64)
+            self.D = torch.empty(B * W * self.p, **f64)
+            self.CD = torch.empty(B * self.m * self.p, **f64)
+            self.ws_gemm = torch.empty(max(256, self.lib.bmm_gemm_f64_workspace(self.m, self.p, W, B)),
+                                       dtype=torch.uint8, device=dev)
         if method == "OPL":
             self.gsq = torch.empty(B * K, **f64)
             self.ws_seg = torch.empty(max(256, self.lib.bmm_segsq_f64_workspace(self.m, self.p, K, B)),
@@ -297,11 +307,18 @@ class SketchPipeline:
         self._c("bmm_sample", P(probs), P(self.cum), P(self.last), P(self.offsets), K, B, n, self.max_len,
                 P(self.budgets),
                 P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
-        self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column), P(self.scale),
-                W, W, B, P(self.C), W, m * W, P(self.D), p, W * p, st)
-        self._c("bmm_gemm_f64", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, B, P(self.CD), p, m * p,
-                P(self.ws_gemm), self.ws_gemm.numel(), st)
-        return self.CD.view(B, m, p) if B > 1 else self.CD.view(m, p)
+        if self.tf32:
+            # float32 inputs: split gather + tcgen05 3xTF32 contraction
+            self._c("bmm_gather_tf32x3", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column), P(self.scale), W, W,
+                    B, P(self.a_hi), P(self.a_lo), P(self.b_hi), P(self.b_lo), st)
+            self._c("bmm_gemm_tf32x3", P(self.a_hi), P(self.a_lo), P(self.b_hi), P(self.b_lo), m, p, W, B,
+                    P(self.CD), p, m * p, st)
+        else:
+            self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column),
+                    P(self.scale), W, W, B, P(self.C), W, m * W, P(self.D), p, W * p, st)
+            self._c("bmm_gemm_f64", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, B, P(self.CD), p, m * p,
+                    P(self.ws_gemm), self.ws_gemm.numel(), st)
+        return self._result()
 
     def _run_ssm(self, M, N, dt, st):
         B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W

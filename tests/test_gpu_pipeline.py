@@ -63,8 +63,10 @@ def test_pipeline_batched_matches_per_problem(dtype):
     Nd = torch.as_tensor(np.stack(Ns), device="cuda")
     sizes = (n // K,) * K
     c = 256
+    tol = 1e-12 if dtype == np.float64 else 1e-5  # float32 inputs run the tcgen05 3xTF32 contraction
     for method in ("ONC", "OPL"):
-        pipe = SketchPipeline(m, n, p, sizes, c, method, batch=B)
+        pipe = SketchPipeline(m, n, p, sizes, c, method, batch=B, dtype=Md.dtype)
+        assert pipe.tf32 == (dtype == np.float32)
         rngs = [workloads.sample_rng(5, b) for b in range(B)]
         CD = pipe.run(Md, Nd, seeds_from_rngs(method, rngs, K)).cpu().numpy()
         pipe.check()
@@ -73,7 +75,27 @@ def test_pipeline_batched_matches_per_problem(dtype):
                                    workloads.sample_rng(5, b))
             assert np.array_equal(pipe.budgets_host()[b], ref["budgets"]), (method, b)
             assert np.array_equal(pipe.columns_host()[b], ref["columns"]), (method, b)
-            assert rel(CD[b], ref["CD"]) < 1e-12
+            assert np.array_equal(pipe.scales_host()[b], ref["scale"]), (method, b)
+            assert rel(CD[b], ref["CD"]) < tol
+
+
+def test_cfg5_subset_against_oracle():
+    """Config 5 problems (float32, 256x4096 . 4096x256, K=64, W=1024): first 8 of the batch."""
+    B, m, n, p, K, W = 8, 256, 4096, 256, 64, 1024
+    probs = [workloads.cfg5_problem(b) for b in range(B)]
+    Md = torch.as_tensor(np.stack([x[0] for x in probs]), device="cuda")
+    Nd = torch.as_tensor(np.stack([x[1] for x in probs]), device="cuda")
+    sizes = (64,) * K
+    pipe = SketchPipeline(m, n, p, sizes, W, "ONC", batch=B, dtype=torch.float32)
+    CD = pipe.run(Md, Nd, seeds_from_rngs("ONC", [workloads.sample_rng(5, b) for b in range(B)], K)).cpu().numpy()
+    pipe.check()
+    for b in range(B):
+        M64, N64 = probs[b][0].astype(np.float64), probs[b][1].astype(np.float64)
+        ref = O.approx_product(M64, N64, sizes, W, "ONC", workloads.sample_rng(5, b))
+        assert np.array_equal(pipe.budgets_host()[b], ref["budgets"])
+        assert np.array_equal(pipe.columns_host()[b], ref["columns"])
+        assert np.array_equal(pipe.scales_host()[b], ref["scale"])
+        assert rel(CD[b], ref["CD"]) < 1e-5
 
 
 def test_pipeline_reports_reference_errors():
