@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     return ap.parse_args()
 
 
@@ -356,10 +356,158 @@ def cpu_baseline(M, N, sizes, runs, cfg, args):
                       f"(NumPy + OpenBLAS, {cpu_cores()} BLAS threads)"}
 
 
+# ---------------------------------------------------------------- float32 device workloads (cfg4, cfg5)
+
+def device_data(torch, name):
+    """Seeded float32 instances generated on the GPU (numpy would take minutes
+    for 2 x 8.6e9 normals); distributions per SURVEY.md §8(d)."""
+    g = torch.Generator(device="cuda").manual_seed(workloads.ROOT + int(name[-1]))
+    if name == "cfg5":
+        B, m, n, p, K = 4096, 256, 4096, 256, 64
+        M = torch.empty((B, m, n), dtype=torch.float32, device="cuda")
+        N = torch.empty((B, n, p), dtype=torch.float32, device="cuda")
+        for b0 in range(0, B, 512):
+            sl = slice(b0, b0 + 512)
+            M[sl].normal_(generator=g).mul_(torch.randn((512, 1, n), generator=g, device="cuda").exp_())
+            N[sl].normal_(generator=g).mul_(torch.randn((512, n, 1), generator=g, device="cuda").exp_())
+        return M, N, (n // K,) * K, B
+    m, n, p, K = 16384, 262144, 16384, 4096
+    cs = (torch.rand(K, generator=g, device="cuda") * 9.9 + 0.1).repeat_interleave(n // K)
+    rs = (torch.rand(K, generator=g, device="cuda") * 9.9 + 0.1).repeat_interleave(n // K)
+    M = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    N = torch.empty((n, p), dtype=torch.float32, device="cuda")
+    for r0 in range(0, m, 1024):
+        M[r0:r0 + 1024].normal_(generator=g).mul_(cs)
+    for r0 in range(0, n, 16384):
+        N[r0:r0 + 16384].normal_(generator=g).mul_(rs[r0:r0 + 16384, None])
+    return M, N, (n // K,) * K, 1
+
+
+def run_device(args):
+    import torch
+    from paper_2105_04940_b200 import _lib
+    from paper_2105_04940_b200.pipeline import SketchPipeline, seeds_from_keys
+    from paper_2105_04940_b200.analysis import sq_diff
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    name = args.workload
+    cfg = int(name[-1])
+    Md, Nd, sizes, B = device_data(torch, name)
+    m, n = Md.shape[-2:]
+    p = Nd.shape[-1]
+    K = len(sizes)
+    W = 1024 if name == "cfg5" else 32768
+    pipe = SketchPipeline(m, n, p, sizes, W, "ONC", batch=B, dtype=torch.float32)
+    keys = np.arange(B)
+
+    def seeds():
+        return seeds_from_keys("ONC", workloads.ROOT, (cfg, 1), keys, K)
+
+    pipe.run(Md, Nd, seeds())
+    pipe.check()
+    pipe.capture(Md, Nd)
+    for _ in range(args.warmup):
+        pipe.run(Md, Nd, seeds())
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler() as clocks:
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pipe.run(Md, Nd, seeds())
+            e1.record()
+            times.append((e0, e1))
+        torch.cuda.synchronize()
+    ms_step = float(np.mean([a.elapsed_time(b) for a, b in times]))
+
+    # per-kernel device times (events on the launching stream)
+    lib, st = _lib.load(), _lib.stream_ptr()
+    P = lambda t: t.data_ptr()  # noqa: E731
+
+    def timed(fn, reps=3):
+        out = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            out.append(e0.elapsed_time(e1))
+        return float(np.median(out))
+
+    norms_ms = timed(lambda: lib.bmm_norms(1, P(Md), m, n, n, m * n, P(Nd), p, p, n * p, B, 0, P(pipe.colsq),
+                                           P(pipe.rowsq), st))
+    gather_ms = timed(lambda: lib.bmm_gather_tf32x3(1, P(Md), n, m * n, P(Nd), p, n * p, m, p, P(pipe.column),
+                                                    P(pipe.scale), W, W, B, P(pipe.a_hi), P(pipe.a_lo),
+                                                    P(pipe.b_hi), P(pipe.b_lo), st))
+    gemm_ms = timed(lambda: lib.bmm_gemm_tf32x3(P(pipe.a_hi), P(pipe.a_lo), P(pipe.b_hi), P(pipe.b_lo), m, p, W, B,
+                                                P(pipe.CD), p, m * p, st))
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peak.get("hbm_gbs", 6650.0))
+    tf32_peak = float(peak.get("bf16_tflops", 1590.0)) / 2  # dense TF32 issues at half the BF16 rate
+    norm_bytes = 4 * B * (m * n + n * p)
+    useful = 2.0 * B * m * p * W
+    executed = 3 * useful
+
+    # error metric on a verification subset (exact product by our DMMA GEMM on float64 upcasts)
+    CD = pipe.run(Md, Nd, seeds())
+    nb = min(B, 32)
+    if name == "cfg5":
+        Mx, Nx = Md[:nb].double(), Nd[:nb].double()
+        exact = torch.empty((nb, m, p), dtype=torch.float64, device="cuda")
+        ws = _lib.workspace(lib.bmm_gemm_f64_workspace(m, p, n, nb))
+        _lib.call("bmm_gemm_f64", P(Mx), n, m * n, P(Nx), p, n * p, m, p, n, nb, P(exact), p, m * p, P(ws),
+                  ws.numel(), st)
+        approx = CD.view(B, m, p)[:nb]
+        err_sq, ref_sq = sq_diff(exact.reshape(nb * m, p), approx.reshape(nb * m, p))
+        fro = float(torch.sqrt((torch.linalg.norm(Md[:nb].double(), dim=(1, 2)) ** 2
+                                * torch.linalg.norm(Nd[:nb].double(), dim=(1, 2)) ** 2).sum()))
+        scope = f"first {nb} problems"
+    else:
+        rows = 256
+        exact = torch.zeros((rows, p), dtype=torch.float64, device="cuda")
+        part = torch.empty((rows, p), dtype=torch.float64, device="cuda")
+        ws = _lib.workspace(lib.bmm_gemm_f64_workspace(rows, p, 16384, 1))
+        for k0 in range(0, n, 16384):
+            Ms = Md[:rows, k0:k0 + 16384].double().contiguous()
+            Ns = Nd[k0:k0 + 16384].double()
+            _lib.call("bmm_gemm_f64", P(Ms), 16384, 0, P(Ns), p, 0, rows, p, 16384, 1, P(part), p, 0, P(ws),
+                      ws.numel(), st)
+            exact += part
+        err_sq, ref_sq = sq_diff(exact, CD.view(m, p)[:rows])
+        fro = float(torch.linalg.norm(Md[:rows].double()) * torch.sqrt(pipe.rowsq.sum()))
+        scope = f"first {rows} rows of C.D"
+    line = {
+        "metric": METRIC, "value": ms_step, "unit": "ms/step", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (3xTF32 tensor, f64 plan)",
+        "data": "synthetic (seeded torch generator on device, SURVEY.md §8(d) distributions)",
+        "config": {"workload": name, "batch": B, "m": m, "n": n, "p": p, "K": K, "W": W, "method": "ONC",
+                   "l2": f"inputs {norm_bytes / 1e9:.1f} GB >> L2"},
+        "gpu_launches": int(pipe.graph_launches),
+        "roofline": {"bound": "tensor", "kernel": "gemm_tf32x3_kernel (tcgen05 kind::tf32 x3)",
+                     "achieved": executed / (gemm_ms * 1e-3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
+                     "frac": executed / (gemm_ms * 1e-3) / 1e12 / tf32_peak,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 rate)",
+                     "useful_fp32_tflops": useful / (gemm_ms * 1e-3) / 1e12, "traffic": None},
+        "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norm_bytes / (norms_ms * 1e-3) / 1e9,
+                           "peak": hbm_peak, "unit": "GB/s", "frac": norm_bytes / (norms_ms * 1e-3) / 1e9 / hbm_peak,
+                           "algorithmic_bytes": norm_bytes},
+        "kernel_ms": {"norms_ms": norms_ms, "gather_tf32x3_ms": gather_ms, "gemm_tf32x3_ms": gemm_ms},
+        "rel_err_reference_metric": float(np.sqrt(err_sq / ref_sq)),
+        "rel_err_baseline_metric": float(np.sqrt(err_sq) / fro), "error_scope": scope,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload in ("cfg4", "cfg5"):
+        return run_device(args)
     return run_ours(args)
 
 

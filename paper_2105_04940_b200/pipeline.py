@@ -71,6 +71,32 @@ def seeds_from_rngs(method: str, rngs: list, K: int, draws: int = 0) -> CallSeed
     return CallSeeds(main=stack([_rng.spawn_words(r, K) for r in rngs]))
 
 
+def seeds_from_keys(method: str, entropy: int, key_prefix: tuple, keys, K: int) -> CallSeeds:
+    """Seeds for a batch of fresh generators ``default_rng(SeedSequence(entropy,
+    spawn_key=key_prefix + (keys[b],)))`` without building them: problem b's
+    estimate spawns children key_prefix + (keys[b], j) (estimators.py:141), and
+    the two-step pilot/main generators are its children 0 and 1
+    (estimators.py:207).  Vectorised; equals seeds_from_rngs on those
+    generators (tests/test_gpu_pipeline.py)."""
+    keys = np.asarray(keys, dtype=np.int64)
+    if (keys < 0).any() or (keys >= 2**32).any():
+        raise ValueError("per-problem keys must fit one 32-bit word")
+    run = _rng._words(int(entropy))
+    run = run + [0] * max(0, 4 - len(run))
+    pre = _rng._words(tuple(key_prefix)) if key_prefix else []
+    base = np.asarray(run + pre, dtype=np.uint32)
+    B = keys.size
+    words = np.concatenate([np.broadcast_to(base, (B, base.size)), keys[:, None].astype(np.uint32)], axis=1)
+    zeros = np.zeros(B, dtype=np.int64)
+    if method in ("ONU", "ONMCNR"):
+        pil = np.concatenate([words, np.zeros((B, 1), np.uint32)], axis=1)
+        mai = np.concatenate([words, np.ones((B, 1), np.uint32)], axis=1)
+        return CallSeeds(main=StreamSeeds(mai, zeros), pilot=StreamSeeds(pil, zeros))
+    if method == "SSM":
+        raise ValueError("SSM draws from the caller's stream; use seeds_from_rngs")
+    return CallSeeds(main=StreamSeeds(np.ascontiguousarray(words), zeros))
+
+
 class SketchPipeline:
     """Preallocated device pipeline for `batch` problems of shape
     M (m x n), N (n x p) sharing one block partition."""

@@ -86,3 +86,15 @@ def test_product_path_fails_loudly_without_gpu():
     import paper_2105_04940_b200 as bm
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         bm.column_norms(np.ones((2, 2)))
+
+
+@pytest.mark.parametrize("method", ["ONC", "ONU"])
+def test_seeds_from_keys_matches_generators(method):
+    from paper_2105_04940_b200.pipeline import seeds_from_keys, seeds_from_rngs
+    keys = np.array([0, 3, 4095])
+    rngs = [np.random.default_rng(np.random.SeedSequence(210504940, spawn_key=(5, 1, int(k)))) for k in keys]
+    a = seeds_from_rngs(method, rngs, 64)
+    b = seeds_from_keys(method, 210504940, (5, 1), keys, 64)
+    assert np.array_equal(a.main.words, b.main.words) and np.array_equal(a.main.first, b.main.first)
+    if method == "ONU":
+        assert np.array_equal(a.pilot.words, b.pilot.words) and np.array_equal(a.pilot.first, b.pilot.first)
