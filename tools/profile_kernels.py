@@ -1,0 +1,32 @@
+"""One pass of each hot kernel at profiling-friendly sizes, for ncu captures.
+
+cfg5-shaped float32 batch (512 problems, ONC, W=1024): norms, plan, sampler,
+split gather, tcgen05 3xTF32 GEMM; cfg2-shaped float64 ONC at W=16000:
+norms, plan, sampler, gather, DMMA GEMM.
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import workloads  # noqa: E402
+from paper_2105_04940_b200.pipeline import SketchPipeline, seeds_from_keys, seeds_from_rngs  # noqa: E402
+
+torch.cuda.set_device(0)
+g = torch.Generator(device="cuda").manual_seed(5)
+B, m, n, p, K, W = 512, 256, 4096, 256, 64, 1024
+M = torch.randn((B, m, n), generator=g, device="cuda") * torch.randn((B, 1, n), generator=g, device="cuda").exp()
+N = torch.randn((B, n, p), generator=g, device="cuda") * torch.randn((B, n, 1), generator=g, device="cuda").exp()
+pipe = SketchPipeline(m, n, p, (64,) * K, W, "ONC", batch=B, dtype=torch.float32)
+pipe.run(M, N, seeds_from_keys("ONC", workloads.ROOT, (5, 1), np.arange(B), K))
+pipe.check()
+
+M2, N2, sizes = workloads.cfg2()
+Md, Nd = torch.as_tensor(M2, device="cuda"), torch.as_tensor(N2, device="cuda")
+pipe2 = SketchPipeline(500, 20000, 500, sizes, 16000, "ONC")
+pipe2.run(Md, Nd, seeds_from_rngs("ONC", [workloads.sample_rng(2, 40)], len(sizes)))
+pipe2.check()
+torch.cuda.synchronize()
+print("profile_kernels ok")
