@@ -134,7 +134,10 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
   constexpr int W = Vec16<T>::N;
   if (M != nullptr) {
     BMM_REQUIRE(colsq != nullptr, BMM_E_ARG, "bmm_norms: colsq is NULL");
-    const bool vec_ok = (reinterpret_cast<uintptr_t>(M) % 16 == 0) && (ldm % W == 0) &&
+    // Few columns (e.g. config 2: 20000): one column per thread in 64-thread CTAs
+    // spreads the chains over every SM and keeps 32 row loads in flight each.
+    const bool narrow = (n / W) * batch < 148LL * 256;
+    const bool vec_ok = !narrow && (reinterpret_cast<uintptr_t>(M) % 16 == 0) && (ldm % W == 0) &&
                         (strideM % W == 0) && n >= W;
     int64_t c_tail = 0;
     if (vec_ok) {
@@ -145,8 +148,13 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
       BMM_CHECK_LAUNCH("colsq_vec_kernel");
     }
     if (c_tail < n) {
-      colsq_scalar_kernel<T, 16><<<grid_for((n - c_tail) * batch, 256, 8, 64), 256, 0, st>>>(
-          M, m, n, c_tail, ldm, strideM, batch, accumulate, colsq);
+      if (narrow) {
+        colsq_scalar_kernel<T, 32><<<grid_for((n - c_tail) * batch, 64, 32, 64), 64, 0, st>>>(
+            M, m, n, c_tail, ldm, strideM, batch, accumulate, colsq);
+      } else {
+        colsq_scalar_kernel<T, 16><<<grid_for((n - c_tail) * batch, 256, 8, 64), 256, 0, st>>>(
+            M, m, n, c_tail, ldm, strideM, batch, accumulate, colsq);
+      }
       BMM_CHECK_LAUNCH("colsq_scalar_kernel");
     }
   }

@@ -31,7 +31,7 @@ __device__ __forceinline__ double pw_leaf(const Src& src, int64_t s, int64_t len
   src.load8(s, r);
   const int64_t body = len - (len % 8);
   int64_t i = 8;
-#pragma unroll 2
+#pragma unroll 4
   for (; i < body; i += 8) {
     double v[8];
     src.load8(s + i, v);

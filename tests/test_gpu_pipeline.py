@@ -98,6 +98,25 @@ def test_cfg5_subset_against_oracle():
         assert rel(CD[b], ref["CD"]) < 1e-5
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("method", ["ONC", "OPL"])
+def test_sharded_world1_matches_pipeline(dtype, method):
+    from paper_2105_04940_b200.distributed import ShardLayout, ShardedApproxProduct
+    M, N, sizes = workloads.cfg2(n=4096, m=256, p=128, K=16)
+    Md = torch.as_tensor(M, device="cuda", dtype=dtype)
+    Nd = torch.as_tensor(N, device="cuda", dtype=dtype)
+    W = 1024
+    sh = ShardedApproxProduct(ShardLayout(1, 0, 256, 4096, 128), sizes, W, method, dtype=dtype)
+    rng = np.random.default_rng(9)
+    seeds = seeds_from_rngs(method, [rng], len(sizes))
+    out = sh.run(Md, Nd, seeds.main.words[0], int(seeds.main.first[0])).cpu().numpy()
+    sh.check()
+    pipe = SketchPipeline(256, 4096, 128, sizes, W, method, dtype=dtype)
+    ref = pipe.run(Md, Nd, seeds_from_rngs(method, [np.random.default_rng(9)], len(sizes))).cpu().numpy()
+    assert np.array_equal(sh.column.cpu().numpy(), pipe.columns_host()[0])
+    assert np.array_equal(out, ref)
+
+
 def test_pipeline_reports_reference_errors():
     M, N, sizes = workloads.cfg1(scale=10)
     Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
