@@ -317,7 +317,7 @@ struct SplitPlan {
 
 inline SplitPlan plan_split(int64_t m, int64_t nc, int64_t k, int64_t batch) {
   const int64_t tiles = ceil_div(m, GB_M) * ceil_div(nc, GB_N) * batch;
-  int64_t splits = ceil_div(2 * 148, tiles);
+  int64_t splits = ceil_div(3 * 148, tiles);  // one full wave at 3 CTAs per SM
   const int64_t max_splits = ceil_div(k, 4 * GB_K);  // at least 64 of k per split
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
@@ -330,7 +330,7 @@ inline SplitPlan plan_split(int64_t m, int64_t nc, int64_t k, int64_t batch) {
 
 inline int64_t segsq_chunks(int64_t m, int64_t nc, int64_t nseg, int64_t batch) {
   const int64_t tiles = ceil_div(m, GB_M) * ceil_div(nc, GB_N) * batch;
-  int64_t ch = ceil_div(2 * 148, tiles);
+  int64_t ch = ceil_div(3 * 148, tiles);
   if (ch > nseg) ch = nseg;
   if (ch < 1) ch = 1;
   if (batch * ch > 65535) ch = 65535 / batch;

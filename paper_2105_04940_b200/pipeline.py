@@ -205,12 +205,35 @@ class SketchPipeline:
             u = np.concatenate([np.full(nk, 1.0 / nk) for nk in self.sizes])
             self._uprobs = torch.as_tensor(np.tile(u, B), device=dev)
         self.graph = None
+        self.timeline = None
 
     # ------------------------------------------------------------------ steps
     def _c(self, name, *args):
         rc = getattr(self.lib, name)(*args)
         if rc < 0:
             raise RuntimeError(f"{name} failed ({rc}): {self.lib.bmm_last_error().decode()}")
+        if self.timeline is not None:  # eager profiling: an event after every stage
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.timeline.append((name, ev))
+
+    def stage_times(self, M, N, seeds) -> list:
+        """Eager run with a CUDA event after every C-ABI call; returns
+        [(entry point, ms)] in launch order (warm caches, real context)."""
+        self.set_seeds(seeds)
+        start = torch.cuda.Event(enable_timing=True)
+        start.record()
+        self.timeline = []
+        try:
+            self.launch(M, N)
+        finally:
+            tl, self.timeline = self.timeline, None
+        torch.cuda.synchronize()
+        out, prev = [], start
+        for name, ev in tl:
+            out.append((name, prev.elapsed_time(ev)))
+            prev = ev
+        return out
 
     def _seed(self, which: str, states: torch.Tensor, st):
         words, first = self._seedbuf[which]
