@@ -95,9 +95,10 @@ int bmm_norms(int dtype,
  *   fnorm[k]= ||M^k||_F * ||N_k||_F (SSM block weights)            plan.py:483-492
  *   cum/last: optional fused inverse-CDF tables of probs (see bmm_block_cdf)
  * probs / s / fnorm / cum may be NULL to skip.  colsq/rowsq/probs/cum stride
- * = n, s/fnorm/last stride = K.  One warp per block.                       */
+ * = n, s/fnorm/last stride = K.  One warp per block; max_len >= the largest
+ * block size (blocks up to 5120 elements are processed in shared memory).  */
 int bmm_block_probs(const double* colsq, const double* rowsq, int64_t n,
-                    const int64_t* offsets, int64_t K, int64_t batch,
+                    const int64_t* offsets, int64_t K, int64_t batch, int64_t max_len,
                     double* probs, double* s, double* fnorm,
                     double* cum, int64_t* last_support, void* stream);
 

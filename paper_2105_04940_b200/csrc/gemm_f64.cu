@@ -17,7 +17,8 @@
 
 namespace bmm {
 
-constexpr int GB_M = 64, GB_N = 64, GB_K = 16, G_STAGES = 4, G_THREADS = 128;
+constexpr int GB_M = 64, GB_N = 64, GB_K = 16, G_STAGES = 3, G_THREADS = 128;
+constexpr int G_CTAS_PER_SM = 4;  // 55.5 KB smem and 128 x 128 registers per CTA
 constexpr int A_STR = GB_K + 4;   // doubles per A smem row
 constexpr int B_STR = GB_N + 4;   // doubles per B smem row
 constexpr int A_TILE = GB_M * A_STR;
@@ -143,7 +144,7 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
 }
 
 template <bool V16>
-__global__ void __launch_bounds__(G_THREADS) gemm_f64_kernel(const double* __restrict__ A, int64_t lda,
+__global__ void __launch_bounds__(G_THREADS, G_CTAS_PER_SM) gemm_f64_kernel(const double* __restrict__ A, int64_t lda,
                                                              int64_t strideA, const double* __restrict__ B,
                                                              int64_t ldb, int64_t strideB, int64_t m, int64_t nc,
                                                              int64_t k, int64_t splits, int64_t kchunk,
@@ -196,7 +197,7 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ part, int64_t sp
 }
 
 // ---- segmented square sums
-__global__ void __launch_bounds__(G_THREADS) segsq_f64_kernel(const double* __restrict__ A, int64_t lda,
+__global__ void __launch_bounds__(G_THREADS, G_CTAS_PER_SM) segsq_f64_kernel(const double* __restrict__ A, int64_t lda,
                                                               int64_t strideA, const double* __restrict__ B,
                                                               int64_t ldb, int64_t strideB, int64_t m,
                                                               int64_t nc, const int64_t* __restrict__ seg,
@@ -317,7 +318,7 @@ struct SplitPlan {
 
 inline SplitPlan plan_split(int64_t m, int64_t nc, int64_t k, int64_t batch) {
   const int64_t tiles = ceil_div(m, GB_M) * ceil_div(nc, GB_N) * batch;
-  int64_t splits = ceil_div(3 * 148, tiles);  // one full wave at 3 CTAs per SM
+  int64_t splits = ceil_div(G_CTAS_PER_SM * 148, tiles);  // one full wave
   const int64_t max_splits = ceil_div(k, 4 * GB_K);  // at least 64 of k per split
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
@@ -330,7 +331,7 @@ inline SplitPlan plan_split(int64_t m, int64_t nc, int64_t k, int64_t batch) {
 
 inline int64_t segsq_chunks(int64_t m, int64_t nc, int64_t nseg, int64_t batch) {
   const int64_t tiles = ceil_div(m, GB_M) * ceil_div(nc, GB_N) * batch;
-  int64_t ch = ceil_div(3 * 148, tiles);
+  int64_t ch = ceil_div(G_CTAS_PER_SM * 148, tiles);
   if (ch > nseg) ch = nseg;
   if (ch < 1) ch = 1;
   if (batch * ch > 65535) ch = 65535 / batch;

@@ -27,15 +27,20 @@ constexpr int kProbWarps = 4;
 
 // One warp per (problem, block).  Elementwise steps are lane-parallel
 // (coalesced); the NumPy sums are warp_pw_sum; the optional CDF is the
-// sequential np.cumsum on lane 0 (estimators.py:37-38) so the sampler can
-// start from it directly.
+// sequential np.cumsum (warp_cumsum, estimators.py:37-38) so the sampler can
+// start from it directly.  SMEM: the block's scores are staged in a per-warp
+// shared-memory slice (max_len doubles), so the three sums, two divisions and
+// the cumsum run on chip; only the score loads and the final stores touch HBM.
+template <bool SMEM>
 __global__ void __launch_bounds__(32 * kProbWarps) block_probs_kernel(
     const double* __restrict__ colsq, const double* __restrict__ rowsq, int64_t n,
     const int64_t* __restrict__ offsets, int64_t K, int64_t batch, double* __restrict__ probs,
     double* __restrict__ s, double* __restrict__ fnorm, double* __restrict__ cum,
-    int64_t* __restrict__ last) {
+    int64_t* __restrict__ last, int64_t max_len) {
   __shared__ WarpPwScratch scratch[kProbWarps];
+  extern __shared__ double dyn[];
   WarpPwScratch* scr = &scratch[threadIdx.x >> 5];
+  double* sbuf = dyn + (SMEM ? (threadIdx.x >> 5) * max_len : 0);
   const int lane = threadIdx.x & 31;
   const int64_t total = K * batch;
   for (int64_t g = blockIdx.x * (int64_t)kProbWarps + (threadIdx.x >> 5); g < total;
@@ -46,32 +51,37 @@ __global__ void __launch_bounds__(32 * kProbWarps) block_probs_kernel(
     const double* rs = rowsq + b * n;
     SrcScore sc{cs, rs};
     if (probs != nullptr) {
-      double* pb = probs + b * n;
-      // stage sc into the output vector, then normalise in place
-      for (int64_t i = lane; i < nk; i += 32) pb[o + i] = sc(o + i);
+      double* pb = probs + b * n + o;
+      double* wb = SMEM ? sbuf : pb;
+      // stage the scores, then normalise in place
+#pragma unroll 4
+      for (int64_t i = lane; i < nk; i += 32) wb[i] = sc(o + i);
       __syncwarp();
-      const SrcF64 sp{pb};
+      const SrcF64 sp{wb};
       // total = sk.sum(); p = sk / total; p / p.sum()      plan.py:199-205
-      const double tot = __dadd_rn(0.0, warp_pw_sum(sp, o, nk, scr));
+      const double tot = __dadd_rn(0.0, warp_pw_sum(sp, 0, nk, scr));
       if (s != nullptr) {
         // np.add.reduceat: first element, then the pairwise sum of the rest   plan.py:173
-        const double rest = warp_pw_sum(sp, o + 1, nk - 1, scr);
-        if (lane == 0) s[g] = __dadd_rn(pb[o], rest);
+        const double rest = warp_pw_sum(sp, 1, nk - 1, scr);
+        if (lane == 0) s[g] = __dadd_rn(wb[0], rest);
       }
       __syncwarp();
       if (tot == 0.0) {
-        for (int64_t i = lane; i < nk; i += 32) pb[o + i] = 0.0;
+        for (int64_t i = lane; i < nk; i += 32) wb[i] = 0.0;
       } else {
-        for (int64_t i = lane; i < nk; i += 32) pb[o + i] = __ddiv_rn(pb[o + i], tot);
+        for (int64_t i = lane; i < nk; i += 32) wb[i] = __ddiv_rn(wb[i], tot);
         __syncwarp();
-        const double tot2 = __dadd_rn(0.0, warp_pw_sum(sp, o, nk, scr));
-        for (int64_t i = lane; i < nk; i += 32) pb[o + i] = __ddiv_rn(pb[o + i], tot2);
+        const double tot2 = __dadd_rn(0.0, warp_pw_sum(sp, 0, nk, scr));
+        for (int64_t i = lane; i < nk; i += 32) wb[i] = __ddiv_rn(wb[i], tot2);
       }
       __syncwarp();
+      if (SMEM)
+        for (int64_t i = lane; i < nk; i += 32) pb[i] = wb[i];
       if (cum != nullptr) {
-        const int64_t lst = warp_cumsum(pb + o, cum + b * n + o, nk);
+        const int64_t lst = warp_cumsum(wb, cum + b * n + o, nk);
         if (lane == 0) last[g] = lst;
       }
+      __syncwarp();
     } else if (s != nullptr) {
       const double rest = warp_pw_sum(sc, o + 1, nk - 1, scr);
       if (lane == 0) s[g] = __dadd_rn(sc(o), rest);
@@ -504,16 +514,28 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
 using namespace bmm;
 
 extern "C" int bmm_block_probs(const double* colsq, const double* rowsq, int64_t n,
-                               const int64_t* offsets, int64_t K, int64_t batch, double* probs,
-                               double* s, double* fnorm, double* cum, int64_t* last_support,
+                               const int64_t* offsets, int64_t K, int64_t batch, int64_t max_len,
+                               double* probs, double* s, double* fnorm, double* cum, int64_t* last_support,
                                void* stream) {
-  BMM_REQUIRE(K >= 1 && batch >= 1 && n >= 1, BMM_E_ARG, "bmm_block_probs: bad shape");
+  BMM_REQUIRE(K >= 1 && batch >= 1 && n >= 1 && max_len >= 1, BMM_E_ARG, "bmm_block_probs: bad shape");
   BMM_REQUIRE(cum == nullptr || (probs != nullptr && last_support != nullptr), BMM_E_ARG,
               "bmm_block_probs: cum needs probs and last_support");
   const int64_t warps = K * batch;
   unsigned grid = (unsigned)std::min<int64_t>(ceil_div(warps, kProbWarps), 148LL * 16 * 64);
-  block_probs_kernel<<<grid, 32 * kProbWarps, 0, as_stream(stream)>>>(colsq, rowsq, n, offsets, K, batch,
-                                                                      probs, s, fnorm, cum, last_support);
+  const int64_t smem = max_len * 8 * kProbWarps;
+  cudaStream_t st = as_stream(stream);
+  if (smem <= 160 * 1024) {
+    static int64_t attr = 0;
+    if (smem > 48 * 1024 && attr == 0) {
+      cudaFuncSetAttribute(block_probs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      attr = 1;
+    }
+    block_probs_kernel<true><<<grid, 32 * kProbWarps, (size_t)smem, st>>>(colsq, rowsq, n, offsets, K, batch, probs,
+                                                                          s, fnorm, cum, last_support, max_len);
+  } else {
+    block_probs_kernel<false><<<grid, 32 * kProbWarps, 0, st>>>(colsq, rowsq, n, offsets, K, batch, probs, s, fnorm,
+                                                               cum, last_support, max_len);
+  }
   BMM_CHECK_LAUNCH("block_probs_kernel");
   return BMM_OK;
 }

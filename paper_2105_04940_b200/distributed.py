@@ -179,7 +179,7 @@ class ShardedApproxProduct:
                     None, P(rowsq), st)
         full = exchange_sum(self.norms_part, self.group)
         colsq, rowsq = full[:n], full[n:]
-        self._c("bmm_block_probs", P(colsq), P(rowsq), n, P(self.offsets), K, 1, P(self.probs), P(self.s), None,
+        self._c("bmm_block_probs", P(colsq), P(rowsq), n, P(self.offsets), K, 1, max(self.sizes), P(self.probs), P(self.s), None,
                 P(self.cum), P(self.last), st)
         aux = None
         if self.method == "OPL":

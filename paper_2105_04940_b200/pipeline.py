@@ -315,7 +315,7 @@ class SketchPipeline:
         if self.method == "SSM":
             return self._run_ssm(M, N, dt, st)
         # probabilities, score sums and (fused) the main CDF of the optimal probabilities
-        self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B,
+        self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B, self.max_len,
                 P(self.probs), P(self.s), None, P(self.cum), P(self.last), st)
         rule = {"ONC": _lib.RULE_ONC, "OPL": _lib.RULE_OPL, "UU": _lib.RULE_UU,
                 "ONU": _lib.RULE_TWO_STEP, "ONMCNR": _lib.RULE_TWO_STEP}[self.method]
@@ -372,7 +372,7 @@ class SketchPipeline:
     def _run_ssm(self, M, N, dt, st):
         B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W
         P = lambda t: t.data_ptr()  # noqa: E731
-        self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B, None, None,
+        self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B, self.max_len, None, None,
                 P(self.fnorm), None, None, st)
         self._c("bmm_normalize", P(self.fnorm), K, B, P(self.q), P(self.status), st)
         self._c("bmm_block_cdf", P(self.q), P(self.qoff), 1, B, K, P(self.qcum), P(self.qlast), st)

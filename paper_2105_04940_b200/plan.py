@@ -181,7 +181,7 @@ class DeviceInstance:
         sk = torch.empty(self.K, dtype=torch.float64, device=dev) if s else None
         fk = torch.empty(self.K, dtype=torch.float64, device=dev) if fnorm else None
         _lib.call("bmm_block_probs", _lib.ptr(colsq), _lib.ptr(rowsq), self.n, _lib.ptr(self.offsets),
-                  self.K, 1, _lib.ptr(pr), _lib.ptr(sk), _lib.ptr(fk), None, None, _lib.stream_ptr())
+                  self.K, 1, self.max_len, _lib.ptr(pr), _lib.ptr(sk), _lib.ptr(fk), None, None, _lib.stream_ptr())
         return pr, sk, fk
 
     def block_product_sq(self) -> torch.Tensor:
