@@ -140,11 +140,16 @@ struct WarpPwScratch {
 
 template <class Src>
 __device__ __forceinline__ double warp_leaf8(const Src& src, int64_t s, int64_t len, int j) {
-  // accumulator j of a leaf with len >= 8
-  double r = src(s + j);
-  const int64_t body = len - (len % 8);
-#pragma unroll 4
-  for (int64_t i = 8; i < body; i += 8) r = __dadd_rn(r, src(s + i + j));
+  // accumulator j of a leaf with 8 <= len <= 128: at most 16 strided elements,
+  // all loaded before the (ordered) adds so the whole leaf is in flight at once
+  const int steps = (int)(len / 8);
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = (q < steps) ? src(s + 8 * q + j) : 0.0;
+  double r = v[0];
+#pragma unroll
+  for (int q = 1; q < 16; ++q)
+    if (q < steps) r = __dadd_rn(r, v[q]);
   return r;
 }
 
