@@ -17,14 +17,6 @@
 
 namespace bmm {
 
-constexpr int GB_M = 64, GB_N = 64, GB_K = 16, G_STAGES = 3, G_THREADS = 128;
-constexpr int G_CTAS_PER_SM = 4;  // 55.5 KB smem and 128 x 128 registers per CTA
-constexpr int A_STR = GB_K + 4;   // doubles per A smem row
-constexpr int B_STR = GB_N + 4;   // doubles per B smem row
-constexpr int A_TILE = GB_M * A_STR;
-constexpr int B_TILE = GB_K * B_STR;
-constexpr int G_SMEM_BYTES = G_STAGES * (A_TILE + B_TILE) * 8;
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -45,6 +37,20 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// CTA tile BM x BN x 16, warp tile WM x WN (FM x FN DMMA 8x8 fragments),
+// STAGES-deep cp.async ring.  Shared rows are padded by 4 doubles so the
+// fragment loads (row g / column t patterns) are conflict-free per half-warp.
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_>
+struct DCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = 16, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int WARPS_N = BN / WN, WARPS = (BM / WM) * WARPS_N, THREADS = 32 * WARPS;
+  static constexpr int FM = WM / 8, FN = WN / 8;
+  static constexpr int A_STR = BK + 4, B_STR = BN + 4;
+  static constexpr int A_TILE = BM * A_STR, B_TILE = BK * B_STR;
+  static constexpr int SMEM = STAGES * (A_TILE + B_TILE) * 8;
+  static_assert((BM * BK / 2) % THREADS == 0 && (BK * BN / 2) % THREADS == 0, "loader split");
+};
+
 struct TileArgs {
   const double* A; int64_t lda;
   const double* B; int64_t ldb;
@@ -53,129 +59,129 @@ struct TileArgs {
 };
 
 // Stage one BK slice [k0, k0+BK) of the A and B tiles; columns at or beyond kend are zero.
-template <bool V16>
+template <class C, bool V16>
 __device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64_t kend, double* as, double* bs) {
   const int tid = threadIdx.x;
   if constexpr (V16) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c = tid + G_THREADS * q;
+    for (int q = 0; q < C::BM * C::BK / 2 / C::THREADS; ++q) {
+      const int c = tid + C::THREADS * q;
       const int row = c >> 3, kc = (c & 7) * 2;
       const int64_t gr = ta.m0 + row, gk = k0 + kc;
       int64_t nv = kend - gk;
       nv = nv < 0 ? 0 : (nv > 2 ? 2 : nv);
       if (gr >= ta.m) nv = 0;
       const double* src = nv ? ta.A + gr * ta.lda + gk : ta.A;
-      cp_async16(smem_u32(as + row * A_STR + kc), src, (int)(nv * 8));
+      cp_async16(smem_u32(as + row * C::A_STR + kc), src, (int)(nv * 8));
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c = tid + G_THREADS * q;
-      const int row = c >> 5, nc2 = (c & 31) * 2;
+    for (int q = 0; q < C::BK * C::BN / 2 / C::THREADS; ++q) {
+      const int c = tid + C::THREADS * q;
+      const int row = c / (C::BN / 2), nc2 = (c % (C::BN / 2)) * 2;
       const int64_t gk = k0 + row, gn = ta.n0 + nc2;
       int64_t nv = ta.nc - gn;
       nv = nv < 0 ? 0 : (nv > 2 ? 2 : nv);
       if (gk >= kend) nv = 0;
       const double* src = nv ? ta.B + gk * ta.ldb + gn : ta.B;
-      cp_async16(smem_u32(bs + row * B_STR + nc2), src, (int)(nv * 8));
+      cp_async16(smem_u32(bs + row * C::B_STR + nc2), src, (int)(nv * 8));
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = tid + G_THREADS * q;
-      const int row = c >> 4, kk = c & 15;
+    for (int q = 0; q < C::BM * C::BK / C::THREADS; ++q) {
+      const int c = tid + C::THREADS * q;
+      const int row = c / C::BK, kk = c % C::BK;
       const int64_t gr = ta.m0 + row, gk = k0 + kk;
       const bool ok = gr < ta.m && gk < kend;
-      cp_async8(smem_u32(as + row * A_STR + kk), ok ? ta.A + gr * ta.lda + gk : ta.A, ok ? 8 : 0);
+      cp_async8(smem_u32(as + row * C::A_STR + kk), ok ? ta.A + gr * ta.lda + gk : ta.A, ok ? 8 : 0);
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = tid + G_THREADS * q;
-      const int row = c >> 6, nn = c & 63;
+    for (int q = 0; q < C::BK * C::BN / C::THREADS; ++q) {
+      const int c = tid + C::THREADS * q;
+      const int row = c / C::BN, nn = c % C::BN;
       const int64_t gk = k0 + row, gn = ta.n0 + nn;
       const bool ok = gk < kend && gn < ta.nc;
-      cp_async8(smem_u32(bs + row * B_STR + nn), ok ? ta.B + gk * ta.ldb + gn : ta.B, ok ? 8 : 0);
+      cp_async8(smem_u32(bs + row * C::B_STR + nn), ok ? ta.B + gk * ta.ldb + gn : ta.B, ok ? 8 : 0);
     }
   }
 }
 
-// acc += A[m0:+64, kbeg:kend] @ B[kbeg:kend, n0:+64]
-template <bool V16>
+// acc += A[m0:+BM, kbeg:kend] @ B[kbeg:kend, n0:+BN]
+template <class C, bool V16>
 __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64_t kend, double* smem,
-                                         double (&acc)[4][4][2]) {
+                                         double (&acc)[C::FM][C::FN][2]) {
   double* As = smem;
-  double* Bs = smem + G_STAGES * A_TILE;
+  double* Bs = smem + C::STAGES * C::A_TILE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t ktiles = (kend - kbeg + GB_K - 1) / GB_K;
+  const int64_t ktiles = (kend - kbeg + C::BK - 1) / C::BK;
 #pragma unroll
-  for (int s = 0; s < G_STAGES - 1; ++s) {
-    if (s < ktiles) load_stage<V16>(ta, kbeg + s * GB_K, kend, As + s * A_TILE, Bs + s * B_TILE);
+  for (int s = 0; s < C::STAGES - 1; ++s) {
+    if (s < ktiles) load_stage<C, V16>(ta, kbeg + s * C::BK, kend, As + s * C::A_TILE, Bs + s * C::B_TILE);
     cp_async_commit();
   }
   for (int64_t kt = 0; kt < ktiles; ++kt) {
-    cp_async_wait<G_STAGES - 2>();
+    cp_async_wait<C::STAGES - 2>();
     __syncthreads();
-    const int64_t nt = kt + G_STAGES - 1;
+    const int64_t nt = kt + C::STAGES - 1;
     if (nt < ktiles) {
-      const int ns = (int)(nt % G_STAGES);
-      load_stage<V16>(ta, kbeg + nt * GB_K, kend, As + ns * A_TILE, Bs + ns * B_TILE);
+      const int ns = (int)(nt % C::STAGES);
+      load_stage<C, V16>(ta, kbeg + nt * C::BK, kend, As + ns * C::A_TILE, Bs + ns * C::B_TILE);
     }
     cp_async_commit();
-    const int cs = (int)(kt % G_STAGES);
-    const double* as = As + cs * A_TILE + (wm * 32 + g) * A_STR + t;
-    const double* bs = Bs + cs * B_TILE + t * B_STR + wn * 32 + g;
+    const int cs = (int)(kt % C::STAGES);
+    const double* as = As + cs * C::A_TILE + (wm * C::WM + g) * C::A_STR + t;
+    const double* bs = Bs + cs * C::B_TILE + t * C::B_STR + wn * C::WN + g;
 #pragma unroll
-    for (int kk = 0; kk < GB_K; kk += 4) {
-      double a[4], b[4];
+    for (int kk = 0; kk < C::BK; kk += 4) {
+      double a[C::FM], b[C::FN];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = as[mi * 8 * A_STR + kk];
+      for (int mi = 0; mi < C::FM; ++mi) a[mi] = as[mi * 8 * C::A_STR + kk];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = bs[kk * B_STR + ni * 8];
+      for (int ni = 0; ni < C::FN; ++ni) b[ni] = bs[kk * C::B_STR + ni * 8];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+        for (int ni = 0; ni < C::FN; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
     }
   }
   cp_async_wait<0>();
   __syncthreads();
 }
 
-template <bool V16>
-__global__ void __launch_bounds__(G_THREADS, G_CTAS_PER_SM) gemm_f64_kernel(const double* __restrict__ A, int64_t lda,
-                                                             int64_t strideA, const double* __restrict__ B,
-                                                             int64_t ldb, int64_t strideB, int64_t m, int64_t nc,
-                                                             int64_t k, int64_t splits, int64_t kchunk,
-                                                             double* __restrict__ out, int64_t ldo,
-                                                             int64_t strideO, double* __restrict__ part) {
+template <class C, bool V16>
+__global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __restrict__ A, int64_t lda,
+                                                              int64_t strideA, const double* __restrict__ B,
+                                                              int64_t ldb, int64_t strideB, int64_t m, int64_t nc,
+                                                              int64_t k, int64_t splits, int64_t kchunk,
+                                                              double* __restrict__ out, int64_t ldo,
+                                                              int64_t strideO, double* __restrict__ part) {
   extern __shared__ __align__(16) double smem[];
   const int64_t z = blockIdx.z;
   const int64_t b = z / splits, sp = z - b * splits;
-  TileArgs ta{A + b * strideA, lda, B + b * strideB, ldb, m, nc, (int64_t)blockIdx.y * GB_M,
-              (int64_t)blockIdx.x * GB_N};
+  TileArgs ta{A + b * strideA, lda, B + b * strideB, ldb, m, nc, (int64_t)blockIdx.y * C::BM,
+              (int64_t)blockIdx.x * C::BN};
   const int64_t kbeg = sp * kchunk;
   const int64_t kend = min(k, kbeg + kchunk);
-  double acc[4][4][2];
+  double acc[C::FM][C::FN][2];
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  if (kbeg < kend) mainloop<V16>(ta, kbeg, kend, smem, acc);
+    for (int ni = 0; ni < C::FN; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  if (kbeg < kend) mainloop<C, V16>(ta, kbeg, kend, smem, acc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N, g = lane >> 2, t = lane & 3;
   double* dst;
   int64_t ld;
   if (splits == 1) { dst = out + b * strideO; ld = ldo; }
   else { dst = part + z * m * nc; ld = nc; }
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
-    const int64_t r = ta.m0 + wm * 32 + mi * 8 + g;
+  for (int mi = 0; mi < C::FM; ++mi) {
+    const int64_t r = ta.m0 + wm * C::WM + mi * 8 + g;
     if (r >= m) continue;
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int64_t c0 = ta.n0 + wn * 32 + ni * 8 + 2 * t;
+    for (int ni = 0; ni < C::FN; ++ni) {
+      const int64_t c0 = ta.n0 + wn * C::WN + ni * 8 + 2 * t;
       if (c0 < nc) dst[r * ld + c0] = acc[mi][ni][0];
       if (c0 + 1 < nc) dst[r * ld + c0 + 1] = acc[mi][ni][1];
     }
@@ -197,35 +203,36 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ part, int64_t sp
 }
 
 // ---- segmented square sums
-__global__ void __launch_bounds__(G_THREADS, G_CTAS_PER_SM) segsq_f64_kernel(const double* __restrict__ A, int64_t lda,
-                                                              int64_t strideA, const double* __restrict__ B,
-                                                              int64_t ldb, int64_t strideB, int64_t m,
-                                                              int64_t nc, const int64_t* __restrict__ seg,
-                                                              int64_t nseg, int64_t seg_stride,
-                                                              int64_t chunks, double* __restrict__ part) {
+template <class C>
+__global__ void __launch_bounds__(C::THREADS) segsq_f64_kernel(const double* __restrict__ A, int64_t lda,
+                                                               int64_t strideA, const double* __restrict__ B,
+                                                               int64_t ldb, int64_t strideB, int64_t m,
+                                                               int64_t nc, const int64_t* __restrict__ seg,
+                                                               int64_t nseg, int64_t seg_stride,
+                                                               int64_t chunks, double* __restrict__ part) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ double red[G_THREADS / 32];
+  __shared__ double red[C::WARPS];
   const int64_t z = blockIdx.z;
   const int64_t b = z / chunks, ch = z - b * chunks;
   const int64_t per = (nseg + chunks - 1) / chunks;
   const int64_t j0 = ch * per, j1 = min(nseg, j0 + per);
-  TileArgs ta{A + b * strideA, lda, B + b * strideB, ldb, m, nc, (int64_t)blockIdx.y * GB_M,
-              (int64_t)blockIdx.x * GB_N};
+  TileArgs ta{A + b * strideA, lda, B + b * strideB, ldb, m, nc, (int64_t)blockIdx.y * C::BM,
+              (int64_t)blockIdx.x * C::BN};
   const int64_t tiles = (int64_t)gridDim.x * gridDim.y;
   const int64_t tile = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
   for (int64_t j = j0; j < j1; ++j) {
     const int64_t kbeg = seg[b * seg_stride + j], kend = seg[b * seg_stride + j + 1];
-    double acc[4][4][2];
+    double acc[C::FM][C::FN][2];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-    if (kbeg < kend) mainloop<false>(ta, kbeg, kend, smem, acc);
+      for (int ni = 0; ni < C::FN; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    if (kbeg < kend) mainloop<C, false>(ta, kbeg, kend, smem, acc);
     double sq = 0.0;
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
+      for (int ni = 0; ni < C::FN; ++ni) {
         sq = fma(acc[mi][ni][0], acc[mi][ni][0], sq);
         sq = fma(acc[mi][ni][1], acc[mi][ni][1], sq);
       }
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(G_THREADS, G_CTAS_PER_SM) segsq_f64_kernel(con
     __syncthreads();
     if (threadIdx.x == 0) {
       double tot = red[0];
-      for (int w = 1; w < G_THREADS / 32; ++w) tot += red[w];
+      for (int w = 1; w < C::WARPS; ++w) tot += red[w];
       part[(b * nseg + j) * tiles + tile] = tot;
     }
     __syncthreads();
@@ -316,34 +323,104 @@ struct SplitPlan {
   int64_t splits, kchunk;
 };
 
-inline SplitPlan plan_split(int64_t m, int64_t nc, int64_t k, int64_t batch) {
-  const int64_t tiles = ceil_div(m, GB_M) * ceil_div(nc, GB_N) * batch;
-  int64_t splits = ceil_div(G_CTAS_PER_SM * 148, tiles);  // one full wave
-  const int64_t max_splits = ceil_div(k, 4 * GB_K);  // at least 64 of k per split
+// ---- tile-configuration variants (selected once; bmm_gemm_f64_set_variant for tuning)
+using DV0 = DCfg<64, 64, 32, 32, 3>;
+using DV1 = DCfg<64, 128, 32, 64, 3>;
+using DV2 = DCfg<128, 64, 64, 32, 3>;
+using DV3 = DCfg<128, 128, 64, 32, 3>;
+using DV4 = DCfg<128, 128, 32, 64, 3>;
+using DV5 = DCfg<64, 64, 32, 32, 4>;
+using DV6 = DCfg<128, 64, 32, 32, 3>;
+constexpr int kVariants = 7;
+static int g_variant = 0;
+
+struct VariantInfo {
+  int BM, BN, BK, threads, smem, occ;
+};
+
+template <class C>
+static VariantInfo info_of() {
+  static int occ = -1;
+  if (occ < 0) {
+    cudaFuncSetAttribute(gemm_f64_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(gemm_f64_kernel<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(segsq_f64_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, gemm_f64_kernel<C, true>, C::THREADS, C::SMEM) !=
+            cudaSuccess || o < 1)
+      o = 1;
+    occ = o;
+  }
+  return VariantInfo{C::BM, C::BN, C::BK, C::THREADS, C::SMEM, occ};
+}
+
+static VariantInfo variant_info(int v) {
+  switch (v) {
+    case 1: return info_of<DV1>();
+    case 2: return info_of<DV2>();
+    case 3: return info_of<DV3>();
+    case 4: return info_of<DV4>();
+    case 5: return info_of<DV5>();
+    case 6: return info_of<DV6>();
+    default: return info_of<DV0>();
+  }
+}
+
+inline SplitPlan plan_split(const VariantInfo& vi, int64_t m, int64_t nc, int64_t k, int64_t batch) {
+  const int64_t tiles = ceil_div(m, vi.BM) * ceil_div(nc, vi.BN) * batch;
+  int64_t splits = ceil_div((int64_t)vi.occ * 148, tiles);  // one full wave
+  const int64_t max_splits = ceil_div(k, 4 * vi.BK);        // at least 64 of k per split
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
   if (batch * splits > 65535) splits = 65535 / batch;
-  int64_t kchunk = ceil_div(ceil_div(k, splits), GB_K) * GB_K;
+  int64_t kchunk = ceil_div(ceil_div(k, splits), vi.BK) * vi.BK;
   splits = ceil_div(k, kchunk);
   if (splits < 1) splits = 1;
   return {splits, kchunk};
 }
 
-inline int64_t segsq_chunks(int64_t m, int64_t nc, int64_t nseg, int64_t batch) {
-  const int64_t tiles = ceil_div(m, GB_M) * ceil_div(nc, GB_N) * batch;
-  int64_t ch = ceil_div(G_CTAS_PER_SM * 148, tiles);
+inline int64_t segsq_chunks(const VariantInfo& vi, int64_t m, int64_t nc, int64_t nseg, int64_t batch) {
+  const int64_t tiles = ceil_div(m, vi.BM) * ceil_div(nc, vi.BN) * batch;
+  int64_t ch = ceil_div((int64_t)vi.occ * 148, tiles);
   if (ch > nseg) ch = nseg;
   if (ch < 1) ch = 1;
   if (batch * ch > 65535) ch = 65535 / batch;
   return ch;
 }
 
+template <class C>
+static void launch_gemm(bool v16, dim3 grid, cudaStream_t st, const double* A, int64_t lda, int64_t strideA,
+                        const double* B, int64_t ldb, int64_t strideB, int64_t m, int64_t nc, int64_t k,
+                        const SplitPlan& sp, double* out, int64_t ldo, int64_t strideO, double* part) {
+  if (v16)
+    gemm_f64_kernel<C, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k, sp.splits,
+                                                               sp.kchunk, out, ldo, strideO, part);
+  else
+    gemm_f64_kernel<C, false><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k, sp.splits,
+                                                                sp.kchunk, out, ldo, strideO, part);
+}
+
+template <class C>
+static void launch_segsq(dim3 grid, cudaStream_t st, const double* A, int64_t lda, int64_t strideA, const double* B,
+                         int64_t ldb, int64_t strideB, int64_t m, int64_t nc, const int64_t* seg, int64_t nseg,
+                         int64_t seg_stride, int64_t chunks, double* part) {
+  segsq_f64_kernel<C><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg,
+                                                          seg_stride, chunks, part);
+}
+
 }  // namespace bmm
 
 using namespace bmm;
 
+extern "C" int bmm_gemm_f64_set_variant(int variant) {
+  BMM_REQUIRE(variant >= 0 && variant < kVariants, BMM_E_ARG, "bmm_gemm_f64_set_variant: unknown variant %d",
+              variant);
+  g_variant = variant;
+  return BMM_OK;
+}
+
 extern "C" int64_t bmm_gemm_f64_workspace(int64_t m, int64_t nc, int64_t k, int64_t batch) {
-  SplitPlan sp = plan_split(m, nc, k, batch);
+  SplitPlan sp = plan_split(variant_info(g_variant), m, nc, k, batch);
   return sp.splits > 1 ? sp.splits * batch * m * nc * 8 : 0;
 }
 
@@ -361,26 +438,24 @@ extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const
       }
     return BMM_OK;
   }
-  SplitPlan sp = plan_split(m, nc, k, batch);
+  const VariantInfo vi = variant_info(g_variant);
+  SplitPlan sp = plan_split(vi, m, nc, k, batch);
   const int64_t need = sp.splits > 1 ? sp.splits * batch * m * nc * 8 : 0;
   BMM_REQUIRE(ws_bytes >= need && (need == 0 || ws != nullptr), BMM_E_ARG,
               "bmm_gemm_f64: workspace too small (%lld < %lld)", (long long)ws_bytes, (long long)need);
-  BMM_REQUIRE(ceil_div(m, GB_M) <= 65535, BMM_E_UNSUPPORTED, "bmm_gemm_f64: m too large");
+  BMM_REQUIRE(ceil_div(m, vi.BM) <= 65535, BMM_E_UNSUPPORTED, "bmm_gemm_f64: m too large");
   const bool v16 = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
                    lda % 2 == 0 && ldb % 2 == 0 && strideA % 2 == 0 && strideB % 2 == 0;
-  dim3 grid((unsigned)ceil_div(nc, GB_N), (unsigned)ceil_div(m, GB_M), (unsigned)(batch * sp.splits));
-  if (v16) {
-    static bool attr_t = false;
-    if (!attr_t) { cudaFuncSetAttribute(gemm_f64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES); attr_t = true; }
-    gemm_f64_kernel<true><<<grid, G_THREADS, G_SMEM_BYTES, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k,
-                                                                sp.splits, sp.kchunk, out, ldo, strideO,
-                                                                (double*)ws);
-  } else {
-    static bool attr_f = false;
-    if (!attr_f) { cudaFuncSetAttribute(gemm_f64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES); attr_f = true; }
-    gemm_f64_kernel<false><<<grid, G_THREADS, G_SMEM_BYTES, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k,
-                                                                 sp.splits, sp.kchunk, out, ldo, strideO,
-                                                                 (double*)ws);
+  dim3 grid((unsigned)ceil_div(nc, vi.BN), (unsigned)ceil_div(m, vi.BM), (unsigned)(batch * sp.splits));
+  double* part = (double*)ws;
+  switch (g_variant) {
+    case 1: launch_gemm<DV1>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
+    case 2: launch_gemm<DV2>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
+    case 3: launch_gemm<DV3>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
+    case 4: launch_gemm<DV4>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
+    case 5: launch_gemm<DV5>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
+    case 6: launch_gemm<DV6>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
+    default: launch_gemm<DV0>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part);
   }
   BMM_CHECK_LAUNCH("gemm_f64_kernel");
   if (sp.splits > 1) {
@@ -392,7 +467,8 @@ extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const
 }
 
 extern "C" int64_t bmm_segsq_f64_workspace(int64_t m, int64_t nc, int64_t nseg, int64_t batch) {
-  return ceil_div(m, GB_M) * ceil_div(nc, GB_N) * nseg * batch * 8;
+  const VariantInfo vi = variant_info(g_variant);
+  return ceil_div(m, vi.BM) * ceil_div(nc, vi.BN) * nseg * batch * 8;
 }
 
 extern "C" int bmm_segsq_f64(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
@@ -400,17 +476,24 @@ extern "C" int bmm_segsq_f64(const double* A, int64_t lda, int64_t strideA, cons
                              int64_t seg_stride, int64_t batch, double* gsq, void* ws, int64_t ws_bytes,
                              void* stream) {
   BMM_REQUIRE(m >= 1 && nc >= 1 && nseg >= 1 && batch >= 1, BMM_E_ARG, "bmm_segsq_f64: bad shape");
-  const int64_t tiles = ceil_div(m, GB_M) * ceil_div(nc, GB_N);
+  const VariantInfo vi = variant_info(g_variant);
+  const int64_t tiles = ceil_div(m, vi.BM) * ceil_div(nc, vi.BN);
   const int64_t need = tiles * nseg * batch * 8;
   BMM_REQUIRE(ws_bytes >= need && ws != nullptr, BMM_E_ARG, "bmm_segsq_f64: workspace too small");
-  BMM_REQUIRE(ceil_div(m, GB_M) <= 65535, BMM_E_UNSUPPORTED, "bmm_segsq_f64: m too large");
+  BMM_REQUIRE(ceil_div(m, vi.BM) <= 65535, BMM_E_UNSUPPORTED, "bmm_segsq_f64: m too large");
   cudaStream_t st = as_stream(stream);
-  const int64_t chunks = segsq_chunks(m, nc, nseg, batch);
-  dim3 grid((unsigned)ceil_div(nc, GB_N), (unsigned)ceil_div(m, GB_M), (unsigned)(batch * chunks));
-  static bool attr_s = false;
-  if (!attr_s) { cudaFuncSetAttribute(segsq_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM_BYTES); attr_s = true; }
-  segsq_f64_kernel<<<grid, G_THREADS, G_SMEM_BYTES, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg,
-                                                          seg_stride, chunks, (double*)ws);
+  const int64_t chunks = segsq_chunks(vi, m, nc, nseg, batch);
+  dim3 grid((unsigned)ceil_div(nc, vi.BN), (unsigned)ceil_div(m, vi.BM), (unsigned)(batch * chunks));
+  double* part = (double*)ws;
+  switch (g_variant) {
+    case 1: launch_segsq<DV1>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
+    case 2: launch_segsq<DV2>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
+    case 3: launch_segsq<DV3>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
+    case 4: launch_segsq<DV4>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
+    case 5: launch_segsq<DV5>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
+    case 6: launch_segsq<DV6>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
+    default: launch_segsq<DV0>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part);
+  }
   BMM_CHECK_LAUNCH("segsq_f64_kernel");
   segsq_reduce_kernel<<<grid_for(nseg * batch, 128), 128, 0, st>>>((const double*)ws, tiles, nseg * batch, gsq);
   BMM_CHECK_LAUNCH("segsq_reduce_kernel");

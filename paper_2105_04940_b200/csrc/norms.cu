@@ -149,7 +149,7 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
     }
     if (c_tail < n) {
       if (narrow) {
-        colsq_scalar_kernel<T, 64><<<grid_for((n - c_tail) * batch, 64, 32, 64), 64, 0, st>>>(
+        colsq_scalar_kernel<T, 32><<<grid_for((n - c_tail) * batch, 64, 32, 64), 64, 0, st>>>(
             M, m, n, c_tail, ldm, strideM, batch, accumulate, colsq);
       } else {
         colsq_scalar_kernel<T, 16><<<grid_for((n - c_tail) * batch, 256, 8, 64), 256, 0, st>>>(
