@@ -191,9 +191,10 @@ int bmm_gather_blocks(int dtype,
  * (deterministic).  Used for C @ D (estimators.py:175,253) and the exact
  * product M @ N (matrix.py:98-104).  ws: bmm_gemm_f64_workspace bytes.    */
 int64_t bmm_gemm_f64_workspace(int64_t m, int64_t nc, int64_t k, int64_t batch);
-/* Tile configuration of the DMMA kernels (0..6; tools/tune_dmma.py).  Affects
- * bmm_gemm_f64 and bmm_segsq_f64 and their workspace sizes; not thread-safe. */
-int bmm_gemm_f64_set_variant(int variant);
+/* Tile configurations of the DMMA kernels (0..6; tools/tune_dmma.py) for
+ * bmm_gemm_f64 and bmm_segsq_f64 (defaults 2 and 0).  Changes their workspace
+ * sizes; process-global, not thread-safe.                                  */
+int bmm_gemm_f64_set_variant(int gemm_variant, int segsq_variant);
 int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA,
                  const double* B, int64_t ldb, int64_t strideB,
                  int64_t m, int64_t nc, int64_t k, int64_t batch,

@@ -332,7 +332,8 @@ using DV4 = DCfg<128, 128, 32, 64, 3>;
 using DV5 = DCfg<64, 64, 32, 32, 4>;
 using DV6 = DCfg<128, 64, 32, 32, 3>;
 constexpr int kVariants = 7;
-static int g_variant = 0;
+static int g_variant = 2;      // C.D / exact-product tiles: 128x64, 4 warps of 64x32 (tools/tune_dmma.py)
+static int g_seg_variant = 0;  // segmented square sums: 64x64, 4 warps of 32x32
 
 struct VariantInfo {
   int BM, BN, BK, threads, smem, occ;
@@ -368,7 +369,7 @@ static VariantInfo variant_info(int v) {
 
 inline SplitPlan plan_split(const VariantInfo& vi, int64_t m, int64_t nc, int64_t k, int64_t batch) {
   const int64_t tiles = ceil_div(m, vi.BM) * ceil_div(nc, vi.BN) * batch;
-  int64_t splits = ceil_div((int64_t)vi.occ * 148, tiles);  // one full wave
+  int64_t splits = ((int64_t)vi.occ * 148) / tiles;  // fill one wave without spilling into a second
   const int64_t max_splits = ceil_div(k, 4 * vi.BK);        // at least 64 of k per split
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
@@ -381,7 +382,7 @@ inline SplitPlan plan_split(const VariantInfo& vi, int64_t m, int64_t nc, int64_
 
 inline int64_t segsq_chunks(const VariantInfo& vi, int64_t m, int64_t nc, int64_t nseg, int64_t batch) {
   const int64_t tiles = ceil_div(m, vi.BM) * ceil_div(nc, vi.BN) * batch;
-  int64_t ch = ceil_div((int64_t)vi.occ * 148, tiles);
+  int64_t ch = ((int64_t)vi.occ * 148) / tiles;
   if (ch > nseg) ch = nseg;
   if (ch < 1) ch = 1;
   if (batch * ch > 65535) ch = 65535 / batch;
@@ -412,10 +413,11 @@ static void launch_segsq(dim3 grid, cudaStream_t st, const double* A, int64_t ld
 
 using namespace bmm;
 
-extern "C" int bmm_gemm_f64_set_variant(int variant) {
-  BMM_REQUIRE(variant >= 0 && variant < kVariants, BMM_E_ARG, "bmm_gemm_f64_set_variant: unknown variant %d",
-              variant);
-  g_variant = variant;
+extern "C" int bmm_gemm_f64_set_variant(int gemm_variant, int segsq_variant) {
+  BMM_REQUIRE(gemm_variant >= 0 && gemm_variant < kVariants && segsq_variant >= 0 && segsq_variant < kVariants,
+              BMM_E_ARG, "bmm_gemm_f64_set_variant: unknown variant %d/%d", gemm_variant, segsq_variant);
+  g_variant = gemm_variant;
+  g_seg_variant = segsq_variant;
   return BMM_OK;
 }
 
@@ -467,7 +469,7 @@ extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const
 }
 
 extern "C" int64_t bmm_segsq_f64_workspace(int64_t m, int64_t nc, int64_t nseg, int64_t batch) {
-  const VariantInfo vi = variant_info(g_variant);
+  const VariantInfo vi = variant_info(g_seg_variant);
   return ceil_div(m, vi.BM) * ceil_div(nc, vi.BN) * nseg * batch * 8;
 }
 
@@ -476,7 +478,7 @@ extern "C" int bmm_segsq_f64(const double* A, int64_t lda, int64_t strideA, cons
                              int64_t seg_stride, int64_t batch, double* gsq, void* ws, int64_t ws_bytes,
                              void* stream) {
   BMM_REQUIRE(m >= 1 && nc >= 1 && nseg >= 1 && batch >= 1, BMM_E_ARG, "bmm_segsq_f64: bad shape");
-  const VariantInfo vi = variant_info(g_variant);
+  const VariantInfo vi = variant_info(g_seg_variant);
   const int64_t tiles = ceil_div(m, vi.BM) * ceil_div(nc, vi.BN);
   const int64_t need = tiles * nseg * batch * 8;
   BMM_REQUIRE(ws_bytes >= need && ws != nullptr, BMM_E_ARG, "bmm_segsq_f64: workspace too small");
@@ -485,7 +487,7 @@ extern "C" int bmm_segsq_f64(const double* A, int64_t lda, int64_t strideA, cons
   const int64_t chunks = segsq_chunks(vi, m, nc, nseg, batch);
   dim3 grid((unsigned)ceil_div(nc, vi.BN), (unsigned)ceil_div(m, vi.BM), (unsigned)(batch * chunks));
   double* part = (double*)ws;
-  switch (g_variant) {
+  switch (g_seg_variant) {
     case 1: launch_segsq<DV1>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
     case 2: launch_segsq<DV2>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
     case 3: launch_segsq<DV3>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;

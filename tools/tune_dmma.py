@@ -21,7 +21,7 @@ for (m, k, n) in shapes:
     B = torch.randn(k, n, dtype=torch.float64, device="cuda")
     ref = None
     for v in range(7):
-        lib.bmm_gemm_f64_set_variant(v)
+        lib.bmm_gemm_f64_set_variant(v, 0)
         out = torch.empty(m, n, dtype=torch.float64, device="cuda")
         f = lambda: lib.bmm_gemm_f64(A.data_ptr(), k, 0, B.data_ptr(), n, 0, m, n, k, 1, out.data_ptr(), n, 0,
                                      ws.data_ptr(), ws.numel(), st)
@@ -43,7 +43,7 @@ M, N, sizes = workloads.cfg2()
 Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
 off = torch.as_tensor(np.concatenate([[0], np.cumsum(sizes)]), device="cuda")
 for v in range(7):
-    lib.bmm_gemm_f64_set_variant(v)
+    lib.bmm_gemm_f64_set_variant(2, v)
     g = torch.empty(len(sizes), dtype=torch.float64, device="cuda")
     f = lambda: lib.bmm_segsq_f64(Md.data_ptr(), 20000, 0, Nd.data_ptr(), 500, 0, 500, 500, off.data_ptr(), len(sizes),
                                   0, 1, g.data_ptr(), ws.data_ptr(), ws.numel(), st)
