@@ -272,6 +272,7 @@ def run_ours(args):
     gemm_ms = kt["gemm_ms"]
     gemm_achieved = sum(gemm_flops) / (sum(gemm_ms) * 1e-3) / 1e12
     norms_achieved = norm_bytes / (kt["norms_ms"] * 1e-3) / 1e9
+    large = norms_large(torch)
 
     # errors of the W=16000 ONC product vs the exact product (verification, untimed)
     from paper_2105_04940_b200.analysis import sq_diff
@@ -297,7 +298,9 @@ def run_ours(args):
                      "traffic": None},
         "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norms_achieved,
                            "peak": hbm_peak, "unit": "GB/s", "frac": norms_achieved / hbm_peak,
-                           "algorithmic_bytes": norm_bytes},
+                           "algorithmic_bytes": norm_bytes,
+                           "note": "160 MB per pass: latency-bound size (SURVEY §7 K1); see roofline_norms_large"},
+        "roofline_norms_large": dict(large, peak=hbm_peak, frac=large["achieved"] / hbm_peak),
         "kernel_ms": {k: v for k, v in kt.items() if k != "gemm_ms"} | {"gemm_ms": gemm_ms},
         "rel_err_baseline_metric": float(np.sqrt(err_sq) / (fro_m * fro_n)),
         "rel_err_reference_metric": float(np.sqrt(err_sq / ref_sq)),
@@ -347,6 +350,34 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
             reps.append(e0.elapsed_time(e1))
         out["gemm_ms"].append(float(np.median(reps)))
     return out
+
+
+def norms_large(torch, problems=1024):
+    """K1 on a bandwidth-scale input: `problems` config-5 problems (float32,
+    256x4096 and 4096x256 each; 8.6 GB at 1024), median of 3 timed launches."""
+    from paper_2105_04940_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(workloads.ROOT)
+    m, n, p = 256, 4096, 256
+    M = torch.randn((problems, m, n), generator=g, device="cuda", dtype=torch.float32)
+    N = torch.randn((problems, n, p), generator=g, device="cuda", dtype=torch.float32)
+    cs = torch.empty(problems * n, dtype=torch.float64, device="cuda")
+    rs = torch.empty(problems * n, dtype=torch.float64, device="cuda")
+    lib, st = _lib.load(), _lib.stream_ptr()
+    reps = []
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.bmm_norms(1, M.data_ptr(), m, n, n, m * n, N.data_ptr(), p, p, n * p, problems, 0, cs.data_ptr(),
+                      rs.data_ptr(), st)
+        e1.record()
+        torch.cuda.synchronize()
+        reps.append(e0.elapsed_time(e1))
+    ms = float(np.median(reps[1:]))
+    nbytes = 4 * problems * (m * n + n * p)
+    del M, N
+    torch.cuda.empty_cache()
+    return {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "input": f"{problems} config-5 problems (float32)",
+            "algorithmic_bytes": nbytes, "ms": ms, "achieved": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s"}
 
 
 def cpu_baseline(M, N, sizes, runs, cfg, args):

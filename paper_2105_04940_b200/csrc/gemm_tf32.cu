@@ -263,54 +263,82 @@ __device__ __forceinline__ void split_tf32(double x, float& hi, float& lo) {
 template <typename T>
 __device__ __forceinline__ double ld_d(const T* p) { return (double)__ldg(p); }
 
-// A_hi/A_lo[b*m + h, t] = split(M[b][h, column[t]] * scale[t])
+// A_hi/A_lo[b*m + h, t] = split(M[b][h, column[t]] * scale[t]).  A CTA owns
+// 256 sketch columns of one problem and walks A_ROWS rows: the column index
+// and scale are loaded once per thread, every row's stores are coalesced.
+constexpr int A_ROWS = 32;
+
 template <typename T>
 __global__ void __launch_bounds__(256) gather_a_split_kernel(const T* __restrict__ M, int64_t ldm, int64_t strideM,
                                                              int64_t m, const int64_t* __restrict__ column,
                                                              const double* __restrict__ scale, int64_t W,
-                                                             int64_t w_stride, int64_t batch, float* __restrict__ ahi,
+                                                             int64_t w_stride, float* __restrict__ ahi,
                                                              float* __restrict__ alo) {
-  const int64_t per_b = m * W;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < per_b * batch;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = g / per_b, r = g - b * per_b;
-    const int64_t h = r / W, t = r - h * W;
-    const double x = __dmul_rn(ld_d(M + b * strideM + h * ldm + column[b * w_stride + t]), scale[b * w_stride + t]);
+  const int64_t b = blockIdx.z;
+  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t h0 = (int64_t)blockIdx.y * A_ROWS;
+  if (t >= W) return;
+  const int64_t col = column[b * w_stride + t];
+  const double sc = scale[b * w_stride + t];
+  const T* src = M + b * strideM + col;
+  const int64_t h1 = min(m, h0 + A_ROWS);
+  float* oh = ahi + (b * m) * W + t;
+  float* ol = alo + (b * m) * W + t;
+#pragma unroll 8
+  for (int64_t h = h0; h < h1; ++h) {
+    const double x = __dmul_rn(ld_d(src + h * ldm), sc);
     float hi, lo;
     split_tf32(x, hi, lo);
-    ahi[g] = hi;
-    alo[g] = lo;
+    oh[h * W] = hi;
+    ol[h * W] = lo;
   }
 }
 
-// B_hi/B_lo[b*p + f, t] = split(N[b][column[t], f] * scale[t]) through a 32x32 smem transpose.
+// B_hi/B_lo[b*p + f, t] = split(N[b][column[t], f] * scale[t]): a CTA stages a
+// 32 (t) x 128 (f) tile through shared memory -- 512-byte coalesced row reads
+// of N, 128-byte coalesced writes of the transposed operand.
 template <typename T>
 __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restrict__ N, int64_t ldn, int64_t strideN,
                                                               int64_t p, const int64_t* __restrict__ column,
                                                               const double* __restrict__ scale, int64_t W,
                                                               int64_t w_stride, float* __restrict__ bhi,
                                                               float* __restrict__ blo) {
-  __shared__ float sh[32][33], sl[32][33];
+  __shared__ float sh[32][129], sl[32][129];
+  __shared__ int64_t scol[32];
+  __shared__ double sscale[32];
   const int64_t b = blockIdx.z;
-  const int64_t t0 = (int64_t)blockIdx.x * 32, f0 = (int64_t)blockIdx.y * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  for (int i = ty; i < 32; i += 8) {
-    const int64_t t = t0 + i, f = f0 + tx;
-    float hi = 0.f, lo = 0.f;
-    if (t < W && f < p) {
-      const double x = __dmul_rn(ld_d(N + b * strideN + column[b * w_stride + t] * ldn + f), scale[b * w_stride + t]);
-      split_tf32(x, hi, lo);
-    }
-    sh[i][tx] = hi;
-    sl[i][tx] = lo;
+  const int64_t t0 = (int64_t)blockIdx.x * 32, f0 = (int64_t)blockIdx.y * 128;
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    const int64_t t = t0 + tid;
+    scol[tid] = t < W ? column[b * w_stride + t] : 0;
+    sscale[tid] = t < W ? scale[b * w_stride + t] : 0.0;
   }
   __syncthreads();
-  for (int i = ty; i < 32; i += 8) {
-    const int64_t f = f0 + i, t = t0 + tx;
-    if (f < p && t < W) {
-      const int64_t o = (b * p + f) * W + t;
-      bhi[o] = sh[tx][i];
-      blo[o] = sl[tx][i];
+  const int fx = tid & 127, ty = tid >> 7;  // 128 x 2
+#pragma unroll 4
+  for (int i = ty; i < 32; i += 2) {
+    const int64_t t = t0 + i, f = f0 + fx;
+    float hi = 0.f, lo = 0.f;
+    if (t < W && f < p) {
+      const double x = __dmul_rn(ld_d(N + b * strideN + scol[i] * ldn + f), sscale[i]);
+      split_tf32(x, hi, lo);
+    }
+    sh[i][fx] = hi;
+    sl[i][fx] = lo;
+  }
+  __syncthreads();
+  const int tx = tid & 31, fy = tid >> 5;  // 32 x 8
+  const int64_t t = t0 + tx;
+  if (t < W) {
+#pragma unroll 4
+    for (int i = fy; i < 128; i += 8) {
+      const int64_t f = f0 + i;
+      if (f < p) {
+        const int64_t o = (b * p + f) * W + t;
+        bhi[o] = sh[tx][i];
+        blo[o] = sl[tx][i];
+      }
     }
   }
 }
@@ -352,18 +380,19 @@ extern "C" int bmm_gather_tf32x3(int dtype, const void* M, int64_t ldm, int64_t 
                                  int64_t W, int64_t w_stride, int64_t batch, float* a_hi, float* a_lo, float* b_hi,
                                  float* b_lo, void* stream) {
   BMM_REQUIRE(m >= 1 && p >= 1 && W >= 1 && batch >= 1, BMM_E_ARG, "bmm_gather_tf32x3: bad shape");
-  BMM_REQUIRE(batch <= 65535 && ceil_div(p, 32) <= 65535, BMM_E_UNSUPPORTED, "bmm_gather_tf32x3: grid too large");
+  BMM_REQUIRE(batch <= 65535 && ceil_div(m, A_ROWS) <= 65535, BMM_E_UNSUPPORTED, "bmm_gather_tf32x3: grid too large");
   cudaStream_t st = as_stream(stream);
-  dim3 tgrid((unsigned)ceil_div(W, 32), (unsigned)ceil_div(p, 32), (unsigned)batch);
+  dim3 agrid((unsigned)ceil_div(W, 256), (unsigned)ceil_div(m, A_ROWS), (unsigned)batch);
+  dim3 tgrid((unsigned)ceil_div(W, 32), (unsigned)ceil_div(p, 128), (unsigned)batch);
   if (dtype == BMM_F32) {
-    gather_a_split_kernel<float><<<grid_for(m * W * batch, 256), 256, 0, st>>>(
-        (const float*)M, ldm, strideM, m, column, scale, W, w_stride, batch, a_hi, a_lo);
+    gather_a_split_kernel<float><<<agrid, 256, 0, st>>>((const float*)M, ldm, strideM, m, column, scale, W, w_stride,
+                                                        a_hi, a_lo);
     BMM_CHECK_LAUNCH("gather_a_split_kernel");
     gather_bt_split_kernel<float><<<tgrid, 256, 0, st>>>((const float*)N, ldn, strideN, p, column, scale, W,
                                                          w_stride, b_hi, b_lo);
   } else if (dtype == BMM_F64) {
-    gather_a_split_kernel<double><<<grid_for(m * W * batch, 256), 256, 0, st>>>(
-        (const double*)M, ldm, strideM, m, column, scale, W, w_stride, batch, a_hi, a_lo);
+    gather_a_split_kernel<double><<<agrid, 256, 0, st>>>((const double*)M, ldm, strideM, m, column, scale, W,
+                                                         w_stride, a_hi, a_lo);
     BMM_CHECK_LAUNCH("gather_a_split_kernel");
     gather_bt_split_kernel<double><<<tgrid, 256, 0, st>>>((const double*)N, ldn, strideN, p, column, scale, W,
                                                           w_stride, b_hi, b_lo);
