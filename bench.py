@@ -402,16 +402,86 @@ def device_data(torch, name):
             M[sl].normal_(generator=g).mul_(torch.randn((512, 1, n), generator=g, device="cuda").exp_())
             N[sl].normal_(generator=g).mul_(torch.randn((512, n, 1), generator=g, device="cuda").exp_())
         return M, N, (n // K,) * K, B
+    M, N = cfg4_shard(torch, (0, 16384), (0, 16384))
+    return M, N, (262144 // 4096,) * 4096, 1
+
+
+def cfg4_shard(torch, rows, cols):
+    """Rows `rows` of config 4's M and columns `cols` of its N, float32 on the
+    GPU.  Generation is chunk-seeded (1024-row chunks of M, 16384-row chunks of
+    N), so every rank of a sharded run regenerates exactly its slice of the
+    same global instance; per-block scales U[0.1, 10] for M^k and N_k."""
     m, n, p, K = 16384, 262144, 16384, 4096
+    g = torch.Generator(device="cuda").manual_seed(workloads.ROOT + 4)
     cs = (torch.rand(K, generator=g, device="cuda") * 9.9 + 0.1).repeat_interleave(n // K)
     rs = (torch.rand(K, generator=g, device="cuda") * 9.9 + 0.1).repeat_interleave(n // K)
-    M = torch.empty((m, n), dtype=torch.float32, device="cuda")
-    N = torch.empty((n, p), dtype=torch.float32, device="cuda")
-    for r0 in range(0, m, 1024):
-        M[r0:r0 + 1024].normal_(generator=g).mul_(cs)
-    for r0 in range(0, n, 16384):
-        N[r0:r0 + 16384].normal_(generator=g).mul_(rs[r0:r0 + 16384, None])
-    return M, N, (n // K,) * K, 1
+    r0, r1 = rows
+    c0, c1 = cols
+    M = torch.empty((r1 - r0, n), dtype=torch.float32, device="cuda")
+    N = torch.empty((n, c1 - c0), dtype=torch.float32, device="cuda")
+    for ch in range(r0 // 1024, (r1 + 1023) // 1024):
+        gc = torch.Generator(device="cuda").manual_seed(workloads.ROOT * 1000 + 40000 + ch)
+        blk = torch.empty((1024, n), dtype=torch.float32, device="cuda").normal_(generator=gc).mul_(cs)
+        a, b = max(r0, ch * 1024), min(r1, ch * 1024 + 1024)
+        M[a - r0:b - r0] = blk[a - ch * 1024:b - ch * 1024]
+        del blk
+    for ch in range(n // 16384):
+        gc = torch.Generator(device="cuda").manual_seed(workloads.ROOT * 1000 + 41000 + ch)
+        blk = torch.empty((16384, p), dtype=torch.float32, device="cuda").normal_(generator=gc)
+        N[ch * 16384:(ch + 1) * 16384] = blk[:, c0:c1] * rs[ch * 16384:(ch + 1) * 16384, None]
+        del blk
+    return M, N
+
+
+def run_cfg4_sharded(args):
+    """Config 4 with M's rows and N's columns sharded over the torchrun group
+    (SURVEY §8(e)); the only exchanges are the norm partials (all-gather +
+    ordered sum).  value = ms per approximate product of the whole problem
+    (strong scaling, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2105_04940_b200.distributed import ShardLayout, ShardedApproxProduct
+    from paper_2105_04940_b200.pipeline import seeds_from_keys
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    m, n, p, K, W = 16384, 262144, 16384, 4096, 32768
+    L = ShardLayout(world, rank, m, n, p)
+    M, N = cfg4_shard(torch, L.rows, L.cols)
+    sh = ShardedApproxProduct(L, (n // K,) * K, W, "ONC", dtype=torch.float32)
+    seeds = seeds_from_keys("ONC", workloads.ROOT, (4, 1), [0], K)
+    words, first = seeds.main.words[0], int(seeds.main.first[0])
+    sh.run(M, N, words, first)
+    sh.check()
+    for _ in range(args.warmup):
+        sh.run(M, N, words, first)
+    times = []
+    with ClockSampler(local) as clocks:
+        dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            sh.run(M, N, words, first)
+            e1.record()
+            times.append((e0, e1))
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in times]))], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": float(ms.item()), "unit": "ms/step", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": float(ms.item()), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (3xTF32 tensor, f64 plan)", "data": "synthetic (chunk-seeded on device)",
+            "config": {"workload": "cfg4-sharded", "grid": list(L.grid), "m": m, "n": n, "p": p, "K": K, "W": W,
+                       "parallelism": f"M rows x N cols over {world} GPUs; colsq/rowsq exchange only"},
+            "clocks": clocks.summary()}), flush=True)
+    dist.destroy_process_group()
+    return 0
 
 
 def run_device(args):
@@ -537,6 +607,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "cfg4" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_cfg4_sharded(args)
     if args.workload in ("cfg4", "cfg5"):
         return run_device(args)
     return run_ours(args)
