@@ -223,23 +223,26 @@ int bmm_sqdiff(int dtype, const void* X, int64_t ldx, int64_t strideX,
                void* ws, int64_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K4/K6 float32 path
- * Split gather for 3xTF32: x = M[h, column[t]] * scale[t] (formed in float64,
- * as the reference does on upcast inputs), hi = tf32_rna(x), lo = x - hi:
- *   a_hi/a_lo [(b*m + h) * W + t]   (A = C, K-major)
- *   b_hi/b_lo [(b*p + f) * W + t]   (B = D^T, K-major)                       */
-int bmm_gather_tf32x3(int dtype, const void* M, int64_t ldm, int64_t strideM,
-                      const void* N, int64_t ldn, int64_t strideN,
-                      int64_t m, int64_t p, const int64_t* column, const double* scale,
-                      int64_t W, int64_t w_stride, int64_t batch,
-                      float* a_hi, float* a_lo, float* b_hi, float* b_lo, void* stream);
+ * Split gather: x = M[h, column[t]] * scale[t] (formed in float64, as the
+ * reference does on upcast inputs), h = tf32_rna(x), l = x - h:
+ *   a_hi[(b*m + h) * W + t]            float32 holding tf32 h   (A = C, K-major)
+ *   a_x [(b*m + h) * 2W + 16*(t/8) ..] bf16 pairs [h(8) | l(8)] per 8-column group
+ *   b_hi, b_x                          the same for B = D^T, pairs [l(8) | h(8)]
+ * W % 8 == 0.  a_x / b_x occupy the same bytes as a float32 W-vector per row. */
+int bmm_gather_f32split(int dtype, const void* M, int64_t ldm, int64_t strideM,
+                        const void* N, int64_t ldn, int64_t strideN,
+                        int64_t m, int64_t p, const int64_t* column, const double* scale,
+                        int64_t W, int64_t w_stride, int64_t batch,
+                        float* a_hi, void* a_x, float* b_hi, void* b_x, void* stream);
 
-/* out[b] (m x nc, float32) = A[b] (m x k) @ B[b]^T with A = a_hi + a_lo,
- * B = b_hi + b_lo as written by bmm_gather_tf32x3: tcgen05.mma kind::tf32,
- * hi.hi + hi.lo + lo.hi accumulated in TMEM (float32), TMA SWIZZLE_128B
- * operand tiles (estimators.py:175 for the float32 configs).  k % 4 == 0.   */
-int bmm_gemm_tf32x3(const float* a_hi, const float* a_lo, const float* b_hi, const float* b_lo,
-                    int64_t m, int64_t nc, int64_t k, int64_t batch,
-                    float* out, int64_t ldo, int64_t strideO, void* stream);
+/* out[b] (m x nc, float32) ~= C[b] (m x k) @ D[b] (k x nc) from the split
+ * operands: tcgen05.mma kind::tf32 for h_C.h_D plus one kind::f16 (bf16) MMA
+ * for both cross terms h_C.l_D + l_C.h_D, float32 TMEM accumulation promoted
+ * to round-to-nearest registers every 128 K-elements, TMA SWIZZLE_128B
+ * operand tiles (estimators.py:175 for the float32 configs).  k % 8 == 0.   */
+int bmm_gemm_f32split(const float* a_hi, const void* a_x, const float* b_hi, const void* b_x,
+                      int64_t m, int64_t nc, int64_t k, int64_t batch,
+                      float* out, int64_t ldo, int64_t strideO, void* stream);
 
 /* sum of a float64 vector segment in numpy pairwise order: out[b] = 0 + pw(x[b, 0:len])
  * (used for ||M||_F^2 = pw(colsq), ||N||_F^2 = pw(rowsq)).                */

@@ -62,9 +62,9 @@ SIGNATURES = {
     "bmm_sqdiff_workspace": (_I64, [_I64, _I64, _I64]),
     "bmm_sqdiff": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P]),
     "bmm_pairwise_sum": (_I, [_P, _I64, _I64, _I64, _P, _P]),
-    "bmm_gather_tf32x3": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _I64,
+    "bmm_gather_f32split": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _I64,
                                _P, _P, _P, _P, _P]),
-    "bmm_gemm_tf32x3": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _I64, _P]),
+    "bmm_gemm_f32split": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _I64, _P]),
 }
 
 _lib = None

@@ -2,21 +2,27 @@
 //
 // C (m x W) @ D (W x p) for float32 inputs (configs 4 and 5), where the
 // reference computes in float64 (estimators.py:143-144,175).  1xTF32 misses
-// the 1e-5 tolerance at W = 32768, so each operand is split once,
-// x = hi + lo with hi = tf32_rna(x) and lo = x - hi (float32), and the tile
-// accumulates hi.hi + hi.lo + lo.hi ("3xTF32") into one float32 TMEM
-// accumulator.
+// the 1e-5 tolerance at W = 32768, so every sketch value is split once,
+// x = h + l with h = tf32_rna(x) and l = x - h, and
+//     x.y ~= h_x.h_y            (kind::tf32, exact products)
+//          + [h_x | l_x].[l_y | h_y]   (kind::f16 on bf16 pairs: both cross
+//                                       terms in ONE K=16 MMA)
+// accumulated into one float32 TMEM accumulator: two tensor instructions per
+// 8 K-elements instead of three for 3xTF32, error ~2^-19 per product.
 //
-//   * bmm_gather_tf32x3: the K4 gather writes the split operands K-major:
-//       A_hi/A_lo[b*m + h, t] = split(M[h, column[t]] * scale[t])
-//       B_hi/B_lo[b*p + f, t] = split(N[column[t], f] * scale[t])   (D^T)
-//   * bmm_gemm_tf32x3: one CTA per 128x128 output tile; warp 0 drives TMA
-//     (SWIZZLE_128B, 32 x 128 float boxes) into a 3-stage mbarrier ring, one
-//     thread of warp 1 issues tcgen05.mma.kind::tf32 (M=128, N=128, K=8) into
-//     a 128-column TMEM accumulator and frees stages with tcgen05.commit,
-//     and all four warps drain TMEM with tcgen05.ld.32x32b for the epilogue.
+//   * bmm_gather_f32split: the K4 gather writes the operands K-major:
+//       a_hi[b*m + h, t]   = h(M[h, column[t]] * scale[t])          (float32 / tf32)
+//       a_x [b*m + h, t']  = bf16 pairs [h_x(8) | l_x(8)] per 8-column group
+//       b_hi[b*p + f, t], b_x: the same for D^T with pairs [l_y(8) | h_y(8)]
+//   * bmm_gemm_f32split: one CTA per 128x128 output tile; warp 0 drives TMA
+//     (SWIZZLE_128B, 128-byte x 128-row boxes) into a 3-stage mbarrier ring,
+//     one thread of warp 1 issues tcgen05.mma (M=128, N=128) into two TMEM
+//     accumulators alternated every 128 K-elements, and four drain warps
+//     promote each finished chunk into round-to-nearest float32 registers.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 
@@ -24,7 +30,7 @@ namespace bmm {
 
 constexpr int T_BM = 128, T_BN = 128, T_BK = 32, T_STAGES = 3;
 constexpr int T_TILE_BYTES = T_BM * T_BK * 4;                // 16 KB: one operand tile
-constexpr int T_STAGE_BYTES = 4 * T_TILE_BYTES;              // A_hi, A_lo, B_hi, B_lo
+constexpr int T_STAGE_BYTES = 4 * T_TILE_BYTES;              // A_hi, A_x, B_hi, B_x
 constexpr int T_SMEM_BYTES = T_STAGES * T_STAGE_BYTES + 1024 + 256;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -83,6 +89,20 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t a, uint64_t b,
       "l"(a), "l"(b), "r"(kIdescTf32), "r"(accumulate));
 }
 
+// kind::f16 with BF16 A/B, F32 accumulate, K-major, M=128, N=128 (K = 16 per MMA).
+constexpr uint32_t kIdescBf16 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T_BN >> 3) << 17) |
+                                ((uint32_t)(T_BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(kIdescBf16), "r"(accumulate));
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
                : "memory");
@@ -117,9 +137,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 constexpr int T_CHUNK = 4;           // stages per accumulation chunk (128 K elements)
 constexpr int T_WARPS = 6;
 
-__global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_tf32x3_kernel(
-    const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
-    const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo, int64_t m, int64_t nc,
+__global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
+    const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_ax,
+    const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_bx, int64_t m, int64_t nc,
     int64_t k, float* __restrict__ out, int64_t ldo, int64_t strideO) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -147,9 +167,9 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_tf32x3_kernel(
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_alo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_ax)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_bhi)) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_blo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_bx)) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
@@ -171,9 +191,9 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_tf32x3_kernel(
         mbar_expect_tx(&full[s], T_STAGE_BYTES);
         const int kc = kt * T_BK;
         tma_load_2d(st + 0 * T_TILE_BYTES, &tm_ahi, &full[s], kc, a_row0);
-        tma_load_2d(st + 1 * T_TILE_BYTES, &tm_alo, &full[s], kc, a_row0);
+        tma_load_2d(st + 1 * T_TILE_BYTES, &tm_ax, &full[s], kc, a_row0);
         tma_load_2d(st + 2 * T_TILE_BYTES, &tm_bhi, &full[s], kc, b_row0);
-        tma_load_2d(st + 3 * T_TILE_BYTES, &tm_blo, &full[s], kc, b_row0);
+        tma_load_2d(st + 3 * T_TILE_BYTES, &tm_bx, &full[s], kc, b_row0);
       }
     }
   } else if (warp == 1) {
@@ -190,15 +210,15 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_tf32x3_kernel(
         const uint32_t acc = tmem + (uint32_t)(q * T_BN);
 #pragma unroll
         for (int kk = 0; kk < T_BK / 8; ++kk) {
-          const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the 128 B swizzle row
+          // 8 K-elements = 32 bytes of the 128-byte swizzle row: 8 tf32 values,
+          // or the 16 bf16 of one cross-term pair group
+          const uint32_t off = kk * 32;
           const uint64_t ahi = umma_desc_sw128(base + 0 * T_TILE_BYTES + off);
-          const uint64_t alo = umma_desc_sw128(base + 1 * T_TILE_BYTES + off);
+          const uint64_t ax = umma_desc_sw128(base + 1 * T_TILE_BYTES + off);
           const uint64_t bhi = umma_desc_sw128(base + 2 * T_TILE_BYTES + off);
-          const uint64_t blo = umma_desc_sw128(base + 3 * T_TILE_BYTES + off);
-          // small cross terms first, then the leading product
-          umma_tf32(acc, alo, bhi, !(first && kk == 0));
-          umma_tf32(acc, ahi, blo, 1);
-          umma_tf32(acc, ahi, bhi, 1);
+          const uint64_t bx = umma_desc_sw128(base + 3 * T_TILE_BYTES + off);
+          umma_bf16(acc, ax, bx, !(first && kk == 0));  // h_x.l_y + l_x.h_y
+          umma_tf32(acc, ahi, bhi, 1);                  // h_x.h_y
         }
         umma_commit(&empty[s]);  // stage s free once these MMAs have read it
         if ((kt % T_CHUNK) == T_CHUNK - 1 || kt == ktiles - 1) umma_commit(&acc_full[q]);
@@ -252,6 +272,9 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_tf32x3_kernel(
 
 // ---- split gather (K4 for the float32 path)
 
+// position of element t inside its row of bf16 pairs: group t/8 holds 16 bf16
+__device__ __forceinline__ int64_t pair_pos(int64_t t) { return 2 * (t & ~int64_t(7)) + (t & 7); }
+
 __device__ __forceinline__ void split_tf32(double x, float& hi, float& lo) {
   const float xf = (float)x;
   uint32_t h;
@@ -263,9 +286,9 @@ __device__ __forceinline__ void split_tf32(double x, float& hi, float& lo) {
 template <typename T>
 __device__ __forceinline__ double ld_d(const T* p) { return (double)__ldg(p); }
 
-// A_hi/A_lo[b*m + h, t] = split(M[b][h, column[t]] * scale[t]).  A CTA owns
-// 256 sketch columns of one problem and walks A_ROWS rows: the column index
-// and scale are loaded once per thread, every row's stores are coalesced.
+// a_hi / a_x for rows of C = M[:, column] * scale.  A CTA owns 256 sketch
+// columns of one problem and walks A_ROWS rows: the column index and scale
+// are loaded once per thread, and every row's stores are coalesced.
 constexpr int A_ROWS = 32;
 
 template <typename T>
@@ -273,7 +296,7 @@ __global__ void __launch_bounds__(256) gather_a_split_kernel(const T* __restrict
                                                              int64_t m, const int64_t* __restrict__ column,
                                                              const double* __restrict__ scale, int64_t W,
                                                              int64_t w_stride, float* __restrict__ ahi,
-                                                             float* __restrict__ alo) {
+                                                             __nv_bfloat16* __restrict__ ax) {
   const int64_t b = blockIdx.z;
   const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
   const int64_t h0 = (int64_t)blockIdx.y * A_ROWS;
@@ -283,26 +306,27 @@ __global__ void __launch_bounds__(256) gather_a_split_kernel(const T* __restrict
   const T* src = M + b * strideM + col;
   const int64_t h1 = min(m, h0 + A_ROWS);
   float* oh = ahi + (b * m) * W + t;
-  float* ol = alo + (b * m) * W + t;
+  __nv_bfloat16* ox = ax + (b * m) * 2 * W + pair_pos(t);
 #pragma unroll 8
   for (int64_t h = h0; h < h1; ++h) {
     const double x = __dmul_rn(ld_d(src + h * ldm), sc);
     float hi, lo;
     split_tf32(x, hi, lo);
     oh[h * W] = hi;
-    ol[h * W] = lo;
+    ox[h * 2 * W] = __float2bfloat16_rn(hi);      // [h_x | l_x]
+    ox[h * 2 * W + 8] = __float2bfloat16_rn(lo);
   }
 }
 
-// B_hi/B_lo[b*p + f, t] = split(N[b][column[t], f] * scale[t]): a CTA stages a
-// 32 (t) x 128 (f) tile through shared memory -- 512-byte coalesced row reads
-// of N, 128-byte coalesced writes of the transposed operand.
+// b_hi / b_x for rows of D^T (D = N[column, :] * scale[:, None]): a CTA stages
+// a 32 (t) x 128 (f) tile through shared memory -- 512-byte coalesced row
+// reads of N, coalesced writes of the transposed operand.
 template <typename T>
 __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restrict__ N, int64_t ldn, int64_t strideN,
                                                               int64_t p, const int64_t* __restrict__ column,
                                                               const double* __restrict__ scale, int64_t W,
                                                               int64_t w_stride, float* __restrict__ bhi,
-                                                              float* __restrict__ blo) {
+                                                              __nv_bfloat16* __restrict__ bx) {
   __shared__ float sh[32][129], sl[32][129];
   __shared__ int64_t scol[32];
   __shared__ double sscale[32];
@@ -331,13 +355,15 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
   const int tx = tid & 31, fy = tid >> 5;  // 32 x 8
   const int64_t t = t0 + tx;
   if (t < W) {
+    const int64_t pp = pair_pos(t);
 #pragma unroll 4
     for (int i = fy; i < 128; i += 8) {
       const int64_t f = f0 + i;
       if (f < p) {
-        const int64_t o = (b * p + f) * W + t;
-        bhi[o] = sh[tx][i];
-        blo[o] = sl[tx][i];
+        const int64_t row = b * p + f;
+        bhi[row * W + t] = sh[tx][i];
+        bx[row * 2 * W + pp] = __float2bfloat16_rn(sl[tx][i]);      // [l_y | h_y]
+        bx[row * 2 * W + pp + 8] = __float2bfloat16_rn(sh[tx][i]);
       }
     }
   }
@@ -375,42 +401,47 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
 
 using namespace bmm;
 
-extern "C" int bmm_gather_tf32x3(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N, int64_t ldn,
-                                 int64_t strideN, int64_t m, int64_t p, const int64_t* column, const double* scale,
-                                 int64_t W, int64_t w_stride, int64_t batch, float* a_hi, float* a_lo, float* b_hi,
-                                 float* b_lo, void* stream) {
-  BMM_REQUIRE(m >= 1 && p >= 1 && W >= 1 && batch >= 1, BMM_E_ARG, "bmm_gather_tf32x3: bad shape");
-  BMM_REQUIRE(batch <= 65535 && ceil_div(m, A_ROWS) <= 65535, BMM_E_UNSUPPORTED, "bmm_gather_tf32x3: grid too large");
+extern "C" int bmm_gather_f32split(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
+                                   int64_t ldn, int64_t strideN, int64_t m, int64_t p, const int64_t* column,
+                                   const double* scale, int64_t W, int64_t w_stride, int64_t batch, float* a_hi,
+                                   void* a_x, float* b_hi, void* b_x, void* stream) {
+  BMM_REQUIRE(m >= 1 && p >= 1 && W >= 1 && batch >= 1, BMM_E_ARG, "bmm_gather_f32split: bad shape");
+  BMM_REQUIRE(W % 8 == 0, BMM_E_UNSUPPORTED, "bmm_gather_f32split: W must be a multiple of 8");
+  __nv_bfloat16* ax = (__nv_bfloat16*)a_x;
+  __nv_bfloat16* bx = (__nv_bfloat16*)b_x;
+  BMM_REQUIRE(batch <= 65535 && ceil_div(m, A_ROWS) <= 65535, BMM_E_UNSUPPORTED, "bmm_gather_f32split: grid too large");
   cudaStream_t st = as_stream(stream);
   dim3 agrid((unsigned)ceil_div(W, 256), (unsigned)ceil_div(m, A_ROWS), (unsigned)batch);
   dim3 tgrid((unsigned)ceil_div(W, 32), (unsigned)ceil_div(p, 128), (unsigned)batch);
   if (dtype == BMM_F32) {
     gather_a_split_kernel<float><<<agrid, 256, 0, st>>>((const float*)M, ldm, strideM, m, column, scale, W, w_stride,
-                                                        a_hi, a_lo);
+                                                        a_hi, ax);
     BMM_CHECK_LAUNCH("gather_a_split_kernel");
     gather_bt_split_kernel<float><<<tgrid, 256, 0, st>>>((const float*)N, ldn, strideN, p, column, scale, W,
-                                                         w_stride, b_hi, b_lo);
+                                                         w_stride, b_hi, bx);
   } else if (dtype == BMM_F64) {
     gather_a_split_kernel<double><<<agrid, 256, 0, st>>>((const double*)M, ldm, strideM, m, column, scale, W,
-                                                         w_stride, a_hi, a_lo);
+                                                         w_stride, a_hi, ax);
     BMM_CHECK_LAUNCH("gather_a_split_kernel");
     gather_bt_split_kernel<double><<<tgrid, 256, 0, st>>>((const double*)N, ldn, strideN, p, column, scale, W,
-                                                          w_stride, b_hi, b_lo);
+                                                          w_stride, b_hi, bx);
   } else {
-    set_error("bmm_gather_tf32x3: unknown dtype %d", dtype);
+    set_error("bmm_gather_f32split: unknown dtype %d", dtype);
     return BMM_E_ARG;
   }
   BMM_CHECK_LAUNCH("gather_bt_split_kernel");
   return BMM_OK;
 }
 
-extern "C" int bmm_gemm_tf32x3(const float* a_hi, const float* a_lo, const float* b_hi, const float* b_lo,
-                               int64_t m, int64_t nc, int64_t k, int64_t batch, float* out, int64_t ldo,
-                               int64_t strideO, void* stream) {
-  BMM_REQUIRE(m >= 1 && nc >= 1 && k >= 1 && batch >= 1, BMM_E_ARG, "bmm_gemm_tf32x3: bad shape");
-  BMM_REQUIRE(k % 4 == 0, BMM_E_UNSUPPORTED, "bmm_gemm_tf32x3: k must be a multiple of 4 (16-byte TMA rows)");
+extern "C" int bmm_gemm_f32split(const float* a_hi, const void* a_x, const float* b_hi, const void* b_x,
+                                 int64_t m, int64_t nc, int64_t k, int64_t batch, float* out, int64_t ldo,
+                                 int64_t strideO, void* stream) {
+  BMM_REQUIRE(m >= 1 && nc >= 1 && k >= 1 && batch >= 1, BMM_E_ARG, "bmm_gemm_f32split: bad shape");
+  BMM_REQUIRE(k % 8 == 0, BMM_E_UNSUPPORTED, "bmm_gemm_f32split: k must be a multiple of 8");
+  const float* a_lo = (const float*)a_x;  // bf16 pairs: the same bytes per row as k floats
+  const float* b_lo = (const float*)b_x;
   BMM_REQUIRE(batch * m < (1LL << 31) && batch * nc < (1LL << 31) && batch <= 65535, BMM_E_UNSUPPORTED,
-              "bmm_gemm_tf32x3: problem too large for 32-bit TMA coordinates");
+              "bmm_gemm_f32split: problem too large for 32-bit TMA coordinates");
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   int rc;
   if ((rc = make_map(&ma_hi, a_hi, batch * m, k)) != BMM_OK) return rc;
@@ -419,12 +450,12 @@ extern "C" int bmm_gemm_tf32x3(const float* a_hi, const float* a_lo, const float
   if ((rc = make_map(&mb_lo, b_lo, batch * nc, k)) != BMM_OK) return rc;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_f32split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM_BYTES);
     attr = true;
   }
   dim3 grid((unsigned)ceil_div(nc, T_BN), (unsigned)ceil_div(m, T_BM), (unsigned)batch);
-  gemm_tf32x3_kernel<<<grid, 32 * T_WARPS, T_SMEM_BYTES, as_stream(stream)>>>(ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out,
+  gemm_f32split_kernel<<<grid, 32 * T_WARPS, T_SMEM_BYTES, as_stream(stream)>>>(ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out,
                                                                          ldo, strideO);
-  BMM_CHECK_LAUNCH("gemm_tf32x3_kernel");
+  BMM_CHECK_LAUNCH("gemm_f32split_kernel");
   return BMM_OK;
 }

@@ -205,16 +205,16 @@ class ShardedApproxProduct:
         self._c("bmm_sample", P(probs), P(self.cum), P(self.last), P(self.offsets), K, 1, n, max(self.sizes),
                 P(self.budgets), P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
         ma, pb = self.ma, self.pb
-        if M_local.dtype == torch.float32 and W % 4 == 0:
+        if M_local.dtype == torch.float32 and W % 8 == 0:
             a_hi = torch.empty(ma * W, dtype=torch.float32, device=M_local.device)
-            a_lo = torch.empty_like(a_hi)
+            a_x = torch.empty_like(a_hi)
             b_hi = torch.empty(pb * W, dtype=torch.float32, device=M_local.device)
-            b_lo = torch.empty_like(b_hi)
+            b_x = torch.empty_like(b_hi)
             Nc = N_local.contiguous()
-            self._c("bmm_gather_tf32x3", dt, P(M_local), M_local.stride(0), 0, P(Nc), Nc.stride(0), 0, ma, pb,
-                    P(self.column), P(self.scale), W, W, 1, P(a_hi), P(a_lo), P(b_hi), P(b_lo), st)
+            self._c("bmm_gather_f32split", dt, P(M_local), M_local.stride(0), 0, P(Nc), Nc.stride(0), 0, ma, pb,
+                    P(self.column), P(self.scale), W, W, 1, P(a_hi), P(a_x), P(b_hi), P(b_x), st)
             out = torch.empty((ma, pb), dtype=torch.float32, device=M_local.device)
-            self._c("bmm_gemm_tf32x3", P(a_hi), P(a_lo), P(b_hi), P(b_lo), ma, pb, W, 1, P(out), pb, 0, st)
+            self._c("bmm_gemm_f32split", P(a_hi), P(a_x), P(b_hi), P(b_x), ma, pb, W, 1, P(out), pb, 0, st)
             return out
         C = torch.empty((ma, W), dtype=torch.float64, device=M_local.device)
         D = torch.empty((W, pb), dtype=torch.float64, device=M_local.device)

@@ -159,14 +159,14 @@ class SketchPipeline:
         self.column = torch.zeros(B * W, **i64)  # zero-init: failed plans gather column 0, never garbage
         self.prob = torch.empty(B * W, **f64)
         self.scale = torch.empty(B * W, **f64)
-        # float32 inputs take the tcgen05 3xTF32 path (TMA rows need W % 4 == 0)
-        self.tf32 = (dtype == torch.float32 and method != "SSM" and W % 4 == 0)
+        # float32 inputs take the tcgen05 split-operand path (pair groups need W % 8 == 0)
+        self.tf32 = (dtype == torch.float32 and method != "SSM" and W % 8 == 0)
         if self.tf32:
             f32 = dict(dtype=torch.float32, device=dev)
             self.a_hi = torch.empty(B * self.m * W, **f32)
-            self.a_lo = torch.empty(B * self.m * W, **f32)
+            self.a_x = torch.empty(B * self.m * W, **f32)
             self.b_hi = torch.empty(B * self.p * W, **f32)
-            self.b_lo = torch.empty(B * self.p * W, **f32)
+            self.b_x = torch.empty(B * self.p * W, **f32)
             self.CD = torch.empty(B * self.m * self.p, **f32)
         else:
             self.C = torch.empty(B * self.m * W, **f64)
@@ -357,10 +357,10 @@ class SketchPipeline:
                 P(self.budgets),
                 P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
         if self.tf32:
-            # float32 inputs: split gather + tcgen05 3xTF32 contraction
-            self._c("bmm_gather_tf32x3", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column), P(self.scale), W, W,
-                    B, P(self.a_hi), P(self.a_lo), P(self.b_hi), P(self.b_lo), st)
-            self._c("bmm_gemm_tf32x3", P(self.a_hi), P(self.a_lo), P(self.b_hi), P(self.b_lo), m, p, W, B,
+            # float32 inputs: split gather + tcgen05 TF32 / BF16-cross-term contraction
+            self._c("bmm_gather_f32split", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column), P(self.scale), W, W,
+                    B, P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), st)
+            self._c("bmm_gemm_f32split", P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), m, p, W, B,
                     P(self.CD), p, m * p, st)
         else:
             self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column),
