@@ -151,8 +151,23 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = blockIdx.z;
-  const int a_row0 = (int)(b * m + (int64_t)blockIdx.y * T_BM);
-  const int b_row0 = (int)(b * nc + (int64_t)blockIdx.x * T_BN);
+  // Grouped rasterisation: consecutive CTAs sweep GROUP_M row tiles before
+  // moving to the next column tile, so the ~148 co-resident CTAs share both
+  // their A row blocks and their B column blocks through L2 (row-major launch
+  // order would re-stream all of B from HBM once per row block).
+  constexpr int GROUP_M = 16;
+  int tile_m, tile_n;
+  {
+    const int tm = gridDim.y, tn = gridDim.x;
+    const int lin = blockIdx.y * tn + blockIdx.x;
+    const int group = lin / (GROUP_M * tn);
+    const int first_m = group * GROUP_M;
+    const int gsz = min(tm - first_m, GROUP_M);
+    tile_m = first_m + (lin % (GROUP_M * tn)) % gsz;
+    tile_n = (lin % (GROUP_M * tn)) / gsz;
+  }
+  const int a_row0 = (int)(b * m + (int64_t)tile_m * T_BM);
+  const int b_row0 = (int)(b * nc + (int64_t)tile_n * T_BN);
   const int ktiles = (int)((k + T_BK - 1) / T_BK);
   const int nchunks = (ktiles + T_CHUNK - 1) / T_CHUNK;
 
@@ -246,10 +261,10 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[q]);
     }
-    const int64_t row = (int64_t)blockIdx.y * T_BM + quarter * 32 + lane;
+    const int64_t row = (int64_t)tile_m * T_BM + quarter * 32 + lane;
     if (row < m) {
       float* orow = out + b * strideO + row * ldo;
-      const int64_t col0 = (int64_t)blockIdx.x * T_BN;
+      const int64_t col0 = (int64_t)tile_n * T_BN;
       const bool vec = (col0 + T_BN <= nc) && (ldo % 4) == 0 && ((reinterpret_cast<uintptr_t>(orow + col0) & 15) == 0);
       if (vec) {
         float4* o4 = reinterpret_cast<float4*>(orow + col0);
