@@ -96,6 +96,62 @@ __global__ void __launch_bounds__(32 * kProbWarps) block_probs_kernel(
   }
 }
 
+// Large blocks (max_len > 256): one 256-thread CTA per block.  The elementwise
+// scores and the two divisions use every thread; warp 0 runs the NumPy sums
+// and the sequential cumsum from the shared-memory copy.  Same arithmetic and
+// order as block_probs_kernel, so the results are bit-identical.
+constexpr int kProbCtaThreads = 256;
+
+__global__ void __launch_bounds__(kProbCtaThreads) block_probs_cta_kernel(
+    const double* __restrict__ colsq, const double* __restrict__ rowsq, int64_t n,
+    const int64_t* __restrict__ offsets, int64_t K, double* __restrict__ probs, double* __restrict__ s,
+    double* __restrict__ cum, int64_t* __restrict__ last) {
+  __shared__ WarpPwScratch scr;
+  __shared__ double sh_tot[2];
+  extern __shared__ double wb[];
+  const int64_t g = blockIdx.x;
+  const int64_t b = g / K, k = g - b * K;
+  const int64_t o = offsets[k], nk = offsets[k + 1] - o;
+  const double* cs = colsq + b * n;
+  const double* rs = rowsq + b * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  SrcScore sc{cs, rs};
+  double* pb = probs + b * n + o;
+#pragma unroll 4
+  for (int64_t i = tid; i < nk; i += kProbCtaThreads) wb[i] = sc(o + i);
+  __syncthreads();
+  const SrcF64 sp{wb};
+  if (warp == 0) {
+    const double tot = __dadd_rn(0.0, warp_pw_sum(sp, 0, nk, &scr));
+    if (s != nullptr) {
+      const double rest = warp_pw_sum(sp, 1, nk - 1, &scr);
+      if (lane == 0) s[g] = __dadd_rn(wb[0], rest);
+    }
+    if (lane == 0) sh_tot[0] = tot;
+  }
+  __syncthreads();
+  const double tot = sh_tot[0];
+  if (tot == 0.0) {
+    for (int64_t i = tid; i < nk; i += kProbCtaThreads) wb[i] = 0.0;
+  } else {
+    for (int64_t i = tid; i < nk; i += kProbCtaThreads) wb[i] = __ddiv_rn(wb[i], tot);
+    __syncthreads();
+    if (warp == 0) {
+      const double tot2 = __dadd_rn(0.0, warp_pw_sum(sp, 0, nk, &scr));
+      if (lane == 0) sh_tot[1] = tot2;
+    }
+    __syncthreads();
+    const double tot2 = sh_tot[1];
+    for (int64_t i = tid; i < nk; i += kProbCtaThreads) wb[i] = __ddiv_rn(wb[i], tot2);
+  }
+  __syncthreads();
+  for (int64_t i = tid; i < nk; i += kProbCtaThreads) pb[i] = wb[i];
+  if (cum != nullptr && warp == 0) {
+    const int64_t lst = warp_cumsum(wb, cum + b * n + o, nk);
+    if (lane == 0) last[g] = lst;
+  }
+}
+
 // q = f / f.sum()   (plan.py:493-496)
 __global__ void normalize_kernel(const double* __restrict__ f, int64_t K, int64_t batch, double* q,
                                  int32_t* status) {
@@ -221,14 +277,17 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
     const int64_t* __restrict__ sizes, const int64_t* __restrict__ caps_in,
     const uint8_t* __restrict__ floors_in, int64_t K, const int64_t* __restrict__ c_arr, int cap,
     int64_t* budgets, int64_t* col_off, int32_t* status, int64_t* diag, int32_t* notes,
-    char* ws_base) {
+    char* ws_base, int use_smem) {
+  // working set in shared memory when it fits (every fixpoint phase then
+  // costs shared- rather than L2-latency round trips); global otherwise
+  extern __shared__ __align__(16) char dyn_ws[];
   __shared__ int64_t red[32];
   __shared__ int64_t sh_scalar[4];
   __shared__ double sh_S;
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x;
   const int NT = blockDim.x;
-  BudgetWs ws = carve_ws(ws_base + b * budget_ws_bytes(K), K);
+  BudgetWs ws = carve_ws(use_smem ? dyn_ws : ws_base + b * budget_ws_bytes(K), K);
   const int64_t c = c_arr[b];
   const double* sb = s ? s + b * K : nullptr;
   const double* ab = aux ? aux + b * K : nullptr;
@@ -524,7 +583,16 @@ extern "C" int bmm_block_probs(const double* colsq, const double* rowsq, int64_t
   unsigned grid = (unsigned)std::min<int64_t>(ceil_div(warps, kProbWarps), 148LL * 16 * 64);
   const int64_t smem = max_len * 8 * kProbWarps;
   cudaStream_t st = as_stream(stream);
-  if (smem <= 160 * 1024) {
+  if (probs != nullptr && fnorm == nullptr && max_len > 256 && max_len * 8 <= 160 * 1024 &&
+      K * batch < (1LL << 31)) {
+    static bool attr_c = false;
+    if (!attr_c) {
+      cudaFuncSetAttribute(block_probs_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      attr_c = true;
+    }
+    block_probs_cta_kernel<<<(unsigned)(K * batch), kProbCtaThreads, (size_t)(max_len * 8), st>>>(
+        colsq, rowsq, n, offsets, K, probs, s, cum, last_support);
+  } else if (smem <= 160 * 1024) {
     static int64_t attr = 0;
     if (smem > 48 * 1024 && attr == 0) {
       cudaFuncSetAttribute(block_probs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
@@ -572,8 +640,17 @@ extern "C" int bmm_budgets(int rule, const double* s, const double* aux, const i
                   aux != nullptr, BMM_E_ARG, "bmm_budgets: aux required");
   BMM_REQUIRE(rule == BMM_RULE_EXPLICIT || rule == BMM_RULE_PILOT || sizes != nullptr, BMM_E_ARG, "bmm_budgets: sizes required");
   BMM_REQUIRE(budgets != nullptr && ws != nullptr && c != nullptr, BMM_E_ARG, "bmm_budgets: null output");
-  budgets_kernel<<<(unsigned)batch, kBudgetThreads, 0, as_stream(stream)>>>(
-      rule, s, aux, sizes, caps, floors, K, c, cap, budgets, col_off, status, diag, notes, (char*)ws);
+  const int64_t bytes = budget_ws_bytes(K);
+  const bool smem = bytes <= 160 * 1024;
+  if (smem && bytes > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(budgets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      attr = true;
+    }
+  }
+  budgets_kernel<<<(unsigned)batch, kBudgetThreads, smem ? (size_t)bytes : 0, as_stream(stream)>>>(
+      rule, s, aux, sizes, caps, floors, K, c, cap, budgets, col_off, status, diag, notes, (char*)ws, smem ? 1 : 0);
   BMM_CHECK_LAUNCH("budgets_kernel");
   return BMM_OK;
 }

@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   if (w >= wpb) return;
-  double* scum = scum_all + (SMEM ? w * max_len : 0);
+  double* scum = scum_all + (SMEM ? 2 * w * max_len : 0);
+  double* sprob = scum + max_len;
   const int64_t warps_total = K * batch;
   for (int64_t g = blockIdx.x * (int64_t)wpb + w; g < warps_total; g += (int64_t)gridDim.x * wpb) {
     const int64_t b = g / K, k = g - b * K;
@@ -75,9 +76,13 @@ __global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
     const double* pb = probs + b * n + o;
     if (SMEM) {
       __syncwarp();
-      for (int64_t i = lane; i < len; i += 32) scum[i] = cb[i];
+      for (int64_t i = lane; i < len; i += 32) {
+        scum[i] = cb[i];
+        sprob[i] = pb[i];
+      }
       __syncwarp();
       cb = scum;
+      pb = sprob;
     }
     const int64_t lst = last[g];
     const uint64_t* sp = states + 4 * g;
@@ -233,7 +238,7 @@ extern "C" int bmm_sample(const double* probs, const double* cum, const int64_t*
   BMM_REQUIRE(K >= 1 && batch >= 1 && max_len >= 1, BMM_E_ARG, "bmm_sample: bad shape");
   const int64_t warps = K * batch;
   cudaStream_t st = as_stream(stream);
-  const int64_t per_warp = max_len * 8;
+  const int64_t per_warp = 2 * max_len * 8;  // CDF and probabilities
   int wpb = kSampleWarps;
   bool smem = true;
   if (per_warp * kSampleWarps > 96 * 1024) wpb = 1;
