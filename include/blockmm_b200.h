@@ -201,6 +201,20 @@ int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA,
                  double* out, int64_t ldo, int64_t strideO,
                  void* ws, int64_t ws_bytes, void* stream);
 
+/* Fused gather + contraction (no sketch in memory): out[b] = C[b] @ D[b] with
+ * C[:, t] = M[:, column[t]] * scale[t], D[t, :] = N[column[t], :] * scale[t],
+ * evaluated as sum_t M[:, col_t] (scale_t^2 N[col_t, :]) on the DMMA pipe: the
+ * A tile is gathered with 8-byte copies, B rows of N are copied whole, and the
+ * B fragments are scaled by scale_t^2 in registers.  Same workspace as
+ * bmm_gemm_f64(m, nc, W, batch).  estimators.py:143-175 without the C, D
+ * round trip through HBM.                                                   */
+int bmm_gemm_f64_gather(const double* M, int64_t ldm, int64_t strideM,
+                        const double* N, int64_t ldn, int64_t strideN,
+                        int64_t m, int64_t nc, const int64_t* column, const double* scale,
+                        int64_t W, int64_t w_stride, int64_t batch,
+                        double* out, int64_t ldo, int64_t strideO,
+                        void* ws, int64_t ws_bytes, void* stream);
+
 /* Segmented square-sum GEMM: gsq[b, j] = || A[:, seg_j] @ B[seg_j, :] ||_F^2
  * for segments seg_j = [seg[j], seg[j+1]) of the inner dimension.
  * OPL block product norms g_k^2 (plan.py:183-188) with seg = offsets, and
@@ -211,6 +225,13 @@ int bmm_segsq_f64(const double* A, int64_t lda, int64_t strideA,
                   const double* B, int64_t ldb, int64_t strideB,
                   int64_t m, int64_t nc, const int64_t* seg, int64_t nseg, int64_t seg_stride,
                   int64_t batch, double* gsq, void* ws, int64_t ws_bytes, void* stream);
+/* The same over a sketch gathered on the fly (as bmm_gemm_f64_gather): the
+ * two-step pilot norms ||C0_k D0_k||_F^2 straight from M and N (plan.py:457-464). */
+int bmm_segsq_f64_gather(const double* M, int64_t ldm, int64_t strideM,
+                         const double* N, int64_t ldn, int64_t strideN,
+                         int64_t m, int64_t nc, const int64_t* column, const double* scale,
+                         int64_t w_stride, const int64_t* seg, int64_t nseg, int64_t seg_stride,
+                         int64_t batch, double* gsq, void* ws, int64_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K9 error
  * err[b] = { sum (X - Y)^2, sum X^2 } over m x nc (X = exact MN, Y = C D),

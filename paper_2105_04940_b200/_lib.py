@@ -56,6 +56,10 @@ SIGNATURES = {
     "bmm_gemm_f64_set_variant": (_I, [_I, _I]),
     "bmm_gemm_f64": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _I64,
                           _P, _I64, _P]),
+    "bmm_gemm_f64_gather": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _I64, _P,
+                                 _I64, _I64, _P, _I64, _P]),
+    "bmm_segsq_f64_gather": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _I64, _I64,
+                                  _I64, _P, _P, _I64, _P]),
     "bmm_segsq_f64_workspace": (_I64, [_I64, _I64, _I64, _I64]),
     "bmm_segsq_f64": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P,
                            _P, _I64, _P]),

@@ -56,13 +56,50 @@ struct TileArgs {
   const double* B; int64_t ldb;
   int64_t m, nc;      // rows of A, columns of B
   int64_t m0, n0;     // tile origin
+  // gather mode (G): the inner index k is a sketch column t; A[h, t] is read as
+  // M[h, col[t]], B[t, f] as N[col[t], f], and each product is scaled by
+  // scale[t]^2 -- C @ D without materialising the sketch.
+  const int64_t* col = nullptr;
+  const double* scale = nullptr;
 };
 
 // Stage one BK slice [k0, k0+BK) of the A and B tiles; columns at or beyond kend are zero.
-template <class C, bool V16>
+template <class C, bool V16, bool G = false>
 __device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64_t kend, double* as, double* bs) {
   const int tid = threadIdx.x;
-  if constexpr (V16) {
+  if constexpr (G) {
+    // A: one gathered element per 8-byte copy; B: rows of N picked by col[t]
+#pragma unroll
+    for (int q = 0; q < C::BM * C::BK / C::THREADS; ++q) {
+      const int c = tid + C::THREADS * q;
+      const int row = c / C::BK, kk = c % C::BK;
+      const int64_t gr = ta.m0 + row, gk = k0 + kk;
+      const bool ok = gr < ta.m && gk < kend;
+      cp_async8(smem_u32(as + row * C::A_STR + kk), ok ? ta.A + gr * ta.lda + ta.col[gk] : ta.A, ok ? 8 : 0);
+    }
+    if constexpr (V16) {
+#pragma unroll
+      for (int q = 0; q < C::BK * C::BN / 2 / C::THREADS; ++q) {
+        const int c = tid + C::THREADS * q;
+        const int row = c / (C::BN / 2), nc2 = (c % (C::BN / 2)) * 2;
+        const int64_t gk = k0 + row, gn = ta.n0 + nc2;
+        int64_t nv = ta.nc - gn;
+        nv = nv < 0 ? 0 : (nv > 2 ? 2 : nv);
+        if (gk >= kend) nv = 0;
+        const double* src = nv ? ta.B + ta.col[gk] * ta.ldb + gn : ta.B;
+        cp_async16(smem_u32(bs + row * C::B_STR + nc2), src, (int)(nv * 8));
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < C::BK * C::BN / C::THREADS; ++q) {
+        const int c = tid + C::THREADS * q;
+        const int row = c / C::BN, nn = c % C::BN;
+        const int64_t gk = k0 + row, gn = ta.n0 + nn;
+        const bool ok = gk < kend && gn < ta.nc;
+        cp_async8(smem_u32(bs + row * C::B_STR + nn), ok ? ta.B + ta.col[gk] * ta.ldb + gn : ta.B, ok ? 8 : 0);
+      }
+    }
+  } else if constexpr (V16) {
 #pragma unroll
     for (int q = 0; q < C::BM * C::BK / 2 / C::THREADS; ++q) {
       const int c = tid + C::THREADS * q;
@@ -106,7 +143,7 @@ __device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64
 }
 
 // acc += A[m0:+BM, kbeg:kend] @ B[kbeg:kend, n0:+BN]
-template <class C, bool V16>
+template <class C, bool V16, bool G = false>
 __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64_t kend, double* smem,
                                          double (&acc)[C::FM][C::FN][2]) {
   double* As = smem;
@@ -117,7 +154,7 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
   const int64_t ktiles = (kend - kbeg + C::BK - 1) / C::BK;
 #pragma unroll
   for (int s = 0; s < C::STAGES - 1; ++s) {
-    if (s < ktiles) load_stage<C, V16>(ta, kbeg + s * C::BK, kend, As + s * C::A_TILE, Bs + s * C::B_TILE);
+    if (s < ktiles) load_stage<C, V16, G>(ta, kbeg + s * C::BK, kend, As + s * C::A_TILE, Bs + s * C::B_TILE);
     cp_async_commit();
   }
   for (int64_t kt = 0; kt < ktiles; ++kt) {
@@ -126,7 +163,7 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
     const int64_t nt = kt + C::STAGES - 1;
     if (nt < ktiles) {
       const int ns = (int)(nt % C::STAGES);
-      load_stage<C, V16>(ta, kbeg + nt * C::BK, kend, As + ns * C::A_TILE, Bs + ns * C::B_TILE);
+      load_stage<C, V16, G>(ta, kbeg + nt * C::BK, kend, As + ns * C::A_TILE, Bs + ns * C::B_TILE);
     }
     cp_async_commit();
     const int cs = (int)(kt % C::STAGES);
@@ -139,6 +176,14 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
       for (int mi = 0; mi < C::FM; ++mi) a[mi] = as[mi * 8 * C::A_STR + kk];
 #pragma unroll
       for (int ni = 0; ni < C::FN; ++ni) b[ni] = bs[kk * C::B_STR + ni * 8];
+      if constexpr (G) {
+        // this lane's B fragment row is sketch column t = k + kk + t_lane: scale it by s_t^2
+        const int64_t gk = kbeg + kt * C::BK + kk + t;
+        const double sv = gk < kend ? ta.scale[gk] : 0.0;
+        const double s2 = __dmul_rn(sv, sv);
+#pragma unroll
+        for (int ni = 0; ni < C::FN; ++ni) b[ni] = __dmul_rn(b[ni], s2);
+      }
 #pragma unroll
       for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
@@ -149,18 +194,24 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
   __syncthreads();
 }
 
-template <class C, bool V16>
+template <class C, bool V16, bool G = false>
 __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __restrict__ A, int64_t lda,
                                                               int64_t strideA, const double* __restrict__ B,
                                                               int64_t ldb, int64_t strideB, int64_t m, int64_t nc,
                                                               int64_t k, int64_t splits, int64_t kchunk,
                                                               double* __restrict__ out, int64_t ldo,
-                                                              int64_t strideO, double* __restrict__ part) {
+                                                              int64_t strideO, double* __restrict__ part,
+                                                              const int64_t* __restrict__ col,
+                                                              const double* __restrict__ scale, int64_t w_stride) {
   extern __shared__ __align__(16) double smem[];
   const int64_t z = blockIdx.z;
   const int64_t b = z / splits, sp = z - b * splits;
   TileArgs ta{A + b * strideA, lda, B + b * strideB, ldb, m, nc, (int64_t)blockIdx.y * C::BM,
               (int64_t)blockIdx.x * C::BN};
+  if constexpr (G) {
+    ta.col = col + b * w_stride;
+    ta.scale = scale + b * w_stride;
+  }
   const int64_t kbeg = sp * kchunk;
   const int64_t kend = min(k, kbeg + kchunk);
   double acc[C::FM][C::FN][2];
@@ -168,7 +219,7 @@ __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __re
   for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
     for (int ni = 0; ni < C::FN; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  if (kbeg < kend) mainloop<C, V16>(ta, kbeg, kend, smem, acc);
+  if (kbeg < kend) mainloop<C, V16, G>(ta, kbeg, kend, smem, acc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N, g = lane >> 2, t = lane & 3;
   double* dst;
@@ -203,13 +254,15 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ part, int64_t sp
 }
 
 // ---- segmented square sums
-template <class C>
+template <class C, bool G = false>
 __global__ void __launch_bounds__(C::THREADS) segsq_f64_kernel(const double* __restrict__ A, int64_t lda,
                                                                int64_t strideA, const double* __restrict__ B,
                                                                int64_t ldb, int64_t strideB, int64_t m,
                                                                int64_t nc, const int64_t* __restrict__ seg,
                                                                int64_t nseg, int64_t seg_stride,
-                                                               int64_t chunks, double* __restrict__ part) {
+                                                               int64_t chunks, double* __restrict__ part,
+                                                               const int64_t* __restrict__ col,
+                                                               const double* __restrict__ scale, int64_t w_stride) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double red[C::WARPS];
   const int64_t z = blockIdx.z;
@@ -218,6 +271,10 @@ __global__ void __launch_bounds__(C::THREADS) segsq_f64_kernel(const double* __r
   const int64_t j0 = ch * per, j1 = min(nseg, j0 + per);
   TileArgs ta{A + b * strideA, lda, B + b * strideB, ldb, m, nc, (int64_t)blockIdx.y * C::BM,
               (int64_t)blockIdx.x * C::BN};
+  if constexpr (G) {
+    ta.col = col + b * w_stride;
+    ta.scale = scale + b * w_stride;
+  }
   const int64_t tiles = (int64_t)gridDim.x * gridDim.y;
   const int64_t tile = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
   for (int64_t j = j0; j < j1; ++j) {
@@ -227,7 +284,7 @@ __global__ void __launch_bounds__(C::THREADS) segsq_f64_kernel(const double* __r
     for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
       for (int ni = 0; ni < C::FN; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-    if (kbeg < kend) mainloop<C, false>(ta, kbeg, kend, smem, acc);
+    if (kbeg < kend) mainloop<C, false, G>(ta, kbeg, kend, smem, acc);
     double sq = 0.0;
 #pragma unroll
     for (int mi = 0; mi < C::FM; ++mi)
@@ -392,21 +449,50 @@ inline int64_t segsq_chunks(const VariantInfo& vi, int64_t m, int64_t nc, int64_
 template <class C>
 static void launch_gemm(bool v16, dim3 grid, cudaStream_t st, const double* A, int64_t lda, int64_t strideA,
                         const double* B, int64_t ldb, int64_t strideB, int64_t m, int64_t nc, int64_t k,
-                        const SplitPlan& sp, double* out, int64_t ldo, int64_t strideO, double* part) {
+                        const SplitPlan& sp, double* out, int64_t ldo, int64_t strideO, double* part,
+                        const int64_t* col = nullptr, const double* scale = nullptr, int64_t w_stride = 0) {
+  if (col != nullptr) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_f64_kernel<C, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      cudaFuncSetAttribute(gemm_f64_kernel<C, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      attr = true;
+    }
+    if (v16)
+      gemm_f64_kernel<C, true, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k,
+                                                                       sp.splits, sp.kchunk, out, ldo, strideO, part,
+                                                                       col, scale, w_stride);
+    else
+      gemm_f64_kernel<C, false, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k,
+                                                                        sp.splits, sp.kchunk, out, ldo, strideO, part,
+                                                                        col, scale, w_stride);
+    return;
+  }
   if (v16)
     gemm_f64_kernel<C, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k, sp.splits,
-                                                               sp.kchunk, out, ldo, strideO, part);
+                                                               sp.kchunk, out, ldo, strideO, part, nullptr, nullptr, 0);
   else
     gemm_f64_kernel<C, false><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k, sp.splits,
-                                                                sp.kchunk, out, ldo, strideO, part);
+                                                                sp.kchunk, out, ldo, strideO, part, nullptr, nullptr, 0);
 }
 
 template <class C>
 static void launch_segsq(dim3 grid, cudaStream_t st, const double* A, int64_t lda, int64_t strideA, const double* B,
                          int64_t ldb, int64_t strideB, int64_t m, int64_t nc, const int64_t* seg, int64_t nseg,
-                         int64_t seg_stride, int64_t chunks, double* part) {
+                         int64_t seg_stride, int64_t chunks, double* part, const int64_t* col = nullptr,
+                         const double* scale = nullptr, int64_t w_stride = 0) {
+  if (col != nullptr) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(segsq_f64_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      attr = true;
+    }
+    segsq_f64_kernel<C, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg,
+                                                                  seg_stride, chunks, part, col, scale, w_stride);
+    return;
+  }
   segsq_f64_kernel<C><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg,
-                                                          seg_stride, chunks, part);
+                                                          seg_stride, chunks, part, nullptr, nullptr, 0);
 }
 
 }  // namespace bmm
@@ -426,12 +512,11 @@ extern "C" int64_t bmm_gemm_f64_workspace(int64_t m, int64_t nc, int64_t k, int6
   return sp.splits > 1 ? sp.splits * batch * m * nc * 8 : 0;
 }
 
-extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
-                            int64_t strideB, int64_t m, int64_t nc, int64_t k, int64_t batch, double* out,
-                            int64_t ldo, int64_t strideO, void* ws, int64_t ws_bytes, void* stream) {
-  BMM_REQUIRE(m >= 0 && nc >= 0 && k >= 0 && batch >= 1, BMM_E_ARG, "bmm_gemm_f64: bad shape");
+static int gemm_impl(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb, int64_t strideB,
+                     int64_t m, int64_t nc, int64_t k, int64_t batch, double* out, int64_t ldo, int64_t strideO,
+                     void* ws, int64_t ws_bytes, cudaStream_t st, const int64_t* col, const double* scale,
+                     int64_t w_stride) {
   if (m == 0 || nc == 0) return BMM_OK;
-  cudaStream_t st = as_stream(stream);
   if (k == 0) {
     for (int64_t b = 0; b < batch; ++b)
       if (cudaMemset2DAsync(out + b * strideO, ldo * 8, 0, nc * 8, m, st) != cudaSuccess) {
@@ -446,19 +531,24 @@ extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const
   BMM_REQUIRE(ws_bytes >= need && (need == 0 || ws != nullptr), BMM_E_ARG,
               "bmm_gemm_f64: workspace too small (%lld < %lld)", (long long)ws_bytes, (long long)need);
   BMM_REQUIRE(ceil_div(m, vi.BM) <= 65535, BMM_E_UNSUPPORTED, "bmm_gemm_f64: m too large");
-  const bool v16 = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
-                   lda % 2 == 0 && ldb % 2 == 0 && strideA % 2 == 0 && strideB % 2 == 0;
+  // 16-byte copies need aligned rows; in gather mode only B's rows are copied in 16-byte chunks
+  const bool v16 = (col != nullptr || ((reinterpret_cast<uintptr_t>(A) % 16 == 0) && lda % 2 == 0 && strideA % 2 == 0)) &&
+                   (reinterpret_cast<uintptr_t>(B) % 16 == 0) && ldb % 2 == 0 && strideB % 2 == 0;
   dim3 grid((unsigned)ceil_div(nc, vi.BN), (unsigned)ceil_div(m, vi.BM), (unsigned)(batch * sp.splits));
   double* part = (double*)ws;
+#define BMM_GEMM_CASE(V)                                                                                       \
+  launch_gemm<V>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part, col, \
+                 scale, w_stride)
   switch (g_variant) {
-    case 1: launch_gemm<DV1>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
-    case 2: launch_gemm<DV2>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
-    case 3: launch_gemm<DV3>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
-    case 4: launch_gemm<DV4>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
-    case 5: launch_gemm<DV5>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
-    case 6: launch_gemm<DV6>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part); break;
-    default: launch_gemm<DV0>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part);
+    case 1: BMM_GEMM_CASE(DV1); break;
+    case 2: BMM_GEMM_CASE(DV2); break;
+    case 3: BMM_GEMM_CASE(DV3); break;
+    case 4: BMM_GEMM_CASE(DV4); break;
+    case 5: BMM_GEMM_CASE(DV5); break;
+    case 6: BMM_GEMM_CASE(DV6); break;
+    default: BMM_GEMM_CASE(DV0);
   }
+#undef BMM_GEMM_CASE
   BMM_CHECK_LAUNCH("gemm_f64_kernel");
   if (sp.splits > 1) {
     splitk_reduce_kernel<<<grid_for(m * nc * batch, 256), 256, 0, st>>>((const double*)ws, sp.splits, m, nc,
@@ -468,38 +558,76 @@ extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const
   return BMM_OK;
 }
 
+extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                            int64_t strideB, int64_t m, int64_t nc, int64_t k, int64_t batch, double* out,
+                            int64_t ldo, int64_t strideO, void* ws, int64_t ws_bytes, void* stream) {
+  BMM_REQUIRE(m >= 0 && nc >= 0 && k >= 0 && batch >= 1, BMM_E_ARG, "bmm_gemm_f64: bad shape");
+  return gemm_impl(A, lda, strideA, B, ldb, strideB, m, nc, k, batch, out, ldo, strideO, ws, ws_bytes,
+                   as_stream(stream), nullptr, nullptr, 0);
+}
+
+extern "C" int bmm_gemm_f64_gather(const double* M, int64_t ldm, int64_t strideM, const double* N, int64_t ldn,
+                                   int64_t strideN, int64_t m, int64_t nc, const int64_t* column,
+                                   const double* scale, int64_t W, int64_t w_stride, int64_t batch, double* out,
+                                   int64_t ldo, int64_t strideO, void* ws, int64_t ws_bytes, void* stream) {
+  BMM_REQUIRE(m >= 0 && nc >= 0 && W >= 0 && batch >= 1 && column != nullptr && scale != nullptr, BMM_E_ARG,
+              "bmm_gemm_f64_gather: bad arguments");
+  return gemm_impl(M, ldm, strideM, N, ldn, strideN, m, nc, W, batch, out, ldo, strideO, ws, ws_bytes,
+                   as_stream(stream), column, scale, w_stride);
+}
+
 extern "C" int64_t bmm_segsq_f64_workspace(int64_t m, int64_t nc, int64_t nseg, int64_t batch) {
   const VariantInfo vi = variant_info(g_seg_variant);
   return ceil_div(m, vi.BM) * ceil_div(nc, vi.BN) * nseg * batch * 8;
 }
 
-extern "C" int bmm_segsq_f64(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
-                             int64_t strideB, int64_t m, int64_t nc, const int64_t* seg, int64_t nseg,
-                             int64_t seg_stride, int64_t batch, double* gsq, void* ws, int64_t ws_bytes,
-                             void* stream) {
+static int segsq_impl(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb, int64_t strideB,
+                      int64_t m, int64_t nc, const int64_t* seg, int64_t nseg, int64_t seg_stride, int64_t batch,
+                      double* gsq, void* ws, int64_t ws_bytes, cudaStream_t st, const int64_t* col,
+                      const double* scale, int64_t w_stride) {
   BMM_REQUIRE(m >= 1 && nc >= 1 && nseg >= 1 && batch >= 1, BMM_E_ARG, "bmm_segsq_f64: bad shape");
   const VariantInfo vi = variant_info(g_seg_variant);
   const int64_t tiles = ceil_div(m, vi.BM) * ceil_div(nc, vi.BN);
   const int64_t need = tiles * nseg * batch * 8;
   BMM_REQUIRE(ws_bytes >= need && ws != nullptr, BMM_E_ARG, "bmm_segsq_f64: workspace too small");
   BMM_REQUIRE(ceil_div(m, vi.BM) <= 65535, BMM_E_UNSUPPORTED, "bmm_segsq_f64: m too large");
-  cudaStream_t st = as_stream(stream);
   const int64_t chunks = segsq_chunks(vi, m, nc, nseg, batch);
   dim3 grid((unsigned)ceil_div(nc, vi.BN), (unsigned)ceil_div(m, vi.BM), (unsigned)(batch * chunks));
   double* part = (double*)ws;
+#define BMM_SEG_CASE(V) \
+  launch_segsq<V>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part, col, scale, w_stride)
   switch (g_seg_variant) {
-    case 1: launch_segsq<DV1>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
-    case 2: launch_segsq<DV2>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
-    case 3: launch_segsq<DV3>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
-    case 4: launch_segsq<DV4>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
-    case 5: launch_segsq<DV5>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
-    case 6: launch_segsq<DV6>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part); break;
-    default: launch_segsq<DV0>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part);
+    case 1: BMM_SEG_CASE(DV1); break;
+    case 2: BMM_SEG_CASE(DV2); break;
+    case 3: BMM_SEG_CASE(DV3); break;
+    case 4: BMM_SEG_CASE(DV4); break;
+    case 5: BMM_SEG_CASE(DV5); break;
+    case 6: BMM_SEG_CASE(DV6); break;
+    default: BMM_SEG_CASE(DV0);
   }
+#undef BMM_SEG_CASE
   BMM_CHECK_LAUNCH("segsq_f64_kernel");
   segsq_reduce_kernel<<<grid_for(nseg * batch, 128), 128, 0, st>>>((const double*)ws, tiles, nseg * batch, gsq);
   BMM_CHECK_LAUNCH("segsq_reduce_kernel");
   return BMM_OK;
+}
+
+extern "C" int bmm_segsq_f64(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                             int64_t strideB, int64_t m, int64_t nc, const int64_t* seg, int64_t nseg,
+                             int64_t seg_stride, int64_t batch, double* gsq, void* ws, int64_t ws_bytes,
+                             void* stream) {
+  return segsq_impl(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, batch, gsq, ws, ws_bytes,
+                    as_stream(stream), nullptr, nullptr, 0);
+}
+
+extern "C" int bmm_segsq_f64_gather(const double* M, int64_t ldm, int64_t strideM, const double* N, int64_t ldn,
+                                    int64_t strideN, int64_t m, int64_t nc, const int64_t* column,
+                                    const double* scale, int64_t w_stride, const int64_t* seg, int64_t nseg,
+                                    int64_t seg_stride, int64_t batch, double* gsq, void* ws, int64_t ws_bytes,
+                                    void* stream) {
+  BMM_REQUIRE(column != nullptr && scale != nullptr, BMM_E_ARG, "bmm_segsq_f64_gather: bad arguments");
+  return segsq_impl(M, ldm, strideM, N, ldn, strideN, m, nc, seg, nseg, seg_stride, batch, gsq, ws, ws_bytes,
+                    as_stream(stream), column, scale, w_stride);
 }
 
 extern "C" int64_t bmm_sqdiff_workspace(int64_t m, int64_t nc, int64_t batch) {

@@ -169,8 +169,12 @@ class SketchPipeline:
             self.b_x = torch.empty(B * self.p * W, **f32)
             self.CD = torch.empty(B * self.m * self.p, **f32)
         else:
-            self.C = torch.empty(B * self.m * W, **f64)
-            self.D = torch.empty(B * W * self.p, **f64)
+            # float64 path: the DMMA kernel gathers and scales the sketch on the fly
+            # (bmm_gemm_f64_gather), so C and D never exist in memory -- except for
+            # the SSM baseline, whose whole-block sketch is gathered explicitly
+            if method == "SSM":
+                self.C = torch.empty(B * self.m * W, **f64)
+                self.D = torch.empty(B * W * self.p, **f64)
             self.CD = torch.empty(B * self.m * self.p, **f64)
             self.ws_gemm = torch.empty(max(256, self.lib.bmm_gemm_f64_workspace(self.m, self.p, W, B)),
                                        dtype=torch.uint8, device=dev)
@@ -191,8 +195,6 @@ class SketchPipeline:
             self.p_column = torch.zeros(B * W0, **i64)
             self.p_prob = torch.zeros(B * W0, **f64)
             self.p_scale = torch.zeros(B * W0, **f64)
-            self.C0 = torch.empty(B * self.m * W0, **f64)
-            self.D0 = torch.empty(B * W0 * self.p, **f64)
             self.pilot_sq = torch.empty(B * K, **f64)
             self.ws_seg = torch.empty(max(256, self.lib.bmm_segsq_f64_workspace(self.m, self.p, K, B)),
                                       dtype=torch.uint8, device=dev)
@@ -340,11 +342,11 @@ class SketchPipeline:
             self._c("bmm_sample", P(p0), P(p0cum), P(p0last), P(self.offsets), K, B, n, self.max_len, P(self.p_bud),
                     P(self.p_coloff), self.W0, P(self.p_states), P(self.p_column), P(self.p_prob),
                     P(self.p_scale), st)
-            self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.p_column),
-                    P(self.p_scale), self.W0, self.W0, B, P(self.C0), self.W0, m * self.W0, P(self.D0), p,
-                    self.W0 * p, st)
-            self._c("bmm_segsq_f64", P(self.C0), self.W0, m * self.W0, P(self.D0), p, self.W0 * p, m, p,
-                    P(self.p_coloff), K, K + 1, B, P(self.pilot_sq), P(self.ws_seg), self.ws_seg.numel(), st)
+            # pilot norms ||C0_k D0_k||_F^2 straight from M and N (sketch gathered on the fly)
+            A, Bm = self._f64(M, N)
+            self._c("bmm_segsq_f64_gather", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p, P(self.p_column),
+                    P(self.p_scale), self.W0, P(self.p_coloff), K, K + 1, B, P(self.pilot_sq), P(self.ws_seg),
+                    self.ws_seg.numel(), st)
             aux = self.pilot_sq
         self._c("bmm_budgets", rule, P(self.s) if rule != _lib.RULE_UU else None, P(aux) if aux is not None else None,
                 P(self.sizes_d), None, None, K, B, P(self.c_arr), int(self.cap), P(self.budgets), P(self.col_off),
@@ -363,10 +365,9 @@ class SketchPipeline:
             self._c("bmm_gemm_f32split", P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), m, p, W, B,
                     P(self.CD), p, m * p, st)
         else:
-            self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column),
-                    P(self.scale), W, W, B, P(self.C), W, m * W, P(self.D), p, W * p, st)
-            self._c("bmm_gemm_f64", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, B, P(self.CD), p, m * p,
-                    P(self.ws_gemm), self.ws_gemm.numel(), st)
+            A, Bm = self._f64(M, N)
+            self._c("bmm_gemm_f64_gather", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p, P(self.column),
+                    P(self.scale), W, W, B, P(self.CD), p, m * p, P(self.ws_gemm), self.ws_gemm.numel(), st)
         return self._result()
 
     def _run_ssm(self, M, N, dt, st):

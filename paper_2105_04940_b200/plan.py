@@ -367,7 +367,7 @@ def allocate_two_step(M, N, part: BlockPartition, c: int, c0: int, p0: BlockProb
 
     floor(c0/K) pilot draws per block on child streams rng.spawn(K); the pilot
     norms ||C0 D0||_F come from the DMMA segmented square-sum GEMM."""
-    from .estimators import sample_blocks, gather_sketch  # estimators builds on plans
+    from .estimators import sample_blocks  # estimators builds on plans
 
     _check_instance(M, N, part)
     p0.check_partition(part)
@@ -389,8 +389,15 @@ def allocate_two_step(M, N, part: BlockPartition, c: int, c0: int, p0: BlockProb
     col, prob, scale, col_off = sample_blocks(inst, p0.flat(), pilot_budgets, words, first)
     W0 = int(col_off[-1].item()) if K else 0
     if W0 > 0:
-        C0, D0 = gather_sketch(inst, col, scale, W0, dtype=torch.float64)
-        pilot_sq = segsq(C0, D0, col_off, K)
+        # ||C0_k D0_k||_F^2 with the pilot sketch gathered on the fly (plan.py:463-464)
+        A = inst.M if inst.M.dtype == torch.float64 else inst.M.to(torch.float64)
+        B = inst.N if inst.N.dtype == torch.float64 else inst.N.to(torch.float64)
+        m, p = A.shape[0], B.shape[1]
+        pilot_sq = torch.empty(K, dtype=torch.float64, device=A.device)
+        ws = _lib.workspace(_lib.load().bmm_segsq_f64_workspace(m, p, K, 1))
+        _lib.call("bmm_segsq_f64_gather", _lib.ptr(A), A.stride(0), 0, _lib.ptr(B), B.stride(0), 0, m, p,
+                  _lib.ptr(col), _lib.ptr(scale), W0, _lib.ptr(col_off), K, 0, 1, _lib.ptr(pilot_sq),
+                  _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
     else:
         pilot_sq = torch.zeros(K, dtype=torch.float64, device=s.device)
     budgets, note = device_budgets(_lib.RULE_TWO_STEP, K, int(c), s=s, aux=pilot_sq, sizes=inst.sizes,
