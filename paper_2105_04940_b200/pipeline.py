@@ -169,12 +169,12 @@ class SketchPipeline:
             self.b_x = torch.empty(B * self.p * W, **f32)
             self.CD = torch.empty(B * self.m * self.p, **f32)
         else:
-            # float64 path: the DMMA kernel gathers and scales the sketch on the fly
-            # (bmm_gemm_f64_gather), so C and D never exist in memory -- except for
-            # the SSM baseline, whose whole-block sketch is gathered explicitly
-            if method == "SSM":
-                self.C = torch.empty(B * self.m * W, **f64)
-                self.D = torch.empty(B * W * self.p, **f64)
+            # float64 path: gather the rescaled sketch (bandwidth-bound kernel at
+            # full occupancy), then C @ D on the DMMA pipe.  Gathering M's columns
+            # inside the GEMM (bmm_gemm_f64_gather) is one 8-byte copy per element
+            # and measured slower on the tensor-bound kernel.
+            self.C = torch.empty(B * self.m * W, **f64)
+            self.D = torch.empty(B * W * self.p, **f64)
             self.CD = torch.empty(B * self.m * self.p, **f64)
             self.ws_gemm = torch.empty(max(256, self.lib.bmm_gemm_f64_workspace(self.m, self.p, W, B)),
                                        dtype=torch.uint8, device=dev)
@@ -365,9 +365,10 @@ class SketchPipeline:
             self._c("bmm_gemm_f32split", P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), m, p, W, B,
                     P(self.CD), p, m * p, st)
         else:
-            A, Bm = self._f64(M, N)
-            self._c("bmm_gemm_f64_gather", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p, P(self.column),
-                    P(self.scale), W, W, B, P(self.CD), p, m * p, P(self.ws_gemm), self.ws_gemm.numel(), st)
+            self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column),
+                    P(self.scale), W, W, B, P(self.C), W, m * W, P(self.D), p, W * p, st)
+            self._c("bmm_gemm_f64", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, B, P(self.CD), p, m * p,
+                    P(self.ws_gemm), self.ws_gemm.numel(), st)
         return self._result()
 
     def _run_ssm(self, M, N, dt, st):

@@ -329,3 +329,37 @@ def test_block_scores_and_relative_error():
     Bm = A + 1e-3 * g.standard_normal(A.shape)
     e, r = O.frob_errors(A, Bm)
     assert abs(bm.relative_error(Bm, A) - np.sqrt(e) / np.sqrt(r)) < 1e-14
+
+
+def test_fused_gather_kernels_match_materialised_sketch():
+    """bmm_gemm_f64_gather / bmm_segsq_f64_gather == gather + GEMM / segsq (float64 rounding level)."""
+    import torch
+    from paper_2105_04940_b200 import _lib
+    g = np.random.default_rng(31)
+    m, n, p, W = 70, 900, 50, 333
+    M = torch.as_tensor(g.standard_normal((m, n)), device="cuda")
+    N = torch.as_tensor(g.standard_normal((n, p)), device="cuda")
+    col = torch.as_tensor(g.integers(0, n, W), device="cuda")
+    sc = torch.as_tensor(g.random(W) + 0.5, device="cuda")
+    st = _lib.stream_ptr()
+    C = torch.empty((m, W), dtype=torch.float64, device="cuda")
+    D = torch.empty((W, p), dtype=torch.float64, device="cuda")
+    _lib.call("bmm_gather", 0, 0, M.data_ptr(), n, 0, N.data_ptr(), p, 0, m, p, col.data_ptr(), sc.data_ptr(), W, W,
+              1, C.data_ptr(), W, 0, D.data_ptr(), p, 0, st)
+    ws = _lib.workspace(1 << 26)
+    ref = torch.empty((m, p), dtype=torch.float64, device="cuda")
+    out = torch.empty_like(ref)
+    _lib.call("bmm_gemm_f64", C.data_ptr(), W, 0, D.data_ptr(), p, 0, m, p, W, 1, ref.data_ptr(), p, 0,
+              ws.data_ptr(), ws.numel(), st)
+    _lib.call("bmm_gemm_f64_gather", M.data_ptr(), n, 0, N.data_ptr(), p, 0, m, p, col.data_ptr(), sc.data_ptr(),
+              W, W, 1, out.data_ptr(), p, 0, ws.data_ptr(), ws.numel(), st)
+    assert ((out - ref).norm() / ref.norm()).item() < 1e-14
+    seg = torch.as_tensor(np.array([0, 7, 7, 100, 333]), device="cuda")
+    g_ref = torch.empty(4, dtype=torch.float64, device="cuda")
+    g_out = torch.empty_like(g_ref)
+    _lib.call("bmm_segsq_f64", C.data_ptr(), W, 0, D.data_ptr(), p, 0, m, p, seg.data_ptr(), 4, 0, 1,
+              g_ref.data_ptr(), ws.data_ptr(), ws.numel(), st)
+    _lib.call("bmm_segsq_f64_gather", M.data_ptr(), n, 0, N.data_ptr(), p, 0, m, p, col.data_ptr(), sc.data_ptr(),
+              W, seg.data_ptr(), 4, 0, 1, g_out.data_ptr(), ws.data_ptr(), ws.numel(), st)
+    np.testing.assert_allclose(g_out.cpu().numpy(), g_ref.cpu().numpy(), rtol=1e-13)
+    assert g_ref[1].item() == 0.0
