@@ -234,7 +234,13 @@ def plan_budgets(rule: str, sizes, c: int, s=None, aux_sq=None, cap: bool = True
         raise ValueError(rule)
     if rule in ("OPL", "TWO_STEP") and w.sum() == 0.0:
         w, note = s, True
-    return integerize(w, c, caps=caps_for(sizes, cap, c, s), floors=s > 0), note
+    budgets = integerize(w, c, caps=caps_for(sizes, cap, c, s), floors=s > 0)
+    # SamplingPlan.__post_init__ (plan.py:146-152): the zero-weight hand-out
+    # (plan.py:311-322) ignores floors, so a scored block can end at 0
+    for k in range(len(sizes)):
+        if (budgets[k] == 0) != (not s[k] > 0):
+            raise ValueError(f"block {k}: zero budget and zero-probability flag must coincide")
+    return budgets, note
 
 
 # ---------------------------------------------------------------- sampling
@@ -278,6 +284,36 @@ def instance_stats(M, N, sizes):
     return cs, rs, probs, s
 
 
+def two_step_pilot(M, N, sizes, c0: int, method: str, rng: np.random.Generator, probs=None, s=None):
+    """Pilot half of estimate_product_two_step (estimators.py:201-208 spawn,
+    plan.py:448-464 pilot): returns (pilot_sq, pilot columns, pilot scales,
+    main generator).  pilot_sq_k = ||C0_k D0_k||_F^2 in BLAS order."""
+    sizes = list(sizes)
+    K = len(sizes)
+    if probs is None or s is None:
+        _, _, probs, s = instance_stats(M, N, sizes)
+    p0 = np.concatenate([np.full(nk, 1.0 / nk) for nk in sizes]) if method == "ONU" else probs
+    pilot_rng, main_rng = rng.spawn(2)
+    pc = int(c0) // K
+    if pc < 1:
+        raise ValueError(f"c0={c0} gives no pilot draws for K={K} blocks")
+    off = offsets_of(sizes)
+    live = np.array([p0[off[k]:off[k + 1]].sum() != 0.0 for k in range(K)])
+    if s.sum() == 0.0:
+        raise ValueError("all blocks have zero score: nothing to sample")
+    pstreams = pilot_rng.spawn(K)
+    pbud = np.where(live, pc, 0)
+    pcols, _, pscale, C0, D0 = sketch(M, N, sizes, p0, pbud, pstreams)
+    pilot_sq = np.zeros(K)
+    po = offsets_of(pbud)
+    for k in range(K):
+        if pbud[k]:
+            P = C0[:, po[k]:po[k + 1]] @ D0[po[k]:po[k + 1], :]
+            f = P.ravel()
+            pilot_sq[k] = float(np.sqrt(f @ f)) ** 2
+    return pilot_sq, pcols, pscale, main_rng
+
+
 def approx_product(M, N, sizes, c: int, method: str, rng: np.random.Generator, c0: int = 0,
                    cap: bool = True, keep_sketch: bool = False) -> dict:
     """One approximate product through the reference composition:
@@ -288,25 +324,7 @@ def approx_product(M, N, sizes, c: int, method: str, rng: np.random.Generator, c
     out: dict = {"method": method}
     cs, rs, probs, s = instance_stats(M, N, sizes)
     if method in ("ONU", "ONMCNR"):
-        p0 = np.concatenate([np.full(nk, 1.0 / nk) for nk in sizes]) if method == "ONU" else probs
-        pilot_rng, main_rng = rng.spawn(2)
-        pc = int(c0) // K
-        if pc < 1:
-            raise ValueError(f"c0={c0} gives no pilot draws for K={K} blocks")
-        off = offsets_of(sizes)
-        live = np.array([p0[off[k]:off[k + 1]].sum() != 0.0 for k in range(K)])
-        if s.sum() == 0.0:
-            raise ValueError("all blocks have zero score: nothing to sample")
-        pstreams = pilot_rng.spawn(K)
-        pbud = np.where(live, pc, 0)
-        pcols, _, pscale, C0, D0 = sketch(M, N, sizes, p0, pbud, pstreams)
-        pilot_sq = np.zeros(K)
-        po = offsets_of(pbud)
-        for k in range(K):
-            if pbud[k]:
-                P = C0[:, po[k]:po[k + 1]] @ D0[po[k]:po[k + 1], :]
-                f = P.ravel()
-                pilot_sq[k] = float(np.sqrt(f @ f)) ** 2
+        pilot_sq, pcols, pscale, main_rng = two_step_pilot(M, N, sizes, c0, method, rng, probs, s)
         budgets, note = plan_budgets("TWO_STEP", sizes, c, s=s, aux_sq=pilot_sq, cap=cap)
         out.update(pilot_sq=pilot_sq, pilot_columns=pcols, pilot_scale=pscale)
         stream_rng = main_rng

@@ -30,6 +30,7 @@ ST_ABOVE_CAPS = 8
 ST_NO_CONVERGE = 9
 ST_NOT_PLACED = 10
 ST_EMPTY_SUPPORT = 11
+ST_PLAN_MISMATCH = 12
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

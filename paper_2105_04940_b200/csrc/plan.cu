@@ -542,6 +542,7 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
   int64_t cnt_total = 0;
   int64_t pos = block_exclusive_scan(cnt_local, red, &cnt_total);
   int64_t run = 0;
+  int64_t first_bad = K;  // SamplingPlan check: budget 0 <=> zero-probability block
   for (int64_t k = k_lo; k < k_hi; ++k) {
     int64_t v;
     if (st != BMM_ST_OK) v = 0;
@@ -551,6 +552,20 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
     budgets[b * K + k] = v;
     ws.maxs[k] = v;  // reuse for the prefix below
     run += v;
+    if (scored && (v == 0) != !(sb[k] > 0.0)) first_bad = min(first_bad, k);
+  }
+  if (st == BMM_ST_OK && scored) {
+    // the zero-weight hand-out (plan.py:311-322) ignores floors, so a scored
+    // block can end at 0; the reference's SamplingPlan then raises  plan.py:146-152
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) first_bad = min(first_bad, (int64_t)__shfl_xor_sync(0xffffffffu, first_bad, o));
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = first_bad;
+    __syncthreads();
+    int64_t fb = K;
+    for (int i = 0; i < (NT >> 5); ++i) fb = min(fb, red[i]);
+    __syncthreads();
+    if (fb < K) { st = BMM_ST_PLAN_MISMATCH; dg = fb; }
   }
   if (col_off != nullptr) {
     int64_t tot = 0;

@@ -77,6 +77,8 @@ def test_status_mapping():
         raise_status(_lib.ST_BELOW_FLOORS, 100, 20)
     with pytest.raises(AssertionError):
         raise_status(_lib.ST_NOT_PLACED, 0, 1)
+    with pytest.raises(ValueError, match="block 3: zero budget and zero-probability flag must coincide"):
+        raise_status(_lib.ST_PLAN_MISMATCH, 3, 10)
 
 
 def test_product_path_fails_loudly_without_gpu():
