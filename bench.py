@@ -186,7 +186,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2105_04940_b200 as bm
     from paper_2105_04940_b200 import _lib
-    from paper_2105_04940_b200.pipeline import SketchPipeline, seeds_from_rngs
+    from paper_2105_04940_b200.pipeline import PipelineGroup, SketchPipeline, seeds_from_rngs
 
     cfg, build, runs = workload_spec(args.workload)
     M_h, N_h, sizes = build()
@@ -196,22 +196,18 @@ def run_ours(args):
     Md = torch.as_tensor(M_h, device="cuda")
     Nd = torch.as_tensor(N_h, device="cuda")
     pipes = [SketchPipeline(m, n, p, sizes, W, meth, c0=c0) for _, W, meth, c0 in runs]
+    group = PipelineGroup(pipes)  # the sweep's products run as concurrent graph branches
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
     def step(Mx, Nx):
-        outs = []
-        for (cb, W, meth, c0), pipe in zip(runs, pipes):
-            rng = workloads.sample_rng(cfg, cb)
-            seeds = seeds_from_rngs(meth, [rng], K)
-            outs.append(pipe.run(Mx, Nx, seeds))
-        return outs
+        seeds = [seeds_from_rngs(meth, [workloads.sample_rng(cfg, cb)], K) for cb, W, meth, c0 in runs]
+        return group.run(Mx, Nx, seeds)
 
     # correctness of the bench configuration itself (untimed), then graph capture
     for pipe_out, pipe in zip(step(Md, Nd), pipes):
         pipe.check()
-    for pipe in pipes:
-        pipe.capture(Md, Nd)
+    group.capture(Md, Nd)
     for _ in range(args.warmup):
         step(Md, Nd)
     torch.cuda.synchronize()
@@ -234,7 +230,7 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
     # eager launches (none when every pipeline replays its CUDA graph) + graph-contained kernels
-    launches = (_lib.launches() - n_launch0) // args.steps + sum(p.graph_launches for p in pipes)
+    launches = (_lib.launches() - n_launch0) // args.steps + group.graph_launches
     ms = [a.elapsed_time(b) for a, b in times]
     ms_step = float(np.mean(ms))
     if world > 1:

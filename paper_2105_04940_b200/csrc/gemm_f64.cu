@@ -63,9 +63,11 @@ struct TileArgs {
   const double* scale = nullptr;
 };
 
-// Stage one BK slice [k0, k0+BK) of the A and B tiles; columns at or beyond kend are zero.
+// Stage one BK slice [k0, k0+BK) of the A and B tiles; inner indices outside [klo, kend) are zero
+// (k0 may start one below klo so that 16-byte copies stay aligned at odd segment starts).
 template <class C, bool V16, bool G = false>
-__device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64_t kend, double* as, double* bs) {
+__device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64_t klo, int64_t kend, double* as,
+                                           double* bs) {
   const int tid = threadIdx.x;
   if constexpr (G) {
     // A: one gathered element per 8-byte copy; B: rows of N picked by col[t]
@@ -85,7 +87,7 @@ __device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64
         const int64_t gk = k0 + row, gn = ta.n0 + nc2;
         int64_t nv = ta.nc - gn;
         nv = nv < 0 ? 0 : (nv > 2 ? 2 : nv);
-        if (gk >= kend) nv = 0;
+        if (gk >= kend || gk < klo) nv = 0;
         const double* src = nv ? ta.B + ta.col[gk] * ta.ldb + gn : ta.B;
         cp_async16(smem_u32(bs + row * C::B_STR + nc2), src, (int)(nv * 8));
       }
@@ -109,7 +111,13 @@ __device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64
       nv = nv < 0 ? 0 : (nv > 2 ? 2 : nv);
       if (gr >= ta.m) nv = 0;
       const double* src = nv ? ta.A + gr * ta.lda + gk : ta.A;
-      cp_async16(smem_u32(as + row * C::A_STR + kc), src, (int)(nv * 8));
+      if (gk < klo) {
+        // the pair straddling an odd segment start: zero, then the element at klo
+        cp_async8(smem_u32(as + row * C::A_STR + kc), ta.A, 0);
+        cp_async8(smem_u32(as + row * C::A_STR + kc + 1), nv == 2 ? src + 1 : ta.A, nv == 2 ? 8 : 0);
+      } else {
+        cp_async16(smem_u32(as + row * C::A_STR + kc), src, (int)(nv * 8));
+      }
     }
 #pragma unroll
     for (int q = 0; q < C::BK * C::BN / 2 / C::THREADS; ++q) {
@@ -118,7 +126,7 @@ __device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64
       const int64_t gk = k0 + row, gn = ta.n0 + nc2;
       int64_t nv = ta.nc - gn;
       nv = nv < 0 ? 0 : (nv > 2 ? 2 : nv);
-      if (gk >= kend) nv = 0;
+      if (gk >= kend || gk < klo) nv = 0;
       const double* src = nv ? ta.B + gk * ta.ldb + gn : ta.B;
       cp_async16(smem_u32(bs + row * C::B_STR + nc2), src, (int)(nv * 8));
     }
@@ -128,7 +136,7 @@ __device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64
       const int c = tid + C::THREADS * q;
       const int row = c / C::BK, kk = c % C::BK;
       const int64_t gr = ta.m0 + row, gk = k0 + kk;
-      const bool ok = gr < ta.m && gk < kend;
+      const bool ok = gr < ta.m && gk < kend && gk >= klo;
       cp_async8(smem_u32(as + row * C::A_STR + kk), ok ? ta.A + gr * ta.lda + gk : ta.A, ok ? 8 : 0);
     }
 #pragma unroll
@@ -136,7 +144,7 @@ __device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64
       const int c = tid + C::THREADS * q;
       const int row = c / C::BN, nn = c % C::BN;
       const int64_t gk = k0 + row, gn = ta.n0 + nn;
-      const bool ok = gk < kend && gn < ta.nc;
+      const bool ok = gk < kend && gk >= klo && gn < ta.nc;
       cp_async8(smem_u32(bs + row * C::B_STR + nn), ok ? ta.B + gk * ta.ldb + gn : ta.B, ok ? 8 : 0);
     }
   }
@@ -151,10 +159,13 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t ktiles = (kend - kbeg + C::BK - 1) / C::BK;
+  // 16-byte A copies need an even start: begin one early at odd kbeg (masked to zero)
+  const int64_t kbase = (V16 && !G) ? (kbeg & ~int64_t(1)) : kbeg;
+  const int64_t ktiles = (kend - kbase + C::BK - 1) / C::BK;
 #pragma unroll
   for (int s = 0; s < C::STAGES - 1; ++s) {
-    if (s < ktiles) load_stage<C, V16, G>(ta, kbeg + s * C::BK, kend, As + s * C::A_TILE, Bs + s * C::B_TILE);
+    if (s < ktiles)
+      load_stage<C, V16, G>(ta, kbase + s * C::BK, kbeg, kend, As + s * C::A_TILE, Bs + s * C::B_TILE);
     cp_async_commit();
   }
   for (int64_t kt = 0; kt < ktiles; ++kt) {
@@ -163,7 +174,7 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
     const int64_t nt = kt + C::STAGES - 1;
     if (nt < ktiles) {
       const int ns = (int)(nt % C::STAGES);
-      load_stage<C, V16, G>(ta, kbeg + nt * C::BK, kend, As + ns * C::A_TILE, Bs + ns * C::B_TILE);
+      load_stage<C, V16, G>(ta, kbase + nt * C::BK, kbeg, kend, As + ns * C::A_TILE, Bs + ns * C::B_TILE);
     }
     cp_async_commit();
     const int cs = (int)(kt % C::STAGES);
@@ -178,7 +189,7 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
       for (int ni = 0; ni < C::FN; ++ni) b[ni] = bs[kk * C::B_STR + ni * 8];
       if constexpr (G) {
         // this lane's B fragment row is sketch column t = k + kk + t_lane: scale it by s_t^2
-        const int64_t gk = kbeg + kt * C::BK + kk + t;
+        const int64_t gk = kbase + kt * C::BK + kk + t;
         const double sv = gk < kend ? ta.scale[gk] : 0.0;
         const double s2 = __dmul_rn(sv, sv);
 #pragma unroll
@@ -254,7 +265,7 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ part, int64_t sp
 }
 
 // ---- segmented square sums
-template <class C, bool G = false>
+template <class C, bool V16, bool G = false>
 __global__ void __launch_bounds__(C::THREADS) segsq_f64_kernel(const double* __restrict__ A, int64_t lda,
                                                                int64_t strideA, const double* __restrict__ B,
                                                                int64_t ldb, int64_t strideB, int64_t m,
@@ -284,7 +295,7 @@ __global__ void __launch_bounds__(C::THREADS) segsq_f64_kernel(const double* __r
     for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
       for (int ni = 0; ni < C::FN; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-    if (kbeg < kend) mainloop<C, false, G>(ta, kbeg, kend, smem, acc);
+    if (kbeg < kend) mainloop<C, V16, G>(ta, kbeg, kend, smem, acc);
     double sq = 0.0;
 #pragma unroll
     for (int mi = 0; mi < C::FM; ++mi)
@@ -402,7 +413,8 @@ static VariantInfo info_of() {
   if (occ < 0) {
     cudaFuncSetAttribute(gemm_f64_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaFuncSetAttribute(gemm_f64_kernel<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    cudaFuncSetAttribute(segsq_f64_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(segsq_f64_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(segsq_f64_kernel<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     int o = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, gemm_f64_kernel<C, true>, C::THREADS, C::SMEM) !=
             cudaSuccess || o < 1)
@@ -477,22 +489,33 @@ static void launch_gemm(bool v16, dim3 grid, cudaStream_t st, const double* A, i
 }
 
 template <class C>
-static void launch_segsq(dim3 grid, cudaStream_t st, const double* A, int64_t lda, int64_t strideA, const double* B,
-                         int64_t ldb, int64_t strideB, int64_t m, int64_t nc, const int64_t* seg, int64_t nseg,
-                         int64_t seg_stride, int64_t chunks, double* part, const int64_t* col = nullptr,
+static void launch_segsq(bool v16, dim3 grid, cudaStream_t st, const double* A, int64_t lda, int64_t strideA,
+                         const double* B, int64_t ldb, int64_t strideB, int64_t m, int64_t nc, const int64_t* seg,
+                         int64_t nseg, int64_t seg_stride, int64_t chunks, double* part, const int64_t* col = nullptr,
                          const double* scale = nullptr, int64_t w_stride = 0) {
   if (col != nullptr) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(segsq_f64_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      cudaFuncSetAttribute(segsq_f64_kernel<C, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      cudaFuncSetAttribute(segsq_f64_kernel<C, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
       attr = true;
     }
-    segsq_f64_kernel<C, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg,
-                                                                  seg_stride, chunks, part, col, scale, w_stride);
+    if (v16)
+      segsq_f64_kernel<C, true, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg,
+                                                                        nseg, seg_stride, chunks, part, col, scale,
+                                                                        w_stride);
+    else
+      segsq_f64_kernel<C, false, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc,
+                                                                         seg, nseg, seg_stride, chunks, part, col,
+                                                                         scale, w_stride);
     return;
   }
-  segsq_f64_kernel<C><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg,
-                                                          seg_stride, chunks, part, nullptr, nullptr, 0);
+  if (v16)
+    segsq_f64_kernel<C, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg,
+                                                                seg_stride, chunks, part, nullptr, nullptr, 0);
+  else
+    segsq_f64_kernel<C, false><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg,
+                                                                 seg_stride, chunks, part, nullptr, nullptr, 0);
 }
 
 }  // namespace bmm
@@ -591,11 +614,17 @@ static int segsq_impl(const double* A, int64_t lda, int64_t strideA, const doubl
   const int64_t need = tiles * nseg * batch * 8;
   BMM_REQUIRE(ws_bytes >= need && ws != nullptr, BMM_E_ARG, "bmm_segsq_f64: workspace too small");
   BMM_REQUIRE(ceil_div(m, vi.BM) <= 65535, BMM_E_UNSUPPORTED, "bmm_segsq_f64: m too large");
-  const int64_t chunks = segsq_chunks(vi, m, nc, nseg, batch);
+  // partition blocks (no gather): one segment per CTA, the block scheduler balances unequal
+  // segments; gathered pilot segments are short, so a CTA walks several
+  int64_t chunks = col == nullptr ? nseg : segsq_chunks(vi, m, nc, nseg, batch);
+  if (batch * chunks > 65535) chunks = 65535 / batch;
+  const bool v16 = (col != nullptr || ((reinterpret_cast<uintptr_t>(A) % 16 == 0) && lda % 2 == 0 && strideA % 2 == 0)) &&
+                   (reinterpret_cast<uintptr_t>(B) % 16 == 0) && ldb % 2 == 0 && strideB % 2 == 0;
   dim3 grid((unsigned)ceil_div(nc, vi.BN), (unsigned)ceil_div(m, vi.BM), (unsigned)(batch * chunks));
   double* part = (double*)ws;
-#define BMM_SEG_CASE(V) \
-  launch_segsq<V>(grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part, col, scale, w_stride)
+#define BMM_SEG_CASE(V)                                                                                             \
+  launch_segsq<V>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, seg, nseg, seg_stride, chunks, part, col, \
+                  scale, w_stride)
   switch (g_seg_variant) {
     case 1: BMM_SEG_CASE(DV1); break;
     case 2: BMM_SEG_CASE(DV2); break;

@@ -10,7 +10,7 @@ from oracle import blockmm_oracle as O
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 bm = pytest.importorskip("paper_2105_04940_b200")
-from paper_2105_04940_b200.pipeline import SketchPipeline, seeds_from_rngs  # noqa: E402
+from paper_2105_04940_b200.pipeline import PipelineGroup, SketchPipeline, seeds_from_rngs  # noqa: E402
 
 
 def rel(a, b):
@@ -36,6 +36,28 @@ def test_pipeline_matches_oracle(method, graph):
         assert np.array_equal(pipe.columns_host()[0], ref["columns"]), method
         assert np.array_equal(pipe.scales_host()[0], ref["scale"]), method
         assert rel(CD, ref["CD"]) < 1e-12
+
+
+def test_pipeline_group_concurrent_replay_is_bit_identical():
+    """A c x method sweep replayed as one graph with concurrent branches gives
+    exactly the products of the member pipelines run one by one."""
+    M, N, sizes = workloads.cfg2(n=4000, m=60, p=50, K=12)
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    runs = [(c, meth) for c in (200, 400) for meth in ("OPL", "ONC", "ONMCNR", "UU")]
+    solo = [SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs]
+    group = PipelineGroup([SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs])
+    seeds = lambda s: [seeds_from_rngs(meth, [np.random.default_rng(s + i)], len(sizes))  # noqa: E731
+                       for i, (c, meth) in enumerate(runs)]
+    group.run(Md, Nd, seeds(0))
+    group.capture(Md, Nd)
+    assert group.graph_launches > 0
+    for s in (10, 20):
+        outs = [o.clone() for o in group.run(Md, Nd, seeds(s))]
+        group.check()
+        for i, pipe in enumerate(solo):
+            ref = pipe.run(Md, Nd, seeds(s)[i])
+            assert torch.equal(outs[i], ref), runs[i]
+            assert np.array_equal(group.pipes[i].columns_host(), pipe.columns_host())
 
 
 def test_pipeline_ssm_matches_oracle():
