@@ -161,6 +161,17 @@ int bmm_sample(const double* probs, const double* cum, const int64_t* last_suppo
                const uint64_t* states, int64_t* column, double* prob, double* scale,
                void* stream);
 
+/* Monte Carlo replications of ONE plan (analysis.py:343-366 coverage_check,
+ * :390-416 normality_diagnostic; bench.py:258-278 rep loop): as bmm_sample,
+ * but probs/cum/last_support/budgets/col_off describe a single problem shared
+ * by all `reps` replications; states (reps x K streams) and the outputs
+ * (stride w_stride) are per replication.                                    */
+int bmm_sample_reps(const double* probs, const double* cum, const int64_t* last_support,
+                    const int64_t* offsets, int64_t K, int64_t reps, int64_t n, int64_t max_len,
+                    const int64_t* budgets, const int64_t* col_off, int64_t w_stride,
+                    const uint64_t* states, int64_t* column, double* prob, double* scale,
+                    void* stream);
+
 /* ---------------------------------------------------------------- K4 gather
  * C[h, t] = M[h, column[t]] * scale[t]        (m x W, ldc)     estimators.py:79
  * D[t, f] = N[column[t], f] * scale[t]        (W x p, ldd)     estimators.py:80
@@ -233,6 +244,27 @@ int bmm_segsq_f64_gather(const double* M, int64_t ldm, int64_t strideM,
                          int64_t m, int64_t nc, const int64_t* column, const double* scale,
                          int64_t w_stride, const int64_t* seg, int64_t nseg, int64_t seg_stride,
                          int64_t batch, double* gsq, void* ws, int64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- exact variance analytics
+ * (analysis.py:57-116)
+ * var[h, f] = sum_i M[h,i]^2 N[i,f]^2 / (c_k p_i)  -  sum_k (M^k N_k)[h,f]^2 / c_k
+ * over p_i > 0 and c_k > 0 (elementwise_variance, analysis.py:57-90): one
+ * squared-mode DMMA GEMM over the inner dimension, then a segmented GEMM whose
+ * epilogue accumulates weighted squares, subtracted in a fixed chunk order.
+ * budgets are real-valued (the reference allows a real override).  *bad gets
+ * K - k for the first block k with a contributing column of zero probability
+ * (analysis.py:77-79 ValueError), 0 if none.  float64 operands.             */
+int64_t bmm_variance_workspace(int64_t m, int64_t p, int64_t n, int64_t K);
+int bmm_elementwise_variance(const double* M, int64_t ldm, const double* N, int64_t ldn,
+                             int64_t m, int64_t n, int64_t p, const int64_t* offsets, int64_t K,
+                             const double* probs, const double* colsq, const double* rowsq,
+                             const double* budgets, double* var, int64_t ldv, int64_t* bad,
+                             void* ws, int64_t ws_bytes, void* stream);
+/* out[k] = sum over p_i > 0 in block k of (sqrt(colsq_i) sqrt(rowsq_i))^2 / p_i
+ * (expected_sq_error's first term, analysis.py:109); *bad as above
+ * (analysis.py:105-107).                                                    */
+int bmm_block_term1(const double* probs, const double* colsq, const double* rowsq,
+                    const int64_t* offsets, int64_t K, double* out, int64_t* bad, void* stream);
 
 /* ---------------------------------------------------------------- K9 error
  * err[b] = { sum (X - Y)^2, sum X^2 } over m x nc (X = exact MN, Y = C D),

@@ -24,6 +24,8 @@ It restates, as plain functions over arrays, the reference package
   two-step         estimators.py:185-210
   SSM estimate     estimators.py:221-253
   relative error   analysis.py:318-325
+  replications     analysis.py:343-366,390-416   (Monte Carlo, §8 f1)
+  variance         analysis.py:57-116            (exact analytics, §8 f2)
 
 Randomness uses numpy's own Generator/PCG64 -- the reference's third-party
 dependency -- so streams are the reference's by construction; the restated
@@ -371,3 +373,69 @@ def frob_errors(exact: np.ndarray, approx: np.ndarray) -> tuple:
     d = (exact - approx).ravel()
     e = exact.ravel()
     return float(d @ d), float(e @ e)
+
+
+# ---------------------------------------------------------------- §8(f): Monte Carlo and analytics
+
+def replicate(M, N, sizes, probs_flat, budgets, rng: np.random.Generator, reps: int, entry=None) -> dict:
+    """``reps`` replications of estimate_product under one plan on
+    ``rng.spawn(reps)`` (analysis.py:359-362, 412-413): per replication the
+    drawn columns, ||CD - MN||_F^2 (reference: frobenius_norm(...)**2) and
+    optionally CD[entry]."""
+    K = len(sizes)
+    exact = M @ N
+    cols, sq, ent = [], [], []
+    for stream in rng.spawn(reps):
+        c, _, _, C, D = sketch(M, N, sizes, probs_flat, budgets, stream.spawn(K))
+        CD = C @ D
+        d = (CD - exact).ravel()
+        sq.append(float(np.sqrt(d @ d)) ** 2)
+        cols.append(c)
+        if entry is not None:
+            ent.append(CD[entry])
+    return {"columns": np.array(cols), "sq_error": np.array(sq), "entry": np.array(ent)}
+
+
+def elementwise_variance(M, N, sizes, probs_flat, budgets) -> np.ndarray:
+    """analysis.py:57-90 (validation errors included)."""
+    off = offsets_of(sizes)
+    b = np.asarray(budgets, dtype=np.float64)
+    var = np.zeros((M.shape[0], N.shape[1]))
+    for k in range(len(sizes)):
+        Mk, Nk = M[:, off[k]:off[k + 1]], N[off[k]:off[k + 1]]
+        p = probs_flat[off[k]:off[k + 1]]
+        contrib = np.sqrt((Mk * Mk).sum(axis=0)) * np.sqrt((Nk * Nk).sum(axis=1))
+        pos = p > 0
+        if (contrib[~pos] > 0).any():
+            raise ValueError(f"block {k}: zero probability at a contributing column")
+        exact_sq = (Mk @ Nk) ** 2
+        term1 = (Mk[:, pos] ** 2 / p[pos]) @ (Nk[pos, :] ** 2)
+        num = term1 - exact_sq
+        if b[k] == 0:
+            if np.abs(num).max(initial=0.0) > 1e-12 * max(1.0, float(term1.max(initial=0.0))):
+                raise ValueError(f"block {k}: zero budget on a block with sampling variance")
+            continue
+        var += num / b[k]
+    return var
+
+
+def expected_sq_error(M, N, sizes, probs_flat, budgets) -> float:
+    """analysis.py:93-116."""
+    off = offsets_of(sizes)
+    b = np.asarray(budgets, dtype=np.float64)
+    total = 0.0
+    for k in range(len(sizes)):
+        Mk, Nk = M[:, off[k]:off[k + 1]], N[off[k]:off[k + 1]]
+        p = probs_flat[off[k]:off[k + 1]]
+        contrib = np.linalg.norm(Mk, axis=0) * np.linalg.norm(Nk, axis=1)
+        pos = p > 0
+        if (contrib[~pos] > 0).any():
+            raise ValueError(f"block {k}: zero probability at a contributing column")
+        term1 = float((contrib[pos] ** 2 / p[pos]).sum())
+        num = term1 - float(((Mk @ Nk) ** 2).sum())
+        if b[k] == 0:
+            if abs(num) > 1e-12 * max(1.0, term1):
+                raise ValueError(f"block {k}: zero budget on a block with sampling variance")
+            continue
+        total += num / b[k]
+    return total

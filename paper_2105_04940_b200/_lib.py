@@ -49,6 +49,7 @@ SIGNATURES = {
     "bmm_block_cdf": (_I, [_P, _P, _I64, _I64, _I64, _P, _P, _P]),
     "bmm_seed_streams": (_I, [_P, _I64, _P, _I64, _I64, _P, _P]),
     "bmm_sample": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
+    "bmm_sample_reps": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "bmm_gather": (_I, [_I, _I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _I64,
                         _P, _I64, _I64, _P, _I64, _I64, _P]),
     "bmm_gather_blocks": (_I, [_I, _P, _I64, _P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64,
@@ -64,6 +65,10 @@ SIGNATURES = {
     "bmm_segsq_f64_workspace": (_I64, [_I64, _I64, _I64, _I64]),
     "bmm_segsq_f64": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P,
                            _P, _I64, _P]),
+    "bmm_variance_workspace": (_I64, [_I64, _I64, _I64, _I64]),
+    "bmm_elementwise_variance": (_I, [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _P, _P, _P, _I64,
+                                      _P, _P, _I64, _P]),
+    "bmm_block_term1": (_I, [_P, _P, _P, _P, _I64, _P, _P, _P]),
     "bmm_sqdiff_workspace": (_I64, [_I64, _I64, _I64]),
     "bmm_sqdiff": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P]),
     "bmm_pairwise_sum": (_I, [_P, _I64, _I64, _I64, _P, _P]),

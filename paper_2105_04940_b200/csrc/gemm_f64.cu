@@ -61,6 +61,9 @@ struct TileArgs {
   // scale[t]^2 -- C @ D without materialising the sketch.
   const int64_t* col = nullptr;
   const double* scale = nullptr;
+  // squared mode (SQ): A and B elements are squared and B row k is weighted
+  // by wk[k] -- sum_k A[h,k]^2 B[k,f]^2 w_k (elementwise variance, term 1)
+  const double* wk = nullptr;
 };
 
 // Stage one BK slice [k0, k0+BK) of the A and B tiles; inner indices outside [klo, kend) are zero
@@ -151,7 +154,7 @@ __device__ __forceinline__ void load_stage(const TileArgs& ta, int64_t k0, int64
 }
 
 // acc += A[m0:+BM, kbeg:kend] @ B[kbeg:kend, n0:+BN]
-template <class C, bool V16, bool G = false>
+template <class C, bool V16, bool G = false, bool SQ = false>
 __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64_t kend, double* smem,
                                          double (&acc)[C::FM][C::FN][2]) {
   double* As = smem;
@@ -195,6 +198,14 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
 #pragma unroll
         for (int ni = 0; ni < C::FN; ++ni) b[ni] = __dmul_rn(b[ni], s2);
       }
+      if constexpr (SQ) {
+        const int64_t gk = kbase + kt * C::BK + kk + t;
+        const double wv = (gk >= kbeg && gk < kend) ? ta.wk[gk] : 0.0;
+#pragma unroll
+        for (int mi = 0; mi < C::FM; ++mi) a[mi] = __dmul_rn(a[mi], a[mi]);
+#pragma unroll
+        for (int ni = 0; ni < C::FN; ++ni) b[ni] = __dmul_rn(__dmul_rn(b[ni], b[ni]), wv);
+      }
 #pragma unroll
       for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
@@ -205,7 +216,7 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
   __syncthreads();
 }
 
-template <class C, bool V16, bool G = false>
+template <class C, bool V16, bool G = false, bool SQ = false>
 __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __restrict__ A, int64_t lda,
                                                               int64_t strideA, const double* __restrict__ B,
                                                               int64_t ldb, int64_t strideB, int64_t m, int64_t nc,
@@ -223,6 +234,7 @@ __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __re
     ta.col = col + b * w_stride;
     ta.scale = scale + b * w_stride;
   }
+  if constexpr (SQ) ta.wk = scale + b * w_stride;
   const int64_t kbeg = sp * kchunk;
   const int64_t kend = min(k, kbeg + kchunk);
   double acc[C::FM][C::FN][2];
@@ -230,7 +242,7 @@ __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __re
   for (int mi = 0; mi < C::FM; ++mi)
 #pragma unroll
     for (int ni = 0; ni < C::FN; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  if (kbeg < kend) mainloop<C, V16, G>(ta, kbeg, kend, smem, acc);
+  if (kbeg < kend) mainloop<C, V16, G, SQ>(ta, kbeg, kend, smem, acc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N, g = lane >> 2, t = lane & 3;
   double* dst;
@@ -325,6 +337,113 @@ __global__ void segsq_reduce_kernel(const double* __restrict__ part, int64_t til
     double acc = 0.0;
     for (int64_t i = 0; i < tiles; ++i) acc += p[i];
     gsq[g] = acc;
+  }
+}
+
+// ---- segmented weighted squares into a matrix: part[ch] = sum_{j in chunk ch} w_j (A_j B_j)^2
+// (elementwise variance, term 2: sum_k (M^k N_k)^2 / c_k;  analysis.py:82-89)
+template <class C, bool V16>
+__global__ void __launch_bounds__(C::THREADS) segsq_mat_kernel(const double* __restrict__ A, int64_t lda,
+                                                               const double* __restrict__ B, int64_t ldb, int64_t m,
+                                                               int64_t nc, const int64_t* __restrict__ seg,
+                                                               int64_t nseg, const double* __restrict__ wseg,
+                                                               int64_t chunks, double* __restrict__ part) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t ch = blockIdx.z;
+  const int64_t per = (nseg + chunks - 1) / chunks;
+  const int64_t j0 = ch * per, j1 = min(nseg, j0 + per);
+  TileArgs ta{A, lda, B, ldb, m, nc, (int64_t)blockIdx.y * C::BM, (int64_t)blockIdx.x * C::BN};
+  double sq[C::FM][C::FN][2];
+#pragma unroll
+  for (int mi = 0; mi < C::FM; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < C::FN; ++ni) sq[mi][ni][0] = sq[mi][ni][1] = 0.0;
+  for (int64_t j = j0; j < j1; ++j) {
+    const double w = wseg[j];
+    const int64_t kbeg = seg[j], kend = seg[j + 1];
+    if (w == 0.0 || kbeg >= kend) continue;
+    double acc[C::FM][C::FN][2];
+#pragma unroll
+    for (int mi = 0; mi < C::FM; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < C::FN; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    mainloop<C, V16>(ta, kbeg, kend, smem, acc);
+#pragma unroll
+    for (int mi = 0; mi < C::FM; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < C::FN; ++ni) {
+        sq[mi][ni][0] = fma(w, acc[mi][ni][0] * acc[mi][ni][0], sq[mi][ni][0]);
+        sq[mi][ni][1] = fma(w, acc[mi][ni][1] * acc[mi][ni][1], sq[mi][ni][1]);
+      }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N, g = lane >> 2, t = lane & 3;
+  double* dst = part + ch * m * nc;
+#pragma unroll
+  for (int mi = 0; mi < C::FM; ++mi) {
+    const int64_t r = ta.m0 + wm * C::WM + mi * 8 + g;
+    if (r >= m) continue;
+#pragma unroll
+    for (int ni = 0; ni < C::FN; ++ni) {
+      const int64_t c0 = ta.n0 + wn * C::WN + ni * 8 + 2 * t;
+      if (c0 < nc) dst[r * nc + c0] = sq[mi][ni][0];
+      if (c0 + 1 < nc) dst[r * nc + c0 + 1] = sq[mi][ni][1];
+    }
+  }
+}
+
+// out[r, c] -= sum over chunks of part[ch][r, c], chunks in order
+__global__ void sub_chunks_kernel(const double* __restrict__ part, int64_t chunks, int64_t m, int64_t nc,
+                                  double* __restrict__ out, int64_t ldo) {
+  const int64_t per = m * nc;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = part[e];
+    for (int64_t c = 1; c < chunks; ++c) acc = __dadd_rn(acc, part[c * per + e]);
+    const int64_t r = e / nc, c = e - r * nc;
+    out[r * ldo + c] = __dsub_rn(out[r * ldo + c], acc);
+  }
+}
+
+// variance weights: w_col[i] = 1 / (c_k p_i) where p_i > 0 and c_k > 0 (else 0),
+// w_blk[k] = 1 / c_k (else 0); bad[0] = first block with a contributing column
+// (sqrt(colsq) sqrt(rowsq) > 0) of zero probability, as K - k (0: none)   analysis.py:77-79
+__global__ void variance_weights_kernel(const double* __restrict__ probs, const double* __restrict__ colsq,
+                                        const double* __restrict__ rowsq, const int64_t* __restrict__ offsets,
+                                        int64_t K, const double* __restrict__ budgets, double* __restrict__ w_col,
+                                        double* __restrict__ w_blk, int64_t* __restrict__ bad) {
+  const int64_t n = offsets[K];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = K;  // block k with offsets[k] <= i < offsets[k+1]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (offsets[mid] <= i) lo = mid; else hi = mid;
+    }
+    const double p = probs[i], ck = budgets[lo];
+    w_col[i] = (p > 0.0 && ck > 0.0) ? __ddiv_rn(1.0, __dmul_rn(ck, p)) : 0.0;
+    if (!(p > 0.0) && __dmul_rn(__dsqrt_rn(colsq[i]), __dsqrt_rn(rowsq[i])) > 0.0)
+      atomicMax(reinterpret_cast<unsigned long long*>(bad), (unsigned long long)(K - lo));  // K - first block
+    if (i == offsets[lo]) w_blk[lo] = ck > 0.0 ? __ddiv_rn(1.0, ck) : 0.0;
+  }
+}
+
+// per block sum over p_i > 0 of sc_i^2 / p_i  (expected_sq_error term 1,
+// analysis.py:109); warp per block, fixed lane order
+__global__ void block_term1_kernel(const double* __restrict__ probs, const double* __restrict__ colsq,
+                                   const double* __restrict__ rowsq, const int64_t* __restrict__ offsets, int64_t K,
+                                   double* __restrict__ out, int64_t* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < K;
+       k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double acc = 0.0;
+    for (int64_t i = offsets[k] + lane; i < offsets[k + 1]; i += 32) {
+      const double p = probs[i];
+      const double sc = __dmul_rn(__dsqrt_rn(colsq[i]), __dsqrt_rn(rowsq[i]));
+      if (p > 0.0) acc = __dadd_rn(acc, __ddiv_rn(__dmul_rn(sc, sc), p));
+      else if (sc > 0.0) atomicMax(reinterpret_cast<unsigned long long*>(bad), (unsigned long long)(K - k));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) out[k] = acc;
   }
 }
 
@@ -684,5 +803,110 @@ extern "C" int bmm_sqdiff(int dtype, const void* X, int64_t ldx, int64_t strideX
   BMM_CHECK_LAUNCH("sqdiff_kernel");
   sqdiff_final_kernel<<<grid_for(batch, 64), 64, 0, st>>>((const double*)ws, parts, batch, err);
   BMM_CHECK_LAUNCH("sqdiff_final_kernel");
+  return BMM_OK;
+}
+
+// ---- exact variance analytics: analysis.py:57-116
+namespace bmm {
+using VarCfg = DV2;     // term 1 GEMM tiles
+using VarSegCfg = DV0;  // term 2: the square accumulators double the register tile, so 32x32 warp tiles
+
+inline int64_t var_chunks(int64_t m, int64_t p, int64_t K) {
+  const VariantInfo vi = variant_info(0);
+  const int64_t tiles = ceil_div(m, vi.BM) * ceil_div(p, vi.BN);
+  int64_t ch = ((int64_t)vi.occ * 148) / tiles;
+  if (ch > K) ch = K;
+  if (ch > 64) ch = 64;
+  if (ch < 1) ch = 1;
+  return ch;
+}
+
+inline int64_t var_ws_head(int64_t n, int64_t K) { return ceil_div(8 * (n + K), 256) * 256; }
+}  // namespace bmm
+
+extern "C" int64_t bmm_variance_workspace(int64_t m, int64_t p, int64_t n, int64_t K) {
+  const SplitPlan sp = plan_split(variant_info(2), m, p, n, 1);
+  const int64_t gemm_need = sp.splits > 1 ? sp.splits * m * p * 8 : 0;
+  const int64_t seg_need = var_chunks(m, p, K) * m * p * 8;
+  return var_ws_head(n, K) + std::max(gemm_need, seg_need);
+}
+
+extern "C" int bmm_elementwise_variance(const double* M, int64_t ldm, const double* N, int64_t ldn, int64_t m,
+                                        int64_t n, int64_t p, const int64_t* offsets, int64_t K,
+                                        const double* probs, const double* colsq, const double* rowsq,
+                                        const double* budgets, double* var, int64_t ldv, int64_t* bad, void* ws,
+                                        int64_t ws_bytes, void* stream) {
+  BMM_REQUIRE(m >= 1 && n >= 1 && p >= 1 && K >= 1 && var != nullptr && bad != nullptr, BMM_E_ARG,
+              "bmm_elementwise_variance: bad arguments");
+  const int64_t need = bmm_variance_workspace(m, p, n, K);
+  BMM_REQUIRE(ws != nullptr && ws_bytes >= need, BMM_E_ARG, "bmm_elementwise_variance: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  double* w_col = (double*)ws;
+  double* w_blk = w_col + n;
+  double* part = (double*)((char*)ws + var_ws_head(n, K));
+  if (cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess) {
+    set_error("bmm_elementwise_variance: memset failed");
+    return BMM_E_CUDA;
+  }
+  variance_weights_kernel<<<grid_for(n, 256), 256, 0, st>>>(probs, colsq, rowsq, offsets, K, budgets, w_col, w_blk,
+                                                            bad);
+  BMM_CHECK_LAUNCH("variance_weights_kernel");
+  // term 1: sum_i M_hi^2 N_if^2 / (c_k p_i)  (one squared-mode GEMM over the whole inner dimension)
+  const VariantInfo vi = variant_info(2);
+  const SplitPlan sp = plan_split(vi, m, p, n, 1);
+  const bool v16 = (reinterpret_cast<uintptr_t>(M) % 16 == 0) && ldm % 2 == 0 &&
+                   (reinterpret_cast<uintptr_t>(N) % 16 == 0) && ldn % 2 == 0;
+  {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_f64_kernel<VarCfg, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           VarCfg::SMEM);
+      cudaFuncSetAttribute(gemm_f64_kernel<VarCfg, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           VarCfg::SMEM);
+      cudaFuncSetAttribute(segsq_mat_kernel<VarSegCfg, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           VarSegCfg::SMEM);
+      cudaFuncSetAttribute(segsq_mat_kernel<VarSegCfg, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           VarSegCfg::SMEM);
+      attr = true;
+    }
+  }
+  dim3 grid((unsigned)ceil_div(p, vi.BN), (unsigned)ceil_div(m, vi.BM), (unsigned)sp.splits);
+  if (v16)
+    gemm_f64_kernel<VarCfg, true, false, true><<<grid, VarCfg::THREADS, VarCfg::SMEM, st>>>(
+        M, ldm, 0, N, ldn, 0, m, p, n, sp.splits, sp.kchunk, var, ldv, 0, part, nullptr, w_col, 0);
+  else
+    gemm_f64_kernel<VarCfg, false, false, true><<<grid, VarCfg::THREADS, VarCfg::SMEM, st>>>(
+        M, ldm, 0, N, ldn, 0, m, p, n, sp.splits, sp.kchunk, var, ldv, 0, part, nullptr, w_col, 0);
+  BMM_CHECK_LAUNCH("gemm_f64_kernel(sq)");
+  if (sp.splits > 1) {
+    splitk_reduce_kernel<<<grid_for(m * p, 256), 256, 0, st>>>(part, sp.splits, m, p, 1, var, ldv, 0);
+    BMM_CHECK_LAUNCH("splitk_reduce_kernel");
+  }
+  // term 2: sum_k (M^k N_k)^2 / c_k, subtracted in chunk order
+  const int64_t chunks = var_chunks(m, p, K);
+  dim3 g2((unsigned)ceil_div(p, VarSegCfg::BN), (unsigned)ceil_div(m, VarSegCfg::BM), (unsigned)chunks);
+  if (v16)
+    segsq_mat_kernel<VarSegCfg, true><<<g2, VarSegCfg::THREADS, VarSegCfg::SMEM, st>>>(M, ldm, N, ldn, m, p, offsets,
+                                                                                       K, w_blk, chunks, part);
+  else
+    segsq_mat_kernel<VarSegCfg, false><<<g2, VarSegCfg::THREADS, VarSegCfg::SMEM, st>>>(M, ldm, N, ldn, m, p,
+                                                                                        offsets, K, w_blk, chunks,
+                                                                                        part);
+  BMM_CHECK_LAUNCH("segsq_mat_kernel");
+  sub_chunks_kernel<<<grid_for(m * p, 256), 256, 0, st>>>(part, chunks, m, p, var, ldv);
+  BMM_CHECK_LAUNCH("sub_chunks_kernel");
+  return BMM_OK;
+}
+
+extern "C" int bmm_block_term1(const double* probs, const double* colsq, const double* rowsq, const int64_t* offsets,
+                               int64_t K, double* out, int64_t* bad, void* stream) {
+  BMM_REQUIRE(K >= 1 && out != nullptr && bad != nullptr, BMM_E_ARG, "bmm_block_term1: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  if (cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess) {
+    set_error("bmm_block_term1: memset failed");
+    return BMM_E_CUDA;
+  }
+  block_term1_kernel<<<grid_for(K * 32, 256), 256, 0, st>>>(probs, colsq, rowsq, offsets, K, out, bad);
+  BMM_CHECK_LAUNCH("block_term1_kernel");
   return BMM_OK;
 }

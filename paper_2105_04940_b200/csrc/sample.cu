@@ -53,7 +53,9 @@ constexpr int kSampleWarps = 4;
 
 // One warp per block.  SMEM: the block's CDF is staged in shared memory
 // (max_len doubles per warp) so the binary searches stay on chip.
-template <bool SMEM>
+// SHARED: one plan (probs, cum, last, budgets, col_off) for every problem b --
+// Monte Carlo replications; only the streams and outputs are per problem.
+template <bool SMEM, bool SHARED = false>
 __global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
     const double* __restrict__ probs, const double* __restrict__ cum,
     const int64_t* __restrict__ last, const int64_t* __restrict__ offsets, int64_t K, int64_t batch,
@@ -69,11 +71,13 @@ __global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
   const int64_t warps_total = K * batch;
   for (int64_t g = blockIdx.x * (int64_t)wpb + w; g < warps_total; g += (int64_t)gridDim.x * wpb) {
     const int64_t b = g / K, k = g - b * K;
-    const int64_t ck = budgets[g];
+    const int64_t pb_ = SHARED ? 0 : b;  // plan index
+    const int64_t gp = pb_ * K + k;
+    const int64_t ck = budgets[gp];
     if (ck <= 0) continue;
     const int64_t o = offsets[k], len = offsets[k + 1] - o;
-    const double* cb = cum + b * n + o;
-    const double* pb = probs + b * n + o;
+    const double* cb = cum + pb_ * n + o;
+    const double* pb = probs + pb_ * n + o;
     if (SMEM) {
       __syncwarp();
       for (int64_t i = lane; i < len; i += 32) {
@@ -84,7 +88,7 @@ __global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
       cb = scum;
       pb = sprob;
     }
-    const int64_t lst = last[g];
+    const int64_t lst = last[gp];
     const uint64_t* sp = states + 4 * g;
     U128 st{sp[0], sp[1]}, inc{sp[2], sp[3]};
     U128 m1, p1, m32, p32;
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
     pcg_jump(32, inc, m32, p32);
     st = add128(mul128(m1, st), p1);
     const double dck = (double)ck;
-    const int64_t t0 = col_off[b * (K + 1) + k];
+    const int64_t t0 = col_off[pb_ * (K + 1) + k];
     for (int64_t j = lane; j < ck; j += 32) {
       const double u = u53(pcg_output(st));
       // first index with cum > u  (searchsorted side="right")
@@ -230,14 +234,13 @@ extern "C" int bmm_seed_streams(const uint32_t* words, int64_t n_words, const in
   return BMM_OK;
 }
 
-extern "C" int bmm_sample(const double* probs, const double* cum, const int64_t* last_support,
-                          const int64_t* offsets, int64_t K, int64_t batch, int64_t n, int64_t max_len,
-                          const int64_t* budgets, const int64_t* col_off, int64_t w_stride,
-                          const uint64_t* states, int64_t* column, double* prob, double* scale,
-                          void* stream) {
+template <bool SHARED>
+static int sample_impl(const double* probs, const double* cum, const int64_t* last_support, const int64_t* offsets,
+                       int64_t K, int64_t batch, int64_t n, int64_t max_len, const int64_t* budgets,
+                       const int64_t* col_off, int64_t w_stride, const uint64_t* states, int64_t* column,
+                       double* prob, double* scale, cudaStream_t st) {
   BMM_REQUIRE(K >= 1 && batch >= 1 && max_len >= 1, BMM_E_ARG, "bmm_sample: bad shape");
   const int64_t warps = K * batch;
-  cudaStream_t st = as_stream(stream);
   const int64_t per_warp = 2 * max_len * 8;  // CDF and probabilities
   int wpb = kSampleWarps;
   bool smem = true;
@@ -248,19 +251,37 @@ extern "C" int bmm_sample(const double* probs, const double* cum, const int64_t*
     const int bytes = (int)(per_warp * wpb);
     static int attr = 0;
     if (bytes > 48 * 1024 && bytes > attr) {
-      cudaFuncSetAttribute(sample_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(sample_kernel<true, SHARED>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = 200 * 1024;
     }
-    sample_kernel<true><<<(unsigned)blocks, 32 * kSampleWarps, bytes, st>>>(
+    sample_kernel<true, SHARED><<<(unsigned)blocks, 32 * kSampleWarps, bytes, st>>>(
         probs, cum, last_support, offsets, K, batch, n, budgets, col_off, w_stride, states, column, prob, scale,
         max_len, wpb);
   } else {
-    sample_kernel<false><<<(unsigned)blocks, 32 * kSampleWarps, 0, st>>>(
+    sample_kernel<false, SHARED><<<(unsigned)blocks, 32 * kSampleWarps, 0, st>>>(
         probs, cum, last_support, offsets, K, batch, n, budgets, col_off, w_stride, states, column, prob, scale,
         max_len, wpb);
   }
   BMM_CHECK_LAUNCH("sample_kernel");
   return BMM_OK;
+}
+
+extern "C" int bmm_sample(const double* probs, const double* cum, const int64_t* last_support,
+                          const int64_t* offsets, int64_t K, int64_t batch, int64_t n, int64_t max_len,
+                          const int64_t* budgets, const int64_t* col_off, int64_t w_stride,
+                          const uint64_t* states, int64_t* column, double* prob, double* scale,
+                          void* stream) {
+  return sample_impl<false>(probs, cum, last_support, offsets, K, batch, n, max_len, budgets, col_off, w_stride,
+                            states, column, prob, scale, as_stream(stream));
+}
+
+extern "C" int bmm_sample_reps(const double* probs, const double* cum, const int64_t* last_support,
+                               const int64_t* offsets, int64_t K, int64_t reps, int64_t n, int64_t max_len,
+                               const int64_t* budgets, const int64_t* col_off, int64_t w_stride,
+                               const uint64_t* states, int64_t* column, double* prob, double* scale,
+                               void* stream) {
+  return sample_impl<true>(probs, cum, last_support, offsets, K, reps, n, max_len, budgets, col_off, w_stride,
+                           states, column, prob, scale, as_stream(stream));
 }
 
 extern "C" int bmm_gather(int dtype, int out_dtype, const void* M, int64_t ldm, int64_t strideM,

@@ -2,7 +2,7 @@
 
 cfg5-shaped float32 batch (512 problems, ONC, W=1024): norms, plan, sampler,
 split gather, tcgen05 3xTF32 GEMM; cfg2-shaped float64 ONC at W=16000:
-norms, plan, sampler, gather, DMMA GEMM.
+norms, plan, sampler, gather, DMMA GEMM; cfg2 OPL: segmented square sums.
 """
 import sys
 from pathlib import Path
@@ -28,5 +28,8 @@ Md, Nd = torch.as_tensor(M2, device="cuda"), torch.as_tensor(N2, device="cuda")
 pipe2 = SketchPipeline(500, 20000, 500, sizes, 16000, "ONC")
 pipe2.run(Md, Nd, seeds_from_rngs("ONC", [workloads.sample_rng(2, 40)], len(sizes)))
 pipe2.check()
+pipe3 = SketchPipeline(500, 20000, 500, sizes, 16000, "OPL")  # + segmented square sums (g_k)
+pipe3.run(Md, Nd, seeds_from_rngs("OPL", [workloads.sample_rng(2, 40)], len(sizes)))
+pipe3.check()
 torch.cuda.synchronize()
 print("profile_kernels ok")

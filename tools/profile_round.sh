@@ -1,0 +1,17 @@
+#!/bin/bash
+# One profiling pass on the GPU box (run under gpurun from the repo root):
+#   1. the default bench line (plain run), then the launch list of the same command under ncu
+#   2. a full ncu capture of the hot kernels at profiling sizes (tools/profile_kernels.py)
+# Outputs land in gpurun_out/; copy the summaries worth keeping into profiles/.
+set -u
+TAG=${1:-r1}
+mkdir -p gpurun_out
+python bench.py --steps 5 --warmup 3 > gpurun_out/${TAG}_bench_plain.log 2>&1 &&
+ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+    --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 5 --warmup 3 > gpurun_out/${TAG}_ncu_launch.log 2>&1
+echo "launch list rc=$?"
+python tools/profile_kernels.py > gpurun_out/${TAG}_pk_plain.log 2>&1 &&
+ncu --set full --clock-control none --import-source on \
+    -k regex:'gemm_f64_kernel|segsq_f64_kernel|colsq|rowsq|gemm_f32split|gather' -c 14 \
+    -o gpurun_out/${TAG}_full python tools/profile_kernels.py > gpurun_out/${TAG}_ncu_full.log 2>&1
+echo "full capture rc=$?"
