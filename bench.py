@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "mc"])
+    ap.add_argument("--reps", type=int, default=1000, help="replications per step (--workload mc)")
     return ap.parse_args()
 
 
@@ -273,8 +274,9 @@ def run_ours(args):
     # errors of the W=16000 ONC product vs the exact product (verification, untimed)
     from paper_2105_04940_b200.analysis import sq_diff
     exact = bm.multiply_exact(Md, Nd)
-    idx = [i for i, r in enumerate(runs) if r[2] == "ONC"][-1]
-    CD = pipes[idx].run(Md, Nd, seeds_from_rngs("ONC", [workloads.sample_rng(cfg, runs[idx][0])], K))
+    idx = len(runs) - 1  # the widest product of the sweep
+    meth_e = runs[idx][2]
+    CD = pipes[idx].run(Md, Nd, seeds_from_rngs(meth_e, [workloads.sample_rng(cfg, runs[idx][0])], K))
     err_sq, ref_sq = sq_diff(exact, CD)
     fro_m = np.linalg.norm(M_h)
     fro_n = np.linalg.norm(N_h)
@@ -599,8 +601,105 @@ def run_device(args):
     return 0
 
 
+def run_mc(args):
+    """--workload mc: the Monte Carlo replication engine --
+    coverage_check_plan's replications of one config-1 OPL plan (W=2000):
+    a step is `reps` replications of estimate_product + their squared errors."""
+    import torch
+    import paper_2105_04940_b200 as bm
+    from paper_2105_04940_b200 import _lib
+    from paper_2105_04940_b200.montecarlo import ReplicationEngine, coverage_check_plan
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    M_h, N_h, sizes = workloads.cfg1()
+    m, n = M_h.shape
+    p = N_h.shape[1]
+    K, W, R = len(sizes), 2000, int(args.reps)
+    Md, Nd = torch.as_tensor(M_h, device="cuda"), torch.as_tensor(N_h, device="cuda")
+    part = bm.BlockPartition(sizes)
+    plan = bm.allocate_optimal(Md, Nd, part, W)
+    eng = ReplicationEngine(Md, Nd, plan)
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    rng_of = lambda i: np.random.default_rng(np.random.SeedSequence(workloads.ROOT, spawn_key=(1, 2, i)))  # noqa: E731
+    n0 = _lib.launches()
+    eng.run(rng_of(0), R)
+    launches = _lib.launches() - n0
+    for i in range(args.warmup):
+        eng.run(rng_of(1 + i), R)
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler() as clocks:
+        for i in range(args.steps):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            eng.run(rng_of(100 + i), R)
+            e1.record()
+            times.append((e0, e1))
+        torch.cuda.synchronize()
+    ms_step = float(np.mean([a.elapsed_time(b) for a, b in times]))
+    # e2e through the public API with host (numpy) inputs: coverage_check_plan
+    err = eng.run(rng_of(7), R)["sq_error"]
+    bound = float(err.quantile(0.9).item())
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        coverage_check_plan(M_h, N_h, plan, bound, R, rng_of(200 + i))
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e.append((time.perf_counter() - t0) * 1e3)
+    # dominant kernel: the batched C_r @ D_r (DMMA), timed on the engine's last chunk
+    lib, st = _lib.load(), _lib.stream_ptr()
+    b = eng.last_chunk
+    Rc = b["reps"]
+    gms = []
+    for _ in range(5):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.bmm_gemm_f64(b["C"].data_ptr(), W, m * W, b["D"].data_ptr(), p, W * p, m, p, W, Rc, b["CD"].data_ptr(),
+                         p, m * p, b["ws_gemm"].data_ptr(), b["ws_gemm"].numel(), st)
+        e1.record()
+        torch.cuda.synchronize()
+        gms.append(e0.elapsed_time(e1))
+    gemm_ms = float(np.median(gms))
+    flops = 2.0 * m * p * W * Rc
+    dgemm_peak = measure_dgemm_peak(torch)
+    # CPU baseline: the oracle's replication loop on a bounded sample, scaled to R
+    from oracle import blockmm_oracle as O
+    sample = 20
+    t0 = time.perf_counter()
+    O.replicate(M_h, N_h, sizes, plan.probs.flat(), plan.budgets, rng_of(300), sample)
+    cpu_ms = (time.perf_counter() - t0) * 1e3 * R / sample
+    line = {
+        "metric": "Monte Carlo replications (coverage_check_plan): time per step of R replications",
+        "value": ms_step, "unit": f"ms/{R} replications", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (config 1, SURVEY.md §8(d))",
+        "config": {"workload": "mc", "base": "cfg1", "m": m, "n": n, "p": p, "K": K, "W": W, "method": "OPL",
+                   "reps_per_step": R, "l2": "flushed (256 MB write) before each step"},
+        "e2e": {"value": float(np.mean(e2e)), "unit": f"ms/{R} replications",
+                "h2d_bytes_per_step": int(M_h.nbytes + N_h.nbytes), "d2h_bytes_per_step": 8,
+                "api": "coverage_check_plan(M, N, plan, bound, reps, rng) on numpy inputs"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "kernel": "gemm_f64_kernel (batched C_r.D_r, DMMA)",
+                     "achieved": flops / (gemm_ms * 1e-3) / 1e12, "peak": dgemm_peak, "unit": "TFLOP/s",
+                     "frac": flops / (gemm_ms * 1e-3) / 1e12 / dgemm_peak,
+                     "peak_source": "cuBLAS dgemm 8192^3 measured in this run", "traffic": None},
+        "kernel_ms": {"gemm_batched_ms": gemm_ms},
+        "cpu_baseline": {"value": cpu_ms, "unit": f"ms/{R} replications", "cores": cpu_cores(), "kind": "port",
+                         "sample": f"{sample} replications with oracle.replicate (NumPy + OpenBLAS), scaled to {R}"},
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    if args.workload == "mc":
+        return run_mc(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "cfg4" and int(os.environ.get("WORLD_SIZE", "1")) > 1:

@@ -169,6 +169,8 @@ class ReplicationEngine:
                 out["entry"][r0:r0 + Rc] = CD.view(R, m, p)[:Rc, h, f]
             if keep_columns:
                 out["columns"][r0:r0 + Rc] = column.view(R, W)[:Rc]
+        # the last chunk's device buffers (for kernel timing / inspection)
+        self.last_chunk = {"C": C, "D": D, "CD": CD, "ws_gemm": ws_g, "reps": Rc, "column": column, "scale": scale}
         return out
 
 
