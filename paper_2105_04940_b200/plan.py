@@ -14,8 +14,9 @@ frozen records the reference returns.
 """
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass
-from typing import Optional
+from typing import NamedTuple, Optional
 
 import numpy as np
 import torch
@@ -427,3 +428,77 @@ def inst_block_q(inst: DeviceInstance):
     status = torch.empty(1, dtype=torch.int32, device=f.device)
     _lib.call("bmm_normalize", _lib.ptr(f), inst.K, 1, _lib.ptr(q), _lib.ptr(status), _lib.stream_ptr())
     return q, int(status.item())
+
+
+# ---------------------------------------------------------------- plan documents
+
+class FloorRatio(NamedTuple):
+    """plan.py:215-217."""
+
+    ratio: float
+    support_mismatch: bool
+
+
+def prob_floor_ratio(probs: BlockProbabilities, reference: BlockProbabilities) -> FloorRatio:
+    """Largest beta with probs >= beta * reference on reference's support,
+    clamped to [0, 1]; (0, True) when probs vanishes there (plan.py:220-239)."""
+    if len(probs.per_block) != len(reference.per_block):
+        raise ValueError("block counts differ")
+    ratio = 1.0
+    for p, r in zip(probs.per_block, reference.per_block):
+        p, r = np.asarray(p), np.asarray(r)
+        if p.shape != r.shape:
+            raise ValueError("per-block shapes differ")
+        sup = r > 0
+        if not sup.any():
+            continue
+        if (p[sup] == 0).any():
+            return FloorRatio(0.0, True)
+        ratio = min(ratio, float((p[sup] / r[sup]).min()))
+    return FloorRatio(min(max(ratio, 0.0), 1.0), False)
+
+
+def plan_to_dict(plan: SamplingPlan, include_probs: Optional[bool] = None) -> dict:
+    """JSON document of a plan (plan.py:499-518): probabilities are written
+    only when no named rule regenerates them, unless forced."""
+    if plan.method not in METHOD_TAGS:
+        raise ValueError(f"method tag {plan.method!r} not in {METHOD_TAGS}")
+    if include_probs is None:
+        include_probs = plan.probs.rule == "explicit"
+    doc = {"method": plan.method, "partition": list(plan.partition.sizes), "total": plan.total,
+           "budgets": [int(b) for b in plan.budgets], "probs_rule": plan.probs.rule}
+    if include_probs:
+        doc["probs"] = [np.asarray(p).tolist() for p in plan.probs.per_block]
+    if plan.pilot_norms is not None:
+        doc["pilot_norms"] = np.asarray(plan.pilot_norms).tolist()
+    return doc
+
+
+def plan_from_dict(doc: dict, M=None, N=None) -> SamplingPlan:
+    """plan.py:521-549; 'optimal' probabilities are regenerated on device from M, N."""
+    part = BlockPartition(tuple(doc["partition"]))
+    rule = doc.get("probs_rule", "explicit")
+    if "probs" in doc:
+        probs = BlockProbabilities(tuple(np.asarray(p) for p in doc["probs"]), rule=rule)
+    elif rule == "uniform":
+        probs = uniform_probabilities(part)
+    elif rule == "optimal":
+        if M is None or N is None:
+            raise ValueError("regenerating 'optimal' probabilities requires the factor matrices")
+        probs = optimal_probabilities(M, N, part)
+    else:
+        raise ValueError(f"cannot reconstruct probabilities for rule {rule!r}")
+    pilot = doc.get("pilot_norms")
+    plan = SamplingPlan(part, probs, np.asarray(doc["budgets"], dtype=np.int64), method=doc.get("method", ""),
+                        pilot_norms=None if pilot is None else np.asarray(pilot))
+    if plan.total != doc.get("total", plan.total):
+        raise ValueError("budget sum disagrees with the recorded total")
+    return plan
+
+
+def plan_to_json(plan: SamplingPlan, include_probs: Optional[bool] = None) -> str:
+    return json.dumps(plan_to_dict(plan, include_probs), indent=2)
+
+
+def plan_from_json(text: str, M=None, N=None) -> SamplingPlan:
+    return plan_from_dict(json.loads(text), M, N)
