@@ -57,6 +57,22 @@ def main():
             cov = ra.coverage_check_plan(M, N, plan, bound, REPS, np.random.default_rng(100 + seed))
             out[key + "__coverage"] = np.array([bound, cov.violations, cov.ci_low, cov.ci_high])
         out[f"s{seed}__mese"] = np.array([ra.minimum_expected_sq_error(M, N, part, c)])
+        # closed-form bounds (analysis.py:148-315), incl. a two-step plan's pilot bound
+        two = ref.estimate_product_two_step(M, N, part, c, 3 * len(sizes), np.random.default_rng(seed),
+                                            pilot="uniform").plan
+        for meth, plan in list(plans(M, N, part, c).items()) + [("ONU", two)]:
+            inp = ra.bound_inputs_for_plan(M, N, plan, 0.1)
+            vals = [inp.prob_floor, inp.cancel_lo, inp.cancel_hi, inp.frob_m, inp.frob_n]
+            vals += list(ra.bounds_optimal_allocation(inp))
+            try:
+                vals += list(ra.bounds_score_allocation(inp))
+            except ValueError:  # pilot statistics outside [0, 1]: the reference refuses
+                vals += [-1.0, -1.0]
+            vals += list(ra.bounds_pilot_allocation(inp)) if inp.cancel_hi_exact is not None else [np.nan, np.nan]
+            out[f"s{seed}_{meth}__bounds"] = np.array(vals)
+            if meth == "ONU":
+                out[f"s{seed}_ONU__budgets"] = plan.budgets
+                out[f"s{seed}_ONU__pilot"] = plan.pilot_norms
     M, N, sizes, c, _ = sweep_params(NORMAL_SEED)
     part = ref.BlockPartition(sizes)
     plan = ref.allocate_optimal(M, N, part, c)
