@@ -36,6 +36,26 @@ def test_norms_bit_exact(m, n, p, dtype):
     assert np.array_equal(rn, np.sqrt(O.rowsq(N.astype(np.float64))))
 
 
+@pytest.mark.parametrize("p,dtype", [(8, np.float32), (100, np.float64), (128, np.float32), (130, np.float64),
+                                     (256, np.float32), (500, np.float64), (1000, np.float64), (4096, np.float32),
+                                     (16384, np.float32), (6000, np.float64)])
+def test_rowsq_staged_bit_exact(p, dtype):
+    """The bulk-copy staged row kernel (inputs >= 8 MB, contiguous 16-byte rows),
+    batched with a problem stride, against NumPy's pairwise order."""
+    import torch
+    g = np.random.default_rng(p)
+    itemsize = np.dtype(dtype).itemsize
+    n = max(64, (12 << 20) // (p * itemsize * 2))
+    N = (g.standard_normal((2, n, p)) * g.lognormal(0, 2, (2, n, 1))).astype(dtype)
+    Nd = torch.as_tensor(N, device="cuda")
+    rs = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    from paper_2105_04940_b200 import _lib
+    _lib.call("bmm_norms", _lib.matrix_dtype(Nd), None, 0, n, 0, 0, Nd.data_ptr(), p, p, n * p, 2, 0, None,
+              rs.data_ptr(), _lib.stream_ptr())
+    ref = np.concatenate([O.rowsq(N[b].astype(np.float64)) for b in range(2)])
+    assert np.array_equal(rs.cpu().numpy(), ref)
+
+
 def test_norms_unaligned_view():
     import torch
     g = np.random.default_rng(4)

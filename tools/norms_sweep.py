@@ -1,0 +1,47 @@
+"""Time the K1 kernels alone (colsq of M, rowsq of N) on the config shapes:
+achieved GB/s and fraction of the measured HBM peak.  Usage: python tools/norms_sweep.py"""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2105_04940_b200 import _lib  # noqa: E402
+
+ROOT = Path(__file__).resolve().parent.parent
+peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 6650.0) \
+    if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+torch.cuda.set_device(0)
+lib, st = _lib.load(), _lib.stream_ptr()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+# (name, dtype, batch, rows_or_m, cols)
+shapes = [("cfg2 N 20000x500 f64", torch.float64, 1, 20000, 500), ("cfg3 N 100000x1000 f64", torch.float64, 1, 100000, 1000),
+          ("cfg5 N 1024x(4096x256) f32", torch.float32, 1024, 4096, 256),
+          ("cfg4 N 65536x16384 f32 (1/4)", torch.float32, 1, 65536, 16384)]
+
+
+def timed(fn, reps=5):
+    out = []
+    for _ in range(reps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1))
+    return sorted(out)[len(out) // 2]
+
+
+for name, dt, B, r, c in shapes:
+    X = torch.randn((B, r, c), dtype=dt, device="cuda")
+    d = _lib.matrix_dtype(X)
+    outv = torch.empty(B * max(r, c), dtype=torch.float64, device="cuda")
+    nbytes = X.numel() * X.element_size()
+    ms_r = timed(lambda: lib.bmm_norms(d, None, 0, r, 0, 0, X.data_ptr(), c, c, r * c, B, 0, None, outv.data_ptr(), st))
+    # the same matrix as a left factor (r x c, colsq over c columns)
+    ms_c = timed(lambda: lib.bmm_norms(d, X.data_ptr(), r, c, c, r * c, None, 0, 0, 0, B, 0, outv.data_ptr(), None, st))
+    print(f"{name:32s} rowsq {ms_r*1e3:9.1f} us {nbytes/ms_r/1e6:7.0f} GB/s ({nbytes/ms_r/1e6/peak:5.1%})   "
+          f"colsq {ms_c*1e3:9.1f} us {nbytes/ms_c/1e6:7.0f} GB/s ({nbytes/ms_c/1e6/peak:5.1%})", flush=True)
+    del X
