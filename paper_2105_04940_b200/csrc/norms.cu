@@ -15,7 +15,8 @@
 //   * rowsq_leaf_kernel  other widths <= 16384: lane per leaf from global memory,
 //                        tree from a per-CTA plan of NumPy's split (60%)
 //   * rowsq_warp_kernel / rowsq_kernel: small inputs and odd layouts
-//   BMM_ROWSQ_VARIANT=1|2 forces the older kernels (A/B timing only).
+//   BMM_ROWSQ_VARIANT=1 skips the TMA kernel, =2 uses only the small-input kernels
+//   (A/B timing in tools/norms_sweep.py).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -595,7 +596,7 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
     const bool big = rows * p * (int64_t)sizeof(T) >= (8LL << 20);
     if (variant == 0 && big && launch_rowsq_tma<T>(N, n, p, ldn, strideN, batch, rowsq, st)) {
       BMM_CHECK_LAUNCH("rowsq_tma_kernel");
-    } else if (variant <= 2 && big && launch_rowsq_leaf<T>(N, n, p, ldn, strideN, batch, rowsq, st)) {
+    } else if (variant <= 1 && big && launch_rowsq_leaf<T>(N, n, p, ldn, strideN, batch, rowsq, st)) {
       BMM_CHECK_LAUNCH("rowsq_leaf_kernel");
     } else if (rows < 148LL * 512 && p > 128) {
       const int64_t blocks = std::min<int64_t>(ceil_div(rows, kRowWarps), 148LL * 8 * 64);
