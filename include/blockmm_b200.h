@@ -303,6 +303,21 @@ int bmm_gemm_f32split(const float* a_hi, const void* a_x, const float* b_hi, con
 int bmm_pairwise_sum(const double* x, int64_t len, int64_t stride, int64_t batch,
                      double* out, void* stream);
 
+/* ---------------------------------------------------------------- instances
+ * gen_normal_instance / gen_heavy_tail_instance (datagen.py:55-110) on device:
+ * M (m x n) columns and N (n x p) rows are AR(1) vectors with covariance
+ * scale * rho^|i-j| (datagen.py:38-42), generated by the recursion that equals
+ * L @ z for the Cholesky factor L; heavy != 0 divides each vector by
+ * sqrt(chi^2(1)) and adds `location`.  Vector j of each side draws from its own
+ * PCG64 stream, SeedSequence-hashed from (seed_lo, seed_hi, side tag) with child
+ * j; normals by Box-Muller.  Deterministic per seed; distribution-identical to,
+ * not bit-identical with, the reference's numpy draws.  Either output may be
+ * NULL.  dtype BMM_F64 or BMM_F32 (generated in float64, rounded once).      */
+int bmm_gen_instance(int heavy, int dtype, int64_t m, int64_t n, int64_t p,
+                     uint64_t seed_hi, uint64_t seed_lo,
+                     double scale_left, double rho_left, double scale_right, double rho_right,
+                     double location, void* M, int64_t ldm, void* N, int64_t ldn, void* stream);
+
 #ifdef __cplusplus
 }
 #endif
