@@ -293,6 +293,7 @@ def run_ours(args):
         "roofline": {"bound": "tensor", "kernel": "gemm_f64_kernel (C.D, DMMA)", "achieved": gemm_achieved,
                      "peak": dgemm_peak, "unit": "TFLOP/s", "frac": gemm_achieved / dgemm_peak,
                      "peak_source": "cuBLAS dgemm 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
+                     "cublas_same_shapes_tflops": sum(gemm_flops) / (sum(kt["cublas_same_shape_ms"]) * 1e-3) / 1e12,
                      "traffic": None},
         "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norms_achieved,
                            "peak": hbm_peak, "unit": "GB/s", "frac": norms_achieved / hbm_peak,
@@ -347,6 +348,21 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
             torch.cuda.synchronize()
             reps.append(e0.elapsed_time(e1))
         out["gemm_ms"].append(float(np.median(reps)))
+    # context: cuBLAS DGEMM on the same operands (reference point only; not on the product path)
+    out["cublas_same_shape_ms"] = []
+    for (cb, W, meth, c0), pipe in zip(runs, pipes):
+        C, D = pipe.C.view(m, W), pipe.D.view(W, p)
+        torch.matmul(C, D)
+        reps = []
+        for _ in range(5):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(C, D)
+            e1.record()
+            torch.cuda.synchronize()
+            reps.append(e0.elapsed_time(e1))
+        out["cublas_same_shape_ms"].append(float(np.median(reps)))
     return out
 
 
