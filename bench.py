@@ -267,6 +267,8 @@ def run_ours(args):
     kt = kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush)
     dgemm_peak = measure_dgemm_peak(torch)
     gemm_ms = kt["gemm_ms"]
+    # executed flops: 2 m p K over the distinct drawn columns the GEMM contracts
+    gemm_flops = [2.0 * m * p * kd for kd in kt["gemm_k"]]
     gemm_achieved = sum(gemm_flops) / (sum(gemm_ms) * 1e-3) / 1e12
     norms_achieved = norm_bytes / (kt["norms_ms"] * 1e-3) / 1e9
     large = norms_large(torch)
@@ -294,6 +296,8 @@ def run_ours(args):
                      "peak": dgemm_peak, "unit": "TFLOP/s", "frac": gemm_achieved / dgemm_peak,
                      "peak_source": "cuBLAS dgemm 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
                      "cublas_same_shapes_tflops": sum(gemm_flops) / (sum(kt["cublas_same_shape_ms"]) * 1e-3) / 1e12,
+                     "flops_note": "executed 2*m*p*K over the distinct drawn columns (gemm_k); the sketch "
+                                   "width W counts duplicates, which the compressed sketch folds into scales",
                      "traffic": None},
         "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norms_achieved,
                            "peak": hbm_peak, "unit": "GB/s", "frac": norms_achieved / hbm_peak,
@@ -335,23 +339,35 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
         torch.cuda.synchronize()
         reps.append(e0.elapsed_time(e1))
     out["norms_ms"] = float(np.median(reps))
-    # the sampled GEMM of each run (C, D already gathered by the last step)
+    # the sampled GEMM of each run (C, D already gathered by the last step): over the
+    # distinct drawn columns when the pipeline compresses the sketch (k_count on device)
+    out["gemm_k"] = []
     for (cb, W, meth, c0), pipe in zip(runs, pipes):
+        kd = int(pipe.k_count[0].item()) if pipe.compress else W
+        out["gemm_k"].append(kd)
+
+        def gemm():
+            if pipe.compress:
+                lib.bmm_gemm_f64_dk(pipe.C.data_ptr(), W, m * W, pipe.D.data_ptr(), p, W * p, m, p, W,
+                                    pipe.k_count.data_ptr(), 1, pipe.CD.data_ptr(), p, m * p, pipe.ws_gemm.data_ptr(),
+                                    pipe.ws_gemm.numel(), st)
+            else:
+                lib.bmm_gemm_f64(pipe.C.data_ptr(), W, m * W, pipe.D.data_ptr(), p, W * p, m, p, W, 1,
+                                 pipe.CD.data_ptr(), p, m * p, pipe.ws_gemm.data_ptr(), pipe.ws_gemm.numel(), st)
         reps = []
         for _ in range(5):
             flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            lib.bmm_gemm_f64(pipe.C.data_ptr(), W, m * W, pipe.D.data_ptr(), p, W * p, m, p, W, 1,
-                             pipe.CD.data_ptr(), p, m * p, pipe.ws_gemm.data_ptr(), pipe.ws_gemm.numel(), st)
+            gemm()
             e1.record()
             torch.cuda.synchronize()
             reps.append(e0.elapsed_time(e1))
         out["gemm_ms"].append(float(np.median(reps)))
     # context: cuBLAS DGEMM on the same operands (reference point only; not on the product path)
     out["cublas_same_shape_ms"] = []
-    for (cb, W, meth, c0), pipe in zip(runs, pipes):
-        C, D = pipe.C.view(m, W), pipe.D.view(W, p)
+    for (cb, W, meth, c0), pipe, kd in zip(runs, pipes, out["gemm_k"]):
+        C, D = pipe.C.view(m, W)[:, :kd], pipe.D.view(W, p)[:kd]
         torch.matmul(C, D)
         reps = []
         for _ in range(5):

@@ -172,6 +172,19 @@ int bmm_sample_reps(const double* probs, const double* cum, const int64_t* last_
                     const uint64_t* states, int64_t* column, double* prob, double* scale,
                     void* stream);
 
+/* Compressed sketch (K4 prologue): the draws of one column share its scale
+ * s_i = 1/sqrt(c_k p_i), so c_i duplicates contribute c_i s_i^2 M[:,i] N[i,:]
+ * to C @ D (estimators.py:78-80,175).  Writes the distinct drawn columns in
+ * column order to out_column[0..count) with out_scale = s_i sqrt(c_i), zero
+ * padding up to W, and count per problem in out_count (device).  Gathering and
+ * contracting (bmm_gemm_f64_dk) the compressed sketch gives C @ D up to
+ * rounding with one rank-1 term per distinct column.  Deterministic.
+ * Workspace bmm_compress_workspace(n, batch) bytes.                          */
+int64_t bmm_compress_workspace(int64_t n, int64_t batch);
+int bmm_compress_sketch(const int64_t* column, const double* scale, int64_t W, int64_t w_stride,
+                        int64_t n, int64_t batch, void* ws, int64_t ws_bytes,
+                        int64_t* out_column, double* out_scale, int64_t* out_count, void* stream);
+
 /* ---------------------------------------------------------------- K4 gather
  * C[h, t] = M[h, column[t]] * scale[t]        (m x W, ldc)     estimators.py:79
  * D[t, f] = N[column[t], f] * scale[t]        (W x p, ldd)     estimators.py:80
@@ -226,6 +239,15 @@ int bmm_gemm_f64_gather(const double* M, int64_t ldm, int64_t strideM,
                         int64_t W, int64_t w_stride, int64_t batch,
                         double* out, int64_t ldo, int64_t strideO,
                         void* ws, int64_t ws_bytes, void* stream);
+
+/* bmm_gemm_f64 with the inner length read from the device (k_dev[b] <= k_max,
+ * e.g. bmm_compress_sketch's count): the split-K plan is re-made on the device
+ * for the actual length, so a shorter K costs proportionally less.  Workspace:
+ * bmm_gemm_f64_workspace(m, nc, k_max, batch).                               */
+int bmm_gemm_f64_dk(const double* A, int64_t lda, int64_t strideA,
+                    const double* B, int64_t ldb, int64_t strideB,
+                    int64_t m, int64_t nc, int64_t k_max, const int64_t* k_dev, int64_t batch,
+                    double* out, int64_t ldo, int64_t strideO, void* ws, int64_t ws_bytes, void* stream);
 
 /* Segmented square-sum GEMM: gsq[b, j] = || A[:, seg_j] @ B[seg_j, :] ||_F^2
  * for segments seg_j = [seg[j], seg[j+1]) of the inner dimension.

@@ -50,6 +50,10 @@ SIGNATURES = {
     "bmm_seed_streams": (_I, [_P, _I64, _P, _I64, _I64, _P, _P]),
     "bmm_sample": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "bmm_sample_reps": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
+    "bmm_compress_workspace": (_I64, [_I64, _I64]),
+    "bmm_compress_sketch": (_I, [_P, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _P, _P]),
+    "bmm_gemm_f64_dk": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P, _I64,
+                             _P]),
     "bmm_gather": (_I, [_I, _I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _I64,
                         _P, _I64, _I64, _P, _I64, _I64, _P]),
     "bmm_gather_blocks": (_I, [_I, _P, _I64, _P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64,

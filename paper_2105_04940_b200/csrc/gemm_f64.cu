@@ -216,6 +216,17 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
   __syncthreads();
 }
 
+// split-K plan for an inner length known only on the device (compressed sketch):
+// the host rule of plan_split (>= 4 k-tiles per split) capped at the launched splits
+__device__ __forceinline__ void device_split(int64_t k, int64_t smax, int bk, int64_t& splits, int64_t& kchunk) {
+  int64_t s = (k + 4 * bk - 1) / (4 * bk);
+  s = s > smax ? smax : (s < 1 ? 1 : s);
+  kchunk = (((k + s - 1) / s) + bk - 1) / bk * bk;
+  if (kchunk < bk) kchunk = bk;
+  splits = (k + kchunk - 1) / kchunk;
+  if (splits < 1) splits = 1;
+}
+
 template <class C, bool V16, bool G = false, bool SQ = false>
 __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __restrict__ A, int64_t lda,
                                                               int64_t strideA, const double* __restrict__ B,
@@ -224,10 +235,17 @@ __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __re
                                                               double* __restrict__ out, int64_t ldo,
                                                               int64_t strideO, double* __restrict__ part,
                                                               const int64_t* __restrict__ col,
-                                                              const double* __restrict__ scale, int64_t w_stride) {
+                                                              const double* __restrict__ scale, int64_t w_stride,
+                                                              const int64_t* __restrict__ kdev = nullptr) {
   extern __shared__ __align__(16) double smem[];
   const int64_t z = blockIdx.z;
   const int64_t b = z / splits, sp = z - b * splits;
+  if (kdev != nullptr) {  // inner length from the device: re-plan the split, idle CTAs leave
+    k = kdev[b];
+    int64_t se;
+    device_split(k, splits, C::BK, se, kchunk);
+    if (sp >= se) return;
+  }
   TileArgs ta{A + b * strideA, lda, B + b * strideB, ldb, m, nc, (int64_t)blockIdx.y * C::BM,
               (int64_t)blockIdx.x * C::BN};
   if constexpr (G) {
@@ -263,14 +281,20 @@ __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __re
 }
 
 __global__ void splitk_reduce_kernel(const double* __restrict__ part, int64_t splits, int64_t m, int64_t nc,
-                                     int64_t batch, double* __restrict__ out, int64_t ldo, int64_t strideO) {
+                                     int64_t batch, double* __restrict__ out, int64_t ldo, int64_t strideO,
+                                     const int64_t* __restrict__ kdev = nullptr, int bk = 16) {
   const int64_t per = m * nc;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < per * batch;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = g / per, e = g - b * per;
     const double* p = part + b * splits * per + e;
+    int64_t se = splits;
+    if (kdev != nullptr) {
+      int64_t kc;
+      device_split(kdev[b], splits, bk, se, kc);
+    }
     double acc = p[0];
-    for (int64_t s = 1; s < splits; ++s) acc = __dadd_rn(acc, p[s * per]);
+    for (int64_t s = 1; s < se; ++s) acc = __dadd_rn(acc, p[s * per]);
     const int64_t r = e / nc, c = e - r * nc;
     out[b * strideO + r * ldo + c] = acc;
   }
@@ -581,7 +605,8 @@ template <class C>
 static void launch_gemm(bool v16, dim3 grid, cudaStream_t st, const double* A, int64_t lda, int64_t strideA,
                         const double* B, int64_t ldb, int64_t strideB, int64_t m, int64_t nc, int64_t k,
                         const SplitPlan& sp, double* out, int64_t ldo, int64_t strideO, double* part,
-                        const int64_t* col = nullptr, const double* scale = nullptr, int64_t w_stride = 0) {
+                        const int64_t* col = nullptr, const double* scale = nullptr, int64_t w_stride = 0,
+                        const int64_t* kdev = nullptr) {
   if (col != nullptr) {
     static bool attr = false;
     if (!attr) {
@@ -601,10 +626,12 @@ static void launch_gemm(bool v16, dim3 grid, cudaStream_t st, const double* A, i
   }
   if (v16)
     gemm_f64_kernel<C, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k, sp.splits,
-                                                               sp.kchunk, out, ldo, strideO, part, nullptr, nullptr, 0);
+                                                               sp.kchunk, out, ldo, strideO, part, nullptr, nullptr, 0,
+                                                               kdev);
   else
     gemm_f64_kernel<C, false><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k, sp.splits,
-                                                                sp.kchunk, out, ldo, strideO, part, nullptr, nullptr, 0);
+                                                                sp.kchunk, out, ldo, strideO, part, nullptr, nullptr, 0,
+                                                                kdev);
 }
 
 template <class C>
@@ -657,7 +684,7 @@ extern "C" int64_t bmm_gemm_f64_workspace(int64_t m, int64_t nc, int64_t k, int6
 static int gemm_impl(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb, int64_t strideB,
                      int64_t m, int64_t nc, int64_t k, int64_t batch, double* out, int64_t ldo, int64_t strideO,
                      void* ws, int64_t ws_bytes, cudaStream_t st, const int64_t* col, const double* scale,
-                     int64_t w_stride) {
+                     int64_t w_stride, const int64_t* kdev = nullptr) {
   if (m == 0 || nc == 0) return BMM_OK;
   if (k == 0) {
     for (int64_t b = 0; b < batch; ++b)
@@ -680,7 +707,7 @@ static int gemm_impl(const double* A, int64_t lda, int64_t strideA, const double
   double* part = (double*)ws;
 #define BMM_GEMM_CASE(V)                                                                                       \
   launch_gemm<V>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part, col, \
-                 scale, w_stride)
+                 scale, w_stride, kdev)
   switch (g_variant) {
     case 1: BMM_GEMM_CASE(DV1); break;
     case 2: BMM_GEMM_CASE(DV2); break;
@@ -694,7 +721,7 @@ static int gemm_impl(const double* A, int64_t lda, int64_t strideA, const double
   BMM_CHECK_LAUNCH("gemm_f64_kernel");
   if (sp.splits > 1) {
     splitk_reduce_kernel<<<grid_for(m * nc * batch, 256), 256, 0, st>>>((const double*)ws, sp.splits, m, nc,
-                                                                        batch, out, ldo, strideO);
+                                                                        batch, out, ldo, strideO, kdev, vi.BK);
     BMM_CHECK_LAUNCH("splitk_reduce_kernel");
   }
   return BMM_OK;
@@ -706,6 +733,16 @@ extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const
   BMM_REQUIRE(m >= 0 && nc >= 0 && k >= 0 && batch >= 1, BMM_E_ARG, "bmm_gemm_f64: bad shape");
   return gemm_impl(A, lda, strideA, B, ldb, strideB, m, nc, k, batch, out, ldo, strideO, ws, ws_bytes,
                    as_stream(stream), nullptr, nullptr, 0);
+}
+
+extern "C" int bmm_gemm_f64_dk(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                               int64_t strideB, int64_t m, int64_t nc, int64_t k_max, const int64_t* k_dev,
+                               int64_t batch, double* out, int64_t ldo, int64_t strideO, void* ws, int64_t ws_bytes,
+                               void* stream) {
+  BMM_REQUIRE(m >= 0 && nc >= 0 && k_max >= 1 && batch >= 1 && k_dev != nullptr, BMM_E_ARG,
+              "bmm_gemm_f64_dk: bad shape");
+  return gemm_impl(A, lda, strideA, B, ldb, strideB, m, nc, k_max, batch, out, ldo, strideO, ws, ws_bytes,
+                   as_stream(stream), nullptr, nullptr, 0, k_dev);
 }
 
 extern "C" int bmm_gemm_f64_gather(const double* M, int64_t ldm, int64_t strideM, const double* N, int64_t ldn,

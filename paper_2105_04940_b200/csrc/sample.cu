@@ -327,3 +327,95 @@ extern "C" int bmm_gather_blocks(int dtype, const void* M, int64_t ldm, const vo
   BMM_CHECK_LAUNCH("gather_blocks_kernel");
   return BMM_OK;
 }
+
+// ---- sketch compression (K4 prologue): all draws of a column i share the
+// scale s_i = 1/sqrt(c_k p_i), so its c_i duplicates contribute
+// c_i s_i^2 M[:, i] N[i, :] to C @ D.  The GEMM then runs over the distinct
+// columns (in column order) with scale s_i sqrt(c_i): the same product up to
+// rounding, and only as many rank-1 terms as distinct draws.  Counts are
+// integers (atomics are order-free), so the result is deterministic.
+__global__ void sketch_count_kernel(const int64_t* __restrict__ column, const double* __restrict__ scale, int64_t W,
+                                    int64_t w_stride, int64_t n, int64_t batch, int32_t* __restrict__ cnt,
+                                    double* __restrict__ sval) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < W * batch;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g / W, t = g - b * W;
+    const int64_t j = column[b * w_stride + t];
+    atomicAdd(&cnt[b * n + j], 1);
+    sval[b * n + j] = scale[b * w_stride + t];  // every draw of column j carries the same scale
+  }
+}
+
+constexpr int kCompactThreads = 1024;
+
+__global__ void __launch_bounds__(kCompactThreads) sketch_compact_kernel(
+    const int32_t* __restrict__ cnt, const double* __restrict__ sval, int64_t n, int64_t W, int64_t w_stride,
+    int64_t* __restrict__ out_col, double* __restrict__ out_scale, int64_t* __restrict__ out_count) {
+  __shared__ int64_t warp_tot[32];
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t per = (n + kCompactThreads - 1) / kCompactThreads;
+  const int64_t lo = tid * per, hi = min(n, lo + per);
+  const int32_t* cb = cnt + b * n;
+  int64_t mine = 0;
+  for (int64_t j = lo; j < hi; ++j) mine += (cb[j] > 0);
+  // block exclusive scan of `mine`
+  int64_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int64_t v = lane < (kCompactThreads / 32) ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    warp_tot[lane] = v;  // inclusive over warps
+  }
+  __syncthreads();
+  int64_t pos = incl - mine + (w ? warp_tot[w - 1] : 0);
+  const int64_t total = warp_tot[kCompactThreads / 32 - 1];
+  int64_t* oc = out_col + b * w_stride;
+  double* os = out_scale + b * w_stride;
+  for (int64_t j = lo; j < hi; ++j) {
+    const int32_t c = cb[j];
+    if (c > 0) {
+      oc[pos] = j;
+      os[pos] = __dmul_rn(sval[b * n + j], __dsqrt_rn((double)c));
+      ++pos;
+    }
+  }
+  for (int64_t u = total + tid; u < W; u += kCompactThreads) {  // padding: zero columns
+    oc[u] = 0;
+    os[u] = 0.0;
+  }
+  if (tid == 0) out_count[b] = total;
+}
+
+extern "C" int64_t bmm_compress_workspace(int64_t n, int64_t batch) { return batch * n * (4 + 8); }
+
+extern "C" int bmm_compress_sketch(const int64_t* column, const double* scale, int64_t W, int64_t w_stride,
+                                   int64_t n, int64_t batch, void* ws, int64_t ws_bytes, int64_t* out_column,
+                                   double* out_scale, int64_t* out_count, void* stream) {
+  BMM_REQUIRE(W >= 1 && n >= 1 && batch >= 1 && w_stride >= W, BMM_E_ARG, "bmm_compress_sketch: bad shape");
+  BMM_REQUIRE(ws != nullptr && ws_bytes >= batch * n * 12, BMM_E_ARG, "bmm_compress_sketch: workspace too small");
+  BMM_REQUIRE(batch <= 65535, BMM_E_UNSUPPORTED, "bmm_compress_sketch: batch too large");
+  cudaStream_t st = as_stream(stream);
+  double* sval = reinterpret_cast<double*>(ws);
+  int32_t* cnt = reinterpret_cast<int32_t*>(sval + batch * n);
+  if (cudaMemsetAsync(cnt, 0, (size_t)(batch * n) * sizeof(int32_t), st) != cudaSuccess) {
+    set_error("bmm_compress_sketch: memset failed");
+    return BMM_E_CUDA;
+  }
+  sketch_count_kernel<<<grid_for(W * batch, 256), 256, 0, st>>>(column, scale, W, w_stride, n, batch, cnt, sval);
+  BMM_CHECK_LAUNCH("sketch_count_kernel");
+  sketch_compact_kernel<<<(unsigned)batch, kCompactThreads, 0, st>>>(cnt, sval, n, W, w_stride, out_column,
+                                                                     out_scale, out_count);
+  BMM_CHECK_LAUNCH("sketch_compact_kernel");
+  return BMM_OK;
+}

@@ -216,13 +216,22 @@ class ShardedApproxProduct:
             out = torch.empty((ma, pb), dtype=torch.float32, device=M_local.device)
             self._c("bmm_gemm_f32split", P(a_hi), P(a_x), P(b_hi), P(b_x), ma, pb, W, 1, P(out), pb, 0, st)
             return out
-        C = torch.empty((ma, W), dtype=torch.float64, device=M_local.device)
-        D = torch.empty((W, pb), dtype=torch.float64, device=M_local.device)
+        # compressed sketch (one term per distinct drawn column), as SketchPipeline
+        dev = M_local.device
+        kcol = torch.empty(W, dtype=torch.int64, device=dev)
+        ksc = torch.empty(W, dtype=torch.float64, device=dev)
+        kcnt = torch.empty(1, dtype=torch.int64, device=dev)
+        wsc = _lib.workspace(self.lib.bmm_compress_workspace(n, 1))
+        self._c("bmm_compress_sketch", P(self.column), P(self.scale), W, W, n, 1, P(wsc), wsc.numel(), P(kcol),
+                P(ksc), P(kcnt), st)
+        C = torch.empty((ma, W), dtype=torch.float64, device=dev)
+        D = torch.empty((W, pb), dtype=torch.float64, device=dev)
         self._c("bmm_gather", dt, _lib.BMM_F64, P(M_local), M_local.stride(0), 0, P(N_local), N_local.stride(0), 0,
-                ma, pb, P(self.column), P(self.scale), W, W, 1, P(C), W, 0, P(D), pb, 0, st)
-        out = torch.empty((ma, pb), dtype=torch.float64, device=M_local.device)
+                ma, pb, P(kcol), P(ksc), W, W, 1, P(C), W, 0, P(D), pb, 0, st)
+        out = torch.empty((ma, pb), dtype=torch.float64, device=dev)
         ws = _lib.workspace(self.lib.bmm_gemm_f64_workspace(ma, pb, W, 1))
-        self._c("bmm_gemm_f64", P(C), W, 0, P(D), pb, 0, ma, pb, W, 1, P(out), pb, 0, P(ws), ws.numel(), st)
+        self._c("bmm_gemm_f64_dk", P(C), W, 0, P(D), pb, 0, ma, pb, W, P(kcnt), 1, P(out), pb, 0, P(ws), ws.numel(),
+                st)
         return out
 
     def check(self):

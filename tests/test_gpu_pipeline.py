@@ -146,3 +146,39 @@ def test_pipeline_reports_reference_errors():
     pipe.run(Md, Nd, seeds_from_rngs("ONC", [np.random.default_rng(0)], len(sizes)))
     with pytest.raises(ValueError, match="required floors"):
         pipe.check()
+
+
+def test_compressed_sketch_matches_draws_and_uncompressed_product():
+    """bmm_compress_sketch: distinct drawn columns in column order, scale
+    s_i sqrt(c_i), zero padding, count; the compressed contraction equals the
+    draw-order one to rounding."""
+    from paper_2105_04940_b200 import _lib
+    M, N, sizes = workloads.cfg2(n=4000, m=60, p=50, K=12)
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    a = SketchPipeline(60, 4000, 50, sizes, 900, "OPL", compress=True)
+    b = SketchPipeline(60, 4000, 50, sizes, 900, "OPL", compress=False)
+    CDa = a.run(Md, Nd, seeds_from_rngs("OPL", [np.random.default_rng(4)], len(sizes))).cpu().numpy()
+    CDb = b.run(Md, Nd, seeds_from_rngs("OPL", [np.random.default_rng(4)], len(sizes))).cpu().numpy()
+    assert np.array_equal(a.columns_host(), b.columns_host())
+    assert rel(CDa, CDb) < 1e-13
+    cols, scales = a.columns_host()[0], a.scales_host()[0]
+    uniq, counts = np.unique(cols, return_counts=True)
+    kd = int(a.k_count[0].item())
+    assert kd == uniq.size
+    kc = a.k_column.cpu().numpy()
+    ks = a.k_scale.cpu().numpy()
+    assert np.array_equal(kc[:kd], uniq) and (kc[kd:] == 0).all() and (ks[kd:] == 0).all()
+    first = {c: s for c, s in zip(cols[::-1], scales[::-1])}
+    assert np.allclose(ks[:kd], np.array([first[c] for c in uniq]) * np.sqrt(counts), rtol=1e-15, atol=0)
+    # direct C-ABI call on a batch of 2 with a stride
+    col2 = torch.as_tensor(np.stack([cols, cols[::-1].copy()]), device="cuda")
+    sc2 = torch.as_tensor(np.stack([scales, scales[::-1].copy()]), device="cuda")
+    W = cols.size
+    oc = torch.empty(2 * W, dtype=torch.int64, device="cuda")
+    os_ = torch.empty(2 * W, dtype=torch.float64, device="cuda")
+    cnt = torch.empty(2, dtype=torch.int64, device="cuda")
+    ws = _lib.workspace(_lib.load().bmm_compress_workspace(4000, 2))
+    _lib.call("bmm_compress_sketch", col2.data_ptr(), sc2.data_ptr(), W, W, 4000, 2, ws.data_ptr(), ws.numel(),
+              oc.data_ptr(), os_.data_ptr(), cnt.data_ptr(), _lib.stream_ptr())
+    assert cnt.cpu().tolist() == [kd, kd]
+    assert np.array_equal(oc.view(2, W)[1, :kd].cpu().numpy(), uniq)
