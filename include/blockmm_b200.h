@@ -199,6 +199,15 @@ int bmm_gather(int dtype, int out_dtype,
                int64_t W, int64_t w_stride, int64_t batch,
                void* C, int64_t ldc, int64_t strideC,
                void* D, int64_t ldd, int64_t strideD, void* stream);
+/* bmm_gather for a compressed sketch: only sketch columns t < w_dev[b]
+ * (device count from bmm_compress_sketch) are written.                      */
+int bmm_gather_dk(int dtype, int out_dtype,
+                  const void* M, int64_t ldm, int64_t strideM,
+                  const void* N, int64_t ldn, int64_t strideN,
+                  int64_t m, int64_t p, const int64_t* column, const double* scale,
+                  int64_t W, int64_t w_stride, const int64_t* w_dev, int64_t batch,
+                  void* C, int64_t ldc, int64_t strideC, void* D, int64_t ldd, int64_t strideD,
+                  void* stream);
 
 /* SSM whole-block gather (estimators.py:244-249): draw t copies block
  * blocks[t] scaled by scale[t]; the sketch columns of draw t start at

@@ -56,6 +56,8 @@ SIGNATURES = {
                              _P]),
     "bmm_gather": (_I, [_I, _I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _I64,
                         _P, _I64, _I64, _P, _I64, _I64, _P]),
+    "bmm_gather_dk": (_I, [_I, _I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _P, _I64,
+                           _P, _I64, _I64, _P, _I64, _I64, _P]),
     "bmm_gather_blocks": (_I, [_I, _P, _I64, _P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64,
                                _P, _I64, _P, _I64, _P]),
     "bmm_gemm_f64_workspace": (_I64, [_I64, _I64, _I64, _I64]),

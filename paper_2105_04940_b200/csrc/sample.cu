@@ -130,13 +130,15 @@ __global__ void __launch_bounds__(256) gather_c_kernel(const T* __restrict__ M, 
                                                        int64_t m, const int64_t* __restrict__ column,
                                                        const double* __restrict__ scale, int64_t W,
                                                        int64_t w_stride, int64_t batch, TO* __restrict__ C,
-                                                       int64_t ldc, int64_t strideC) {
+                                                       int64_t ldc, int64_t strideC,
+                                                       const int64_t* __restrict__ wdev) {
   const int64_t per_b = m * W;
   const int64_t total = per_b * batch;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = g / per_b, r = g - b * per_b;
     const int64_t h = r / W, t = r - h * W;
+    if (wdev != nullptr && t >= wdev[b]) continue;  // compressed sketch: columns past the count are unused
     const int64_t col = column[b * w_stride + t];
     const double s = scale[b * w_stride + t];
     store_val(C + b * strideC + h * ldc + t, __dmul_rn(load_as_double(M + b * strideM + h * ldm + col), s));
@@ -149,13 +151,15 @@ __global__ void __launch_bounds__(256) gather_d_kernel(const T* __restrict__ N, 
                                                        int64_t p, const int64_t* __restrict__ column,
                                                        const double* __restrict__ scale, int64_t W,
                                                        int64_t w_stride, int64_t batch, TO* __restrict__ D,
-                                                       int64_t ldd, int64_t strideD) {
+                                                       int64_t ldd, int64_t strideD,
+                                                       const int64_t* __restrict__ wdev) {
   const int64_t per_b = W * p;
   const int64_t total = per_b * batch;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = g / per_b, r = g - b * per_b;
     const int64_t t = r / p, f = r - t * p;
+    if (wdev != nullptr && t >= wdev[b]) continue;
     const int64_t row = column[b * w_stride + t];
     const double s = scale[b * w_stride + t];
     store_val(D + b * strideD + t * ldd + f, __dmul_rn(load_as_double(N + b * strideN + row * ldn + f), s));
@@ -195,15 +199,15 @@ template <typename T, typename TO>
 int launch_gather(const T* M, int64_t ldm, int64_t strideM, const T* N, int64_t ldn, int64_t strideN,
                   int64_t m, int64_t p, const int64_t* column, const double* scale, int64_t W,
                   int64_t w_stride, int64_t batch, TO* C, int64_t ldc, int64_t strideC, TO* D,
-                  int64_t ldd, int64_t strideD, cudaStream_t st) {
+                  int64_t ldd, int64_t strideD, cudaStream_t st, const int64_t* wdev = nullptr) {
   if (C != nullptr && m > 0) {
     gather_c_kernel<T, TO><<<grid_for(m * W * batch, 256), 256, 0, st>>>(M, ldm, strideM, m, column, scale, W,
-                                                                     w_stride, batch, C, ldc, strideC);
+                                                                     w_stride, batch, C, ldc, strideC, wdev);
     BMM_CHECK_LAUNCH("gather_c_kernel");
   }
   if (D != nullptr && p > 0) {
     gather_d_kernel<T, TO><<<grid_for(W * p * batch, 256), 256, 0, st>>>(N, ldn, strideN, p, column, scale, W,
-                                                                     w_stride, batch, D, ldd, strideD);
+                                                                     w_stride, batch, D, ldd, strideD, wdev);
     BMM_CHECK_LAUNCH("gather_d_kernel");
   }
   return BMM_OK;
@@ -284,17 +288,15 @@ extern "C" int bmm_sample_reps(const double* probs, const double* cum, const int
                            states, column, prob, scale, as_stream(stream));
 }
 
-extern "C" int bmm_gather(int dtype, int out_dtype, const void* M, int64_t ldm, int64_t strideM,
-                          const void* N, int64_t ldn, int64_t strideN, int64_t m, int64_t p,
-                          const int64_t* column, const double* scale, int64_t W, int64_t w_stride,
-                          int64_t batch, void* C, int64_t ldc, int64_t strideC, void* D, int64_t ldd,
-                          int64_t strideD, void* stream) {
+static int gather_impl(int dtype, int out_dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
+                       int64_t ldn, int64_t strideN, int64_t m, int64_t p, const int64_t* column,
+                       const double* scale, int64_t W, int64_t w_stride, const int64_t* w_dev, int64_t batch, void* C,
+                       int64_t ldc, int64_t strideC, void* D, int64_t ldd, int64_t strideD, cudaStream_t st) {
   BMM_REQUIRE(W >= 0 && batch >= 1, BMM_E_ARG, "bmm_gather: bad shape");
   if (W == 0) return BMM_OK;
-  cudaStream_t st = as_stream(stream);
 #define BMM_GATHER_CASE(TI, TO)                                                                       \
   return launch_gather<TI, TO>((const TI*)M, ldm, strideM, (const TI*)N, ldn, strideN, m, p, column, \
-                               scale, W, w_stride, batch, (TO*)C, ldc, strideC, (TO*)D, ldd, strideD, st)
+                               scale, W, w_stride, batch, (TO*)C, ldc, strideC, (TO*)D, ldd, strideD, st, w_dev)
   if (dtype == BMM_F64 && out_dtype == BMM_F64) BMM_GATHER_CASE(double, double);
   if (dtype == BMM_F32 && out_dtype == BMM_F64) BMM_GATHER_CASE(float, double);
   if (dtype == BMM_F32 && out_dtype == BMM_F32) BMM_GATHER_CASE(float, float);
@@ -302,6 +304,25 @@ extern "C" int bmm_gather(int dtype, int out_dtype, const void* M, int64_t ldm, 
 #undef BMM_GATHER_CASE
   set_error("bmm_gather: unknown dtype %d/%d", dtype, out_dtype);
   return BMM_E_ARG;
+}
+
+extern "C" int bmm_gather(int dtype, int out_dtype, const void* M, int64_t ldm, int64_t strideM,
+                          const void* N, int64_t ldn, int64_t strideN, int64_t m, int64_t p,
+                          const int64_t* column, const double* scale, int64_t W, int64_t w_stride,
+                          int64_t batch, void* C, int64_t ldc, int64_t strideC, void* D, int64_t ldd,
+                          int64_t strideD, void* stream) {
+  return gather_impl(dtype, out_dtype, M, ldm, strideM, N, ldn, strideN, m, p, column, scale, W, w_stride, nullptr,
+                     batch, C, ldc, strideC, D, ldd, strideD, as_stream(stream));
+}
+
+extern "C" int bmm_gather_dk(int dtype, int out_dtype, const void* M, int64_t ldm, int64_t strideM,
+                             const void* N, int64_t ldn, int64_t strideN, int64_t m, int64_t p,
+                             const int64_t* column, const double* scale, int64_t W, int64_t w_stride,
+                             const int64_t* w_dev, int64_t batch, void* C, int64_t ldc, int64_t strideC, void* D,
+                             int64_t ldd, int64_t strideD, void* stream) {
+  BMM_REQUIRE(w_dev != nullptr, BMM_E_ARG, "bmm_gather_dk: w_dev is NULL");
+  return gather_impl(dtype, out_dtype, M, ldm, strideM, N, ldn, strideN, m, p, column, scale, W, w_stride, w_dev,
+                     batch, C, ldc, strideC, D, ldd, strideD, as_stream(stream));
 }
 
 extern "C" int bmm_gather_blocks(int dtype, const void* M, int64_t ldm, const void* N, int64_t ldn,

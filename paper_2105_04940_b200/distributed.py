@@ -226,8 +226,8 @@ class ShardedApproxProduct:
                 P(ksc), P(kcnt), st)
         C = torch.empty((ma, W), dtype=torch.float64, device=dev)
         D = torch.empty((W, pb), dtype=torch.float64, device=dev)
-        self._c("bmm_gather", dt, _lib.BMM_F64, P(M_local), M_local.stride(0), 0, P(N_local), N_local.stride(0), 0,
-                ma, pb, P(kcol), P(ksc), W, W, 1, P(C), W, 0, P(D), pb, 0, st)
+        self._c("bmm_gather_dk", dt, _lib.BMM_F64, P(M_local), M_local.stride(0), 0, P(N_local), N_local.stride(0),
+                0, ma, pb, P(kcol), P(ksc), W, W, P(kcnt), 1, P(C), W, 0, P(D), pb, 0, st)
         out = torch.empty((ma, pb), dtype=torch.float64, device=dev)
         ws = _lib.workspace(self.lib.bmm_gemm_f64_workspace(ma, pb, W, 1))
         self._c("bmm_gemm_f64_dk", P(C), W, 0, P(D), pb, 0, ma, pb, W, P(kcnt), 1, P(out), pb, 0, P(ws), ws.numel(),

@@ -377,8 +377,8 @@ class SketchPipeline:
             # duplicates of a column share its scale: contract the distinct columns only
             self._c("bmm_compress_sketch", P(self.column), P(self.scale), W, W, n, B, P(self.ws_cmp),
                     self.ws_cmp.numel(), P(self.k_column), P(self.k_scale), P(self.k_count), st)
-            self._c("bmm_gather", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
-                    P(self.k_scale), W, W, B, P(self.C), W, m * W, P(self.D), p, W * p, st)
+            self._c("bmm_gather_dk", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
+                    P(self.k_scale), W, W, P(self.k_count), B, P(self.C), W, m * W, P(self.D), p, W * p, st)
             self._c("bmm_gemm_f64_dk", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, P(self.k_count), B,
                     P(self.CD), p, m * p, P(self.ws_gemm), self.ws_gemm.numel(), st)
         else:
