@@ -568,16 +568,18 @@ def run_device(args):
 
     norms_ms = timed(lambda: lib.bmm_norms(1, P(Md), m, n, n, m * n, P(Nd), p, p, n * p, B, 0, P(pipe.colsq),
                                            P(pipe.rowsq), st))
-    gather_ms = timed(lambda: lib.bmm_gather_f32split(1, P(Md), n, m * n, P(Nd), p, n * p, m, p, P(pipe.column),
-                                                    P(pipe.scale), W, W, B, P(pipe.a_hi), P(pipe.a_x),
-                                                    P(pipe.b_hi), P(pipe.b_x), st))
-    gemm_ms = timed(lambda: lib.bmm_gemm_f32split(P(pipe.a_hi), P(pipe.a_x), P(pipe.b_hi), P(pipe.b_x), m, p, W, B,
-                                                P(pipe.CD), p, m * p, st))
+    gather_ms = timed(lambda: lib.bmm_gather_f32split_dk(1, P(Md), n, m * n, P(Nd), p, n * p, m, p,
+                                                       P(pipe.k_column), P(pipe.k_scale), W, W, P(pipe.k_count), B,
+                                                       P(pipe.a_hi), P(pipe.a_x), P(pipe.b_hi), P(pipe.b_x), st))
+    gemm_ms = timed(lambda: lib.bmm_gemm_f32split_dk(P(pipe.a_hi), P(pipe.a_x), P(pipe.b_hi), P(pipe.b_x), m, p, W,
+                                                   P(pipe.k_count), B, P(pipe.CD), p, m * p, st))
+    kcounts = pipe.k_count.cpu().numpy()
+    k_exec = int((((kcounts + 31) // 32) * 32).sum())  # columns the compressed contraction runs over
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peak.get("hbm_gbs", 6650.0))
     tf32_peak = float(peak.get("bf16_tflops", 1590.0)) / 2  # dense TF32 issues at half the BF16 rate
     norm_bytes = 4 * B * (m * n + n * p)
-    useful = 2.0 * B * m * p * W
+    useful = 2.0 * m * p * k_exec  # over the distinct drawn columns (compressed sketch, padded to 32)
     executed = 2 * useful  # one TF32 K=8 MMA + one BF16 K=16 MMA (same cycles) per 8 K-elements
 
     # error metric on a verification subset (exact product by our DMMA GEMM on float64 upcasts)
@@ -614,6 +616,7 @@ def run_device(args):
         "vs_baseline": None, "dtype": "f32 (TF32 + BF16 split-operand tensor, f64 plan)",
         "data": "synthetic (seeded torch generator on device, SURVEY.md §8(d) distributions)",
         "config": {"workload": name, "batch": B, "m": m, "n": n, "p": p, "K": K, "W": W, "method": "ONC",
+                   "distinct_columns_mean": float(kcounts.mean()),
                    "l2": f"inputs {norm_bytes / 1e9:.1f} GB >> L2"},
         "gpu_launches": int(pipe.graph_launches),
         "roofline": {"bound": "tensor", "kernel": "gemm_f32split_kernel (tcgen05 kind::tf32 + kind::f16 cross terms)",

@@ -328,6 +328,17 @@ int bmm_gather_f32split(int dtype, const void* M, int64_t ldm, int64_t strideM,
 int bmm_gemm_f32split(const float* a_hi, const void* a_x, const float* b_hi, const void* b_x,
                       int64_t m, int64_t nc, int64_t k, int64_t batch,
                       float* out, int64_t ldo, int64_t strideO, void* stream);
+/* Compressed-sketch variants (bmm_compress_sketch): the gather writes and the
+ * contraction reads only the first ceil(count[b] / 32) * 32 sketch columns of
+ * problem b (the compression zero-pads the scales past the count).          */
+int bmm_gather_f32split_dk(int dtype, const void* M, int64_t ldm, int64_t strideM,
+                           const void* N, int64_t ldn, int64_t strideN, int64_t m, int64_t p,
+                           const int64_t* column, const double* scale, int64_t W, int64_t w_stride,
+                           const int64_t* w_dev, int64_t batch, float* a_hi, void* a_x,
+                           float* b_hi, void* b_x, void* stream);
+int bmm_gemm_f32split_dk(const float* a_hi, const void* a_x, const float* b_hi, const void* b_x,
+                         int64_t m, int64_t nc, int64_t k_max, const int64_t* k_dev, int64_t batch,
+                         float* out, int64_t ldo, int64_t strideO, void* stream);
 
 /* sum of a float64 vector segment in numpy pairwise order: out[b] = 0 + pw(x[b, 0:len])
  * (used for ||M||_F^2 = pw(colsq), ||N||_F^2 = pw(rowsq)).                */

@@ -83,6 +83,9 @@ SIGNATURES = {
     "bmm_pairwise_sum": (_I, [_P, _I64, _I64, _I64, _P, _P]),
     "bmm_gather_f32split": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _I64,
                                _P, _P, _P, _P, _P]),
+    "bmm_gather_f32split_dk": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _P, _I64,
+                                    _P, _P, _P, _P, _P]),
+    "bmm_gemm_f32split_dk": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P]),
     "bmm_gemm_f32split": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _I64, _P]),
 }
 

@@ -140,7 +140,7 @@ constexpr int T_WARPS = 6;
 __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
     const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_ax,
     const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_bx, int64_t m, int64_t nc,
-    int64_t k, float* __restrict__ out, int64_t ldo, int64_t strideO) {
+    int64_t k, float* __restrict__ out, int64_t ldo, int64_t strideO, const int64_t* __restrict__ kdev) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_STAGES * T_STAGE_BYTES);
@@ -165,6 +165,10 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
     const int gsz = min(tm - first_m, GROUP_M);
     tile_m = first_m + (lin % (GROUP_M * tn)) % gsz;
     tile_n = (lin % (GROUP_M * tn)) / gsz;
+  }
+  if (kdev != nullptr) {  // compressed sketch: contract the first ceil32(count) columns (zero-padded)
+    const int64_t kd = ((kdev[b] + T_BK - 1) / T_BK) * T_BK;
+    k = kd < k ? kd : k;
   }
   const int a_row0 = (int)(b * m + (int64_t)tile_m * T_BM);
   const int b_row0 = (int)(b * nc + (int64_t)tile_n * T_BN);
@@ -311,11 +315,13 @@ __global__ void __launch_bounds__(256) gather_a_split_kernel(const T* __restrict
                                                              int64_t m, const int64_t* __restrict__ column,
                                                              const double* __restrict__ scale, int64_t W,
                                                              int64_t w_stride, float* __restrict__ ahi,
-                                                             __nv_bfloat16* __restrict__ ax) {
+                                                             __nv_bfloat16* __restrict__ ax,
+                                                             const int64_t* __restrict__ wdev) {
   const int64_t b = blockIdx.z;
   const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
   const int64_t h0 = (int64_t)blockIdx.y * A_ROWS;
   if (t >= W) return;
+  if (wdev != nullptr && t >= ((wdev[b] + 31) / 32) * 32) return;  // past the GEMM's K of a compressed sketch
   const int64_t col = column[b * w_stride + t];
   const double sc = scale[b * w_stride + t];
   const T* src = M + b * strideM + col;
@@ -341,12 +347,14 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
                                                               int64_t p, const int64_t* __restrict__ column,
                                                               const double* __restrict__ scale, int64_t W,
                                                               int64_t w_stride, float* __restrict__ bhi,
-                                                              __nv_bfloat16* __restrict__ bx) {
+                                                              __nv_bfloat16* __restrict__ bx,
+                                                              const int64_t* __restrict__ wdev) {
   __shared__ float sh[32][129], sl[32][129];
   __shared__ int64_t scol[32];
   __shared__ double sscale[32];
   const int64_t b = blockIdx.z;
   const int64_t t0 = (int64_t)blockIdx.x * 32, f0 = (int64_t)blockIdx.y * 128;
+  if (wdev != nullptr && t0 >= ((wdev[b] + 31) / 32) * 32) return;  // whole CTA past the compressed K
   const int tid = threadIdx.x;
   if (tid < 32) {
     const int64_t t = t0 + tid;
@@ -416,30 +424,29 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
 
 using namespace bmm;
 
-extern "C" int bmm_gather_f32split(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
-                                   int64_t ldn, int64_t strideN, int64_t m, int64_t p, const int64_t* column,
-                                   const double* scale, int64_t W, int64_t w_stride, int64_t batch, float* a_hi,
-                                   void* a_x, float* b_hi, void* b_x, void* stream) {
+static int gather_split_impl(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N, int64_t ldn,
+                             int64_t strideN, int64_t m, int64_t p, const int64_t* column, const double* scale,
+                             int64_t W, int64_t w_stride, const int64_t* w_dev, int64_t batch, float* a_hi, void* a_x,
+                             float* b_hi, void* b_x, cudaStream_t st) {
   BMM_REQUIRE(m >= 1 && p >= 1 && W >= 1 && batch >= 1, BMM_E_ARG, "bmm_gather_f32split: bad shape");
   BMM_REQUIRE(W % 8 == 0, BMM_E_UNSUPPORTED, "bmm_gather_f32split: W must be a multiple of 8");
   __nv_bfloat16* ax = (__nv_bfloat16*)a_x;
   __nv_bfloat16* bx = (__nv_bfloat16*)b_x;
   BMM_REQUIRE(batch <= 65535 && ceil_div(m, A_ROWS) <= 65535, BMM_E_UNSUPPORTED, "bmm_gather_f32split: grid too large");
-  cudaStream_t st = as_stream(stream);
   dim3 agrid((unsigned)ceil_div(W, 256), (unsigned)ceil_div(m, A_ROWS), (unsigned)batch);
   dim3 tgrid((unsigned)ceil_div(W, 32), (unsigned)ceil_div(p, 128), (unsigned)batch);
   if (dtype == BMM_F32) {
     gather_a_split_kernel<float><<<agrid, 256, 0, st>>>((const float*)M, ldm, strideM, m, column, scale, W, w_stride,
-                                                        a_hi, ax);
+                                                        a_hi, ax, w_dev);
     BMM_CHECK_LAUNCH("gather_a_split_kernel");
     gather_bt_split_kernel<float><<<tgrid, 256, 0, st>>>((const float*)N, ldn, strideN, p, column, scale, W,
-                                                         w_stride, b_hi, bx);
+                                                         w_stride, b_hi, bx, w_dev);
   } else if (dtype == BMM_F64) {
     gather_a_split_kernel<double><<<agrid, 256, 0, st>>>((const double*)M, ldm, strideM, m, column, scale, W,
-                                                         w_stride, a_hi, ax);
+                                                         w_stride, a_hi, ax, w_dev);
     BMM_CHECK_LAUNCH("gather_a_split_kernel");
     gather_bt_split_kernel<double><<<tgrid, 256, 0, st>>>((const double*)N, ldn, strideN, p, column, scale, W,
-                                                          w_stride, b_hi, bx);
+                                                          w_stride, b_hi, bx, w_dev);
   } else {
     set_error("bmm_gather_f32split: unknown dtype %d", dtype);
     return BMM_E_ARG;
@@ -448,9 +455,26 @@ extern "C" int bmm_gather_f32split(int dtype, const void* M, int64_t ldm, int64_
   return BMM_OK;
 }
 
-extern "C" int bmm_gemm_f32split(const float* a_hi, const void* a_x, const float* b_hi, const void* b_x,
-                                 int64_t m, int64_t nc, int64_t k, int64_t batch, float* out, int64_t ldo,
-                                 int64_t strideO, void* stream) {
+extern "C" int bmm_gather_f32split(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
+                                   int64_t ldn, int64_t strideN, int64_t m, int64_t p, const int64_t* column,
+                                   const double* scale, int64_t W, int64_t w_stride, int64_t batch, float* a_hi,
+                                   void* a_x, float* b_hi, void* b_x, void* stream) {
+  return gather_split_impl(dtype, M, ldm, strideM, N, ldn, strideN, m, p, column, scale, W, w_stride, nullptr, batch,
+                           a_hi, a_x, b_hi, b_x, as_stream(stream));
+}
+
+extern "C" int bmm_gather_f32split_dk(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
+                                      int64_t ldn, int64_t strideN, int64_t m, int64_t p, const int64_t* column,
+                                      const double* scale, int64_t W, int64_t w_stride, const int64_t* w_dev,
+                                      int64_t batch, float* a_hi, void* a_x, float* b_hi, void* b_x, void* stream) {
+  BMM_REQUIRE(w_dev != nullptr, BMM_E_ARG, "bmm_gather_f32split_dk: w_dev is NULL");
+  return gather_split_impl(dtype, M, ldm, strideM, N, ldn, strideN, m, p, column, scale, W, w_stride, w_dev, batch,
+                           a_hi, a_x, b_hi, b_x, as_stream(stream));
+}
+
+static int gemm_split_impl(const float* a_hi, const void* a_x, const float* b_hi, const void* b_x, int64_t m,
+                           int64_t nc, int64_t k, const int64_t* k_dev, int64_t batch, float* out, int64_t ldo,
+                           int64_t strideO, void* stream) {
   BMM_REQUIRE(m >= 1 && nc >= 1 && k >= 1 && batch >= 1, BMM_E_ARG, "bmm_gemm_f32split: bad shape");
   BMM_REQUIRE(k % 8 == 0, BMM_E_UNSUPPORTED, "bmm_gemm_f32split: k must be a multiple of 8");
   const float* a_lo = (const float*)a_x;  // bf16 pairs: the same bytes per row as k floats
@@ -470,7 +494,20 @@ extern "C" int bmm_gemm_f32split(const float* a_hi, const void* a_x, const float
   }
   dim3 grid((unsigned)ceil_div(nc, T_BN), (unsigned)ceil_div(m, T_BM), (unsigned)batch);
   gemm_f32split_kernel<<<grid, 32 * T_WARPS, T_SMEM_BYTES, as_stream(stream)>>>(ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out,
-                                                                         ldo, strideO);
+                                                                         ldo, strideO, k_dev);
   BMM_CHECK_LAUNCH("gemm_f32split_kernel");
   return BMM_OK;
+}
+
+extern "C" int bmm_gemm_f32split(const float* a_hi, const void* a_x, const float* b_hi, const void* b_x,
+                                 int64_t m, int64_t nc, int64_t k, int64_t batch, float* out, int64_t ldo,
+                                 int64_t strideO, void* stream) {
+  return gemm_split_impl(a_hi, a_x, b_hi, b_x, m, nc, k, nullptr, batch, out, ldo, strideO, stream);
+}
+
+extern "C" int bmm_gemm_f32split_dk(const float* a_hi, const void* a_x, const float* b_hi, const void* b_x,
+                                    int64_t m, int64_t nc, int64_t k_max, const int64_t* k_dev, int64_t batch,
+                                    float* out, int64_t ldo, int64_t strideO, void* stream) {
+  BMM_REQUIRE(k_dev != nullptr, BMM_E_ARG, "bmm_gemm_f32split_dk: k_dev is NULL");
+  return gemm_split_impl(a_hi, a_x, b_hi, b_x, m, nc, k_max, k_dev, batch, out, ldo, strideO, stream);
 }

@@ -205,17 +205,6 @@ class ShardedApproxProduct:
         self._c("bmm_sample", P(probs), P(self.cum), P(self.last), P(self.offsets), K, 1, n, max(self.sizes),
                 P(self.budgets), P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
         ma, pb = self.ma, self.pb
-        if M_local.dtype == torch.float32 and W % 8 == 0:
-            a_hi = torch.empty(ma * W, dtype=torch.float32, device=M_local.device)
-            a_x = torch.empty_like(a_hi)
-            b_hi = torch.empty(pb * W, dtype=torch.float32, device=M_local.device)
-            b_x = torch.empty_like(b_hi)
-            Nc = N_local.contiguous()
-            self._c("bmm_gather_f32split", dt, P(M_local), M_local.stride(0), 0, P(Nc), Nc.stride(0), 0, ma, pb,
-                    P(self.column), P(self.scale), W, W, 1, P(a_hi), P(a_x), P(b_hi), P(b_x), st)
-            out = torch.empty((ma, pb), dtype=torch.float32, device=M_local.device)
-            self._c("bmm_gemm_f32split", P(a_hi), P(a_x), P(b_hi), P(b_x), ma, pb, W, 1, P(out), pb, 0, st)
-            return out
         # compressed sketch (one term per distinct drawn column), as SketchPipeline
         dev = M_local.device
         kcol = torch.empty(W, dtype=torch.int64, device=dev)
@@ -224,6 +213,18 @@ class ShardedApproxProduct:
         wsc = _lib.workspace(self.lib.bmm_compress_workspace(n, 1))
         self._c("bmm_compress_sketch", P(self.column), P(self.scale), W, W, n, 1, P(wsc), wsc.numel(), P(kcol),
                 P(ksc), P(kcnt), st)
+        if M_local.dtype == torch.float32 and W % 8 == 0:
+            a_hi = torch.empty(ma * W, dtype=torch.float32, device=dev)
+            a_x = torch.empty_like(a_hi)
+            b_hi = torch.empty(pb * W, dtype=torch.float32, device=dev)
+            b_x = torch.empty_like(b_hi)
+            Nc = N_local.contiguous()
+            self._c("bmm_gather_f32split_dk", dt, P(M_local), M_local.stride(0), 0, P(Nc), Nc.stride(0), 0, ma, pb,
+                    P(kcol), P(ksc), W, W, P(kcnt), 1, P(a_hi), P(a_x), P(b_hi), P(b_x), st)
+            out = torch.empty((ma, pb), dtype=torch.float32, device=dev)
+            self._c("bmm_gemm_f32split_dk", P(a_hi), P(a_x), P(b_hi), P(b_x), ma, pb, W, P(kcnt), 1, P(out), pb, 0,
+                    st)
+            return out
         C = torch.empty((ma, W), dtype=torch.float64, device=dev)
         D = torch.empty((W, pb), dtype=torch.float64, device=dev)
         self._c("bmm_gather_dk", dt, _lib.BMM_F64, P(M_local), M_local.stride(0), 0, P(N_local), N_local.stride(0),

@@ -161,7 +161,13 @@ class SketchPipeline:
         self.scale = torch.empty(B * W, **f64)
         # float32 inputs take the tcgen05 split-operand path (pair groups need W % 8 == 0)
         self.tf32 = (dtype == torch.float32 and method != "SSM" and W % 8 == 0)
-        self.compress = False
+        # compressed sketch: one rank-1 term per distinct drawn column (bmm_compress_sketch)
+        self.compress = bool(compress) and method != "SSM"
+        if self.compress:
+            self.k_column = torch.empty(B * W, **i64)
+            self.k_scale = torch.empty(B * W, **f64)
+            self.k_count = torch.empty(B, **i64)
+            self.ws_cmp = torch.empty(max(256, self.lib.bmm_compress_workspace(n_, B)), dtype=torch.uint8, device=dev)
         if self.tf32:
             f32 = dict(dtype=torch.float32, device=dev)
             self.a_hi = torch.empty(B * self.m * W, **f32)
@@ -179,14 +185,6 @@ class SketchPipeline:
             self.CD = torch.empty(B * self.m * self.p, **f64)
             self.ws_gemm = torch.empty(max(256, self.lib.bmm_gemm_f64_workspace(self.m, self.p, W, B)),
                                        dtype=torch.uint8, device=dev)
-            # compressed sketch: one rank-1 term per distinct drawn column (bmm_compress_sketch)
-            self.compress = bool(compress) and method != "SSM"
-            if self.compress:
-                self.k_column = torch.empty(B * W, **i64)
-                self.k_scale = torch.empty(B * W, **f64)
-                self.k_count = torch.empty(B, **i64)
-                self.ws_cmp = torch.empty(max(256, self.lib.bmm_compress_workspace(n_, B)), dtype=torch.uint8,
-                                          device=dev)
         if method == "OPL":
             self.gsq = torch.empty(B * K, **f64)
             self.ws_seg = torch.empty(max(256, self.lib.bmm_segsq_f64_workspace(self.m, self.p, K, B)),
@@ -367,16 +365,23 @@ class SketchPipeline:
         self._c("bmm_sample", P(probs), P(self.cum), P(self.last), P(self.offsets), K, B, n, self.max_len,
                 P(self.budgets),
                 P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
-        if self.tf32:
+        if self.compress:
+            # duplicates of a column share its scale: contract the distinct columns only
+            self._c("bmm_compress_sketch", P(self.column), P(self.scale), W, W, n, B, P(self.ws_cmp),
+                    self.ws_cmp.numel(), P(self.k_column), P(self.k_scale), P(self.k_count), st)
+        if self.tf32 and self.compress:
             # float32 inputs: split gather + tcgen05 TF32 / BF16-cross-term contraction
+            self._c("bmm_gather_f32split_dk", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
+                    P(self.k_scale), W, W, P(self.k_count), B, P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x),
+                    st)
+            self._c("bmm_gemm_f32split_dk", P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), m, p, W,
+                    P(self.k_count), B, P(self.CD), p, m * p, st)
+        elif self.tf32:
             self._c("bmm_gather_f32split", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column), P(self.scale), W, W,
                     B, P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), st)
             self._c("bmm_gemm_f32split", P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), m, p, W, B,
                     P(self.CD), p, m * p, st)
         elif self.compress:
-            # duplicates of a column share its scale: contract the distinct columns only
-            self._c("bmm_compress_sketch", P(self.column), P(self.scale), W, W, n, B, P(self.ws_cmp),
-                    self.ws_cmp.numel(), P(self.k_column), P(self.k_scale), P(self.k_count), st)
             self._c("bmm_gather_dk", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
                     P(self.k_scale), W, W, P(self.k_count), B, P(self.C), W, m * W, P(self.D), p, W * p, st)
             self._c("bmm_gemm_f64_dk", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, P(self.k_count), B,
