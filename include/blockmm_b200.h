@@ -176,7 +176,7 @@ int bmm_sample_reps(const double* probs, const double* cum, const int64_t* last_
  * s_i = 1/sqrt(c_k p_i), so c_i duplicates contribute c_i s_i^2 M[:,i] N[i,:]
  * to C @ D (estimators.py:78-80,175).  Writes the distinct drawn columns in
  * column order to out_column[0..count) with out_scale = s_i sqrt(c_i), zero
- * padding up to W, and count per problem in out_count (device).  Gathering and
+ * padding up to min(W, ceil32(count)), and count per problem in out_count.  Gathering and
  * contracting (bmm_gemm_f64_dk) the compressed sketch gives C @ D up to
  * rounding with one rank-1 term per distinct column.  Deterministic.
  * Workspace bmm_compress_workspace(n, batch) bytes.                          */

@@ -544,7 +544,7 @@ using DV5 = DCfg<64, 64, 32, 32, 4>;
 using DV6 = DCfg<128, 64, 32, 32, 3>;
 constexpr int kVariants = 7;
 static int g_variant = 2;      // C.D / exact-product tiles: 128x64, 4 warps of 64x32 (tools/tune_dmma.py)
-static int g_seg_variant = 0;  // segmented square sums: 64x64, 4 warps of 32x32
+static int g_seg_variant = 5;  // segmented square sums: 64x64, 4 warps of 32x32, 4 stages (tools/tune_dmma.py)
 
 struct VariantInfo {
   int BM, BN, BK, threads, smem, occ;

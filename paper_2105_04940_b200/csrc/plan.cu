@@ -146,9 +146,37 @@ __global__ void __launch_bounds__(kProbCtaThreads) block_probs_cta_kernel(
   }
   __syncthreads();
   for (int64_t i = tid; i < nk; i += kProbCtaThreads) pb[i] = wb[i];
-  if (cum != nullptr && warp == 0) {
-    const int64_t lst = warp_cumsum(wb, cum + b * n + o, nk);
-    if (lane == 0) last[g] = lst;
+  if (cum != nullptr) {
+    // np.cumsum: one thread runs the chain out of shared memory (independent
+    // loads, one dependent add per element), then the CTA stores it
+    double* wc = wb + nk;
+    if (tid == 0) {
+      double acc = 0.0;  // 0 + p[0] == p[0]: probabilities are never -0
+#pragma unroll 8
+      for (int64_t i = 0; i < nk; ++i) {
+        acc = __dadd_rn(acc, wb[i]);
+        wc[i] = acc;
+      }
+    }
+    // last index with p > 0 (the support clamp of _draw_indices, estimators.py:38-44)
+    int64_t lst = -1;
+    for (int64_t i = tid; i < nk; i += kProbCtaThreads)
+      if (wb[i] > 0.0) lst = i;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const int64_t v = __shfl_xor_sync(0xffffffffu, lst, off);
+      lst = v > lst ? v : lst;
+    }
+    __shared__ int64_t wl[kProbCtaThreads / 32];
+    if (lane == 0) wl[warp] = lst;
+    __syncthreads();
+    double* cb = cum + b * n + o;
+    for (int64_t i = tid; i < nk; i += kProbCtaThreads) cb[i] = wc[i];
+    if (tid == 0) {
+      int64_t m = -1;
+      for (int w = 0; w < kProbCtaThreads / 32; ++w) m = wl[w] > m ? wl[w] : m;
+      last[g] = m;
+    }
   }
 }
 
@@ -598,14 +626,14 @@ extern "C" int bmm_block_probs(const double* colsq, const double* rowsq, int64_t
   unsigned grid = (unsigned)std::min<int64_t>(ceil_div(warps, kProbWarps), 148LL * 16 * 64);
   const int64_t smem = max_len * 8 * kProbWarps;
   cudaStream_t st = as_stream(stream);
-  if (probs != nullptr && fnorm == nullptr && max_len > 256 && max_len * 8 <= 160 * 1024 &&
+  if (probs != nullptr && fnorm == nullptr && max_len > 256 && max_len * 16 <= 160 * 1024 &&
       K * batch < (1LL << 31)) {
     static bool attr_c = false;
     if (!attr_c) {
       cudaFuncSetAttribute(block_probs_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
       attr_c = true;
     }
-    block_probs_cta_kernel<<<(unsigned)(K * batch), kProbCtaThreads, (size_t)(max_len * 8), st>>>(
+    block_probs_cta_kernel<<<(unsigned)(K * batch), kProbCtaThreads, (size_t)(max_len * 16), st>>>(
         colsq, rowsq, n, offsets, K, probs, s, cum, last_support);
   } else if (smem <= 160 * 1024) {
     static int64_t attr = 0;
@@ -664,7 +692,9 @@ extern "C" int bmm_budgets(int rule, const double* s, const double* aux, const i
       attr = true;
     }
   }
-  budgets_kernel<<<(unsigned)batch, kBudgetThreads, smem ? (size_t)bytes : 0, as_stream(stream)>>>(
+  // few blocks: fewer threads, so the fixpoint's block-wide reductions and barriers are cheap
+  const int nt = K <= 64 ? 64 : (K <= 128 ? 128 : kBudgetThreads);
+  budgets_kernel<<<(unsigned)batch, nt, smem ? (size_t)bytes : 0, as_stream(stream)>>>(
       rule, s, aux, sizes, caps, floors, K, c, cap, budgets, col_off, status, diag, notes, (char*)ws, smem ? 1 : 0);
   BMM_CHECK_LAUNCH("budgets_kernel");
   return BMM_OK;

@@ -53,6 +53,8 @@ constexpr int kSampleWarps = 4;
 
 // One warp per block.  SMEM: the block's CDF is staged in shared memory
 // (max_len doubles per warp) so the binary searches stay on chip.
+constexpr int64_t kSampleChunk = 128;  // draws per warp work item
+
 // SHARED: one plan (probs, cum, last, budgets, col_off) for every problem b --
 // Monte Carlo replications; only the streams and outputs are per problem.
 template <bool SMEM, bool SHARED = false>
@@ -68,13 +70,20 @@ __global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
   if (w >= wpb) return;
   double* scum = scum_all + (SMEM ? 2 * w * max_len : 0);
   double* sprob = scum + max_len;
-  const int64_t warps_total = K * batch;
+  // work slots: (draw chunk, problem, block), chunk-major so that the first
+  // chunks of every block come first and empty slots (chunk beyond the budget)
+  // cluster at the end; a chunk is kSampleChunk consecutive draws of one block
+  const int64_t cmax = (w_stride + kSampleChunk - 1) / kSampleChunk;
+  const int64_t warps_total = K * batch * cmax;
   for (int64_t g = blockIdx.x * (int64_t)wpb + w; g < warps_total; g += (int64_t)gridDim.x * wpb) {
-    const int64_t b = g / K, k = g - b * K;
+    const int64_t ch = g / (K * batch), r = g - ch * (K * batch);
+    const int64_t b = r / K, k = r - b * K;
     const int64_t pb_ = SHARED ? 0 : b;  // plan index
     const int64_t gp = pb_ * K + k;
     const int64_t ck = budgets[gp];
-    if (ck <= 0) continue;
+    const int64_t c0 = ch * kSampleChunk;
+    if (c0 >= ck) continue;
+    const int64_t c1 = min(ck, c0 + kSampleChunk);
     const int64_t o = offsets[k], len = offsets[k + 1] - o;
     const double* cb = cum + pb_ * n + o;
     const double* pb = probs + pb_ * n + o;
@@ -89,15 +98,15 @@ __global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
       pb = sprob;
     }
     const int64_t lst = last[gp];
-    const uint64_t* sp = states + 4 * g;
+    const uint64_t* sp = states + 4 * (b * K + k);
     U128 st{sp[0], sp[1]}, inc{sp[2], sp[3]};
     U128 m1, p1, m32, p32;
-    pcg_jump((uint64_t)lane + 1, inc, m1, p1);
+    pcg_jump((uint64_t)(c0 + lane) + 1, inc, m1, p1);
     pcg_jump(32, inc, m32, p32);
     st = add128(mul128(m1, st), p1);
     const double dck = (double)ck;
     const int64_t t0 = col_off[pb_ * (K + 1) + k];
-    for (int64_t j = lane; j < ck; j += 32) {
+    for (int64_t j = c0 + lane; j < c1; j += 32) {
       const double u = u53(pcg_output(st));
       // first index with cum > u  (searchsorted side="right")
       int64_t lo = 0, hi = len;
@@ -244,7 +253,7 @@ static int sample_impl(const double* probs, const double* cum, const int64_t* la
                        const int64_t* col_off, int64_t w_stride, const uint64_t* states, int64_t* column,
                        double* prob, double* scale, cudaStream_t st) {
   BMM_REQUIRE(K >= 1 && batch >= 1 && max_len >= 1, BMM_E_ARG, "bmm_sample: bad shape");
-  const int64_t warps = K * batch;
+  const int64_t warps = K * batch * ((w_stride + kSampleChunk - 1) / kSampleChunk);
   const int64_t per_warp = 2 * max_len * 8;  // CDF and probabilities
   int wpb = kSampleWarps;
   bool smem = true;
@@ -411,7 +420,9 @@ __global__ void __launch_bounds__(kCompactThreads) sketch_compact_kernel(
       ++pos;
     }
   }
-  for (int64_t u = total + tid; u < W; u += kCompactThreads) {  // padding: zero columns
+  // zero padding up to the next multiple of 32 (the float32 contraction's K step)
+  const int64_t pad_end = min(W, ((total + 31) / 32) * 32);
+  for (int64_t u = total + tid; u < pad_end; u += kCompactThreads) {
     oc[u] = 0;
     os[u] = 0.0;
   }

@@ -12,6 +12,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
 echo "launch list rc=$?"
 python tools/profile_kernels.py > gpurun_out/${TAG}_pk_plain.log 2>&1 &&
 ncu --set full --clock-control none --import-source on \
-    -k regex:'gemm_f64_kernel|segsq_f64_kernel|colsq|rowsq|gemm_f32split|gather' -c 14 \
+    -k regex:'gemm_f64_kernel|segsq_f64_kernel|colsq|rowsq|gemm_f32split|gather|compact|block_probs|budgets|sample_kernel' -c 24 \
     -o gpurun_out/${TAG}_full python tools/profile_kernels.py > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "full capture rc=$?"
