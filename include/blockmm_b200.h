@@ -71,6 +71,13 @@ const char* bmm_last_error(void);
 /* number of kernels this library has launched since load (evidence counter) */
 int64_t bmm_launch_count(void);
 
+/* Strided copy (cudaMemcpy2DAsync; kind 1 = host->device, 2 = device->host,
+ * 3 = device->device), graph-capturable: the streamed end-to-end path copies
+ * block-column slabs of a pinned host M so work on early blocks overlaps the
+ * transfer of later ones.                                                    */
+int bmm_copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes,
+               int64_t height, int kind, void* stream);
+
 /* ---------------------------------------------------------------- K1 norms
  * colsq[b, i] = sum_h M[b][h, i]^2, accumulated sequentially over h in float64
  * (numpy's order for np.linalg.norm(M, axis=0) on a C-ordered matrix,

@@ -41,6 +41,7 @@ SIGNATURES = {
     "bmm_version": (_I, []),
     "bmm_last_error": (ctypes.c_char_p, []),
     "bmm_launch_count": (_I64, []),
+    "bmm_copy2d": (_I, [_P, _I64, _P, _I64, _I64, _I64, _I, _P]),
     "bmm_norms": (_I, [_I, _P, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I, _P, _P, _P]),
     "bmm_block_probs": (_I, [_P, _P, _I64, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
     "bmm_normalize": (_I, [_P, _I64, _I64, _P, _P, _P]),

@@ -312,15 +312,35 @@ class SketchPipeline:
             return self.CD.view(self.m, self.p)
         return self.CD.view(self.B, self.m, self.p) if self.B > 1 else self.CD.view(self.m, self.p)
 
-    def launch(self, M: torch.Tensor, N: torch.Tensor) -> torch.Tensor:
-        """Enqueue the whole pipeline on the current stream (graph-capturable)."""
+    def launch(self, M: torch.Tensor, N: torch.Tensor, chunks=None) -> torch.Tensor:
+        """Enqueue the whole pipeline on the current stream (graph-capturable).
+
+        chunks: optional [(c0, c1, k0, k1, event)] -- block-aligned ranges of the
+        inner dimension whose M columns and N rows are valid once `event` has
+        completed (a chunked host->device transfer).  The norm pass and OPL's
+        segmented square sums then run chunk by chunk behind the transfer; the
+        rest of the pipeline is unchanged (single problem, float64 inputs)."""
         B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W
         dt = _lib.matrix_dtype(M)
         st = _lib.stream_ptr()
         sM, sN = m * n, n * p
         ldm, ldn = M.stride(-2), N.stride(-2)
         P = lambda t: t.data_ptr()  # noqa: E731
-        self._c("bmm_norms", dt, P(M), m, n, ldm, sM, P(N), p, ldn, sN, B, 0, P(self.colsq), P(self.rowsq), st)
+        seg_done = False
+        if chunks is None:
+            self._c("bmm_norms", dt, P(M), m, n, ldm, sM, P(N), p, ldn, sN, B, 0, P(self.colsq), P(self.rowsq), st)
+        else:
+            if B != 1 or M.dtype != torch.float64 or self.method == "SSM":
+                raise ValueError("chunked launch: one float64 problem, non-SSM method")
+            cur = torch.cuda.current_stream()
+            for c0, c1, k0, k1, ev in chunks:
+                cur.wait_event(ev)
+                self._c("bmm_norms", dt, P(M) + 8 * c0, m, c1 - c0, ldm, 0, P(N) + 8 * c0 * ldn, p, ldn, 0, 1, 0,
+                        P(self.colsq) + 8 * c0, P(self.rowsq) + 8 * c0, st)
+                if self.method == "OPL":
+                    self._c("bmm_segsq_f64", P(M), ldm, 0, P(N), ldn, 0, m, p, P(self.offsets) + 8 * k0, k1 - k0,
+                            0, 1, P(self.gsq) + 8 * k0, P(self.ws_seg), self.ws_seg.numel(), st)
+            seg_done = True
         if self.method == "SSM":
             return self._run_ssm(M, N, dt, st)
         # probabilities, score sums and (fused) the main CDF of the optimal probabilities
@@ -330,9 +350,10 @@ class SketchPipeline:
                 "ONU": _lib.RULE_TWO_STEP, "ONMCNR": _lib.RULE_TWO_STEP}[self.method]
         aux = None
         if self.method == "OPL":
-            A, Bm = self._f64(M, N)
-            self._c("bmm_segsq_f64", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p, P(self.offsets), K,
-                    0, B, P(self.gsq), P(self.ws_seg), self.ws_seg.numel(), st)
+            if not seg_done:
+                A, Bm = self._f64(M, N)
+                self._c("bmm_segsq_f64", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p, P(self.offsets), K,
+                        0, B, P(self.gsq), P(self.ws_seg), self.ws_seg.numel(), st)
             aux = self.gsq
         if self.method in ("ONU", "ONMCNR"):
             p0 = self.p0 if self.method == "ONU" else self.probs
@@ -479,6 +500,68 @@ class PipelineGroup:
                 cap.wait_stream(s)
         self.graph_launches = _lib.launches() - n0
         self.graph, self._graph_ptrs = g, (M.data_ptr(), N.data_ptr())
+
+    def capture_host(self, M: torch.Tensor, N: torch.Tensor, M_host: torch.Tensor, N_host: torch.Tensor,
+                     out_host: list, seeds: list, n_chunks: int = 8) -> None:
+        """End-to-end graph from pinned host inputs to pinned host products: M's
+        block-column slabs and N's row slabs are copied chunk by chunk on a copy
+        stream, every branch runs its norm pass (and OPL segmented square sums)
+        on each chunk as it lands, then the rest of its pipeline, then copies its
+        product back.  Replay with run_host()."""
+        pipes = self.pipes
+        sizes = pipes[0].sizes
+        n, m, p = pipes[0].n, pipes[0].m, pipes[0].p
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        bounds = [0]
+        for c in range(1, n_chunks):
+            k = int(np.searchsorted(off, c * n / n_chunks))
+            if bounds[-1] < k < len(sizes):
+                bounds.append(k)
+        bounds.append(len(sizes))
+        plan = [(int(off[k0]), int(off[k1]), k0, k1) for k0, k1 in zip(bounds[:-1], bounds[1:])]
+        for pipe, sd in zip(pipes, seeds):  # seed buffers exist before the warm-up and the capture
+            pipe.set_seeds(sd)
+        cur = torch.cuda.current_stream()
+        side = torch.cuda.Stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):  # warm-up: lazy buffers outside the capture
+            for pipe in pipes:
+                pipe.launch(M, N)
+        cur.wait_stream(side)
+        copy = torch.cuda.Stream()
+        streams = [torch.cuda.Stream() for _ in pipes]
+        g = torch.cuda.CUDAGraph()
+        n0 = _lib.launches()
+        with torch.cuda.graph(g):
+            cap = torch.cuda.current_stream()
+            copy.wait_stream(cap)
+            chunks = []
+            with torch.cuda.stream(copy):
+                cs = _lib.stream_ptr()
+                for c0, c1, k0, k1 in plan:
+                    _lib.call("bmm_copy2d", M.data_ptr() + 8 * c0, 8 * n, M_host.data_ptr() + 8 * c0, 8 * n,
+                              8 * (c1 - c0), m, 1, cs)
+                    nb = 8 * (c1 - c0) * p
+                    _lib.call("bmm_copy2d", N.data_ptr() + 8 * c0 * p, nb, N_host.data_ptr() + 8 * c0 * p, nb, nb, 1,
+                              1, cs)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+                    chunks.append((c0, c1, k0, k1, ev))
+            for s, pipe, oh in zip(streams, pipes, out_host):
+                s.wait_stream(cap)
+                with torch.cuda.stream(s):
+                    out = pipe.launch(M, N, chunks=chunks)
+                    oh.copy_(out.reshape(oh.shape), non_blocking=True)
+            for s in streams + [copy]:
+                cap.wait_stream(s)
+        self.host_graph_launches = _lib.launches() - n0
+        self.host_graph = g
+
+    def run_host(self, seeds: list) -> None:
+        """Replay the end-to-end graph (capture_host); products land in out_host."""
+        for pipe, s in zip(self.pipes, seeds):
+            pipe.set_seeds(s)
+        self.host_graph.replay()
 
     def run(self, M: torch.Tensor, N: torch.Tensor, seeds: list) -> list:
         """One call per member pipeline (same seeds contract as SketchPipeline.run)."""

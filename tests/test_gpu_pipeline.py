@@ -183,3 +183,30 @@ def test_compressed_sketch_matches_draws_and_uncompressed_product():
               oc.data_ptr(), os_.data_ptr(), cnt.data_ptr(), _lib.stream_ptr())
     assert cnt.cpu().tolist() == [kd, kd]
     assert np.array_equal(oc.view(2, W)[1, :kd].cpu().numpy(), uniq)
+
+
+def test_streamed_end_to_end_graph_matches_resident_run():
+    """PipelineGroup.capture_host: chunked host->device transfer with the norm
+    pass and OPL's segmented square sums behind it, products copied back to
+    pinned host buffers -- bit-identical to the device-resident replay."""
+    M, N, sizes = workloads.cfg2(n=4000, m=60, p=50, K=12)
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    runs = [(c, meth) for c in (200, 400) for meth in ("OPL", "ONC", "ONMCNR")]
+    mk = lambda: PipelineGroup([SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs])  # noqa: E731
+    seeds = lambda s: [seeds_from_rngs(meth, [np.random.default_rng(s + i)], len(sizes))  # noqa: E731
+                       for i, (c, meth) in enumerate(runs)]
+    ref = mk()
+    want = [o.cpu().numpy() for o in ref.run(Md, Nd, seeds(7))]
+    grp = mk()
+    Mh, Nh = torch.from_numpy(M).pin_memory(), torch.from_numpy(N).pin_memory()
+    Mx, Nx = torch.empty_like(Md), torch.empty_like(Nd)
+    outs = [torch.empty((60, 50), dtype=torch.float64).pin_memory() for _ in runs]
+    grp.capture_host(Mx, Nx, Mh, Nh, outs, seeds(0), n_chunks=5)
+    for rep in range(2):
+        Mx.zero_()
+        Nx.zero_()
+        grp.run_host(seeds(7))
+        torch.cuda.synchronize()
+        for o, w in zip(outs, want):
+            assert np.array_equal(o.numpy(), w)
+    assert np.array_equal(Mx.cpu().numpy(), M)
