@@ -362,31 +362,54 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
     sscale[tid] = t < W ? scale[b * w_stride + t] : 0.0;
   }
   __syncthreads();
-  const int fx = tid & 127, ty = tid >> 7;  // 128 x 2
-#pragma unroll 4
-  for (int i = ty; i < 32; i += 2) {
-    const int64_t t = t0 + i, f = f0 + fx;
-    float hi = 0.f, lo = 0.f;
-    if (t < W && f < p) {
-      const double x = __dmul_rn(ld_d(N + b * strideN + scol[i] * ldn + f), sscale[i]);
-      split_tf32(x, hi, lo);
+  // reads: 32 lanes x 4 consecutive f per row (16-byte loads when the rows allow),
+  // 8 rows per pass, all 4 passes' loads issued before any is used
+  const int fq = (tid & 31) * 4, ty = tid >> 5;  // 32 x 8
+  const bool vec = (sizeof(T) == 4) && (ldn % 4 == 0) && (strideN % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(N) & 15) == 0) && (f0 + 128 <= p);
+  double v[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = ty + 8 * r;
+    const int64_t t = t0 + i;
+    const T* src = N + b * strideN + scol[i] * ldn + f0 + fq;
+    if (t < W && vec) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(src));
+      v[r][0] = q.x; v[r][1] = q.y; v[r][2] = q.z; v[r][3] = q.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[r][e] = (t < W && f0 + fq + e < p) ? ld_d(src + e) : 0.0;
     }
-    sh[i][fx] = hi;
-    sl[i][fx] = lo;
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = ty + 8 * r;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float hi = 0.f, lo = 0.f;
+      if (t0 + i < W && f0 + fq + e < p) split_tf32(__dmul_rn(v[r][e], sscale[i]), hi, lo);
+      sh[i][fq + e] = hi;
+      sl[i][fq + e] = lo;
+    }
   }
   __syncthreads();
+  // writes: per f row a warp stores 32 hi floats (128 B) and the 64 bf16 of the
+  // pair groups [l_y(8) | h_y(8)] x 4 as 32 packed bf16x2 words (128 B)
   const int tx = tid & 31, fy = tid >> 5;  // 32 x 8
   const int64_t t = t0 + tx;
-  if (t < W) {
-    const int64_t pp = pair_pos(t);
+  const int q = (2 * tx) & 15, tl = 8 * (tx >> 3) + (q & 7);  // this lane's bf16 pair
+  const bool is_h = q >= 8;
 #pragma unroll 4
-    for (int i = fy; i < 128; i += 8) {
-      const int64_t f = f0 + i;
-      if (f < p) {
-        const int64_t row = b * p + f;
-        bhi[row * W + t] = sh[tx][i];
-        bx[row * 2 * W + pp] = __float2bfloat16_rn(sl[tx][i]);      // [l_y | h_y]
-        bx[row * 2 * W + pp + 8] = __float2bfloat16_rn(sh[tx][i]);
+  for (int i = fy; i < 128; i += 8) {
+    const int64_t f = f0 + i;
+    if (f < p) {
+      const int64_t row = b * p + f;
+      if (t < W) bhi[row * W + t] = sh[tx][i];
+      if (t0 + tl < W) {
+        const float a = is_h ? sh[tl][i] : sl[tl][i];
+        const float c = is_h ? sh[tl + 1][i] : sl[tl + 1][i];
+        *reinterpret_cast<__nv_bfloat162*>(bx + row * 2 * W + 2 * t0 + 2 * tx) =
+            __halves2bfloat162(__float2bfloat16_rn(a), __float2bfloat16_rn(c));
       }
     }
   }
