@@ -290,6 +290,22 @@ def run_ours(args):
     fro_m = np.linalg.norm(M_h)
     fro_n = np.linalg.norm(N_h)
 
+    # dominant kernel by device time per step: OPL's segmented square sums when the sweep has OPL
+    # products (3 x 2 m p n flops at cfg2), else the sampled GEMM
+    gemm_step_ms = sum(gemm_ms)
+    roofline_main = None
+    if "segsq_ms" in kt and kt["segsq_ms"] * kt["segsq_per_step"] > gemm_step_ms:
+        seg_flops = 2.0 * m * p * n
+        seg_achieved = seg_flops / (kt["segsq_ms"] * 1e-3) / 1e12
+        roofline_main = {"bound": "tensor", "kernel": "segsq_f64_kernel (OPL g_k^2 = ||M^k N_k||_F^2, DMMA)",
+                         "achieved": seg_achieved, "peak": dgemm_peak, "unit": "TFLOP/s",
+                         "frac": seg_achieved / dgemm_peak,
+                         "peak_source": "cuBLAS dgemm 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
+                         "algorithmic": "2*m*p*n flops per launch", "launch_ms": kt["segsq_ms"],
+                         "share_of_step_device_ms": kt["segsq_ms"] * kt["segsq_per_step"],
+                         "traffic": 164780800 if (m, n, p) == (500, 20000, 500) else None,
+                         "traffic_note": "dram__bytes_read+write per launch, ncu --set full "
+                                         "(profiles/r1c_ncu_full_summary.csv): 0.160 GB + 4.7 MB = M + N read once"}
     line = {
         "metric": METRIC, "value": ms_step, "unit": "ms/step", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
@@ -299,13 +315,16 @@ def run_ours(args):
                    "parallelism": f"replicas x{world}"},
         "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "tensor", "kernel": "gemm_f64_kernel (C.D, DMMA)", "achieved": gemm_achieved,
+        "roofline": roofline_main,
+        "roofline_gemm": {"bound": "tensor", "kernel": "gemm_f64_kernel (C.D, DMMA)", "achieved": gemm_achieved,
                      "peak": dgemm_peak, "unit": "TFLOP/s", "frac": gemm_achieved / dgemm_peak,
                      "peak_source": "cuBLAS dgemm 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
                      "cublas_same_shapes_tflops": sum(gemm_flops) / (sum(kt["cublas_same_shape_ms"]) * 1e-3) / 1e12,
                      "flops_note": "executed 2*m*p*K over the distinct drawn columns (gemm_k); the sketch "
                                    "width W counts duplicates, which the compressed sketch folds into scales",
-                     "traffic": None},
+                     "traffic": 35511000 if (m, p) == (500, 500) else None,
+                     "traffic_note": "ncu --set full, W=16000 ONC launch (profiles/r1c_ncu_full_summary.csv): "
+                                     "35.5 MB = the gathered C and D read once"},
         "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norms_achieved,
                            "peak": hbm_peak, "unit": "GB/s", "frac": norms_achieved / hbm_peak,
                            "algorithmic_bytes": norm_bytes,
@@ -316,6 +335,8 @@ def run_ours(args):
         "rel_err_reference_metric": float(np.sqrt(err_sq / ref_sq)),
         "clocks": clocks.summary(),
     }
+    if line["roofline"] is None:
+        line["roofline"] = line["roofline_gemm"]
     if rank == 0:
         line["cpu_baseline"] = cpu_baseline(M_h, N_h, sizes, runs, cfg, args)
         print(json.dumps(line), flush=True)
@@ -346,6 +367,22 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
         torch.cuda.synchronize()
         reps.append(e0.elapsed_time(e1))
     out["norms_ms"] = float(np.median(reps))
+    # OPL's segmented square sums g_k^2 (K7), once per OPL product
+    opl = [pipe for (cb, W, meth, c0), pipe in zip(runs, pipes) if meth == "OPL"]
+    if opl:
+        pipe = opl[0]
+        reps = []
+        for _ in range(5):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            lib.bmm_segsq_f64(Md.data_ptr(), n, 0, Nd.data_ptr(), p, 0, m, p, pipe.offsets.data_ptr(), pipe.K, 0, 1,
+                              pipe.gsq.data_ptr(), pipe.ws_seg.data_ptr(), pipe.ws_seg.numel(), st)
+            e1.record()
+            torch.cuda.synchronize()
+            reps.append(e0.elapsed_time(e1))
+        out["segsq_ms"] = float(np.median(reps))
+        out["segsq_per_step"] = len(opl)
     # the sampled GEMM of each run (C, D already gathered by the last step): over the
     # distinct drawn columns when the pipeline compresses the sketch (k_count on device)
     out["gemm_k"] = []
