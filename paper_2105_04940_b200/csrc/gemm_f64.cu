@@ -324,7 +324,27 @@ __global__ void __launch_bounds__(C::THREADS) segsq_f64_kernel(const double* __r
   }
   const int64_t tiles = (int64_t)gridDim.x * gridDim.y;
   const int64_t tile = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-  for (int64_t j = j0; j < j1; ++j) {
+  // one segment per CTA (few, unequal segments): longest first, so the tail of
+  // the grid is short segments (rank = # longer segments, ties by index)
+  __shared__ int64_t lpt_j;
+  const bool lpt = (chunks == nseg) && nseg <= 128;
+  if (lpt) {
+    const int64_t* sb = seg + b * seg_stride;
+    if (threadIdx.x == 0) lpt_j = -1;
+    __syncthreads();
+    for (int64_t jj = threadIdx.x; jj < nseg; jj += C::THREADS) {
+      const int64_t lj = sb[jj + 1] - sb[jj];
+      int64_t rank = 0;
+      for (int64_t i = 0; i < nseg; ++i) {
+        const int64_t li = sb[i + 1] - sb[i];
+        rank += (li > lj) || (li == lj && i < jj);
+      }
+      if (rank == ch) lpt_j = jj;
+    }
+    __syncthreads();
+  }
+  for (int64_t jl = j0; jl < j1; ++jl) {
+    const int64_t j = lpt ? lpt_j : jl;
     const int64_t kbeg = seg[b * seg_stride + j], kend = seg[b * seg_stride + j + 1];
     double acc[C::FM][C::FN][2];
 #pragma unroll
