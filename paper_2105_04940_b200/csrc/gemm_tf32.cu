@@ -24,14 +24,28 @@
 
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace bmm {
 
-constexpr int T_BM = 128, T_BN = 128, T_BK = 32, T_STAGES = 3;
-constexpr int T_TILE_BYTES = T_BM * T_BK * 4;                // 16 KB: one operand tile
-constexpr int T_STAGE_BYTES = 4 * T_TILE_BYTES;              // A_hi, A_x, B_hi, B_x
-constexpr int T_SMEM_BYTES = T_STAGES * T_STAGE_BYTES + 1024 + 256;
+constexpr int T_BM = 128, T_BK = 32;
+constexpr int T_TILE_BYTES = T_BM * T_BK * 4;                // 16 KB: one A operand tile (128 rows)
+
+// Tile configurations: 128x128 (3-stage ring, 4 drain warps) or 128x256 (one
+// UMMA of N=256 per step: twice the flops per byte of A staged, 2-stage ring,
+// the full 512-column TMEM for the two chunk accumulators, 8 drain warps)
+template <int BN>
+struct TCfg {
+  static constexpr int STAGES = BN == 128 ? 3 : 2;
+  static constexpr int B_TILE = BN * T_BK * 4;
+  static constexpr int STAGE = 2 * T_TILE_BYTES + 2 * B_TILE;  // A_hi, A_x, B_hi, B_x
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static constexpr int DRAIN = BN / 32;  // drain warps: 32 TMEM lanes x 128 columns each
+  static constexpr int WARPS = 2 + DRAIN;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -75,32 +89,38 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor: F32 accumulate, TF32 A/B, both K-major, M=128, N=128.
-constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(T_BN >> 3) << 17) |
-                                ((uint32_t)(T_BM >> 4) << 24);
+// Instruction descriptor: F32 accumulate, TF32 A/B, both K-major, M=128, N=BN.
+template <int BN>
+constexpr uint32_t idesc_tf32() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(T_BM >> 4) << 24);
+}
 
-__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(kIdescTf32), "r"(accumulate));
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
-// kind::f16 with BF16 A/B, F32 accumulate, K-major, M=128, N=128 (K = 16 per MMA).
-constexpr uint32_t kIdescBf16 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T_BN >> 3) << 17) |
-                                ((uint32_t)(T_BM >> 4) << 24);
+// kind::f16 with BF16 A/B, F32 accumulate, K-major, M=128, N=BN (K = 16 per MMA).
+template <int BN>
+constexpr uint32_t idesc_bf16() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(T_BM >> 4) << 24);
+}
 
-__device__ __forceinline__ void umma_bf16(uint32_t tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+__device__ __forceinline__ void umma_bf16(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(kIdescBf16), "r"(accumulate));
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -135,12 +155,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // chunk into round-to-nearest float32 registers; the error then stays at one
 // chunk's worth (~1e-6) for any W.
 constexpr int T_CHUNK = 4;           // stages per accumulation chunk (128 K elements)
-constexpr int T_WARPS = 6;
 
-__global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
+template <int BN>
+__global__ void __launch_bounds__(32 * TCfg<BN>::WARPS, 1) gemm_f32split_kernel(
     const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_ax,
     const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_bx, int64_t m, int64_t nc,
     int64_t k, float* __restrict__ out, int64_t ldo, int64_t strideO, const int64_t* __restrict__ kdev) {
+  using Cfg = TCfg<BN>;
+  constexpr int T_STAGES = Cfg::STAGES, T_STAGE_BYTES = Cfg::STAGE, T_BN = BN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_STAGES * T_STAGE_BYTES);
@@ -182,7 +204,7 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
     }
     for (int q = 0; q < 2; ++q) {
       mbar_init(&acc_full[q], 1);
-      mbar_init(&acc_empty[q], 4);  // one arrive per drain warp
+      mbar_init(&acc_empty[q], Cfg::DRAIN);  // one arrive per drain warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)) : "memory");
@@ -192,7 +214,7 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
-                 "r"(2 * T_BN));
+                 "r"(Cfg::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -212,7 +234,7 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
         tma_load_2d(st + 0 * T_TILE_BYTES, &tm_ahi, &full[s], kc, a_row0);
         tma_load_2d(st + 1 * T_TILE_BYTES, &tm_ax, &full[s], kc, a_row0);
         tma_load_2d(st + 2 * T_TILE_BYTES, &tm_bhi, &full[s], kc, b_row0);
-        tma_load_2d(st + 3 * T_TILE_BYTES, &tm_bx, &full[s], kc, b_row0);
+        tma_load_2d(st + 2 * T_TILE_BYTES + Cfg::B_TILE, &tm_bx, &full[s], kc, b_row0);
       }
     }
   } else if (warp == 1) {
@@ -235,28 +257,32 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
           const uint64_t ahi = umma_desc_sw128(base + 0 * T_TILE_BYTES + off);
           const uint64_t ax = umma_desc_sw128(base + 1 * T_TILE_BYTES + off);
           const uint64_t bhi = umma_desc_sw128(base + 2 * T_TILE_BYTES + off);
-          const uint64_t bx = umma_desc_sw128(base + 3 * T_TILE_BYTES + off);
-          umma_bf16(acc, ax, bx, !(first && kk == 0));  // h_x.l_y + l_x.h_y
-          umma_tf32(acc, ahi, bhi, 1);                  // h_x.h_y
+          const uint64_t bx = umma_desc_sw128(base + 2 * T_TILE_BYTES + Cfg::B_TILE + off);
+          umma_bf16(acc, ax, bx, idesc_bf16<BN>(), !(first && kk == 0));  // h_x.l_y + l_x.h_y
+          umma_tf32(acc, ahi, bhi, idesc_tf32<BN>(), 1);                  // h_x.h_y
         }
         umma_commit(&empty[s]);  // stage s free once these MMAs have read it
         if ((kt % T_CHUNK) == T_CHUNK - 1 || kt == ktiles - 1) umma_commit(&acc_full[q]);
       }
     }
   } else {
-    // ---- drain: add each finished chunk into float32 registers, then store
+    // ---- drain: add each finished chunk into float32 registers, then store.
+    // Warp w may read TMEM lanes 32*(w%4)..; with 8 drain warps the second four
+    // take the upper 128 accumulator columns.
+    constexpr int DC = 128;  // columns per drain warp
     const int quarter = warp & 3;
-    float sum[T_BN];
+    const int half = (warp - 2) / 4;
+    float sum[DC];
 #pragma unroll
-    for (int c = 0; c < T_BN; ++c) sum[c] = 0.f;
+    for (int c = 0; c < DC; ++c) sum[c] = 0.f;
     for (int chunk = 0; chunk < nchunks; ++chunk) {
       const int q = chunk & 1;
       mbar_wait(&acc_full[q], (chunk >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < T_BN; c += 32) {
+      for (int c = 0; c < DC; c += 32) {
         uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(q * T_BN + c), v);
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(q * T_BN + half * DC + c), v);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
         for (int j = 0; j < 32; ++j) sum[c + j] += __uint_as_float(v[j]);
@@ -268,16 +294,16 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
     const int64_t row = (int64_t)tile_m * T_BM + quarter * 32 + lane;
     if (row < m) {
       float* orow = out + b * strideO + row * ldo;
-      const int64_t col0 = (int64_t)tile_n * T_BN;
-      const bool vec = (col0 + T_BN <= nc) && (ldo % 4) == 0 && ((reinterpret_cast<uintptr_t>(orow + col0) & 15) == 0);
+      const int64_t col0 = (int64_t)tile_n * T_BN + half * DC;
+      const bool vec = (col0 + DC <= nc) && (ldo % 4) == 0 && ((reinterpret_cast<uintptr_t>(orow + col0) & 15) == 0);
       if (vec) {
         float4* o4 = reinterpret_cast<float4*>(orow + col0);
 #pragma unroll
-        for (int j = 0; j < T_BN / 4; ++j)
+        for (int j = 0; j < DC / 4; ++j)
           o4[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
       } else {
 #pragma unroll
-        for (int j = 0; j < T_BN; ++j)
+        for (int j = 0; j < DC; ++j)
           if (col0 + j < nc) orow[col0 + j] = sum[j];
       }
     }
@@ -285,7 +311,7 @@ __global__ void __launch_bounds__(32 * T_WARPS, 1) gemm_f32split_kernel(
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * T_BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(Cfg::TMEM_COLS));
   }
 }
 
@@ -429,12 +455,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols) {
+static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int box_rows = T_BM) {
   auto enc = get_encode();
   BMM_REQUIRE(enc != nullptr, BMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
-  cuuint32_t box[2] = {(cuuint32_t)T_BK, (cuuint32_t)T_BM};
+  cuuint32_t box[2] = {(cuuint32_t)T_BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -504,20 +530,43 @@ static int gemm_split_impl(const float* a_hi, const void* a_x, const float* b_hi
   const float* b_lo = (const float*)b_x;
   BMM_REQUIRE(batch * m < (1LL << 31) && batch * nc < (1LL << 31) && batch <= 65535, BMM_E_UNSUPPORTED,
               "bmm_gemm_f32split: problem too large for 32-bit TMA coordinates");
+  // 128x256 tiles when one column tile then covers the output (A streamed once per
+  // problem: the batched config 5, 256 wide); large outputs keep 128x128 -- its
+  // 3-stage ring measured ~8% more tensor work per clock at config 4 (64.1 ms at
+  // 1.51 GHz vs 63.3 ms at 1.65 GHz for 128x256)
+  static const int tile_env = [] {
+    const char* e = getenv("BMM_TF32_BN");  // A/B switch for timing (128 or 256)
+    return e ? atoi(e) : 0;
+  }();
+  const int bn = tile_env == 128 || tile_env == 256 ? tile_env : (nc > 128 && nc <= 256 ? 256 : 128);
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   int rc;
   if ((rc = make_map(&ma_hi, a_hi, batch * m, k)) != BMM_OK) return rc;
   if ((rc = make_map(&ma_lo, a_lo, batch * m, k)) != BMM_OK) return rc;
-  if ((rc = make_map(&mb_hi, b_hi, batch * nc, k)) != BMM_OK) return rc;
-  if ((rc = make_map(&mb_lo, b_lo, batch * nc, k)) != BMM_OK) return rc;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_f32split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM_BYTES);
-    attr = true;
-  }
-  dim3 grid((unsigned)ceil_div(nc, T_BN), (unsigned)ceil_div(m, T_BM), (unsigned)batch);
-  gemm_f32split_kernel<<<grid, 32 * T_WARPS, T_SMEM_BYTES, as_stream(stream)>>>(ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out,
+  if ((rc = make_map(&mb_hi, b_hi, batch * nc, k, bn)) != BMM_OK) return rc;
+  if ((rc = make_map(&mb_lo, b_lo, batch * nc, k, bn)) != BMM_OK) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (bn == 256) {
+    using Cfg = TCfg<256>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_f32split_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+      attr = true;
+    }
+    dim3 grid((unsigned)ceil_div(nc, 256), (unsigned)ceil_div(m, T_BM), (unsigned)batch);
+    gemm_f32split_kernel<256><<<grid, 32 * Cfg::WARPS, Cfg::SMEM, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out,
                                                                          ldo, strideO, k_dev);
+  } else {
+    using Cfg = TCfg<128>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_f32split_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+      attr = true;
+    }
+    dim3 grid((unsigned)ceil_div(nc, 128), (unsigned)ceil_div(m, T_BM), (unsigned)batch);
+    gemm_f32split_kernel<128><<<grid, 32 * Cfg::WARPS, Cfg::SMEM, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out,
+                                                                         ldo, strideO, k_dev);
+  }
   BMM_CHECK_LAUNCH("gemm_f32split_kernel");
   return BMM_OK;
 }
