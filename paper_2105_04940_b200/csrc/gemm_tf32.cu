@@ -123,6 +123,31 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem, uint64_t a, uint64_t b,
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// TMA load broadcast to the CTAs of `mask` in the cluster (same smem offset and
+// mbarrier offset in each)
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;\n" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+// MMA completion arriving on the mbarrier at the same offset in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          su32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
                : "memory");
@@ -156,7 +181,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // chunk's worth (~1e-6) for any W.
 constexpr int T_CHUNK = 4;           // stages per accumulation chunk (128 K elements)
 
-template <int BN>
+// MC = 2: CTA pairs (a cluster along the column-tile axis) compute two adjacent
+// 128-column tiles of the same 128 rows; each CTA loads one 64-row half of the
+// shared A tiles and multicasts it to both, so A is read from L2 once per pair
+// (a quarter less operand traffic per flop).  A stage may be refilled only when
+// both CTAs' MMAs have read it: the MMA commits arrive on both CTAs' `empty`
+// barriers (count 2).
+template <int BN, int MC = 1>
 __global__ void __launch_bounds__(32 * TCfg<BN>::WARPS, 1) gemm_f32split_kernel(
     const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_ax,
     const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_bx, int64_t m, int64_t nc,
@@ -173,20 +204,22 @@ __global__ void __launch_bounds__(32 * TCfg<BN>::WARPS, 1) gemm_f32split_kernel(
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = blockIdx.z;
-  // Grouped rasterisation: consecutive CTAs sweep GROUP_M row tiles before
-  // moving to the next column tile, so the ~148 co-resident CTAs share both
-  // their A row blocks and their B column blocks through L2 (row-major launch
-  // order would re-stream all of B from HBM once per row block).
+  uint32_t rank = 0;
+  if constexpr (MC > 1) asm("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  // Grouped rasterisation: consecutive CTAs (clusters) sweep GROUP_M row tiles
+  // before moving to the next column tile, so the ~148 co-resident CTAs share
+  // both their A row blocks and their B column blocks through L2 (row-major
+  // launch order would re-stream all of B from HBM once per row block).
   constexpr int GROUP_M = 16;
   int tile_m, tile_n;
   {
-    const int tm = gridDim.y, tn = gridDim.x;
-    const int lin = blockIdx.y * tn + blockIdx.x;
+    const int tm = gridDim.y, tn = gridDim.x / MC;
+    const int lin = blockIdx.y * tn + blockIdx.x / MC;
     const int group = lin / (GROUP_M * tn);
     const int first_m = group * GROUP_M;
     const int gsz = min(tm - first_m, GROUP_M);
     tile_m = first_m + (lin % (GROUP_M * tn)) % gsz;
-    tile_n = (lin % (GROUP_M * tn)) / gsz;
+    tile_n = ((lin % (GROUP_M * tn)) / gsz) * MC + (int)rank;
   }
   if (kdev != nullptr) {  // compressed sketch: contract the first ceil32(count) columns (zero-padded)
     const int64_t kd = ((kdev[b] + T_BK - 1) / T_BK) * T_BK;
@@ -200,7 +233,7 @@ __global__ void __launch_bounds__(32 * TCfg<BN>::WARPS, 1) gemm_f32split_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < T_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // every CTA of the pair commits its reads of the stage
     }
     for (int q = 0; q < 2; ++q) {
       mbar_init(&acc_full[q], 1);
@@ -219,6 +252,7 @@ __global__ void __launch_bounds__(32 * TCfg<BN>::WARPS, 1) gemm_f32split_kernel(
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if constexpr (MC > 1) cluster_sync_all();  // peers' barriers exist before any multicast lands
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -231,8 +265,15 @@ __global__ void __launch_bounds__(32 * TCfg<BN>::WARPS, 1) gemm_f32split_kernel(
         uint8_t* st = smem + s * T_STAGE_BYTES;
         mbar_expect_tx(&full[s], T_STAGE_BYTES);
         const int kc = kt * T_BK;
-        tma_load_2d(st + 0 * T_TILE_BYTES, &tm_ahi, &full[s], kc, a_row0);
-        tma_load_2d(st + 1 * T_TILE_BYTES, &tm_ax, &full[s], kc, a_row0);
+        if constexpr (MC > 1) {
+          // this CTA's 64-row half of the shared A tiles, to both CTAs
+          const uint32_t half = rank * (T_TILE_BYTES / 2);
+          tma_load_2d_mc(st + 0 * T_TILE_BYTES + half, &tm_ahi, &full[s], kc, a_row0 + (int)rank * 64, 0x3);
+          tma_load_2d_mc(st + 1 * T_TILE_BYTES + half, &tm_ax, &full[s], kc, a_row0 + (int)rank * 64, 0x3);
+        } else {
+          tma_load_2d(st + 0 * T_TILE_BYTES, &tm_ahi, &full[s], kc, a_row0);
+          tma_load_2d(st + 1 * T_TILE_BYTES, &tm_ax, &full[s], kc, a_row0);
+        }
         tma_load_2d(st + 2 * T_TILE_BYTES, &tm_bhi, &full[s], kc, b_row0);
         tma_load_2d(st + 2 * T_TILE_BYTES + Cfg::B_TILE, &tm_bx, &full[s], kc, b_row0);
       }
@@ -261,7 +302,8 @@ __global__ void __launch_bounds__(32 * TCfg<BN>::WARPS, 1) gemm_f32split_kernel(
           umma_bf16(acc, ax, bx, idesc_bf16<BN>(), !(first && kk == 0));  // h_x.l_y + l_x.h_y
           umma_tf32(acc, ahi, bhi, idesc_tf32<BN>(), 1);                  // h_x.h_y
         }
-        umma_commit(&empty[s]);  // stage s free once these MMAs have read it
+        if constexpr (MC > 1) umma_commit_mc(&empty[s], 0x3);  // both CTAs may refill after both read
+        else umma_commit(&empty[s]);  // stage s free once these MMAs have read it
         if ((kt % T_CHUNK) == T_CHUNK - 1 || kt == ktiles - 1) umma_commit(&acc_full[q]);
       }
     }
@@ -313,6 +355,8 @@ __global__ void __launch_bounds__(32 * TCfg<BN>::WARPS, 1) gemm_f32split_kernel(
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(Cfg::TMEM_COLS));
   }
+  // the peer's last MMA commits arrive on this CTA's barriers: leave together
+  if constexpr (MC > 1) cluster_sync_all();
 }
 
 // ---- split gather (K4 for the float32 path)
@@ -539,6 +583,14 @@ static int gemm_split_impl(const float* a_hi, const void* a_x, const float* b_hi
     return e ? atoi(e) : 0;
   }();
   const int bn = tile_env == 128 || tile_env == 256 ? tile_env : (nc > 128 && nc <= 256 ? 256 : 128);
+  // CTA pairs sharing A by TMA multicast (BMM_TF32_PAIR=1): 3.6% more tensor work per
+  // clock at config 4, but the power-capped clock fell further (65.2 ms at 1.46 GHz vs
+  // 64.3 ms at 1.53 GHz), so single CTAs stay the default
+  static const int pair_env = [] {
+    const char* e = getenv("BMM_TF32_PAIR");
+    return e ? atoi(e) : 0;
+  }();
+  const bool pair = bn == 128 && pair_env != 0 && nc > 256;
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   int rc;
   if ((rc = make_map(&ma_hi, a_hi, batch * m, k)) != BMM_OK) return rc;
@@ -556,6 +608,34 @@ static int gemm_split_impl(const float* a_hi, const void* a_x, const float* b_hi
     dim3 grid((unsigned)ceil_div(nc, 256), (unsigned)ceil_div(m, T_BM), (unsigned)batch);
     gemm_f32split_kernel<256><<<grid, 32 * Cfg::WARPS, Cfg::SMEM, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out,
                                                                          ldo, strideO, k_dev);
+  } else if (pair) {
+    // CTA pairs sharing A through TMA multicast (cluster 2 x 1 x 1 along the column tiles)
+    using Cfg = TCfg<128>;
+    CUtensorMap pa_hi, pa_lo;
+    if ((rc = make_map(&pa_hi, a_hi, batch * m, k, 64)) != BMM_OK) return rc;
+    if ((rc = make_map(&pa_lo, a_lo, batch * m, k, 64)) != BMM_OK) return rc;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_f32split_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+      attr = true;
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(2 * ceil_div(ceil_div(nc, 128), 2)), (unsigned)ceil_div(m, T_BM), (unsigned)batch);
+    lc.blockDim = dim3(32 * Cfg::WARPS, 1, 1);
+    lc.dynamicSmemBytes = Cfg::SMEM;
+    lc.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = 2;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    lc.attrs = la;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, gemm_f32split_kernel<128, 2>, pa_hi, pa_lo, mb_hi, mb_lo, m, nc, k, out, ldo,
+                           strideO, k_dev) != cudaSuccess) {
+      set_error("bmm_gemm_f32split: cluster launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      return BMM_E_CUDA;
+    }
   } else {
     using Cfg = TCfg<128>;
     static bool attr = false;

@@ -34,7 +34,8 @@ def unpair(x, W, first):
 
 
 @pytest.mark.parametrize("B,m,n,p,W", [(1, 128, 300, 128, 32), (1, 200, 2000, 72, 1000), (3, 256, 4096, 256, 1024),
-                                       (2, 130, 777, 260, 4096), (1, 128, 64, 128, 8), (1, 128, 999, 128, 32768)])
+                                       (2, 130, 777, 260, 4096), (1, 128, 64, 128, 8), (1, 128, 999, 128, 32768),
+                                       (2, 384, 1500, 640, 512), (1, 256, 3000, 1024, 2048)])
 def test_split_gather_and_gemm(B, m, n, p, W):
     g = torch.Generator(device="cuda").manual_seed(B * 1000 + m + n + p + W)
     M = torch.randn((B, m, n), generator=g, device="cuda", dtype=torch.float32)
@@ -59,3 +60,33 @@ def test_split_gather_and_gemm(B, m, n, p, W):
     # and it is genuinely better than a single TF32 pass would be
     one_pass = torch.bmm(hi, hi_d)
     assert err < 0.1 * ((one_pass - ref).norm() / ref.norm()).item()
+
+
+def test_cta_pair_multicast_variant_matches():
+    """The opt-in CTA-pair (TMA multicast) contraction, run in a fresh process with
+    BMM_TF32_PAIR=1, gives bit-identical products to the default single-CTA one
+    (same MMAs per tile, same accumulation order)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = (
+        "import torch, numpy as np, sys\n"
+        "sys.path[:0] = [%r, %r]\n"
+        "from test_gpu_tf32 import run_split_gemm\n"
+        "g = torch.Generator(device='cuda').manual_seed(5)\n"
+        "M = torch.randn((2, 384, 1500), generator=g, device='cuda')\n"
+        "N = torch.randn((2, 1500, 640), generator=g, device='cuda')\n"
+        "col = torch.randint(0, 1500, (2, 512), generator=g, device='cuda')\n"
+        "sc = torch.rand((2, 512), generator=g, device='cuda', dtype=torch.float64) + 0.5\n"
+        "out, _ = run_split_gemm(M, N, col, sc, 512)\n"
+        "np.save(sys.argv[1], out.cpu().numpy())\n" % (str(Path(__file__).resolve().parent),
+                                                         str(Path(__file__).resolve().parent.parent)))
+    outs = []
+    for pair in ("0", "1"):
+        f = Path(os.environ.get("TMPDIR", "/tmp")) / f"bmm_pair_{pair}_{os.getpid()}.npy"
+        env = dict(os.environ, BMM_TF32_PAIR=pair)
+        subprocess.run([sys.executable, "-c", code, str(f)], env=env, check=True, timeout=300)
+        outs.append(np.load(f))
+        f.unlink()
+    assert np.array_equal(outs[0], outs[1])
