@@ -562,7 +562,8 @@ using DV3 = DCfg<128, 128, 64, 32, 3>;
 using DV4 = DCfg<128, 128, 32, 64, 3>;
 using DV5 = DCfg<64, 64, 32, 32, 4>;
 using DV6 = DCfg<128, 64, 32, 32, 3>;
-constexpr int kVariants = 7;
+using DV7 = DCfg<40, 40, 40, 40, 3>;  // one warp, 5x5 fragments: small outputs (200 = 5 x 40, no padding)
+constexpr int kVariants = 8;
 static int g_variant = 2;      // C.D / exact-product tiles: 128x64, 4 warps of 64x32 (tools/tune_dmma.py)
 static int g_seg_variant = 5;  // segmented square sums: 64x64, 4 warps of 32x32, 4 stages (tools/tune_dmma.py)
 
@@ -595,6 +596,7 @@ static VariantInfo variant_info(int v) {
     case 4: return info_of<DV4>();
     case 5: return info_of<DV5>();
     case 6: return info_of<DV6>();
+    case 7: return info_of<DV7>();
     default: return info_of<DV0>();
   }
 }
@@ -696,8 +698,17 @@ extern "C" int bmm_gemm_f64_set_variant(int gemm_variant, int segsq_variant) {
   return BMM_OK;
 }
 
+// Small outputs (e.g. the Monte Carlo engine's 200 x 200 products): the
+// 40 x 40 single-warp tiles when they waste much less padding than the default
+static int pick_variant(int64_t m, int64_t nc) {
+  if (g_variant != 2 || m > 256 || nc > 256) return g_variant;
+  const int64_t a40 = ceil_div(m, 40) * 40 * ceil_div(nc, 40) * 40;
+  const int64_t a2 = ceil_div(m, 128) * 128 * ceil_div(nc, 64) * 64;
+  return 5 * a40 < 4 * a2 ? 7 : g_variant;
+}
+
 extern "C" int64_t bmm_gemm_f64_workspace(int64_t m, int64_t nc, int64_t k, int64_t batch) {
-  SplitPlan sp = plan_split(variant_info(g_variant), m, nc, k, batch);
+  SplitPlan sp = plan_split(variant_info(pick_variant(m, nc)), m, nc, k, batch);
   return sp.splits > 1 ? sp.splits * batch * m * nc * 8 : 0;
 }
 
@@ -714,7 +725,8 @@ static int gemm_impl(const double* A, int64_t lda, int64_t strideA, const double
       }
     return BMM_OK;
   }
-  const VariantInfo vi = variant_info(g_variant);
+  const int variant = pick_variant(m, nc);
+  const VariantInfo vi = variant_info(variant);
   SplitPlan sp = plan_split(vi, m, nc, k, batch);
   const int64_t need = sp.splits > 1 ? sp.splits * batch * m * nc * 8 : 0;
   BMM_REQUIRE(ws_bytes >= need && (need == 0 || ws != nullptr), BMM_E_ARG,
@@ -728,13 +740,14 @@ static int gemm_impl(const double* A, int64_t lda, int64_t strideA, const double
 #define BMM_GEMM_CASE(V)                                                                                       \
   launch_gemm<V>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part, col, \
                  scale, w_stride, kdev)
-  switch (g_variant) {
+  switch (variant) {
     case 1: BMM_GEMM_CASE(DV1); break;
     case 2: BMM_GEMM_CASE(DV2); break;
     case 3: BMM_GEMM_CASE(DV3); break;
     case 4: BMM_GEMM_CASE(DV4); break;
     case 5: BMM_GEMM_CASE(DV5); break;
     case 6: BMM_GEMM_CASE(DV6); break;
+    case 7: BMM_GEMM_CASE(DV7); break;
     default: BMM_GEMM_CASE(DV0);
   }
 #undef BMM_GEMM_CASE
