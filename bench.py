@@ -248,7 +248,8 @@ def run_ours(args):
     outs_h = [torch.empty((m, p), dtype=torch.float64).pin_memory() for _ in runs]
     host_group = PipelineGroup([SketchPipeline(m, n, p, sizes, W, meth, c0=c0) for _, W, meth, c0 in runs])
     host_group.capture_host(Mx, Nx, M_pin, N_pin, outs_h,
-                            [seeds_from_rngs(meth, [workloads.sample_rng(cfg, cb)], K) for cb, W, meth, c0 in runs])
+                            [seeds_from_rngs(meth, [workloads.sample_rng(cfg, cb)], K) for cb, W, meth, c0 in runs],
+                            n_chunks=int(os.environ.get("BMM_E2E_CHUNKS", "8")))
     e2e = []
     for it in range(args.warmup + args.steps):
         seeds = [seeds_from_rngs(meth, [workloads.sample_rng(cfg, cb)], K) for cb, W, meth, c0 in runs]
