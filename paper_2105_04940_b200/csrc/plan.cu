@@ -151,11 +151,25 @@ __global__ void __launch_bounds__(kProbCtaThreads) block_probs_cta_kernel(
     // loads, one dependent add per element), then the CTA stores it
     double* wc = wb + nk;
     if (tid == 0) {
+      // batches of 8: the loads of a batch are independent of its stores, so one
+      // shared-memory latency per 8 elements instead of one per element
+      const double* __restrict__ src = wb;
+      double* __restrict__ dst = wc;
       double acc = 0.0;  // 0 + p[0] == p[0]: probabilities are never -0
-#pragma unroll 8
-      for (int64_t i = 0; i < nk; ++i) {
-        acc = __dadd_rn(acc, wb[i]);
-        wc[i] = acc;
+      int64_t i = 0;
+      for (; i + 8 <= nk; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = src[i + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc = __dadd_rn(acc, v[j]);
+          dst[i + j] = acc;
+        }
+      }
+      for (; i < nk; ++i) {
+        acc = __dadd_rn(acc, src[i]);
+        dst[i] = acc;
       }
     }
     // last index with p > 0 (the support clamp of _draw_indices, estimators.py:38-44)
