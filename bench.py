@@ -306,7 +306,7 @@ def run_ours(args):
                          "share_of_step_device_ms": kt["segsq_ms"] * kt["segsq_per_step"],
                          "traffic": 164780800 if (m, n, p) == (500, 20000, 500) else None,
                          "traffic_note": "dram__bytes_read+write per launch, ncu --set full "
-                                         "(profiles/r1c_ncu_full_summary.csv): 0.160 GB + 4.7 MB = M + N read once"}
+                                         "(profiles/r1e_ncu_full_summary.csv): 0.160 GB + 4.7 MB = M + N read once"}
     line = {
         "metric": METRIC, "value": ms_step, "unit": "ms/step", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
@@ -324,7 +324,7 @@ def run_ours(args):
                      "flops_note": "executed 2*m*p*K over the distinct drawn columns (gemm_k); the sketch "
                                    "width W counts duplicates, which the compressed sketch folds into scales",
                      "traffic": 35511000 if (m, p) == (500, 500) else None,
-                     "traffic_note": "ncu --set full, W=16000 ONC launch (profiles/r1c_ncu_full_summary.csv): "
+                     "traffic_note": "ncu --set full, W=16000 ONC launch (profiles/r1e_ncu_full_summary.csv): "
                                      "35.5 MB = the gathered C and D read once"},
         "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norms_achieved,
                            "peak": hbm_peak, "unit": "GB/s", "frac": norms_achieved / hbm_peak,
