@@ -95,7 +95,7 @@ def two_step_case(M, N, sizes, part, c, c0, seed, meth, pil):
     assert rel(got.product, ref["CD"]) < 1e-12
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(16))
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_random_pipeline_parity(seed, dtype):
     g = np.random.default_rng(2000 + seed)
@@ -107,6 +107,8 @@ def test_random_pipeline_parity(seed, dtype):
     Ms = [(g.standard_normal((m, n)) * g.lognormal(0, 1, n)).astype(dtype) for _ in range(B)]
     Ns = [(g.standard_normal((n, p)) * g.lognormal(0, 1, (n, 1))).astype(dtype) for _ in range(B)]
     c = 8 * int(g.integers(max(1, (K + 7) // 8), max(2, n // 8) + 1))
+    if seed >= 8:  # widths off the 8-column pair groups: float32 takes the float64 gather + DMMA path
+        c = int(min(n, max(K, c - 3)))
     method = ["ONC", "OPL", "UU", "ONU", "ONMCNR"][seed % 5]
     c0 = 2 * K
     Md = torch.as_tensor(np.stack(Ms), device="cuda")
