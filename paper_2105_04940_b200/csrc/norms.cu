@@ -571,8 +571,18 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
     if (vec_ok) {
       const int64_t groups = n / W;
       c_tail = groups * W;
-      colsq_vec_kernel<T, 16><<<grid_for(groups * batch, 256, 8, 64), 256, 0, st>>>(
-          M, m, n, ldm, strideM, batch, accumulate, colsq);
+      // few column groups (< 8 warps per SM): twice the rows in flight per thread
+      static const int rdeep = [] {
+        const char* e = getenv("BMM_COLSQ_R");  // A/B switch (16 or 32)
+        return e ? atoi(e) : 0;
+      }();
+      const bool deep = rdeep == 32 || (rdeep == 0 && groups * batch < 148LL * 256 * 2);
+      if (deep)
+        colsq_vec_kernel<T, 32><<<grid_for(groups * batch, 256, 8, 64), 256, 0, st>>>(
+            M, m, n, ldm, strideM, batch, accumulate, colsq);
+      else
+        colsq_vec_kernel<T, 16><<<grid_for(groups * batch, 256, 8, 64), 256, 0, st>>>(
+            M, m, n, ldm, strideM, batch, accumulate, colsq);
       BMM_CHECK_LAUNCH("colsq_vec_kernel");
     }
     if (c_tail < n) {
