@@ -10,7 +10,7 @@ norm pass -> probabilities/sizes -> sampling -> gather/rescale -> C.D.
                   [--workload cfg1|cfg2|cfg3]
 
 value  = approx-product time per step (ms), device-timed with CUDA events,
-         inputs resident in HBM, L2 flushed (256 MB write) before every step.
+         inputs resident in HBM, L2 flushed (256 MB write + 256 MB read) before every step.
 e2e    = the same step through the public API with the inputs copied from
          pinned host memory and the nine C.D results read back, every step.
 --impl reference times the CPU port of the reference (oracle/, kind "port")
@@ -158,6 +158,22 @@ def run_reference(args):
 
 # ---------------------------------------------------------------- our arm
 
+class L2Flush:
+    """Cold L2 before a timed step: write a 256 MB buffer (> the 126 MB L2), then
+    read a second 256 MB buffer so the L2 is left holding clean lines -- the
+    write-back of the flush's own dirty lines is not charged to the step."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.w = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
+        self.r = torch.ones(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
+        self.out = torch.empty((), dtype=torch.float32, device="cuda")
+
+    def __call__(self):
+        self.w.fill_(1.0)
+        self.torch.sum(self.r, dim=0, out=self.out)
+
+
 def measure_dgemm_peak(torch):
     """cuBLAS float64 GEMM 8192^3 (best of 5): the measured FP64 tensor ceiling."""
     a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
@@ -198,7 +214,7 @@ def run_ours(args):
     Nd = torch.as_tensor(N_h, device="cuda")
     pipes = [SketchPipeline(m, n, p, sizes, W, meth, c0=c0) for _, W, meth, c0 in runs]
     group = PipelineGroup(pipes)  # the sweep's products run as concurrent graph branches
-    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    flush = L2Flush(torch)
     stream = torch.cuda.current_stream()
 
     def step(Mx, Nx):
@@ -221,7 +237,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         for _ in range(args.steps):
-            flush.fill_(1.0)
+            flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             step(Md, Nd)
@@ -312,7 +328,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8(d))",
         "config": {"workload": args.workload, "m": m, "n": n, "p": p, "K": K,
-                   "runs": [f"{meth}@W={W}" for _, W, meth, _ in runs], "l2": "flushed (256 MB write) before each step",
+                   "runs": [f"{meth}@W={W}" for _, W, meth, _ in runs], "l2": "flushed (256 MB write, then 256 MB read) before each step",
                    "parallelism": f"replicas x{world}"},
         "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
@@ -359,7 +375,7 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
     pipe = pipes[0]
     reps = []
     for _ in range(5):
-        flush.fill_(1.0)
+        flush()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         lib.bmm_norms(0, Md.data_ptr(), m, n, n, 0, Nd.data_ptr(), p, p, 0, 1, 0, pipe.colsq.data_ptr(),
@@ -374,7 +390,7 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
         pipe = opl[0]
         reps = []
         for _ in range(5):
-            flush.fill_(1.0)
+            flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             lib.bmm_segsq_f64(Md.data_ptr(), n, 0, Nd.data_ptr(), p, 0, m, p, pipe.offsets.data_ptr(), pipe.K, 0, 1,
@@ -401,7 +417,7 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
                                  pipe.CD.data_ptr(), p, m * p, pipe.ws_gemm.data_ptr(), pipe.ws_gemm.numel(), st)
         reps = []
         for _ in range(5):
-            flush.fill_(1.0)
+            flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             gemm()
@@ -416,7 +432,7 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
         torch.matmul(C, D)
         reps = []
         for _ in range(5):
-            flush.fill_(1.0)
+            flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             torch.matmul(C, D)
@@ -699,7 +715,7 @@ def run_mc(args):
     part = bm.BlockPartition(sizes)
     plan = bm.allocate_optimal(Md, Nd, part, W)
     eng = ReplicationEngine(Md, Nd, plan)
-    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    flush = L2Flush(torch)
     rng_of = lambda i: np.random.default_rng(np.random.SeedSequence(workloads.ROOT, spawn_key=(1, 2, i)))  # noqa: E731
     n0 = _lib.launches()
     eng.run(rng_of(0), R)
@@ -710,7 +726,7 @@ def run_mc(args):
     times = []
     with ClockSampler() as clocks:
         for i in range(args.steps):
-            flush.fill_(1.0)
+            flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             eng.run(rng_of(100 + i), R)
@@ -735,7 +751,7 @@ def run_mc(args):
     Rc = b["reps"]
     gms = []
     for _ in range(5):
-        flush.fill_(1.0)
+        flush()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         lib.bmm_gemm_f64(b["C"].data_ptr(), W, m * W, b["D"].data_ptr(), p, W * p, m, p, W, Rc, b["CD"].data_ptr(),
@@ -758,7 +774,7 @@ def run_mc(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (config 1, SURVEY.md §8(d))",
         "config": {"workload": "mc", "base": "cfg1", "m": m, "n": n, "p": p, "K": K, "W": W, "method": "OPL",
-                   "reps_per_step": R, "l2": "flushed (256 MB write) before each step"},
+                   "reps_per_step": R, "l2": "flushed (256 MB write, then 256 MB read) before each step"},
         "e2e": {"value": float(np.mean(e2e)), "unit": f"ms/{R} replications",
                 "h2d_bytes_per_step": int(M_h.nbytes + N_h.nbytes), "d2h_bytes_per_step": 8,
                 "api": "coverage_check_plan(M, N, plan, bound, reps, rng) on numpy inputs"},

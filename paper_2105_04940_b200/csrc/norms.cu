@@ -555,6 +555,433 @@ static bool launch_rowsq_tma(const T* N, int64_t n, int64_t p, int64_t ldn, int6
   return true;
 }
 
+// ---- Any width (e.g. config 2: p = 500, config 3: p = 1000): lane = ROW.  A
+// warp owns 32 consecutive rows and streams them left to right in column
+// stages (NBOX SWIZZLE_128B boxes of 32 rows x 128 bytes each) through its own
+// TMA ring.  NumPy's split tree for width p is the same for every row, so it is
+// compiled once per CTA into one op per 8-element group (start a leaf, add to
+// its 8 accumulators, close the leaf body with ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+// add a tail element, push the leaf and fold `combines` pairs of a post-order
+// stack) and every lane executes the same op stream on its own row: no
+// divergence, no per-row tree walks, conflict-free 16-byte swizzled loads.
+enum : uint16_t { kOpStart = 1, kOpEndMain = 2, kOpTail = 4, kOpPush = 8 };
+constexpr int kRsStack = 16;
+
+// ops[g] for the 8-element group g of a row of width p (p >= 8): bits 0-3 flags,
+// bits 4-6 tail count, bits 8-11 post-order combines after the push.
+__device__ void build_row_ops(int64_t p, uint16_t* ops) {
+  int64_t fs[40], fl[40];
+  int fstage[40];
+  int sp = 0, last_leaf_group = -1;
+  fs[0] = 0; fl[0] = p; fstage[0] = 0;
+  for (;;) {
+    const int64_t len = fl[sp];
+    if (len > 128) {
+      int64_t n2 = len / 2;
+      n2 -= n2 % 8;
+      fstage[sp] = 0;
+      ++sp;
+      fs[sp] = fs[sp - 1];
+      fl[sp] = n2;
+      continue;
+    }
+    // leaf [fs, fs + len): fs is a multiple of 8, only the row's last leaf has a tail
+    const int g0 = (int)(fs[sp] / 8), full = (int)(len / 8), tail = (int)(len % 8);
+    for (int j = 0; j < full; ++j) ops[g0 + j] = (uint16_t)((j == 0 ? kOpStart : 0) | (j == full - 1 ? kOpEndMain : 0));
+    if (tail) ops[g0 + full] = (uint16_t)(kOpTail | (tail << 4));
+    last_leaf_group = tail ? g0 + full : g0 + full - 1;
+    ops[last_leaf_group] |= kOpPush;
+    bool done = false;
+    for (;;) {
+      if (sp == 0) { done = true; break; }
+      --sp;
+      const int64_t plen = fl[sp];
+      int64_t n2 = plen / 2;
+      n2 -= n2 % 8;
+      if (fstage[sp] == 0) {
+        fstage[sp] = 1;
+        ++sp;
+        fs[sp] = fs[sp - 1] + n2;
+        fl[sp] = plen - n2;
+        fstage[sp] = 0;
+        break;
+      }
+      ops[last_leaf_group] += (uint16_t)(1 << 8);  // node = left + right, right after its last leaf
+    }
+    if (done) break;
+  }
+}
+
+template <typename T, int WARPS, int STAGES, int NBOX>
+__global__ void __launch_bounds__(32 * WARPS) rowsq_stream_kernel(const __grid_constant__ CUtensorMap map,
+                                                                  int64_t total_rows, int64_t p,
+                                                                  double* __restrict__ rowsq) {
+  constexpr int BOXC = tma_box_elems<T>(), SC = NBOX * BOXC, GPS = SC / 8, SB = NBOX * kTmaBoxBytes;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[WARPS][STAGES];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int G = (int)((p + 7) / 8), U = (int)((p + SC - 1) / SC);
+  uint16_t* ops = reinterpret_cast<uint16_t*>(smem + (int64_t)WARPS * STAGES * SB);
+  unsigned char* ring = smem + (int64_t)w * STAGES * SB;
+  if (threadIdx.x == 0) build_row_ops(p, ops);
+  if (lane == 0) {
+    for (int s = 0; s < STAGES; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm_addr(&bars[w][s])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t units = (total_rows + 31) / 32;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + w, Wt = (int64_t)gridDim.x * WARPS;
+  const int64_t nseq = gw < units ? ((units - 1 - gw) / Wt + 1) * U : 0;
+  auto issue = [&](int64_t sq) {
+    if (lane == 0 && sq < nseq) {
+      const int64_t unit = gw + (sq / U) * Wt;
+      const int64_t c0 = (sq % U) * SC;
+      const int nb = (int)min((int64_t)NBOX, (p - c0 + BOXC - 1) / BOXC);  // boxes that start inside the row
+      uint64_t* bar = &bars[w][sq % STAGES];
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm_addr(bar)),
+                   "r"(nb * kTmaBoxBytes)
+                   : "memory");
+      unsigned char* dst = ring + (int64_t)(sq % STAGES) * SB;
+      for (int c = 0; c < nb; ++c)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+                sm_addr(dst + c * kTmaBoxBytes)),
+            "l"(reinterpret_cast<uint64_t>(&map)), "r"(sm_addr(bar)), "r"((int)(c0 + c * BOXC)), "r"((int)(unit * 32))
+            : "memory");
+    }
+  };
+  for (int s = 0; s < STAGES; ++s) issue(s);
+  double stk[kRsStack];
+  int sp = 0;
+  double r[8], acc = 0.0;
+  for (int64_t sq = 0; sq < nseq; ++sq) {
+    const int st = (int)(sq % STAGES);
+    const int u = (int)(sq % U);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(sm_addr(&bars[w][st])),
+        "r"((uint32_t)((sq / STAGES) & 1))
+        : "memory");
+    const unsigned char* stage = ring + (int64_t)st * SB;
+    const int gend = min(GPS, G - u * GPS);
+#pragma unroll
+    for (int j = 0; j < GPS; ++j) {
+      if (j < gend) {
+        const uint16_t op = ops[u * GPS + j];
+        double q[8];
+        const unsigned char* box = stage + ((8 * j) / BOXC) * kTmaBoxBytes;
+        const int k0 = ((8 * j) % BOXC) * (int)sizeof(T) / 16;
+        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 a = *reinterpret_cast<const float4*>(swz(box, lane, k0 + h));
+            q[4 * h] = sq_of(a.x); q[4 * h + 1] = sq_of(a.y); q[4 * h + 2] = sq_of(a.z); q[4 * h + 3] = sq_of(a.w);
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const double2 a = *reinterpret_cast<const double2*>(swz(box, lane, k0 + h));
+            q[2 * h] = sq_of(a.x); q[2 * h + 1] = sq_of(a.y);
+          }
+        }
+        if (op & kOpTail) {
+          const int t = (op >> 4) & 7;
+#pragma unroll
+          for (int k = 0; k < 7; ++k)
+            if (k < t) acc = __dadd_rn(acc, q[k]);
+        } else {
+          if (op & kOpStart) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r[k] = q[k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], q[k]);
+          }
+          if (op & kOpEndMain)
+            acc = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        }
+        if (op & kOpPush) {
+          stk[sp++] = acc;
+          for (int c = op >> 8; c > 0; --c) {
+            const double b = stk[--sp];
+            stk[sp - 1] = __dadd_rn(stk[sp - 1], b);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    issue(sq + STAGES);  // stage st consumed by every lane
+    if (u == U - 1) {
+      const int64_t row = (gw + (sq / U) * Wt) * 32 + lane;
+      if (row < total_rows) rowsq[row] = __dadd_rn(0.0, stk[0]);
+      sp = 0;
+    }
+  }
+}
+
+template <typename T, int WARPS, int STAGES, int NBOX>
+static bool launch_rowsq_stream_cfg(const CUtensorMap& map, int64_t total_rows, int64_t p, double* rowsq,
+                                    cudaStream_t st) {
+  auto kern = rowsq_stream_kernel<T, WARPS, STAGES, NBOX>;
+  const int smem = WARPS * STAGES * NBOX * kTmaBoxBytes + 1024 + (int)(2 * ((p + 7) / 8) + 16);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+  int occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * WARPS, smem) != cudaSuccess || occ < 1) occ = 1;
+  const int64_t units = (total_rows + 31) / 32;
+  const int64_t blocks = std::min<int64_t>(ceil_div(units, WARPS), 148LL * occ);
+  kern<<<(unsigned)blocks, 32 * WARPS, smem, st>>>(map, total_rows, p, rowsq);
+  return true;
+}
+
+template <typename T>
+static bool launch_rowsq_stream(const T* N, int64_t n, int64_t p, int64_t ldn, int64_t strideN, int64_t batch,
+                                double* rowsq, int cfg, cudaStream_t st) {
+  const int64_t total_rows = n * batch;
+  // op-stream stack: depth <= 2 + log2(p / 64)
+  if (p < 32 || p > 16384 || (ldn * (int64_t)sizeof(T)) % 16 != 0 || (batch > 1 && strideN != n * ldn) ||
+      reinterpret_cast<uintptr_t>(N) % 16 != 0 || total_rows >= (1LL << 31))
+    return false;
+  auto enc = tma_encode_fn();
+  if (enc == nullptr) return false;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)p, (cuuint64_t)total_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ldn * sizeof(T))};
+  cuuint32_t box[2] = {(cuuint32_t)tma_box_elems<T>(), 32};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  if (enc(&map, dt, 2, const_cast<T*>(N), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return false;
+  // auto: few 32-row units (config 2: 625) -> one warp per CTA so all of them are
+  // resident at once, 8 KB stages; many (config 3: 3125) -> 4 warps, 4 KB stages
+  if (cfg == 0) cfg = (total_rows + 31) / 32 < 148LL * 8 ? 1 : 3;
+  switch (cfg) {
+    case 1: return launch_rowsq_stream_cfg<T, 1, 4, 2>(map, total_rows, p, rowsq, st);
+    case 2: return launch_rowsq_stream_cfg<T, 2, 3, 4>(map, total_rows, p, rowsq, st);
+    case 3: return launch_rowsq_stream_cfg<T, 4, 4, 1>(map, total_rows, p, rowsq, st);
+    default: return launch_rowsq_stream_cfg<T, 2, 4, 2>(map, total_rows, p, rowsq, st);
+  }
+}
+
+// ---- TMA-staged column sums for few columns (e.g. config 2: 20000 columns,
+// 500 rows): a warp owns a strip of 32 columns, its lane j the chain of column
+// j.  Row slabs (32 rows x 32 columns, 4-8 KB) stream into a per-warp ring by
+// TMA, so many slabs are in flight without registers while each lane walks its
+// chain out of shared memory (adjacent lanes read adjacent columns: conflict
+// free).  Persistent warps take strips round robin.  Default shape (measured,
+// tools/norms_sweep.py): the CTA-wide variant below with 2 warps sharing 64-column
+// slabs of 16 rows, 6 stages (config 2: 36.9 -> 22.7 us with the old scalar
+// kernel as baseline); BMM_COLSQ_VARIANT=2..9 selects the other shapes.
+template <typename T, int kCsWarps, int kCsStages, int kCsRows>
+__global__ void __launch_bounds__(32 * kCsWarps) colsq_tma_kernel(const __grid_constant__ CUtensorMap map,
+                                                                  int64_t m, int64_t n, int64_t batch,
+                                                                  int accumulate, double* __restrict__ colsq) {
+  constexpr int SLAB = kCsRows * 32 * (int)sizeof(T);
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bars[kCsWarps][kCsStages];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const T* ring = reinterpret_cast<const T*>(smem + (int64_t)w * kCsStages * SLAB);
+  if (lane == 0) {
+    for (int s = 0; s < kCsStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm_addr(&bars[w][s])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t strips_per_b = (n + 31) / 32;
+  const int64_t strips = strips_per_b * batch;
+  const int64_t slabs = (m + kCsRows - 1) / kCsRows;
+  const int64_t gw = (int64_t)blockIdx.x * kCsWarps + w, Wt = (int64_t)gridDim.x * kCsWarps;
+  int64_t it = 0;  // slab counter across this warp's strips (ring position and phase)
+  for (int64_t sid = gw; sid < strips; sid += Wt) {
+    const int64_t b = sid / strips_per_b, c0 = (sid - b * strips_per_b) * 32;
+    const int64_t row0 = b * m;  // rows of problem b in the [batch * m, n] view
+    auto issue = [&](int64_t q) {  // slab q of this strip into ring slot (it + q) % S
+      if (lane == 0 && q < slabs) {
+        const int64_t pos = it + q;
+        uint64_t* bar = &bars[w][pos % kCsStages];
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(SLAB)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+                sm_addr(ring + (pos % kCsStages) * (SLAB / (int)sizeof(T)))),
+            "l"(reinterpret_cast<uint64_t>(&map)), "r"(sm_addr(bar)), "r"((int)c0), "r"((int)(row0 + q * kCsRows))
+            : "memory");
+      }
+    };
+    for (int64_t q = 0; q < kCsStages - 1; ++q) issue(q);
+    const int64_t col = c0 + lane;
+    double acc = (accumulate && col < n) ? colsq[b * n + col] : 0.0;
+    for (int64_t q = 0; q < slabs; ++q) {
+      issue(q + kCsStages - 1);
+      const int64_t pos = it + q;
+      asm volatile(
+          "{\n"
+          ".reg .pred P1;\n"
+          "WAIT_%=:\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+          "@!P1 bra WAIT_%=;\n"
+          "}\n" ::"r"(sm_addr(&bars[w][pos % kCsStages])),
+          "r"((uint32_t)((pos / kCsStages) & 1))
+          : "memory");
+      const T* slab = ring + (pos % kCsStages) * (SLAB / (int)sizeof(T));
+      const int rows = (int)min((int64_t)kCsRows, m - q * kCsRows);  // rows past m belong to the next problem
+      double v[kCsRows];
+#pragma unroll
+      for (int r = 0; r < kCsRows; ++r) v[r] = r < rows ? (double)slab[r * 32 + lane] : 0.0;
+#pragma unroll
+      for (int r = 0; r < kCsRows; ++r)
+        if (r < rows) acc = __dadd_rn(acc, __dmul_rn(v[r], v[r]));
+      __syncwarp();  // slot is refilled by the issue of a later iteration
+    }
+    if (col < n) colsq[b * n + col] = acc;
+    it += slabs;
+  }
+}
+
+// CTA-wide variant: the CTA's warps share one slab of 32*WARPS columns, so
+// each TMA row segment is 32*WARPS*sizeof(T) contiguous bytes.
+template <typename T, int WARPS, int STAGES, int ROWS>
+__global__ void __launch_bounds__(32 * WARPS) colsq_tma_cta_kernel(const __grid_constant__ CUtensorMap map, int64_t m,
+                                                                   int64_t n, int64_t batch, int accumulate,
+                                                                   double* __restrict__ colsq) {
+  constexpr int COLS = 32 * WARPS, SLAB = ROWS * COLS * (int)sizeof(T);
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bars[STAGES];
+  const T* ring = reinterpret_cast<const T*>(smem);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm_addr(&bars[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t strips_per_b = (n + COLS - 1) / COLS;
+  const int64_t strips = strips_per_b * batch;
+  const int64_t slabs = (m + ROWS - 1) / ROWS;
+  int64_t it = 0;
+  for (int64_t sid = blockIdx.x; sid < strips; sid += gridDim.x) {
+    const int64_t b = sid / strips_per_b, c0 = (sid - b * strips_per_b) * COLS;
+    const int64_t row0 = b * m;
+    auto issue = [&](int64_t q) {
+      if (threadIdx.x == 0 && q < slabs) {
+        const int64_t pos = it + q;
+        uint64_t* bar = &bars[pos % STAGES];
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(SLAB)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+                sm_addr(ring + (pos % STAGES) * (SLAB / (int)sizeof(T)))),
+            "l"(reinterpret_cast<uint64_t>(&map)), "r"(sm_addr(bar)), "r"((int)c0), "r"((int)(row0 + q * ROWS))
+            : "memory");
+      }
+    };
+    for (int64_t q = 0; q < STAGES - 1; ++q) issue(q);
+    const int64_t col = c0 + threadIdx.x;
+    double acc = (accumulate && col < n) ? colsq[b * n + col] : 0.0;
+    for (int64_t q = 0; q < slabs; ++q) {
+      issue(q + STAGES - 1);
+      const int64_t pos = it + q;
+      asm volatile(
+          "{\n"
+          ".reg .pred P1;\n"
+          "WAIT_%=:\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+          "@!P1 bra WAIT_%=;\n"
+          "}\n" ::"r"(sm_addr(&bars[pos % STAGES])),
+          "r"((uint32_t)((pos / STAGES) & 1))
+          : "memory");
+      const T* slab = ring + (pos % STAGES) * (SLAB / (int)sizeof(T));
+      const int rows = (int)min((int64_t)ROWS, m - q * ROWS);
+      double v[ROWS];
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) v[r] = r < rows ? (double)slab[r * COLS + threadIdx.x] : 0.0;
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r)
+        if (r < rows) acc = __dadd_rn(acc, __dmul_rn(v[r], v[r]));
+      __syncthreads();  // every warp is done with the slot before it is refilled
+    }
+    if (col < n) colsq[b * n + col] = acc;
+    it += slabs;
+  }
+}
+
+template <typename T, int WARPS, int STAGES, int ROWS>
+static bool launch_colsq_tma_cta(const CUtensorMap& map, int64_t m, int64_t n, int64_t batch, int accumulate,
+                                 double* colsq, cudaStream_t st) {
+  auto kern = colsq_tma_cta_kernel<T, WARPS, STAGES, ROWS>;
+  constexpr int smem = STAGES * ROWS * 32 * WARPS * (int)sizeof(T);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+    attr = true;
+  }
+  int occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * WARPS, smem) != cudaSuccess || occ < 1) occ = 1;
+  const int64_t strips = ((n + 32 * WARPS - 1) / (32 * WARPS)) * batch;
+  const int64_t blocks = std::min<int64_t>(strips, 148LL * occ);
+  kern<<<(unsigned)blocks, 32 * WARPS, smem, st>>>(map, m, n, batch, accumulate, colsq);
+  return true;
+}
+
+template <typename T, int kCsWarps, int kCsStages, int kCsRows>
+static bool launch_colsq_tma_cfg(const CUtensorMap& map, int64_t m, int64_t n, int64_t batch, int accumulate,
+                                 double* colsq, cudaStream_t st) {
+  auto kern = colsq_tma_kernel<T, kCsWarps, kCsStages, kCsRows>;
+  constexpr int smem = kCsWarps * kCsStages * kCsRows * 32 * (int)sizeof(T);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+    attr = true;
+  }
+  int occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kCsWarps, smem) != cudaSuccess || occ < 1)
+    occ = 1;
+  const int64_t strips = ((n + 31) / 32) * batch;
+  const int64_t blocks = std::min<int64_t>(ceil_div(strips, kCsWarps), 148LL * occ);
+  kern<<<(unsigned)blocks, 32 * kCsWarps, smem, st>>>(map, m, n, batch, accumulate, colsq);
+  return true;
+}
+
+template <typename T>
+static bool launch_colsq_tma(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM, int64_t batch,
+                             int accumulate, double* colsq, int variant, cudaStream_t st) {
+  if (ldm != n || (batch > 1 && strideM != m * n) || (n * (int64_t)sizeof(T)) % 16 != 0 ||
+      reinterpret_cast<uintptr_t>(M) % 16 != 0 || batch * m >= (1LL << 31) || n >= (1LL << 31))
+    return false;
+  auto enc = tma_encode_fn();
+  if (enc == nullptr) return false;
+  const int rows = (variant == 2 || variant == 5 || variant == 8) ? 32 : 16;
+  const int bcols = variant == 6 || variant == 8 ? 128 : (variant == 7 || variant == 0) ? 64 : 32;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)(batch * m)};
+  cuuint64_t strides[1] = {(cuuint64_t)(n * sizeof(T))};
+  cuuint32_t box[2] = {(cuuint32_t)bcols, (cuuint32_t)rows};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  if (enc(&map, dt, 2, const_cast<T*>(M), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return false;
+  switch (variant) {
+    case 2: return launch_colsq_tma_cfg<T, 1, 4, 32>(map, m, n, batch, accumulate, colsq, st);
+    case 3: return launch_colsq_tma_cfg<T, 2, 6, 16>(map, m, n, batch, accumulate, colsq, st);
+    case 4: return launch_colsq_tma_cfg<T, 1, 3, 16>(map, m, n, batch, accumulate, colsq, st);
+    case 5: return launch_colsq_tma_cfg<T, 4, 6, 32>(map, m, n, batch, accumulate, colsq, st);
+    case 6: return launch_colsq_tma_cta<T, 4, 6, 16>(map, m, n, batch, accumulate, colsq, st);
+    case 7: return launch_colsq_tma_cta<T, 2, 6, 16>(map, m, n, batch, accumulate, colsq, st);
+    case 8: return launch_colsq_tma_cta<T, 4, 4, 32>(map, m, n, batch, accumulate, colsq, st);
+    case 9: return launch_colsq_tma_cfg<T, 4, 4, 16>(map, m, n, batch, accumulate, colsq, st);
+    default: return launch_colsq_tma_cta<T, 2, 6, 16>(map, m, n, batch, accumulate, colsq, st);
+  }
+}
+
 template <typename T>
 int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM, const T* N,
                  int64_t p, int64_t ldn, int64_t strideN, int64_t batch, int accumulate,
@@ -565,7 +992,14 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
     // Few columns (e.g. config 2: 20000): one column per thread in 64-thread CTAs
     // spreads the chains over every SM and keeps 32 row loads in flight each.
     const bool narrow = (n / W) * batch < 148LL * 256;
-    const bool vec_ok = !narrow && (reinterpret_cast<uintptr_t>(M) % 16 == 0) && (ldm % W == 0) &&
+    static const int cs_variant = [] {
+      const char* e = getenv("BMM_COLSQ_VARIANT");  // A/B switch: 1 disables the TMA-staged kernel, 2-5 pick its shape
+      return e ? atoi(e) : 0;
+    }();
+    const bool done = narrow && cs_variant != 1 &&
+                      launch_colsq_tma<T>(M, m, n, ldm, strideM, batch, accumulate, colsq, cs_variant, st);
+    if (done) BMM_CHECK_LAUNCH("colsq_tma_kernel");
+    const bool vec_ok = !done && !narrow && (reinterpret_cast<uintptr_t>(M) % 16 == 0) && (ldm % W == 0) &&
                         (strideM % W == 0) && n >= W;
     int64_t c_tail = 0;
     if (vec_ok) {
@@ -585,7 +1019,7 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
             M, m, n, ldm, strideM, batch, accumulate, colsq);
       BMM_CHECK_LAUNCH("colsq_vec_kernel");
     }
-    if (c_tail < n) {
+    if (!done && c_tail < n) {
       if (narrow) {
         colsq_scalar_kernel<T, 32><<<grid_for((n - c_tail) * batch, 64, 32, 64), 64, 0, st>>>(
             M, m, n, c_tail, ldm, strideM, batch, accumulate, colsq);
@@ -600,12 +1034,19 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
     BMM_REQUIRE(rowsq != nullptr, BMM_E_ARG, "bmm_norms: rowsq is NULL");
     const int64_t rows = n * batch;
     static const int variant = [] {
-      const char* e = getenv("BMM_ROWSQ_VARIANT");  // A/B switch for tools/norms_sweep.py
+      // A/B switch for tools/norms_sweep.py: 1 skips the TMA kernels, 2 uses the small-row kernels only
+      const char* e = getenv("BMM_ROWSQ_VARIANT");
       return e ? atoi(e) : 0;
     }();
     const bool big = rows * p * (int64_t)sizeof(T) >= (8LL << 20);
+    static const int scfg = [] {
+      const char* e = getenv("BMM_ROWSQ_STREAM");  // A/B: shape of the streamed kernel
+      return e ? atoi(e) : 0;
+    }();
     if (variant == 0 && big && launch_rowsq_tma<T>(N, n, p, ldn, strideN, batch, rowsq, st)) {
       BMM_CHECK_LAUNCH("rowsq_tma_kernel");
+    } else if (variant == 0 && big && launch_rowsq_stream<T>(N, n, p, ldn, strideN, batch, rowsq, scfg, st)) {
+      BMM_CHECK_LAUNCH("rowsq_stream_kernel");
     } else if (variant <= 1 && big && launch_rowsq_leaf<T>(N, n, p, ldn, strideN, batch, rowsq, st)) {
       BMM_CHECK_LAUNCH("rowsq_leaf_kernel");
     } else if (rows < 148LL * 512 && p > 128) {

@@ -38,7 +38,8 @@ def test_norms_bit_exact(m, n, p, dtype):
 
 @pytest.mark.parametrize("p,dtype", [(8, np.float32), (100, np.float64), (128, np.float32), (130, np.float64),
                                      (256, np.float32), (500, np.float64), (1000, np.float64), (4096, np.float32),
-                                     (16384, np.float32), (6000, np.float64)])
+                                     (16384, np.float32), (6000, np.float64), (33, np.float64), (1001, np.float32),
+                                     (4097, np.float64), (12345, np.float64), (16383, np.float32)])
 def test_rowsq_staged_bit_exact(p, dtype):
     """The bulk-copy staged row kernel (inputs >= 8 MB, contiguous 16-byte rows),
     batched with a problem stride, against NumPy's pairwise order."""
@@ -53,6 +54,23 @@ def test_rowsq_staged_bit_exact(p, dtype):
     _lib.call("bmm_norms", _lib.matrix_dtype(Nd), None, 0, n, 0, 0, Nd.data_ptr(), p, p, n * p, 2, 0, None,
               rs.data_ptr(), _lib.stream_ptr())
     ref = np.concatenate([O.rowsq(N[b].astype(np.float64)) for b in range(2)])
+    assert np.array_equal(rs.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("p,ld,dtype", [(500, 504, np.float64), (1000, 1024, np.float32), (300, 302, np.float64)])
+def test_rowsq_padded_rows_bit_exact(p, ld, dtype):
+    """Rows with a leading dimension larger than p (padded, 16-byte pitch or not)."""
+    import torch
+    g = np.random.default_rng(p + ld)
+    itemsize = np.dtype(dtype).itemsize
+    n = (20 << 20) // (ld * itemsize * 2)
+    full = g.standard_normal((2, n, ld)).astype(dtype)
+    Nd = torch.as_tensor(full, device="cuda")
+    rs = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    from paper_2105_04940_b200 import _lib
+    _lib.call("bmm_norms", _lib.matrix_dtype(Nd), None, 0, n, 0, 0, Nd.data_ptr(), p, ld, n * ld, 2, 0, None,
+              rs.data_ptr(), _lib.stream_ptr())
+    ref = np.concatenate([O.rowsq(full[b, :, :p].astype(np.float64)) for b in range(2)])
     assert np.array_equal(rs.cpu().numpy(), ref)
 
 

@@ -15,6 +15,10 @@ peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 665
 torch.cuda.set_device(0)
 lib, st = _lib.load(), _lib.stream_ptr()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+# BMM_FLUSH=wr: after the 256 MB write, read a second 256 MB buffer so the L2 holds
+# clean lines and the kernel is not charged the write-back of the flush itself
+flush_rd = torch.ones(64 << 20, dtype=torch.float32, device="cuda") \
+    if __import__("os").environ.get("BMM_FLUSH") == "wr" else None
 # rowsq shapes (N: rows x p) and colsq shapes (M: m x n) of the configs
 ROWS = [("cfg2 N 20000x500 f64", torch.float64, 1, 20000, 500), ("cfg3 N 100000x1000 f64", torch.float64, 1, 100000, 1000),
         ("cfg5 N 1024x(4096x256) f32", torch.float32, 1024, 4096, 256),
@@ -28,6 +32,8 @@ def timed(fn, reps=5):
     out = []
     for _ in range(reps):
         flush.fill_(1)
+        if flush_rd is not None:
+            flush_rd.sum()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         fn()
