@@ -283,6 +283,22 @@ int bmm_segsq_f64_gather(const double* M, int64_t ldm, int64_t strideM,
                          int64_t w_stride, const int64_t* seg, int64_t nseg, int64_t seg_stride,
                          int64_t batch, double* gsq, void* ws, int64_t ws_bytes, void* stream);
 
+/* The same segmented square sums on the int8 tensor cores (Ozaki scheme):
+ * every value is split exactly into 8 balanced int8 digits under a power-of-two
+ * scale per row of A^k / column of B_k (55 bits), the digit-plane products are
+ * accumulated exactly in int32 by tcgen05 kind::i8 MMAs (levels t+u <= 7) and
+ * recombined in float64 in the epilogue: float64-level accuracy (~1e-16
+ * relative) at int8 tensor-core throughput.  plan.py:183-188 (OPL g_k^2).
+ * dtype BMM_F64 or BMM_F32 (float32 read directly, exact upcast).  n_inner
+ * bounds seg[nseg] - seg[0] (it sizes the digit planes); a segment longer than
+ * 65504 or a negative one, or n_inner exceeded, gives NaN for that problem.
+ * Deterministic (fixed-order tile and row reductions).                     */
+int64_t bmm_segsq_i8_workspace(int64_t m, int64_t nc, int64_t n_inner, int64_t nseg, int64_t batch);
+int bmm_segsq_i8(int dtype, const void* A, int64_t lda, int64_t strideA,
+                 const void* B, int64_t ldb, int64_t strideB,
+                 int64_t m, int64_t nc, int64_t n_inner, const int64_t* seg, int64_t nseg, int64_t seg_stride,
+                 int64_t batch, double* gsq, void* ws, int64_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- exact variance analytics
  * (analysis.py:57-116)
  * var[h, f] = sum_i M[h,i]^2 N[i,f]^2 / (c_k p_i)  -  sum_k (M^k N_k)[h,f]^2 / c_k

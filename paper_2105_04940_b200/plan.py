@@ -204,6 +204,22 @@ def segsq(A: torch.Tensor, B: torch.Tensor, seg: torch.Tensor, nseg: int) -> tor
     return out
 
 
+def segsq_i8(A: torch.Tensor, B: torch.Tensor, seg: torch.Tensor, nseg: int, n_inner: int | None = None
+             ) -> torch.Tensor:
+    """g_j^2 = ||A[:, seg_j] B[seg_j, :]||_F^2 on the int8 tensor cores (Ozaki
+    split, float64 accuracy; bmm_segsq_i8).  float32 or float64 operands."""
+    if A.dtype != B.dtype or A.dtype not in (torch.float32, torch.float64):
+        raise TypeError("segsq_i8: A and B must both be float32 or float64")
+    A, B = A.contiguous(), B.contiguous()
+    m, p = A.shape[0], B.shape[1]
+    n_inner = A.shape[1] if n_inner is None else n_inner
+    out = torch.empty(nseg, dtype=torch.float64, device=A.device)
+    ws = _lib.workspace(_lib.load().bmm_segsq_i8_workspace(m, p, n_inner, nseg, 1))
+    _lib.call("bmm_segsq_i8", _lib.matrix_dtype(A), _lib.ptr(A), A.stride(0), 0, _lib.ptr(B), B.stride(0), 0,
+              m, p, n_inner, _lib.ptr(seg), nseg, 0, 1, _lib.ptr(out), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    return out
+
+
 def split_blocks(flat: np.ndarray, part: BlockPartition) -> tuple:
     off = part.offsets
     return tuple(flat[off[k]:off[k + 1]].copy() for k in range(part.num_blocks))
