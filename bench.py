@@ -21,6 +21,7 @@ shard; "replicas only"); value is the max over ranks.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -311,7 +312,33 @@ def run_ours(args):
     # products (3 x 2 m p n flops at cfg2), else the sampled GEMM
     gemm_step_ms = sum(gemm_ms)
     roofline_main = None
-    if "segsq_ms" in kt and kt["segsq_ms"] * kt["segsq_per_step"] > gemm_step_ms:
+    roofline_segsq = None
+    if "segsq_ms" in kt and kt["segsq_engine"] == "i8":
+        # OPL g_k^2 on the int8 tensor cores: 36 int8 digit-plane products (levels t+u <= 7 of
+        # 8 x 8 planes) per float64 multiply-add, 2*m*p*n float64 flops per launch
+        i8_ops = 36 * 2.0 * m * p * n
+        i8_peak = 2.0 * float(peak.get("bf16_tflops", 1635.9))
+        i8_achieved = i8_ops / (kt["segsq_contract_ms"] * 1e-3) / 1e12
+        roofline_main = {"bound": "tensor", "kernel": "oz_segsq_kernel (OPL g_k^2 = ||M^k N_k||_F^2: int8 tcgen05 "
+                                                     "contraction of the Ozaki digit planes)",
+                         "achieved": i8_achieved, "peak": i8_peak, "unit": "TOPS (int8)",
+                         "frac": i8_achieved / i8_peak,
+                         "peak_source": "dense int8 = 2 x MEASURED_PEAKS bf16_tflops (burst): the same tcgen05 "
+                                        "cycles per dispatch at K=32 int8 vs K=16 bf16",
+                         "algorithmic": "36 x 2*m*p*n int8 ops per launch (8 digit planes per operand, "
+                                        "products with t+u <= 7)",
+                         "launch_ms": kt["segsq_contract_ms"],
+                         "share_of_step_device_ms": kt["segsq_ms"] * kt["segsq_per_step"],
+                         "segsq_total_ms": kt["segsq_ms"], "split_ms": kt["segsq_split_ms"],
+                         "f64_equivalent_tflops": 2.0 * m * p * n / (kt["segsq_ms"] * 1e-3) / 1e12,
+                         "f64_equivalent_frac_of_dgemm": 2.0 * m * p * n / (kt["segsq_ms"] * 1e-3) / 1e12 / dgemm_peak,
+                         "traffic": None,
+                         "traffic_note": "see profiles/ (ncu --set full of oz_segsq_kernel)"}
+        # the dominant kernel by device time per step: the contraction (3 launches at cfg2) or
+        # the nine sampled DMMA GEMMs
+        if kt["segsq_contract_ms"] * kt["segsq_per_step"] < gemm_step_ms:
+            roofline_segsq, roofline_main = roofline_main, None
+    elif "segsq_ms" in kt and kt["segsq_ms"] * kt["segsq_per_step"] > gemm_step_ms:
         seg_flops = 2.0 * m * p * n
         seg_achieved = seg_flops / (kt["segsq_ms"] * 1e-3) / 1e12
         roofline_main = {"bound": "tensor", "kernel": "segsq_f64_kernel (OPL g_k^2 = ||M^k N_k||_F^2, DMMA)",
@@ -342,6 +369,7 @@ def run_ours(args):
                      "traffic": 35511000 if (m, p) == (500, 500) else None,
                      "traffic_note": "ncu --set full, W=16000 ONC launch (profiles/r1e_ncu_full_summary.csv): "
                                      "35.5 MB = the gathered C and D read once"},
+        "roofline_segsq": roofline_segsq,
         "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norms_achieved,
                            "peak": hbm_peak, "unit": "GB/s", "frac": norms_achieved / hbm_peak,
                            "algorithmic_bytes": norm_bytes,
@@ -388,9 +416,17 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
     opl = [pipe for (cb, W, meth, c0), pipe in zip(runs, pipes) if meth == "OPL"]
     if opl:
         pipe = opl[0]
-        reps = []
+        reps, parts = [], []
         for _ in range(5):
             flush()
+            if pipe.seg_engine == "i8":
+                ms3 = (ctypes.c_float * 3)()
+                _lib.call("bmm_segsq_i8_timed", 0, Md.data_ptr(), n, 0, Nd.data_ptr(), p, 0, m, p, n,
+                          pipe.offsets.data_ptr(), pipe.K, 0, 1, pipe.gsq.data_ptr(), pipe.ws_seg.data_ptr(),
+                          pipe.ws_seg.numel(), st, ms3)
+                parts.append(list(ms3))
+                reps.append(sum(ms3))
+                continue
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             lib.bmm_segsq_f64(Md.data_ptr(), n, 0, Nd.data_ptr(), p, 0, m, p, pipe.offsets.data_ptr(), pipe.K, 0, 1,
@@ -400,6 +436,10 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
             reps.append(e0.elapsed_time(e1))
         out["segsq_ms"] = float(np.median(reps))
         out["segsq_per_step"] = len(opl)
+        out["segsq_engine"] = pipe.seg_engine
+        if parts:
+            med = np.median(np.asarray(parts), axis=0)
+            out["segsq_split_ms"], out["segsq_contract_ms"], out["segsq_reduce_ms"] = (float(x) for x in med)
     # the sampled GEMM of each run (C, D already gathered by the last step): over the
     # distinct drawn columns when the pipeline compresses the sketch (k_count on device)
     out["gemm_k"] = []

@@ -291,13 +291,20 @@ int bmm_segsq_f64_gather(const double* M, int64_t ldm, int64_t strideM,
  * relative) at int8 tensor-core throughput.  plan.py:183-188 (OPL g_k^2).
  * dtype BMM_F64 or BMM_F32 (float32 read directly, exact upcast).  n_inner
  * bounds seg[nseg] - seg[0] (it sizes the digit planes); a segment longer than
- * 65504 or a negative one, or n_inner exceeded, gives NaN for that problem.
+ * 32768 or a negative one, or n_inner exceeded, gives NaN for that problem.
  * Deterministic (fixed-order tile and row reductions).                     */
 int64_t bmm_segsq_i8_workspace(int64_t m, int64_t nc, int64_t n_inner, int64_t nseg, int64_t batch);
 int bmm_segsq_i8(int dtype, const void* A, int64_t lda, int64_t strideA,
                  const void* B, int64_t ldb, int64_t strideB,
                  int64_t m, int64_t nc, int64_t n_inner, const int64_t* seg, int64_t nseg, int64_t seg_stride,
                  int64_t batch, double* gsq, void* ws, int64_t ws_bytes, void* stream);
+/* bmm_segsq_i8 with device timing (CUDA events on `stream`, synchronizes):
+ * ms[0] = segment prep + digit split, ms[1] = the int8 tcgen05 contraction,
+ * ms[2] = the ordered tile reduction.  For benchmarks and profiling.       */
+int bmm_segsq_i8_timed(int dtype, const void* A, int64_t lda, int64_t strideA,
+                       const void* B, int64_t ldb, int64_t strideB,
+                       int64_t m, int64_t nc, int64_t n_inner, const int64_t* seg, int64_t nseg, int64_t seg_stride,
+                       int64_t batch, double* gsq, void* ws, int64_t ws_bytes, void* stream, float* ms);
 
 /* ---------------------------------------------------------------- exact variance analytics
  * (analysis.py:57-116)

@@ -75,6 +75,8 @@ SIGNATURES = {
     "bmm_segsq_i8_workspace": (_I64, [_I64, _I64, _I64, _I64, _I64]),
     "bmm_segsq_i8": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P,
                           _P, _I64, _P]),
+    "bmm_segsq_i8_timed": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P,
+                                _P, _I64, _P, _P]),
     "bmm_variance_workspace": (_I64, [_I64, _I64, _I64, _I64]),
     "bmm_elementwise_variance": (_I, [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _P, _P, _P, _I64,
                                       _P, _P, _I64, _P]),

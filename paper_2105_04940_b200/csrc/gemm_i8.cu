@@ -9,19 +9,19 @@
 //
 //   * scale: each row h of A^k (one block's columns of M) gets sigma = 2^e with
 //     max_i |A[h,i]| < 2^e; each column f of B_k likewise (tau = 2^e').
-//   * digits: F = rint(|x| 2^(55-e)) < 2^55 (exact for |x| >= 2^(e-2); one
+//   * digits: F = rint(x 2^(54-e)), |F| < 2^54 (exact for |x| >= 2^(e-1); one
 //     rounding below), written in balanced base 128 as S = 8 digits
-//     d_0..d_7 in [-64, 64] (d_0 most significant) and the sign applied, so
-//     x = sigma 2^-55 sum_t d_t 128^(7-t) up to 2^-56 sigma.
-//   * products: A B = sigma tau 2^-12 sum_d 2^-7d acc_d with
-//     acc_d = sum_{t+u=d} D_t E_u (d = 0..7; levels d >= 8 weigh < 2^-56 and are
-//     dropped).  |acc_d| <= 8 * 64 * 64 * K < 2^31 for K <= 65504: int32 exact.
+//     d_0..d_7 in [-64, 63] (d_0 most significant), so
+//     x = sigma 2^-54 sum_t d_t 128^(7-t) up to 2^-55 sigma.
+//   * products: A B = sigma tau 2^-10 sum_d 2^-7d acc_d with
+//     acc_d = sum_{t+u=d} D_t E_u (d = 0..7; levels d >= 8 weigh < 2^-55 and are
+//     dropped).  |acc_d| <= 8 * 64 * 64 * K < 2^31 for K <= 32768: int32 exact.
 //   * epilogue: hi = sum_{d<4} acc_d 128^(3-d), lo = sum_{d>=4} acc_d 128^(7-d)
-//     (exact int64, < 2^53), v = hi 2^-21 + lo 2^-49 (one rounding), and the
-//     per-tile partial sum of (sigma tau 2^-12 v)^2, reduced in a fixed order.
+//     (exact int64, < 2^51), v = hi 2^-21 + lo 2^-49 (one rounding), and the
+//     per-tile partial sum of (sigma tau 2^-10 v)^2, reduced in a fixed order.
 //
 // The result agrees with a float64 GEMM to ~1e-16 relative (the split is exact
-// to 55 bits per row/column scale, the integer sums are exact), deterministic.
+// to 54 bits per row/column scale, the integer sums are exact), deterministic.
 //
 // Kernels: oz_prep (segment padding to 32, longest-first order), oz_split_rows
 // (A: warp per row segment, digits written K-major), oz_split_cols (B: CTA per
@@ -35,6 +35,7 @@
 #include <cudaTypedefs.h>
 
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "tcgen05.cuh"
@@ -45,7 +46,7 @@ constexpr int OZ_S = 8;            // digit planes per operand
 constexpr int OZ_BM = 128;         // output rows per tile (UMMA M)
 constexpr int OZ_BN = 64;          // output columns per tile (one level = 64 TMEM columns)
 constexpr int OZ_BK = 32;          // K per stage = one kind::i8 MMA = one 32-byte swizzle row
-constexpr int OZ_KMAX = 65504;     // segment length bound for exact int32 levels
+constexpr int OZ_KMAX = 32768;     // segment length bound: exact int32 levels, |hi|, |lo| < 2^51
 constexpr int OZ_A_PLANE = OZ_BM * OZ_BK;            // 4 KB
 constexpr int OZ_B_PLANE = OZ_BN * OZ_BK;            // 2 KB
 constexpr int OZ_STAGE = OZ_S * (OZ_A_PLANE + OZ_B_PLANE);  // 48 KB
@@ -60,38 +61,45 @@ constexpr uint64_t OZ_C = 0x0081020408102040ull;  // sum_{t=0..7} 64 * 128^t
 
 // ---------------------------------------------------------------- digits
 
+// 7-bit fields f (bits 21, 14, 7, 0 of a 28-bit value, most significant first)
+// spread into bytes 0..3 as f - 64 (two's complement; per-byte, no carries:
+// ((b | 0x80) - 0x40) ^ 0x80 = b - 64 mod 256 for b < 128)
+__device__ __forceinline__ uint32_t oz_spread(uint32_t v) {
+  const uint32_t w = (v >> 21) | ((v >> 6) & 0x7F00u) | ((v << 9) & 0x7F0000u) | ((v << 24) & 0x7F000000u);
+  return ((w | 0x80808080u) - 0x40404040u) ^ 0x80808080u;
+}
+
 // The two packed words of one value: byte t of w0 = digit t (t = 0..3, most
-// significant first), byte t of w1 = digit 4 + t.  e = the row/column scale.
+// significant first), byte t of w1 = digit 4 + t.  s1 s2 = 2^(54-e).
+// Fs = rint(x 2^(54-e)) in (-2^54, 2^54); G = Fs + C has eight 7-bit fields
+// f_t (C > 2^54 keeps G positive, the top field in [32, 96]) and
+// Fs = sum_t (f_t - 64) 128^(7-t): balanced digits in [-64, 63].
 __device__ __forceinline__ void oz_digits(double x, double s1, double s2, uint32_t& w0, uint32_t& w1) {
-  const double y = (fabs(x) * s1) * s2;  // exact: powers of two, y < 2^55
-  const uint64_t F = __double2ull_rn(y);
-  const uint64_t G = F + OZ_C;
-  const uint32_t hi = (uint32_t)(G >> 28);           // fields 3,2,1 (7 bits) and 0 (8 bits)
-  const uint32_t lo = (uint32_t)G & 0x0FFFFFFFu;     // fields 7,6,5,4
-  w0 = ((hi >> 21) & 0xFFu) | (((hi >> 14) & 127u) << 8) | (((hi >> 7) & 127u) << 16) | ((hi & 127u) << 24);
-  w1 = ((lo >> 21) & 127u) | (((lo >> 14) & 127u) << 8) | (((lo >> 7) & 127u) << 16) | ((lo & 127u) << 24);
-  w0 = __vsub4(w0, 0x40404040u);
-  w1 = __vsub4(w1, 0x40404040u);
-  if (x < 0.0) {
-    w0 = __vneg4(w0);
-    w1 = __vneg4(w1);
-  }
+  const long long Fs = __double2ll_rn((x * s1) * s2);  // the scaling is exact (powers of two)
+  const uint64_t G = (uint64_t)(Fs + (long long)OZ_C);
+  w0 = oz_spread((uint32_t)(G >> 28));
+  w1 = oz_spread((uint32_t)G & 0x0FFFFFFFu);
 }
 
-// scale factors for exponent e: x * 2^(55-e) as two exact multiplies
+__device__ __forceinline__ double oz_pow2(int k) {  // k in [-1022, 1023]
+  return __longlong_as_double((long long)(k + 1023) << 52);
+}
+
+// scale factors for exponent e: x * 2^(54-e) as two exact multiplies
 __device__ __forceinline__ void oz_scales(int e, double& s1, double& s2) {
-  const int k = 55 - e;
+  const int k = 54 - e;
   const int k1 = k / 2;
-  s1 = ldexp(1.0, k1);
-  s2 = ldexp(1.0, k - k1);
+  s1 = oz_pow2(k1);
+  s2 = oz_pow2(k - k1);
 }
 
-__device__ __forceinline__ int oz_exponent(double mx) {
-  if (!(mx > 0.0)) return 0;  // all-zero row/column: digits are all zero
-  int e;
-  frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): every |x| <= mx < 2^e
-  return e;
-}
+// biased float64 exponent field of x (the scale only needs the largest one:
+// integer max instead of fmax and its NaN handling)
+__device__ __forceinline__ uint32_t oz_ebits(double x) { return ((uint32_t)__double2hiint(x) >> 20) & 0x7FFu; }
+
+// e with every |x| < 2^e from the largest biased exponent field: a normal x
+// is below 2^(field - 1022); subnormals (field 0) are below 2^-1022
+__device__ __forceinline__ int oz_exponent_from_bits(uint32_t eb) { return (int)(eb > 1u ? eb : 1u) - 1022; }
 
 template <typename T>
 __device__ __forceinline__ double oz_ld(const T* p) { return (double)__ldg(p); }
@@ -184,7 +192,8 @@ __global__ void __launch_bounds__(1024) oz_prep_kernel(const int64_t* __restrict
 // ---------------------------------------------------------------- split of A
 // Warp per (row h, segment j): row maximum, exponent, then the 8 digit planes
 // of the row segment (zero-padded to L_j), 4 consecutive values per lane so
-// each plane store is one coalesced 128-byte row piece.
+// each plane store is one coalesced 128-byte row piece (the second read of the
+// row segment hits L1).
 template <typename T>
 __global__ void __launch_bounds__(256) oz_split_rows_kernel(const T* __restrict__ A, int64_t lda, int64_t strideA,
                                                             int64_t m, const int64_t* __restrict__ seg,
@@ -197,46 +206,51 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const T* __restrict_
   const int64_t h = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t j = blockIdx.y, b = blockIdx.z;
   if (h >= m || flag[b] != 0) return;  // bad segments: no writes (the result is NaN)
-  const int64_t Lj = L[b * nseg + j];
+  const int Lj = L[b * nseg + j];
   if (Lj == 0) return;
   const int64_t s0 = seg[b * seg_stride + j];
-  const int64_t len = seg[b * seg_stride + j + 1] - s0;
+  const int len = (int)(seg[b * seg_stride + j + 1] - s0);
   const T* row = A + b * strideA + h * lda + s0;
-  double mx = 0.0;
-  for (int64_t i0 = 4 * lane; i0 < len; i0 += 128) {
+  uint32_t eb = 0;
+  for (int i0 = 4 * lane; i0 < len; i0 += 128) {
+    double v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (i0 + q < len) mx = fmax(mx, fabs(oz_ld(row + i0 + q)));
+    for (int q = 0; q < 4; ++q) v[q] = i0 + q < len ? oz_ld(row + i0 + q) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) eb = max(eb, oz_ebits(v[q]));
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  const int e = oz_exponent(mx);
+  eb = __reduce_max_sync(0xffffffffu, eb);
+  const int e = oz_exponent_from_bits(eb);
   if (lane == 0) ex[(b * nseg + j) * m + h] = e;
   double s1, s2;
   oz_scales(e, s1, s2);
-  const int64_t pob = po[b * nseg + j];
-  uint8_t* out = planes + ((b * OZ_S) * m + h) * P + pob;
+  uint8_t* out = planes + ((b * OZ_S) * m + h) * P + po[b * nseg + j];
   const int64_t plane = m * P;
-  for (int64_t i0 = 4 * lane; i0 < Lj; i0 += 128) {
+  for (int i0 = 4 * lane; i0 < Lj; i0 += 128) {
     uint32_t w0[4], w1[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const double x = i0 + q < len ? oz_ld(row + i0 + q) : 0.0;
       oz_digits(x, s1, s2, w0[q], w1[q]);
     }
+    uint8_t* o = out + i0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      *reinterpret_cast<uint32_t*>(out + u * plane + i0) = oz_gather_byte(w0, u);
-      *reinterpret_cast<uint32_t*>(out + (4 + u) * plane + i0) = oz_gather_byte(w1, u);
+      *reinterpret_cast<uint32_t*>(o + u * plane) = oz_gather_byte(w0, u);
+      *reinterpret_cast<uint32_t*>(o + (4 + u) * plane) = oz_gather_byte(w1, u);
     }
   }
 }
 
 // ---------------------------------------------------------------- split of B
-// CTA per (segment j, 64 columns): column maxima over the segment's rows, then
+// Cluster of OZ_CL CTAs per (segment j, 64 columns), each owning a contiguous
+// piece of the segment's rows: column maxima of the piece, exchanged through
+// distributed shared memory (every CTA takes the max over the cluster), then
 // 32-row chunks: thread (g, c) converts rows 8g..8g+7 of column c, the digit
 // bytes are transposed into a [plane][column][32] shared tile and written as
 // 16-byte pieces of the K-major planes B^T.
+constexpr int OZ_CL = 8;
+
 template <typename T>
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const T* __restrict__ B, int64_t ldb, int64_t strideB,
                                                             int64_t nc, const int64_t* __restrict__ seg,
@@ -245,39 +259,77 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const T* __restrict_
                                                             const int32_t* __restrict__ L, int64_t P,
                                                             uint8_t* __restrict__ planes, int32_t* __restrict__ ex,
                                                             const int32_t* __restrict__ flag) {
-  __shared__ double red[4][64];
+  __shared__ uint32_t red[4][64];
+  __shared__ uint32_t cmax[64];
   __shared__ __align__(16) uint8_t tile[OZ_S][64][32];
-  const int64_t j = blockIdx.y, b = blockIdx.z;
-  const int64_t Lj = L[b * nseg + j];
-  if (Lj == 0 || flag[b] != 0) return;
+  const int64_t j = blockIdx.y % nseg, b = blockIdx.y / nseg;
+  const int piece = blockIdx.z;  // == cluster rank (cluster dims 1 x 1 x OZ_CL)
+  const int Lj = L[b * nseg + j];
+  const bool active = Lj > 0 && flag[b] == 0;  // uniform over the cluster
   const int g = threadIdx.x >> 6, c = threadIdx.x & 63;
   const int64_t f0 = (int64_t)blockIdx.x * 64;
   const int64_t f = f0 + c;
   const bool fv = f < nc;
-  const int64_t s0 = seg[b * seg_stride + j];
-  const int64_t len = seg[b * seg_stride + j + 1] - s0;
+  const int64_t s0 = active ? seg[b * seg_stride + j] : 0;
+  const int len = active ? (int)(seg[b * seg_stride + j + 1] - s0) : 0;
+  // this CTA's rows: [r0, r1) in 32-row chunks
+  const int nch = Lj / 32;
+  const int per = (nch + OZ_CL - 1) / OZ_CL;
+  const int r0 = min(piece * per, nch) * 32, r1 = min((piece + 1) * per, nch) * 32;
   const T* col = B + b * strideB + s0 * ldb + f;
-  double mx = 0.0;
-  if (fv)
-    for (int64_t i = g; i < len; i += 4) mx = fmax(mx, fabs(oz_ld(col + i * ldb)));
-  red[g][c] = mx;
+  uint32_t eb = 0;
+  if (fv) {
+    const int hi = min(r1, len);
+    int i = r0 + g;
+    const T* pc = col + (int64_t)i * ldb;
+    const int64_t step = 4 * ldb;
+    for (; i + 28 < hi; i += 32, pc += 8 * step) {  // 8 rows in flight per thread
+      double v[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[r] = oz_ld(pc + r * step);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) eb = max(eb, oz_ebits(v[r]));
+    }
+    for (; i < hi; i += 4, pc += step) eb = max(eb, oz_ebits(oz_ld(pc)));
+  }
+  red[g][c] = eb;
   __syncthreads();
-  mx = fmax(fmax(red[0][c], red[1][c]), fmax(red[2][c], red[3][c]));
-  const int e = oz_exponent(mx);
-  if (g == 0 && fv) ex[(b * nseg + j) * nc + f] = e;
+  if (g == 0) cmax[c] = max(max(red[0][c], red[1][c]), max(red[2][c], red[3][c]));
+  // the cluster's column maxima
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  eb = 0;
+  {
+    const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&cmax[c]));
+#pragma unroll
+    for (int rk = 0; rk < OZ_CL; ++rk) {
+      uint32_t remote, v;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local), "r"(rk));
+      asm volatile("ld.shared::cluster.u32 %0, [%1];\n" : "=r"(v) : "r"(remote) : "memory");
+      eb = max(eb, v);
+    }
+  }
+  // peers may exit (their shared memory vanishes) only after everyone has read it
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (!active || r0 >= r1) return;
+  const int e = oz_exponent_from_bits(eb);
+  if (g == 0 && piece == 0 && fv) ex[(b * nseg + j) * nc + f] = e;
   double s1, s2;
   oz_scales(e, s1, s2);
-  const int64_t pob = po[b * nseg + j];
   const int64_t plane = nc * P;
-  uint8_t* out = planes + (b * OZ_S) * plane + pob;
-  for (int64_t i0 = 0; i0 < Lj; i0 += 32) {
+  uint8_t* out = planes + (b * OZ_S) * plane + po[b * nseg + j];
+  double x[8];
+  const int lim = fv ? min(len, r1) : 0;  // rows this thread may read
+  const T* pr = col + (int64_t)(r0 + 8 * g) * ldb;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) x[r] = (r0 + 8 * g + r < lim) ? oz_ld(pr + r * ldb) : 0.0;
+  for (int i0 = r0; i0 < r1; i0 += 32) {
     uint32_t w0[8], w1[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int64_t i = i0 + 8 * g + r;
-      const double x = (fv && i < len) ? oz_ld(col + i * ldb) : 0.0;
-      oz_digits(x, s1, s2, w0[r], w1[r]);
-    }
+    for (int r = 0; r < 8; ++r) oz_digits(x[r], s1, s2, w0[r], w1[r]);
+    // next chunk's values in flight during the transpose and stores
+    pr += 32 * ldb;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) x[r] = (i0 + 32 + 8 * g + r < lim) ? oz_ld(pr + r * ldb) : 0.0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t a0[4] = {w0[0], w0[1], w0[2], w0[3]}, a1[4] = {w0[4], w0[5], w0[6], w0[7]};
@@ -336,6 +388,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
+// one box of all S digit planes: {32 bytes of K, rows, S planes}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
@@ -374,7 +435,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_co
                                                                  const int32_t* __restrict__ L,
                                                                  const int32_t* __restrict__ exA,
                                                                  const int32_t* __restrict__ exB,
-                                                                 double* __restrict__ part) {
+                                                                 double* __restrict__ part, int mode) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * OZ_STAGE);
@@ -413,19 +474,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_co
       uint32_t it = 0;
       for (int64_t w = blockIdx.x; w < geo.items; w += gridDim.x) {
         const OzItem I = oz_item(geo, w, perm, po, L);
-        const int arow = (int)(I.b * OZ_S * geo.m + I.tm * OZ_BM);
-        const int brow = (int)(I.b * OZ_S * geo.nc + I.tn * OZ_BN);
+        const int arow = (int)(I.tm * OZ_BM), brow = (int)(I.tn * OZ_BN), plane0 = (int)(I.b * OZ_S);
         for (int kt = 0; kt < I.ktiles; ++kt, ++it) {
           const int s = it % OZ_STAGES;
           if (it >= OZ_STAGES) mbar_wait(&empty[s], ((it / OZ_STAGES) - 1) & 1);
           uint8_t* st = smem + s * OZ_STAGE;
+          if (mode == 2) {  // timing experiment: no operand loads
+            mbar_arrive(&full[s]);
+            continue;
+          }
           mbar_expect_tx(&full[s], OZ_STAGE);
           const int kc = (int)(I.k0 + kt * OZ_BK);
-#pragma unroll
-          for (int t = 0; t < OZ_S; ++t) tma_load_2d(st + t * OZ_A_PLANE, &tm_a, &full[s], kc, arow + t * (int)geo.m);
-#pragma unroll
-          for (int u = 0; u < OZ_S; ++u)
-            tma_load_2d(st + OZ_S * OZ_A_PLANE + u * OZ_B_PLANE, &tm_b, &full[s], kc, brow + u * (int)geo.nc);
+          // rows past m / nc are zero-filled by the tensor map bounds
+          tma_load_3d(st, &tm_a, &full[s], kc, arow, plane0);
+          tma_load_3d(st + OZ_S * OZ_A_PLANE, &tm_b, &full[s], kc, brow, plane0);
         }
       }
     }
@@ -443,6 +505,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_co
           mbar_wait(&full[s], (it / OZ_STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           const uint32_t base = su32(smem + s * OZ_STAGE);
+          if (mode >= 3) {  // timing experiment: the same MACs as 9 (mode 3) or 18 (mode 4) uniform MMAs
+            const int nn = mode == 3 ? 256 : 128;
+            for (int i = 0; i < (mode == 3 ? 9 : 18); ++i)
+              umma_i8(tmem + (uint32_t)((i & 1) * 256), umma_desc_sw32(base + (i & 7) * OZ_A_PLANE),
+                      umma_desc_sw32(base + OZ_S * OZ_A_PLANE), idesc_i8(nn), (kt > 0 || i > 1) ? 1u : 0u);
+            umma_commit(&empty[s]);
+            continue;
+          }
 #pragma unroll
           for (int t = 0; t < OZ_S; ++t) {
             const uint64_t adesc = umma_desc_sw32(base + t * OZ_A_PLANE);
@@ -475,11 +545,18 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_co
       double* wc = wcol + 64 * (n_items & 1);
       if (e_id < 64) {
         const int64_t f = I.tn * OZ_BN + e_id;
-        wc[e_id] = f < geo.nc ? ldexp(1.0, exB[(I.b * geo.nseg + I.j) * geo.nc + f] - 12) : 0.0;
+        wc[e_id] = f < geo.nc ? ldexp(1.0, exB[(I.b * geo.nseg + I.j) * geo.nc + f] - 10) : 0.0;
       }
       named_sync(1, 128);
       mbar_wait(acc_full, n_items & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (mode == 1) {  // timing experiment: release the accumulators at once
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+        ++n_items;
+        continue;
+      }
       const int64_t row = I.tm * OZ_BM + quarter * 32 + lane;
       double R = 0.0;
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16);
@@ -496,11 +573,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_co
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const int64_t hi = ((((int64_t)(int32_t)v[0][q] * 128 + (int32_t)v[1][q]) * 128 + (int32_t)v[2][q]) * 128) +
-                             (int32_t)v[3][q];
-          const int64_t lo = ((((int64_t)(int32_t)v[4][q] * 128 + (int32_t)v[5][q]) * 128 + (int32_t)v[6][q]) * 128) +
-                             (int32_t)v[7][q];
-          const double x = fma((double)lo, 0x1p-49, (double)hi * 0x1p-21) * wc[c0 + q];
+          const int64_t hi = ((int64_t)(int32_t)v[0][q] << 21) + ((int64_t)(int32_t)v[1][q] << 14) +
+                             ((int64_t)(int32_t)v[2][q] << 7) + (int64_t)(int32_t)v[3][q];
+          const int64_t lo = ((int64_t)(int32_t)v[4][q] << 21) + ((int64_t)(int32_t)v[5][q] << 14) +
+                             ((int64_t)(int32_t)v[6][q] << 7) + (int64_t)(int32_t)v[7][q];
+          // exact int64 -> double for |x| < 2^51 without the conversion unit
+          const double hd = __longlong_as_double(hi + 0x4338000000000000ll) - 6755399441055744.0;
+          const double ld = __longlong_as_double(lo + 0x4338000000000000ll) - 6755399441055744.0;
+          const double x = fma(ld, 0x1p-49, hd * 0x1p-21) * wc[c0 + q];
           R = fma(x, x, R);
         }
       }
@@ -567,14 +647,16 @@ static OzLayout oz_layout(int64_t m, int64_t nc, int64_t n_inner, int64_t nseg, 
   return l;
 }
 
-static int oz_map(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_t P, int box_rows) {
+// digit planes [plane][rows][P] as a 3-D tensor; box = all S planes of one
+// 32-byte K slice of `box_rows` rows (SWIZZLE_32B)
+static int oz_map(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_t planes, int64_t P, int box_rows) {
   auto enc = get_encode();
   BMM_REQUIRE(enc != nullptr, BMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)P};
-  cuuint32_t box[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+  cuuint64_t dims[3] = {(cuuint64_t)P, (cuuint64_t)rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)P, (cuuint64_t)(P * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows, (cuuint32_t)OZ_S};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   BMM_REQUIRE(r == CUDA_SUCCESS, BMM_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -590,10 +672,10 @@ extern "C" int64_t bmm_segsq_i8_workspace(int64_t m, int64_t nc, int64_t n_inner
   return oz_layout(m, nc, n_inner, nseg, batch).total;
 }
 
-extern "C" int bmm_segsq_i8(int dtype, const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
-                            int64_t strideB, int64_t m, int64_t nc, int64_t n_inner, const int64_t* seg, int64_t nseg,
-                            int64_t seg_stride, int64_t batch, double* gsq, void* ws, int64_t ws_bytes,
-                            void* stream) {
+static int segsq_i8_impl(int dtype, const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                         int64_t strideB, int64_t m, int64_t nc, int64_t n_inner, const int64_t* seg, int64_t nseg,
+                         int64_t seg_stride, int64_t batch, double* gsq, void* ws, int64_t ws_bytes, void* stream,
+                         cudaEvent_t* ev) {
   BMM_REQUIRE(m >= 1 && nc >= 1 && n_inner >= 0 && nseg >= 1 && batch >= 1, BMM_E_ARG, "bmm_segsq_i8: bad shape");
   BMM_REQUIRE(A != nullptr && B != nullptr && seg != nullptr && gsq != nullptr, BMM_E_ARG,
               "bmm_segsq_i8: null pointer");
@@ -603,7 +685,8 @@ extern "C" int bmm_segsq_i8(int dtype, const void* A, int64_t lda, int64_t strid
               (long long)ws_bytes, (long long)l.total);
   BMM_REQUIRE(batch * OZ_S * (m > nc ? m : nc) < (1LL << 31) && l.P < (1LL << 31), BMM_E_UNSUPPORTED,
               "bmm_segsq_i8: problem too large for 32-bit TMA coordinates");
-  BMM_REQUIRE(nseg <= 65535 && batch <= 65535 && ceil_div(m, 8) <= (1LL << 31) - 1, BMM_E_UNSUPPORTED,
+  BMM_REQUIRE(nseg <= 65535 && batch <= 65535 && nseg * batch <= 65535 && ceil_div(m, 8) <= (1LL << 31) - 1,
+              BMM_E_UNSUPPORTED,
               "bmm_segsq_i8: grid too large");
   uint8_t* w = (uint8_t*)ws;
   uint8_t* pa = w + l.off_a;
@@ -617,29 +700,45 @@ extern "C" int bmm_segsq_i8(int dtype, const void* A, int64_t lda, int64_t strid
   double* part = (double*)(w + l.off_part);
   cudaStream_t st = as_stream(stream);
 
+  if (ev) cudaEventRecord(ev[0], st);
   oz_prep_kernel<<<(unsigned)batch, 1024, 0, st>>>(seg, nseg, seg_stride, l.P, po, L, perm, flag);
   BMM_CHECK_LAUNCH("oz_prep_kernel");
   dim3 ga((unsigned)ceil_div(m, 8), (unsigned)nseg, (unsigned)batch);
-  dim3 gb((unsigned)ceil_div(nc, 64), (unsigned)nseg, (unsigned)batch);
+  dim3 gb((unsigned)ceil_div(nc, 64), (unsigned)(nseg * batch), OZ_CL);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = gb;
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = 0;
+  lc.stream = st;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = 1;
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = OZ_CL;
+  lc.attrs = la;
+  lc.numAttrs = 1;
+  cudaError_t ce;
   if (dtype == BMM_F64) {
     oz_split_rows_kernel<double><<<ga, 256, 0, st>>>((const double*)A, lda, strideA, m, seg, nseg, seg_stride, po, L,
                                                      l.P, pa, exa, flag);
     BMM_CHECK_LAUNCH("oz_split_rows_kernel");
-    oz_split_cols_kernel<double><<<gb, 256, 0, st>>>((const double*)B, ldb, strideB, nc, seg, nseg, seg_stride, po, L,
-                                                     l.P, pb, exb, flag);
+    ce = cudaLaunchKernelEx(&lc, oz_split_cols_kernel<double>, (const double*)B, ldb, strideB, nc, seg, nseg,
+                            seg_stride, (const int64_t*)po, (const int32_t*)L, l.P, pb, exb, (const int32_t*)flag);
   } else {
     oz_split_rows_kernel<float><<<ga, 256, 0, st>>>((const float*)A, lda, strideA, m, seg, nseg, seg_stride, po, L,
                                                     l.P, pa, exa, flag);
     BMM_CHECK_LAUNCH("oz_split_rows_kernel");
-    oz_split_cols_kernel<float><<<gb, 256, 0, st>>>((const float*)B, ldb, strideB, nc, seg, nseg, seg_stride, po, L,
-                                                    l.P, pb, exb, flag);
+    ce = cudaLaunchKernelEx(&lc, oz_split_cols_kernel<float>, (const float*)B, ldb, strideB, nc, seg, nseg,
+                            seg_stride, (const int64_t*)po, (const int32_t*)L, l.P, pb, exb, (const int32_t*)flag);
   }
+  BMM_REQUIRE(ce == cudaSuccess, BMM_E_CUDA, "oz_split_cols_kernel: cluster launch failed: %s",
+              cudaGetErrorString(cudaGetLastError()));
   BMM_CHECK_LAUNCH("oz_split_cols_kernel");
 
   CUtensorMap ma, mb;
   int rc;
-  if ((rc = oz_map(&ma, pa, batch * OZ_S * m, l.P, OZ_BM)) != BMM_OK) return rc;
-  if ((rc = oz_map(&mb, pb, batch * OZ_S * nc, l.P, OZ_BN)) != BMM_OK) return rc;
+  if ((rc = oz_map(&ma, pa, m, batch * OZ_S, l.P, OZ_BM)) != BMM_OK) return rc;
+  if ((rc = oz_map(&mb, pb, nc, batch * OZ_S, l.P, OZ_BN)) != BMM_OK) return rc;
   OzGeom geo;
   geo.m = m;
   geo.nc = nc;
@@ -658,9 +757,43 @@ extern "C" int bmm_segsq_i8(int dtype, const void* A, int64_t lda, int64_t strid
     return n;
   }();
   const unsigned grid = (unsigned)(geo.items < nsm ? geo.items : nsm);
-  oz_segsq_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(ma, mb, geo, perm, po, L, exa, exb, part);
+  static const int mode = [] {
+    const char* e = getenv("BMM_OZ_MODE");  // timing experiments only (1: no epilogue, 2: no loads)
+    return e ? atoi(e) : 0;
+  }();
+  if (ev) cudaEventRecord(ev[1], st);
+  oz_segsq_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(ma, mb, geo, perm, po, L, exa, exb, part, mode);
   BMM_CHECK_LAUNCH("oz_segsq_kernel");
+  if (ev) cudaEventRecord(ev[2], st);
   oz_reduce_kernel<<<grid_for(batch * nseg, 128), 128, 0, st>>>(part, geo.TM * geo.TN, nseg, batch * nseg, flag, gsq);
   BMM_CHECK_LAUNCH("oz_reduce_kernel");
+  if (ev) cudaEventRecord(ev[3], st);
   return BMM_OK;
+}
+
+extern "C" int bmm_segsq_i8(int dtype, const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                            int64_t strideB, int64_t m, int64_t nc, int64_t n_inner, const int64_t* seg, int64_t nseg,
+                            int64_t seg_stride, int64_t batch, double* gsq, void* ws, int64_t ws_bytes,
+                            void* stream) {
+  return segsq_i8_impl(dtype, A, lda, strideA, B, ldb, strideB, m, nc, n_inner, seg, nseg, seg_stride, batch, gsq, ws,
+                       ws_bytes, stream, nullptr);
+}
+
+extern "C" int bmm_segsq_i8_timed(int dtype, const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                                  int64_t strideB, int64_t m, int64_t nc, int64_t n_inner, const int64_t* seg,
+                                  int64_t nseg, int64_t seg_stride, int64_t batch, double* gsq, void* ws,
+                                  int64_t ws_bytes, void* stream, float* ms) {
+  BMM_REQUIRE(ms != nullptr, BMM_E_ARG, "bmm_segsq_i8_timed: ms is NULL");
+  cudaEvent_t ev[4];
+  for (auto& e : ev) cudaEventCreate(&e);
+  int rc = segsq_i8_impl(dtype, A, lda, strideA, B, ldb, strideB, m, nc, n_inner, seg, nseg, seg_stride, batch, gsq,
+                         ws, ws_bytes, stream, ev);
+  if (rc == BMM_OK) {
+    cudaEventSynchronize(ev[3]);
+    cudaEventElapsedTime(&ms[0], ev[0], ev[1]);
+    cudaEventElapsedTime(&ms[1], ev[1], ev[2]);
+    cudaEventElapsedTime(&ms[2], ev[2], ev[3]);
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
 }

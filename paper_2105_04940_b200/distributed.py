@@ -29,6 +29,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
+from .plan import segsq_engine
 
 
 def grid_shape(world: int) -> tuple:
@@ -184,12 +185,21 @@ class ShardedApproxProduct:
         aux = None
         if self.method == "OPL":
             # C2: g_k^2 partials of this rank's output tile
-            A = M_local.double() if M_local.dtype != torch.float64 else M_local
-            B = N_local.double().contiguous() if N_local.dtype != torch.float64 else N_local.contiguous()
-            gpart = torch.empty(K, dtype=torch.float64, device=A.device)
-            ws = _lib.workspace(self.lib.bmm_segsq_f64_workspace(A.shape[0], B.shape[1], K, 1))
-            self._c("bmm_segsq_f64", P(A), A.stride(0), 0, P(B), B.stride(0), 0, A.shape[0], B.shape[1],
-                    P(self.offsets), K, 0, 1, P(gpart), P(ws), ws.numel(), st)
+            if segsq_engine(max(self.sizes)) == "i8":
+                A, B = M_local.contiguous(), N_local.contiguous()
+                if A.dtype != B.dtype:
+                    A, B = A.double(), B.double()
+                gpart = torch.empty(K, dtype=torch.float64, device=A.device)
+                ws = _lib.workspace(self.lib.bmm_segsq_i8_workspace(A.shape[0], B.shape[1], n, K, 1))
+                self._c("bmm_segsq_i8", _lib.matrix_dtype(A), P(A), A.stride(0), 0, P(B), B.stride(0), 0,
+                        A.shape[0], B.shape[1], n, P(self.offsets), K, 0, 1, P(gpart), P(ws), ws.numel(), st)
+            else:
+                A = M_local.double() if M_local.dtype != torch.float64 else M_local
+                B = N_local.double().contiguous() if N_local.dtype != torch.float64 else N_local.contiguous()
+                gpart = torch.empty(K, dtype=torch.float64, device=A.device)
+                ws = _lib.workspace(self.lib.bmm_segsq_f64_workspace(A.shape[0], B.shape[1], K, 1))
+                self._c("bmm_segsq_f64", P(A), A.stride(0), 0, P(B), B.stride(0), 0, A.shape[0], B.shape[1],
+                        P(self.offsets), K, 0, 1, P(gpart), P(ws), ws.numel(), st)
             aux = exchange_sum(gpart, self.group)
         rule = {"ONC": _lib.RULE_ONC, "OPL": _lib.RULE_OPL, "UU": _lib.RULE_UU}[self.method]
         self._c("bmm_budgets", rule, P(self.s) if rule != _lib.RULE_UU else None, P(aux) if aux is not None else None,

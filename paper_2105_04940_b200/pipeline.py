@@ -4,7 +4,7 @@ One object holds every buffer for a fixed (shape, partition, method, budget,
 batch), so a call is a fixed sequence of kernel launches on the current
 stream with no allocation and no host synchronisation:
 
-  K1 bmm_norms -> K2 bmm_block_probs -> [OPL: bmm_segsq_f64 of M^k N_k]
+  K1 bmm_norms -> K2 bmm_block_probs -> [OPL: bmm_segsq_i8 of M^k N_k]
   [two-step: pilot budgets -> CDF -> child seeds -> draws -> gather -> segsq]
   -> bmm_budgets -> bmm_block_cdf -> bmm_seed_streams -> bmm_sample
   -> bmm_gather -> bmm_gemm_f64  (C @ D)
@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from . import rng as _rng
-from .plan import raise_status
+from .plan import raise_status, segsq_engine
 
 METHODS = ("OPL", "ONC", "UU", "ONU", "ONMCNR", "SSM")
 
@@ -187,8 +187,11 @@ class SketchPipeline:
                                        dtype=torch.uint8, device=dev)
         if method == "OPL":
             self.gsq = torch.empty(B * K, **f64)
-            self.ws_seg = torch.empty(max(256, self.lib.bmm_segsq_f64_workspace(self.m, self.p, K, B)),
-                                      dtype=torch.uint8, device=dev)
+            # g_k^2 on the int8 tensor cores (Ozaki split; float32 inputs read directly)
+            self.seg_engine = segsq_engine(self.max_len)
+            wsb = (self.lib.bmm_segsq_i8_workspace(self.m, self.p, self.n, K, B) if self.seg_engine == "i8"
+                   else self.lib.bmm_segsq_f64_workspace(self.m, self.p, K, B))
+            self.ws_seg = torch.empty(max(256, wsb), dtype=torch.uint8, device=dev)
         if method in ("ONU", "ONMCNR"):
             self.pc = self.c0 // K
             if self.pc < 1:
@@ -338,8 +341,7 @@ class SketchPipeline:
                 self._c("bmm_norms", dt, P(M) + 8 * c0, m, c1 - c0, ldm, 0, P(N) + 8 * c0 * ldn, p, ldn, 0, 1, 0,
                         P(self.colsq) + 8 * c0, P(self.rowsq) + 8 * c0, st)
                 if self.method == "OPL":
-                    self._c("bmm_segsq_f64", P(M), ldm, 0, P(N), ldn, 0, m, p, P(self.offsets) + 8 * k0, k1 - k0,
-                            0, 1, P(self.gsq) + 8 * k0, P(self.ws_seg), self.ws_seg.numel(), st)
+                    self._segsq(M, N, dt, k0, k1, 1, st)
             seg_done = True
         if self.method == "SSM":
             return self._run_ssm(M, N, dt, st)
@@ -351,9 +353,7 @@ class SketchPipeline:
         aux = None
         if self.method == "OPL":
             if not seg_done:
-                A, Bm = self._f64(M, N)
-                self._c("bmm_segsq_f64", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p, P(self.offsets), K,
-                        0, B, P(self.gsq), P(self.ws_seg), self.ws_seg.numel(), st)
+                self._segsq(M, N, dt, 0, K, B, st)
             aux = self.gsq
         if self.method in ("ONU", "ONMCNR"):
             p0 = self.p0 if self.method == "ONU" else self.probs
@@ -432,6 +432,23 @@ class SketchPipeline:
         self._c("bmm_gemm_f64", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, B, P(self.CD), p, m * p,
                 P(self.ws_gemm), self.ws_gemm.numel(), st)
         return self.CD.view(m, p)
+
+    def _segsq(self, M, N, dt, k0, k1, B, st):
+        """OPL g_k^2 for blocks k0..k1-1 of every problem (k0 > 0: one problem, a
+        streamed chunk)."""
+        P = lambda t: t.data_ptr()  # noqa: E731
+        m, p = self.m, self.p
+        sM, sN = m * self.n, self.n * p
+        if self.seg_engine == "i8":
+            n_inner = int(sum(self.sizes[k0:k1]))
+            self._c("bmm_segsq_i8", dt, P(M), M.stride(-2), sM, P(N), N.stride(-2), sN, m, p, n_inner,
+                    P(self.offsets) + 8 * k0, k1 - k0, 0, B, P(self.gsq) + 8 * k0, P(self.ws_seg),
+                    self.ws_seg.numel(), st)
+        else:
+            A, Bm = self._f64(M, N)
+            self._c("bmm_segsq_f64", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p,
+                    P(self.offsets) + 8 * k0, k1 - k0, 0, B, P(self.gsq) + 8 * k0, P(self.ws_seg),
+                    self.ws_seg.numel(), st)
 
     def _f64(self, M, N):
         if M.dtype == torch.float64:

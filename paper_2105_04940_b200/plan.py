@@ -14,6 +14,8 @@ frozen records the reference returns.
 """
 from __future__ import annotations
 
+import os
+
 import json
 from dataclasses import dataclass
 from typing import NamedTuple, Optional
@@ -186,8 +188,24 @@ class DeviceInstance:
         return pr, sk, fk
 
     def block_product_sq(self) -> torch.Tensor:
-        """g_k^2 = ||M^k N_k||_F^2 for every block (DMMA segmented square sums)."""
+        """g_k^2 = ||M^k N_k||_F^2 for every block (segmented square sums: int8
+        tensor-core Ozaki split, or DMMA; see segsq_engine)."""
+        if segsq_engine(self.max_len) == "i8":
+            return segsq_i8(self.M, self.N, self.offsets, self.K)
         return segsq(self.M, self.N, self.offsets, self.K)
+
+
+SEGSQ_I8_MAX_LEN = 32768  # bmm_segsq_i8's exact-accumulation bound per segment
+
+
+def segsq_engine(max_len: int) -> str:
+    """Kernel for the OPL block-product norms g_k^2: "i8" (bmm_segsq_i8, int8
+    tensor cores, float64-accurate Ozaki split) unless a block exceeds its
+    length bound or BMM_SEGSQ=dmma selects the DMMA kernel (bmm_segsq_f64)."""
+    forced = os.environ.get("BMM_SEGSQ", "").lower()
+    if forced in ("dmma", "f64"):
+        return "dmma"
+    return "i8" if max_len <= SEGSQ_I8_MAX_LEN else "dmma"
 
 
 def segsq(A: torch.Tensor, B: torch.Tensor, seg: torch.Tensor, nseg: int) -> torch.Tensor:
