@@ -312,6 +312,21 @@ def run_ours(args):
     # products (3 x 2 m p n flops at cfg2), else the sampled GEMM
     gemm_step_ms = sum(gemm_ms)
     roofline_main = None
+    roofline_gemm_i8 = None
+    if all(e == "i8" for e in kt["gemm_engine"]):
+        i8_peak = 2.0 * float(peak.get("bf16_tflops", 1635.9))
+        i8_ops = sum(36.0 * f for f in gemm_flops)
+        roofline_gemm_i8 = {
+            "bound": "tensor", "kernel": "bmm_gemm_i8_gather (C.D: sketch gather fused into the Ozaki digit split, "
+                                        "int8 tcgen05 contraction, split-K reduction)",
+            "achieved": i8_ops / (sum(gemm_ms) * 1e-3) / 1e12, "peak": i8_peak, "unit": "TOPS (int8)",
+            "frac": i8_ops / (sum(gemm_ms) * 1e-3) / 1e12 / i8_peak,
+            "peak_source": "dense int8 = 2 x MEASURED_PEAKS bf16_tflops (burst)",
+            "algorithmic": "36 x 2*m*p*K int8 ops over the distinct drawn columns; the time includes the gather "
+                           "and digit split",
+            "f64_equivalent_tflops": gemm_achieved, "dgemm_peak_tflops": dgemm_peak,
+            "cublas_same_shapes_tflops": sum(gemm_flops) / (sum(kt["cublas_same_shape_ms"]) * 1e-3) / 1e12,
+            "traffic": None}
     roofline_segsq = None
     if "segsq_ms" in kt and kt["segsq_engine"] == "i8":
         # OPL g_k^2 on the int8 tensor cores: 36 int8 digit-plane products (levels t+u <= 7 of
@@ -360,7 +375,8 @@ def run_ours(args):
         "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "roofline": roofline_main,
-        "roofline_gemm": {"bound": "tensor", "kernel": "gemm_f64_kernel (C.D, DMMA)", "achieved": gemm_achieved,
+        "roofline_gemm": roofline_gemm_i8 if roofline_gemm_i8 is not None else
+                    {"bound": "tensor", "kernel": "gemm_f64_kernel (C.D, DMMA)", "achieved": gemm_achieved,
                      "peak": dgemm_peak, "unit": "TFLOP/s", "frac": gemm_achieved / dgemm_peak,
                      "peak_source": "cuBLAS dgemm 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
                      "cublas_same_shapes_tflops": sum(gemm_flops) / (sum(kt["cublas_same_shape_ms"]) * 1e-3) / 1e12,
@@ -448,7 +464,9 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
         out["gemm_k"].append(kd)
 
         def gemm():
-            if pipe.compress:
+            if getattr(pipe, "gemm_engine", "dmma") == "i8":
+                pipe.contract(Md, Nd, st)
+            elif pipe.compress:
                 lib.bmm_gemm_f64_dk(pipe.C.data_ptr(), W, m * W, pipe.D.data_ptr(), p, W * p, m, p, W,
                                     pipe.k_count.data_ptr(), 1, pipe.CD.data_ptr(), p, m * p, pipe.ws_gemm.data_ptr(),
                                     pipe.ws_gemm.numel(), st)
@@ -467,8 +485,14 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush):
         out["gemm_ms"].append(float(np.median(reps)))
     # context: cuBLAS DGEMM on the same operands (reference point only; not on the product path)
     out["cublas_same_shape_ms"] = []
+    out["gemm_engine"] = [getattr(pipe, "gemm_engine", "dmma") for pipe in pipes]
     for (cb, W, meth, c0), pipe, kd in zip(runs, pipes, out["gemm_k"]):
-        C, D = pipe.C.view(m, W)[:, :kd], pipe.D.view(W, p)[:kd]
+        if hasattr(pipe, "C"):
+            C, D = pipe.C.view(m, W)[:, :kd], pipe.D.view(W, p)[:kd]
+        else:  # the i8 engine gathers inside its split: build C, D for the cuBLAS reference point
+            col, sc = (pipe.k_column, pipe.k_scale) if pipe.compress else (pipe.column, pipe.scale)
+            C = Md[:, col[:kd]] * sc[:kd]
+            D = Nd[col[:kd], :] * sc[:kd, None]
         torch.matmul(C, D)
         reps = []
         for _ in range(5):

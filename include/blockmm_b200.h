@@ -306,6 +306,38 @@ int bmm_segsq_i8_timed(int dtype, const void* A, int64_t lda, int64_t strideA,
                        int64_t m, int64_t nc, int64_t n_inner, const int64_t* seg, int64_t nseg, int64_t seg_stride,
                        int64_t batch, double* gsq, void* ws, int64_t ws_bytes, void* stream, float* ms);
 
+/* C @ D on the int8 tensor cores (the same Ozaki digit planes, one
+ * power-of-two scale per row of A / column of B): out[b] = A[b] (m x k) @ B[b]
+ * (k x nc) in float64 (estimators.py:175).  k = k_dev[b] <= k_max when k_dev
+ * != NULL (the compressed sketch's device count).  kexp (optional, per k,
+ * stride k_max per problem): A[:, k] 2^kexp[k], B[k, :] 2^-kexp[k] -- exact
+ * balancing that keeps the digit scales set by the dominant terms; without
+ * it heavy-tailed operands lose a few bits (~1e-13 relative instead of
+ * ~1e-15).  The K dimension is split across CTAs when the output has few
+ * tiles; partials are summed in a fixed order (deterministic).  float64 or
+ * float32 operands, row-major, lda/ldb in elements.                         */
+int64_t bmm_gemm_i8_workspace(int64_t m, int64_t nc, int64_t k_max, int64_t batch);
+int bmm_gemm_i8(int dtype, const void* A, int64_t lda, int64_t strideA,
+                const void* B, int64_t ldb, int64_t strideB,
+                int64_t m, int64_t nc, int64_t k_max, const int64_t* k_dev, const int32_t* kexp, int64_t batch,
+                double* out, int64_t ldo, int64_t strideO, void* ws, int64_t ws_bytes, void* stream);
+/* The same with the sketch gathered on the fly (estimators.py:78-81):
+ * A[h, t] = M[h, column[t]] * scale[t], B[t, f] = N[column[t], f] * scale[t]
+ * (one float64 rounding each, as the reference's C and D), column/scale/kexp
+ * per problem at b * w_stride.  Workspace: bmm_gemm_i8_workspace(m, nc, k_max, batch). */
+int bmm_gemm_i8_gather(int dtype, const void* M, int64_t ldm, int64_t strideM,
+                       const void* N, int64_t ldn, int64_t strideN,
+                       const int64_t* column, const double* scale, const int32_t* kexp, int64_t w_stride,
+                       int64_t m, int64_t nc, int64_t k_max, const int64_t* k_dev, int64_t batch,
+                       double* out, int64_t ldo, int64_t strideO, void* ws, int64_t ws_bytes, void* stream);
+/* Balance exponents for the above from the norm pass: kexp[b*w_stride + t] =
+ * round(log2(||N_i|| / ||M_i||) / 2) with i = column[b*w_stride + t] (t when
+ * column is NULL), colsq/rowsq = squared column norms of M / row norms of N
+ * (bmm_norms), n_stride per problem; 0 past k_dev[b] and for zero norms.   */
+int bmm_balance_exponents(const double* colsq, const double* rowsq, int64_t n_stride,
+                          const int64_t* column, int64_t w, int64_t w_stride, const int64_t* k_dev,
+                          int64_t batch, int32_t* kexp, void* stream);
+
 /* ---------------------------------------------------------------- exact variance analytics
  * (analysis.py:57-116)
  * var[h, f] = sum_i M[h,i]^2 N[i,f]^2 / (c_k p_i)  -  sum_k (M^k N_k)[h,f]^2 / c_k

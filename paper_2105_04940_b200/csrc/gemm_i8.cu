@@ -403,32 +403,56 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 
 struct OzItem {
   int64_t b, j, tm, tn;
-  int64_t k0;   // padded offset of the segment
+  int64_t k0;   // first K column of the planes (segment start / split start)
   int ktiles;   // stages (32 K each)
 };
 
 struct OzGeom {
   int64_t m, nc, nseg, TM, TN, items;
+  // product mode (EPI_OUT): nseg = K splits, kinfo[2b] = inner length, kinfo[2b+1] = split chunk
+  const int64_t* kinfo;
+  double* out;
+  int64_t ldo, strideO;
 };
 
+enum { EPI_SEG = 0, EPI_OUT = 1 };
+
+template <int EPI>
 __device__ __forceinline__ OzItem oz_item(const OzGeom& g, int64_t it, const int32_t* __restrict__ perm,
                                           const int64_t* __restrict__ po, const int32_t* __restrict__ L) {
   OzItem r;
   const int64_t tiles = g.TM * g.TN;
-  const int64_t tile = it % tiles;
-  const int64_t rest = it / tiles;
-  const int64_t rank = rest % g.nseg;
-  r.b = rest / g.nseg;
-  r.j = perm[r.b * g.nseg + rank];
-  r.tn = tile % g.TN;
-  r.tm = tile / g.TN;
-  r.k0 = po[r.b * g.nseg + r.j];
-  r.ktiles = L[r.b * g.nseg + r.j] / OZ_BK;
+  if constexpr (EPI == EPI_SEG) {
+    const int64_t tile = it % tiles;
+    const int64_t rest = it / tiles;
+    const int64_t rank = rest % g.nseg;
+    r.b = rest / g.nseg;
+    r.j = perm[r.b * g.nseg + rank];
+    r.tn = tile % g.TN;
+    r.tm = tile / g.TN;
+    r.k0 = po[r.b * g.nseg + r.j];
+    r.ktiles = L[r.b * g.nseg + r.j] / OZ_BK;
+  } else {
+    r.j = it % g.nseg;  // K split
+    const int64_t tile = (it / g.nseg) % tiles;
+    r.b = it / (g.nseg * tiles);
+    r.tn = tile % g.TN;
+    r.tm = tile / g.TN;
+    const int64_t kd = g.kinfo[2 * r.b], chunk = g.kinfo[2 * r.b + 1];
+    r.k0 = r.j * chunk;
+    const int64_t k1 = min(kd, r.k0 + chunk);
+    r.ktiles = k1 > r.k0 ? (int)((k1 - r.k0 + OZ_BK - 1) / OZ_BK) : 0;
+  }
   return r;
 }
 
-// Persistent: CTA c takes items c, c + G, ... of the longest-first item list.
-__global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_constant__ CUtensorMap tm_a,
+// Persistent: CTA c takes items c, c + G, ... of the item list (segments
+// longest first).  EPI_SEG: per-tile square sums of the product into part;
+// EPI_OUT: the product tile itself (float64) into out, or into the split-K
+// partials part[b][split] when nseg > 1.  Exponents: EPI_SEG int e per
+// (segment, row/column); EPI_OUT biased exponent fields (oz_exponent_from_bits).
+template <int EPI>
+__global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_constant__ CUtensorMap tm_a,
                                                                  const __grid_constant__ CUtensorMap tm_b, OzGeom geo,
                                                                  const int32_t* __restrict__ perm,
                                                                  const int64_t* __restrict__ po,
@@ -473,7 +497,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_co
       // ---- TMA producer: the S digit planes of A and B for every stage
       uint32_t it = 0;
       for (int64_t w = blockIdx.x; w < geo.items; w += gridDim.x) {
-        const OzItem I = oz_item(geo, w, perm, po, L);
+        const OzItem I = oz_item<EPI>(geo, w, perm, po, L);
         const int arow = (int)(I.tm * OZ_BM), brow = (int)(I.tn * OZ_BN), plane0 = (int)(I.b * OZ_S);
         for (int kt = 0; kt < I.ktiles; ++kt, ++it) {
           const int s = it % OZ_STAGES;
@@ -496,7 +520,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_co
       // ---- MMA issuer: per stage, A plane t x B planes 0..S-1-t into levels t..S-1
       uint32_t it = 0, n_items = 0;
       for (int64_t w = blockIdx.x; w < geo.items; w += gridDim.x) {
-        const OzItem I = oz_item(geo, w, perm, po, L);
+        const OzItem I = oz_item<EPI>(geo, w, perm, po, L);
         if (I.ktiles == 0) continue;
         if (n_items > 0) mbar_wait(acc_empty, (n_items - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -536,16 +560,31 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_co
     const int quarter = warp & 3;
     uint32_t n_items = 0;
     for (int64_t w = blockIdx.x; w < geo.items; w += gridDim.x) {
-      const OzItem I = oz_item(geo, w, perm, po, L);
+      const OzItem I = oz_item<EPI>(geo, w, perm, po, L);
       double* prow = part + ((I.b * geo.nseg + I.j) * geo.TM + I.tm) * geo.TN + I.tn;
+      const int64_t row = I.tm * OZ_BM + quarter * 32 + lane;
+      const int64_t col0 = I.tn * OZ_BN;
+      double* orow = nullptr;  // EPI_OUT: this thread's output row (64 columns from col0)
+      if constexpr (EPI == EPI_OUT) {
+        orow = geo.nseg > 1 ? part + ((I.b * geo.nseg + I.j) * geo.m + row) * geo.nc
+                            : geo.out + I.b * geo.strideO + row * geo.ldo;
+      }
       if (I.ktiles == 0) {
-        if (e_id == 0) *prow = 0.0;
+        if constexpr (EPI == EPI_SEG) {
+          if (e_id == 0) *prow = 0.0;
+        } else if (row < geo.m) {
+          for (int q = 0; q < OZ_BN; ++q)
+            if (col0 + q < geo.nc) orow[col0 + q] = 0.0;
+        }
         continue;
       }
       double* wc = wcol + 64 * (n_items & 1);
       if (e_id < 64) {
-        const int64_t f = I.tn * OZ_BN + e_id;
-        wc[e_id] = f < geo.nc ? ldexp(1.0, exB[(I.b * geo.nseg + I.j) * geo.nc + f] - 10) : 0.0;
+        const int64_t f = col0 + e_id;
+        if constexpr (EPI == EPI_SEG)
+          wc[e_id] = f < geo.nc ? ldexp(1.0, exB[(I.b * geo.nseg + I.j) * geo.nc + f] - 10) : 0.0;
+        else
+          wc[e_id] = f < geo.nc ? ldexp(1.0, oz_exponent_from_bits((uint32_t)exB[I.b * geo.nc + f]) - 10) : 0.0;
       }
       named_sync(1, 128);
       mbar_wait(acc_full, n_items & 1);
@@ -557,8 +596,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_co
         ++n_items;
         continue;
       }
-      const int64_t row = I.tm * OZ_BM + quarter * 32 + lane;
       double R = 0.0;
+      double sr = 0.0;  // row scale 2^e_h
+      if (row < geo.m) {
+        if constexpr (EPI == EPI_SEG)
+          sr = ldexp(1.0, exA[(I.b * geo.nseg + I.j) * geo.m + row]);
+        else
+          sr = ldexp(1.0, oz_exponent_from_bits((uint32_t)exA[I.b * geo.m + row]));
+      }
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16);
 #pragma unroll 1
       for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
@@ -581,20 +626,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_segsq_kernel(const __grid_co
           const double hd = __longlong_as_double(hi + 0x4338000000000000ll) - 6755399441055744.0;
           const double ld = __longlong_as_double(lo + 0x4338000000000000ll) - 6755399441055744.0;
           const double x = fma(ld, 0x1p-49, hd * 0x1p-21) * wc[c0 + q];
-          R = fma(x, x, R);
+          if constexpr (EPI == EPI_SEG) {
+            R = fma(x, x, R);
+          } else {
+            if (row < geo.m && col0 + c0 + q < geo.nc) orow[col0 + c0 + q] = x * sr;
+          }
         }
       }
-      if (row < geo.m) {
-        const double sr = ldexp(1.0, exA[(I.b * geo.nseg + I.j) * geo.m + row]);
+      if constexpr (EPI == EPI_SEG) {
         R = (R * sr) * sr;
-      } else {
-        R = 0.0;
-      }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) R += __shfl_xor_sync(0xffffffffu, R, o);
-      if (lane == 0) red[quarter] = R;
-      named_sync(1, 128);
-      if (e_id == 0) *prow = (red[0] + red[1]) + (red[2] + red[3]);
+        for (int o = 16; o > 0; o >>= 1) R += __shfl_xor_sync(0xffffffffu, R, o);
+        if (lane == 0) red[quarter] = R;
+        named_sync(1, 128);
+        if (e_id == 0) *prow = (red[0] + red[1]) + (red[2] + red[3]);
+      }
       ++n_items;
     }
   }
@@ -617,6 +663,222 @@ __global__ void oz_reduce_kernel(const double* __restrict__ part, int64_t tiles,
     double acc = 0.0;
     for (int64_t i = 0; i < tiles; ++i) acc += p[i];
     gsq[g] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- product mode
+// out[b] = A[b] (m x k) @ B[b] (k x nc) in float64 through the same digit planes:
+// one scale per row of A / column of B over the whole inner length (biased
+// exponent fields, atomicMax over K chunks), digits written chunk-parallel,
+// K split across CTAs when the output has few tiles, partials reduced in a
+// fixed order.  Gathered operands (the sampled sketch, estimators.py:78-81):
+// A[h, t] = M[h, col[t]] * scale[t], B[t, f] = N[col[t], f] * scale[t], one
+// float64 rounding as in the reference, then split.
+
+// Optional balance exponents kx[k]: A[:, k] 2^kx[k] and B[k, :] 2^-kx[k] (exact;
+// the product is unchanged) so the per-row / per-column digit scales are set
+// by the terms that dominate the product rather than by one operand's range.
+template <typename T, bool G>
+struct OzRows {  // A[h, k]
+  const T* base; int64_t ld; const int64_t* col; const double* sc; const int32_t* kx;
+  __device__ __forceinline__ double at(int64_t h, int64_t k) const {
+    double v;
+    if constexpr (G) v = __dmul_rn(oz_ld(base + h * ld + col[k]), sc[k]);
+    else v = oz_ld(base + h * ld + k);
+    return kx != nullptr ? v * oz_pow2(kx[k]) : v;
+  }
+};
+
+template <typename T, bool G>
+struct OzCols {  // B[k, f]
+  const T* base; int64_t ld; const int64_t* col; const double* sc; const int32_t* kx;
+  __device__ __forceinline__ double at(int64_t k, int64_t f) const {
+    double v;
+    if constexpr (G) v = __dmul_rn(oz_ld(base + col[k] * ld + f), sc[k]);
+    else v = oz_ld(base + k * ld + f);
+    return kx != nullptr ? v * oz_pow2(-kx[k]) : v;
+  }
+};
+
+// kexp[t] = round(log2(||N_i|| / ||M_i||) / 2), i = column[t] (or t): the sketch
+// columns of C and rows of D both scaled to ~sqrt(||M_i|| ||N_i||) s_t
+__global__ void oz_balance_kernel(const double* __restrict__ colsq, const double* __restrict__ rowsq,
+                                  int64_t n_stride, const int64_t* __restrict__ column, int64_t w, int64_t w_stride,
+                                  const int64_t* __restrict__ kdev, int32_t* __restrict__ kexp) {
+  const int64_t b = blockIdx.y;
+  const int64_t kd = kdev != nullptr ? min(kdev[b], w) : w;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < w; t += (int64_t)gridDim.x * blockDim.x) {
+    int32_t e = 0;
+    if (t < kd) {
+      const int64_t i = column != nullptr ? column[b * w_stride + t] : t;
+      const double c = colsq[b * n_stride + i], r = rowsq[b * n_stride + i];
+      if (c > 0.0 && r > 0.0 && c < 1e300 && r < 1e300) {
+        const int d = ilogb(r) - ilogb(c);  // log2(||N_i||^2 / ||M_i||^2)
+        e = (int32_t)((d >= 0 ? d + 2 : d - 2) / 4);
+        e = max(-200, min(200, e));
+      }
+    }
+    kexp[b * w_stride + t] = e;
+  }
+}
+
+// per problem: inner length, split chunk; zero the exponent maxima
+__global__ void oz_gemm_prep_kernel(const int64_t* __restrict__ kdev, int64_t kmax, int64_t splits, int64_t m,
+                                    int64_t nc, int64_t* __restrict__ kinfo, uint32_t* __restrict__ exA,
+                                    uint32_t* __restrict__ exB) {
+  const int64_t b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    int64_t kd = kdev != nullptr ? kdev[b] : kmax;
+    kd = kd < 0 ? 0 : (kd > kmax ? kmax : kd);
+    int64_t chunk = (kd + splits - 1) / splits;
+    chunk = ((chunk + OZ_BK - 1) / OZ_BK) * OZ_BK;
+    kinfo[2 * b] = kd;
+    kinfo[2 * b + 1] = chunk < OZ_BK ? OZ_BK : chunk;
+  }
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) exA[b * m + i] = 0u;
+  for (int64_t i = threadIdx.x; i < nc; i += blockDim.x) exB[b * nc + i] = 0u;
+}
+
+// row maxima of A: warp per (row, 128-column chunk)
+template <typename T, bool G>
+__global__ void __launch_bounds__(256) oz_rowmax_kernel(OzRows<T, G> A, int64_t strideA, int64_t w_stride, int64_t m,
+                                                        const int64_t* __restrict__ kinfo, uint32_t* __restrict__ exA) {
+  const int lane = threadIdx.x & 31;
+  const int64_t h = (int64_t)blockIdx.y * 8 + (threadIdx.x >> 5), b = blockIdx.z;
+  const int64_t kd = kinfo[2 * b];
+  const int64_t i0 = (int64_t)blockIdx.x * 128 + 4 * lane;
+  if (h >= m || (int64_t)blockIdx.x * 128 >= kd) return;
+  OzRows<T, G> a = A;
+  a.base += b * strideA;
+  if constexpr (G) { a.col += b * w_stride; a.sc += b * w_stride; }
+  if (a.kx != nullptr) a.kx += b * w_stride;
+  uint32_t eb = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (i0 + q < kd) eb = max(eb, oz_ebits(a.at(h, i0 + q)));
+  eb = __reduce_max_sync(0xffffffffu, eb);
+  if (lane == 0 && eb != 0) atomicMax(&exA[b * m + h], eb);
+}
+
+// column maxima of B: thread per column, 32 rows
+template <typename T, bool G>
+__global__ void __launch_bounds__(256) oz_colmax_kernel(OzCols<T, G> B, int64_t strideB, int64_t w_stride, int64_t nc,
+                                                        const int64_t* __restrict__ kinfo, uint32_t* __restrict__ exB) {
+  const int64_t f = (int64_t)blockIdx.y * 256 + threadIdx.x, b = blockIdx.z;
+  const int64_t kd = kinfo[2 * b];
+  const int64_t k0 = (int64_t)blockIdx.x * 32;
+  if (f >= nc || k0 >= kd) return;
+  OzCols<T, G> a = B;
+  a.base += b * strideB;
+  if constexpr (G) { a.col += b * w_stride; a.sc += b * w_stride; }
+  if (a.kx != nullptr) a.kx += b * w_stride;
+  const int64_t k1 = min(kd, k0 + 32);
+  uint32_t eb = 0;
+  int64_t k = k0;
+  for (; k + 8 <= k1; k += 8) {
+    double v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = a.at(k + r, f);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) eb = max(eb, oz_ebits(v[r]));
+  }
+  for (; k < k1; ++k) eb = max(eb, oz_ebits(a.at(k, f)));
+  if (eb != 0) atomicMax(&exB[b * nc + f], eb);
+}
+
+// digit planes of A: warp per (row, 128-column chunk), zero past the inner length
+template <typename T, bool G>
+__global__ void __launch_bounds__(256) oz_rowdigits_kernel(OzRows<T, G> A, int64_t strideA, int64_t w_stride, int64_t m,
+                                                           const int64_t* __restrict__ kinfo,
+                                                           const uint32_t* __restrict__ exA, int64_t P,
+                                                           uint8_t* __restrict__ planes) {
+  const int lane = threadIdx.x & 31;
+  const int64_t h = (int64_t)blockIdx.y * 8 + (threadIdx.x >> 5), b = blockIdx.z;
+  const int64_t kd = kinfo[2 * b];
+  const int64_t kpad = ((kd + OZ_BK - 1) / OZ_BK) * OZ_BK;
+  const int64_t i0 = (int64_t)blockIdx.x * 128 + 4 * lane;
+  if (h >= m || i0 >= kpad) return;
+  OzRows<T, G> a = A;
+  a.base += b * strideA;
+  if constexpr (G) { a.col += b * w_stride; a.sc += b * w_stride; }
+  if (a.kx != nullptr) a.kx += b * w_stride;
+  double s1, s2;
+  oz_scales(oz_exponent_from_bits(exA[b * m + h]), s1, s2);
+  uint32_t w0[4], w1[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double x = i0 + q < kd ? a.at(h, i0 + q) : 0.0;
+    oz_digits(x, s1, s2, w0[q], w1[q]);
+  }
+  uint8_t* o = planes + ((b * OZ_S) * m + h) * P + i0;
+  const int64_t plane = m * P;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    *reinterpret_cast<uint32_t*>(o + u * plane) = oz_gather_byte(w0, u);
+    *reinterpret_cast<uint32_t*>(o + (4 + u) * plane) = oz_gather_byte(w1, u);
+  }
+}
+
+// digit planes of B^T: CTA per (32-row chunk, 64 columns), transposed in shared memory
+template <typename T, bool G>
+__global__ void __launch_bounds__(256) oz_coldigits_kernel(OzCols<T, G> B, int64_t strideB, int64_t w_stride,
+                                                           int64_t nc, const int64_t* __restrict__ kinfo,
+                                                           const uint32_t* __restrict__ exB, int64_t P,
+                                                           uint8_t* __restrict__ planes) {
+  __shared__ __align__(16) uint8_t tile[OZ_S][64][32];
+  const int64_t b = blockIdx.z;
+  const int64_t kd = kinfo[2 * b];
+  const int64_t k0 = (int64_t)blockIdx.x * 32;
+  if (k0 >= ((kd + OZ_BK - 1) / OZ_BK) * OZ_BK) return;
+  const int g = threadIdx.x >> 6, c = threadIdx.x & 63;
+  const int64_t f0 = (int64_t)blockIdx.y * 64, f = f0 + c;
+  const bool fv = f < nc;
+  OzCols<T, G> a = B;
+  a.base += b * strideB;
+  if constexpr (G) { a.col += b * w_stride; a.sc += b * w_stride; }
+  if (a.kx != nullptr) a.kx += b * w_stride;
+  double s1 = 0.0, s2 = 0.0;
+  if (fv) oz_scales(oz_exponent_from_bits(exB[b * nc + f]), s1, s2);
+  uint32_t w0[8], w1[8];
+  double x[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int64_t k = k0 + 8 * g + r;
+    x[r] = (fv && k < kd) ? a.at(k, f) : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) oz_digits(x[r], s1, s2, w0[r], w1[r]);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t a0[4] = {w0[0], w0[1], w0[2], w0[3]}, a1[4] = {w0[4], w0[5], w0[6], w0[7]};
+    const uint32_t b0[4] = {w1[0], w1[1], w1[2], w1[3]}, b1[4] = {w1[4], w1[5], w1[6], w1[7]};
+    *reinterpret_cast<uint2*>(&tile[u][c][8 * g]) = make_uint2(oz_gather_byte(a0, u), oz_gather_byte(a1, u));
+    *reinterpret_cast<uint2*>(&tile[4 + u][c][8 * g]) = make_uint2(oz_gather_byte(b0, u), oz_gather_byte(b1, u));
+  }
+  __syncthreads();
+  const int64_t plane = nc * P;
+  uint8_t* out = planes + (b * OZ_S) * plane + k0;
+#pragma unroll
+  for (int z = 0; z < 4; ++z) {
+    const int q = threadIdx.x + 256 * z;
+    const int u = q >> 7, cc = (q >> 1) & 63, half = q & 1;
+    if (f0 + cc < nc)
+      *reinterpret_cast<uint4*>(out + u * plane + (f0 + cc) * P + 16 * half) =
+          *reinterpret_cast<const uint4*>(&tile[u][cc][16 * half]);
+  }
+}
+
+// out[b] = sum over splits (fixed order) of part[b][split]
+__global__ void oz_splitk_reduce_kernel(const double* __restrict__ part, int64_t splits, int64_t m, int64_t nc,
+                                        int64_t batch, double* __restrict__ out, int64_t ldo, int64_t strideO) {
+  const int64_t total = batch * m * nc;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g / (m * nc), r = g % (m * nc);
+    const int64_t h = r / nc, f = r % nc;
+    const double* p = part + (b * splits) * m * nc + r;
+    double acc = p[0];
+    for (int64_t s = 1; s < splits; ++s) acc += p[s * m * nc];
+    out[b * strideO + h * ldo + f] = acc;
   }
 }
 
@@ -746,9 +1008,12 @@ static int segsq_i8_impl(int dtype, const void* A, int64_t lda, int64_t strideA,
   geo.TM = ceil_div(m, OZ_BM);
   geo.TN = ceil_div(nc, OZ_BN);
   geo.items = batch * nseg * geo.TM * geo.TN;
+  geo.kinfo = nullptr;
+  geo.out = nullptr;
+  geo.ldo = geo.strideO = 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(oz_segsq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+    cudaFuncSetAttribute(oz_mma_kernel<EPI_SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
     attr = true;
   }
   static int nsm = [] {
@@ -762,8 +1027,8 @@ static int segsq_i8_impl(int dtype, const void* A, int64_t lda, int64_t strideA,
     return e ? atoi(e) : 0;
   }();
   if (ev) cudaEventRecord(ev[1], st);
-  oz_segsq_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(ma, mb, geo, perm, po, L, exa, exb, part, mode);
-  BMM_CHECK_LAUNCH("oz_segsq_kernel");
+  oz_mma_kernel<EPI_SEG><<<grid, OZ_THREADS, OZ_SMEM, st>>>(ma, mb, geo, perm, po, L, exa, exb, part, mode);
+  BMM_CHECK_LAUNCH("oz_mma_kernel");
   if (ev) cudaEventRecord(ev[2], st);
   oz_reduce_kernel<<<grid_for(batch * nseg, 128), 128, 0, st>>>(part, geo.TM * geo.TN, nseg, batch * nseg, flag, gsq);
   BMM_CHECK_LAUNCH("oz_reduce_kernel");
@@ -796,4 +1061,173 @@ extern "C" int bmm_segsq_i8_timed(int dtype, const void* A, int64_t lda, int64_t
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return rc;
+}
+
+// ---------------------------------------------------------------- product mode host side
+namespace bmm {
+struct OzGemmLayout {
+  int64_t P, splits;
+  int64_t off_a, off_b, off_exa, off_exb, off_kinfo, off_part, total;
+};
+
+static int oz_nsm() {
+  static int nsm = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return nsm;
+}
+
+// K splits: minimise waves x (stages per item + epilogue allowance), at least 8 stages per item
+static int64_t oz_splits(int64_t tiles, int64_t k_max) {
+  const int64_t kt = (k_max + OZ_BK - 1) / OZ_BK;
+  const int64_t nsm = oz_nsm();
+  const int64_t s_min = ceil_div(k_max, OZ_KMAX);  // exact int32 levels per split
+  int64_t best = s_min;
+  double best_cost = 1e300;
+  for (int64_t s = s_min; s <= 16; ++s) {
+    if (s > s_min && ceil_div(kt, s) < 8) break;
+    const double cost = (double)ceil_div(tiles * s, nsm) * (double)(ceil_div(kt, s) + 3);
+    if (cost < best_cost * 0.97) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
+}
+
+static OzGemmLayout oz_gemm_layout(int64_t m, int64_t nc, int64_t k_max, int64_t batch) {
+  OzGemmLayout l;
+  l.P = ((k_max + OZ_BK - 1) / OZ_BK) * OZ_BK;
+  l.splits = oz_splits(batch * ceil_div(m, OZ_BM) * ceil_div(nc, OZ_BN), k_max);
+  int64_t o = 0;
+  l.off_a = o;     o = al256(o + batch * OZ_S * m * l.P);
+  l.off_b = o;     o = al256(o + batch * OZ_S * nc * l.P);
+  l.off_exa = o;   o = al256(o + batch * m * 4);
+  l.off_exb = o;   o = al256(o + batch * nc * 4);
+  l.off_kinfo = o; o = al256(o + batch * 16);
+  l.off_part = o;  o = al256(o + (l.splits > 1 ? batch * l.splits * m * nc * 8 : 0));
+  l.total = o;
+  return l;
+}
+}  // namespace bmm
+
+extern "C" int64_t bmm_gemm_i8_workspace(int64_t m, int64_t nc, int64_t k_max, int64_t batch) {
+  if (m < 1 || nc < 1 || k_max < 1 || batch < 1) return 0;
+  return oz_gemm_layout(m, nc, k_max, batch).total;
+}
+
+template <typename T, bool G>
+static void oz_gemm_split_launch(const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                                 int64_t strideB, const int64_t* col, const double* scale, const int32_t* kexp,
+                                 int64_t w_stride, int64_t m, int64_t nc, int64_t batch, const OzGemmLayout& l,
+                                 uint8_t* w, cudaStream_t st) {
+  const int64_t* kinfo = (const int64_t*)(w + l.off_kinfo);
+  uint32_t* exa = (uint32_t*)(w + l.off_exa);
+  uint32_t* exb = (uint32_t*)(w + l.off_exb);
+  OzRows<T, G> ra{(const T*)A, lda, col, scale, kexp};
+  OzCols<T, G> cb{(const T*)B, ldb, col, scale, kexp};
+  dim3 gr((unsigned)ceil_div(l.P, 128), (unsigned)ceil_div(m, 8), (unsigned)batch);
+  dim3 gc((unsigned)ceil_div(l.P, 32), (unsigned)ceil_div(nc, 256), (unsigned)batch);
+  dim3 gd((unsigned)ceil_div(l.P, 32), (unsigned)ceil_div(nc, 64), (unsigned)batch);
+  oz_rowmax_kernel<T, G><<<gr, 256, 0, st>>>(ra, strideA, w_stride, m, kinfo, exa);
+  oz_colmax_kernel<T, G><<<gc, 256, 0, st>>>(cb, strideB, w_stride, nc, kinfo, exb);
+  oz_rowdigits_kernel<T, G><<<gr, 256, 0, st>>>(ra, strideA, w_stride, m, kinfo, exa, l.P, w + l.off_a);
+  oz_coldigits_kernel<T, G><<<gd, 256, 0, st>>>(cb, strideB, w_stride, nc, kinfo, exb, l.P, w + l.off_b);
+  count_launch(3);
+}
+
+static int gemm_i8_impl(int dtype, const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                        int64_t strideB, const int64_t* col, const double* scale, const int32_t* kexp,
+                        int64_t w_stride, int64_t m,
+                        int64_t nc, int64_t k_max, const int64_t* k_dev, int64_t batch, double* out, int64_t ldo,
+                        int64_t strideO, void* ws, int64_t ws_bytes, void* stream) {
+  BMM_REQUIRE(m >= 1 && nc >= 1 && k_max >= 1 && batch >= 1, BMM_E_ARG, "bmm_gemm_i8: bad shape");
+  BMM_REQUIRE(A != nullptr && B != nullptr && out != nullptr, BMM_E_ARG, "bmm_gemm_i8: null pointer");
+  BMM_REQUIRE(dtype == BMM_F64 || dtype == BMM_F32, BMM_E_ARG, "bmm_gemm_i8: unknown dtype %d", dtype);
+  BMM_REQUIRE(k_max <= OZ_KMAX * 16, BMM_E_UNSUPPORTED, "bmm_gemm_i8: k_max > %d", OZ_KMAX * 16);
+  const OzGemmLayout l = oz_gemm_layout(m, nc, k_max, batch);
+  BMM_REQUIRE(ceil_div(k_max, l.splits) <= OZ_KMAX, BMM_E_UNSUPPORTED, "bmm_gemm_i8: split longer than %d",
+              OZ_KMAX);
+  BMM_REQUIRE(ws != nullptr && ws_bytes >= l.total, BMM_E_ARG, "bmm_gemm_i8: workspace too small (%lld < %lld)",
+              (long long)ws_bytes, (long long)l.total);
+  BMM_REQUIRE(batch * OZ_S <= 65535 && batch <= 65535 && l.P < (1LL << 31) && m < (1LL << 31) && nc < (1LL << 31),
+              BMM_E_UNSUPPORTED, "bmm_gemm_i8: problem too large");
+  uint8_t* w = (uint8_t*)ws;
+  cudaStream_t st = as_stream(stream);
+  int64_t* kinfo = (int64_t*)(w + l.off_kinfo);
+  oz_gemm_prep_kernel<<<(unsigned)batch, 256, 0, st>>>(k_dev, k_max, l.splits, m, nc, kinfo,
+                                                       (uint32_t*)(w + l.off_exa), (uint32_t*)(w + l.off_exb));
+  BMM_CHECK_LAUNCH("oz_gemm_prep_kernel");
+  const bool g = col != nullptr;
+  if (dtype == BMM_F64) {
+    if (g) oz_gemm_split_launch<double, true>(A, lda, strideA, B, ldb, strideB, col, scale, kexp, w_stride, m, nc, batch, l, w, st);
+    else oz_gemm_split_launch<double, false>(A, lda, strideA, B, ldb, strideB, col, scale, kexp, w_stride, m, nc, batch, l, w, st);
+  } else {
+    if (g) oz_gemm_split_launch<float, true>(A, lda, strideA, B, ldb, strideB, col, scale, kexp, w_stride, m, nc, batch, l, w, st);
+    else oz_gemm_split_launch<float, false>(A, lda, strideA, B, ldb, strideB, col, scale, kexp, w_stride, m, nc, batch, l, w, st);
+  }
+  BMM_CHECK_LAUNCH("oz_digits_kernel");
+  CUtensorMap ma, mb;
+  int rc;
+  if ((rc = oz_map(&ma, w + l.off_a, m, batch * OZ_S, l.P, OZ_BM)) != BMM_OK) return rc;
+  if ((rc = oz_map(&mb, w + l.off_b, nc, batch * OZ_S, l.P, OZ_BN)) != BMM_OK) return rc;
+  OzGeom geo;
+  geo.m = m;
+  geo.nc = nc;
+  geo.nseg = l.splits;
+  geo.TM = ceil_div(m, OZ_BM);
+  geo.TN = ceil_div(nc, OZ_BN);
+  geo.items = batch * l.splits * geo.TM * geo.TN;
+  geo.kinfo = kinfo;
+  geo.out = out;
+  geo.ldo = ldo;
+  geo.strideO = strideO;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(oz_mma_kernel<EPI_OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+    attr = true;
+  }
+  const unsigned grid = (unsigned)(geo.items < oz_nsm() ? geo.items : oz_nsm());
+  double* part = (double*)(w + l.off_part);
+  oz_mma_kernel<EPI_OUT><<<grid, OZ_THREADS, OZ_SMEM, st>>>(ma, mb, geo, nullptr, nullptr, nullptr,
+                                                            (const int32_t*)(w + l.off_exa),
+                                                            (const int32_t*)(w + l.off_exb), part, 0);
+  BMM_CHECK_LAUNCH("oz_mma_kernel");
+  if (l.splits > 1) {
+    oz_splitk_reduce_kernel<<<grid_for(batch * m * nc, 256), 256, 0, st>>>(part, l.splits, m, nc, batch, out, ldo,
+                                                                          strideO);
+    BMM_CHECK_LAUNCH("oz_splitk_reduce_kernel");
+  }
+  return BMM_OK;
+}
+
+extern "C" int bmm_gemm_i8(int dtype, const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                           int64_t strideB, int64_t m, int64_t nc, int64_t k_max, const int64_t* k_dev,
+                           const int32_t* kexp, int64_t batch, double* out, int64_t ldo, int64_t strideO, void* ws,
+                           int64_t ws_bytes, void* stream) {
+  return gemm_i8_impl(dtype, A, lda, strideA, B, ldb, strideB, nullptr, nullptr, kexp, k_max, m, nc, k_max, k_dev,
+                      batch, out, ldo, strideO, ws, ws_bytes, stream);
+}
+
+extern "C" int bmm_gemm_i8_gather(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
+                                  int64_t ldn, int64_t strideN, const int64_t* column, const double* scale,
+                                  const int32_t* kexp, int64_t w_stride, int64_t m, int64_t nc, int64_t k_max,
+                                  const int64_t* k_dev, int64_t batch, double* out, int64_t ldo, int64_t strideO,
+                                  void* ws, int64_t ws_bytes, void* stream) {
+  BMM_REQUIRE(column != nullptr && scale != nullptr, BMM_E_ARG, "bmm_gemm_i8_gather: column/scale is NULL");
+  return gemm_i8_impl(dtype, M, ldm, strideM, N, ldn, strideN, column, scale, kexp, w_stride, m, nc, k_max, k_dev,
+                      batch, out, ldo, strideO, ws, ws_bytes, stream);
+}
+
+extern "C" int bmm_balance_exponents(const double* colsq, const double* rowsq, int64_t n_stride,
+                                     const int64_t* column, int64_t w, int64_t w_stride, const int64_t* k_dev,
+                                     int64_t batch, int32_t* kexp, void* stream) {
+  BMM_REQUIRE(colsq != nullptr && rowsq != nullptr && kexp != nullptr && w >= 1 && batch >= 1 && batch <= 65535,
+              BMM_E_ARG, "bmm_balance_exponents: bad arguments");
+  dim3 grid((unsigned)ceil_div(w, 256) < 1024u ? (unsigned)ceil_div(w, 256) : 1024u, (unsigned)batch);
+  oz_balance_kernel<<<grid, 256, 0, as_stream(stream)>>>(colsq, rowsq, n_stride, column, w, w_stride, k_dev, kexp);
+  BMM_CHECK_LAUNCH("oz_balance_kernel");
+  return BMM_OK;
 }

@@ -7,7 +7,7 @@ stream with no allocation and no host synchronisation:
   K1 bmm_norms -> K2 bmm_block_probs -> [OPL: bmm_segsq_i8 of M^k N_k]
   [two-step: pilot budgets -> CDF -> child seeds -> draws -> gather -> segsq]
   -> bmm_budgets -> bmm_block_cdf -> bmm_seed_streams -> bmm_sample
-  -> bmm_gather -> bmm_gemm_f64  (C @ D)
+  -> bmm_gather -> bmm_gemm_f64  (C @ D), or bmm_gemm_i8_gather for large contractions
 
 It computes exactly what the reference composition computes
 (allocate_* + estimate_product, estimate_product_two_step,
@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from . import rng as _rng
-from .plan import raise_status, segsq_engine
+from .plan import gemm_engine, raise_status, segsq_engine
 
 METHODS = ("OPL", "ONC", "UU", "ONU", "ONMCNR", "SSM")
 
@@ -176,15 +176,21 @@ class SketchPipeline:
             self.b_x = torch.empty(B * self.p * W, **f32)
             self.CD = torch.empty(B * self.m * self.p, **f32)
         else:
-            # float64 path: gather the rescaled sketch (bandwidth-bound kernel at
-            # full occupancy), then C @ D on the DMMA pipe.  Gathering M's columns
-            # inside the GEMM (bmm_gemm_f64_gather) is one 8-byte copy per element
-            # and measured slower on the tensor-bound kernel.
-            self.C = torch.empty(B * self.m * W, **f64)
-            self.D = torch.empty(B * W * self.p, **f64)
+            # float64 path.  Large contractions: the int8 Ozaki path with the sketch
+            # gathered inside its digit split (bmm_gemm_i8_gather).  Otherwise gather the
+            # rescaled sketch (bandwidth-bound kernel at full occupancy), then C @ D on
+            # the DMMA pipe.
+            self.gemm_engine = "dmma" if method == "SSM" else gemm_engine(self.m, self.p, W)
             self.CD = torch.empty(B * self.m * self.p, **f64)
-            self.ws_gemm = torch.empty(max(256, self.lib.bmm_gemm_f64_workspace(self.m, self.p, W, B)),
-                                       dtype=torch.uint8, device=dev)
+            if self.gemm_engine == "i8":
+                self.ws_gemm = torch.empty(max(256, self.lib.bmm_gemm_i8_workspace(self.m, self.p, W, B)),
+                                           dtype=torch.uint8, device=dev)
+                self.kexp = torch.empty(B * W, dtype=torch.int32, device=dev)
+            else:
+                self.C = torch.empty(B * self.m * W, **f64)
+                self.D = torch.empty(B * W * self.p, **f64)
+                self.ws_gemm = torch.empty(max(256, self.lib.bmm_gemm_f64_workspace(self.m, self.p, W, B)),
+                                           dtype=torch.uint8, device=dev)
         if method == "OPL":
             self.gsq = torch.empty(B * K, **f64)
             # g_k^2 on the int8 tensor cores (Ozaki split; float32 inputs read directly)
@@ -402,6 +408,26 @@ class SketchPipeline:
                     B, P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), st)
             self._c("bmm_gemm_f32split", P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), m, p, W, B,
                     P(self.CD), p, m * p, st)
+        else:
+            self.contract(M, N, st)
+        return self._result()
+
+    def contract(self, M, N, st=None):
+        """C @ D of the current sketch on the float64 path (gather + DMMA GEMM, or
+        the int8 Ozaki contraction with the gather fused into its digit split)."""
+        B, m, n, p, W = self.B, self.m, self.n, self.p, self.W
+        st = _lib.stream_ptr() if st is None else st
+        dt = _lib.matrix_dtype(M)
+        sM, sN = m * n, n * p
+        ldm, ldn = M.stride(-2), N.stride(-2)
+        P = lambda t: t.data_ptr()  # noqa: E731
+        col, sc = (self.k_column, self.k_scale) if self.compress else (self.column, self.scale)
+        if self.gemm_engine == "i8":
+            kd = P(self.k_count) if self.compress else None
+            # balance C's columns against D's rows with the norm pass (exact powers of two)
+            self._c("bmm_balance_exponents", P(self.colsq), P(self.rowsq), n, P(col), W, W, kd, B, P(self.kexp), st)
+            self._c("bmm_gemm_i8_gather", dt, P(M), ldm, sM, P(N), ldn, sN, P(col), P(sc), P(self.kexp), W, m, p, W,
+                    kd, B, P(self.CD), p, m * p, P(self.ws_gemm), self.ws_gemm.numel(), st)
         elif self.compress:
             self._c("bmm_gather_dk", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
                     P(self.k_scale), W, W, P(self.k_count), B, P(self.C), W, m * W, P(self.D), p, W * p, st)
@@ -412,7 +438,6 @@ class SketchPipeline:
                     P(self.scale), W, W, B, P(self.C), W, m * W, P(self.D), p, W * p, st)
             self._c("bmm_gemm_f64", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, B, P(self.CD), p, m * p,
                     P(self.ws_gemm), self.ws_gemm.numel(), st)
-        return self._result()
 
     def _run_ssm(self, M, N, dt, st):
         B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W

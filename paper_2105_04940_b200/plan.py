@@ -208,6 +208,19 @@ def segsq_engine(max_len: int) -> str:
     return "i8" if max_len <= SEGSQ_I8_MAX_LEN else "dmma"
 
 
+GEMM_I8_MIN_FLOPS = 1e10  # below this the DMMA GEMM's single pass beats the split + int8 contraction
+
+
+def gemm_engine(m: int, p: int, k: int) -> str:
+    """Kernel for the float64 sampled contraction C @ D: "i8" (bmm_gemm_i8_gather,
+    int8 tensor cores on Ozaki digit planes, gather fused into the split) for
+    2 m p k >= GEMM_I8_MIN_FLOPS, else "dmma"; BMM_GEMM=i8|dmma forces one."""
+    forced = os.environ.get("BMM_GEMM", "").lower()
+    if forced in ("i8", "dmma"):
+        return forced
+    return "i8" if 2.0 * m * p * k >= GEMM_I8_MIN_FLOPS else "dmma"
+
+
 def segsq(A: torch.Tensor, B: torch.Tensor, seg: torch.Tensor, nseg: int) -> torch.Tensor:
     if A.dtype != torch.float64:
         A = A.to(torch.float64)
