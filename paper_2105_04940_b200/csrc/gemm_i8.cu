@@ -52,7 +52,9 @@ constexpr int OZ_B_PLANE = OZ_BN * OZ_BK;            // 2 KB
 constexpr int OZ_STAGE = OZ_S * (OZ_A_PLANE + OZ_B_PLANE);  // 48 KB
 constexpr int OZ_STAGES = 4;
 constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE + 1024 + 1024;
-constexpr int OZ_THREADS = 192;    // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int OZ_EPI_WARPS = 8;    // two per TMEM lane quarter, 32 columns each
+constexpr int OZ_EPI_COLS = OZ_BN / (OZ_EPI_WARPS / 4);
+constexpr int OZ_THREADS = 64 + 32 * OZ_EPI_WARPS;  // warp 0 TMA, warp 1 MMA, then the epilogue warps
 constexpr int OZ_TMEM_COLS = 512;
 
 // balanced base-128 offset: 64 in every digit position (F + C has fields f_t,
@@ -118,7 +120,7 @@ __device__ __forceinline__ uint32_t oz_gather_byte(const uint32_t (&a)[4], int u
 __global__ void __launch_bounds__(1024) oz_prep_kernel(const int64_t* __restrict__ seg, int64_t nseg,
                                                        int64_t seg_stride, int64_t cap, int64_t* __restrict__ po,
                                                        int32_t* __restrict__ L, int32_t* __restrict__ perm,
-                                                       int32_t* __restrict__ flag) {
+                                                       int32_t* __restrict__ flag, int4* __restrict__ cmap) {
   __shared__ int64_t wsum[32];
   __shared__ int64_t base_s;
   __shared__ int flag_s;
@@ -187,6 +189,20 @@ __global__ void __launch_bounds__(1024) oz_prep_kernel(const int64_t* __restrict
     pb[r] = (int32_t)j;
   }
   if (threadIdx.x == 0) flag[b] = flag_s;
+  // chunk map over the padded inner extent: chunk c (32 padded positions) ->
+  // (segment, first original row, real rows in the chunk); -1 past the end
+  const int64_t nch = cap / 32;
+  int4* cm = cmap + b * nch;
+  const int64_t used = flag_s ? 0 : base_s / 32;
+  for (int64_t j = threadIdx.x; j < nseg && !flag_s; j += 1024) {
+    const int64_t len = s[j + 1] - s[j];
+    const int64_t c0 = pob[j] / 32, nc = Lb[j] / 32;
+    for (int64_t c = 0; c < nc; ++c) {
+      const int64_t k = s[j] + 32 * c;  // < 2^31: checked on the host
+      cm[c0 + c] = make_int4((int)j, (int)k, (int)min((int64_t)32, len - 32 * c), 0);
+    }
+  }
+  for (int64_t c = used + threadIdx.x; c < nch; c += 1024) cm[c] = make_int4(-1, 0, 0, 0);
 }
 
 // ---------------------------------------------------------------- split of A
@@ -243,110 +259,74 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const T* __restrict_
 }
 
 // ---------------------------------------------------------------- split of B
-// Cluster of OZ_CL CTAs per (segment j, 64 columns), each owning a contiguous
-// piece of the segment's rows: column maxima of the piece, exchanged through
-// distributed shared memory (every CTA takes the max over the cluster), then
-// 32-row chunks: thread (g, c) converts rows 8g..8g+7 of column c, the digit
-// bytes are transposed into a [plane][column][32] shared tile and written as
-// 16-byte pieces of the K-major planes B^T.
-constexpr int OZ_CL = 8;
+// Chunk-parallel over the padded inner extent (32 rows of N per chunk, each
+// inside one segment): (1) column maxima as biased exponent fields, atomicMax
+// into the segment's per-column slot; (2) digits: CTA per (chunk, 64 columns),
+// thread (g, c) converts rows 8g..8g+7 of column c, the digit bytes are
+// transposed into a [plane][column][32] shared tile and written as 16-byte
+// pieces of the K-major planes B^T.
+template <typename T>
+__global__ void __launch_bounds__(256) oz_seg_colmax_kernel(const T* __restrict__ B, int64_t ldb, int64_t strideB,
+                                                            int64_t nc, int64_t nseg, int64_t nch,
+                                                            const int4* __restrict__ cmap,
+                                                            uint32_t* __restrict__ ex) {
+  const int64_t c = blockIdx.x, b = blockIdx.z;
+  const int4 cm = cmap[b * nch + c];
+  const int64_t f = (int64_t)blockIdx.y * 256 + threadIdx.x;
+  if (cm.x < 0 || f >= nc) return;
+  const T* p = B + b * strideB + (int64_t)cm.y * ldb + f;
+  uint32_t eb = 0;
+  int r = 0;
+  for (; r + 8 <= cm.z; r += 8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = oz_ld(p + (int64_t)(r + q) * ldb);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) eb = max(eb, oz_ebits(v[q]));
+  }
+  for (; r < cm.z; ++r) eb = max(eb, oz_ebits(oz_ld(p + (int64_t)r * ldb)));
+  if (eb != 0) atomicMax(&ex[(b * nseg + cm.x) * nc + f], eb);
+}
 
 template <typename T>
-__global__ void __launch_bounds__(256) oz_split_cols_kernel(const T* __restrict__ B, int64_t ldb, int64_t strideB,
-                                                            int64_t nc, const int64_t* __restrict__ seg,
-                                                            int64_t nseg, int64_t seg_stride,
-                                                            const int64_t* __restrict__ po,
-                                                            const int32_t* __restrict__ L, int64_t P,
-                                                            uint8_t* __restrict__ planes, int32_t* __restrict__ ex,
-                                                            const int32_t* __restrict__ flag) {
-  __shared__ uint32_t red[4][64];
-  __shared__ uint32_t cmax[64];
+__global__ void __launch_bounds__(256) oz_seg_coldigits_kernel(const T* __restrict__ B, int64_t ldb, int64_t strideB,
+                                                               int64_t nc, int64_t nseg, int64_t nch,
+                                                               const int4* __restrict__ cmap,
+                                                               const uint32_t* __restrict__ ex, int64_t P,
+                                                               uint8_t* __restrict__ planes) {
   __shared__ __align__(16) uint8_t tile[OZ_S][64][32];
-  const int64_t j = blockIdx.y % nseg, b = blockIdx.y / nseg;
-  const int piece = blockIdx.z;  // == cluster rank (cluster dims 1 x 1 x OZ_CL)
-  const int Lj = L[b * nseg + j];
-  const bool active = Lj > 0 && flag[b] == 0;  // uniform over the cluster
-  const int g = threadIdx.x >> 6, c = threadIdx.x & 63;
-  const int64_t f0 = (int64_t)blockIdx.x * 64;
-  const int64_t f = f0 + c;
+  const int64_t c = blockIdx.x, b = blockIdx.z;
+  const int4 cm = cmap[b * nch + c];
+  if (cm.x < 0) return;
+  const int g = threadIdx.x >> 6, cc = threadIdx.x & 63;
+  const int64_t f0 = (int64_t)blockIdx.y * 64, f = f0 + cc;
   const bool fv = f < nc;
-  const int64_t s0 = active ? seg[b * seg_stride + j] : 0;
-  const int len = active ? (int)(seg[b * seg_stride + j + 1] - s0) : 0;
-  // this CTA's rows: [r0, r1) in 32-row chunks
-  const int nch = Lj / 32;
-  const int per = (nch + OZ_CL - 1) / OZ_CL;
-  const int r0 = min(piece * per, nch) * 32, r1 = min((piece + 1) * per, nch) * 32;
-  const T* col = B + b * strideB + s0 * ldb + f;
-  uint32_t eb = 0;
-  if (fv) {
-    const int hi = min(r1, len);
-    int i = r0 + g;
-    const T* pc = col + (int64_t)i * ldb;
-    const int64_t step = 4 * ldb;
-    for (; i + 28 < hi; i += 32, pc += 8 * step) {  // 8 rows in flight per thread
-      double v[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) v[r] = oz_ld(pc + r * step);
-#pragma unroll
-      for (int r = 0; r < 8; ++r) eb = max(eb, oz_ebits(v[r]));
-    }
-    for (; i < hi; i += 4, pc += step) eb = max(eb, oz_ebits(oz_ld(pc)));
-  }
-  red[g][c] = eb;
-  __syncthreads();
-  if (g == 0) cmax[c] = max(max(red[0][c], red[1][c]), max(red[2][c], red[3][c]));
-  // the cluster's column maxima
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-  eb = 0;
-  {
-    const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&cmax[c]));
-#pragma unroll
-    for (int rk = 0; rk < OZ_CL; ++rk) {
-      uint32_t remote, v;
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local), "r"(rk));
-      asm volatile("ld.shared::cluster.u32 %0, [%1];\n" : "=r"(v) : "r"(remote) : "memory");
-      eb = max(eb, v);
-    }
-  }
-  // peers may exit (their shared memory vanishes) only after everyone has read it
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-  if (!active || r0 >= r1) return;
-  const int e = oz_exponent_from_bits(eb);
-  if (g == 0 && piece == 0 && fv) ex[(b * nseg + j) * nc + f] = e;
-  double s1, s2;
-  oz_scales(e, s1, s2);
-  const int64_t plane = nc * P;
-  uint8_t* out = planes + (b * OZ_S) * plane + po[b * nseg + j];
+  double s1 = 0.0, s2 = 0.0;
+  if (fv) oz_scales(oz_exponent_from_bits(ex[(b * nseg + cm.x) * nc + f]), s1, s2);
+  const T* p = B + b * strideB + (int64_t)cm.y * ldb + f;
   double x[8];
-  const int lim = fv ? min(len, r1) : 0;  // rows this thread may read
-  const T* pr = col + (int64_t)(r0 + 8 * g) * ldb;
 #pragma unroll
-  for (int r = 0; r < 8; ++r) x[r] = (r0 + 8 * g + r < lim) ? oz_ld(pr + r * ldb) : 0.0;
-  for (int i0 = r0; i0 < r1; i0 += 32) {
-    uint32_t w0[8], w1[8];
+  for (int r = 0; r < 8; ++r) x[r] = (fv && 8 * g + r < cm.z) ? oz_ld(p + (int64_t)(8 * g + r) * ldb) : 0.0;
+  uint32_t w0[8], w1[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) oz_digits(x[r], s1, s2, w0[r], w1[r]);
-    // next chunk's values in flight during the transpose and stores
-    pr += 32 * ldb;
+  for (int r = 0; r < 8; ++r) oz_digits(x[r], s1, s2, w0[r], w1[r]);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) x[r] = (i0 + 32 + 8 * g + r < lim) ? oz_ld(pr + r * ldb) : 0.0;
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t a0[4] = {w0[0], w0[1], w0[2], w0[3]}, a1[4] = {w0[4], w0[5], w0[6], w0[7]};
+    const uint32_t b0[4] = {w1[0], w1[1], w1[2], w1[3]}, b1[4] = {w1[4], w1[5], w1[6], w1[7]};
+    *reinterpret_cast<uint2*>(&tile[u][cc][8 * g]) = make_uint2(oz_gather_byte(a0, u), oz_gather_byte(a1, u));
+    *reinterpret_cast<uint2*>(&tile[4 + u][cc][8 * g]) = make_uint2(oz_gather_byte(b0, u), oz_gather_byte(b1, u));
+  }
+  __syncthreads();
+  const int64_t plane = nc * P;
+  uint8_t* out = planes + (b * OZ_S) * plane + 32 * c;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t a0[4] = {w0[0], w0[1], w0[2], w0[3]}, a1[4] = {w0[4], w0[5], w0[6], w0[7]};
-      const uint32_t b0[4] = {w1[0], w1[1], w1[2], w1[3]}, b1[4] = {w1[4], w1[5], w1[6], w1[7]};
-      *reinterpret_cast<uint2*>(&tile[u][c][8 * g]) = make_uint2(oz_gather_byte(a0, u), oz_gather_byte(a1, u));
-      *reinterpret_cast<uint2*>(&tile[4 + u][c][8 * g]) = make_uint2(oz_gather_byte(b0, u), oz_gather_byte(b1, u));
-    }
-    __syncthreads();
-#pragma unroll
-    for (int z = 0; z < 4; ++z) {
-      const int q = threadIdx.x + 256 * z;  // 1024 pieces of 16 bytes
-      const int u = q >> 7, cc = (q >> 1) & 63, half = q & 1;
-      if (f0 + cc < nc)
-        *reinterpret_cast<uint4*>(out + u * plane + (f0 + cc) * P + i0 + 16 * half) =
-            *reinterpret_cast<const uint4*>(&tile[u][cc][16 * half]);
-    }
-    __syncthreads();
+  for (int z = 0; z < 4; ++z) {
+    const int q = threadIdx.x + 256 * z;  // 1024 pieces of 16 bytes
+    const int u = q >> 7, c2 = (q >> 1) & 63, half = q & 1;
+    if (f0 + c2 < nc)
+      *reinterpret_cast<uint4*>(out + u * plane + (f0 + c2) * P + 16 * half) =
+          *reinterpret_cast<const uint4*>(&tile[u][c2][16 * half]);
   }
 }
 
@@ -468,7 +448,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
   uint64_t* acc_empty = acc_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
   double* wcol = reinterpret_cast<double*>(smem + OZ_STAGES * OZ_STAGE + 256);  // [2][64]
-  double* red = wcol + 128;                                                     // [4]
+  double* red = wcol + 128;                                                     // [OZ_EPI_WARPS]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -477,7 +457,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 4);
+    mbar_init(acc_empty, OZ_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
@@ -556,8 +536,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
     }
   } else {
     // ---- epilogue: drain the 8 levels, square-sum the tile
-    const int e_id = threadIdx.x - 64;  // 0..127
-    const int quarter = warp & 3;
+    const int e_id = threadIdx.x - 64;  // 0 .. 32 * OZ_EPI_WARPS - 1
+    const int quarter = warp & 3;       // TMEM lanes this warp may read
+    const int cpart = (warp - 2) / 4;   // which OZ_EPI_COLS columns of the tile
+    constexpr int EPI_T = 32 * OZ_EPI_WARPS;
     uint32_t n_items = 0;
     for (int64_t w = blockIdx.x; w < geo.items; w += gridDim.x) {
       const OzItem I = oz_item<EPI>(geo, w, perm, po, L);
@@ -582,11 +564,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
       if (e_id < 64) {
         const int64_t f = col0 + e_id;
         if constexpr (EPI == EPI_SEG)
-          wc[e_id] = f < geo.nc ? ldexp(1.0, exB[(I.b * geo.nseg + I.j) * geo.nc + f] - 10) : 0.0;
+          wc[e_id] = f < geo.nc
+                         ? ldexp(1.0, oz_exponent_from_bits((uint32_t)exB[(I.b * geo.nseg + I.j) * geo.nc + f]) - 10)
+                         : 0.0;
         else
           wc[e_id] = f < geo.nc ? ldexp(1.0, oz_exponent_from_bits((uint32_t)exB[I.b * geo.nc + f]) - 10) : 0.0;
       }
-      named_sync(1, 128);
+      named_sync(1, EPI_T);
       mbar_wait(acc_full, n_items & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       if (mode == 1) {  // timing experiment: release the accumulators at once
@@ -606,12 +590,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
       }
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16);
 #pragma unroll 1
-      for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
+      for (int c0 = cpart * OZ_EPI_COLS; c0 < (cpart + 1) * OZ_EPI_COLS; c0 += 16) {
         uint32_t v[OZ_S][16];
 #pragma unroll
         for (int d = 0; d < OZ_S; ++d) tmem_ld16(tbase + (uint32_t)(d * OZ_BN + c0), v[d]);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (c0 + 16 == OZ_BN) {
+        if (c0 + 16 == (cpart + 1) * OZ_EPI_COLS) {
           asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty);
@@ -637,9 +621,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
         R = (R * sr) * sr;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) R += __shfl_xor_sync(0xffffffffu, R, o);
-        if (lane == 0) red[quarter] = R;
-        named_sync(1, 128);
-        if (e_id == 0) *prow = (red[0] + red[1]) + (red[2] + red[3]);
+        if (lane == 0) red[warp - 2] = R;
+        named_sync(1, EPI_T);
+        if (e_id == 0) {
+          double t = 0.0;
+#pragma unroll
+          for (int q = 0; q < OZ_EPI_WARPS; ++q) t += red[q];
+          *prow = t;
+        }
       }
       ++n_items;
     }
@@ -886,7 +875,7 @@ __global__ void oz_splitk_reduce_kernel(const double* __restrict__ part, int64_t
 
 struct OzLayout {
   int64_t P;                 // padded inner extent (row pitch of the planes)
-  int64_t off_a, off_b, off_exa, off_exb, off_po, off_L, off_perm, off_flag, off_part, total;
+  int64_t off_a, off_b, off_exa, off_exb, off_po, off_L, off_perm, off_flag, off_part, off_cmap, total;
 };
 
 static inline int64_t al256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -905,6 +894,7 @@ static OzLayout oz_layout(int64_t m, int64_t nc, int64_t n_inner, int64_t nseg, 
   l.off_perm = o; o = al256(o + batch * nseg * 4);
   l.off_flag = o; o = al256(o + batch * 4);
   l.off_part = o; o = al256(o + batch * nseg * TM * TN * 8);
+  l.off_cmap = o; o = al256(o + batch * (l.P / 32) * 16);
   l.total = o;
   return l;
 }
@@ -947,7 +937,8 @@ static int segsq_i8_impl(int dtype, const void* A, int64_t lda, int64_t strideA,
               (long long)ws_bytes, (long long)l.total);
   BMM_REQUIRE(batch * OZ_S * (m > nc ? m : nc) < (1LL << 31) && l.P < (1LL << 31), BMM_E_UNSUPPORTED,
               "bmm_segsq_i8: problem too large for 32-bit TMA coordinates");
-  BMM_REQUIRE(nseg <= 65535 && batch <= 65535 && nseg * batch <= 65535 && ceil_div(m, 8) <= (1LL << 31) - 1,
+  BMM_REQUIRE(nseg <= 65535 && batch <= 65535 && l.P / 32 < (1LL << 31) && ceil_div(m, 8) <= (1LL << 31) - 1 &&
+                  ceil_div(nc, 64) <= 65535,
               BMM_E_UNSUPPORTED,
               "bmm_segsq_i8: grid too large");
   uint8_t* w = (uint8_t*)ws;
@@ -963,39 +954,31 @@ static int segsq_i8_impl(int dtype, const void* A, int64_t lda, int64_t strideA,
   cudaStream_t st = as_stream(stream);
 
   if (ev) cudaEventRecord(ev[0], st);
-  oz_prep_kernel<<<(unsigned)batch, 1024, 0, st>>>(seg, nseg, seg_stride, l.P, po, L, perm, flag);
+  int4* cmap = (int4*)(w + l.off_cmap);
+  const int64_t nch = l.P / 32;
+  oz_prep_kernel<<<(unsigned)batch, 1024, 0, st>>>(seg, nseg, seg_stride, l.P, po, L, perm, flag, cmap);
   BMM_CHECK_LAUNCH("oz_prep_kernel");
+  cudaMemsetAsync(exb, 0, (size_t)batch * nseg * nc * 4, st);
   dim3 ga((unsigned)ceil_div(m, 8), (unsigned)nseg, (unsigned)batch);
-  dim3 gb((unsigned)ceil_div(nc, 64), (unsigned)(nseg * batch), OZ_CL);
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = gb;
-  lc.blockDim = dim3(256, 1, 1);
-  lc.dynamicSmemBytes = 0;
-  lc.stream = st;
-  cudaLaunchAttribute la[1];
-  la[0].id = cudaLaunchAttributeClusterDimension;
-  la[0].val.clusterDim.x = 1;
-  la[0].val.clusterDim.y = 1;
-  la[0].val.clusterDim.z = OZ_CL;
-  lc.attrs = la;
-  lc.numAttrs = 1;
-  cudaError_t ce;
+  dim3 gm((unsigned)nch, (unsigned)ceil_div(nc, 256), (unsigned)batch);
+  dim3 gd((unsigned)nch, (unsigned)ceil_div(nc, 64), (unsigned)batch);
   if (dtype == BMM_F64) {
     oz_split_rows_kernel<double><<<ga, 256, 0, st>>>((const double*)A, lda, strideA, m, seg, nseg, seg_stride, po, L,
                                                      l.P, pa, exa, flag);
-    BMM_CHECK_LAUNCH("oz_split_rows_kernel");
-    ce = cudaLaunchKernelEx(&lc, oz_split_cols_kernel<double>, (const double*)B, ldb, strideB, nc, seg, nseg,
-                            seg_stride, (const int64_t*)po, (const int32_t*)L, l.P, pb, exb, (const int32_t*)flag);
+    oz_seg_colmax_kernel<double><<<gm, 256, 0, st>>>((const double*)B, ldb, strideB, nc, nseg, nch, cmap,
+                                                     (uint32_t*)exb);
+    oz_seg_coldigits_kernel<double><<<gd, 256, 0, st>>>((const double*)B, ldb, strideB, nc, nseg, nch, cmap,
+                                                        (const uint32_t*)exb, l.P, pb);
   } else {
     oz_split_rows_kernel<float><<<ga, 256, 0, st>>>((const float*)A, lda, strideA, m, seg, nseg, seg_stride, po, L,
                                                     l.P, pa, exa, flag);
-    BMM_CHECK_LAUNCH("oz_split_rows_kernel");
-    ce = cudaLaunchKernelEx(&lc, oz_split_cols_kernel<float>, (const float*)B, ldb, strideB, nc, seg, nseg,
-                            seg_stride, (const int64_t*)po, (const int32_t*)L, l.P, pb, exb, (const int32_t*)flag);
+    oz_seg_colmax_kernel<float><<<gm, 256, 0, st>>>((const float*)B, ldb, strideB, nc, nseg, nch, cmap,
+                                                    (uint32_t*)exb);
+    oz_seg_coldigits_kernel<float><<<gd, 256, 0, st>>>((const float*)B, ldb, strideB, nc, nseg, nch, cmap,
+                                                       (const uint32_t*)exb, l.P, pb);
   }
-  BMM_REQUIRE(ce == cudaSuccess, BMM_E_CUDA, "oz_split_cols_kernel: cluster launch failed: %s",
-              cudaGetErrorString(cudaGetLastError()));
-  BMM_CHECK_LAUNCH("oz_split_cols_kernel");
+  count_launch(2);
+  BMM_CHECK_LAUNCH("oz_split_kernels");
 
   CUtensorMap ma, mb;
   int rc;

@@ -185,7 +185,7 @@ class ShardedApproxProduct:
         aux = None
         if self.method == "OPL":
             # C2: g_k^2 partials of this rank's output tile
-            if segsq_engine(max(self.sizes)) == "i8":
+            if segsq_engine(max(self.sizes), M_local.shape[0], N_local.shape[1], n) == "i8":
                 A, B = M_local.contiguous(), N_local.contiguous()
                 if A.dtype != B.dtype:
                     A, B = A.double(), B.double()

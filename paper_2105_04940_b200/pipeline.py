@@ -194,7 +194,7 @@ class SketchPipeline:
         if method == "OPL":
             self.gsq = torch.empty(B * K, **f64)
             # g_k^2 on the int8 tensor cores (Ozaki split; float32 inputs read directly)
-            self.seg_engine = segsq_engine(self.max_len)
+            self.seg_engine = segsq_engine(self.max_len, self.m, self.p, self.n)
             wsb = (self.lib.bmm_segsq_i8_workspace(self.m, self.p, self.n, K, B) if self.seg_engine == "i8"
                    else self.lib.bmm_segsq_f64_workspace(self.m, self.p, K, B))
             self.ws_seg = torch.empty(max(256, wsb), dtype=torch.uint8, device=dev)

@@ -190,22 +190,26 @@ class DeviceInstance:
     def block_product_sq(self) -> torch.Tensor:
         """g_k^2 = ||M^k N_k||_F^2 for every block (segmented square sums: int8
         tensor-core Ozaki split, or DMMA; see segsq_engine)."""
-        if segsq_engine(self.max_len) == "i8":
+        if segsq_engine(self.max_len, self.M.shape[0], self.N.shape[1], self.n) == "i8":
             return segsq_i8(self.M, self.N, self.offsets, self.K)
         return segsq(self.M, self.N, self.offsets, self.K)
 
 
 SEGSQ_I8_MAX_LEN = 32768  # bmm_segsq_i8's exact-accumulation bound per segment
+SEGSQ_I8_MIN_FLOPS = 2e9  # below this the DMMA kernel's single pass beats split + int8 contraction
 
 
-def segsq_engine(max_len: int) -> str:
+def segsq_engine(max_len: int, m: int, p: int, n: int) -> str:
     """Kernel for the OPL block-product norms g_k^2: "i8" (bmm_segsq_i8, int8
-    tensor cores, float64-accurate Ozaki split) unless a block exceeds its
-    length bound or BMM_SEGSQ=dmma selects the DMMA kernel (bmm_segsq_f64)."""
+    tensor cores, float64-accurate Ozaki split) for 2 m p n >= SEGSQ_I8_MIN_FLOPS
+    unless a block exceeds its length bound; else "dmma" (bmm_segsq_f64).
+    BMM_SEGSQ=i8|dmma forces one (i8 still needs blocks <= SEGSQ_I8_MAX_LEN)."""
     forced = os.environ.get("BMM_SEGSQ", "").lower()
-    if forced in ("dmma", "f64"):
+    if max_len > SEGSQ_I8_MAX_LEN or forced in ("dmma", "f64"):
         return "dmma"
-    return "i8" if max_len <= SEGSQ_I8_MAX_LEN else "dmma"
+    if forced == "i8":
+        return "i8"
+    return "i8" if 2.0 * m * p * n >= SEGSQ_I8_MIN_FLOPS else "dmma"
 
 
 GEMM_I8_MIN_FLOPS = 1e10  # below this the DMMA GEMM's single pass beats the split + int8 contraction
