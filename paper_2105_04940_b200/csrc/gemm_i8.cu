@@ -288,46 +288,77 @@ __global__ void __launch_bounds__(256) oz_seg_colmax_kernel(const T* __restrict_
   if (eb != 0) atomicMax(&ex[(b * nseg + cm.x) * nc + f], eb);
 }
 
+// Column digit kernels: CTA per (128 padded rows, 32 columns).  Thread (g, c)
+// converts rows 16g..16g+15 of column c; the digit bytes go to a
+// [plane][column][128] shared tile, written out as full 128-byte rows of the
+// K-major planes B^T.
+constexpr int OZ_CD_ROWS = 128, OZ_CD_COLS = 32;
+
+// 8 values' digit bytes of plane u -> tile[u][c][16g + 8hh .. +7]
+__device__ __forceinline__ void oz_cd_stash8(uint8_t (*tile)[OZ_CD_COLS][OZ_CD_ROWS], int g, int c, int hh,
+                                             const uint32_t (&w0)[8], const uint32_t (&w1)[8]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t a0[4] = {w0[0], w0[1], w0[2], w0[3]}, a1[4] = {w0[4], w0[5], w0[6], w0[7]};
+    const uint32_t b0[4] = {w1[0], w1[1], w1[2], w1[3]}, b1[4] = {w1[4], w1[5], w1[6], w1[7]};
+    // 16-byte chunks of a tile row XOR-swizzled by the column: lanes (columns) 128 B
+    // apart would otherwise all hit the same banks
+    const int off = 16 * (g ^ (c & 7)) + 8 * hh;
+    *reinterpret_cast<uint2*>(&tile[u][c][off]) = make_uint2(oz_gather_byte(a0, u), oz_gather_byte(a1, u));
+    *reinterpret_cast<uint2*>(&tile[4 + u][c][off]) = make_uint2(oz_gather_byte(b0, u), oz_gather_byte(b1, u));
+  }
+}
+
+// tile -> planes: 8 x 32 rows of 128 bytes (rows >= valid_rows of the block skipped)
+__device__ __forceinline__ void oz_cd_store(const uint8_t (*tile)[OZ_CD_COLS][OZ_CD_ROWS], uint8_t* out,
+                                            int64_t plane, int64_t P, int64_t f0, int64_t nc, int bytes) {
+#pragma unroll
+  for (int z = 0; z < 8; ++z) {
+    const int q = threadIdx.x + 256 * z;  // 2048 pieces of 16 bytes
+    const int u = q >> 8, c = (q >> 3) & 31, piece = q & 7;
+    if (f0 + c < nc && 16 * piece < bytes)
+      *reinterpret_cast<uint4*>(out + u * plane + (f0 + c) * P + 16 * piece) =
+          *reinterpret_cast<const uint4*>(&tile[u][c][16 * (piece ^ (c & 7))]);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) oz_seg_coldigits_kernel(const T* __restrict__ B, int64_t ldb, int64_t strideB,
                                                                int64_t nc, int64_t nseg, int64_t nch,
                                                                const int4* __restrict__ cmap,
                                                                const uint32_t* __restrict__ ex, int64_t P,
                                                                uint8_t* __restrict__ planes) {
-  __shared__ __align__(16) uint8_t tile[OZ_S][64][32];
-  const int64_t c = blockIdx.x, b = blockIdx.z;
-  const int4 cm = cmap[b * nch + c];
-  if (cm.x < 0) return;
-  const int g = threadIdx.x >> 6, cc = threadIdx.x & 63;
-  const int64_t f0 = (int64_t)blockIdx.y * 64, f = f0 + cc;
+  __shared__ __align__(16) uint8_t tile[OZ_S][OZ_CD_COLS][OZ_CD_ROWS];
+  const int64_t b = blockIdx.z;
+  const int64_t ch0 = (int64_t)blockIdx.x * (OZ_CD_ROWS / 32);
+  if (cmap[b * nch + ch0].x < 0) return;  // the block starts past the used extent
+  const int g = threadIdx.x >> 5, c = threadIdx.x & 31;
+  const int64_t f0 = (int64_t)blockIdx.y * OZ_CD_COLS, f = f0 + c;
   const bool fv = f < nc;
+  const int4 cm = ch0 + g / 2 < nch ? cmap[b * nch + ch0 + g / 2] : make_int4(-1, 0, 0, 0);
+  const int r0 = 16 * (g & 1);  // first row of this thread inside its 32-row chunk
   double s1 = 0.0, s2 = 0.0;
-  if (fv) oz_scales(oz_exponent_from_bits(ex[(b * nseg + cm.x) * nc + f]), s1, s2);
+  if (fv && cm.x >= 0) oz_scales(oz_exponent_from_bits(ex[(b * nseg + cm.x) * nc + f]), s1, s2);
   const T* p = B + b * strideB + (int64_t)cm.y * ldb + f;
-  double x[8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) x[r] = (fv && 8 * g + r < cm.z) ? oz_ld(p + (int64_t)(8 * g + r) * ldb) : 0.0;
-  uint32_t w0[8], w1[8];
+  for (int hh = 0; hh < 2; ++hh) {
+    double x[8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) oz_digits(x[r], s1, s2, w0[r], w1[r]);
+    for (int r = 0; r < 8; ++r) {
+      const int rr = r0 + 8 * hh + r;
+      x[r] = (fv && cm.x >= 0 && rr < cm.z) ? oz_ld(p + (int64_t)rr * ldb) : 0.0;
+    }
+    uint32_t w0[8], w1[8];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const uint32_t a0[4] = {w0[0], w0[1], w0[2], w0[3]}, a1[4] = {w0[4], w0[5], w0[6], w0[7]};
-    const uint32_t b0[4] = {w1[0], w1[1], w1[2], w1[3]}, b1[4] = {w1[4], w1[5], w1[6], w1[7]};
-    *reinterpret_cast<uint2*>(&tile[u][cc][8 * g]) = make_uint2(oz_gather_byte(a0, u), oz_gather_byte(a1, u));
-    *reinterpret_cast<uint2*>(&tile[4 + u][cc][8 * g]) = make_uint2(oz_gather_byte(b0, u), oz_gather_byte(b1, u));
+    for (int r = 0; r < 8; ++r) oz_digits(x[r], s1, s2, w0[r], w1[r]);
+    oz_cd_stash8(tile, g, c, hh, w0, w1);
   }
   __syncthreads();
-  const int64_t plane = nc * P;
-  uint8_t* out = planes + (b * OZ_S) * plane + 32 * c;
-#pragma unroll
-  for (int z = 0; z < 4; ++z) {
-    const int q = threadIdx.x + 256 * z;  // 1024 pieces of 16 bytes
-    const int u = q >> 7, c2 = (q >> 1) & 63, half = q & 1;
-    if (f0 + c2 < nc)
-      *reinterpret_cast<uint4*>(out + u * plane + (f0 + c2) * P + 16 * half) =
-          *reinterpret_cast<const uint4*>(&tile[u][c2][16 * half]);
-  }
+  // chunks past the used extent have no planes to fill (the tensor maps never read them)
+  int used = 0;
+  for (int q = 0; q < OZ_CD_ROWS / 32; ++q)
+    if (ch0 + q < nch && cmap[b * nch + ch0 + q].x >= 0) used = q + 1;
+  oz_cd_store(tile, planes + (b * OZ_S) * (nc * P) + 32 * ch0, nc * P, P, f0, nc, 32 * used);
 }
 
 // ---------------------------------------------------------------- tcgen05 kernel
@@ -413,8 +444,10 @@ __device__ __forceinline__ OzItem oz_item(const OzGeom& g, int64_t it, const int
     r.k0 = po[r.b * g.nseg + r.j];
     r.ktiles = L[r.b * g.nseg + r.j] / OZ_BK;
   } else {
-    r.j = it % g.nseg;  // K split
-    const int64_t tile = (it / g.nseg) % tiles;
+    // every tile of one K split before the next split: the co-resident CTAs share
+    // that split's digit planes through L2
+    const int64_t tile = it % tiles;
+    r.j = (it / tiles) % g.nseg;  // K split
     r.b = it / (g.nseg * tiles);
     r.tn = tile % g.TN;
     r.tm = tile / g.TN;
@@ -728,23 +761,31 @@ __global__ void oz_gemm_prep_kernel(const int64_t* __restrict__ kdev, int64_t km
   for (int64_t i = threadIdx.x; i < nc; i += blockDim.x) exB[b * nc + i] = 0u;
 }
 
-// row maxima of A: warp per (row, 128-column chunk)
+// row maxima of A: warp per (row, OZ_RM_SPAN columns), all loads in flight
+constexpr int OZ_RM_SPAN = 512;
 template <typename T, bool G>
 __global__ void __launch_bounds__(256) oz_rowmax_kernel(OzRows<T, G> A, int64_t strideA, int64_t w_stride, int64_t m,
                                                         const int64_t* __restrict__ kinfo, uint32_t* __restrict__ exA) {
   const int lane = threadIdx.x & 31;
   const int64_t h = (int64_t)blockIdx.y * 8 + (threadIdx.x >> 5), b = blockIdx.z;
   const int64_t kd = kinfo[2 * b];
-  const int64_t i0 = (int64_t)blockIdx.x * 128 + 4 * lane;
-  if (h >= m || (int64_t)blockIdx.x * 128 >= kd) return;
+  const int64_t base = (int64_t)blockIdx.x * OZ_RM_SPAN;
+  if (h >= m || base >= kd) return;
   OzRows<T, G> a = A;
   a.base += b * strideA;
   if constexpr (G) { a.col += b * w_stride; a.sc += b * w_stride; }
   if (a.kx != nullptr) a.kx += b * w_stride;
+  double v[OZ_RM_SPAN / 32];
+#pragma unroll
+  for (int it = 0; it < OZ_RM_SPAN / 128; ++it)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = base + 128 * it + 4 * lane + q;
+      v[4 * it + q] = i < kd ? a.at(h, i) : 0.0;
+    }
   uint32_t eb = 0;
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (i0 + q < kd) eb = max(eb, oz_ebits(a.at(h, i0 + q)));
+  for (int q = 0; q < OZ_RM_SPAN / 32; ++q) eb = max(eb, oz_ebits(v[q]));
   eb = __reduce_max_sync(0xffffffffu, eb);
   if (lane == 0 && eb != 0) atomicMax(&exA[b * m + h], eb);
 }
@@ -775,7 +816,8 @@ __global__ void __launch_bounds__(256) oz_colmax_kernel(OzCols<T, G> B, int64_t 
   if (eb != 0) atomicMax(&exB[b * nc + f], eb);
 }
 
-// digit planes of A: warp per (row, 128-column chunk), zero past the inner length
+// digit planes of A: warp per (row, OZ_RD_SPAN columns), zero past the inner length
+constexpr int OZ_RD_SPAN = 256;
 template <typename T, bool G>
 __global__ void __launch_bounds__(256) oz_rowdigits_kernel(OzRows<T, G> A, int64_t strideA, int64_t w_stride, int64_t m,
                                                            const int64_t* __restrict__ kinfo,
@@ -785,42 +827,53 @@ __global__ void __launch_bounds__(256) oz_rowdigits_kernel(OzRows<T, G> A, int64
   const int64_t h = (int64_t)blockIdx.y * 8 + (threadIdx.x >> 5), b = blockIdx.z;
   const int64_t kd = kinfo[2 * b];
   const int64_t kpad = ((kd + OZ_BK - 1) / OZ_BK) * OZ_BK;
-  const int64_t i0 = (int64_t)blockIdx.x * 128 + 4 * lane;
-  if (h >= m || i0 >= kpad) return;
+  const int64_t base = (int64_t)blockIdx.x * OZ_RD_SPAN;
+  if (h >= m || base >= kpad) return;
   OzRows<T, G> a = A;
   a.base += b * strideA;
   if constexpr (G) { a.col += b * w_stride; a.sc += b * w_stride; }
   if (a.kx != nullptr) a.kx += b * w_stride;
   double s1, s2;
   oz_scales(oz_exponent_from_bits(exA[b * m + h]), s1, s2);
-  uint32_t w0[4], w1[4];
+  double x[OZ_RD_SPAN / 32];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const double x = i0 + q < kd ? a.at(h, i0 + q) : 0.0;
-    oz_digits(x, s1, s2, w0[q], w1[q]);
-  }
-  uint8_t* o = planes + ((b * OZ_S) * m + h) * P + i0;
+  for (int it = 0; it < OZ_RD_SPAN / 128; ++it)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = base + 128 * it + 4 * lane + q;
+      x[4 * it + q] = i < kd ? a.at(h, i) : 0.0;
+    }
   const int64_t plane = m * P;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    *reinterpret_cast<uint32_t*>(o + u * plane) = oz_gather_byte(w0, u);
-    *reinterpret_cast<uint32_t*>(o + (4 + u) * plane) = oz_gather_byte(w1, u);
+  for (int it = 0; it < OZ_RD_SPAN / 128; ++it) {
+    const int64_t i0 = base + 128 * it + 4 * lane;
+    if (i0 >= kpad) break;
+    uint32_t w0[4], w1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) oz_digits(x[4 * it + q], s1, s2, w0[q], w1[q]);
+    uint8_t* o = planes + ((b * OZ_S) * m + h) * P + i0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      *reinterpret_cast<uint32_t*>(o + u * plane) = oz_gather_byte(w0, u);
+      *reinterpret_cast<uint32_t*>(o + (4 + u) * plane) = oz_gather_byte(w1, u);
+    }
   }
 }
 
-// digit planes of B^T: CTA per (32-row chunk, 64 columns), transposed in shared memory
+// digit planes of B^T: CTA per (128 rows, 32 columns), transposed in shared memory
 template <typename T, bool G>
 __global__ void __launch_bounds__(256) oz_coldigits_kernel(OzCols<T, G> B, int64_t strideB, int64_t w_stride,
                                                            int64_t nc, const int64_t* __restrict__ kinfo,
                                                            const uint32_t* __restrict__ exB, int64_t P,
                                                            uint8_t* __restrict__ planes) {
-  __shared__ __align__(16) uint8_t tile[OZ_S][64][32];
+  __shared__ __align__(16) uint8_t tile[OZ_S][OZ_CD_COLS][OZ_CD_ROWS];
   const int64_t b = blockIdx.z;
   const int64_t kd = kinfo[2 * b];
-  const int64_t k0 = (int64_t)blockIdx.x * 32;
-  if (k0 >= ((kd + OZ_BK - 1) / OZ_BK) * OZ_BK) return;
-  const int g = threadIdx.x >> 6, c = threadIdx.x & 63;
-  const int64_t f0 = (int64_t)blockIdx.y * 64, f = f0 + c;
+  const int64_t kpad = ((kd + OZ_BK - 1) / OZ_BK) * OZ_BK;
+  const int64_t k0 = (int64_t)blockIdx.x * OZ_CD_ROWS;
+  if (k0 >= kpad) return;
+  const int g = threadIdx.x >> 5, c = threadIdx.x & 31;
+  const int64_t f0 = (int64_t)blockIdx.y * OZ_CD_COLS, f = f0 + c;
   const bool fv = f < nc;
   OzCols<T, G> a = B;
   a.base += b * strideB;
@@ -828,33 +881,22 @@ __global__ void __launch_bounds__(256) oz_coldigits_kernel(OzCols<T, G> B, int64
   if (a.kx != nullptr) a.kx += b * w_stride;
   double s1 = 0.0, s2 = 0.0;
   if (fv) oz_scales(oz_exponent_from_bits(exB[b * nc + f]), s1, s2);
-  uint32_t w0[8], w1[8];
-  double x[8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int64_t k = k0 + 8 * g + r;
-    x[r] = (fv && k < kd) ? a.at(k, f) : 0.0;
-  }
+  for (int hh = 0; hh < 2; ++hh) {
+    double x[8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) oz_digits(x[r], s1, s2, w0[r], w1[r]);
+    for (int r = 0; r < 8; ++r) {
+      const int64_t k = k0 + 16 * g + 8 * hh + r;
+      x[r] = (fv && k < kd) ? a.at(k, f) : 0.0;
+    }
+    uint32_t w0[8], w1[8];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const uint32_t a0[4] = {w0[0], w0[1], w0[2], w0[3]}, a1[4] = {w0[4], w0[5], w0[6], w0[7]};
-    const uint32_t b0[4] = {w1[0], w1[1], w1[2], w1[3]}, b1[4] = {w1[4], w1[5], w1[6], w1[7]};
-    *reinterpret_cast<uint2*>(&tile[u][c][8 * g]) = make_uint2(oz_gather_byte(a0, u), oz_gather_byte(a1, u));
-    *reinterpret_cast<uint2*>(&tile[4 + u][c][8 * g]) = make_uint2(oz_gather_byte(b0, u), oz_gather_byte(b1, u));
+    for (int r = 0; r < 8; ++r) oz_digits(x[r], s1, s2, w0[r], w1[r]);
+    oz_cd_stash8(tile, g, c, hh, w0, w1);
   }
   __syncthreads();
-  const int64_t plane = nc * P;
-  uint8_t* out = planes + (b * OZ_S) * plane + k0;
-#pragma unroll
-  for (int z = 0; z < 4; ++z) {
-    const int q = threadIdx.x + 256 * z;
-    const int u = q >> 7, cc = (q >> 1) & 63, half = q & 1;
-    if (f0 + cc < nc)
-      *reinterpret_cast<uint4*>(out + u * plane + (f0 + cc) * P + 16 * half) =
-          *reinterpret_cast<const uint4*>(&tile[u][cc][16 * half]);
-  }
+  oz_cd_store(tile, planes + (b * OZ_S) * (nc * P) + k0, nc * P, P, f0, nc,
+              (int)(kpad - k0 < OZ_CD_ROWS ? kpad - k0 : OZ_CD_ROWS));
 }
 
 // out[b] = sum over splits (fixed order) of part[b][split]
@@ -961,7 +1003,7 @@ static int segsq_i8_impl(int dtype, const void* A, int64_t lda, int64_t strideA,
   cudaMemsetAsync(exb, 0, (size_t)batch * nseg * nc * 4, st);
   dim3 ga((unsigned)ceil_div(m, 8), (unsigned)nseg, (unsigned)batch);
   dim3 gm((unsigned)nch, (unsigned)ceil_div(nc, 256), (unsigned)batch);
-  dim3 gd((unsigned)nch, (unsigned)ceil_div(nc, 64), (unsigned)batch);
+  dim3 gd((unsigned)ceil_div(nch, OZ_CD_ROWS / 32), (unsigned)ceil_div(nc, OZ_CD_COLS), (unsigned)batch);
   if (dtype == BMM_F64) {
     oz_split_rows_kernel<double><<<ga, 256, 0, st>>>((const double*)A, lda, strideA, m, seg, nseg, seg_stride, po, L,
                                                      l.P, pa, exa, flag);
@@ -1111,12 +1153,13 @@ static void oz_gemm_split_launch(const void* A, int64_t lda, int64_t strideA, co
   uint32_t* exb = (uint32_t*)(w + l.off_exb);
   OzRows<T, G> ra{(const T*)A, lda, col, scale, kexp};
   OzCols<T, G> cb{(const T*)B, ldb, col, scale, kexp};
-  dim3 gr((unsigned)ceil_div(l.P, 128), (unsigned)ceil_div(m, 8), (unsigned)batch);
+  dim3 grm((unsigned)ceil_div(l.P, OZ_RM_SPAN), (unsigned)ceil_div(m, 8), (unsigned)batch);
+  dim3 grd((unsigned)ceil_div(l.P, OZ_RD_SPAN), (unsigned)ceil_div(m, 8), (unsigned)batch);
   dim3 gc((unsigned)ceil_div(l.P, 32), (unsigned)ceil_div(nc, 256), (unsigned)batch);
-  dim3 gd((unsigned)ceil_div(l.P, 32), (unsigned)ceil_div(nc, 64), (unsigned)batch);
-  oz_rowmax_kernel<T, G><<<gr, 256, 0, st>>>(ra, strideA, w_stride, m, kinfo, exa);
+  dim3 gd((unsigned)ceil_div(l.P, OZ_CD_ROWS), (unsigned)ceil_div(nc, OZ_CD_COLS), (unsigned)batch);
+  oz_rowmax_kernel<T, G><<<grm, 256, 0, st>>>(ra, strideA, w_stride, m, kinfo, exa);
   oz_colmax_kernel<T, G><<<gc, 256, 0, st>>>(cb, strideB, w_stride, nc, kinfo, exb);
-  oz_rowdigits_kernel<T, G><<<gr, 256, 0, st>>>(ra, strideA, w_stride, m, kinfo, exa, l.P, w + l.off_a);
+  oz_rowdigits_kernel<T, G><<<grd, 256, 0, st>>>(ra, strideA, w_stride, m, kinfo, exa, l.P, w + l.off_a);
   oz_coldigits_kernel<T, G><<<gd, 256, 0, st>>>(cb, strideB, w_stride, nc, kinfo, exb, l.P, w + l.off_b);
   count_launch(3);
 }
