@@ -133,7 +133,10 @@ __device__ __forceinline__ double load_as_double(const float* p) { return (doubl
 __device__ __forceinline__ void store_val(double* p, double v) { *p = v; }
 __device__ __forceinline__ void store_val(float* p, double v) { *p = (float)v; }
 
-// C[h, t] = M[h, column[t]] * scale[t]
+// C[h, t] = M[h, column[t]] * scale[t]: thread per sketch column t (index and
+// scale loaded once), GC_ROWS rows per CTA, coalesced stores along t; columns
+// past the device count of a compressed sketch exit at once
+constexpr int GC_ROWS = 16;
 template <typename T, typename TO>
 __global__ void __launch_bounds__(256) gather_c_kernel(const T* __restrict__ M, int64_t ldm, int64_t strideM,
                                                        int64_t m, const int64_t* __restrict__ column,
@@ -141,37 +144,42 @@ __global__ void __launch_bounds__(256) gather_c_kernel(const T* __restrict__ M, 
                                                        int64_t w_stride, int64_t batch, TO* __restrict__ C,
                                                        int64_t ldc, int64_t strideC,
                                                        const int64_t* __restrict__ wdev) {
-  const int64_t per_b = m * W;
-  const int64_t total = per_b * batch;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = g / per_b, r = g - b * per_b;
-    const int64_t h = r / W, t = r - h * W;
-    if (wdev != nullptr && t >= wdev[b]) continue;  // compressed sketch: columns past the count are unused
+  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t h0 = (int64_t)blockIdx.y * GC_ROWS;
+  for (int64_t b = blockIdx.z; b < batch; b += gridDim.z) {
+    if (t >= W || (wdev != nullptr && t >= wdev[b])) continue;  // compressed sketch: unused columns
     const int64_t col = column[b * w_stride + t];
     const double s = scale[b * w_stride + t];
-    store_val(C + b * strideC + h * ldc + t, __dmul_rn(load_as_double(M + b * strideM + h * ldm + col), s));
+    const T* src = M + b * strideM + col;
+    TO* dst = C + b * strideC + t;
+    const int64_t h1 = min(m, h0 + GC_ROWS);
+#pragma unroll 8
+    for (int64_t h = h0; h < h1; ++h) store_val(dst + h * ldc, __dmul_rn(load_as_double(src + h * ldm), s));
   }
 }
 
-// D[t, f] = N[column[t], f] * scale[t]
+// D[t, f] = N[column[t], f] * scale[t]: CTA per GD_ROWS sketch rows, threads
+// along the contiguous row of N
+constexpr int GD_ROWS = 4;
 template <typename T, typename TO>
-__global__ void __launch_bounds__(256) gather_d_kernel(const T* __restrict__ N, int64_t ldn, int64_t strideN,
+__global__ void __launch_bounds__(128) gather_d_kernel(const T* __restrict__ N, int64_t ldn, int64_t strideN,
                                                        int64_t p, const int64_t* __restrict__ column,
                                                        const double* __restrict__ scale, int64_t W,
                                                        int64_t w_stride, int64_t batch, TO* __restrict__ D,
                                                        int64_t ldd, int64_t strideD,
                                                        const int64_t* __restrict__ wdev) {
-  const int64_t per_b = W * p;
-  const int64_t total = per_b * batch;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = g / per_b, r = g - b * per_b;
-    const int64_t t = r / p, f = r - t * p;
-    if (wdev != nullptr && t >= wdev[b]) continue;
-    const int64_t row = column[b * w_stride + t];
-    const double s = scale[b * w_stride + t];
-    store_val(D + b * strideD + t * ldd + f, __dmul_rn(load_as_double(N + b * strideN + row * ldn + f), s));
+  for (int64_t b = blockIdx.y; b < batch; b += gridDim.y) {
+    const int64_t wend = wdev != nullptr ? min(W, wdev[b]) : W;
+#pragma unroll
+    for (int r = 0; r < GD_ROWS; ++r) {
+      const int64_t t = (int64_t)blockIdx.x * GD_ROWS + r;
+      if (t >= wend) break;
+      const int64_t row = column[b * w_stride + t];
+      const double s = scale[b * w_stride + t];
+      const T* src = N + b * strideN + row * ldn;
+      TO* dst = D + b * strideD + t * ldd;
+      for (int64_t f = threadIdx.x; f < p; f += 128) store_val(dst + f, __dmul_rn(load_as_double(src + f), s));
+    }
   }
 }
 
@@ -210,13 +218,18 @@ int launch_gather(const T* M, int64_t ldm, int64_t strideM, const T* N, int64_t 
                   int64_t w_stride, int64_t batch, TO* C, int64_t ldc, int64_t strideC, TO* D,
                   int64_t ldd, int64_t strideD, cudaStream_t st, const int64_t* wdev = nullptr) {
   if (C != nullptr && m > 0) {
-    gather_c_kernel<T, TO><<<grid_for(m * W * batch, 256), 256, 0, st>>>(M, ldm, strideM, m, column, scale, W,
-                                                                     w_stride, batch, C, ldc, strideC, wdev);
+    BMM_REQUIRE(ceil_div(W, 256) < (1LL << 31) && ceil_div(m, GC_ROWS) <= 65535, BMM_E_UNSUPPORTED,
+                "gather: sketch too large");
+    dim3 g((unsigned)ceil_div(W, 256), (unsigned)ceil_div(m, GC_ROWS), (unsigned)std::min<int64_t>(batch, 65535));
+    gather_c_kernel<T, TO><<<g, 256, 0, st>>>(M, ldm, strideM, m, column, scale, W, w_stride, batch, C, ldc, strideC,
+                                              wdev);
     BMM_CHECK_LAUNCH("gather_c_kernel");
   }
   if (D != nullptr && p > 0) {
-    gather_d_kernel<T, TO><<<grid_for(W * p * batch, 256), 256, 0, st>>>(N, ldn, strideN, p, column, scale, W,
-                                                                     w_stride, batch, D, ldd, strideD, wdev);
+    BMM_REQUIRE(ceil_div(W, GD_ROWS) < (1LL << 31), BMM_E_UNSUPPORTED, "gather: sketch too large");
+    dim3 g((unsigned)ceil_div(W, GD_ROWS), (unsigned)std::min<int64_t>(batch, 65535));
+    gather_d_kernel<T, TO><<<g, 128, 0, st>>>(N, ldn, strideN, p, column, scale, W, w_stride, batch, D, ldd, strideD,
+                                              wdev);
     BMM_CHECK_LAUNCH("gather_d_kernel");
   }
   return BMM_OK;
