@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
   }
 }
 
+__device__ __forceinline__ int64_t ceil_div_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
 // ---- K4 gather
 
 __device__ __forceinline__ double load_as_double(const double* p) { return __ldg(p); }
@@ -391,47 +393,47 @@ __global__ void sketch_count_kernel(const int64_t* __restrict__ column, const do
 
 constexpr int kCompactThreads = 1024;
 
+// One CTA per problem; warp w owns a contiguous range of columns (a multiple of
+// 32), walked 32 columns at a time with coalesced loads: pass 1 counts the
+// drawn columns by ballot, a prefix over the warps gives each warp its output
+// base, pass 2 writes the distinct columns in column order.
 __global__ void __launch_bounds__(kCompactThreads) sketch_compact_kernel(
     const int32_t* __restrict__ cnt, const double* __restrict__ sval, int64_t n, int64_t W, int64_t w_stride,
     int64_t* __restrict__ out_col, double* __restrict__ out_scale, int64_t* __restrict__ out_count) {
-  __shared__ int64_t warp_tot[32];
+  __shared__ int64_t warp_base[kCompactThreads / 32 + 1];
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int64_t per = (n + kCompactThreads - 1) / kCompactThreads;
-  const int64_t lo = tid * per, hi = min(n, lo + per);
+  const int64_t per = ((ceil_div_dev(n, kCompactThreads / 32) + 31) / 32) * 32;
+  const int64_t lo = min(n, w * per), hi = min(n, lo + per);
   const int32_t* cb = cnt + b * n;
   int64_t mine = 0;
-  for (int64_t j = lo; j < hi; ++j) mine += (cb[j] > 0);
-  // block exclusive scan of `mine`
-  int64_t incl = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
+#pragma unroll 4
+  for (int64_t j0 = lo; j0 < hi; j0 += 32) {
+    const int64_t j = j0 + lane;
+    mine += __popc(__ballot_sync(0xffffffffu, j < hi && cb[j] > 0));
   }
-  if (lane == 31) warp_tot[w] = incl;
+  if (lane == 0) warp_base[w + 1] = mine;
   __syncthreads();
-  if (w == 0) {
-    int64_t v = lane < (kCompactThreads / 32) ? warp_tot[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += u;
-    }
-    warp_tot[lane] = v;  // inclusive over warps
+  if (tid == 0) {
+    warp_base[0] = 0;
+    for (int i = 1; i <= kCompactThreads / 32; ++i) warp_base[i] += warp_base[i - 1];
   }
   __syncthreads();
-  int64_t pos = incl - mine + (w ? warp_tot[w - 1] : 0);
-  const int64_t total = warp_tot[kCompactThreads / 32 - 1];
+  int64_t pos = warp_base[w];
+  const int64_t total = warp_base[kCompactThreads / 32];
   int64_t* oc = out_col + b * w_stride;
   double* os = out_scale + b * w_stride;
-  for (int64_t j = lo; j < hi; ++j) {
-    const int32_t c = cb[j];
+  const unsigned below = (1u << lane) - 1u;
+  for (int64_t j0 = lo; j0 < hi; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const int32_t c = j < hi ? cb[j] : 0;
+    const unsigned mk = __ballot_sync(0xffffffffu, c > 0);
     if (c > 0) {
-      oc[pos] = j;
-      os[pos] = __dmul_rn(sval[b * n + j], __dsqrt_rn((double)c));
-      ++pos;
+      const int64_t q = pos + __popc(mk & below);
+      oc[q] = j;
+      os[q] = __dmul_rn(sval[b * n + j], __dsqrt_rn((double)c));
     }
+    pos += __popc(mk);
   }
   // zero padding up to the next multiple of 32 (the float32 contraction's K step)
   const int64_t pad_end = min(W, ((total + 31) / 32) * 32);
