@@ -428,19 +428,22 @@ struct OzGeom {
 
 enum { EPI_SEG = 0, EPI_OUT = 1 };
 
-template <int EPI>
+// MC = 2: items are column-tile PAIRS (tn = 2 tnp + rank) computed by a CTA pair
+template <int EPI, int MC = 1>
 __device__ __forceinline__ OzItem oz_item(const OzGeom& g, int64_t it, const int32_t* __restrict__ perm,
-                                          const int64_t* __restrict__ po, const int32_t* __restrict__ L) {
+                                          const int64_t* __restrict__ po, const int32_t* __restrict__ L,
+                                          int rank = 0) {
   OzItem r;
-  const int64_t tiles = g.TM * g.TN;
+  const int64_t TNI = (g.TN + MC - 1) / MC;  // column tiles (or pairs) per row of tiles
+  const int64_t tiles = g.TM * TNI;
   if constexpr (EPI == EPI_SEG) {
     const int64_t tile = it % tiles;
     const int64_t rest = it / tiles;
-    const int64_t rank = rest % g.nseg;
+    const int64_t rank_ = rest % g.nseg;
     r.b = rest / g.nseg;
-    r.j = perm[r.b * g.nseg + rank];
-    r.tn = tile % g.TN;
-    r.tm = tile / g.TN;
+    r.j = perm[r.b * g.nseg + rank_];
+    r.tn = (tile % TNI) * MC + rank;
+    r.tm = tile / TNI;
     r.k0 = po[r.b * g.nseg + r.j];
     r.ktiles = L[r.b * g.nseg + r.j] / OZ_BK;
   } else {
@@ -449,8 +452,8 @@ __device__ __forceinline__ OzItem oz_item(const OzGeom& g, int64_t it, const int
     const int64_t tile = it % tiles;
     r.j = (it / tiles) % g.nseg;  // K split
     r.b = it / (g.nseg * tiles);
-    r.tn = tile % g.TN;
-    r.tm = tile / g.TN;
+    r.tn = (tile % TNI) * MC + rank;
+    r.tm = tile / TNI;
     const int64_t kd = g.kinfo[2 * r.b], chunk = g.kinfo[2 * r.b + 1];
     r.k0 = r.j * chunk;
     const int64_t k1 = min(kd, r.k0 + chunk);
@@ -464,9 +467,14 @@ __device__ __forceinline__ OzItem oz_item(const OzGeom& g, int64_t it, const int
 // EPI_OUT: the product tile itself (float64) into out, or into the split-K
 // partials part[b][split] when nseg > 1.  Exponents: EPI_SEG int e per
 // (segment, row/column); EPI_OUT biased exponent fields (oz_exponent_from_bits).
-template <int EPI>
+// MC = 2: a cluster of two CTAs computes two adjacent column tiles of the same
+// rows; each loads one 64-row half of every A digit plane and multicasts it to
+// both (A read from L2 once per pair: a third less operand traffic), and a
+// stage is refilled only after both CTAs' MMAs have read it.
+template <int EPI, int MC = 1>
 __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_constant__ CUtensorMap tm_a,
-                                                                 const __grid_constant__ CUtensorMap tm_b, OzGeom geo,
+                                                                 const __grid_constant__ CUtensorMap tm_b,
+                                                                 const __grid_constant__ CUtensorMap tm_a2, OzGeom geo,
                                                                  const int32_t* __restrict__ perm,
                                                                  const int64_t* __restrict__ po,
                                                                  const int32_t* __restrict__ L,
@@ -484,10 +492,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
   double* red = wcol + 128;                                                     // [OZ_EPI_WARPS]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t crank = 0;
+  if constexpr (MC > 1) asm("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+  const int64_t first = blockIdx.x / MC, step = gridDim.x / MC;
   if (threadIdx.x == 0) {
     for (int s = 0; s < OZ_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // every CTA of the pair commits its reads of the stage
     }
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, OZ_EPI_WARPS);
@@ -502,6 +513,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if constexpr (MC > 1) cluster_sync_all();  // the peer's barriers exist before any multicast lands
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -509,8 +521,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
     if (lane == 0) {
       // ---- TMA producer: the S digit planes of A and B for every stage
       uint32_t it = 0;
-      for (int64_t w = blockIdx.x; w < geo.items; w += gridDim.x) {
-        const OzItem I = oz_item<EPI>(geo, w, perm, po, L);
+      for (int64_t w = first; w < geo.items; w += step) {
+        const OzItem I = oz_item<EPI, MC>(geo, w, perm, po, L, (int)crank);
         const int arow = (int)(I.tm * OZ_BM), brow = (int)(I.tn * OZ_BN), plane0 = (int)(I.b * OZ_S);
         for (int kt = 0; kt < I.ktiles; ++kt, ++it) {
           const int s = it % OZ_STAGES;
@@ -523,7 +535,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
           mbar_expect_tx(&full[s], OZ_STAGE);
           const int kc = (int)(I.k0 + kt * OZ_BK);
           // rows past m / nc are zero-filled by the tensor map bounds
-          tma_load_3d(st, &tm_a, &full[s], kc, arow, plane0);
+          if constexpr (MC > 1) {
+            // this CTA's 64-row half of every A plane, to both CTAs (2-D map over the
+            // stacked planes: rows past m belong to the next plane, masked in the epilogue)
+#pragma unroll
+            for (int t = 0; t < OZ_S; ++t)
+              tma_load_2d_mc(st + t * OZ_A_PLANE + crank * (OZ_A_PLANE / 2), &tm_a2, &full[s], kc,
+                             (int)((I.b * OZ_S + t) * geo.m) + arow + (int)crank * 64, 0x3);
+          } else {
+            tma_load_3d(st, &tm_a, &full[s], kc, arow, plane0);
+          }
           tma_load_3d(st + OZ_S * OZ_A_PLANE, &tm_b, &full[s], kc, brow, plane0);
         }
       }
@@ -532,8 +553,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
     if (lane == 0) {
       // ---- MMA issuer: per stage, A plane t x B planes 0..S-1-t into levels t..S-1
       uint32_t it = 0, n_items = 0;
-      for (int64_t w = blockIdx.x; w < geo.items; w += gridDim.x) {
-        const OzItem I = oz_item<EPI>(geo, w, perm, po, L);
+      for (int64_t w = first; w < geo.items; w += step) {
+        const OzItem I = oz_item<EPI, MC>(geo, w, perm, po, L, (int)crank);
         if (I.ktiles == 0) continue;
         if (n_items > 0) mbar_wait(acc_empty, (n_items - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -561,7 +582,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
                       (kt > 0 || t > 0) ? 1u : 0u);
             }
           }
-          umma_commit(&empty[s]);
+          if constexpr (MC > 1) umma_commit_mc(&empty[s], 0x3);  // both CTAs may refill after both read
+          else umma_commit(&empty[s]);
         }
         umma_commit(acc_full);
         ++n_items;
@@ -574,8 +596,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
     const int cpart = (warp - 2) / 4;   // which OZ_EPI_COLS columns of the tile
     constexpr int EPI_T = 32 * OZ_EPI_WARPS;
     uint32_t n_items = 0;
-    for (int64_t w = blockIdx.x; w < geo.items; w += gridDim.x) {
-      const OzItem I = oz_item<EPI>(geo, w, perm, po, L);
+    for (int64_t w = first; w < geo.items; w += step) {
+      const OzItem I = oz_item<EPI, MC>(geo, w, perm, po, L, (int)crank);
       double* prow = part + ((I.b * geo.nseg + I.j) * geo.TM + I.tm) * geo.TN + I.tn;
       const int64_t row = I.tm * OZ_BM + quarter * 32 + lane;
       const int64_t col0 = I.tn * OZ_BN;
@@ -586,7 +608,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
       }
       if (I.ktiles == 0) {
         if constexpr (EPI == EPI_SEG) {
-          if (e_id == 0) *prow = 0.0;
+          if (e_id == 0 && I.tn < geo.TN) *prow = 0.0;
         } else if (row < geo.m) {
           for (int q = 0; q < OZ_BN; ++q)
             if (col0 + q < geo.nc) orow[col0 + q] = 0.0;
@@ -656,7 +678,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
         for (int o = 16; o > 0; o >>= 1) R += __shfl_xor_sync(0xffffffffu, R, o);
         if (lane == 0) red[warp - 2] = R;
         named_sync(1, EPI_T);
-        if (e_id == 0) {
+        if (e_id == 0 && I.tn < geo.TN) {  // (a pair's phantom tile past the last column has no slot)
           double t = 0.0;
 #pragma unroll
           for (int q = 0; q < OZ_EPI_WARPS; ++q) t += red[q];
@@ -671,6 +693,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_mma_kernel(const __grid_cons
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(OZ_TMEM_COLS));
   }
+  // the peer's last multicast loads and MMA commits target this CTA's shared memory
+  if constexpr (MC > 1) cluster_sync_all();
 }
 
 __global__ void oz_reduce_kernel(const double* __restrict__ part, int64_t tiles, int64_t nseg, int64_t total,
@@ -957,6 +981,88 @@ static int oz_map(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_t p
   return BMM_OK;
 }
 
+// 2-D view of the stacked digit planes ([planes * rows] x P) with 64-row boxes:
+// the halves a CTA pair multicasts
+static int oz_map2d(CUtensorMap* map, const uint8_t* base, int64_t rows, int64_t P) {
+  auto enc = get_encode();
+  BMM_REQUIRE(enc != nullptr, BMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)P};
+  cuuint32_t box[2] = {(cuuint32_t)OZ_BK, 64u};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BMM_REQUIRE(r == CUDA_SUCCESS, BMM_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return BMM_OK;
+}
+
+static int oz_nsm_count() {
+  static int nsm = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return nsm;
+}
+
+// Launch the persistent MMA kernel: CTA pairs sharing the A planes by multicast
+// when there are at least two column tiles (BMM_OZ_PAIR=0 disables), else
+// single CTAs.  geo.items is set here from the per-row item count `rows_items`
+// (items with one column tile each = rows_items * TN).
+template <int EPI>
+static int oz_launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const uint8_t* planes_a, int64_t a_rows,
+                         int64_t P, OzGeom geo, int64_t rows_items, const int32_t* perm, const int64_t* po,
+                         const int32_t* L, const int32_t* exa, const int32_t* exb, double* part, int mode,
+                         cudaStream_t st) {
+  static const int pair_env = [] {
+    const char* e = getenv("BMM_OZ_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  const bool pair = pair_env != 0 && geo.TN >= 2 && mode == 0;
+  static bool attr1 = false, attr2 = false;
+  const int nsm = oz_nsm_count();
+  if (!pair) {
+    if (!attr1) {
+      cudaFuncSetAttribute(oz_mma_kernel<EPI, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+      attr1 = true;
+    }
+    geo.items = rows_items * geo.TN;
+    const unsigned grid = (unsigned)(geo.items < nsm ? geo.items : nsm);
+    oz_mma_kernel<EPI, 1><<<grid, OZ_THREADS, OZ_SMEM, st>>>(ma, mb, ma, geo, perm, po, L, exa, exb, part, mode);
+    BMM_CHECK_LAUNCH("oz_mma_kernel");
+    return BMM_OK;
+  }
+  if (!attr2) {
+    cudaFuncSetAttribute(oz_mma_kernel<EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+    attr2 = true;
+  }
+  CUtensorMap ma2;
+  int rc;
+  if ((rc = oz_map2d(&ma2, planes_a, a_rows, P)) != BMM_OK) return rc;
+  geo.items = rows_items * ((geo.TN + 1) / 2);
+  const int64_t clusters = geo.items < nsm / 2 ? geo.items : nsm / 2;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(2 * clusters), 1, 1);
+  lc.blockDim = dim3(OZ_THREADS, 1, 1);
+  lc.dynamicSmemBytes = OZ_SMEM;
+  lc.stream = st;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = 2;
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = 1;
+  lc.attrs = la;
+  lc.numAttrs = 1;
+  if (cudaLaunchKernelEx(&lc, oz_mma_kernel<EPI, 2>, ma, mb, ma2, geo, perm, po, L, exa, exb, part, mode) !=
+      cudaSuccess) {
+    set_error("oz_mma_kernel: cluster launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return BMM_E_CUDA;
+  }
+  count_launch();
+  return BMM_OK;
+}
+
 }  // namespace bmm
 
 using namespace bmm;
@@ -1032,28 +1138,17 @@ static int segsq_i8_impl(int dtype, const void* A, int64_t lda, int64_t strideA,
   geo.nseg = nseg;
   geo.TM = ceil_div(m, OZ_BM);
   geo.TN = ceil_div(nc, OZ_BN);
-  geo.items = batch * nseg * geo.TM * geo.TN;
   geo.kinfo = nullptr;
   geo.out = nullptr;
   geo.ldo = geo.strideO = 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(oz_mma_kernel<EPI_SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
-    attr = true;
-  }
-  static int nsm = [] {
-    int dev = 0, n = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-  }();
-  const unsigned grid = (unsigned)(geo.items < nsm ? geo.items : nsm);
   static const int mode = [] {
     const char* e = getenv("BMM_OZ_MODE");  // timing experiments only (1: no epilogue, 2: no loads)
     return e ? atoi(e) : 0;
   }();
   if (ev) cudaEventRecord(ev[1], st);
-  oz_mma_kernel<EPI_SEG><<<grid, OZ_THREADS, OZ_SMEM, st>>>(ma, mb, geo, perm, po, L, exa, exb, part, mode);
-  BMM_CHECK_LAUNCH("oz_mma_kernel");
+  if ((rc = oz_launch_mma<EPI_SEG>(ma, mb, pa, batch * OZ_S * m, l.P, geo, batch * nseg * geo.TM, perm, po, L, exa,
+                                   exb, part, mode, st)) != BMM_OK)
+    return rc;
   if (ev) cudaEventRecord(ev[2], st);
   oz_reduce_kernel<<<grid_for(batch * nseg, 128), 128, 0, st>>>(part, geo.TM * geo.TN, nseg, batch * nseg, flag, gsq);
   BMM_CHECK_LAUNCH("oz_reduce_kernel");
@@ -1205,22 +1300,15 @@ static int gemm_i8_impl(int dtype, const void* A, int64_t lda, int64_t strideA, 
   geo.nseg = l.splits;
   geo.TM = ceil_div(m, OZ_BM);
   geo.TN = ceil_div(nc, OZ_BN);
-  geo.items = batch * l.splits * geo.TM * geo.TN;
   geo.kinfo = kinfo;
   geo.out = out;
   geo.ldo = ldo;
   geo.strideO = strideO;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(oz_mma_kernel<EPI_OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
-    attr = true;
-  }
-  const unsigned grid = (unsigned)(geo.items < oz_nsm() ? geo.items : oz_nsm());
   double* part = (double*)(w + l.off_part);
-  oz_mma_kernel<EPI_OUT><<<grid, OZ_THREADS, OZ_SMEM, st>>>(ma, mb, geo, nullptr, nullptr, nullptr,
-                                                            (const int32_t*)(w + l.off_exa),
-                                                            (const int32_t*)(w + l.off_exb), part, 0);
-  BMM_CHECK_LAUNCH("oz_mma_kernel");
+  if ((rc = oz_launch_mma<EPI_OUT>(ma, mb, w + l.off_a, batch * OZ_S * m, l.P, geo, batch * l.splits * geo.TM,
+                                   nullptr, nullptr, nullptr, (const int32_t*)(w + l.off_exa),
+                                   (const int32_t*)(w + l.off_exb), part, 0, st)) != BMM_OK)
+    return rc;
   if (l.splits > 1) {
     oz_splitk_reduce_kernel<<<grid_for(batch * m * nc, 256), 256, 0, st>>>(part, l.splits, m, nc, batch, out, ldo,
                                                                           strideO);
