@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from . import rng as _rng
-from .plan import gemm_engine, raise_status, segsq_engine
+from .plan import PILOT_GRAM_MAX, gemm_engine, raise_status, segsq_engine
 
 METHODS = ("OPL", "ONC", "UU", "ONU", "ONMCNR", "SSM")
 
@@ -376,11 +376,16 @@ class SketchPipeline:
             self._c("bmm_sample", P(p0), P(p0cum), P(p0last), P(self.offsets), K, B, n, self.max_len, P(self.p_bud),
                     P(self.p_coloff), self.W0, P(self.p_states), P(self.p_column), P(self.p_prob),
                     P(self.p_scale), st)
-            # pilot norms ||C0_k D0_k||_F^2 straight from M and N (sketch gathered on the fly)
-            A, Bm = self._f64(M, N)
-            self._c("bmm_segsq_f64_gather", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p, P(self.p_column),
-                    P(self.p_scale), self.W0, P(self.p_coloff), K, K + 1, B, P(self.pilot_sq), P(self.ws_seg),
-                    self.ws_seg.numel(), st)
+            # pilot norms ||C0_k D0_k||_F^2 straight from M and N (sketch gathered on the fly):
+            # few draws per block -> two L x L Gram matrices per block instead of an m x p product
+            if self.pc <= PILOT_GRAM_MAX:
+                self._c("bmm_segsq_gram_gather", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.p_column),
+                        P(self.p_scale), self.W0, P(self.p_coloff), K, K + 1, B, P(self.pilot_sq), st)
+            else:
+                A, Bm = self._f64(M, N)
+                self._c("bmm_segsq_f64_gather", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p,
+                        P(self.p_column), P(self.p_scale), self.W0, P(self.p_coloff), K, K + 1, B,
+                        P(self.pilot_sq), P(self.ws_seg), self.ws_seg.numel(), st)
             aux = self.pilot_sq
         self._c("bmm_budgets", rule, P(self.s) if rule != _lib.RULE_UU else None, P(aux) if aux is not None else None,
                 P(self.sizes_d), None, None, K, B, P(self.c_arr), int(self.cap), P(self.budgets), P(self.col_off),

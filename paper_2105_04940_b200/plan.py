@@ -212,6 +212,7 @@ def segsq_engine(max_len: int, m: int, p: int, n: int) -> str:
     return "i8" if 2.0 * m * p * n >= SEGSQ_I8_MIN_FLOPS else "dmma"
 
 
+PILOT_GRAM_MAX = 16  # two-step pilot norms by Gram matrices up to this many draws per block
 GEMM_I8_MIN_FLOPS = 1e10  # below this the DMMA GEMM's single pass beats the split + int8 contraction
 
 
@@ -443,14 +444,19 @@ def allocate_two_step(M, N, part: BlockPartition, c: int, c0: int, p0: BlockProb
     W0 = int(col_off[-1].item()) if K else 0
     if W0 > 0:
         # ||C0_k D0_k||_F^2 with the pilot sketch gathered on the fly (plan.py:463-464)
-        A = inst.M if inst.M.dtype == torch.float64 else inst.M.to(torch.float64)
-        B = inst.N if inst.N.dtype == torch.float64 else inst.N.to(torch.float64)
-        m, p = A.shape[0], B.shape[1]
-        pilot_sq = torch.empty(K, dtype=torch.float64, device=A.device)
-        ws = _lib.workspace(_lib.load().bmm_segsq_f64_workspace(m, p, K, 1))
-        _lib.call("bmm_segsq_f64_gather", _lib.ptr(A), A.stride(0), 0, _lib.ptr(B), B.stride(0), 0, m, p,
-                  _lib.ptr(col), _lib.ptr(scale), W0, _lib.ptr(col_off), K, 0, 1, _lib.ptr(pilot_sq),
-                  _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+        m, p = inst.M.shape[0], inst.N.shape[1]
+        pilot_sq = torch.empty(K, dtype=torch.float64, device=inst.M.device)
+        if int(pilot_budgets.max()) <= PILOT_GRAM_MAX:  # few draws per block: Gram matrices
+            _lib.call("bmm_segsq_gram_gather", _lib.matrix_dtype(inst.M), _lib.ptr(inst.M), inst.M.stride(0), 0,
+                      _lib.ptr(inst.N), inst.N.stride(0), 0, m, p, _lib.ptr(col), _lib.ptr(scale), W0,
+                      _lib.ptr(col_off), K, 0, 1, _lib.ptr(pilot_sq), _lib.stream_ptr())
+        else:
+            A = inst.M if inst.M.dtype == torch.float64 else inst.M.to(torch.float64)
+            B = inst.N if inst.N.dtype == torch.float64 else inst.N.to(torch.float64)
+            ws = _lib.workspace(_lib.load().bmm_segsq_f64_workspace(m, p, K, 1))
+            _lib.call("bmm_segsq_f64_gather", _lib.ptr(A), A.stride(0), 0, _lib.ptr(B), B.stride(0), 0, m, p,
+                      _lib.ptr(col), _lib.ptr(scale), W0, _lib.ptr(col_off), K, 0, 1, _lib.ptr(pilot_sq),
+                      _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
     else:
         pilot_sq = torch.zeros(K, dtype=torch.float64, device=s.device)
     budgets, note = device_budgets(_lib.RULE_TWO_STEP, K, int(c), s=s, aux=pilot_sq, sizes=inst.sizes,
