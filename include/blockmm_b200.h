@@ -343,12 +343,13 @@ int bmm_balance_exponents(const double* colsq, const double* rowsq, int64_t n_st
  * ||C_j D_j||_F^2 = sum_{a,a'} (C_j^T C_j)[a,a'] (D_j D_j^T)[a,a'], two streaming
  * passes over the gathered columns instead of an m x p product per segment.
  * plan.py:457-464.  Float64 (float32 inputs upcast), deterministic; parity to
- * rounding like the DMMA kernel.  No workspace.                              */
+ * rounding like the DMMA kernel.  max_len bounds every segment's length
+ * (<= 8: a single-tile variant).  No workspace.                             */
 int bmm_segsq_gram_gather(int dtype, const void* M, int64_t ldm, int64_t strideM,
                           const void* N, int64_t ldn, int64_t strideN,
                           int64_t m, int64_t nc, const int64_t* column, const double* scale,
                           int64_t w_stride, const int64_t* seg, int64_t nseg, int64_t seg_stride,
-                          int64_t batch, double* gsq, void* stream);
+                          int64_t max_len, int64_t batch, double* gsq, void* stream);
 
 /* ---------------------------------------------------------------- exact variance analytics
  * (analysis.py:57-116)

@@ -380,7 +380,7 @@ class SketchPipeline:
             # few draws per block -> two L x L Gram matrices per block instead of an m x p product
             if self.pc <= PILOT_GRAM_MAX:
                 self._c("bmm_segsq_gram_gather", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.p_column),
-                        P(self.p_scale), self.W0, P(self.p_coloff), K, K + 1, B, P(self.pilot_sq), st)
+                        P(self.p_scale), self.W0, P(self.p_coloff), K, K + 1, self.pc, B, P(self.pilot_sq), st)
             else:
                 A, Bm = self._f64(M, N)
                 self._c("bmm_segsq_f64_gather", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p,

@@ -449,7 +449,7 @@ def allocate_two_step(M, N, part: BlockPartition, c: int, c0: int, p0: BlockProb
         if int(pilot_budgets.max()) <= PILOT_GRAM_MAX:  # few draws per block: Gram matrices
             _lib.call("bmm_segsq_gram_gather", _lib.matrix_dtype(inst.M), _lib.ptr(inst.M), inst.M.stride(0), 0,
                       _lib.ptr(inst.N), inst.N.stride(0), 0, m, p, _lib.ptr(col), _lib.ptr(scale), W0,
-                      _lib.ptr(col_off), K, 0, 1, _lib.ptr(pilot_sq), _lib.stream_ptr())
+                      _lib.ptr(col_off), K, 0, int(pilot_budgets.max()), 1, _lib.ptr(pilot_sq), _lib.stream_ptr())
         else:
             A = inst.M if inst.M.dtype == torch.float64 else inst.M.to(torch.float64)
             B = inst.N if inst.N.dtype == torch.float64 else inst.N.to(torch.float64)

@@ -19,7 +19,7 @@ def _ref(M, N, col, sc, seg):
     return np.array(out)
 
 
-def _gram(M, N, col, sc, seg, dtype=np.float64, batch=1):
+def _gram(M, N, col, sc, seg, dtype=np.float64, batch=1, max_len=None):
     from paper_2105_04940_b200 import _lib
     Md = torch.as_tensor(np.ascontiguousarray(M.astype(dtype)), device="cuda")
     Nd = torch.as_tensor(np.ascontiguousarray(N.astype(dtype)), device="cuda")
@@ -31,7 +31,8 @@ def _gram(M, N, col, sc, seg, dtype=np.float64, batch=1):
     out = torch.empty(batch * K, dtype=torch.float64, device="cuda")
     _lib.call("bmm_segsq_gram_gather", _lib.matrix_dtype(Md), Md.data_ptr(), n, m * n if batch > 1 else 0,
               Nd.data_ptr(), p, n * p if batch > 1 else 0, m, p, cd.data_ptr(), sd.data_ptr(), W, gd.data_ptr(), K,
-              K + 1, batch, out.data_ptr(), _lib.stream_ptr())
+              K + 1, int(np.diff(seg, axis=-1).max()) if max_len is None else max_len, batch, out.data_ptr(),
+              _lib.stream_ptr())
     return out.cpu().numpy().reshape(batch, K) if batch > 1 else out.cpu().numpy()
 
 
