@@ -414,6 +414,18 @@ int bmm_gather_f32split_dk(int dtype, const void* M, int64_t ldm, int64_t stride
 int bmm_gemm_f32split_dk(const float* a_hi, const void* a_x, const float* b_hi, const void* b_x,
                          int64_t m, int64_t nc, int64_t k_max, const int64_t* k_dev, int64_t batch,
                          float* out, int64_t ldo, int64_t strideO, void* stream);
+/* The gather and the contraction in ONE kernel (float32 inputs): producer warps
+ * gather C = M[:, column] * scale and D = N[column, :] * scale[:, None] (the
+ * sketch, estimators.py:78-80 / 244-249), split them (tf32 hi + bf16 pairs, in
+ * float32 arithmetic) straight into the swizzled shared-memory stages of the
+ * tcgen05 contraction (estimators.py:175), so the split operands never reach
+ * HBM.  out[b] = C[b] @ D[b] over the first min(w_dev[b], W) sketch columns
+ * (w_dev NULL: all W).  128 x 128 output tiles; dtype BMM_F32 only.          */
+int bmm_gemm_f32split_gather(int dtype, const void* M, int64_t ldm, int64_t strideM,
+                             const void* N, int64_t ldn, int64_t strideN, int64_t m, int64_t p,
+                             const int64_t* column, const double* scale, int64_t W, int64_t w_stride,
+                             const int64_t* w_dev, int64_t batch, float* out, int64_t ldo,
+                             int64_t strideO, void* stream);
 
 /* sum of a float64 vector segment in numpy pairwise order: out[b] = 0 + pw(x[b, 0:len])
  * (used for ||M||_F^2 = pw(colsq), ||N||_F^2 = pw(rowsq)).                */

@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "tcgen05.cuh"
@@ -287,6 +288,13 @@ __device__ __forceinline__ void split_tf32(double x, float& hi, float& lo) {
 template <typename T>
 __device__ __forceinline__ double ld_d(const T* p) { return (double)__ldg(p); }
 
+// x = hi + lo, hi = x rounded to tf32 (nearest, ties away: cvt.rna.tf32), lo exact;
+// float32 arithmetic only (the float32 inputs' sketch values are scaled in float32)
+__device__ __forceinline__ void split_rna(float x, float& hi, float& lo) {
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+  lo = x - hi;
+}
+
 // a_hi / a_x for rows of C = M[:, column] * scale.  A CTA owns 256 sketch
 // columns of one problem and walks A_ROWS rows: the column index and scale
 // are loaded once per thread, and every row's stores are coalesced.
@@ -310,11 +318,15 @@ __global__ void __launch_bounds__(256) gather_a_split_kernel(const T* __restrict
   const int64_t h1 = min(m, h0 + A_ROWS);
   float* oh = ahi + (b * m) * W + t;
   __nv_bfloat16* ox = ax + (b * m) * 2 * W + pair_pos(t);
+  const float scf = (float)sc;
 #pragma unroll 8
   for (int64_t h = h0; h < h1; ++h) {
-    const double x = __dmul_rn(ld_d(src + h * ldm), sc);
     float hi, lo;
-    split_tf32(x, hi, lo);
+    if constexpr (sizeof(T) == 4) {
+      split_rna(__fmul_rn(__ldg(src + h * ldm), scf), hi, lo);  // float32 inputs: no float64 conversions
+    } else {
+      split_tf32(__dmul_rn(ld_d(src + h * ldm), sc), hi, lo);
+    }
     oh[h * W] = hi;
     ox[h * 2 * W] = __float2bfloat16_rn(hi);      // [h_x | l_x]
     ox[h * 2 * W + 8] = __float2bfloat16_rn(lo);
@@ -349,7 +361,8 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
   const int fq = (tid & 31) * 4, ty = tid >> 5;  // 32 x 8
   const bool vec = (sizeof(T) == 4) && (ldn % 4 == 0) && (strideN % 4 == 0) &&
                    ((reinterpret_cast<uintptr_t>(N) & 15) == 0) && (f0 + 128 <= p);
-  double v[4][4];
+  using VT = typename std::conditional<sizeof(T) == 4, float, double>::type;
+  VT v[4][4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int i = ty + 8 * r;
@@ -360,7 +373,7 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
       v[r][0] = q.x; v[r][1] = q.y; v[r][2] = q.z; v[r][3] = q.w;
     } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) v[r][e] = (t < W && f0 + fq + e < p) ? ld_d(src + e) : 0.0;
+      for (int e = 0; e < 4; ++e) v[r][e] = (t < W && f0 + fq + e < p) ? (VT)__ldg(src + e) : (VT)0;
     }
   }
 #pragma unroll
@@ -369,7 +382,10 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       float hi = 0.f, lo = 0.f;
-      if (t0 + i < W && f0 + fq + e < p) split_tf32(__dmul_rn(v[r][e], sscale[i]), hi, lo);
+      if (t0 + i < W && f0 + fq + e < p) {
+        if constexpr (sizeof(T) == 4) split_rna(__fmul_rn((float)v[r][e], (float)sscale[i]), hi, lo);
+        else split_tf32(__dmul_rn(v[r][e], sscale[i]), hi, lo);
+      }
       sh[i][fq + e] = hi;
       sl[i][fq + e] = lo;
     }
@@ -394,6 +410,298 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
             __halves2bfloat162(__float2bfloat16_rn(a), __float2bfloat16_rn(c));
       }
     }
+  }
+}
+
+// ---- fused split gather + contraction (float32 inputs, compressed sketches)
+//
+// The split operands of the two kernels above cost a write and a read of
+// 8 bytes per sketch element and problem (config 5: ~23 GB per step, more than
+// the gather's own reads of M).  Here the producer warps gather the sketch
+// straight into the swizzled shared-memory stages the MMA reads, so the split
+// operands never reach HBM:
+//   warp 0       tcgen05.mma issuer (as gemm_f32split_kernel<128>)
+//   warps 1-4    A = C tile: lane = sketch column t (the compressed columns are
+//                in ascending order, so a warp's 32 loads of one row of M share
+//                sectors), 32 rows per warp; hi and the [h|l] bf16 pair words
+//                are 4-byte shared stores, conflict-free under the swizzle
+//   warps 5-8    B = D^T tile: lane = output column f (each load of a row of N
+//                is one coalesced 128-byte line), 8 t per 16-byte chunk
+//   warps 9-12   drain: one warp per TMEM lane quarter (128 running sums each)
+// Scaling and the split run in float32 (x = M * float(s); hi = rna_tf32(x),
+// lo = x - hi exactly): no float64 conversions on the producer path.  Output
+// tiles are 128 x 128, so A is gathered once per column tile and B once per row
+// tile (the sibling CTAs of a problem are adjacent in launch order: their
+// second reads hit L2).
+constexpr int FG_PA = 4, FG_PB = 4, FG_DRAIN = 4;
+constexpr int FG_WARPS = 1 + FG_PA + FG_PB + FG_DRAIN;
+constexpr int FG_STAGES = 2;                // MMA operand ring
+constexpr int FG_STAGE = 4 * T_TILE_BYTES;  // A_hi, A_x, B_hi, B_x (128 rows x 128 B each)
+constexpr int FG_SDEPTH = 3;                // cp.async staging ring: 32 floats per producer thread
+constexpr int FG_STAGING = FG_SDEPTH * 32 * 256 * 4;
+constexpr int FG_SMEM = FG_STAGES * FG_STAGE + FG_STAGING + 1024 + 256;
+constexpr int FG_PRODUCERS = 32 * (FG_PA + FG_PB);
+
+// byte offset of (row r, byte c of its 128-byte K row) in a SWIZZLE_128B tile
+__device__ __forceinline__ uint32_t sw128(int r, int c) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((((c >> 4) ^ (r & 7)) << 4) | (c & 15)));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo_addr, float hi_addr) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo_addr, hi_addr);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// 4-byte cp.async (zero-filled when !ok; src must still be a valid address)
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
+
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32s(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts128s(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+
+__device__ __forceinline__ void sts32(uint8_t* p, uint32_t v) { *reinterpret_cast<uint32_t*>(p) = v; }
+__device__ __forceinline__ void sts128(uint8_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  *reinterpret_cast<uint4*>(p) = make_uint4(a, b, c, d);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(32 * FG_WARPS, 1) gemm_f32split_gather_kernel(
+    const float* __restrict__ M, int64_t ldm, int64_t strideM, const float* __restrict__ N, int64_t ldn,
+    int64_t strideN, int64_t m, int64_t nc, const int64_t* __restrict__ column, const double* __restrict__ scale,
+    int64_t W, int64_t w_stride, const int64_t* __restrict__ count, float* __restrict__ out, int64_t ldo,
+    int64_t strideO) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + FG_STAGES * FG_STAGE + FG_STAGING);
+  uint64_t* empty = full + FG_STAGES;
+  uint64_t* acc_full = empty + FG_STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = blockIdx.z;
+  const int tile_n = blockIdx.x, tile_m = blockIdx.y;
+  int64_t cnt = W;
+  if (count != nullptr) cnt = count[b] < W ? count[b] : W;
+  const int ktiles = (int)((cnt + T_BK - 1) / T_BK);
+  const int nchunks = (ktiles + T_CHUNK - 1) / T_CHUNK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < FG_STAGES; ++s) {
+      mbar_init(&full[s], FG_PRODUCERS);  // every producer thread arrives after its stores
+      mbar_init(&empty[s], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&acc_full[q], 1);
+      mbar_init(&acc_empty[q], FG_DRAIN);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(2 * 128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- MMA issuer (gemm_f32split_kernel<128>)
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % FG_STAGES;
+        const int chunk = kt / T_CHUNK, q = chunk & 1;
+        const bool first = (kt % T_CHUNK) == 0;
+        if (first && chunk >= 2) mbar_wait(&acc_empty[q], ((chunk >> 1) - 1) & 1);
+        mbar_wait(&full[s], (kt / FG_STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t base = su32(smem + s * FG_STAGE);
+        const uint32_t acc = tmem + (uint32_t)(q * 128);
+#pragma unroll
+        for (int kk = 0; kk < T_BK / 8; ++kk) {
+          const uint32_t off = kk * 32;
+          const uint64_t ahi = umma_desc_sw128(base + 0 * T_TILE_BYTES + off);
+          const uint64_t ax = umma_desc_sw128(base + 1 * T_TILE_BYTES + off);
+          const uint64_t bhi = umma_desc_sw128(base + 2 * T_TILE_BYTES + off);
+          const uint64_t bx = umma_desc_sw128(base + 3 * T_TILE_BYTES + off);
+          umma_bf16(acc, ax, bx, idesc_bf16<128>(), !(first && kk == 0));
+          umma_tf32(acc, ahi, bhi, idesc_tf32<128>(), 1);
+        }
+        umma_commit(&empty[s]);
+        if ((kt % T_CHUNK) == T_CHUNK - 1 || kt == ktiles - 1) umma_commit(&acc_full[q]);
+      }
+    }
+  } else if (warp <= FG_PA + FG_PB) {
+    // ---- producers.  The gathers go through cp.async into a per-thread staging
+    // ring (FG_SDEPTH stages of 32 values, [value][thread] so every access is
+    // conflict-free): two stages of loads are in flight while a thread splits
+    // and stores the third, without holding them in registers.  Sketch indices
+    // are fetched one stage before their loads are issued.
+    const int ptid = threadIdx.x - 32;  // 0..255
+    const bool is_a = warp <= FG_PA;
+    const int pw = is_a ? warp - 1 : warp - 1 - FG_PA;
+    const int64_t* colp = column + b * w_stride;
+    const double* scp = scale + b * w_stride;
+    const int r0 = pw * 32;  // A: first tile row of this warp
+    const int64_t f = (int64_t)tile_n * 128 + pw * 32 + lane;  // B: this lane's output column
+    const bool fvalid = f < nc;
+    const int64_t rleft = m - ((int64_t)tile_m * 128 + r0);
+    const int rows = rleft < 32 ? (int)rleft : 32;  // A rows of this warp inside M (may be <= 0)
+    const float* Mb = M + b * strideM + ((int64_t)tile_m * 128 + (rows > 0 ? r0 : 0)) * ldm;
+    const float* Nb = N + b * strideN + (fvalid ? f : 0);
+    const uint32_t stg = su32(smem + FG_STAGES * FG_STAGE) + 4u * ptid;  // + (buf*32 + j) * 1024
+    // A: lane t's column of M; B: lane t's row offset into N (shuffled to the f lanes); -1 = none
+    auto index = [&](int kt, int64_t& ci, float& si) {
+      const int64_t t = (int64_t)kt * T_BK + lane;
+      const bool tv = kt < ktiles && t < cnt;
+      const int64_t c = tv ? __ldg(colp + t) : (int64_t)-1;
+      ci = (is_a || c < 0) ? c : c * ldn;
+      si = tv ? (float)__ldg(scp + t) : 0.f;
+    };
+    auto issue = [&](int kt, int64_t ci) {
+      const uint32_t dst = stg + (uint32_t)((kt % FG_SDEPTH) * 32) * 1024u;
+      if (is_a) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const bool ok = ci >= 0 && j < rows;
+          cp_async4(dst + j * 1024u, ok ? (const void*)(Mb + ci + (int64_t)j * ldm) : (const void*)M, ok);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int64_t o = __shfl_sync(0xffffffffu, ci, j);
+          const bool ok = fvalid && o >= 0;
+          cp_async4(dst + j * 1024u, ok ? (const void*)(Nb + o) : (const void*)N, ok);
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    int64_t c0, c1, c2;
+    float s0, s1, s2;
+    index(0, c0, s0);
+    index(1, c1, s1);
+    issue(0, c0);
+    issue(1, c1);
+    index(2, c2, s2);
+    const int g = lane >> 3, e = lane & 7;
+    const int xb = (lane & 1) ? g * 32 + 16 + (e - 1) * 2 : g * 32 + e * 2;  // A: this lane's pair word
+    const int fr = pw * 32 + lane;                                           // B: this lane's tile row
+    const uint32_t svs = stg;  // staging: + (buf * 32 + j) * 1024
+    const uint32_t sbase = su32(smem);
+    uint32_t offh[8], offx[8], offb[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      offh[q] = (uint32_t)((((lane >> 2) ^ q) << 4) | ((lane & 3) << 2));          // A hi: byte 4t of row (q)
+      offx[q] = (uint32_t)((((xb >> 4) ^ q) << 4) | (xb & 15));                   // A pair word of row (q)
+      offb[q] = sw128(fr, 16 * q);                                                  // B row fr: chunk q
+    }
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int s = kt % FG_STAGES;
+      if (MODE != 2) issue(kt + 2, c2);  // staging buffer (kt+2) % 3 held stage kt-1: already consumed
+      int64_t c3;
+      float s3;
+      index(kt + 3, c3, s3);
+      if (MODE != 2) asm volatile("cp.async.wait_group 2;\n" ::: "memory");  // this thread's stage-kt values landed
+      else asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      const uint32_t v = svs + (uint32_t)((kt % FG_SDEPTH) * 32) * 1024u;  // this thread's staged values
+      if (kt >= FG_STAGES) mbar_wait(&empty[s], ((kt / FG_STAGES) - 1) & 1);
+      const uint32_t st = sbase + (uint32_t)(s * FG_STAGE);
+      if (is_a) {
+        // tile rows r0 + j: (r >> 3) * 1024 + (r & 7) * 128 are immediates, the swizzled
+        // 16-byte chunk depends on j & 7 only (precomputed per lane)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float hi, lo;
+          split_rna(lds_f32(v + j * 1024u) * s0, hi, lo);
+          const uint32_t row = st + (uint32_t)(r0 * 128 + (j >> 3) * 1024 + (j & 7) * 128);
+          sts32s(row + offh[j & 7], __float_as_uint(hi));
+          // pair words: even lanes (h_t, h_t+1), odd lanes (l_t-1, l_t)
+          const float recv = __shfl_xor_sync(0xffffffffu, (lane & 1) ? hi : lo, 1);
+          sts32s(row + T_TILE_BYTES + offx[j & 7], (lane & 1) ? pack_bf16(recv, lo) : pack_bf16(hi, recv));
+        }
+      } else {
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg) {
+          float h[8], l[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            split_rna(lds_f32(v + (8 * gg + j) * 1024u) * __shfl_sync(0xffffffffu, s0, 8 * gg + j), h[j], l[j]);
+          const uint32_t bh = st + 2 * T_TILE_BYTES, bx = st + 3 * T_TILE_BYTES;
+          sts128s(bh + offb[2 * gg], __float_as_uint(h[0]), __float_as_uint(h[1]), __float_as_uint(h[2]),
+                  __float_as_uint(h[3]));
+          sts128s(bh + offb[2 * gg + 1], __float_as_uint(h[4]), __float_as_uint(h[5]), __float_as_uint(h[6]),
+                  __float_as_uint(h[7]));
+          // B pairs: [l(8) | h(8)]
+          sts128s(bx + offb[2 * gg], pack_bf16(l[0], l[1]), pack_bf16(l[2], l[3]), pack_bf16(l[4], l[5]),
+                  pack_bf16(l[6], l[7]));
+          sts128s(bx + offb[2 * gg + 1], pack_bf16(h[0], h[1]), pack_bf16(h[2], h[3]), pack_bf16(h[4], h[5]),
+                  pack_bf16(h[6], h[7]));
+        }
+      }
+      // generic-proxy stores -> visible to the tensor core's async proxy, then arrive
+      if (MODE != 1) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive(&full[s]);
+      if (MODE == 2) issue(kt + 2, c2);
+      c2 = c3;
+      s0 = s1;
+      s1 = s2;
+      s2 = s3;
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  } else {
+    // ---- drain: warp w reads TMEM lanes 32*(w%4), all 128 columns
+    const int quarter = warp & 3;
+    float sum[128];
+#pragma unroll
+    for (int c = 0; c < 128; ++c) sum[c] = 0.f;
+    for (int chunk = 0; chunk < nchunks; ++chunk) {
+      const int q = chunk & 1;
+      mbar_wait(&acc_full[q], (chunk >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < 128; c += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(q * 128 + c), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sum[c + j] += __uint_as_float(v[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[q]);
+    }
+    const int64_t row = (int64_t)tile_m * 128 + quarter * 32 + lane;
+    if (row < m) {
+      float* orow = out + b * strideO + row * ldo;
+      const int64_t col0 = (int64_t)tile_n * 128;
+      const bool vec = (col0 + 128 <= nc) && ((reinterpret_cast<uintptr_t>(orow + col0) & 15) == 0);
+      if (vec) {
+        float4* o4 = reinterpret_cast<float4*>(orow + col0);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o4[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 128; ++j)
+          if (col0 + j < nc) orow[col0 + j] = sum[j];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * 128));
   }
 }
 
@@ -562,4 +870,33 @@ extern "C" int bmm_gemm_f32split_dk(const float* a_hi, const void* a_x, const fl
                                     float* out, int64_t ldo, int64_t strideO, void* stream) {
   BMM_REQUIRE(k_dev != nullptr, BMM_E_ARG, "bmm_gemm_f32split_dk: k_dev is NULL");
   return gemm_split_impl(a_hi, a_x, b_hi, b_x, m, nc, k_max, k_dev, batch, out, ldo, strideO, stream);
+}
+
+extern "C" int bmm_gemm_f32split_gather(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
+                                        int64_t ldn, int64_t strideN, int64_t m, int64_t p, const int64_t* column,
+                                        const double* scale, int64_t W, int64_t w_stride, const int64_t* w_dev,
+                                        int64_t batch, float* out, int64_t ldo, int64_t strideO, void* stream) {
+  BMM_REQUIRE(m >= 1 && p >= 1 && W >= 1 && batch >= 1, BMM_E_ARG, "bmm_gemm_f32split_gather: bad shape");
+  BMM_REQUIRE(dtype == BMM_F32, BMM_E_UNSUPPORTED, "bmm_gemm_f32split_gather: float32 inputs only");
+  BMM_REQUIRE(batch <= 65535 && ceil_div(m, 128) <= 65535, BMM_E_UNSUPPORTED,
+              "bmm_gemm_f32split_gather: grid too large");
+  static const int mode = [] {
+    const char* e = getenv("BMM_FG_MODE");  // timing experiments only
+    return e ? atoi(e) : 0;
+  }();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_f32split_gather_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FG_SMEM);
+    cudaFuncSetAttribute(gemm_f32split_gather_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FG_SMEM);
+    cudaFuncSetAttribute(gemm_f32split_gather_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, FG_SMEM);
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div(p, 128), (unsigned)ceil_div(m, 128), (unsigned)batch);
+  auto kern = mode == 1 ? gemm_f32split_gather_kernel<1> : mode == 2 ? gemm_f32split_gather_kernel<2>
+                                                                     : gemm_f32split_gather_kernel<0>;
+  kern<<<grid, 32 * FG_WARPS, FG_SMEM, as_stream(stream)>>>((const float*)M, ldm, strideM, (const float*)N, ldn,
+                                                            strideN, m, p, column, scale, W, w_stride, w_dev, out,
+                                                            ldo, strideO);
+  BMM_CHECK_LAUNCH("gemm_f32split_gather_kernel");
+  return BMM_OK;
 }

@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from . import rng as _rng
-from .plan import PILOT_GRAM_MAX, gemm_engine, raise_status, segsq_engine
+from .plan import PILOT_GRAM_MAX, f32_fused, gemm_engine, raise_status, segsq_engine
 
 METHODS = ("OPL", "ONC", "UU", "ONU", "ONMCNR", "SSM")
 
@@ -168,12 +168,16 @@ class SketchPipeline:
             self.k_scale = torch.empty(B * W, **f64)
             self.k_count = torch.empty(B, **i64)
             self.ws_cmp = torch.empty(max(256, self.lib.bmm_compress_workspace(n_, B)), dtype=torch.uint8, device=dev)
+        # small float32 outputs (at most 4 x 4 tiles of 128): gather inside the contraction
+        # (bmm_gemm_f32split_gather); large ones would re-gather A once per column tile
+        self.fused = self.tf32 and self.compress and f32_fused(self.m, self.p)
         if self.tf32:
             f32 = dict(dtype=torch.float32, device=dev)
-            self.a_hi = torch.empty(B * self.m * W, **f32)
-            self.a_x = torch.empty(B * self.m * W, **f32)
-            self.b_hi = torch.empty(B * self.p * W, **f32)
-            self.b_x = torch.empty(B * self.p * W, **f32)
+            if not self.fused:
+                self.a_hi = torch.empty(B * self.m * W, **f32)
+                self.a_x = torch.empty(B * self.m * W, **f32)
+                self.b_hi = torch.empty(B * self.p * W, **f32)
+                self.b_x = torch.empty(B * self.p * W, **f32)
             self.CD = torch.empty(B * self.m * self.p, **f32)
         else:
             # float64 path.  Large contractions: the int8 Ozaki path with the sketch
@@ -401,7 +405,11 @@ class SketchPipeline:
             # duplicates of a column share its scale: contract the distinct columns only
             self._c("bmm_compress_sketch", P(self.column), P(self.scale), W, W, n, B, P(self.ws_cmp),
                     self.ws_cmp.numel(), P(self.k_column), P(self.k_scale), P(self.k_count), st)
-        if self.tf32 and self.compress:
+        if self.fused:
+            # float32 inputs: the split gather runs inside the tcgen05 contraction's producer warps
+            self._c("bmm_gemm_f32split_gather", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
+                    P(self.k_scale), W, W, P(self.k_count), B, P(self.CD), p, m * p, st)
+        elif self.tf32 and self.compress:
             # float32 inputs: split gather + tcgen05 TF32 / BF16-cross-term contraction
             self._c("bmm_gather_f32split_dk", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
                     P(self.k_scale), W, W, P(self.k_count), B, P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x),

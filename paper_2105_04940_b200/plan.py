@@ -226,6 +226,20 @@ def gemm_engine(m: int, p: int, k: int) -> str:
     return "i8" if 2.0 * m * p * k >= GEMM_I8_MIN_FLOPS else "dmma"
 
 
+def f32_fused(m: int, p: int) -> bool:
+    """float32 compressed sketches: gather inside the tcgen05 contraction
+    (bmm_gemm_f32split_gather) when the output is one 128 x 128 tile.  Each CTA
+    re-gathers its A rows per column tile and its B rows per row tile, so wider
+    outputs keep the separate split gather (measured, tools/fused_probe.py,
+    4096 x 1024 sketches of 680 distinct columns: 128 x 128 outputs 1.34 ms
+    fused vs 1.76 ms for 2048 problems; 256 x 256 outputs 1.27 vs 0.96 ms for
+    512 problems); BMM_F32_FUSED=0|1 forces either."""
+    forced = os.environ.get("BMM_F32_FUSED", "")
+    if forced in ("0", "1"):
+        return forced == "1"
+    return m <= 128 and p <= 128
+
+
 def segsq(A: torch.Tensor, B: torch.Tensor, seg: torch.Tensor, nseg: int) -> torch.Tensor:
     if A.dtype != torch.float64:
         A = A.to(torch.float64)

@@ -90,3 +90,46 @@ def test_cta_pair_multicast_variant_matches():
         outs.append(np.load(f))
         f.unlink()
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("B,m,n,p,W", [(3, 256, 4096, 256, 1024), (2, 130, 777, 260, 512), (1, 200, 2000, 72, 1000),
+                                       (4, 128, 300, 128, 32), (1, 512, 3000, 512, 4096), (2, 64, 500, 200, 200)])
+def test_fused_gather_gemm(B, m, n, p, W):
+    """bmm_gemm_f32split_gather (the split gather inside the contraction's producer
+    warps) against the float64 product of the same sketch prefix (first count[b]
+    columns; one problem with count 0), and against the two-kernel path."""
+    g = torch.Generator(device="cuda").manual_seed(7 * B + m + n + p + W)
+    M = torch.randn((B, m, n), generator=g, device="cuda", dtype=torch.float32)
+    N = torch.randn((B, n, p), generator=g, device="cuda", dtype=torch.float32)
+    column = torch.sort(torch.randint(0, n, (B, W), generator=g, device="cuda", dtype=torch.int64), dim=1).values
+    scale = torch.rand((B, W), generator=g, device="cuda", dtype=torch.float64) * 3 + 0.1
+    count = torch.randint(W // 2, W + 1, (B,), generator=g, device="cuda", dtype=torch.int64)
+    count[0] = W
+    if B > 2:
+        count[1] = 0
+    out = torch.full((B, m, p), float("nan"), dtype=torch.float32, device="cuda")
+    _lib.call("bmm_gemm_f32split_gather", _lib.BMM_F32, M.data_ptr(), n, m * n, N.data_ptr(), p, n * p, m, p,
+              column.data_ptr(), scale.data_ptr(), W, W, count.data_ptr(), B, out.data_ptr(), p, m * p,
+              _lib.stream_ptr())
+    torch.cuda.synchronize()
+    C64 = torch.gather(M.double(), 2, column[:, None, :].expand(B, m, W)) * scale[:, None, :]
+    D64 = torch.gather(N.double(), 1, column[:, :, None].expand(B, W, p)) * scale[:, :, None]
+    keep = (torch.arange(W, device="cuda")[None, :] < count[:, None]).double()
+    ref = torch.bmm(C64 * keep[:, None, :], D64)
+    assert torch.isfinite(out).all()
+    for b in range(B):
+        if int(count[b]) == 0:
+            assert (out[b] == 0).all()
+            continue
+        err = ((out[b].double() - ref[b]).norm() / ref[b].norm()).item()
+        assert err < 1e-5, (b, err)
+    # without counts: all W columns, close to the two-kernel path on the same sketch
+    if W % 8 == 0:
+        _lib.call("bmm_gemm_f32split_gather", _lib.BMM_F32, M.data_ptr(), n, m * n, N.data_ptr(), p, n * p, m, p,
+                  column.data_ptr(), scale.data_ptr(), W, W, None, B, out.data_ptr(), p, m * p, _lib.stream_ptr())
+        two, _ = run_split_gemm(M, N, column, scale, W)
+        full = torch.bmm(C64, D64)
+        torch.cuda.synchronize()
+        e_fused = ((out.double() - full).norm() / full.norm()).item()
+        e_two = ((two.double() - full).norm() / full.norm()).item()
+        assert e_fused < 1e-5 and e_two < 1e-5, (e_fused, e_two)
