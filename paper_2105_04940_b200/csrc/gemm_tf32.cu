@@ -433,6 +433,15 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
 // tiles are 128 x 128, so A is gathered once per column tile and B once per row
 // tile (the sibling CTAs of a problem are adjacent in launch order: their
 // second reads hit L2).
+// Measured (tools/fused_probe.py, sketches of 680 sorted distinct columns of
+// 4096): single-tile outputs (128 x 128, 2048 problems) 1.34 ms vs 1.76 ms for
+// the two kernels; 256 x 256 outputs (512 problems) 1.27 vs 0.90 ms -- the
+// producers, one CTA per SM, process every element twice there.  A 2 x 2
+// cluster variant that gathered each element once and stored it into the
+// sibling CTAs through distributed shared memory was slower still (1.47 ms):
+// its cluster-scope proxy fences and release/acquire barriers compile to
+// MEMBAR.ALL.GPU / CCTL.IVALL per stage.  So plan.f32_fused picks this kernel
+// for single-tile outputs only.
 constexpr int FG_PA = 4, FG_PB = 4, FG_DRAIN = 4;
 constexpr int FG_WARPS = 1 + FG_PA + FG_PB + FG_DRAIN;
 constexpr int FG_STAGES = 2;                // MMA operand ring
@@ -474,7 +483,6 @@ __device__ __forceinline__ void sts128(uint8_t* p, uint32_t a, uint32_t b, uint3
   *reinterpret_cast<uint4*>(p) = make_uint4(a, b, c, d);
 }
 
-template <int MODE>
 __global__ void __launch_bounds__(32 * FG_WARPS, 1) gemm_f32split_gather_kernel(
     const float* __restrict__ M, int64_t ldm, int64_t strideM, const float* __restrict__ N, int64_t ldn,
     int64_t strideN, int64_t m, int64_t nc, const int64_t* __restrict__ column, const double* __restrict__ scale,
@@ -609,12 +617,11 @@ __global__ void __launch_bounds__(32 * FG_WARPS, 1) gemm_f32split_gather_kernel(
     }
     for (int kt = 0; kt < ktiles; ++kt) {
       const int s = kt % FG_STAGES;
-      if (MODE != 2) issue(kt + 2, c2);  // staging buffer (kt+2) % 3 held stage kt-1: already consumed
+      issue(kt + 2, c2);  // staging buffer (kt+2) % 3 held stage kt-1: already consumed
       int64_t c3;
       float s3;
       index(kt + 3, c3, s3);
-      if (MODE != 2) asm volatile("cp.async.wait_group 2;\n" ::: "memory");  // this thread's stage-kt values landed
-      else asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 2;\n" ::: "memory");  // this thread's stage-kt values landed
       const uint32_t v = svs + (uint32_t)((kt % FG_SDEPTH) * 32) * 1024u;  // this thread's staged values
       if (kt >= FG_STAGES) mbar_wait(&empty[s], ((kt / FG_STAGES) - 1) & 1);
       const uint32_t st = sbase + (uint32_t)(s * FG_STAGE);
@@ -651,9 +658,8 @@ __global__ void __launch_bounds__(32 * FG_WARPS, 1) gemm_f32split_gather_kernel(
         }
       }
       // generic-proxy stores -> visible to the tensor core's async proxy, then arrive
-      if (MODE != 1) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       mbar_arrive(&full[s]);
-      if (MODE == 2) issue(kt + 2, c2);
       c2 = c3;
       s0 = s1;
       s1 = s2;
@@ -880,23 +886,15 @@ extern "C" int bmm_gemm_f32split_gather(int dtype, const void* M, int64_t ldm, i
   BMM_REQUIRE(dtype == BMM_F32, BMM_E_UNSUPPORTED, "bmm_gemm_f32split_gather: float32 inputs only");
   BMM_REQUIRE(batch <= 65535 && ceil_div(m, 128) <= 65535, BMM_E_UNSUPPORTED,
               "bmm_gemm_f32split_gather: grid too large");
-  static const int mode = [] {
-    const char* e = getenv("BMM_FG_MODE");  // timing experiments only
-    return e ? atoi(e) : 0;
-  }();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_f32split_gather_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FG_SMEM);
-    cudaFuncSetAttribute(gemm_f32split_gather_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FG_SMEM);
-    cudaFuncSetAttribute(gemm_f32split_gather_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, FG_SMEM);
+    cudaFuncSetAttribute(gemm_f32split_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FG_SMEM);
     attr = true;
   }
   dim3 grid((unsigned)ceil_div(p, 128), (unsigned)ceil_div(m, 128), (unsigned)batch);
-  auto kern = mode == 1 ? gemm_f32split_gather_kernel<1> : mode == 2 ? gemm_f32split_gather_kernel<2>
-                                                                     : gemm_f32split_gather_kernel<0>;
-  kern<<<grid, 32 * FG_WARPS, FG_SMEM, as_stream(stream)>>>((const float*)M, ldm, strideM, (const float*)N, ldn,
-                                                            strideN, m, p, column, scale, W, w_stride, w_dev, out,
-                                                            ldo, strideO);
+  gemm_f32split_gather_kernel<<<grid, 32 * FG_WARPS, FG_SMEM, as_stream(stream)>>>(
+      (const float*)M, ldm, strideM, (const float*)N, ldn, strideN, m, p, column, scale, W, w_stride, w_dev, out, ldo,
+      strideO);
   BMM_CHECK_LAUNCH("gemm_f32split_gather_kernel");
   return BMM_OK;
 }
