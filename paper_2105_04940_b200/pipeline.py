@@ -18,6 +18,7 @@ ValueError/AssertionError cases) are read only by ``check()``.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -161,6 +162,7 @@ class SketchPipeline:
         self.scale = torch.empty(B * W, **f64)
         # float32 inputs take the tcgen05 split-operand path (pair groups need W % 8 == 0)
         self.tf32 = (dtype == torch.float32 and method != "SSM" and W % 8 == 0)
+        self._joint = None  # row stride of the pooled C when a joint PipelineGroup contracts
         # compressed sketch: one rank-1 term per distinct drawn column (bmm_compress_sketch)
         self.compress = bool(compress) and method != "SSM"
         if self.compress:
@@ -314,6 +316,8 @@ class SketchPipeline:
 
     def run(self, M: torch.Tensor, N: torch.Tensor, seeds: CallSeeds) -> torch.Tensor:
         """Approximate products of the batch; returns CD as (B, m, p) (or (m, p))."""
+        if self._joint is not None:
+            raise RuntimeError("this pipeline is contracted by its joint PipelineGroup: run the group")
         self.set_seeds(seeds)
         if getattr(self, "graph", None) is not None and self._graph_ptrs == (M.data_ptr(), N.data_ptr()):
             self.graph.replay()
@@ -441,6 +445,12 @@ class SketchPipeline:
             self._c("bmm_balance_exponents", P(self.colsq), P(self.rowsq), n, P(col), W, W, kd, B, P(self.kexp), st)
             self._c("bmm_gemm_i8_gather", dt, P(M), ldm, sM, P(N), ldn, sN, P(col), P(sc), P(self.kexp), W, m, p, W,
                     kd, B, P(self.CD), p, m * p, P(self.ws_gemm), self.ws_gemm.numel(), st)
+        elif self.compress and self._joint is not None:
+            # member of a joint PipelineGroup: gather into the group's pooled operands
+            # (row stride ldc); the group contracts every member in one batched GEMM
+            ldc = self._joint
+            self._c("bmm_gather_dk", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
+                    P(self.k_scale), W, W, P(self.k_count), B, P(self.C), ldc, m * ldc, P(self.D), p, ldc * p, st)
         elif self.compress:
             self._c("bmm_gather_dk", dt, _lib.BMM_F64, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
                     P(self.k_scale), W, W, P(self.k_count), B, P(self.C), W, m * W, P(self.D), p, W * p, st)
@@ -529,18 +539,64 @@ class PipelineGroup:
     GEMM. Results are those of the member pipelines run one after another
     (each branch owns its buffers and workspaces; no kernel keeps global state)."""
 
-    def __init__(self, pipes):
+    def __init__(self, pipes, joint=None):
         self.pipes = list(pipes)
         self.graph = None
         self.graph_launches = 0
+        # joint contraction: float64 compressed members on the DMMA engine with one output
+        # shape gather into pooled operands, and ONE batched GEMM contracts all of them
+        # (per-member inner lengths read on the device).  Nine 500 x ~3000 x 500 products
+        # then fill the GPU with their own tiles instead of split-K partials.
+        # BMM_JOINT=0 (or joint=False) keeps one GEMM per member.
+        if joint is None:
+            joint = os.environ.get("BMM_JOINT", "1") != "0"
+        p0 = self.pipes[0] if self.pipes else None
+        self.joint = bool(joint) and len(self.pipes) > 1 and all(
+            q.B == 1 and q.method != "SSM" and not q.tf32 and q.compress and q.gemm_engine == "dmma"
+            and (q.m, q.p) == (p0.m, p0.p) and q.C.device == p0.C.device for q in self.pipes)
+        self._jgroups = []
+        if self.joint:
+            # one batched GEMM per sketch width: its members finish planning at about the
+            # same time, and each width's GEMM can start while the other widths still plan
+            m, p, dev = p0.m, p0.p, p0.C.device
+            f64 = dict(dtype=torch.float64, device=dev)
+            by_w = {}
+            for i, q in enumerate(self.pipes):
+                by_w.setdefault(q.W, []).append(i)
+            for Wj, idx in by_w.items():
+                G = len(idx)
+                jg = dict(idx=idx, W=Wj, C=torch.zeros((G, m, Wj), **f64), D=torch.zeros((G, Wj, p), **f64),
+                          k=torch.zeros(G, dtype=torch.int64, device=dev), CD=torch.empty((G, m, p), **f64),
+                          ws=torch.empty(max(256, p0.lib.bmm_gemm_f64_workspace(m, p, Wj, G)), dtype=torch.uint8,
+                                         device=dev))
+                for j, i in enumerate(idx):
+                    q = self.pipes[i]
+                    q.C, q.D = jg["C"][j].view(-1), jg["D"][j].view(-1)
+                    q.k_count, q.CD = jg["k"][j:j + 1], jg["CD"][j].view(-1)
+                    q._joint = Wj
+                    del q.ws_gemm
+                self._jgroups.append(jg)
+
+    def _joint_gemm(self, jg=None) -> None:
+        m, p = self.pipes[0].m, self.pipes[0].p
+        for g in ([jg] if jg is not None else self._jgroups):
+            G, Wj = len(g["idx"]), g["W"]
+            _lib.call("bmm_gemm_f64_dk", g["C"].data_ptr(), Wj, m * Wj, g["D"].data_ptr(), p, Wj * p, m, p, Wj,
+                      g["k"].data_ptr(), G, g["CD"].data_ptr(), p, m * p, g["ws"].data_ptr(), g["ws"].numel(),
+                      _lib.stream_ptr())
+
+    def _launch_all(self, M: torch.Tensor, N: torch.Tensor) -> None:
+        for pipe in self.pipes:
+            pipe.launch(M, N)
+        if self.joint:
+            self._joint_gemm()
 
     def capture(self, M: torch.Tensor, N: torch.Tensor) -> None:
         cur = torch.cuda.current_stream()
         side = torch.cuda.Stream()
         side.wait_stream(cur)
         with torch.cuda.stream(side):  # warm-up: lazy buffers outside the capture
-            for pipe in self.pipes:
-                pipe.launch(M, N)
+            self._launch_all(M, N)
         cur.wait_stream(side)
         streams = [torch.cuda.Stream() for _ in self.pipes]
         g = torch.cuda.CUDAGraph()
@@ -551,6 +607,13 @@ class PipelineGroup:
                 s.wait_stream(cap)
                 with torch.cuda.stream(s):
                     pipe.launch(M, N)
+            for jg in self._jgroups:  # each width's GEMM after its own members
+                js = torch.cuda.Stream()
+                for i in jg["idx"]:
+                    js.wait_stream(streams[i])
+                with torch.cuda.stream(js):
+                    self._joint_gemm(jg)
+                streams.append(js)
             for s in streams:
                 cap.wait_stream(s)
         self.graph_launches = _lib.launches() - n0
@@ -563,6 +626,8 @@ class PipelineGroup:
         stream, every branch runs its norm pass (and OPL segmented square sums)
         on each chunk as it lands, then the rest of its pipeline, then copies its
         product back.  Replay with run_host()."""
+        if self.joint:
+            raise ValueError("capture_host: build the group with joint=False (each branch copies its own product)")
         pipes = self.pipes
         sizes = pipes[0].sizes
         n, m, p = pipes[0].n, pipes[0].m, pipes[0].p
@@ -621,7 +686,12 @@ class PipelineGroup:
     def run(self, M: torch.Tensor, N: torch.Tensor, seeds: list) -> list:
         """One call per member pipeline (same seeds contract as SketchPipeline.run)."""
         if self.graph is None or self._graph_ptrs != (M.data_ptr(), N.data_ptr()):
-            return [pipe.run(M, N, s) for pipe, s in zip(self.pipes, seeds)]
+            if not self.joint:
+                return [pipe.run(M, N, s) for pipe, s in zip(self.pipes, seeds)]
+            for pipe, s in zip(self.pipes, seeds):
+                pipe.set_seeds(s)
+            self._launch_all(M, N)
+            return [pipe._result() for pipe in self.pipes]
         for pipe, s in zip(self.pipes, seeds):
             pipe.set_seeds(s)
         self.graph.replay()

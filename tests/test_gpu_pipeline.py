@@ -45,7 +45,7 @@ def test_pipeline_group_concurrent_replay_is_bit_identical():
     Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
     runs = [(c, meth) for c in (200, 400) for meth in ("OPL", "ONC", "ONMCNR", "UU")]
     solo = [SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs]
-    group = PipelineGroup([SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs])
+    group = PipelineGroup([SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs], joint=False)
     seeds = lambda s: [seeds_from_rngs(meth, [np.random.default_rng(s + i)], len(sizes))  # noqa: E731
                        for i, (c, meth) in enumerate(runs)]
     group.run(Md, Nd, seeds(0))
@@ -58,6 +58,39 @@ def test_pipeline_group_concurrent_replay_is_bit_identical():
             ref = pipe.run(Md, Nd, seeds(s)[i])
             assert torch.equal(outs[i], ref), runs[i]
             assert np.array_equal(group.pipes[i].columns_host(), pipe.columns_host())
+
+
+@pytest.mark.parametrize("m,p", [(60, 50), (200, 130)])
+def test_pipeline_group_joint_gemm(m, p):
+    """Joint mode: the members gather into pooled operands and ONE batched GEMM
+    contracts them all.  Draws, budgets and scales are bit-identical to solo runs,
+    products agree to 1e-13 (only the split of the inner sum differs) and match the
+    oracle to 1e-12, eagerly and replayed; a member cannot be run on its own."""
+    M, N, sizes = workloads.cfg2(n=4000, m=m, p=p, K=12)
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    runs = [(c, meth) for c in (200, 400, 900) for meth in ("OPL", "ONC", "ONMCNR")]
+    solo = [SketchPipeline(m, 4000, p, sizes, c, meth, c0=120) for c, meth in runs]
+    group = PipelineGroup([SketchPipeline(m, 4000, p, sizes, c, meth, c0=120) for c, meth in runs])
+    assert group.joint
+    seeds = lambda s: [seeds_from_rngs(meth, [np.random.default_rng(s + i)], len(sizes))  # noqa: E731
+                       for i, (c, meth) in enumerate(runs)]
+    eager = [o.clone() for o in group.run(Md, Nd, seeds(3))]
+    group.capture(Md, Nd)
+    for s in (3, 11):
+        outs = [o.clone() for o in group.run(Md, Nd, seeds(s))]
+        group.check()
+        for i, pipe in enumerate(solo):
+            ref = pipe.run(Md, Nd, seeds(s)[i])
+            assert np.array_equal(group.pipes[i].columns_host(), pipe.columns_host()), runs[i]
+            assert np.array_equal(group.pipes[i].scales_host(), pipe.scales_host()), runs[i]
+            assert ((outs[i] - ref).norm() / ref.norm()).item() < 1e-13, runs[i]
+            if s == 3:
+                assert torch.equal(outs[i], eager[i])
+            c, meth = runs[i]
+            o = O.approx_product(M, N, sizes, c, meth, np.random.default_rng(s + i), c0=120)
+            assert rel(outs[i].cpu().numpy(), o["CD"]) < 1e-12, runs[i]
+    with pytest.raises(RuntimeError):
+        group.pipes[0].run(Md, Nd, seeds(3)[0])
 
 
 def test_pipeline_ssm_matches_oracle():
@@ -192,7 +225,8 @@ def test_streamed_end_to_end_graph_matches_resident_run():
     M, N, sizes = workloads.cfg2(n=4000, m=60, p=50, K=12)
     Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
     runs = [(c, meth) for c in (200, 400) for meth in ("OPL", "ONC", "ONMCNR")]
-    mk = lambda: PipelineGroup([SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs])  # noqa: E731
+    mk = lambda: PipelineGroup([SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs],  # noqa: E731
+                               joint=False)
     seeds = lambda s: [seeds_from_rngs(meth, [np.random.default_rng(s + i)], len(sizes))  # noqa: E731
                        for i, (c, meth) in enumerate(runs)]
     ref = mk()
