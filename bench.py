@@ -264,7 +264,7 @@ def run_ours(args):
     Mx, Nx = torch.empty_like(Md), torch.empty_like(Nd)
     outs_h = [torch.empty((m, p), dtype=torch.float64).pin_memory() for _ in runs]
     host_group = PipelineGroup([SketchPipeline(m, n, p, sizes, W, meth, c0=c0) for _, W, meth, c0 in runs],
-                               joint=False)  # each branch copies its own product back as soon as it is done
+                               joint=os.environ.get("BMM_E2E_JOINT", "0") == "1")  # per-branch GEMMs measured faster end to end
     host_group.capture_host(Mx, Nx, M_pin, N_pin, outs_h,
                             [seeds_from_rngs(meth, [workloads.sample_rng(cfg, cb)], K) for cb, W, meth, c0 in runs],
                             n_chunks=int(os.environ.get("BMM_E2E_CHUNKS", "8")))
@@ -283,7 +283,8 @@ def run_ours(args):
         # (bit-identical draws and sketches; the resident group's joint batched GEMM splits
         # the inner sum differently from the per-branch GEMMs of the streamed graph)
         o = o.cpu()
-        same = torch.equal(o, h) if not group.joint else bool(((o - h).norm() <= 1e-13 * o.norm()).item())
+        same = (torch.equal(o, h) if group.joint == host_group.joint
+                else bool(((o - h).norm() <= 1e-13 * o.norm()).item()))
         if not same:
             raise RuntimeError("streamed end-to-end products differ from the resident run")
     e2e_ms = float(np.mean(e2e))

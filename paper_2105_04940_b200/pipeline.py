@@ -626,8 +626,6 @@ class PipelineGroup:
         stream, every branch runs its norm pass (and OPL segmented square sums)
         on each chunk as it lands, then the rest of its pipeline, then copies its
         product back.  Replay with run_host()."""
-        if self.joint:
-            raise ValueError("capture_host: build the group with joint=False (each branch copies its own product)")
         pipes = self.pipes
         sizes = pipes[0].sizes
         n, m, p = pipes[0].n, pipes[0].m, pipes[0].p
@@ -671,7 +669,17 @@ class PipelineGroup:
                 s.wait_stream(cap)
                 with torch.cuda.stream(s):
                     out = pipe.launch(M, N, chunks=chunks)
-                    oh.copy_(out.reshape(oh.shape), non_blocking=True)
+                    if not self.joint:
+                        oh.copy_(out.reshape(oh.shape), non_blocking=True)
+            for jg in self._jgroups:  # joint mode: each width's GEMM, then its products go home
+                js = torch.cuda.Stream()
+                for i in jg["idx"]:
+                    js.wait_stream(streams[i])
+                with torch.cuda.stream(js):
+                    self._joint_gemm(jg)
+                    for j, i in enumerate(jg["idx"]):
+                        out_host[i].copy_(jg["CD"][j].reshape(out_host[i].shape), non_blocking=True)
+                streams.append(js)
             for s in streams + [copy]:
                 cap.wait_stream(s)
         self.host_graph_launches = _lib.launches() - n0

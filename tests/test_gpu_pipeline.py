@@ -218,7 +218,8 @@ def test_compressed_sketch_matches_draws_and_uncompressed_product():
     assert np.array_equal(oc.view(2, W)[1, :kd].cpu().numpy(), uniq)
 
 
-def test_streamed_end_to_end_graph_matches_resident_run():
+@pytest.mark.parametrize("joint", [False, True])
+def test_streamed_end_to_end_graph_matches_resident_run(joint):
     """PipelineGroup.capture_host: chunked host->device transfer with the norm
     pass and OPL's segmented square sums behind it, products copied back to
     pinned host buffers -- bit-identical to the device-resident replay."""
@@ -226,7 +227,7 @@ def test_streamed_end_to_end_graph_matches_resident_run():
     Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
     runs = [(c, meth) for c in (200, 400) for meth in ("OPL", "ONC", "ONMCNR")]
     mk = lambda: PipelineGroup([SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs],  # noqa: E731
-                               joint=False)
+                               joint=joint)
     seeds = lambda s: [seeds_from_rngs(meth, [np.random.default_rng(s + i)], len(sizes))  # noqa: E731
                        for i, (c, meth) in enumerate(runs)]
     ref = mk()
