@@ -427,6 +427,10 @@ int bmm_gemm_f32split_gather(int dtype, const void* M, int64_t ldm, int64_t stri
                              const int64_t* w_dev, int64_t batch, float* out, int64_t ldo,
                              int64_t strideO, void* stream);
 
+/* Diagnostics: the device clock (%globaltimer, ns) written to out[0] by a
+ * one-thread kernel on `stream` (graph-capturable; tools/timeline.py).        */
+int bmm_timestamp(unsigned long long* out, void* stream);
+
 /* sum of a float64 vector segment in numpy pairwise order: out[b] = 0 + pw(x[b, 0:len])
  * (used for ||M||_F^2 = pw(colsq), ||N||_F^2 = pw(rowsq)).                */
 int bmm_pairwise_sum(const double* x, int64_t len, int64_t stride, int64_t batch,

@@ -101,6 +101,7 @@ SIGNATURES = {
                                     _P, _P, _P, _P, _P]),
     "bmm_gemm_f32split_dk": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P]),
     "bmm_gemm_f32split": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _I64, _P]),
+    "bmm_timestamp": (_I, [_P, _P]),
     "bmm_gemm_f32split_gather": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _P, _I64,
                                       _P, _I64, _I64, _P]),
 }

@@ -44,3 +44,22 @@ extern "C" int bmm_copy2d(void* dst, int64_t dpitch, const void* src, int64_t sp
   }
   return BMM_OK;
 }
+
+// Device clock stamp (%globaltimer, ns) into out[0]: a one-thread kernel that
+// tools/timeline.py records after every stage of a captured pipeline group, to see
+// when each branch's kernels finish inside one graph replay.
+__global__ void stamp_kernel(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  out[0] = t;
+}
+
+extern "C" int bmm_timestamp(unsigned long long* out, void* stream) {
+  stamp_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(out);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    bmm::set_error("bmm_timestamp: %s", cudaGetErrorString(e));
+    return BMM_E_CUDA;
+  }
+  return BMM_OK;
+}

@@ -230,6 +230,7 @@ class SketchPipeline:
             self._uprobs = torch.as_tensor(np.tile(u, B), device=dev)
         self.graph = None
         self.timeline = None
+        self.stamps = None  # (device int64 buffer, [entry names]) for tools/timeline.py
 
     # ------------------------------------------------------------------ steps
     def _c(self, name, *args):
@@ -240,6 +241,10 @@ class SketchPipeline:
             ev = torch.cuda.Event(enable_timing=True)
             ev.record()
             self.timeline.append((name, ev))
+        if self.stamps is not None:  # graph profiling: a device clock stamp after every stage
+            buf, names = self.stamps
+            self.lib.bmm_timestamp(buf.data_ptr() + 8 * len(names), _lib.stream_ptr())
+            names.append(name)
 
     def stage_times(self, M, N, seeds) -> list:
         """Eager run with a CUDA event after every C-ABI call; returns
@@ -585,6 +590,15 @@ class PipelineGroup:
                       g["k"].data_ptr(), G, g["CD"].data_ptr(), p, m * p, g["ws"].data_ptr(), g["ws"].numel(),
                       _lib.stream_ptr())
 
+    def _branch_streams(self) -> list:
+        """One stream per member.  OPL members (the longest chains: their g_k
+        contraction occupies every SM) get the high priority, so their kernels take
+        SMs first and the other branches fill the gaps (BMM_BRANCH_PRIORITY=0: all
+        equal)."""
+        if os.environ.get("BMM_BRANCH_PRIORITY", "1") == "0":
+            return [torch.cuda.Stream() for _ in self.pipes]
+        return [torch.cuda.Stream(priority=-1 if q.method == "OPL" else 0) for q in self.pipes]
+
     def _launch_all(self, M: torch.Tensor, N: torch.Tensor) -> None:
         for pipe in self.pipes:
             pipe.launch(M, N)
@@ -598,7 +612,7 @@ class PipelineGroup:
         with torch.cuda.stream(side):  # warm-up: lazy buffers outside the capture
             self._launch_all(M, N)
         cur.wait_stream(side)
-        streams = [torch.cuda.Stream() for _ in self.pipes]
+        streams = self._branch_streams()
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launches()
         with torch.cuda.graph(g):
