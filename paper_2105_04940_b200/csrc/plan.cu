@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kProbCtaThreads) block_probs_cta_kernel(
     const double* __restrict__ colsq, const double* __restrict__ rowsq, int64_t n,
     const int64_t* __restrict__ offsets, int64_t K, double* __restrict__ probs, double* __restrict__ s,
     double* __restrict__ cum, int64_t* __restrict__ last) {
-  __shared__ WarpPwScratch scr;
+  __shared__ WarpPwScratch scr, scr1;
   __shared__ double sh_tot[2];
   extern __shared__ double wb[];
   const int64_t g = blockIdx.x;
@@ -121,13 +121,13 @@ __global__ void __launch_bounds__(kProbCtaThreads) block_probs_cta_kernel(
   for (int64_t i = tid; i < nk; i += kProbCtaThreads) wb[i] = sc(o + i);
   __syncthreads();
   const SrcF64 sp{wb};
+  // the block total and the score sum's reduceat tail are independent trees: two warps
   if (warp == 0) {
     const double tot = __dadd_rn(0.0, warp_pw_sum(sp, 0, nk, &scr));
-    if (s != nullptr) {
-      const double rest = warp_pw_sum(sp, 1, nk - 1, &scr);
-      if (lane == 0) s[g] = __dadd_rn(wb[0], rest);
-    }
     if (lane == 0) sh_tot[0] = tot;
+  } else if (warp == 1 && s != nullptr) {
+    const double rest = warp_pw_sum(sp, 1, nk - 1, &scr1);
+    if (lane == 0) s[g] = __dadd_rn(wb[0], rest);
   }
   __syncthreads();
   const double tot = sh_tot[0];
