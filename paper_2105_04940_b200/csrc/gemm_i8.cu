@@ -992,6 +992,9 @@ static int oz_nsm_count() {
   static int nsm = [] {
     int dev = 0, n = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    // BMM_OZ_CTAS: persistent CTAs of the g_k contraction (fewer leave SMs to concurrent graph branches)
+    const char* e = getenv("BMM_OZ_CTAS");
+    if (e != nullptr && atoi(e) >= 2 && atoi(e) < n) n = atoi(e) & ~1;
     return n;
   }();
   return nsm;
