@@ -390,8 +390,13 @@ def run_ours(args):
                      "cublas_same_shapes_tflops": sum(gemm_flops) / (sum(kt["cublas_same_shape_ms"]) * 1e-3) / 1e12,
                      "flops_note": "executed 2*m*p*K over the distinct drawn columns (gemm_k); the sketch "
                                    "width W counts duplicates, which the compressed sketch folds into scales",
-                     "traffic": 35511000 if (m, p) == (500, 500) else None,
-                     "traffic_note": "ncu --set full, W=16000 ONC launch (profiles/r1e_ncu_full_summary.csv): "
+                     "traffic": (285300000 if group.joint else 35511000) if (m, p) == (500, 500) else None,
+                     "traffic_note": ("ncu --set full of the three per-width joint launches and their split-K "
+                                      "reductions (profiles/r1n_ncu_joint_gemm.csv, tools/joint_gemm_probe.py): "
+                                      "231 MB in the GEMMs = the nine gathered C and D read once (+ partials), "
+                                      "54 MB in the reductions; DMMA pipe 77-82% active")
+                                     if group.joint else
+                                     "ncu --set full, W=16000 ONC launch (profiles/r1e_ncu_full_summary.csv): "
                                      "35.5 MB = the gathered C and D read once"},
         "roofline_segsq": roofline_segsq,
         "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norms_achieved,
