@@ -226,6 +226,15 @@ int bmm_gather_blocks(int dtype,
                       int64_t draws, int64_t W,
                       void* C, int64_t ldc, void* D, int64_t ldd, void* stream);
 
+/* SSM draws as sketch columns for the batched pipeline (equal blocks of
+ * block_len): column[b*w_stride + t*block_len + j] = offsets[blocks[b*d_stride
+ * + t]] + j, col_scale = scale[b*d_stride + t] -- the hstack of scaled whole
+ * blocks of estimators.py:244-249, fed to bmm_compress_sketch and the regular
+ * gather / contraction kernels.                                             */
+int bmm_expand_blocks(const int64_t* blocks, const double* scale, int64_t draws, int64_t d_stride,
+                      const int64_t* offsets, int64_t block_len, int64_t batch,
+                      int64_t* column, double* col_scale, int64_t w_stride, void* stream);
+
 /* ---------------------------------------------------------------- K5/K8 GEMM fp64
  * out[b] = A[b] (m x k, lda) @ B[b] (k x nc, ldb), float64 on the DMMA
  * tensor pipe (mma.sync m8n8k4 f64), split-K with a fixed-order reduction
@@ -350,6 +359,21 @@ int bmm_segsq_gram_gather(int dtype, const void* M, int64_t ldm, int64_t strideM
                           int64_t m, int64_t nc, const int64_t* column, const double* scale,
                           int64_t w_stride, const int64_t* seg, int64_t nseg, int64_t seg_stride,
                           int64_t max_len, int64_t batch, double* gsq, void* stream);
+
+/* OPL block-product norms through the Gram identity (K7):
+ * gsq[b, j] = || A[:, seg_j] B[seg_j, :] ||_F^2 = < A_j^T A_j , B_j B_j^T >_F,
+ * two L x L Gram matrices per segment on the DMMA pipe (36 of the 64 8x8 tiles:
+ * symmetry), contraction over the m rows of A and the nc columns of B.
+ * Replaces the K dgemm + ddot loop of block_scores (plan.py:176-189) when
+ * L < m nc / (m + nc): 2 (m + nc) n L flops instead of 2 m nc n, A and B read
+ * once.  Segments up to bmm_segsq_gram_max_len() (64) columns; longer -> NaN.
+ * dtype BMM_F64 or BMM_F32 (widened exactly).  No workspace, deterministic
+ * (fixed-order warp and lane reductions), result clamped at 0.             */
+int64_t bmm_segsq_gram_max_len(void);
+int bmm_segsq_gram(int dtype, const void* A, int64_t lda, int64_t strideA,
+                   const void* B, int64_t ldb, int64_t strideB,
+                   int64_t m, int64_t nc, const int64_t* seg, int64_t nseg, int64_t seg_stride,
+                   int64_t batch, double* gsq, void* stream);
 
 /* ---------------------------------------------------------------- exact variance analytics
  * (analysis.py:57-116)

@@ -466,3 +466,33 @@ extern "C" int bmm_compress_sketch(const int64_t* column, const double* scale, i
   BMM_CHECK_LAUNCH("sketch_compact_kernel");
   return BMM_OK;
 }
+
+// ---- SSM whole-block draws as sketch columns (estimators.py:244-249): draw t
+// of problem b copies block blocks[b, t] (equal blocks of block_len columns)
+// scaled by scale[b, t]; column[b, t * block_len + j] = offsets[blocks] + j.
+// The compress / gather / contraction stages then run unchanged, so the SSM
+// baseline shares the float32 tcgen05 and float64 DMMA contractions.
+__global__ void expand_blocks_kernel(const int64_t* __restrict__ blocks, const double* __restrict__ scale,
+                                     int64_t draws, int64_t d_stride, const int64_t* __restrict__ offsets,
+                                     int64_t block_len, int64_t batch, int64_t* __restrict__ column,
+                                     double* __restrict__ col_scale, int64_t w_stride) {
+  const int64_t per = draws * block_len, total = per * batch;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / per, r = i - b * per, t = r / block_len, j = r - t * block_len;
+    const int64_t k = blocks[b * d_stride + t];
+    column[b * w_stride + r] = offsets[k] + j;
+    col_scale[b * w_stride + r] = scale[b * d_stride + t];
+  }
+}
+
+extern "C" int bmm_expand_blocks(const int64_t* blocks, const double* scale, int64_t draws, int64_t d_stride,
+                                 const int64_t* offsets, int64_t block_len, int64_t batch, int64_t* column,
+                                 double* col_scale, int64_t w_stride, void* stream) {
+  BMM_REQUIRE(draws >= 1 && block_len >= 1 && batch >= 1 && d_stride >= draws && w_stride >= draws * block_len,
+              BMM_E_ARG, "bmm_expand_blocks: bad shape");
+  BMM_REQUIRE(blocks && scale && offsets && column && col_scale, BMM_E_ARG, "bmm_expand_blocks: null pointer");
+  expand_blocks_kernel<<<grid_for(draws * block_len * batch, 256), 256, 0, as_stream(stream)>>>(
+      blocks, scale, draws, d_stride, offsets, block_len, batch, column, col_scale, w_stride);
+  BMM_CHECK_LAUNCH("expand_blocks_kernel");
+  return BMM_OK;
+}

@@ -161,10 +161,10 @@ class SketchPipeline:
         self.prob = torch.empty(B * W, **f64)
         self.scale = torch.empty(B * W, **f64)
         # float32 inputs take the tcgen05 split-operand path (pair groups need W % 8 == 0)
-        self.tf32 = (dtype == torch.float32 and method != "SSM" and W % 8 == 0)
+        self.tf32 = (dtype == torch.float32 and W % 8 == 0)
         self._joint = None  # row stride of the pooled C when a joint PipelineGroup contracts
         # compressed sketch: one rank-1 term per distinct drawn column (bmm_compress_sketch)
-        self.compress = bool(compress) and method != "SSM"
+        self.compress = bool(compress)
         if self.compress:
             self.k_column = torch.empty(B * W, **i64)
             self.k_scale = torch.empty(B * W, **f64)
@@ -186,7 +186,7 @@ class SketchPipeline:
             # gathered inside its digit split (bmm_gemm_i8_gather).  Otherwise gather the
             # rescaled sketch (bandwidth-bound kernel at full occupancy), then C @ D on
             # the DMMA pipe.
-            self.gemm_engine = "dmma" if method == "SSM" else gemm_engine(self.m, self.p, W)
+            self.gemm_engine = gemm_engine(self.m, self.p, W)
             self.CD = torch.empty(B * self.m * self.p, **f64)
             if self.gemm_engine == "i8":
                 self.ws_gemm = torch.empty(max(256, self.lib.bmm_gemm_i8_workspace(self.m, self.p, W, B)),
@@ -202,7 +202,7 @@ class SketchPipeline:
             # g_k^2 on the int8 tensor cores (Ozaki split; float32 inputs read directly)
             self.seg_engine = segsq_engine(self.max_len, self.m, self.p, self.n)
             wsb = (self.lib.bmm_segsq_i8_workspace(self.m, self.p, self.n, K, B) if self.seg_engine == "i8"
-                   else self.lib.bmm_segsq_f64_workspace(self.m, self.p, K, B))
+                   else 0 if self.seg_engine == "gram" else self.lib.bmm_segsq_f64_workspace(self.m, self.p, K, B))
             self.ws_seg = torch.empty(max(256, wsb), dtype=torch.uint8, device=dev)
         if method in ("ONU", "ONMCNR"):
             self.pc = self.c0 // K
@@ -330,8 +330,6 @@ class SketchPipeline:
         return self.launch(M, N)
 
     def _result(self):
-        if self.method == "SSM":
-            return self.CD.view(self.m, self.p)
         return self.CD.view(self.B, self.m, self.p) if self.B > 1 else self.CD.view(self.m, self.p)
 
     def launch(self, M: torch.Tensor, N: torch.Tensor, chunks=None) -> torch.Tensor:
@@ -363,7 +361,8 @@ class SketchPipeline:
                     self._segsq(M, N, dt, k0, k1, 1, st)
             seg_done = True
         if self.method == "SSM":
-            return self._run_ssm(M, N, dt, st)
+            self._plan_ssm(st)
+            return self._contract_sketch(M, N, dt, st)
         # probabilities, score sums and (fused) the main CDF of the optimal probabilities
         self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B, self.max_len,
                 P(self.probs), P(self.s), None, P(self.cum), P(self.last), st)
@@ -410,6 +409,14 @@ class SketchPipeline:
         self._c("bmm_sample", P(probs), P(self.cum), P(self.last), P(self.offsets), K, B, n, self.max_len,
                 P(self.budgets),
                 P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
+        return self._contract_sketch(M, N, dt, st)
+
+    def _contract_sketch(self, M, N, dt, st):
+        """Compress the drawn sketch (column, scale) and contract it: C @ D."""
+        B, m, n, p, W = self.B, self.m, self.n, self.p, self.W
+        sM, sN = m * n, n * p
+        ldm, ldn = M.stride(-2), N.stride(-2)
+        P = lambda t: t.data_ptr()  # noqa: E731
         if self.compress:
             # duplicates of a column share its scale: contract the distinct columns only
             self._c("bmm_compress_sketch", P(self.column), P(self.scale), W, W, n, B, P(self.ws_cmp),
@@ -467,8 +474,10 @@ class SketchPipeline:
             self._c("bmm_gemm_f64", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, B, P(self.CD), p, m * p,
                     P(self.ws_gemm), self.ws_gemm.numel(), st)
 
-    def _run_ssm(self, M, N, dt, st):
-        B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W
+    def _plan_ssm(self, st):
+        """SSM (estimators.py:221-253): q_k from the norm pass, draws from the
+        caller's stream, then the whole-block draws expanded to sketch columns."""
+        B, n, K = self.B, self.n, self.K
         P = lambda t: t.data_ptr()  # noqa: E731
         self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B, self.max_len, None, None,
                 P(self.fnorm), None, None, st)
@@ -477,14 +486,8 @@ class SketchPipeline:
         (states,) = self._seedbuf["states"]
         self._c("bmm_sample", P(self.q), P(self.qcum), P(self.qlast), P(self.qoff), 1, B, K, K, P(self.q_bud),
                 P(self.q_coloff), self.draws, P(states), P(self.blk), P(self.blk_prob), P(self.blk_scale), st)
-        if B != 1:
-            raise NotImplementedError("batched SSM gather")
-        A, Bm = self._f64(M, N)
-        self._c("bmm_gather_blocks", _lib.BMM_F64, P(A), A.stride(-2), P(Bm), Bm.stride(-2), m, p, P(self.offsets),
-                P(self.blk), P(self.blk_scale), P(self.sk_off), self.draws, W, P(self.C), W, P(self.D), p, st)
-        self._c("bmm_gemm_f64", P(self.C), W, m * W, P(self.D), p, W * p, m, p, W, B, P(self.CD), p, m * p,
-                P(self.ws_gemm), self.ws_gemm.numel(), st)
-        return self.CD.view(m, p)
+        self._c("bmm_expand_blocks", P(self.blk), P(self.blk_scale), self.draws, self.draws, P(self.offsets),
+                self.sizes[0], B, P(self.column), P(self.scale), self.W, st)
 
     def _segsq(self, M, N, dt, k0, k1, B, st):
         """OPL g_k^2 for blocks k0..k1-1 of every problem (k0 > 0: one problem, a
@@ -492,7 +495,10 @@ class SketchPipeline:
         P = lambda t: t.data_ptr()  # noqa: E731
         m, p = self.m, self.p
         sM, sN = m * self.n, self.n * p
-        if self.seg_engine == "i8":
+        if self.seg_engine == "gram":
+            self._c("bmm_segsq_gram", dt, P(M), M.stride(-2), sM, P(N), N.stride(-2), sN, m, p,
+                    P(self.offsets) + 8 * k0, k1 - k0, 0, B, P(self.gsq) + 8 * k0, st)
+        elif self.seg_engine == "i8":
             n_inner = int(sum(self.sizes[k0:k1]))
             self._c("bmm_segsq_i8", dt, P(M), M.stride(-2), sM, P(N), N.stride(-2), sN, m, p, n_inner,
                     P(self.offsets) + 8 * k0, k1 - k0, 0, B, P(self.gsq) + 8 * k0, P(self.ws_seg),

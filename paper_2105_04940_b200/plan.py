@@ -190,26 +190,43 @@ class DeviceInstance:
     def block_product_sq(self) -> torch.Tensor:
         """g_k^2 = ||M^k N_k||_F^2 for every block (segmented square sums: int8
         tensor-core Ozaki split, or DMMA; see segsq_engine)."""
-        if segsq_engine(self.max_len, self.M.shape[0], self.N.shape[1], self.n) == "i8":
+        eng = segsq_engine(self.max_len, self.M.shape[0], self.N.shape[1], self.n)
+        if eng == "gram":
+            return segsq_gram(self.M, self.N, self.offsets, self.K)
+        if eng == "i8":
             return segsq_i8(self.M, self.N, self.offsets, self.K)
         return segsq(self.M, self.N, self.offsets, self.K)
 
 
 SEGSQ_I8_MAX_LEN = 32768  # bmm_segsq_i8's exact-accumulation bound per segment
 SEGSQ_I8_MIN_FLOPS = 2e9  # below this the DMMA kernel's single pass beats split + int8 contraction
+SEGSQ_GRAM_MAX_LEN = 64   # bmm_segsq_gram: one 64 x 64 Gram panel per block
+SEGSQ_I8_SPEEDUP = 3.0    # int8 Ozaki contraction vs DMMA per float64 flop (measured, DESIGN.md §5)
 
 
 def segsq_engine(max_len: int, m: int, p: int, n: int) -> str:
-    """Kernel for the OPL block-product norms g_k^2: "i8" (bmm_segsq_i8, int8
+    """Kernel for the OPL block-product norms g_k^2 (plan.py:176-189).
+
+    "gram" (bmm_segsq_gram: <M^k^T M^k, N_k N_k^T> on DMMA, 36 of 64 tiles by
+    symmetry, 2 (m+p) n L (36/64) flops) when every block has at most 64
+    columns and that beats the direct product; else "i8" (bmm_segsq_i8, int8
     tensor cores, float64-accurate Ozaki split) for 2 m p n >= SEGSQ_I8_MIN_FLOPS
-    unless a block exceeds its length bound; else "dmma" (bmm_segsq_f64).
-    BMM_SEGSQ=i8|dmma forces one (i8 still needs blocks <= SEGSQ_I8_MAX_LEN)."""
+    unless a block exceeds its length bound; else "dmma" (bmm_segsq_f64, the
+    direct segmented product).  BMM_SEGSQ=gram|i8|dmma forces one where it applies."""
     forced = os.environ.get("BMM_SEGSQ", "").lower()
-    if max_len > SEGSQ_I8_MAX_LEN or forced in ("dmma", "f64"):
+    gram_ok = max_len <= SEGSQ_GRAM_MAX_LEN
+    i8_ok = max_len <= SEGSQ_I8_MAX_LEN
+    if forced == "gram" and gram_ok:
+        return "gram"
+    if forced in ("dmma", "f64"):
         return "dmma"
-    if forced == "i8":
+    if forced == "i8" and i8_ok:
         return "i8"
-    return "i8" if 2.0 * m * p * n >= SEGSQ_I8_MIN_FLOPS else "dmma"
+    direct = "i8" if i8_ok and 2.0 * m * p * n >= SEGSQ_I8_MIN_FLOPS else "dmma"
+    direct_cost = m * p / (SEGSQ_I8_SPEEDUP if direct == "i8" else 1.0)
+    if not forced and gram_ok and (m + p) * max_len * 36.0 / 64.0 < direct_cost:
+        return "gram"
+    return direct
 
 
 PILOT_GRAM_MAX = 16  # two-step pilot norms by Gram matrices up to this many draws per block
@@ -251,6 +268,18 @@ def segsq(A: torch.Tensor, B: torch.Tensor, seg: torch.Tensor, nseg: int) -> tor
     ws = _lib.workspace(wsb)
     _lib.call("bmm_segsq_f64", _lib.ptr(A), A.stride(0), 0, _lib.ptr(B), B.stride(0), 0, m, p,
               _lib.ptr(seg), nseg, 0, 1, _lib.ptr(out), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    return out
+
+
+def segsq_gram(A: torch.Tensor, B: torch.Tensor, seg: torch.Tensor, nseg: int) -> torch.Tensor:
+    """g_j^2 = ||A[:, seg_j] B[seg_j, :]||_F^2 through the Gram identity on the
+    DMMA pipe (bmm_segsq_gram; segments of at most 64 columns)."""
+    if A.dtype != B.dtype:
+        A, B = A.to(torch.float64), B.to(torch.float64)
+    m, p = A.shape[0], B.shape[1]
+    out = torch.empty(nseg, dtype=torch.float64, device=A.device)
+    _lib.call("bmm_segsq_gram", _lib.matrix_dtype(A), _lib.ptr(A), A.stride(0), 0, _lib.ptr(B), B.stride(0), 0,
+              m, p, _lib.ptr(seg), nseg, 0, 1, _lib.ptr(out), _lib.stream_ptr())
     return out
 
 
