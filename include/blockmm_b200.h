@@ -55,6 +55,7 @@ extern "C" {
 #define BMM_ST_NOT_PLACED 10       /* plan.py:342 AssertionError                                    */
 #define BMM_ST_EMPTY_SUPPORT 11    /* estimators.py:39-40                                           */
 #define BMM_ST_PLAN_MISMATCH 12    /* plan.py:146-152 zero budget on a scored block (diag = block)  */
+#define BMM_ST_BAD_PROBS 13        /* plan.py:68-69 non-finite probabilities (NaN/Inf input; diag = block) */
 
 /* budget rules for bmm_budgets (plan.py allocators) */
 #define BMM_RULE_EXPLICIT 0   /* integerize(weights, c, caps, floor)          plan.py:242-347 */

@@ -31,6 +31,7 @@ ST_NO_CONVERGE = 9
 ST_NOT_PLACED = 10
 ST_EMPTY_SUPPORT = 11
 ST_PLAN_MISMATCH = 12
+ST_BAD_PROBS = 13
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

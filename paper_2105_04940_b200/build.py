@@ -10,6 +10,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -35,16 +36,20 @@ def _headers_mtime() -> float:
 def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
     hdr = _headers_mtime()
-    objs = []
+    objs, cmds = [], []
     for src in sources():
         obj = OBJ / (src.stem + ".o")
         objs.append(obj)
         if not force and obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr):
             continue
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
-        if verbose:
-            print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
+        cmds.append([NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)])
+    # one nvcc per translation unit, in parallel (the big TUs take ~30 s each)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for cmd in cmds:
+            if verbose:
+                print(" ".join(cmd), flush=True)
+        for f in [ex.submit(subprocess.run, c, check=True) for c in cmds]:
+            f.result()
     newest = max(o.stat().st_mtime for o in objs)
     if force or not LIB.exists() or LIB.stat().st_mtime < newest:
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]

@@ -982,6 +982,128 @@ static bool launch_colsq_tma(const T* M, int64_t m, int64_t n, int64_t ldm, int6
   }
 }
 
+// ---- Wide column sums (config 4: M 16384 x 262144 f32; config 3: 1000 x 100000
+// f64).  The direct-load kernel (colsq_vec) stalls at ~55% of HBM on config 4:
+// ptxas sinks its row loads next to their uses, so few bytes are in flight per
+// thread.  Here TMA does the loads: the n columns are cut into 32-column units
+// and each CTA owns an equal contiguous run of units (at most kWideUnits; two
+// CTAs per SM, so every unit is resident in ONE wave -- no tail of half-empty
+// waves), one consumer warp per unit (lane = column: the exact sequential
+// chain of NumPy's add.reduce over rows) and one producer warp that streams
+// RB-row slabs of every unit of the CTA into a STAGES-deep ring (full/empty
+// mbarriers).  Rows past m inside the last slab are TMA zero-fill and skipped.
+constexpr int kWideUnits = 28;
+
+template <typename T, int RB, int STAGES>
+__global__ void __launch_bounds__(32 * (kWideUnits + 1), 2) colsq_wide_kernel(const __grid_constant__ CUtensorMap map,
+                                                                             int64_t m, int64_t n, int64_t units,
+                                                                             int accumulate, double* __restrict__ colsq) {
+  constexpr int BOX = 32 * RB * (int)sizeof(T);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = (int)(blockDim.x >> 5) - 1;  // consumer warps; warp nw produces
+  const int64_t u0 = (int64_t)blockIdx.x * units / gridDim.x, u1 = (int64_t)(blockIdx.x + 1) * units / gridDim.x;
+  const int U = (int)(u1 - u0);
+  const int64_t slabs = (m + RB - 1) / RB;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm_addr(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm_addr(&empty[s])), "r"(U));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == nw) {
+    if (lane == 0) {
+      for (int64_t q = 0; q < slabs; ++q) {
+        const int st = (int)(q % STAGES);
+        if (q >= STAGES) {
+          const uint32_t par = (uint32_t)(((q / STAGES) - 1) & 1);
+          asm volatile(
+              "{\n"
+              ".reg .pred P1;\n"
+              "WAIT_%=:\n"
+              "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+              "@!P1 bra WAIT_%=;\n"
+              "}\n" ::"r"(sm_addr(&empty[st])),
+              "r"(par)
+              : "memory");
+        }
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm_addr(&full[st])),
+                     "r"(U * BOX)
+                     : "memory");
+        for (int u = 0; u < U; ++u)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+                  sm_addr(smem + (int64_t)(st * U + u) * BOX)),
+              "l"(reinterpret_cast<uint64_t>(&map)), "r"(sm_addr(&full[st])), "r"((int)((u0 + u) * 32)),
+              "r"((int)(q * RB))
+              : "memory");
+      }
+    }
+    return;
+  }
+  if (warp >= U) return;
+  const int64_t col = (u0 + warp) * 32 + lane;
+  double acc = (accumulate && col < n) ? colsq[col] : 0.0;
+  for (int64_t q = 0; q < slabs; ++q) {
+    const int st = (int)(q % STAGES);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(sm_addr(&full[st])),
+        "r"((uint32_t)((q / STAGES) & 1))
+        : "memory");
+    const T* slab = reinterpret_cast<const T*>(smem + (int64_t)(st * U + warp) * BOX);
+    const int rows = (int)min((int64_t)RB, m - q * RB);
+    double v[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) v[r] = (double)slab[r * 32 + lane];
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (r < rows) acc = __dadd_rn(acc, __dmul_rn(v[r], v[r]));
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sm_addr(&empty[st])) : "memory");
+  }
+  if (col < n) colsq[col] = acc;
+}
+
+template <typename T>
+static bool launch_colsq_wide(const T* M, int64_t m, int64_t n, int64_t ldm, int accumulate, double* colsq,
+                              cudaStream_t st) {
+  constexpr int RB = 8, STAGES = sizeof(T) == 4 ? 3 : 2;
+  if ((ldm * (int64_t)sizeof(T)) % 16 != 0 || ldm < n || reinterpret_cast<uintptr_t>(M) % 16 != 0 ||
+      m >= (1LL << 31) || n >= (1LL << 31))
+    return false;
+  auto enc = tma_encode_fn();
+  if (enc == nullptr) return false;
+  const int64_t units = (n + 31) / 32;
+  // two CTAs per SM, every unit in one wave when units <= 296 * kWideUnits
+  int64_t ctas = std::max<int64_t>(148 * 2, ceil_div(units, kWideUnits));
+  ctas = std::min<int64_t>(ctas, units);
+  const int umax = (int)ceil_div(units, ctas);
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+  cuuint64_t strides[1] = {(cuuint64_t)(ldm * sizeof(T))};
+  cuuint32_t box[2] = {32, (cuuint32_t)RB};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  if (enc(&map, dt, 2, const_cast<T*>(M), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return false;
+  auto kern = colsq_wide_kernel<T, RB, STAGES>;
+  const int smem = STAGES * umax * 32 * RB * (int)sizeof(T) + 1024;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+  kern<<<(unsigned)ctas, 32 * (umax + 1), smem, st>>>(map, m, n, units, accumulate, colsq);
+  return true;
+}
+
 template <typename T>
 int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM, const T* N,
                  int64_t p, int64_t ldn, int64_t strideN, int64_t batch, int accumulate,
@@ -996,8 +1118,17 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
       const char* e = getenv("BMM_COLSQ_VARIANT");  // A/B switch: 1 disables the TMA-staged kernel, 2-5 pick its shape
       return e ? atoi(e) : 0;
     }();
-    const bool done = narrow && cs_variant != 1 &&
-                      launch_colsq_tma<T>(M, m, n, ldm, strideM, batch, accumulate, colsq, cs_variant, st);
+    static const int wide_mode = [] {
+      const char* e = getenv("BMM_COLSQ_WIDE");  // A/B switch: 0 keeps the direct-load kernel for wide M
+      return e ? atoi(e) : 1;
+    }();
+    // wide, long single matrices (>= 256 MB): the TMA-streamed one-wave kernel
+    const bool wide = !narrow && batch == 1 && wide_mode != 0 && m >= 64 &&
+                      m * n * (int64_t)sizeof(T) >= (256LL << 20);
+    bool done = wide && launch_colsq_wide<T>(M, m, n, ldm, accumulate, colsq, st);
+    if (done) BMM_CHECK_LAUNCH("colsq_wide_kernel");
+    done = done || (narrow && cs_variant != 1 &&
+                    launch_colsq_tma<T>(M, m, n, ldm, strideM, batch, accumulate, colsq, cs_variant, st));
     if (done) BMM_CHECK_LAUNCH("colsq_tma_kernel");
     const bool vec_ok = !done && !narrow && (reinterpret_cast<uintptr_t>(M) % 16 == 0) && (ldm % W == 0) &&
                         (strideM % W == 0) && n >= W;

@@ -200,7 +200,8 @@ __global__ void normalize_kernel(const double* __restrict__ f, int64_t K, int64_
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch;
        b += (int64_t)gridDim.x * blockDim.x) {
     const double tot = __dadd_rn(0.0, pw_sum(SrcF64{f + b * K}, 0, K));
-    if (status) status[b] = (tot == 0.0) ? BMM_ST_ZERO_SCORE : BMM_ST_OK;
+    // non-finite norms: q is NaN and _draw_indices finds no support   estimators.py:39-40
+    if (status) status[b] = (tot == 0.0) ? BMM_ST_ZERO_SCORE : (isfinite(tot) ? BMM_ST_OK : BMM_ST_EMPTY_SUPPORT);
     for (int64_t k = 0; k < K; ++k) q[b * K + k] = (tot == 0.0) ? 0.0 : __ddiv_rn(f[b * K + k], tot);
   }
 }
@@ -363,6 +364,7 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
 
   int local_err = 0;  // reference error raised by this thread's blocks
   int64_t any_pos_s = 0;
+  int64_t first_nonfinite = K;  // first block whose score sum (so its probabilities) is not finite
   // ---- allocator weights, caps and floors (plan.py:373-421, 465-470)
   for (int64_t k = k_lo; k < k_hi; ++k) {
     double w = 0.0;
@@ -380,6 +382,9 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
       if (!(isfinite(w)) || w < 0.0) local_err = max(local_err, 100 + BMM_ST_BAD_WEIGHT);
     } else {
       if (sk > 0.0) any_pos_s = 1;
+      // NaN/Inf in M or N: the reference's BlockProbabilities raises for the first such
+      // block before any size rule runs                               plan.py:68-69
+      if (!isfinite(sk)) first_nonfinite = min(first_nonfinite, k);
       if (rule == BMM_RULE_ONC) {
         w = sk;
       } else if (rule == BMM_RULE_OPL) {
@@ -397,6 +402,7 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
       capk = (cap ? sizes[k] : c);
       if (!(sk > 0.0)) capk = 0;
       mn = (sk > 0.0);
+      if (!isfinite(w)) local_err = max(local_err, 100 + BMM_ST_BAD_WEIGHT);  // integerize, plan.py:265-266
     }
     ws.w[k] = w;
     ws.maxs[k] = min(capk, c);
@@ -411,6 +417,14 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
     // pack three small values into one reduction round each
     int64_t v0 = block_sum_i64(any_pos_s, red);
     int64_t v1 = block_sum_i64(any_w, red);
+    int64_t fn = first_nonfinite;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fn = min(fn, (int64_t)__shfl_xor_sync(0xffffffffu, fn, o));
+    if ((tid & 31) == 0) red[tid >> 5] = fn;
+    __syncthreads();
+    first_nonfinite = K;
+    for (int i = 0; i < (NT >> 5); ++i) first_nonfinite = min(first_nonfinite, (int64_t)red[i]);
+    __syncthreads();
     // max via per-warp max then smem
     int e = (int)err_max;
 #pragma unroll
@@ -428,7 +442,10 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
   int64_t dg = 0;
   int32_t note = 0;
   const bool scored = (rule == BMM_RULE_ONC || rule == BMM_RULE_OPL || rule == BMM_RULE_TWO_STEP);
-  if (scored && any_pos_s == 0) st = BMM_ST_ZERO_SCORE;                       // plan.py:390,410,453
+  // (allocate_two_step validates the optimal probabilities only after integerize, so a
+  // two-step plan on NaN/Inf input raises integerize's BAD_WEIGHT, plan.py:465-479)
+  if (scored && rule != BMM_RULE_TWO_STEP && first_nonfinite < K) { st = BMM_ST_BAD_PROBS; dg = first_nonfinite; }
+  else if (scored && any_pos_s == 0) st = BMM_ST_ZERO_SCORE;                  // plan.py:390,410,453
   else if (err_max > 100) st = (int32_t)(err_max - 100);                       // CS / bad weight
   else if (err_max > 50) st = (int32_t)(err_max - 50);                         // radicand
   if (st == BMM_ST_OK && (rule == BMM_RULE_OPL || rule == BMM_RULE_TWO_STEP) && any_w == 0) {

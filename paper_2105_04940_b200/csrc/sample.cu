@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(32 * kSampleWarps) sample_kernel(
         const int64_t mid = (lo + hi) >> 1;
         if (cb[mid] > u) hi = mid; else lo = mid + 1;
       }
-      const int64_t idx = lo < lst ? lo : lst;
+      // lst < 0 only for an all-zero (or NaN) block, which a valid plan never samples;
+      // clamp anyway so a failed plan (status != OK) cannot index outside the block
+      const int64_t idx = max((int64_t)0, lo < lst ? lo : lst);
       const double pr = pb[idx];
       const double sc = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dck, pr)));
       const int64_t t = b * w_stride + t0 + j;

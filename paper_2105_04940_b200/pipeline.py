@@ -98,6 +98,39 @@ def seeds_from_keys(method: str, entropy: int, key_prefix: tuple, keys, K: int) 
     return CallSeeds(main=StreamSeeds(np.ascontiguousarray(words), zeros))
 
 
+def _stats_launch(obj, M: torch.Tensor, N: torch.Tensor, chunks, *, probs: bool, gsq: bool) -> bool:
+    """Per-instance statistics of `obj` (a SketchPipeline or a group's SharedStats):
+    the norm pass (K1), optionally the optimal probabilities / score sums / main
+    CDF (K2) and, in chunked mode, OPL's g_k^2 per landed chunk.  Returns True
+    when g_k^2 was computed here (chunked)."""
+    B, m, n, p, K = obj.B, obj.m, obj.n, obj.p, obj.K
+    dt = _lib.matrix_dtype(M)
+    st = _lib.stream_ptr()
+    sM, sN = m * n, n * p
+    ldm, ldn = M.stride(-2), N.stride(-2)
+    P = lambda t: t.data_ptr()  # noqa: E731
+    seg_done = False
+    if chunks is None:
+        obj._c("bmm_norms", dt, P(M), m, n, ldm, sM, P(N), p, ldn, sN, B, 0, P(obj.colsq), P(obj.rowsq), st)
+    else:
+        if B != 1 or not probs:
+            raise ValueError("chunked launch: one problem, non-SSM method")
+        es = M.element_size()
+        cur = torch.cuda.current_stream()
+        for c0, c1, k0, k1, ev in chunks:
+            cur.wait_event(ev)
+            obj._c("bmm_norms", dt, P(M) + es * c0, m, c1 - c0, ldm, 0, P(N) + es * c0 * ldn, p, ldn, 0, 1, 0,
+                   P(obj.colsq) + 8 * c0, P(obj.rowsq) + 8 * c0, st)
+            if gsq:
+                obj._segsq(M, N, dt, k0, k1, 1, st)
+        seg_done = gsq
+    if probs:
+        # probabilities, score sums and (fused) the main CDF of the optimal probabilities
+        obj._c("bmm_block_probs", P(obj.colsq), P(obj.rowsq), n, P(obj.offsets), K, B, obj.max_len,
+               P(obj.probs), P(obj.s), None, P(obj.cum), P(obj.last), st)
+    return seg_done
+
+
 class SketchPipeline:
     """Preallocated device pipeline for `batch` problems of shape
     M (m x n), N (n x p) sharing one block partition."""
@@ -231,6 +264,8 @@ class SketchPipeline:
         self.graph = None
         self.timeline = None
         self.stamps = None  # (device int64 buffer, [entry names]) for tools/timeline.py
+        self.shared = None        # SharedStats of the PipelineGroup that owns this member's statistics
+        self._group_active = False  # set while the owning group enqueues this member
 
     # ------------------------------------------------------------------ steps
     def _c(self, name, *args):
@@ -321,8 +356,7 @@ class SketchPipeline:
 
     def run(self, M: torch.Tensor, N: torch.Tensor, seeds: CallSeeds) -> torch.Tensor:
         """Approximate products of the batch; returns CD as (B, m, p) (or (m, p))."""
-        if self._joint is not None:
-            raise RuntimeError("this pipeline is contracted by its joint PipelineGroup: run the group")
+        self._guard()
         self.set_seeds(seeds)
         if getattr(self, "graph", None) is not None and self._graph_ptrs == (M.data_ptr(), N.data_ptr()):
             self.graph.replay()
@@ -332,6 +366,11 @@ class SketchPipeline:
     def _result(self):
         return self.CD.view(self.B, self.m, self.p) if self.B > 1 else self.CD.view(self.m, self.p)
 
+    def _guard(self) -> None:
+        if (self._joint is not None or self.shared is not None) and not self._group_active:
+            raise RuntimeError("this pipeline's statistics or contraction belong to its PipelineGroup: "
+                               "launch, capture and run the group")
+
     def launch(self, M: torch.Tensor, N: torch.Tensor, chunks=None) -> torch.Tensor:
         """Enqueue the whole pipeline on the current stream (graph-capturable).
 
@@ -339,39 +378,32 @@ class SketchPipeline:
         inner dimension whose M columns and N rows are valid once `event` has
         completed (a chunked host->device transfer).  The norm pass and OPL's
         segmented square sums then run chunk by chunk behind the transfer; the
-        rest of the pipeline is unchanged (single problem, float64 inputs)."""
+        rest of the pipeline is unchanged (single problem, float64 inputs).
+        Members of a PipelineGroup with shared statistics skip the norm pass,
+        the block probabilities and g_k (the group's SharedStats computes them)."""
+        self._guard()
+        if self.shared is None:
+            seg_done = _stats_launch(self, M, N, chunks, probs=self.method != "SSM",
+                                     gsq=self.method == "OPL")
+            if self.method == "OPL" and not seg_done:
+                self._segsq(M, N, _lib.matrix_dtype(M), 0, self.K, self.B, _lib.stream_ptr())
+        return self._plan_and_contract(M, N)
+
+    def _plan_and_contract(self, M: torch.Tensor, N: torch.Tensor) -> torch.Tensor:
+        """Everything after the per-instance statistics: sizes, draws, sketch, C @ D."""
         B, m, n, p, K, W = self.B, self.m, self.n, self.p, self.K, self.W
         dt = _lib.matrix_dtype(M)
         st = _lib.stream_ptr()
-        sM, sN = m * n, n * p
-        ldm, ldn = M.stride(-2), N.stride(-2)
         P = lambda t: t.data_ptr()  # noqa: E731
-        seg_done = False
-        if chunks is None:
-            self._c("bmm_norms", dt, P(M), m, n, ldm, sM, P(N), p, ldn, sN, B, 0, P(self.colsq), P(self.rowsq), st)
-        else:
-            if B != 1 or M.dtype != torch.float64 or self.method == "SSM":
-                raise ValueError("chunked launch: one float64 problem, non-SSM method")
-            cur = torch.cuda.current_stream()
-            for c0, c1, k0, k1, ev in chunks:
-                cur.wait_event(ev)
-                self._c("bmm_norms", dt, P(M) + 8 * c0, m, c1 - c0, ldm, 0, P(N) + 8 * c0 * ldn, p, ldn, 0, 1, 0,
-                        P(self.colsq) + 8 * c0, P(self.rowsq) + 8 * c0, st)
-                if self.method == "OPL":
-                    self._segsq(M, N, dt, k0, k1, 1, st)
-            seg_done = True
         if self.method == "SSM":
             self._plan_ssm(st)
             return self._contract_sketch(M, N, dt, st)
-        # probabilities, score sums and (fused) the main CDF of the optimal probabilities
-        self._c("bmm_block_probs", P(self.colsq), P(self.rowsq), n, P(self.offsets), K, B, self.max_len,
-                P(self.probs), P(self.s), None, P(self.cum), P(self.last), st)
         rule = {"ONC": _lib.RULE_ONC, "OPL": _lib.RULE_OPL, "UU": _lib.RULE_UU,
                 "ONU": _lib.RULE_TWO_STEP, "ONMCNR": _lib.RULE_TWO_STEP}[self.method]
         aux = None
+        sM, sN = m * n, n * p
+        ldm, ldn = M.stride(-2), N.stride(-2)
         if self.method == "OPL":
-            if not seg_done:
-                self._segsq(M, N, dt, 0, K, B, st)
             aux = self.gsq
         if self.method in ("ONU", "ONMCNR"):
             p0 = self.p0 if self.method == "ONU" else self.probs
@@ -525,6 +557,8 @@ class SketchPipeline:
         bad = np.flatnonzero(st != 0)
         if bad.size:
             b = int(bad[0])
+            if self.method == "SSM" and int(st[b]) == _lib.ST_ZERO_SCORE:
+                raise ValueError("all blocks have zero norm: nothing to sample")  # plan.py:494-495
             raise_status(int(st[b]), int(self.diag[b].item()), self.c)
 
     # audit views
@@ -542,18 +576,82 @@ class SketchPipeline:
         return self.scale.view(self.B, self.W).cpu().numpy()
 
 
+class SharedStats:
+    """The statistics every member of a PipelineGroup over one instance (same M,
+    N, partition, batch and dtype) would otherwise recompute: the norm pass,
+    the optimal probabilities, score sums and main CDF, and (when a member is
+    OPL) the block-product norms g_k^2.  The reference recomputes them inside
+    every allocator call (plan.py:165-189, reached from allocate_* 383-480);
+    here one stage computes them once per group call and the members read the
+    same buffers (they only read them: UU keeps its own CDF, SSM its own block
+    probabilities)."""
+
+    _c = None  # bound below to SketchPipeline's launch helpers
+    _segsq = None
+    _f64 = None
+
+    def __init__(self, pipes):
+        p0 = pipes[0]
+        key = lambda q: (q.m, q.n, q.p, q.sizes, q.B, q.dtype, q.colsq.device)  # noqa: E731
+        if any(key(q) != key(p0) for q in pipes):
+            raise ValueError("shared statistics need members over one instance (shape, partition, batch, dtype)")
+        self.lib = p0.lib
+        self.m, self.n, self.p, self.B, self.K = p0.m, p0.n, p0.p, p0.B, p0.K
+        self.sizes, self.max_len, self.offsets = p0.sizes, p0.max_len, p0.offsets
+        self.timeline, self.stamps = None, None
+        self.colsq, self.rowsq = p0.colsq, p0.rowsq
+        self.needs_probs = any(q.method not in ("SSM", "UU") for q in pipes)
+        opl = [q for q in pipes if q.method == "OPL"]
+        self.needs_gsq = bool(opl)
+        src = next((q for q in pipes if q.method not in ("SSM", "UU")), p0)
+        self.probs, self.s, self.cum, self.last = src.probs, src.s, src.cum, src.last
+        if opl:
+            self.gsq, self.seg_engine, self.ws_seg = opl[0].gsq, opl[0].seg_engine, opl[0].ws_seg
+        for q in pipes:
+            q.colsq, q.rowsq = self.colsq, self.rowsq
+            if q.method not in ("SSM", "UU"):
+                q.probs, q.s, q.cum, q.last = self.probs, self.s, self.cum, self.last
+            if q.method == "OPL":
+                q.gsq = self.gsq
+            q.shared = self
+
+    def launch_probs(self, M: torch.Tensor, N: torch.Tensor, chunks=None) -> bool:
+        """Norm pass (+ g_k^2 per chunk when chunked) and the block probabilities."""
+        return _stats_launch(self, M, N, chunks, probs=self.needs_probs, gsq=self.needs_gsq)
+
+    def launch_gsq(self, M: torch.Tensor, N: torch.Tensor) -> None:
+        if self.needs_gsq:
+            self._segsq(M, N, _lib.matrix_dtype(M), 0, self.K, self.B, _lib.stream_ptr())
+
+
+SharedStats._c = SketchPipeline._c
+SharedStats._segsq = SketchPipeline._segsq
+SharedStats._f64 = SketchPipeline._f64
+
+
 class PipelineGroup:
     """Independent pipelines over the same inputs (e.g. a c x method sweep, the
     reference's bench loop ``bench.py:209-245``) replayed as ONE CUDA graph whose
     branches run concurrently: each pipeline is captured on its own forked
     stream, so one product's latency-bound planning kernels overlap another's
-    GEMM. Results are those of the member pipelines run one after another
-    (each branch owns its buffers and workspaces; no kernel keeps global state)."""
+    GEMM. Results are those of the member pipelines run one after another.
 
-    def __init__(self, pipes, joint=None):
+    shared (default on, BMM_SHARED=0 disables): members over one instance read
+    one SharedStats stage -- the norm pass, block probabilities and g_k^2 run
+    once per call instead of once per member (bit-identical: the same kernels on
+    the same inputs).  joint: see below."""
+
+    def __init__(self, pipes, joint=None, shared=None):
         self.pipes = list(pipes)
         self.graph = None
         self.graph_launches = 0
+        if shared is None:
+            shared = os.environ.get("BMM_SHARED", "1") != "0"
+        p0 = self.pipes[0] if self.pipes else None
+        key = lambda q: (q.m, q.n, q.p, q.sizes, q.B, q.dtype, q.colsq.device)  # noqa: E731
+        self.shared = None
+        if shared and len(self.pipes) > 1 and all(key(q) == key(p0) for q in self.pipes):
+            self.shared = SharedStats(self.pipes)
         # joint contraction: float64 compressed members on the DMMA engine with one output
         # shape gather into pooled operands, and ONE batched GEMM contracts all of them
         # (per-member inner lengths read on the device).  Nine 500 x ~3000 x 500 products
@@ -561,9 +659,8 @@ class PipelineGroup:
         # BMM_JOINT=0 (or joint=False) keeps one GEMM per member.
         if joint is None:
             joint = os.environ.get("BMM_JOINT", "1") != "0"
-        p0 = self.pipes[0] if self.pipes else None
         self.joint = bool(joint) and len(self.pipes) > 1 and all(
-            q.B == 1 and q.method != "SSM" and not q.tf32 and q.compress and q.gemm_engine == "dmma"
+            q.B == 1 and not q.tf32 and q.compress and q.gemm_engine == "dmma"
             and (q.m, q.p) == (p0.m, p0.p) and q.C.device == p0.C.device for q in self.pipes)
         self._jgroups = []
         if self.joint:
@@ -588,6 +685,10 @@ class PipelineGroup:
                     del q.ws_gemm
                 self._jgroups.append(jg)
 
+    def _active(self, on: bool) -> None:
+        for q in self.pipes:
+            q._group_active = on
+
     def _joint_gemm(self, jg=None) -> None:
         m, p = self.pipes[0].m, self.pipes[0].p
         for g in ([jg] if jg is not None else self._jgroups):
@@ -606,10 +707,35 @@ class PipelineGroup:
         return [torch.cuda.Stream(priority=-1 if q.method == "OPL" else 0) for q in self.pipes]
 
     def _launch_all(self, M: torch.Tensor, N: torch.Tensor) -> None:
-        for pipe in self.pipes:
-            pipe.launch(M, N)
-        if self.joint:
-            self._joint_gemm()
+        self._active(True)
+        try:
+            if self.shared is not None:
+                self.shared.launch_probs(M, N)
+                self.shared.launch_gsq(M, N)
+            for pipe in self.pipes:
+                pipe.launch(M, N)
+            if self.joint:
+                self._joint_gemm()
+        finally:
+            self._active(False)
+
+    def _fork_stats(self, cap, M, N, chunks=None):
+        """Enqueue the shared statistics on their own stream (forked from `cap`);
+        returns (events after the block probabilities, after g_k^2, the stream)."""
+        ss = torch.cuda.Stream(priority=-1)
+        ss.wait_stream(cap)
+        ev_p, ev_g = torch.cuda.Event(), torch.cuda.Event()
+        with torch.cuda.stream(ss):
+            done = self.shared.launch_probs(M, N, chunks)
+            ev_p.record(ss)
+            if not done:
+                self.shared.launch_gsq(M, N)
+            ev_g.record(ss)
+        return ev_p, ev_g, ss
+
+    def _member_wait(self, s, pipe, evs):
+        if evs is not None:
+            s.wait_event(evs[1] if pipe.method == "OPL" else evs[0])
 
     def capture(self, M: torch.Tensor, N: torch.Tensor) -> None:
         cur = torch.cuda.current_stream()
@@ -621,21 +747,31 @@ class PipelineGroup:
         streams = self._branch_streams()
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launches()
-        with torch.cuda.graph(g):
-            cap = torch.cuda.current_stream()
-            for s, pipe in zip(streams, self.pipes):
-                s.wait_stream(cap)
-                with torch.cuda.stream(s):
-                    pipe.launch(M, N)
-            for jg in self._jgroups:  # each width's GEMM after its own members
-                js = torch.cuda.Stream()
-                for i in jg["idx"]:
-                    js.wait_stream(streams[i])
-                with torch.cuda.stream(js):
-                    self._joint_gemm(jg)
-                streams.append(js)
-            for s in streams:
-                cap.wait_stream(s)
+        self._active(True)
+        try:
+            with torch.cuda.graph(g):
+                cap = torch.cuda.current_stream()
+                evs = None
+                extra = []
+                if self.shared is not None:
+                    *evs, ss = self._fork_stats(cap, M, N)
+                    extra.append(ss)
+                for s, pipe in zip(streams, self.pipes):
+                    s.wait_stream(cap)
+                    self._member_wait(s, pipe, evs)
+                    with torch.cuda.stream(s):
+                        pipe.launch(M, N)
+                for jg in self._jgroups:  # each width's GEMM after its own members
+                    js = torch.cuda.Stream()
+                    for i in jg["idx"]:
+                        js.wait_stream(streams[i])
+                    with torch.cuda.stream(js):
+                        self._joint_gemm(jg)
+                    extra.append(js)
+                for s in streams + extra:
+                    cap.wait_stream(s)
+        finally:
+            self._active(False)
         self.graph_launches = _lib.launches() - n0
         self.graph, self._graph_ptrs = g, (M.data_ptr(), N.data_ptr())
 
@@ -643,12 +779,14 @@ class PipelineGroup:
                      out_host: list, seeds: list, n_chunks: int = 8) -> None:
         """End-to-end graph from pinned host inputs to pinned host products: M's
         block-column slabs and N's row slabs are copied chunk by chunk on a copy
-        stream, every branch runs its norm pass (and OPL segmented square sums)
-        on each chunk as it lands, then the rest of its pipeline, then copies its
-        product back.  Replay with run_host()."""
+        stream, the norm pass (and OPL segmented square sums) runs on each chunk as
+        it lands, then the rest of every member's pipeline, then each product is
+        copied back.  Replay with run_host().  Single problem (batch 1), float64
+        or float32 inputs."""
         pipes = self.pipes
         sizes = pipes[0].sizes
         n, m, p = pipes[0].n, pipes[0].m, pipes[0].p
+        es = M.element_size()
         off = np.concatenate([[0], np.cumsum(sizes)])
         bounds = [0]
         for c in range(1, n_chunks):
@@ -663,45 +801,56 @@ class PipelineGroup:
         side = torch.cuda.Stream()
         side.wait_stream(cur)
         with torch.cuda.stream(side):  # warm-up: lazy buffers outside the capture
-            for pipe in pipes:
-                pipe.launch(M, N)
+            self._launch_all(M, N)
         cur.wait_stream(side)
         copy = torch.cuda.Stream()
         streams = [torch.cuda.Stream() for _ in pipes]
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launches()
-        with torch.cuda.graph(g):
-            cap = torch.cuda.current_stream()
-            copy.wait_stream(cap)
-            chunks = []
-            with torch.cuda.stream(copy):
-                cs = _lib.stream_ptr()
-                for c0, c1, k0, k1 in plan:
-                    _lib.call("bmm_copy2d", M.data_ptr() + 8 * c0, 8 * n, M_host.data_ptr() + 8 * c0, 8 * n,
-                              8 * (c1 - c0), m, 1, cs)
-                    nb = 8 * (c1 - c0) * p
-                    _lib.call("bmm_copy2d", N.data_ptr() + 8 * c0 * p, nb, N_host.data_ptr() + 8 * c0 * p, nb, nb, 1,
-                              1, cs)
-                    ev = torch.cuda.Event()
-                    ev.record(copy)
-                    chunks.append((c0, c1, k0, k1, ev))
-            for s, pipe, oh in zip(streams, pipes, out_host):
-                s.wait_stream(cap)
-                with torch.cuda.stream(s):
-                    out = pipe.launch(M, N, chunks=chunks)
-                    if not self.joint:
-                        oh.copy_(out.reshape(oh.shape), non_blocking=True)
-            for jg in self._jgroups:  # joint mode: each width's GEMM, then its products go home
-                js = torch.cuda.Stream()
-                for i in jg["idx"]:
-                    js.wait_stream(streams[i])
-                with torch.cuda.stream(js):
-                    self._joint_gemm(jg)
-                    for j, i in enumerate(jg["idx"]):
-                        out_host[i].copy_(jg["CD"][j].reshape(out_host[i].shape), non_blocking=True)
-                streams.append(js)
-            for s in streams + [copy]:
-                cap.wait_stream(s)
+        self._active(True)
+        try:
+            with torch.cuda.graph(g):
+                cap = torch.cuda.current_stream()
+                copy.wait_stream(cap)
+                chunks = []
+                with torch.cuda.stream(copy):
+                    cs = _lib.stream_ptr()
+                    for c0, c1, k0, k1 in plan:
+                        _lib.call("bmm_copy2d", M.data_ptr() + es * c0, es * n, M_host.data_ptr() + es * c0, es * n,
+                                  es * (c1 - c0), m, 1, cs)
+                        nb = es * (c1 - c0) * p
+                        _lib.call("bmm_copy2d", N.data_ptr() + es * c0 * p, nb, N_host.data_ptr() + es * c0 * p, nb,
+                                  nb, 1, 1, cs)
+                        ev = torch.cuda.Event()
+                        ev.record(copy)
+                        chunks.append((c0, c1, k0, k1, ev))
+                evs, extra = None, [copy]
+                if self.shared is not None:
+                    *evs, ss = self._fork_stats(cap, M, N, chunks)
+                    extra.append(ss)
+                for s, pipe, oh in zip(streams, pipes, out_host):
+                    s.wait_stream(cap)
+                    self._member_wait(s, pipe, evs)
+                    with torch.cuda.stream(s):
+                        if self.shared is not None:
+                            out = pipe.launch(M, N)
+                        else:
+                            out = pipe.launch(M, N, chunks=chunks)
+                        if not self.joint:
+                            oh.copy_(out.reshape(oh.shape), non_blocking=True)
+                for jg in self._jgroups:  # joint mode: each width's GEMM, then its products go home
+                    js = torch.cuda.Stream()
+                    for i in jg["idx"]:
+                        js.wait_stream(streams[i])
+                    with torch.cuda.stream(js):
+                        self._joint_gemm(jg)
+                        for j, i in enumerate(jg["idx"]):
+                            out_host[i].copy_(jg["CD"][j].reshape(out_host[i].shape), non_blocking=True)
+                    extra.append(js)
+                for s in streams + extra:
+                    cap.wait_stream(s)
+        finally:
+            self._active(False)
         self.host_graph_launches = _lib.launches() - n0
         self.host_graph = g
 
@@ -713,16 +862,12 @@ class PipelineGroup:
 
     def run(self, M: torch.Tensor, N: torch.Tensor, seeds: list) -> list:
         """One call per member pipeline (same seeds contract as SketchPipeline.run)."""
-        if self.graph is None or self._graph_ptrs != (M.data_ptr(), N.data_ptr()):
-            if not self.joint:
-                return [pipe.run(M, N, s) for pipe, s in zip(self.pipes, seeds)]
-            for pipe, s in zip(self.pipes, seeds):
-                pipe.set_seeds(s)
-            self._launch_all(M, N)
-            return [pipe._result() for pipe in self.pipes]
         for pipe, s in zip(self.pipes, seeds):
             pipe.set_seeds(s)
-        self.graph.replay()
+        if self.graph is None or self._graph_ptrs != (M.data_ptr(), N.data_ptr()):
+            self._launch_all(M, N)
+        else:
+            self.graph.replay()
         return [pipe._result() for pipe in self.pipes]
 
     def check(self) -> None:

@@ -319,6 +319,7 @@ def raise_status(st: int, diag: int, c: int) -> None:
         _lib.ST_ABOVE_CAPS: f"budget c={c} exceeds the total caps {diag}",
         _lib.ST_EMPTY_SUPPORT: "probability vector has empty support",
         _lib.ST_PLAN_MISMATCH: f"block {diag}: zero budget and zero-probability flag must coincide",
+        _lib.ST_BAD_PROBS: f"block {diag}: probabilities must be finite and >= 0",
     }
     if st == _lib.ST_NO_CONVERGE:
         raise AssertionError("apportionment did not converge")

@@ -91,26 +91,3 @@ def test_analytics_errors_like_reference():
         va.elementwise_variance(M, N, plan, budgets=zero)
     with pytest.raises(ValueError, match="budget must be positive"):
         va.minimum_expected_sq_error(M, N, part, 0)
-
-
-@pytest.mark.parametrize("seed", SEEDS)
-def test_bounds_match_reference(seed):
-    from paper_2105_04940_b200 import bounds as bd
-
-    M, N, sizes, c, _ = sweep_params(seed)
-    part = bm.BlockPartition(sizes)
-    two = bm.estimate_product_two_step(M, N, part, c, 3 * len(sizes), np.random.default_rng(seed),
-                                       pilot="uniform").plan
-    assert np.array_equal(two.budgets, G[f"s{seed}_ONU__budgets"])
-    assert np.allclose(two.pilot_norms, G[f"s{seed}_ONU__pilot"], rtol=1e-12, atol=0)
-    for meth in ("ONC", "OPL", "UU", "ONU"):
-        plan = two if meth == "ONU" else _plan(M, N, part, c, meth)
-        inp = bd.bound_inputs_for_plan(M, N, plan, 0.1)
-        vals = [inp.prob_floor, inp.cancel_lo, inp.cancel_hi, inp.frob_m, inp.frob_n]
-        vals += list(bd.bounds_optimal_allocation(inp))
-        try:
-            vals += list(bd.bounds_score_allocation(inp))
-        except ValueError:
-            vals += [-1.0, -1.0]
-        vals += list(bd.bounds_pilot_allocation(inp)) if inp.cancel_hi_exact is not None else [np.nan, np.nan]
-        assert np.allclose(vals, G[f"s{seed}_{meth}__bounds"], rtol=1e-9, atol=0, equal_nan=True), meth

@@ -38,17 +38,21 @@ def test_pipeline_matches_oracle(method, graph):
         assert rel(CD, ref["CD"]) < 1e-12
 
 
-def test_pipeline_group_concurrent_replay_is_bit_identical():
+@pytest.mark.parametrize("shared", [False, True])
+def test_pipeline_group_concurrent_replay_is_bit_identical(shared):
     """A c x method sweep replayed as one graph with concurrent branches gives
-    exactly the products of the member pipelines run one by one."""
+    exactly the products of the member pipelines run one by one -- also when the
+    members share one statistics stage (norms, probabilities, g_k once)."""
     M, N, sizes = workloads.cfg2(n=4000, m=60, p=50, K=12)
     Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
-    runs = [(c, meth) for c in (200, 400) for meth in ("OPL", "ONC", "ONMCNR", "UU")]
+    runs = [(c, meth) for c in (200, 400) for meth in ("OPL", "ONC", "ONMCNR", "UU", "ONU")]
     solo = [SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs]
-    group = PipelineGroup([SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs], joint=False)
+    group = PipelineGroup([SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs], joint=False,
+                          shared=shared)
+    assert (group.shared is not None) == shared
     seeds = lambda s: [seeds_from_rngs(meth, [np.random.default_rng(s + i)], len(sizes))  # noqa: E731
                        for i, (c, meth) in enumerate(runs)]
-    group.run(Md, Nd, seeds(0))
+    eager = [o.clone() for o in group.run(Md, Nd, seeds(10))]
     group.capture(Md, Nd)
     assert group.graph_launches > 0
     for s in (10, 20):
@@ -58,6 +62,50 @@ def test_pipeline_group_concurrent_replay_is_bit_identical():
             ref = pipe.run(Md, Nd, seeds(s)[i])
             assert torch.equal(outs[i], ref), runs[i]
             assert np.array_equal(group.pipes[i].columns_host(), pipe.columns_host())
+            if s == 10:
+                assert torch.equal(eager[i], ref), runs[i]
+    if shared:
+        with pytest.raises(RuntimeError):
+            group.pipes[1].run(Md, Nd, seeds(3)[1])
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_shared_stats_group_with_ssm_matches_oracle(dtype):
+    """OPL, ONC and SSM over one instance with one shared statistics stage (the
+    config-4 step): budgets, draws and scales bit-exact to the oracle, products
+    within the dtype's bar, eager and replayed."""
+    g = np.random.default_rng(44)
+    sizes = (64,) * 40
+    n = sum(sizes)
+    M = (g.standard_normal((96, n)) * np.repeat(g.uniform(0.1, 10, 40), 64)).astype(dtype)
+    N = (g.standard_normal((n, 80)) * np.repeat(g.uniform(0.1, 10, 40), 64)[:, None]).astype(dtype)
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    W, draws = 640, 10
+    group = PipelineGroup([SketchPipeline(96, n, 80, sizes, W, "OPL", dtype=tdt),
+                           SketchPipeline(96, n, 80, sizes, W, "ONC", dtype=tdt),
+                           SketchPipeline(96, n, 80, sizes, 0, "SSM", draws=draws, dtype=tdt)])
+    assert group.shared is not None and group.shared.needs_gsq
+    tol = 1e-12 if dtype == np.float64 else 1e-5
+    M64, N64 = M.astype(np.float64), N.astype(np.float64)
+    for rep, s in enumerate((5, 6, 7)):
+        if rep == 1:
+            group.capture(Md, Nd)
+        rngs = [np.random.default_rng(s + i) for i in range(3)]
+        sd = [seeds_from_rngs("OPL", [rngs[0]], 40), seeds_from_rngs("ONC", [rngs[1]], 40),
+              seeds_from_rngs("SSM", [rngs[2]], 40, draws=draws)]
+        outs = [o.cpu().numpy() for o in group.run(Md, Nd, sd)]
+        group.check()
+        for i, meth in enumerate(("OPL", "ONC")):
+            ref = O.approx_product(M64, N64, sizes, W, meth, np.random.default_rng(s + i))
+            assert np.array_equal(group.pipes[i].budgets_host()[0], ref["budgets"]), meth
+            assert np.array_equal(group.pipes[i].columns_host()[0], ref["columns"]), meth
+            assert np.array_equal(group.pipes[i].scales_host()[0], ref["scale"]), meth
+            assert rel(outs[i], ref["CD"]) < tol, meth
+        ref = O.ssm_product(M64, N64, sizes, draws, np.random.default_rng(s + 2))
+        assert np.array_equal(group.pipes[2].columns_host()[0], ref["blocks"])
+        np.testing.assert_allclose(group.pipes[2].scales_host()[0], ref["scale"], rtol=1e-13)
+        assert rel(outs[2], ref["CD"]) < tol
 
 
 @pytest.mark.parametrize("m,p", [(60, 50), (200, 130)])
@@ -218,8 +266,8 @@ def test_compressed_sketch_matches_draws_and_uncompressed_product():
     assert np.array_equal(oc.view(2, W)[1, :kd].cpu().numpy(), uniq)
 
 
-@pytest.mark.parametrize("joint", [False, True])
-def test_streamed_end_to_end_graph_matches_resident_run(joint):
+@pytest.mark.parametrize("joint,shared", [(False, False), (True, False), (False, True), (True, True)])
+def test_streamed_end_to_end_graph_matches_resident_run(joint, shared):
     """PipelineGroup.capture_host: chunked host->device transfer with the norm
     pass and OPL's segmented square sums behind it, products copied back to
     pinned host buffers -- bit-identical to the device-resident replay."""
@@ -227,7 +275,7 @@ def test_streamed_end_to_end_graph_matches_resident_run(joint):
     Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
     runs = [(c, meth) for c in (200, 400) for meth in ("OPL", "ONC", "ONMCNR")]
     mk = lambda: PipelineGroup([SketchPipeline(60, 4000, 50, sizes, c, meth, c0=120) for c, meth in runs],  # noqa: E731
-                               joint=joint)
+                               joint=joint, shared=shared)
     seeds = lambda s: [seeds_from_rngs(meth, [np.random.default_rng(s + i)], len(sizes))  # noqa: E731
                        for i, (c, meth) in enumerate(runs)]
     ref = mk()
@@ -245,3 +293,62 @@ def test_streamed_end_to_end_graph_matches_resident_run(joint):
         for o, w in zip(outs, want):
             assert np.array_equal(o.numpy(), w)
     assert np.array_equal(Mx.cpu().numpy(), M)
+
+
+def test_streamed_end_to_end_float32_shared_group():
+    """The config-4 end-to-end shape at small size: float32 host inputs streamed in
+    chunks under the shared statistics stage (norms and Gram g_k per chunk), OPL,
+    ONC and SSM members, products copied back -- bit-identical to the resident run."""
+    g = np.random.default_rng(8)
+    sizes = (64,) * 48
+    n = sum(sizes)
+    M = (g.standard_normal((72, n)) * np.repeat(g.uniform(0.1, 10, 48), 64)).astype(np.float32)
+    N = (g.standard_normal((n, 40)) * np.repeat(g.uniform(0.1, 10, 48), 64)[:, None]).astype(np.float32)
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    mk = lambda: PipelineGroup([SketchPipeline(72, n, 40, sizes, 768, "OPL", dtype=torch.float32),  # noqa: E731
+                                SketchPipeline(72, n, 40, sizes, 768, "ONC", dtype=torch.float32),
+                                SketchPipeline(72, n, 40, sizes, 0, "SSM", draws=12, dtype=torch.float32)])
+
+    def seeds(s):
+        return [seeds_from_rngs("OPL", [np.random.default_rng(s)], 48),
+                seeds_from_rngs("ONC", [np.random.default_rng(s + 1)], 48),
+                seeds_from_rngs("SSM", [np.random.default_rng(s + 2)], 48, draws=12)]
+
+    want = [o.cpu().numpy() for o in mk().run(Md, Nd, seeds(4))]
+    grp = mk()
+    Mh, Nh = torch.from_numpy(M).pin_memory(), torch.from_numpy(N).pin_memory()
+    Mx, Nx = torch.empty_like(Md), torch.empty_like(Nd)
+    outs = [torch.empty((72, 40), dtype=torch.float32).pin_memory() for _ in range(3)]
+    grp.capture_host(Mx, Nx, Mh, Nh, outs, seeds(0), n_chunks=6)
+    for _ in range(2):
+        Mx.zero_()
+        Nx.zero_()
+        grp.run_host(seeds(4))
+        torch.cuda.synchronize()
+        for o, w in zip(outs, want):
+            assert np.array_equal(o.numpy(), w)
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_nonfinite_input_raises_like_the_reference(bad, dtype):
+    """NaN/Inf in M: the pipeline reports the reference's exception (first bad
+    block's probabilities for OPL/ONC, integerize's weights for the two-step
+    plan, empty support for SSM) and never indexes outside the inputs."""
+    M, N, sizes = workloads.cfg2(n=4000, m=60, p=50, K=12)
+    M = M.astype(dtype)
+    N = N.astype(dtype)
+    col = sizes[0] + sizes[1] + 5  # a column of block 2
+    M[7, col] = bad
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    want = {"OPL": "block 2: probabilities must be finite", "ONC": "block 2: probabilities must be finite",
+            "ONU": "weights must be finite", "SSM": "probability vector has empty support"}
+    for meth, msg in want.items():
+        pipe = (SketchPipeline(60, 4000, 50, sizes, 0, "SSM", draws=5, dtype=tdt) if meth == "SSM" else
+                SketchPipeline(60, 4000, 50, sizes, 400, meth, c0=120, dtype=tdt))
+        pipe.run(Md, Nd, seeds_from_rngs(meth, [np.random.default_rng(1)], len(sizes), draws=5))
+        torch.cuda.synchronize()
+        with pytest.raises(ValueError, match=msg):
+            pipe.check()
+    torch.cuda.synchronize()
