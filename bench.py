@@ -118,14 +118,6 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- reference arm
 
-def cpu_step(M, N, sizes, runs, cfg):
-    from oracle import blockmm_oracle as O
-    t0 = time.perf_counter()
-    for cb, W, meth, c0 in runs:
-        O.approx_product(M, N, sizes, W, meth, workloads.sample_rng(cfg, cb), c0=c0)
-    return (time.perf_counter() - t0) * 1e3
-
-
 def cpu_cores():
     for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS"):
         if os.environ.get(var):
@@ -140,17 +132,20 @@ def run_reference(args):
     cfg, build, runs = workload_spec(args.workload)
     M, N, sizes = build()
     for _ in range(args.warmup):
-        cpu_step(M, N, sizes, runs, cfg)
-    times = [cpu_step(M, N, sizes, runs, cfg) for _ in range(args.steps)]
-    v = float(np.mean(times))
-    sample = f"{args.workload}: full step ({len(runs)} approx products), mean of {args.steps}"
+        cpu_staged_step(M, N, sizes, runs, cfg)
+    staged = [cpu_staged_step(M, N, sizes, runs, cfg)[0] for _ in range(args.steps)]
+    times = [sum(t.values()) for t in staged]
+    v = float(np.median(times))
+    stages = staged[int(np.argsort(times)[len(times) // 2])]
+    sample = f"{args.workload}: full step ({len(runs)} approx products), median of {args.steps}, wall clock"
     line = {
         "metric": METRIC, "value": v, "unit": "ms/step", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8(d))",
         "config": {"workload": args.workload, "runs": [f"{m}@W={W}" for _, W, m, _ in runs]},
         "impl": "reference",
-        "cpu_baseline": {"value": v, "unit": "ms/step", "cores": cpu_cores(), "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "ms/step", "cores": cpu_cores(), "kind": "port", "sample": sample,
+                         "stages_ms": stages, **cpu_info()},
         "e2e": {"value": v, "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -206,7 +201,13 @@ def run_ours(args):
     from paper_2105_04940_b200 import _lib
     from paper_2105_04940_b200.pipeline import PipelineGroup, SketchPipeline, seeds_from_rngs
 
-    cfg, build, runs = workload_spec(args.workload)
+    cfg, build, runs_all = workload_spec(args.workload)
+    if world > 1 and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    # N GPUs: the sweep's independent products are split over the ranks (strong scaling);
+    # a single-product workload (cfg3) runs as replicas
+    split = world > 1 and len(runs_all) >= world
+    runs = runs_all[rank::world] if split else runs_all
     M_h, N_h, sizes = build()
     m, n = M_h.shape
     p = N_h.shape[1]
@@ -223,8 +224,10 @@ def run_ours(args):
         return group.run(Mx, Nx, seeds)
 
     # correctness of the bench configuration itself (untimed), then graph capture
-    for pipe_out, pipe in zip(step(Md, Nd), pipes):
+    first = [o.cpu().numpy() for o in step(Md, Nd)]
+    for pipe in pipes:
         pipe.check()
+    parity = golden_parity(args.workload, runs, pipes, first)
     group.capture(Md, Nd)
     for _ in range(args.warmup):
         step(Md, Nd)
@@ -373,11 +376,13 @@ def run_ours(args):
                                          "(profiles/r1e_ncu_full_summary.csv): 0.160 GB + 4.7 MB = M + N read once"}
     line = {
         "metric": METRIC, "value": ms_step, "unit": "ms/step", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8(d))",
         "config": {"workload": args.workload, "m": m, "n": n, "p": p, "K": K,
-                   "runs": [f"{meth}@W={W}" for _, W, meth, _ in runs], "l2": "flushed (256 MB write, then 256 MB read) before each step",
-                   "parallelism": f"replicas x{world}"},
+                   "runs": [f"{meth}@W={W}" for _, W, meth, _ in runs_all], "l2": "flushed (256 MB write, then 256 MB read) before each step",
+                   "parallelism": (f"the sweep's {len(runs_all)} products split over {world} GPUs" if split else
+                                   f"replicas x{world}" if world > 1 else "1 GPU")},
+        "scaling": "strong" if split else "weak",
         "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "roofline": roofline_main,
@@ -412,7 +417,11 @@ def run_ours(args):
     if line["roofline"] is None:
         line["roofline"] = line["roofline_gemm"]
     if rank == 0:
-        line["cpu_baseline"] = cpu_baseline(M_h, N_h, sizes, runs, cfg, args)
+        if world == 1:
+            cb, oracle_out = cpu_baseline(M_h, N_h, sizes, runs, cfg, args)
+            line["cpu_baseline"] = cb
+            parity.update(oracle_parity(runs, pipes, first, oracle_out))
+        line["parity"] = parity
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -571,28 +580,145 @@ def norms_large(torch, problems=1024):
             "algorithmic_bytes": nbytes, "ms": ms, "achieved": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s"}
 
 
-def cpu_baseline(M, N, sizes, runs, cfg, args):
-    t = cpu_step(M, N, sizes, runs, cfg)
-    return {"value": t, "unit": "ms/step", "cores": cpu_cores(), "kind": "port",
-            "sample": f"{args.workload}: one full step ({len(runs)} approx products) with oracle/blockmm_oracle.py "
-                      f"(NumPy + OpenBLAS, {cpu_cores()} BLAS threads)"}
+def cpu_staged_step(M, N, sizes, runs, cfg):
+    """One step of the reference path with the oracle port (NumPy + BLAS), timed
+    per stage as SURVEY.md §8(d5) asks: the norm pass (colsq, rowsq, probabilities),
+    the plan (g_k for OPL, the pilot for two-step, integerize), the sample (child
+    streams, draws, gather of C and D) and C @ D.  Returns ({stage: ms}, outputs)."""
+    from oracle import blockmm_oracle as O
+    t = {"norms": 0.0, "plan": 0.0, "sample": 0.0, "gemm": 0.0}
+    outs = []
+    K = len(sizes)
+
+    def clock(key, fn):
+        t0 = time.perf_counter()
+        r = fn()
+        t[key] += (time.perf_counter() - t0) * 1e3
+        return r
+
+    for cb, W, meth, c0 in runs:
+        rng = workloads.sample_rng(cfg, cb)
+        # the reference recomputes the norm pass inside every allocator (plan.py:165-189)
+        cs, rs, probs, s = clock("norms", lambda: O.instance_stats(M, N, sizes))
+        if meth in ("ONU", "ONMCNR"):
+            pilot_sq, _, _, main_rng = clock("plan", lambda: O.two_step_pilot(M, N, sizes, c0, meth, rng, probs, s))
+            budgets, _ = clock("plan", lambda: O.plan_budgets("TWO_STEP", sizes, W, s=s, aux_sq=pilot_sq))
+            srng = main_rng
+        elif meth == "OPL":
+            gsq = clock("plan", lambda: O.block_product_sq(M, N, sizes))
+            budgets, _ = clock("plan", lambda: O.plan_budgets("OPL", sizes, W, s=s, aux_sq=gsq))
+            srng = rng
+        elif meth == "ONC":
+            budgets, _ = clock("plan", lambda: O.plan_budgets("ONC", sizes, W, s=s))
+            srng = rng
+        else:  # UU
+            probs = np.concatenate([np.full(nk, 1.0 / nk) for nk in sizes])
+            budgets, _ = clock("plan", lambda: O.plan_budgets("UU", sizes, W))
+            srng = rng
+        cols, _, scale, C, D = clock("sample", lambda: O.sketch(M, N, sizes, probs, budgets, srng.spawn(K)))
+        CD = clock("gemm", lambda: C @ D)
+        outs.append({"budgets": budgets, "columns": cols, "scale": scale, "CD": CD})
+    return t, outs
+
+
+def cpu_baseline(M, N, sizes, runs, cfg, args, reps=5):
+    """The CPU port of the step at all BLAS threads and at 1 thread (medians of
+    `reps`), with the stage split and the host description."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    res, out = {}, None
+    for label, lim in (("all", None), ("1", 1)):
+        ctx = threadpool_limits(limits=lim) if (threadpool_limits and lim) else None
+        if ctx is not None:
+            ctx.__enter__()
+        try:
+            runs_t = []
+            for _ in range(reps):
+                tt, o = cpu_staged_step(M, N, sizes, runs, cfg)
+                runs_t.append(tt)
+                out = out or o
+        finally:
+            if ctx is not None:
+                ctx.__exit__(None, None, None)
+        tot = [sum(r.values()) for r in runs_t]
+        med = int(np.argsort(tot)[len(tot) // 2])
+        res[label] = {"ms": float(np.median(tot)), "stages_ms": runs_t[med]}
+    cb = {"value": res["all"]["ms"], "unit": "ms/step", "cores": cpu_cores(), "kind": "port",
+          "value_1thread": res["1"]["ms"], "stages_ms": res["all"]["stages_ms"],
+          "stages_ms_1thread": res["1"]["stages_ms"], "median_of": reps,
+          "sample": f"{args.workload}: full step ({len(runs)} approx products) with oracle/blockmm_oracle.py "
+                    f"(NumPy + BLAS); medians of {reps} at all BLAS threads and at 1 thread; wall clock",
+          **cpu_info()}
+    return cb, out
+
+
+def golden_parity(workload, runs, pipes, outs):
+    """Untimed: the benched products against the reference's own outputs
+    (tests/golden/cfg2.npz, written by running the reference): budgets, draws
+    and scales bit-exact, C.D (every 7th row/column and the Frobenius norm)
+    within 1e-12."""
+    path = ROOT / "tests" / "golden" / f"{workload}.npz"
+    if workload != "cfg2" or not path.exists():
+        return {}
+    g = np.load(path)
+    worst = 0.0
+    for (cb, W, meth, c0), pipe, CD in zip(runs, pipes, outs):
+        key = f"{meth}_{W}"
+        if not (np.array_equal(pipe.budgets_host()[0], g[key + "_budgets"])
+                and np.array_equal(pipe.columns_host()[0], g[key + "_columns"])
+                and np.array_equal(pipe.scales_host()[0], g[key + "_scale"])):
+            raise RuntimeError(f"{workload} {key}: budgets / draws differ from the reference golden")
+        sub = g[key + "_CDsub"]
+        e = max(float(np.linalg.norm(CD[::7, ::7] - sub) / np.linalg.norm(sub)),
+                abs(float(np.linalg.norm(CD)) - float(g[key + "_CDfrob"])) / float(g[key + "_CDfrob"]))
+        if e > 1e-12:
+            raise RuntimeError(f"{workload} {key}: C.D rel err {e:.2e} vs the reference golden")
+        worst = max(worst, e)
+    return {"golden_ok": True, "golden": str(path.relative_to(ROOT)), "golden_cd_max_rel_err": worst}
+
+
+def oracle_parity(runs, pipes, outs, oracle_outs):
+    """Untimed: the benched products against the CPU baseline's own oracle run
+    of the same step (budgets, draws, scales bit-exact; C.D within 1e-12)."""
+    worst = 0.0
+    for (cb, W, meth, c0), pipe, CD, ref in zip(runs, pipes, outs, oracle_outs):
+        if not (np.array_equal(pipe.budgets_host()[0], ref["budgets"])
+                and np.array_equal(pipe.columns_host()[0], ref["columns"])
+                and np.array_equal(pipe.scales_host()[0], ref["scale"])):
+            raise RuntimeError(f"{meth}@W={W}: budgets / draws differ from the oracle")
+        e = float(np.linalg.norm(CD - ref["CD"]) / np.linalg.norm(ref["CD"]))
+        if e > 1e-12:
+            raise RuntimeError(f"{meth}@W={W}: C.D rel err {e:.2e} vs the oracle")
+        worst = max(worst, e)
+    return {"ok": True, "oracle_cd_max_rel_err": worst,
+            "checked": "budgets, every draw and scale bit-exact; C.D within 1e-12 (float64)"}
 
 
 # ---------------------------------------------------------------- float32 device workloads (cfg4, cfg5)
 
-def device_data(torch, name):
+def device_data(torch, name, problems=None):
     """Seeded float32 instances generated on the GPU (numpy would take minutes
-    for 2 x 8.6e9 normals); distributions per SURVEY.md §8(d)."""
-    g = torch.Generator(device="cuda").manual_seed(workloads.ROOT + int(name[-1]))
+    for 2 x 8.6e9 normals); distributions per SURVEY.md §8(d).  cfg5 is
+    generated in chunks of 256 problems, each chunk from its own seed, so a rank
+    of a sharded run regenerates exactly its problems (`problems` = (lo, hi))."""
     if name == "cfg5":
-        B, m, n, p, K = 4096, 256, 4096, 256, 64
-        M = torch.empty((B, m, n), dtype=torch.float32, device="cuda")
-        N = torch.empty((B, n, p), dtype=torch.float32, device="cuda")
-        for b0 in range(0, B, 512):
-            sl = slice(b0, b0 + 512)
-            M[sl].normal_(generator=g).mul_(torch.randn((512, 1, n), generator=g, device="cuda").exp_())
-            N[sl].normal_(generator=g).mul_(torch.randn((512, n, 1), generator=g, device="cuda").exp_())
-        return M, N, (n // K,) * K, B
+        B, m, n, p, K, CH = 4096, 256, 4096, 256, 64, 256
+        lo, hi = problems or (0, B)
+        M = torch.empty((hi - lo, m, n), dtype=torch.float32, device="cuda")
+        N = torch.empty((hi - lo, n, p), dtype=torch.float32, device="cuda")
+        for c in range(lo // CH, (hi + CH - 1) // CH):
+            g = torch.Generator(device="cuda").manual_seed(workloads.ROOT * 1000 + 50000 + c)
+            Mc = torch.empty((CH, m, n), dtype=torch.float32, device="cuda").normal_(generator=g)
+            Mc.mul_(torch.randn((CH, 1, n), generator=g, device="cuda").exp_())
+            Nc = torch.empty((CH, n, p), dtype=torch.float32, device="cuda").normal_(generator=g)
+            Nc.mul_(torch.randn((CH, n, 1), generator=g, device="cuda").exp_())
+            a, b = max(lo, c * CH), min(hi, c * CH + CH)
+            M[a - lo:b - lo] = Mc[a - c * CH:b - c * CH]
+            N[a - lo:b - lo] = Nc[a - c * CH:b - c * CH]
+            del Mc, Nc
+        return M, N, (n // K,) * K, hi - lo
     M, N = cfg4_shard(torch, (0, 16384), (0, 16384))
     return M, N, (262144 // 4096,) * 4096, 1
 
@@ -626,71 +752,136 @@ def cfg4_shard(torch, rows, cols):
 
 def run_cfg4_sharded(args):
     """Config 4 with M's rows and N's columns sharded over the torchrun group
-    (SURVEY §8(e)); the only exchanges are the norm partials (all-gather +
-    ordered sum).  value = ms per approximate product of the whole problem
-    (strong scaling, max over ranks)."""
+    (SURVEY.md §8(e), strong scaling): the same step as run_cfg4 (OPL, ONC,
+    SSM over one instance) through distributed.ShardedApproxProduct.  The only
+    exchanges are the exact norm pass (chained colsq stages, tree-combined
+    rowsq: plans and draws bit-identical to one GPU) and the K-length g_k^2
+    partials.  value = ms per step of the whole problem, max over ranks."""
     import torch
     import torch.distributed as dist
     from paper_2105_04940_b200.distributed import ShardLayout, ShardedApproxProduct
-    from paper_2105_04940_b200.pipeline import seeds_from_keys
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    m, n, p, K, W = 16384, 262144, 16384, 4096, 32768
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    m, n, p, K = 16384, 262144, 16384, 4096
+    sizes = (n // K,) * K
     L = ShardLayout(world, rank, m, n, p)
     M, N = cfg4_shard(torch, L.rows, L.cols)
-    sh = ShardedApproxProduct(L, (n // K,) * K, W, "ONC", dtype=torch.float32)
-    seeds = seeds_from_keys("ONC", workloads.ROOT, (4, 1), [0], K)
-    words, first = seeds.main.words[0], int(seeds.main.first[0])
-    sh.run(M, N, words, first)
+    sh = ShardedApproxProduct(L, sizes, [(meth, w) for meth, w, _ in CFG4_RUNS], dtype=torch.float32)
+    tiles = sh.run(M, N, cfg4_seeds(K))
     sh.check()
+    # every rank drew the single-GPU sample: compare the draws across ranks (identical bits)
+    cols = torch.cat([q.column[:q.W] if q.method != "SSM" else q.blk for q in sh.pipes]).contiguous()
+    allc = [torch.empty_like(cols) for _ in range(world)]
+    dist.all_gather(allc, cols)
+    same_draws = all(torch.equal(c, cols) for c in allc)
     for _ in range(args.warmup):
-        sh.run(M, N, words, first)
+        sh.run(M, N, cfg4_seeds(K))
+    torch.cuda.synchronize()
     times = []
     with ClockSampler(local) as clocks:
         dist.barrier()
         torch.cuda.synchronize()
         for _ in range(args.steps):
+            seeds = cfg4_seeds(K)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            sh.run(M, N, words, first)
+            sh.run(M, N, seeds)
             e1.record()
             times.append((e0, e1))
         torch.cuda.synchronize()
         dist.barrier()
     ms = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in times]))], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    # e2e: this rank's shard from pinned host memory, its tiles back, every step
+    M_pin = torch.empty(M.shape, dtype=M.dtype).pin_memory()
+    N_pin = torch.empty(N.shape, dtype=N.dtype).pin_memory()
+    M_pin.copy_(M)
+    N_pin.copy_(N)
+    outs = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in tiles]
+    e2e = []
+    for it in range(1 + args.steps):
+        seeds = cfg4_seeds(K)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        M.copy_(M_pin, non_blocking=True)
+        N.copy_(N_pin, non_blocking=True)
+        for o, t in zip(outs, sh.run(M, N, seeds)):
+            o.copy_(t, non_blocking=True)
+        torch.cuda.synchronize()
+        if it >= 1:
+            e2e.append((time.perf_counter() - t0) * 1e3)
+    e2e_t = torch.tensor([float(np.mean(e2e))], device="cuda")
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": float(ms.item()), "unit": "ms/step", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": float(ms.item()), "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 (TF32 + BF16 split-operand tensor, f64 plan)", "data": "synthetic (chunk-seeded on device)",
-            "config": {"workload": "cfg4-sharded", "grid": list(L.grid), "m": m, "n": n, "p": p, "K": K, "W": W,
-                       "parallelism": f"M rows x N cols over {world} GPUs; colsq/rowsq exchange only"},
+            "vs_baseline": None, "dtype": "f32 (TF32 + BF16 split-operand tensor contraction, f64 norms/plan)",
+            "data": "synthetic (chunk-seeded on device: every rank regenerates exactly its slice)",
+            "config": {"workload": "cfg4", "grid": list(L.grid), "m": m, "n": n, "p": p, "K": K, "block": 64,
+                       "runs": ["OPL@W=32768", "ONC@W=32768", "SSM@draws=512"],
+                       "parallelism": f"M rows x N cols over {world} GPUs ({L.grid[0]}x{L.grid[1]}); exact norm "
+                                      "exchange + g_k^2 partials (NCCL all-gather)",
+                       "l2": "inputs >> L2"},
+            "draws_identical_on_all_ranks": bool(same_draws),
+            "gpu_launches": None,
+            "e2e": {"value": float(e2e_t.item()), "unit": "ms/step",
+                    "h2d_bytes_per_step": int(M.numel() * 4 + N.numel() * 4) * world,
+                    "d2h_bytes_per_step": int(sum(t.numel() for t in tiles) * 4) * world,
+                    "api": "ShardedApproxProduct.run on each rank's shard copied from pinned host memory"},
             "clocks": clocks.summary()}), flush=True)
     dist.destroy_process_group()
     return 0
 
 
+def relaunch_distributed(args):
+    """`--gpus N` (N > 1) outside torchrun: start N ranks of this same command
+    with torch.distributed.run on 127.0.0.1 (NCCL INFO logs to stderr so the
+    ranks can be counted)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"),
+               NCCL_DEBUG_FILE=os.environ.get("NCCL_DEBUG_FILE", "/dev/stderr"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def run_device(args):
+    """cfg5: 4096 independent problems (per-problem seeds).  Under torchrun the
+    problems are split over the ranks (no collective; weak in data, the whole
+    job's 4096 problems at every N: strong scaling), value = max over ranks."""
     import torch
+    import torch.distributed as dist
     from paper_2105_04940_b200 import _lib
     from paper_2105_04940_b200.pipeline import SketchPipeline, seeds_from_keys
     from paper_2105_04940_b200.analysis import sq_diff
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     name = args.workload
     cfg = int(name[-1])
-    Md, Nd, sizes, B = device_data(torch, name)
+    lo, hi = (rank * 4096 // world, (rank + 1) * 4096 // world)
+    Md, Nd, sizes, B = device_data(torch, name, (lo, hi))
     m, n = Md.shape[-2:]
     p = Nd.shape[-1]
     K = len(sizes)
     W = 1024 if name == "cfg5" else 32768
     pipe = SketchPipeline(m, n, p, sizes, W, "ONC", batch=B, dtype=torch.float32)
-    keys = np.arange(B)
+    keys = np.arange(lo, hi)
 
     def seeds():
         return seeds_from_keys("ONC", workloads.ROOT, (cfg, 1), keys, K)
@@ -702,7 +893,10 @@ def run_device(args):
         pipe.run(Md, Nd, seeds())
     torch.cuda.synchronize()
     times = []
-    with ClockSampler() as clocks:
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         for _ in range(args.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -710,7 +904,13 @@ def run_device(args):
             e1.record()
             times.append((e0, e1))
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
     ms_step = float(np.mean([a.elapsed_time(b) for a, b in times]))
+    if world > 1:
+        t = torch.tensor([ms_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
 
     # per-kernel device times (events on the launching stream)
     lib, st = _lib.load(), _lib.stream_ptr()
@@ -786,11 +986,11 @@ def run_device(args):
         fro = float(torch.linalg.norm(Md[:rows].double()) * torch.sqrt(pipe.rowsq.sum()))
         scope = f"first {rows} rows of C.D"
     line = {
-        "metric": METRIC, "value": ms_step, "unit": "ms/step", "n_gpus": 1, "steps": args.steps,
+        "metric": METRIC, "value": ms_step, "unit": "ms/step", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 (TF32 + BF16 split-operand tensor, f64 plan)",
         "data": "synthetic (seeded torch generator on device, SURVEY.md §8(d) distributions)",
-        "config": {"workload": name, "batch": B, "m": m, "n": n, "p": p, "K": K, "W": W, "method": "ONC",
+        "config": {"workload": name, "batch": 4096, "batch_per_gpu": B, "m": m, "n": n, "p": p, "K": K, "W": W, "method": "ONC",
                    "distinct_columns_mean": float(kcounts.mean()),
                    "l2": f"inputs {norm_bytes / 1e9:.1f} GB >> L2"},
         "gpu_launches": int(pipe.graph_launches),
@@ -813,7 +1013,13 @@ def run_device(args):
         "rel_err_baseline_metric": float(np.sqrt(err_sq) / fro), "error_scope": scope,
         "clocks": clocks.summary(),
     }
-    print(json.dumps(line), flush=True)
+    if world > 1:
+        line["scaling"] = "strong"
+        line["config"]["parallelism"] = f"the 4096 problems split over {world} GPUs, no collective"
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
@@ -1363,6 +1569,8 @@ def run_mc(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
     if args.workload == "mc":
         return run_mc(args)
     if args.impl == "reference":

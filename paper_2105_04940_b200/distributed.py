@@ -2,34 +2,44 @@
 
 SURVEY.md §8(e): output tiles of C.D need only the replicated sample (indices,
 scales) plus the local M rows / N columns, so the data path has no
-communication.  The exchanges are small and happen once per call:
+communication.  Ranks form a Gr x Gc grid; rank (a, b) = a * Gc + b owns
+M[rows_a, :] and N[:, cols_b] and produces CD[rows_a, cols_b].  The exchanges
+are small and happen once per call (C1-C3 of the survey):
 
-  C1  colsq (n) and rowsq (n) partial sums of squares      -> every rank
-  C2  K-length g_k^2 partials (OPL) / pilot^2 partials      -> every rank
-  C3  two error scalars (verification only)
+  C1  the norm pass.  Made EXACT -- every rank ends with the bits a single GPU
+      computes, so plans and draws are bit-identical at any GPU count:
+      * colsq is NumPy's sequential chain over the rows of M (matrix.py:107-109).
+        The columns are split into Gc slabs; rank (a, b) continues the chain of
+        column slab b over its rows_a, starting from the accumulator rank
+        (a-1, b) handed on (Gr stages, one all-gather each): the chain runs over
+        rows 0..m-1 in order, exactly as on one device.
+      * rowsq is NumPy's pairwise tree over a row of N (matrix.py:112-114).  The
+        column shards cols_b are cut at nodes of that tree (pairwise_shards), so
+        rank (a, b) sums complete subtrees for the rows of slab a, and the
+        partials are combined in the tree's own order (tree_combine).
+      Every byte of M and N is read once across the job.
+  C2  K-length partials of the block-product norms g_k^2 (OPL) and of the
+      two-step pilot norms over the output tiles: ||X||_F^2 of the whole
+      product is the sum of its tiles' (an all-gather and a fixed rank-order
+      sum, so every rank holds identical bits whatever algorithm NCCL picks).
+  C3  two error scalars (verification only).
 
-Ranks form a Gr x Gc grid; rank (a, b) owns M[rows_a, :] and N[:, cols_b] and
-produces CD[rows_a, cols_b].  The norm-pass *work* is split further so each
-byte of M and N is read once across the job: rank (a, b) sums squares over
-the b-th sub-slab of rows_a (M) and the a-th sub-slab of cols_b (N).
-
-Exchanges are an all-gather of the partials followed by a fixed rank-order
-sum, so every rank holds identical bits (identical plans and draws without a
-broadcast) and results do not depend on the collective algorithm NCCL picks.
-Sharded partial sums change the float64 rounding of colsq/rowsq at the 1e-16
-level, so sampled indices match the single-GPU run except with probability
-~1e-8 per problem; they are identical across ranks always.
+Plans, child streams and draws are then computed redundantly on every rank from
+identical inputs, so no broadcast is needed.  Grids with Gc not a power of two
+(world sizes other than 1, 2, 4, 8, ...) or widths whose tree cannot be cut
+into Gc subtrees fall back to balanced column shards and a rank-ordered sum of
+row partials (deterministic, equal on all ranks, within rounding of the
+single-GPU norms).
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import _lib
-from .plan import segsq_engine
 
 
 def grid_shape(world: int) -> tuple:
@@ -45,6 +55,37 @@ def shard_range(total: int, parts: int, idx: int) -> tuple:
     base, extra = divmod(total, parts)
     lo = idx * base + min(idx, extra)
     return lo, lo + base + (1 if idx < extra else 0)
+
+
+def _pw_split(length: int) -> int:
+    """NumPy's pairwise split point (numpy/core/src/umath/loops_utils.h: n2 = n/2, n2 -= n2 % 8)."""
+    n2 = length // 2
+    return n2 - n2 % 8
+
+
+def pairwise_shards(p: int, parts: int):
+    """Cut [0, p) into `parts` contiguous pieces that are nodes of NumPy's
+    pairwise summation tree over a row of width p (parts a power of two and
+    every cut node longer than the 128-element leaf), or None if impossible."""
+    if parts < 1 or parts & (parts - 1):
+        return None
+    segs = [(0, p)]
+    while len(segs) < parts:
+        nxt = []
+        for lo, hi in segs:
+            if hi - lo <= 128:
+                return None
+            h = _pw_split(hi - lo)
+            nxt += [(lo, lo + h), (lo + h, hi)]
+        segs = nxt
+    return segs
+
+
+def tree_combine(parts: list):
+    """Combine subtree sums in the pairwise tree's order: ((p0 + p1) + (p2 + p3)) ..."""
+    while len(parts) > 1:
+        parts = [parts[i] + parts[i + 1] for i in range(0, len(parts), 2)]
+    return parts[0]
 
 
 @dataclass(frozen=True)
@@ -65,186 +106,181 @@ class ShardLayout:
         return divmod(self.rank, gc)  # (a, b)
 
     @property
+    def exact_rows(self) -> bool:
+        """Column shards are pairwise-tree nodes (rowsq combines exactly)."""
+        return pairwise_shards(self.p, self.grid[1]) is not None
+
+    def col_shard(self, b: int) -> tuple:
+        segs = pairwise_shards(self.p, self.grid[1])
+        return segs[b] if segs is not None else shard_range(self.p, self.grid[1], b)
+
+    def row_shard(self, a: int) -> tuple:
+        return shard_range(self.m, self.grid[0], a)
+
+    @property
     def rows(self):
-        gr, _ = self.grid
-        return shard_range(self.m, gr, self.coords[0])
+        return self.row_shard(self.coords[0])
 
     @property
     def cols(self):
-        _, gc = self.grid
-        return shard_range(self.p, gc, self.coords[1])
+        return self.col_shard(self.coords[1])
 
-    @property
-    def norm_rows(self):
-        """Rows of the local M slab whose squares this rank sums (global row ids)."""
-        _, gc = self.grid
-        lo, hi = self.rows
-        a, b = self.coords
-        s0, s1 = shard_range(hi - lo, gc, b)
-        return lo + s0, lo + s1
+    def colsq_slab(self, b: int) -> tuple:
+        """Columns of M whose chains rank (., b) carries (32-column aligned)."""
+        units = (self.n + 31) // 32
+        lo, hi = shard_range(units, self.grid[1], b)
+        return min(self.n, 32 * lo), min(self.n, 32 * hi)
 
-    @property
-    def norm_cols(self):
-        """Columns of the local N slab whose squares this rank sums (global column ids)."""
-        gr, _ = self.grid
-        lo, hi = self.cols
-        a, b = self.coords
-        s0, s1 = shard_range(hi - lo, gr, a)
-        return lo + s0, lo + s1
+    def rowsq_slab(self, a: int) -> tuple:
+        """Rows of N whose partial row sums rank (a, .) computes."""
+        return shard_range(self.n, self.grid[0], a)
+
+
+def _world(group=None) -> int:
+    return dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+
+
+def _all_gather(buf: torch.Tensor, group=None) -> torch.Tensor:
+    """(world, len) gathered copy of every rank's `buf` (gloo: staged through host)."""
+    world = _world(group)
+    if world == 1:
+        return buf[None]
+    src = buf.contiguous()
+    if dist.get_backend(group) == "gloo":  # host collectives: stage device buffers through host memory
+        src = src.cpu()
+        parts = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(parts, src, group=group)
+        return torch.stack(parts).to(buf.device)
+    out = torch.empty((world,) + tuple(src.shape), dtype=src.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src, group=group)
+    return out
 
 
 def exchange_sum(partial: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather `partial` from every rank and sum in rank order (deterministic,
     identical on all ranks)."""
-    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
-    if world == 1:
+    if _world(group) == 1:
         return partial
-    parts = [torch.empty_like(partial) for _ in range(world)]
-    dist.all_gather(parts, partial.contiguous(), group=group)
+    parts = _all_gather(partial, group)
     acc = parts[0].clone()
     for t in parts[1:]:
         acc += t
     return acc
 
 
+def _kernel_colsq(Mslab: torch.Tensor, acc: torch.Tensor, accumulate: bool) -> None:
+    rows, cols = Mslab.shape
+    if rows == 0 or cols == 0:
+        return
+    _lib.call("bmm_norms", _lib.matrix_dtype(Mslab), Mslab.data_ptr(), rows, cols, Mslab.stride(0), 0, None, 0, 0,
+              0, 1, int(accumulate), acc.data_ptr(), None, _lib.stream_ptr())
+
+
+def _kernel_rowsq(Nslab: torch.Tensor, out: torch.Tensor) -> None:
+    rows, cols = Nslab.shape
+    if rows == 0 or cols == 0:
+        return
+    _lib.call("bmm_norms", _lib.matrix_dtype(Nslab), None, 0, rows, 0, 0, Nslab.data_ptr(), cols, Nslab.stride(0),
+              0, 1, 0, None, out.data_ptr(), _lib.stream_ptr())
+
+
+@dataclass
+class ShardExchange:
+    """The cross-rank steps of one sharded pipeline (see the module docstring).
+    colsq_fn / rowsq_fn are the per-rank norm kernels (the C-ABI by default;
+    the CPU tests substitute the oracle's NumPy chains to check the exchange)."""
+
+    layout: ShardLayout
+    group: object = None
+    colsq_fn: object = field(default=_kernel_colsq)
+    rowsq_fn: object = field(default=_kernel_rowsq)
+
+    def norms(self, M_local: torch.Tensor, N_local: torch.Tensor, colsq: torch.Tensor, rowsq: torch.Tensor) -> None:
+        """Full-length colsq and rowsq (bit-identical to one device when the
+        layout is exact) from this rank's M rows and N columns."""
+        L = self.layout
+        gr, gc = L.grid
+        a, b = L.coords
+        n = L.n
+        dev = colsq.device
+        cmax = max(hi - lo for lo, hi in (L.colsq_slab(j) for j in range(gc)))
+        rmax = max(hi - lo for lo, hi in (L.rowsq_slab(j) for j in range(gr)))
+        buf = torch.zeros(cmax + rmax, dtype=torch.float64, device=dev)
+        acc, rpart = buf[:cmax], buf[cmax:]
+        r0, r1 = L.rowsq_slab(a)
+        self.rowsq_fn(N_local[r0:r1], rpart[:r1 - r0])
+        c0, c1 = L.colsq_slab(b)
+        gathered0 = None
+        for j in range(gr):
+            if a == j:
+                self.colsq_fn(M_local[:, c0:c1], acc[:c1 - c0], j > 0)
+            g = _all_gather(buf if j == 0 else acc, self.group)
+            if j == 0:
+                gathered0 = g
+            if j + 1 < gr:  # the next row group continues the chains of the same column slab
+                acc.copy_(g[(j * gc + b), :cmax])
+        for bb in range(gc):
+            lo, hi = L.colsq_slab(bb)
+            colsq[lo:hi] = g[(gr - 1) * gc + bb, :hi - lo]
+        for aa in range(gr):
+            lo, hi = L.rowsq_slab(aa)
+            parts = [gathered0[aa * gc + bb, cmax:cmax + hi - lo] for bb in range(gc)]
+            rowsq[lo:hi] = tree_combine(parts) if L.exact_rows else exchange_sum_list(parts)
+
+    def sum_(self, t: torch.Tensor) -> None:
+        """In place: the rank-ordered sum of every rank's partial `t`."""
+        t.copy_(exchange_sum(t, self.group))
+
+
+def exchange_sum_list(parts: list):
+    acc = parts[0].clone()
+    for t in parts[1:]:
+        acc = acc + t
+    return acc
+
+
 class ShardedApproxProduct:
-    """One approximate product (methods ONC / OPL / UU) of a problem whose M rows
-    and N columns are sharded over the process group; returns this rank's
-    CD[rows_a, cols_b] tile.  The device steps are the same C-ABI kernels as
-    the single-GPU pipeline."""
+    """The sharded form of a PipelineGroup over ONE instance: approximate
+    products (any of OPL, ONC, UU, ONU, ONMCNR, SSM) of a problem whose M rows
+    and N columns are sharded over the process group.  Each member is a
+    SketchPipeline of this rank's tile (m_a x n x p_b) whose statistics go
+    through a ShardExchange; run() returns this rank's CD[rows_a, cols_b] tile
+    for each member.  Buffers are allocated once (construction), the kernels
+    are those of the single-GPU pipeline.
 
-    def __init__(self, layout: ShardLayout, sizes, c: int, method: str = "ONC", dtype=torch.float32,
-                 cap: bool = True, group=None):
-        if method not in ("ONC", "OPL", "UU"):
-            raise ValueError("sharded path supports ONC, OPL and UU")
-        self.L, self.sizes, self.c, self.method, self.cap, self.group = layout, tuple(sizes), int(c), method, cap, group
-        self.dtype = dtype
-        self.lib = _lib.load()
-        dev = _lib.device()
-        K, n = len(self.sizes), layout.n
-        self.K = K
-        off = np.zeros(K + 1, dtype=np.int64)
-        np.cumsum(self.sizes, out=off[1:])
-        self.offsets = torch.as_tensor(off, device=dev)
-        self.sizes_d = torch.as_tensor(np.asarray(self.sizes, np.int64), device=dev)
-        f64 = dict(dtype=torch.float64, device=dev)
-        i64 = dict(dtype=torch.int64, device=dev)
-        self.norms_part = torch.zeros(2 * n, **f64)
-        self.probs = torch.empty(n, **f64)
-        self.s = torch.empty(K, **f64)
-        self.cum = torch.empty(n, **f64)
-        self.last = torch.empty(K, **i64)
-        self.budgets = torch.empty(K, **i64)
-        self.col_off = torch.empty(K + 1, **i64)
-        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.diag = torch.zeros(1, **i64)
-        self.c_arr = torch.full((1,), self.c, **i64)
-        self.ws_budget = _lib.workspace(self.lib.bmm_budgets_workspace(K))
-        self.states = torch.empty(4 * K, **i64)
-        W = self.c
-        self.column = torch.zeros(W, **i64)
-        self.prob = torch.empty(W, **f64)
-        self.scale = torch.empty(W, **f64)
-        ma = layout.rows[1] - layout.rows[0]
-        pb = layout.cols[1] - layout.cols[0]
-        self.ma, self.pb = ma, pb
-        if method == "UU":
-            u = np.concatenate([np.full(nk, 1.0 / nk) for nk in self.sizes])
-            self.uprobs = torch.as_tensor(u, device=dev)
+    runs: [(method, c)] (SSM: c = number of whole-block draws); c0 for two-step."""
 
-    def _c(self, name, *args):
-        rc = getattr(self.lib, name)(*args)
-        if rc < 0:
-            raise RuntimeError(f"{name} failed ({rc}): {self.lib.bmm_last_error().decode()}")
-
-    def run(self, M_local: torch.Tensor, N_local: torch.Tensor, words: np.ndarray, first: int) -> torch.Tensor:
-        L, K, n, W = self.L, self.K, self.L.n, self.c
-        st = _lib.stream_ptr()
-        P = lambda t: t.data_ptr()  # noqa: E731
-        dt = _lib.matrix_dtype(M_local)
-        r0, r1 = L.rows
-        c0, c1 = L.cols
-        nr0, nr1 = L.norm_rows
-        nc0, nc1 = L.norm_cols
-        # C1: partial sums of squares over this rank's share of the bytes
-        colsq, rowsq = self.norms_part[:n], self.norms_part[n:]
-        colsq.zero_()
-        rowsq.zero_()
-        Mpart = M_local[nr0 - r0:nr1 - r0]
-        Npart = N_local[:, nc0 - c0:nc1 - c0]
-        if Mpart.shape[0] > 0:
-            self._c("bmm_norms", dt, P(Mpart), Mpart.shape[0], n, M_local.stride(0), 0, None, 0, 0, 0, 1, 0,
-                    P(colsq), None, st)
-        if Npart.shape[1] > 0:
-            self._c("bmm_norms", dt, None, 0, n, 0, 0, Npart.data_ptr(), Npart.shape[1], N_local.stride(0), 0, 1, 0,
-                    None, P(rowsq), st)
-        full = exchange_sum(self.norms_part, self.group)
-        colsq, rowsq = full[:n], full[n:]
-        self._c("bmm_block_probs", P(colsq), P(rowsq), n, P(self.offsets), K, 1, max(self.sizes), P(self.probs), P(self.s), None,
-                P(self.cum), P(self.last), st)
-        aux = None
-        if self.method == "OPL":
-            # C2: g_k^2 partials of this rank's output tile
-            if segsq_engine(max(self.sizes), M_local.shape[0], N_local.shape[1], n) == "i8":
-                A, B = M_local.contiguous(), N_local.contiguous()
-                if A.dtype != B.dtype:
-                    A, B = A.double(), B.double()
-                gpart = torch.empty(K, dtype=torch.float64, device=A.device)
-                ws = _lib.workspace(self.lib.bmm_segsq_i8_workspace(A.shape[0], B.shape[1], n, K, 1))
-                self._c("bmm_segsq_i8", _lib.matrix_dtype(A), P(A), A.stride(0), 0, P(B), B.stride(0), 0,
-                        A.shape[0], B.shape[1], n, P(self.offsets), K, 0, 1, P(gpart), P(ws), ws.numel(), st)
+    def __init__(self, layout: ShardLayout, sizes, runs, *, dtype=torch.float32, c0: int = 0, cap: bool = True,
+                 group=None):
+        from .pipeline import PipelineGroup, SketchPipeline
+        self.L, self.sizes, self.runs = layout, tuple(int(s) for s in sizes), [(str(mt), int(c)) for mt, c in runs]
+        if sum(self.sizes) != layout.n:
+            raise ValueError("partition does not cover n")
+        self.exchange = ShardExchange(layout, group)
+        r0, r1 = layout.rows
+        b0, b1 = layout.cols
+        self.ma, self.pb = r1 - r0, b1 - b0
+        pipes = []
+        for meth, c in self.runs:
+            if meth == "SSM":
+                q = SketchPipeline(self.ma, layout.n, self.pb, self.sizes, 0, "SSM", draws=c, dtype=dtype, cap=cap)
             else:
-                A = M_local.double() if M_local.dtype != torch.float64 else M_local
-                B = N_local.double().contiguous() if N_local.dtype != torch.float64 else N_local.contiguous()
-                gpart = torch.empty(K, dtype=torch.float64, device=A.device)
-                ws = _lib.workspace(self.lib.bmm_segsq_f64_workspace(A.shape[0], B.shape[1], K, 1))
-                self._c("bmm_segsq_f64", P(A), A.stride(0), 0, P(B), B.stride(0), 0, A.shape[0], B.shape[1],
-                        P(self.offsets), K, 0, 1, P(gpart), P(ws), ws.numel(), st)
-            aux = exchange_sum(gpart, self.group)
-        rule = {"ONC": _lib.RULE_ONC, "OPL": _lib.RULE_OPL, "UU": _lib.RULE_UU}[self.method]
-        self._c("bmm_budgets", rule, P(self.s) if rule != _lib.RULE_UU else None, P(aux) if aux is not None else None,
-                P(self.sizes_d), None, None, K, 1, P(self.c_arr), int(self.cap), P(self.budgets), P(self.col_off),
-                P(self.status), P(self.diag), None, P(self.ws_budget), st)
-        probs = self.probs
-        if self.method == "UU":
-            probs = self.uprobs
-            self._c("bmm_block_cdf", P(probs), P(self.offsets), K, 1, n, P(self.cum), P(self.last), st)
-        words_d = torch.as_tensor(np.ascontiguousarray(words, dtype=np.uint32).view(np.int32), device=M_local.device)
-        first_d = torch.as_tensor(np.array([first], dtype=np.int64), device=M_local.device)
-        self._c("bmm_seed_streams", P(words_d), len(words), P(first_d), K, 1, P(self.states), st)
-        self._c("bmm_sample", P(probs), P(self.cum), P(self.last), P(self.offsets), K, 1, n, max(self.sizes),
-                P(self.budgets), P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
-        ma, pb = self.ma, self.pb
-        # compressed sketch (one term per distinct drawn column), as SketchPipeline
-        dev = M_local.device
-        kcol = torch.empty(W, dtype=torch.int64, device=dev)
-        ksc = torch.empty(W, dtype=torch.float64, device=dev)
-        kcnt = torch.empty(1, dtype=torch.int64, device=dev)
-        wsc = _lib.workspace(self.lib.bmm_compress_workspace(n, 1))
-        self._c("bmm_compress_sketch", P(self.column), P(self.scale), W, W, n, 1, P(wsc), wsc.numel(), P(kcol),
-                P(ksc), P(kcnt), st)
-        if M_local.dtype == torch.float32 and W % 8 == 0:
-            a_hi = torch.empty(ma * W, dtype=torch.float32, device=dev)
-            a_x = torch.empty_like(a_hi)
-            b_hi = torch.empty(pb * W, dtype=torch.float32, device=dev)
-            b_x = torch.empty_like(b_hi)
-            Nc = N_local.contiguous()
-            self._c("bmm_gather_f32split_dk", dt, P(M_local), M_local.stride(0), 0, P(Nc), Nc.stride(0), 0, ma, pb,
-                    P(kcol), P(ksc), W, W, P(kcnt), 1, P(a_hi), P(a_x), P(b_hi), P(b_x), st)
-            out = torch.empty((ma, pb), dtype=torch.float32, device=dev)
-            self._c("bmm_gemm_f32split_dk", P(a_hi), P(a_x), P(b_hi), P(b_x), ma, pb, W, P(kcnt), 1, P(out), pb, 0,
-                    st)
-            return out
-        C = torch.empty((ma, W), dtype=torch.float64, device=dev)
-        D = torch.empty((W, pb), dtype=torch.float64, device=dev)
-        self._c("bmm_gather_dk", dt, _lib.BMM_F64, P(M_local), M_local.stride(0), 0, P(N_local), N_local.stride(0),
-                0, ma, pb, P(kcol), P(ksc), W, W, P(kcnt), 1, P(C), W, 0, P(D), pb, 0, st)
-        out = torch.empty((ma, pb), dtype=torch.float64, device=dev)
-        ws = _lib.workspace(self.lib.bmm_gemm_f64_workspace(ma, pb, W, 1))
-        self._c("bmm_gemm_f64_dk", P(C), W, 0, P(D), pb, 0, ma, pb, W, P(kcnt), 1, P(out), pb, 0, P(ws), ws.numel(),
-                st)
-        return out
+                q = SketchPipeline(self.ma, layout.n, self.pb, self.sizes, c, meth, dtype=dtype, c0=c0, cap=cap)
+            q.exchange = self.exchange
+            pipes.append(q)
+        self.group = PipelineGroup(pipes, joint=False, shared=len(pipes) > 1)
+        self.pipes = pipes
 
-    def check(self):
-        from .plan import raise_status
-        raise_status(int(self.status.item()), int(self.diag.item()), self.c)
+    def run(self, M_local: torch.Tensor, N_local: torch.Tensor, seeds: list) -> list:
+        """This rank's tiles CD[rows_a, cols_b], one per run (seeds: one CallSeeds
+        per run, identical on every rank)."""
+        if tuple(M_local.shape) != (self.ma, self.L.n) or tuple(N_local.shape) != (self.L.n, self.pb):
+            raise ValueError("local shards do not match the layout")
+        if len(self.pipes) == 1:
+            q = self.pipes[0]
+            q.set_seeds(seeds[0])
+            return [q.launch(M_local, N_local)]
+        return self.group.run(M_local, N_local, seeds)
+
+    def check(self) -> None:
+        self.group.check()

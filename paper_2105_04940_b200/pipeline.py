@@ -110,7 +110,12 @@ def _stats_launch(obj, M: torch.Tensor, N: torch.Tensor, chunks, *, probs: bool,
     ldm, ldn = M.stride(-2), N.stride(-2)
     P = lambda t: t.data_ptr()  # noqa: E731
     seg_done = False
-    if chunks is None:
+    if getattr(obj, "exchange", None) is not None:
+        # one rank of a sharded product: exact cross-rank norm pass (distributed.ShardExchange)
+        if B != 1 or chunks is not None:
+            raise ValueError("sharded pipelines run one problem, without chunked transfer")
+        obj.exchange.norms(M, N, obj.colsq, obj.rowsq)
+    elif chunks is None:
         obj._c("bmm_norms", dt, P(M), m, n, ldm, sM, P(N), p, ldn, sN, B, 0, P(obj.colsq), P(obj.rowsq), st)
     else:
         if B != 1 or not probs:
@@ -265,6 +270,7 @@ class SketchPipeline:
         self.timeline = None
         self.stamps = None  # (device int64 buffer, [entry names]) for tools/timeline.py
         self.shared = None        # SharedStats of the PipelineGroup that owns this member's statistics
+        self.exchange = None      # distributed.ShardExchange when this pipeline computes one rank's tile
         self._group_active = False  # set while the owning group enqueues this member
 
     # ------------------------------------------------------------------ steps
@@ -342,6 +348,8 @@ class SketchPipeline:
 
     def capture(self, M: torch.Tensor, N: torch.Tensor) -> None:
         """Record the launch sequence for these input buffers as a CUDA graph."""
+        if self.exchange is not None:
+            raise RuntimeError("a sharded pipeline exchanges through host collectives: run it eagerly")
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
@@ -430,6 +438,8 @@ class SketchPipeline:
                 self._c("bmm_segsq_f64_gather", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p,
                         P(self.p_column), P(self.p_scale), self.W0, P(self.p_coloff), K, K + 1, B,
                         P(self.pilot_sq), P(self.ws_seg), self.ws_seg.numel(), st)
+            if self.exchange is not None:
+                self.exchange.sum_(self.pilot_sq)  # C2: pilot norms over the output tiles
             aux = self.pilot_sq
         self._c("bmm_budgets", rule, P(self.s) if rule != _lib.RULE_UU else None, P(aux) if aux is not None else None,
                 P(self.sizes_d), None, None, K, B, P(self.c_arr), int(self.cap), P(self.budgets), P(self.col_off),
@@ -540,6 +550,8 @@ class SketchPipeline:
             self._c("bmm_segsq_f64", P(A), A.stride(-2), sM, P(Bm), Bm.stride(-2), sN, m, p,
                     P(self.offsets) + 8 * k0, k1 - k0, 0, B, P(self.gsq) + 8 * k0, P(self.ws_seg),
                     self.ws_seg.numel(), st)
+        if getattr(self, "exchange", None) is not None and k0 == 0 and k1 == self.K:
+            self.exchange.sum_(self.gsq)  # C2: ||M^k N_k||_F^2 is the sum over the output tiles
 
     def _f64(self, M, N):
         if M.dtype == torch.float64:
@@ -599,6 +611,9 @@ class SharedStats:
         self.m, self.n, self.p, self.B, self.K = p0.m, p0.n, p0.p, p0.B, p0.K
         self.sizes, self.max_len, self.offsets = p0.sizes, p0.max_len, p0.offsets
         self.timeline, self.stamps = None, None
+        self.exchange = p0.exchange
+        if any(q.exchange is not p0.exchange for q in pipes):
+            raise ValueError("shared statistics need one exchange for every member")
         self.colsq, self.rowsq = p0.colsq, p0.rowsq
         self.needs_probs = any(q.method not in ("SSM", "UU") for q in pipes)
         opl = [q for q in pipes if q.method == "OPL"]
@@ -738,6 +753,8 @@ class PipelineGroup:
             s.wait_event(evs[1] if pipe.method == "OPL" else evs[0])
 
     def capture(self, M: torch.Tensor, N: torch.Tensor) -> None:
+        if any(q.exchange is not None for q in self.pipes):
+            raise RuntimeError("sharded members exchange through host collectives: run them eagerly")
         cur = torch.cuda.current_stream()
         side = torch.cuda.Stream()
         side.wait_stream(cur)

@@ -202,21 +202,21 @@ def test_cfg5_subset_against_oracle():
 
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
-@pytest.mark.parametrize("method", ["ONC", "OPL"])
+@pytest.mark.parametrize("method", ["ONC", "OPL", "SSM"])
 def test_sharded_world1_matches_pipeline(dtype, method):
     from paper_2105_04940_b200.distributed import ShardLayout, ShardedApproxProduct
-    M, N, sizes = workloads.cfg2(n=4096, m=256, p=128, K=16)
+    M, N, sizes = workloads.cfg1(scale=10)  # equal blocks (SSM)
+    m, n, p = M.shape[0], M.shape[1], N.shape[1]
     Md = torch.as_tensor(M, device="cuda", dtype=dtype)
     Nd = torch.as_tensor(N, device="cuda", dtype=dtype)
-    W = 1024
-    sh = ShardedApproxProduct(ShardLayout(1, 0, 256, 4096, 128), sizes, W, method, dtype=dtype)
-    rng = np.random.default_rng(9)
-    seeds = seeds_from_rngs(method, [rng], len(sizes))
-    out = sh.run(Md, Nd, seeds.main.words[0], int(seeds.main.first[0])).cpu().numpy()
+    c = 8 if method == "SSM" else 512
+    sh = ShardedApproxProduct(ShardLayout(1, 0, m, n, p), sizes, [(method, c)], dtype=dtype)
+    out = sh.run(Md, Nd, [seeds_from_rngs(method, [np.random.default_rng(9)], len(sizes), draws=c)])[0].cpu().numpy()
     sh.check()
-    pipe = SketchPipeline(256, 4096, 128, sizes, W, method, dtype=dtype)
-    ref = pipe.run(Md, Nd, seeds_from_rngs(method, [np.random.default_rng(9)], len(sizes))).cpu().numpy()
-    assert np.array_equal(sh.column.cpu().numpy(), pipe.columns_host()[0])
+    pipe = (SketchPipeline(m, n, p, sizes, 0, "SSM", draws=c, dtype=dtype) if method == "SSM" else
+            SketchPipeline(m, n, p, sizes, c, method, dtype=dtype))
+    ref = pipe.run(Md, Nd, seeds_from_rngs(method, [np.random.default_rng(9)], len(sizes), draws=c)).cpu().numpy()
+    assert np.array_equal(sh.pipes[0].columns_host(), pipe.columns_host())
     assert np.array_equal(out, ref)
 
 
@@ -335,18 +335,18 @@ def test_nonfinite_input_raises_like_the_reference(bad, dtype):
     """NaN/Inf in M: the pipeline reports the reference's exception (first bad
     block's probabilities for OPL/ONC, integerize's weights for the two-step
     plan, empty support for SSM) and never indexes outside the inputs."""
-    M, N, sizes = workloads.cfg2(n=4000, m=60, p=50, K=12)
+    M, N, sizes = workloads.cfg1(scale=10)  # 200 x 1000, ten equal blocks of 100 (SSM needs equal blocks)
     M = M.astype(dtype)
     N = N.astype(dtype)
-    col = sizes[0] + sizes[1] + 5  # a column of block 2
-    M[7, col] = bad
+    M[7, 2 * 100 + 5] = bad  # a column of block 2
+    m, n, p = M.shape[0], M.shape[1], N.shape[1]
     tdt = torch.float64 if dtype == np.float64 else torch.float32
     Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
     want = {"OPL": "block 2: probabilities must be finite", "ONC": "block 2: probabilities must be finite",
             "ONU": "weights must be finite", "SSM": "probability vector has empty support"}
     for meth, msg in want.items():
-        pipe = (SketchPipeline(60, 4000, 50, sizes, 0, "SSM", draws=5, dtype=tdt) if meth == "SSM" else
-                SketchPipeline(60, 4000, 50, sizes, 400, meth, c0=120, dtype=tdt))
+        pipe = (SketchPipeline(m, n, p, sizes, 0, "SSM", draws=5, dtype=tdt) if meth == "SSM" else
+                SketchPipeline(m, n, p, sizes, 400, meth, c0=40, dtype=tdt))
         pipe.run(Md, Nd, seeds_from_rngs(meth, [np.random.default_rng(1)], len(sizes), draws=5))
         torch.cuda.synchronize()
         with pytest.raises(ValueError, match=msg):
