@@ -272,6 +272,235 @@ __global__ void __launch_bounds__(32 * TCfg<BN>::WARPS, 1) gemm_f32split_kernel(
   if constexpr (MC > 1) cluster_sync_all();
 }
 
+// ---- cta_group::2: one 256 x 256 output tile per CTA pair (a 2-CTA cluster on
+// one TPC).  Each CTA stages 128 rows of A and 128 rows of B^T (its halves, 64 KB
+// per stage as above); the leader issues tcgen05.mma.cta_group::2 with M = 256,
+// N = 256, so each MMA reads A and B from BOTH CTAs' shared memory and writes
+// each CTA's 128 rows x 256 columns of the accumulator into its own TMEM.  Per
+// SM that is twice the outputs of the 128 x 128 kernel for the same shared
+// memory, L2 and HBM operand bytes: half the operand traffic per flop.
+//   * TMA: both CTAs load their halves with .cta_group::2, completing bytes on
+//     the LEADER's full[s] barrier (expect_tx of both halves);
+//   * MMA commits go to both CTAs' empty[s] (each refills its own stage) and,
+//     at a chunk end, to both CTAs' acc_full[q];
+//   * the 8 drain warps of each CTA promote their TMEM rows into float32
+//     registers (as above) and arrive on the leader's acc_empty[q] (16 arrivals).
+constexpr int P_STAGES = 3;
+constexpr int P_STAGE = 4 * T_TILE_BYTES;           // A_hi, A_x, B_hi, B_x halves: 64 KB
+constexpr int P_SMEM = P_STAGES * P_STAGE + 1024 + 256;
+constexpr int P_DRAIN = 8;                           // 32 TMEM lanes x 128 columns each
+constexpr int P_WARPS = 2 + P_DRAIN;
+
+template <int M_, int N_>
+constexpr uint32_t idesc_tf32_mn() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N_ >> 3) << 17) | ((uint32_t)(M_ >> 4) << 24);
+}
+template <int M_, int N_>
+constexpr uint32_t idesc_bf16_mn() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N_ >> 3) << 17) | ((uint32_t)(M_ >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(su32(p)), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];\n" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma2_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma2_bf16(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma2_commit_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          su32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(32 * P_WARPS, 1) gemm_f32split_2sm_kernel(
+    const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_ax,
+    const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_bx, int64_t m, int64_t nc,
+    int64_t k, float* __restrict__ out, int64_t ldo, int64_t strideO, const int64_t* __restrict__ kdev) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* acc_full = empty + P_STAGES;   // [2]
+  uint64_t* acc_empty = acc_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = blockIdx.z;
+  uint32_t rank;
+  asm("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  constexpr int GROUP_M = 8;  // grouped rasterisation over 256 x 256 pair tiles
+  int tile_m, tile_n;
+  {
+    const int tm = gridDim.y, tn = gridDim.x / 2;
+    const int lin = blockIdx.y * tn + blockIdx.x / 2;
+    const int group = lin / (GROUP_M * tn);
+    const int first_m = group * GROUP_M;
+    const int gsz = min(tm - first_m, GROUP_M);
+    tile_m = first_m + (lin % (GROUP_M * tn)) % gsz;
+    tile_n = (lin % (GROUP_M * tn)) / gsz;
+  }
+  if (kdev != nullptr) {
+    const int64_t kd = ((kdev[b] + T_BK - 1) / T_BK) * T_BK;
+    k = kd < k ? kd : k;
+  }
+  // this CTA's halves: A rows and B^T rows (= output columns) [128 * rank, +128) of the pair tile
+  const int a_row0 = (int)(b * m + (int64_t)tile_m * 256 + 128 * rank);
+  const int b_row0 = (int)(b * nc + (int64_t)tile_n * 256 + 128 * rank);
+  const int ktiles = (int)((k + T_BK - 1) / T_BK);
+  const int nchunks = (ktiles + T_CHUNK - 1) / T_CHUNK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&full[s], 1);   // the leader's producer arrives (with both halves' bytes)
+      mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both CTAs
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&acc_full[q], 1);
+      mbar_init(&acc_empty[q], 2 * P_DRAIN);  // both CTAs' drain warps (leader's barrier is used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_ax)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_bhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_bx)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers and TMEM exist before any cross-CTA signal
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t full0 = cluster_addr(&full[0], 0);  // the leader's full[] (same layout in both CTAs)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer (both CTAs): this CTA's halves into its own stage
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % P_STAGES;
+        if (kt >= P_STAGES) mbar_wait(&empty[s], ((kt / P_STAGES) - 1) & 1);
+        uint8_t* st = smem + s * P_STAGE;
+        if (rank == 0) mbar_expect_tx(&full[s], 2 * P_STAGE);
+        const uint32_t fb = full0 + (uint32_t)(s * sizeof(uint64_t));
+        const int kc = kt * T_BK;
+        tma_load_2d_2sm(st + 0 * T_TILE_BYTES, &tm_ahi, fb, kc, a_row0);
+        tma_load_2d_2sm(st + 1 * T_TILE_BYTES, &tm_ax, fb, kc, a_row0);
+        tma_load_2d_2sm(st + 2 * T_TILE_BYTES, &tm_bhi, fb, kc, b_row0);
+        tma_load_2d_2sm(st + 3 * T_TILE_BYTES, &tm_bx, fb, kc, b_row0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---- MMA issuer (leader only): M = 256 (both CTAs' A halves), N = 256 (both B halves)
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % P_STAGES;
+        const int chunk = kt / T_CHUNK, q = chunk & 1;
+        const bool first = (kt % T_CHUNK) == 0;
+        if (first && chunk >= 2) mbar_wait(&acc_empty[q], ((chunk >> 1) - 1) & 1);
+        mbar_wait(&full[s], (kt / P_STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t base = su32(smem + s * P_STAGE);
+        const uint32_t acc = tmem + (uint32_t)(q * 256);
+#pragma unroll
+        for (int kk = 0; kk < T_BK / 8; ++kk) {
+          const uint32_t off = kk * 32;
+          const uint64_t ahi = umma_desc_sw128(base + 0 * T_TILE_BYTES + off);
+          const uint64_t ax = umma_desc_sw128(base + 1 * T_TILE_BYTES + off);
+          const uint64_t bhi = umma_desc_sw128(base + 2 * T_TILE_BYTES + off);
+          const uint64_t bx = umma_desc_sw128(base + 3 * T_TILE_BYTES + off);
+          umma2_bf16(acc, ax, bx, idesc_bf16_mn<256, 256>(), !(first && kk == 0));  // h_x.l_y + l_x.h_y
+          umma2_tf32(acc, ahi, bhi, idesc_tf32_mn<256, 256>(), 1);                  // h_x.h_y
+        }
+        umma2_commit_mc(&empty[s]);  // both CTAs may refill stage s once these MMAs have read it
+        if ((kt % T_CHUNK) == T_CHUNK - 1 || kt == ktiles - 1) umma2_commit_mc(&acc_full[q]);
+      }
+    }
+  } else {
+    // ---- drain (both CTAs): warp w reads TMEM lanes 32*(w%4).. of this CTA's 128 rows,
+    // columns half*128 .. +128 of the 256
+    constexpr int DC = 128;
+    const int quarter = warp & 3;
+    const int half = (warp - 2) / 4;
+    const uint32_t ae0 = cluster_addr(&acc_empty[0], 0);
+    float sum[DC];
+#pragma unroll
+    for (int c = 0; c < DC; ++c) sum[c] = 0.f;
+    for (int chunk = 0; chunk < nchunks; ++chunk) {
+      const int q = chunk & 1;
+      mbar_wait(&acc_full[q], (chunk >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < DC; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(q * 256 + half * DC + c), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum[c + j] += __uint_as_float(v[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(
+                         ae0 + (uint32_t)(q * sizeof(uint64_t)))
+                     : "memory");
+    }
+    const int64_t row = (int64_t)tile_m * 256 + 128 * rank + quarter * 32 + lane;
+    if (row < m) {
+      float* orow = out + b * strideO + row * ldo;
+      const int64_t col0 = (int64_t)tile_n * 256 + half * DC;
+      const bool vec = (col0 + DC <= nc) && (ldo % 4) == 0 && ((reinterpret_cast<uintptr_t>(orow + col0) & 15) == 0);
+      if (vec) {
+        float4* o4 = reinterpret_cast<float4*>(orow + col0);
+#pragma unroll
+        for (int j = 0; j < DC / 4; ++j)
+          o4[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < DC; ++j)
+          if (col0 + j < nc) orow[col0 + j] = sum[j];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();  // the peer's MMAs and arrivals target this CTA: leave together
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+  }
+}
+
 // ---- split gather (K4 for the float32 path)
 
 // position of element t inside its row of bf16 pairs: group t/8 holds 16 bf16
@@ -805,6 +1034,12 @@ static int gemm_split_impl(const float* a_hi, const void* a_x, const float* b_hi
     return e ? atoi(e) : 0;
   }();
   const bool pair = bn == 128 && pair_env != 0 && nc > 256;
+  // cta_group::2 (256 x 256 per CTA pair): large outputs (BMM_TF32_2SM=0 disables)
+  static const int sm2_env = [] {
+    const char* e = getenv("BMM_TF32_2SM");
+    return e ? atoi(e) : 1;
+  }();
+  const bool two_sm = sm2_env != 0 && tile_env == 0 && pair_env == 0 && m >= 256 && nc >= 512;
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   int rc;
   if ((rc = make_map(&ma_hi, a_hi, batch * m, k)) != BMM_OK) return rc;
@@ -812,7 +1047,30 @@ static int gemm_split_impl(const float* a_hi, const void* a_x, const float* b_hi
   if ((rc = make_map(&mb_hi, b_hi, batch * nc, k, bn)) != BMM_OK) return rc;
   if ((rc = make_map(&mb_lo, b_lo, batch * nc, k, bn)) != BMM_OK) return rc;
   cudaStream_t st = as_stream(stream);
-  if (bn == 256) {
+  if (two_sm) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_f32split_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
+      attr = true;
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(2 * ceil_div(nc, 256)), (unsigned)ceil_div(m, 256), (unsigned)batch);
+    lc.blockDim = dim3(32 * P_WARPS, 1, 1);
+    lc.dynamicSmemBytes = P_SMEM;
+    lc.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = 2;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    lc.attrs = la;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, gemm_f32split_2sm_kernel, ma_hi, ma_lo, mb_hi, mb_lo, m, nc, k, out, ldo, strideO,
+                           k_dev) != cudaSuccess) {
+      set_error("bmm_gemm_f32split: 2-SM cluster launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      return BMM_E_CUDA;
+    }
+  } else if (bn == 256) {
     using Cfg = TCfg<256>;
     static bool attr = false;
     if (!attr) {

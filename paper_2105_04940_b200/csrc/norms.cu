@@ -992,10 +992,12 @@ static bool launch_colsq_tma(const T* M, int64_t m, int64_t n, int64_t ldm, int6
 // chain of NumPy's add.reduce over rows) and one producer warp that streams
 // RB-row slabs of every unit of the CTA into a STAGES-deep ring (full/empty
 // mbarriers).  Rows past m inside the last slab are TMA zero-fill and skipped.
-constexpr int kWideUnits = 28;
+constexpr int kWideWarps = 28;  // consumer warps per CTA
 
-template <typename T, int RB, int STAGES>
-__global__ void __launch_bounds__(32 * (kWideUnits + 1), 2) colsq_wide_kernel(const __grid_constant__ CUtensorMap map,
+// UPW units (32-column strips) per consumer warp: lane j owns columns j, j+32, ...
+// of the warp's units (UPW independent chains per lane).
+template <typename T, int RB, int STAGES, int UPW>
+__global__ void __launch_bounds__(32 * (kWideWarps + 1), UPW == 1 ? 2 : 1) colsq_wide_kernel(const __grid_constant__ CUtensorMap map,
                                                                              int64_t m, int64_t n, int64_t units,
                                                                              int accumulate, double* __restrict__ colsq) {
   constexpr int BOX = 32 * RB * (int)sizeof(T);
@@ -1006,11 +1008,12 @@ __global__ void __launch_bounds__(32 * (kWideUnits + 1), 2) colsq_wide_kernel(co
   const int nw = (int)(blockDim.x >> 5) - 1;  // consumer warps; warp nw produces
   const int64_t u0 = (int64_t)blockIdx.x * units / gridDim.x, u1 = (int64_t)(blockIdx.x + 1) * units / gridDim.x;
   const int U = (int)(u1 - u0);
+  const int busy = (U + UPW - 1) / UPW;  // consumer warps with at least one unit
   const int64_t slabs = (m + RB - 1) / RB;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm_addr(&full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm_addr(&empty[s])), "r"(U));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm_addr(&empty[s])), "r"(busy));
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -1045,9 +1048,14 @@ __global__ void __launch_bounds__(32 * (kWideUnits + 1), 2) colsq_wide_kernel(co
     }
     return;
   }
-  if (warp >= U) return;
-  const int64_t col = (u0 + warp) * 32 + lane;
-  double acc = (accumulate && col < n) ? colsq[col] : 0.0;
+  if (warp >= busy) return;
+  double acc[UPW];
+  int64_t col[UPW];
+#pragma unroll
+  for (int j = 0; j < UPW; ++j) {
+    col[j] = (u0 + warp * UPW + j) * 32 + lane;
+    acc[j] = (accumulate && warp * UPW + j < U && col[j] < n) ? colsq[col[j]] : 0.0;
+  }
   for (int64_t q = 0; q < slabs; ++q) {
     const int st = (int)(q % STAGES);
     asm volatile(
@@ -1059,34 +1067,58 @@ __global__ void __launch_bounds__(32 * (kWideUnits + 1), 2) colsq_wide_kernel(co
         "}\n" ::"r"(sm_addr(&full[st])),
         "r"((uint32_t)((q / STAGES) & 1))
         : "memory");
-    const T* slab = reinterpret_cast<const T*>(smem + (int64_t)(st * U + warp) * BOX);
     const int rows = (int)min((int64_t)RB, m - q * RB);
-    double v[RB];
 #pragma unroll
-    for (int r = 0; r < RB; ++r) v[r] = (double)slab[r * 32 + lane];
+    for (int j = 0; j < UPW; ++j) {
+      if (warp * UPW + j < U) {
+        const T* slab = reinterpret_cast<const T*>(smem + (int64_t)(st * U + warp * UPW + j) * BOX);
+        double v[RB];
 #pragma unroll
-    for (int r = 0; r < RB; ++r)
-      if (r < rows) acc = __dadd_rn(acc, __dmul_rn(v[r], v[r]));
+        for (int r = 0; r < RB; ++r) v[r] = (double)slab[r * 32 + lane];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+          if (r < rows) acc[j] = __dadd_rn(acc[j], __dmul_rn(v[r], v[r]));
+      }
+    }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sm_addr(&empty[st])) : "memory");
   }
-  if (col < n) colsq[col] = acc;
+#pragma unroll
+  for (int j = 0; j < UPW; ++j)
+    if (warp * UPW + j < U && col[j] < n) colsq[col[j]] = acc[j];
+}
+
+template <typename T, int RB, int STAGES, int UPW>
+static bool launch_colsq_wide_cfg(const CUtensorMap& map, int64_t m, int64_t n, int accumulate, double* colsq,
+                                  cudaStream_t st) {
+  const int64_t units = (n + 31) / 32;
+  // UPW = 1: two CTAs per SM, UPW = 2: one CTA per SM; every unit in ONE wave when
+  // units <= 296 (148) * kWideWarps * UPW -- no tail of half-empty waves
+  const int64_t slots = UPW == 1 ? 296 : 148;
+  int64_t ctas = std::max<int64_t>(slots, ceil_div(units, (int64_t)kWideWarps * UPW));
+  ctas = std::min<int64_t>(ctas, units);
+  const int umax = (int)ceil_div(units, ctas);
+  const int warps = (int)ceil_div(umax, UPW);
+  auto kern = colsq_wide_kernel<T, RB, STAGES, UPW>;
+  const int smem = STAGES * umax * 32 * RB * (int)sizeof(T) + 1024;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+  kern<<<(unsigned)ctas, 32 * (warps + 1), smem, st>>>(map, m, n, units, accumulate, colsq);
+  return true;
 }
 
 template <typename T>
 static bool launch_colsq_wide(const T* M, int64_t m, int64_t n, int64_t ldm, int accumulate, double* colsq,
                               cudaStream_t st) {
-  constexpr int RB = 8, STAGES = sizeof(T) == 4 ? 3 : 2;
   if ((ldm * (int64_t)sizeof(T)) % 16 != 0 || ldm < n || reinterpret_cast<uintptr_t>(M) % 16 != 0 ||
       m >= (1LL << 31) || n >= (1LL << 31))
     return false;
   auto enc = tma_encode_fn();
   if (enc == nullptr) return false;
-  const int64_t units = (n + 31) / 32;
-  // two CTAs per SM, every unit in one wave when units <= 296 * kWideUnits
-  int64_t ctas = std::max<int64_t>(148 * 2, ceil_div(units, kWideUnits));
-  ctas = std::min<int64_t>(ctas, units);
-  const int umax = (int)ceil_div(units, ctas);
+  static const int cfg = [] {
+    const char* e = getenv("BMM_COLSQ_WIDE_CFG");  // A/B switch (tools/cfg4_norms_probe.py)
+    return e ? atoi(e) : 0;
+  }();
+  const int RB = (cfg == 2) ? 4 : 8;
   CUtensorMap map;
   cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
   cuuint64_t strides[1] = {(cuuint64_t)(ldm * sizeof(T))};
@@ -1097,11 +1129,14 @@ static bool launch_colsq_wide(const T* M, int64_t m, int64_t n, int64_t ldm, int
           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
       CUDA_SUCCESS)
     return false;
-  auto kern = colsq_wide_kernel<T, RB, STAGES>;
-  const int smem = STAGES * umax * 32 * RB * (int)sizeof(T) + 1024;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
-  kern<<<(unsigned)ctas, 32 * (umax + 1), smem, st>>>(map, m, n, units, accumulate, colsq);
-  return true;
+  if constexpr (sizeof(T) == 8) return launch_colsq_wide_cfg<T, 8, 2, 1>(map, m, n, accumulate, colsq, st);
+  switch (cfg) {
+    case 1: return launch_colsq_wide_cfg<T, 8, 3, 2>(map, m, n, accumulate, colsq, st);
+    case 2: return launch_colsq_wide_cfg<T, 4, 6, 1>(map, m, n, accumulate, colsq, st);
+    case 3: return launch_colsq_wide_cfg<T, 8, 2, 2>(map, m, n, accumulate, colsq, st);
+    case 4: return launch_colsq_wide_cfg<T, 8, 4, 2>(map, m, n, accumulate, colsq, st);
+    default: return launch_colsq_wide_cfg<T, 8, 3, 1>(map, m, n, accumulate, colsq, st);
+  }
 }
 
 template <typename T>
@@ -1123,8 +1158,9 @@ int launch_norms(const T* M, int64_t m, int64_t n, int64_t ldm, int64_t strideM,
       return e ? atoi(e) : 1;
     }();
     // wide, long single matrices (>= 256 MB): the TMA-streamed one-wave kernel
-    const bool wide = !narrow && batch == 1 && wide_mode != 0 && m >= 64 &&
-                      m * n * (int64_t)sizeof(T) >= (256LL << 20);
+    // (BMM_COLSQ_WIDE=2 forces it for any single matrix: sanitizer runs on small inputs)
+    const bool wide = batch == 1 && ((wide_mode == 2 && n >= 32) ||
+                                     (!narrow && wide_mode != 0 && m >= 64 && m * n * (int64_t)sizeof(T) >= (256LL << 20)));
     bool done = wide && launch_colsq_wide<T>(M, m, n, ldm, accumulate, colsq, st);
     if (done) BMM_CHECK_LAUNCH("colsq_wide_kernel");
     done = done || (narrow && cs_variant != 1 &&

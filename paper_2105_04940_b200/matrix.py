@@ -168,3 +168,12 @@ def frobenius_norm(M) -> float:
         Md = Md.reshape(1, -1)
     colsq, _ = device_norms_sq(Md, None)
     return float(torch.sqrt(device_pairwise_sum(colsq)).item())
+
+
+def __getattr__(name):
+    """The reference defines its matrix file formats in matrix.py (121-140); here
+    they live in io.py.  Resolve them lazily (io imports this module)."""
+    if name in ("load_matrix", "load_matrix_csv", "save_matrix", "save_matrix_csv"):
+        from . import io
+        return getattr(io, name)
+    raise AttributeError(name)

@@ -1,12 +1,16 @@
-"""Config 4 at full size (M 16384 x 262144, N 262144 x 16384 float32, K=4096,
-W=32768, ONC): norms, budgets, sampled indices and scales bit-exact against the
-NumPy oracle (norms restated chunk-by-chunk with the exact sequential
-continuation, on the float64 upcast); C.D against a float64 product of the
-same sketch on a 256-row slab within 1e-5."""
+"""Config 4 at full size (M 16384 x 262144, N 262144 x 16384 float32, K=4096
+blocks of 64): the benched step -- OPL and ONC with W=32768 and SSM with 512
+draws over one shared statistics stage -- against the NumPy oracle.
+* norms: every column of M and every row of N bit-exact, restated chunk by chunk
+  with the exact sequential continuation on the float64 upcast (the full upcast
+  needs 69 GB);
+* plan and draws: probabilities, score sums, ONC/OPL budgets, every draw and
+  scale bit-exact; SSM block probabilities (1e-13) and draws (bench.cfg4_parity);
+* g_k^2 of sampled blocks vs the oracle's multiplied-out blocks (1e-12);
+* C.D on 4 row slabs (first, last, two inner) vs float64 of the same sketch (1e-5)."""
 import numpy as np
 import pytest
 
-import workloads
 from oracle import blockmm_oracle as O
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
@@ -15,15 +19,12 @@ torch = pytest.importorskip("torch")
 
 def test_cfg4_full_size_parity():
     import bench
-    from paper_2105_04940_b200.pipeline import SketchPipeline, seeds_from_keys
 
-    Md, Nd, sizes, _ = bench.device_data(torch, "cfg4")
-    m, n = Md.shape
-    p = Nd.shape[1]
-    K, W = len(sizes), 32768
-    pipe = SketchPipeline(m, n, p, sizes, W, "ONC", dtype=torch.float32)
-    CD = pipe.run(Md, Nd, seeds_from_keys("ONC", workloads.ROOT, (4, 1), [0], K))
-    pipe.check()
+    m, n, p, K = 16384, 262144, 16384, 4096
+    Md, Nd = bench.cfg4_shard(torch, (0, m), (0, p))
+    group = bench.cfg4_group(torch, m, n, p, (n // K,) * K)
+    outs = [o.clone() for o in group.run(Md, Nd, bench.cfg4_seeds(K))]
+    group.check()
 
     # oracle norm pass on host copies (float64 upcast, exact chunk continuation)
     acc = None
@@ -33,35 +34,13 @@ def test_cfg4_full_size_parity():
         if acc is not None:
             sq = np.concatenate([acc[None, :], sq], axis=0)
         acc = np.add.reduce(sq, axis=0)
-    colsq = acc
     rowsq = np.empty(n)
     for r0 in range(0, n, 4096):
         sl = Nd[r0:r0 + 4096].cpu().numpy().astype(np.float64)
         rowsq[r0:r0 + 4096] = np.add.reduce(sl * sl, axis=1)
-    assert np.array_equal(pipe.colsq.cpu().numpy(), colsq)
-    assert np.array_equal(pipe.rowsq.cpu().numpy(), rowsq)
+    assert np.array_equal(group.shared.colsq.cpu().numpy(), acc)
+    assert np.array_equal(group.shared.rowsq.cpu().numpy(), rowsq)
 
-    probs, s = O.block_stats(colsq, rowsq, sizes)
-    budgets, _ = O.plan_budgets("ONC", sizes, W, s=s)
-    assert np.array_equal(pipe.budgets_host()[0], budgets)
-    streams = workloads.sample_rng(4).spawn(K)
-    off = O.offsets_of(sizes)
-    cols, scales = [], []
-    for k in range(K):
-        if budgets[k]:
-            pk = probs[off[k]:off[k + 1]]
-            idx = O.draw(pk, int(budgets[k]), streams[k])
-            cols.append(off[k] + idx)
-            scales.append(1.0 / np.sqrt(int(budgets[k]) * pk[idx]))
-    cols, scales = np.concatenate(cols), np.concatenate(scales)
-    assert np.array_equal(pipe.columns_host()[0], cols)
-    assert np.array_equal(pipe.scales_host()[0], scales)
-
-    # C.D on a row slab against float64 of the same sketch
-    ci = torch.as_tensor(cols, device="cuda")
-    sc = torch.as_tensor(scales, device="cuda")
-    C64 = Md[:256].index_select(1, ci).double() * sc
-    D64 = Nd.index_select(0, ci).double() * sc[:, None]
-    ref = C64 @ D64
-    err = ((CD[:256].double() - ref).norm() / ref.norm()).item()
-    assert err < 1e-5, err
+    res = bench.cfg4_parity(torch, group, Md, Nd, outs)  # raises on any mismatch
+    assert res["ok"]
+    assert max(res["cd_rel_err_vs_f64_same_sketch"].values()) < 1e-5

@@ -35,7 +35,10 @@ def unpair(x, W, first):
 
 @pytest.mark.parametrize("B,m,n,p,W", [(1, 128, 300, 128, 32), (1, 200, 2000, 72, 1000), (3, 256, 4096, 256, 1024),
                                        (2, 130, 777, 260, 4096), (1, 128, 64, 128, 8), (1, 128, 999, 128, 32768),
-                                       (2, 384, 1500, 640, 512), (1, 256, 3000, 1024, 2048)])
+                                       (2, 384, 1500, 640, 512), (1, 256, 3000, 1024, 2048),
+                                       # cta_group::2 (256 x 256 pair tiles): partial pair tiles, long K
+                                       (1, 300, 2000, 520, 1024), (1, 512, 5000, 768, 4096),
+                                       (1, 256, 999, 512, 32768), (3, 260, 700, 1030, 256)])
 def test_split_gather_and_gemm(B, m, n, p, W):
     g = torch.Generator(device="cuda").manual_seed(B * 1000 + m + n + p + W)
     M = torch.randn((B, m, n), generator=g, device="cuda", dtype=torch.float32)
