@@ -403,13 +403,19 @@ __device__ __forceinline__ const unsigned char* swz(const unsigned char* box, in
   return box + q * 128 + ((k ^ (q & 7)) << 4);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(32 * kTmaWarps) rowsq_tma_kernel(const __grid_constant__ CUtensorMap map,
-                                                                   int64_t total_rows, int L, int log2L,
-                                                                   double* __restrict__ rowsq) {
-  constexpr int NB = tma_boxes<T>(), SB = tma_stage_bytes<T>();
+// WARPS warps per CTA (one CTA per SM), each with its own 3-stage ring; a stage
+// holds NBS of the NB boxes of a 32-leaf unit (P = NB / NBS stages per unit): the
+// lane's 8 accumulator chains continue across the P stages of its leaf.  Smaller
+// stages let more warps share the SM's shared memory -- with 4 warps and whole
+// units per stage each SM sub-partition ran one dependent chain at a time.
+template <typename T, int WARPS, int NBS>
+__global__ void __launch_bounds__(32 * WARPS) rowsq_tma_kernel(const __grid_constant__ CUtensorMap map,
+                                                               int64_t total_rows, int L, int log2L,
+                                                               double* __restrict__ rowsq) {
+  constexpr int NB = tma_boxes<T>(), SB = NBS * kTmaBoxBytes, P = NB / NBS;
+  static_assert(NB % NBS == 0, "boxes per stage must divide the boxes of a leaf");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bars[kTmaWarps][kTmaStages];
+  __shared__ __align__(8) uint64_t bars[WARPS][kTmaStages];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   unsigned char* ring = smem + (int64_t)w * kTmaStages * SB;
@@ -420,32 +426,37 @@ __global__ void __launch_bounds__(32 * kTmaWarps) rowsq_tma_kernel(const __grid_
   }
   __syncwarp();
   const bool packed = L <= 32;
-  const int U = packed ? 1 : L / 32;              // stages per row
-  const int RG = packed ? 32 / L : 1;             // rows per stage
+  const int U = packed ? 1 : L / 32;              // 32-leaf units per row
+  const int RG = packed ? 32 / L : 1;             // rows per unit
   const int64_t units = packed ? (total_rows + RG - 1) / RG : total_rows;
-  const int64_t gw = (int64_t)blockIdx.x * kTmaWarps + w, Wt = (int64_t)gridDim.x * kTmaWarps;
-  const int64_t nseq = gw < units ? ((units - 1 - gw) / Wt + 1) * U : 0;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + w, Wt = (int64_t)gridDim.x * WARPS;
+  const int64_t nseq = gw < units ? ((units - 1 - gw) / Wt + 1) * U * P : 0;
   auto issue = [&](int64_t sq) {
     if (lane == 0 && sq < nseq) {
-      const int64_t unit = gw + (sq / U) * Wt;
-      const int64_t leaf0 = packed ? unit * 32 : unit * L + (sq % U) * 32;
+      const int64_t su = sq / P;  // unit-stage index (as without the split)
+      const int part = (int)(sq % P);
+      const int64_t unit = gw + (su / U) * Wt;
+      const int64_t leaf0 = packed ? unit * 32 : unit * L + (su % U) * 32;
       uint64_t* bar = &bars[w][sq % kTmaStages];
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(SB)
                    : "memory");
       unsigned char* dst = ring + (int64_t)(sq % kTmaStages) * SB;
 #pragma unroll
-      for (int c = 0; c < NB; ++c)
+      for (int c = 0; c < NBS; ++c)
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
                 sm_addr(dst + c * kTmaBoxBytes)),
-            "l"(reinterpret_cast<uint64_t>(&map)), "r"(sm_addr(bar)), "r"(c * tma_box_elems<T>()), "r"((int)leaf0)
+            "l"(reinterpret_cast<uint64_t>(&map)), "r"(sm_addr(bar)), "r"((part * NBS + c) * tma_box_elems<T>()),
+            "r"((int)leaf0)
             : "memory");
     }
   };
   for (int s = 0; s < kTmaStages; ++s) issue(s);
-  double part[4];
+  double part_sum[4];
+  double r[8];
   for (int64_t sq = 0; sq < nseq; ++sq) {
     const int st = (int)(sq % kTmaStages);
+    const int part = (int)(sq % P);
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -456,12 +467,15 @@ __global__ void __launch_bounds__(32 * kTmaWarps) rowsq_tma_kernel(const __grid_
         "r"((uint32_t)((sq / kTmaStages) & 1))
         : "memory");
     const unsigned char* stage = ring + (int64_t)st * SB;
-    // this lane's leaf: 16 steps of 8 elements
-    double r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (part == 0) {
 #pragma unroll
-    for (int s8 = 0; s8 < 16; ++s8) {
+      for (int k = 0; k < 8; ++k) r[k] = 0.0;
+    }
+    // this lane's leaf, elements [part * 128 / P, +128 / P): steps of 8
+#pragma unroll
+    for (int s8 = 0; s8 < 16 / P; ++s8) {
       constexpr int CPS = 8 * (int)sizeof(T) / 16;  // 16-byte chunks per step
-      const int e0 = 8 * s8;                        // first element of the step
+      const int e0 = 8 * s8;                        // first element of the step within the stage
       const unsigned char* box = stage + (e0 / tma_box_elems<T>()) * kTmaBoxBytes;
       const int k0 = (e0 % tma_box_elems<T>()) * (int)sizeof(T) / 16;
 #pragma unroll
@@ -482,25 +496,27 @@ __global__ void __launch_bounds__(32 * kTmaWarps) rowsq_tma_kernel(const __grid_
         }
       }
     }
-    double t = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
     __syncwarp();
     issue(sq + kTmaStages);  // stage st is consumed (all lanes past their loads)
+    if (part != P - 1) continue;
+    double t = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
     // perfect tree over the 32 leaves: xor 1, 2, 4, ... (stops at the row width when packed)
     const int lim = packed ? L : 32;
     for (int o = 1; o < lim; o <<= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
+    const int64_t su = sq / P;
     if (packed) {
-      const int64_t row0 = (gw + (sq / U) * Wt) * RG;
+      const int64_t row0 = (gw + (su / U) * Wt) * RG;
       const int sub = lane >> log2L;
       if ((lane & (L - 1)) == 0 && row0 + sub < total_rows) rowsq[row0 + sub] = __dadd_rn(0.0, t);
     } else {
-      const int u = (int)(sq % U);
-      part[u & 3] = t;
+      const int u = (int)(su % U);
+      part_sum[u & 3] = t;
       if (u == U - 1) {
         double rt;
-        if (U == 2) rt = __dadd_rn(part[0], part[1]);
-        else rt = __dadd_rn(__dadd_rn(part[0], part[1]), __dadd_rn(part[2], part[3]));
-        if (lane == 0) rowsq[gw + (sq / U) * Wt] = __dadd_rn(0.0, rt);
+        if (U == 2) rt = __dadd_rn(part_sum[0], part_sum[1]);
+        else rt = __dadd_rn(__dadd_rn(part_sum[0], part_sum[1]), __dadd_rn(part_sum[2], part_sum[3]));
+        if (lane == 0) rowsq[gw + (su / U) * Wt] = __dadd_rn(0.0, rt);
       }
     }
   }
@@ -540,19 +556,32 @@ static bool launch_rowsq_tma(const T* N, int64_t n, int64_t p, int64_t ldn, int6
           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
       CUDA_SUCCESS)
     return false;
-  constexpr int smem = tma_smem<T>();
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(rowsq_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return false;
-    attr = true;
-  }
   int log2L = 0;
   while ((1 << log2L) < L) ++log2L;
   const int64_t units = L <= 32 ? ceil_div(total_rows, 32 / L) : total_rows;
-  const int64_t blocks = std::min<int64_t>(ceil_div(units, kTmaWarps), 148);
-  rowsq_tma_kernel<T><<<(unsigned)blocks, 32 * kTmaWarps, smem, st>>>(map, total_rows, L, log2L, rowsq);
-  return true;
+  static const int rcfg = [] {
+    const char* e = getenv("BMM_ROWSQ_TMA_CFG");  // A/B switch (tools/cfg4_norms_probe.py)
+    return e ? atoi(e) : -1;
+  }();
+  // default: float32 8 warps x 3 stages of half units (8 KB); float64 8 warps x quarter units
+  const int cfgsel = rcfg >= 0 ? rcfg : 1;
+  auto go = [&](auto kern, int warps, int nbs) {
+    const int smem = warps * kTmaStages * nbs * kTmaBoxBytes + 1024;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+    const int64_t blocks = std::min<int64_t>(ceil_div(units, warps), 148);
+    kern<<<(unsigned)blocks, 32 * warps, smem, st>>>(map, total_rows, L, log2L, rowsq);
+    return true;
+  };
+  if constexpr (sizeof(T) == 4) {
+    switch (cfgsel) {
+      case 0: return go(rowsq_tma_kernel<T, 4, 4>, 4, 4);   // round-1 shape: whole units per stage
+      case 2: return go(rowsq_tma_kernel<T, 16, 1>, 16, 1);
+      default: return go(rowsq_tma_kernel<T, 8, 2>, 8, 2);
+    }
+  } else {
+    if (cfgsel == 2) return go(rowsq_tma_kernel<T, 16, 1>, 16, 1);
+    return go(rowsq_tma_kernel<T, 8, 2>, 8, 2);
+  }
 }
 
 // ---- Any width (e.g. config 2: p = 500, config 3: p = 1000): lane = ROW.  A
@@ -992,28 +1021,32 @@ static bool launch_colsq_tma(const T* M, int64_t m, int64_t n, int64_t ldm, int6
 // chain of NumPy's add.reduce over rows) and one producer warp that streams
 // RB-row slabs of every unit of the CTA into a STAGES-deep ring (full/empty
 // mbarriers).  Rows past m inside the last slab are TMA zero-fill and skipped.
-constexpr int kWideWarps = 28;  // consumer warps per CTA
+constexpr int kWideWarps = 28;  // consumer warps per CTA (at most)
 
-// UPW units (32-column strips) per consumer warp: lane j owns columns j, j+32, ...
-// of the warp's units (UPW independent chains per lane).
-template <typename T, int RB, int STAGES, int UPW>
-__global__ void __launch_bounds__(32 * (kWideWarps + 1), UPW == 1 ? 2 : 1) colsq_wide_kernel(const __grid_constant__ CUtensorMap map,
-                                                                             int64_t m, int64_t n, int64_t units,
+// QB units (32-column strips) per TMA box: a box is 32*QB columns x RB rows, so the
+// single producer thread issues 1/QB as many bulk copies (measured: the copy issue
+// rate, not HBM, bounded the 1-unit boxes at ~4.9 TB/s).  Consumer warp w owns
+// unit w (lane = column): box w / QB, columns 32 * (w % QB) + lane.
+template <typename T, int RB, int STAGES, int QB>
+__global__ void __launch_bounds__(32 * (kWideWarps + 1), 2) colsq_wide_kernel(const __grid_constant__ CUtensorMap map,
+                                                                             int64_t m, int64_t n, int64_t groups,
                                                                              int accumulate, double* __restrict__ colsq) {
-  constexpr int BOX = 32 * RB * (int)sizeof(T);
+  constexpr int BOX = 32 * QB * RB * (int)sizeof(T);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = (int)(blockDim.x >> 5) - 1;  // consumer warps; warp nw produces
-  const int64_t u0 = (int64_t)blockIdx.x * units / gridDim.x, u1 = (int64_t)(blockIdx.x + 1) * units / gridDim.x;
-  const int U = (int)(u1 - u0);
-  const int busy = (U + UPW - 1) / UPW;  // consumer warps with at least one unit
+  // this CTA's boxes: groups [g0, g1) of 32*QB columns
+  const int64_t g0 = (int64_t)blockIdx.x * groups / gridDim.x, g1 = (int64_t)(blockIdx.x + 1) * groups / gridDim.x;
+  const int G = (int)(g1 - g0);
+  const int64_t c_end = min(n, g1 * 32 * QB);                       // columns this CTA owns
+  const int U = (int)((c_end - g0 * 32 * QB + 31) / 32);            // its units (<= G * QB)
   const int64_t slabs = (m + RB - 1) / RB;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm_addr(&full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm_addr(&empty[s])), "r"(busy));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm_addr(&empty[s])), "r"(U));
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -1035,27 +1068,23 @@ __global__ void __launch_bounds__(32 * (kWideWarps + 1), UPW == 1 ? 2 : 1) colsq
               : "memory");
         }
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm_addr(&full[st])),
-                     "r"(U * BOX)
+                     "r"(G * BOX)
                      : "memory");
-        for (int u = 0; u < U; ++u)
+        for (int g = 0; g < G; ++g)
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
-                  sm_addr(smem + (int64_t)(st * U + u) * BOX)),
-              "l"(reinterpret_cast<uint64_t>(&map)), "r"(sm_addr(&full[st])), "r"((int)((u0 + u) * 32)),
+                  sm_addr(smem + (int64_t)(st * G + g) * BOX)),
+              "l"(reinterpret_cast<uint64_t>(&map)), "r"(sm_addr(&full[st])), "r"((int)((g0 + g) * 32 * QB)),
               "r"((int)(q * RB))
               : "memory");
       }
     }
     return;
   }
-  if (warp >= busy) return;
-  double acc[UPW];
-  int64_t col[UPW];
-#pragma unroll
-  for (int j = 0; j < UPW; ++j) {
-    col[j] = (u0 + warp * UPW + j) * 32 + lane;
-    acc[j] = (accumulate && warp * UPW + j < U && col[j] < n) ? colsq[col[j]] : 0.0;
-  }
+  if (warp >= U) return;
+  const int64_t col = g0 * 32 * QB + warp * 32 + lane;
+  double acc = (accumulate && col < n) ? colsq[col] : 0.0;
+  const int bx = warp / QB, sub = (warp % QB) * 32 + lane;
   for (int64_t q = 0; q < slabs; ++q) {
     const int st = (int)(q % STAGES);
     asm volatile(
@@ -1067,42 +1096,44 @@ __global__ void __launch_bounds__(32 * (kWideWarps + 1), UPW == 1 ? 2 : 1) colsq
         "}\n" ::"r"(sm_addr(&full[st])),
         "r"((uint32_t)((q / STAGES) & 1))
         : "memory");
+    const T* slab = reinterpret_cast<const T*>(smem + (int64_t)(st * G + bx) * BOX);
     const int rows = (int)min((int64_t)RB, m - q * RB);
+    double v[RB];
 #pragma unroll
-    for (int j = 0; j < UPW; ++j) {
-      if (warp * UPW + j < U) {
-        const T* slab = reinterpret_cast<const T*>(smem + (int64_t)(st * U + warp * UPW + j) * BOX);
-        double v[RB];
+    for (int r = 0; r < RB; ++r) v[r] = (double)slab[r * 32 * QB + sub];
 #pragma unroll
-        for (int r = 0; r < RB; ++r) v[r] = (double)slab[r * 32 + lane];
-#pragma unroll
-        for (int r = 0; r < RB; ++r)
-          if (r < rows) acc[j] = __dadd_rn(acc[j], __dmul_rn(v[r], v[r]));
-      }
-    }
+    for (int r = 0; r < RB; ++r)
+      if (r < rows) acc = __dadd_rn(acc, __dmul_rn(v[r], v[r]));
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sm_addr(&empty[st])) : "memory");
   }
-#pragma unroll
-  for (int j = 0; j < UPW; ++j)
-    if (warp * UPW + j < U && col[j] < n) colsq[col[j]] = acc[j];
+  if (col < n) colsq[col] = acc;
 }
 
-template <typename T, int RB, int STAGES, int UPW>
-static bool launch_colsq_wide_cfg(const CUtensorMap& map, int64_t m, int64_t n, int accumulate, double* colsq,
+template <typename T, int RB, int STAGES, int QB>
+static bool launch_colsq_wide_cfg(const T* M, int64_t m, int64_t n, int64_t ldm, int accumulate, double* colsq,
                                   cudaStream_t st) {
-  const int64_t units = (n + 31) / 32;
-  // UPW = 1: two CTAs per SM, UPW = 2: one CTA per SM; every unit in ONE wave when
-  // units <= 296 (148) * kWideWarps * UPW -- no tail of half-empty waves
-  const int64_t slots = UPW == 1 ? 296 : 148;
-  int64_t ctas = std::max<int64_t>(slots, ceil_div(units, (int64_t)kWideWarps * UPW));
-  ctas = std::min<int64_t>(ctas, units);
-  const int umax = (int)ceil_div(units, ctas);
-  const int warps = (int)ceil_div(umax, UPW);
-  auto kern = colsq_wide_kernel<T, RB, STAGES, UPW>;
-  const int smem = STAGES * umax * 32 * RB * (int)sizeof(T) + 1024;
+  auto enc = tma_encode_fn();
+  if (enc == nullptr) return false;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+  cuuint64_t strides[1] = {(cuuint64_t)(ldm * sizeof(T))};
+  cuuint32_t box[2] = {(cuuint32_t)(32 * QB), (cuuint32_t)RB};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  if (enc(&map, dt, 2, const_cast<T*>(M), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return false;
+  const int64_t groups = (n + 32 * QB - 1) / (32 * QB);
+  // two CTAs per SM; every group in ONE wave while groups <= 296 * (kWideWarps / QB)
+  int64_t ctas = std::max<int64_t>(296, ceil_div(groups, (int64_t)(kWideWarps / QB)));
+  ctas = std::min<int64_t>(ctas, groups);
+  const int gmax = (int)ceil_div(groups, ctas);
+  auto kern = colsq_wide_kernel<T, RB, STAGES, QB>;
+  const int smem = STAGES * gmax * 32 * QB * RB * (int)sizeof(T) + 1024;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
-  kern<<<(unsigned)ctas, 32 * (warps + 1), smem, st>>>(map, m, n, units, accumulate, colsq);
+  kern<<<(unsigned)ctas, 32 * (gmax * QB + 1), smem, st>>>(map, m, n, groups, accumulate, colsq);
   return true;
 }
 
@@ -1112,30 +1143,20 @@ static bool launch_colsq_wide(const T* M, int64_t m, int64_t n, int64_t ldm, int
   if ((ldm * (int64_t)sizeof(T)) % 16 != 0 || ldm < n || reinterpret_cast<uintptr_t>(M) % 16 != 0 ||
       m >= (1LL << 31) || n >= (1LL << 31))
     return false;
-  auto enc = tma_encode_fn();
-  if (enc == nullptr) return false;
   static const int cfg = [] {
     const char* e = getenv("BMM_COLSQ_WIDE_CFG");  // A/B switch (tools/cfg4_norms_probe.py)
     return e ? atoi(e) : 0;
   }();
-  const int RB = (cfg == 2) ? 4 : 8;
-  CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
-  cuuint64_t strides[1] = {(cuuint64_t)(ldm * sizeof(T))};
-  cuuint32_t box[2] = {32, (cuuint32_t)RB};
-  cuuint32_t estr[2] = {1, 1};
-  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
-  if (enc(&map, dt, 2, const_cast<T*>(M), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-      CUDA_SUCCESS)
-    return false;
-  if constexpr (sizeof(T) == 8) return launch_colsq_wide_cfg<T, 8, 2, 1>(map, m, n, accumulate, colsq, st);
-  switch (cfg) {
-    case 1: return launch_colsq_wide_cfg<T, 8, 3, 2>(map, m, n, accumulate, colsq, st);
-    case 2: return launch_colsq_wide_cfg<T, 4, 6, 1>(map, m, n, accumulate, colsq, st);
-    case 3: return launch_colsq_wide_cfg<T, 8, 2, 2>(map, m, n, accumulate, colsq, st);
-    case 4: return launch_colsq_wide_cfg<T, 8, 4, 2>(map, m, n, accumulate, colsq, st);
-    default: return launch_colsq_wide_cfg<T, 8, 3, 1>(map, m, n, accumulate, colsq, st);
+  if constexpr (sizeof(T) == 8) {
+    if (cfg == 1) return launch_colsq_wide_cfg<T, 8, 2, 1>(M, m, n, ldm, accumulate, colsq, st);
+    return launch_colsq_wide_cfg<T, 8, 2, 4>(M, m, n, ldm, accumulate, colsq, st);
+  } else {
+    switch (cfg) {
+      case 1: return launch_colsq_wide_cfg<T, 8, 3, 1>(M, m, n, ldm, accumulate, colsq, st);
+      case 2: return launch_colsq_wide_cfg<T, 16, 2, 2>(M, m, n, ldm, accumulate, colsq, st);
+      case 3: return launch_colsq_wide_cfg<T, 4, 6, 4>(M, m, n, ldm, accumulate, colsq, st);
+      default: return launch_colsq_wide_cfg<T, 8, 3, 4>(M, m, n, ldm, accumulate, colsq, st);
+    }
   }
 }
 

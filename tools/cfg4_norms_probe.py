@@ -49,11 +49,11 @@ def both_concurrent():
 
 half = 4.0 * m * n
 tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("BMM_")) or "default"
-for name, fn, nb in (
+for name, fn, nb in [(k, f, b) for k, f, b in (
         ("colsq M", lambda: lib.bmm_norms(1, M.data_ptr(), m, n, n, 0, None, p, p, 0, 1, 0, cs.data_ptr(), None, st), half),
         ("rowsq N", lambda: lib.bmm_norms(1, None, m, n, n, 0, N.data_ptr(), p, p, 0, 1, 0, None, rs.data_ptr(), st), half),
         ("bmm_norms M+N", lambda: lib.bmm_norms(1, M.data_ptr(), m, n, n, 0, N.data_ptr(), p, p, 0, 1, 0, cs.data_ptr(),
                                                 rs.data_ptr(), st), 2 * half),
-        ("two streams M||N", both_concurrent, 2 * half)):
+        ("two streams M||N", both_concurrent, 2 * half)) if os.environ.get("BMM_PROBE_ONLY", k) in k]:
     ms = timed(fn)
     print(f"[{tag}] {name:18s} {ms:8.3f} ms {nb / ms / 1e6:7.0f} GB/s ({nb / ms / 1e6 / peak:5.1%})", flush=True)
