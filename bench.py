@@ -856,6 +856,54 @@ def relaunch_distributed(args):
     return subprocess.call(cmd, env=env)
 
 
+def cfg5_cpu_baseline(pipe, CD, Md, Nd, sizes, W, keys, sample=16):
+    """Config 5 on the host: the oracle port (NumPy + BLAS) over `sample`
+    problems spread across the batch, per-problem stages timed and scaled to
+    4096 problems (all BLAS threads and 1 thread; medians of 3).  The same run
+    checks the benched outputs of those problems: budgets, draws and scales
+    bit-exact, C.D within 1e-5 (float32)."""
+    from oracle import blockmm_oracle as O
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    B = len(keys)
+    pick = np.linspace(0, B - 1, sample).astype(int)
+    probs = [(Md[b].cpu().numpy().astype(np.float64), Nd[b].cpu().numpy().astype(np.float64)) for b in pick]
+    worst = 0.0
+    res = {}
+    for label, lim in (("all", None), ("1", 1)):
+        ctx = threadpool_limits(limits=lim) if (threadpool_limits and lim) else None
+        if ctx is not None:
+            ctx.__enter__()
+        try:
+            tots = []
+            for rep in range(3):
+                t0 = time.perf_counter()
+                outs = [O.approx_product(M64, N64, sizes, W, "ONC", workloads.sample_rng(5, int(keys[b])))
+                        for (M64, N64), b in zip(probs, pick)]
+                tots.append((time.perf_counter() - t0) * 1e3 * B / sample)
+        finally:
+            if ctx is not None:
+                ctx.__exit__(None, None, None)
+        res[label] = float(np.median(tots))
+    bud, cols, scl = pipe.budgets_host(), pipe.columns_host(), pipe.scales_host()
+    for b, ref in zip(pick, outs):
+        if not (np.array_equal(bud[b], ref["budgets"]) and np.array_equal(cols[b], ref["columns"])
+                and np.array_equal(scl[b], ref["scale"])):
+            raise RuntimeError(f"cfg5 problem {b}: budgets / draws differ from the oracle")
+        e = float(np.linalg.norm(CD[b].double().cpu().numpy() - ref["CD"]) / np.linalg.norm(ref["CD"]))
+        if e > 1e-5:
+            raise RuntimeError(f"cfg5 problem {b}: C.D rel err {e:.2e}")
+        worst = max(worst, e)
+    cb = {"value": res["all"], "unit": "ms/step", "cores": cpu_cores(), "kind": "port", "value_1thread": res["1"],
+          "median_of": 3, "sample": f"{sample} of the 4096 problems (evenly spread) through oracle.approx_product "
+                                    f"(NumPy + BLAS, float64 upcast), scaled to 4096; wall clock", **cpu_info()}
+    par = {"ok": True, "problems_checked": [int(b) for b in pick], "cd_max_rel_err": worst,
+           "checked": "budgets, every draw and scale bit-exact vs the oracle; C.D within 1e-5 (float32 bar)"}
+    return cb, par
+
+
 def run_device(args):
     """cfg5: 4096 independent problems (per-problem seeds).  Under torchrun the
     problems are split over the ranks (no collective; weak in data, the whole
@@ -911,6 +959,48 @@ def run_device(args):
         t = torch.tensor([ms_step], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
+    first_CD = pipe.run(Md, Nd, seeds()).clone()
+
+    # e2e: this rank's problems from pinned host memory, products back, every step --
+    # 8 sub-batches on their own pipelines so one batch's copy overlaps another's work
+    SUB = 8
+    subs = []
+    per = (B + SUB - 1) // SUB
+    M_pin = torch.empty(Md.shape, dtype=Md.dtype).pin_memory()
+    N_pin = torch.empty(Nd.shape, dtype=Nd.dtype).pin_memory()
+    M_pin.copy_(Md)
+    N_pin.copy_(Nd)
+    out_pin = torch.empty((B, m, p), dtype=torch.float32).pin_memory()
+    copy_s = torch.cuda.Stream()
+    for j in range(SUB):
+        a, bnd = j * per, min(B, (j + 1) * per)
+        if a >= bnd:
+            continue
+        q = SketchPipeline(m, n, p, sizes, W, "ONC", batch=bnd - a, dtype=torch.float32)
+        subs.append((a, bnd, q))
+    def e2e_step():
+        cur = torch.cuda.current_stream()
+        for a, bnd, q in subs:
+            with torch.cuda.stream(copy_s):
+                Md[a:bnd].copy_(M_pin[a:bnd], non_blocking=True)
+                Nd[a:bnd].copy_(N_pin[a:bnd], non_blocking=True)
+            cur.wait_stream(copy_s)
+            ks = keys[a:bnd]
+            q.run(Md[a:bnd], Nd[a:bnd], seeds_from_keys("ONC", workloads.ROOT, (cfg, 1), ks, K))
+            out_pin[a:bnd].copy_(q._result().view(bnd - a, m, p), non_blocking=True)
+    e2e_step()
+    e2e = []
+    for it in range(1 + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_step()
+        torch.cuda.synchronize()
+        if it >= 1:
+            e2e.append((time.perf_counter() - t0) * 1e3)
+    if not torch.equal(out_pin, first_CD.view(B, m, p).cpu()):
+        raise RuntimeError("cfg5 end-to-end products differ from the resident run")
+    e2e_ms = float(np.mean(e2e))
+    del M_pin, N_pin, out_pin, subs
 
     # per-kernel device times (events on the launching stream)
     lib, st = _lib.load(), _lib.stream_ptr()
@@ -1013,10 +1103,17 @@ def run_device(args):
         "rel_err_baseline_metric": float(np.sqrt(err_sq) / fro), "error_scope": scope,
         "clocks": clocks.summary(),
     }
+    line["e2e"] = {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": int(norm_bytes),
+                   "d2h_bytes_per_step": int(B * m * p * 4),
+                   "api": "SketchPipeline.run on 8 sub-batches: pinned host M, N -> device -> pinned host products"}
     if world > 1:
         line["scaling"] = "strong"
         line["config"]["parallelism"] = f"the 4096 problems split over {world} GPUs, no collective"
     if rank == 0:
+        if world == 1:
+            cb, par = cfg5_cpu_baseline(pipe, first_CD, Md, Nd, sizes, W, keys)
+            line["cpu_baseline"] = cb
+            line["parity"] = par
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -1320,7 +1417,8 @@ def run_cfg4(args):
     lib, st = _lib.load(), _lib.stream_ptr()
     P = lambda t: t.data_ptr()  # noqa: E731
 
-    def timed(fn, reps=3):
+    def timed(fn, reps=5):
+        fn()  # warm: tensor maps, function attributes
         out = []
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

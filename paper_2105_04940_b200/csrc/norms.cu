@@ -36,6 +36,16 @@ __device__ __forceinline__ void unpack(const float4& v, double* o) {
   o[0] = (double)v.x; o[1] = (double)v.y; o[2] = (double)v.z; o[3] = (double)v.w;
 }
 
+// acc + x*x with NumPy's rounding: float64 data rounds the square, then the sum
+// (dmul, dadd); float32 data (x exactly representable, x*x exact in 48 bits) has
+// ONE rounding either way, so a fused multiply-add gives the same bits with one
+// float64 instruction fewer per element.
+template <typename T>
+__device__ __forceinline__ double add_sq(double acc, double x) {
+  if constexpr (sizeof(T) == 4) return __fma_rn(x, x, acc);
+  else return __dadd_rn(acc, __dmul_rn(x, x));
+}
+
 template <typename T, int R>
 __global__ void __launch_bounds__(256) colsq_vec_kernel(const T* __restrict__ M, int64_t m, int64_t n,
                                                         int64_t ldm, int64_t strideM, int64_t batch,
@@ -62,7 +72,7 @@ __global__ void __launch_bounds__(256) colsq_vec_kernel(const T* __restrict__ M,
         double x[W];
         unpack(v[r], x);
 #pragma unroll
-        for (int j = 0; j < W; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn(x[j], x[j]));
+        for (int j = 0; j < W; ++j) acc[j] = add_sq<T>(acc[j], x[j]);
       }
     }
     for (; h < m; ++h) {
@@ -70,7 +80,7 @@ __global__ void __launch_bounds__(256) colsq_vec_kernel(const T* __restrict__ M,
       double x[W];
       unpack(v, x);
 #pragma unroll
-      for (int j = 0; j < W; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn(x[j], x[j]));
+      for (int j = 0; j < W; ++j) acc[j] = add_sq<T>(acc[j], x[j]);
     }
 #pragma unroll
     for (int j = 0; j < W; ++j) out[j] = acc[j];
@@ -96,9 +106,9 @@ __global__ void __launch_bounds__(256) colsq_scalar_kernel(const T* __restrict__
 #pragma unroll
       for (int r = 0; r < R; ++r) v[r] = (double)base[(h + r) * ldm];
 #pragma unroll
-      for (int r = 0; r < R; ++r) acc = __dadd_rn(acc, __dmul_rn(v[r], v[r]));
+      for (int r = 0; r < R; ++r) acc = add_sq<T>(acc, v[r]);
     }
-    for (; h < m; ++h) { double x = (double)base[h * ldm]; acc = __dadd_rn(acc, __dmul_rn(x, x)); }
+    for (; h < m; ++h) { double x = (double)base[h * ldm]; acc = add_sq<T>(acc, x); }
     colsq[b * n + c] = acc;
   }
 }
@@ -487,7 +497,7 @@ __global__ void __launch_bounds__(32 * WARPS) rowsq_tma_kernel(const __grid_cons
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const double d = (double)f[k];
-            r[4 * h + k] = __dadd_rn(r[4 * h + k], __dmul_rn(d, d));
+            r[4 * h + k] = add_sq<T>(r[4 * h + k], d);
           }
         } else {
           const double2 a = *reinterpret_cast<const double2*>(p);
@@ -867,7 +877,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) colsq_tma_kernel(const __grid_c
       for (int r = 0; r < kCsRows; ++r) v[r] = r < rows ? (double)slab[r * 32 + lane] : 0.0;
 #pragma unroll
       for (int r = 0; r < kCsRows; ++r)
-        if (r < rows) acc = __dadd_rn(acc, __dmul_rn(v[r], v[r]));
+        if (r < rows) acc = add_sq<T>(acc, v[r]);
       __syncwarp();  // slot is refilled by the issue of a later iteration
     }
     if (col < n) colsq[b * n + col] = acc;
@@ -933,7 +943,7 @@ __global__ void __launch_bounds__(32 * WARPS) colsq_tma_cta_kernel(const __grid_
       for (int r = 0; r < ROWS; ++r) v[r] = r < rows ? (double)slab[r * COLS + threadIdx.x] : 0.0;
 #pragma unroll
       for (int r = 0; r < ROWS; ++r)
-        if (r < rows) acc = __dadd_rn(acc, __dmul_rn(v[r], v[r]));
+        if (r < rows) acc = add_sq<T>(acc, v[r]);
       __syncthreads();  // every warp is done with the slot before it is refilled
     }
     if (col < n) colsq[b * n + col] = acc;
@@ -1103,7 +1113,7 @@ __global__ void __launch_bounds__(32 * (kWideWarps + 1), 2) colsq_wide_kernel(co
     for (int r = 0; r < RB; ++r) v[r] = (double)slab[r * 32 * QB + sub];
 #pragma unroll
     for (int r = 0; r < RB; ++r)
-      if (r < rows) acc = __dadd_rn(acc, __dmul_rn(v[r], v[r]));
+      if (r < rows) acc = add_sq<T>(acc, v[r]);
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sm_addr(&empty[st])) : "memory");
   }

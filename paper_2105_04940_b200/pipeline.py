@@ -735,16 +735,24 @@ class PipelineGroup:
             self._active(False)
 
     def _fork_stats(self, cap, M, N, chunks=None):
-        """Enqueue the shared statistics on their own stream (forked from `cap`);
-        returns (events after the block probabilities, after g_k^2, the stream)."""
+        """Enqueue the shared statistics on their own streams (forked from `cap`):
+        the norm pass and block probabilities on one, OPL's g_k^2 (which needs only
+        M and N) concurrently on another.  Returns (event after the probabilities,
+        event after probabilities AND g_k^2, the joined stream)."""
         ss = torch.cuda.Stream(priority=-1)
         ss.wait_stream(cap)
         ev_p, ev_g = torch.cuda.Event(), torch.cuda.Event()
-        with torch.cuda.stream(ss):
-            done = self.shared.launch_probs(M, N, chunks)
-            ev_p.record(ss)
-            if not done:
+        gs = None
+        if chunks is None and self.shared.needs_gsq:
+            gs = torch.cuda.Stream(priority=-1)
+            gs.wait_stream(cap)
+            with torch.cuda.stream(gs):
                 self.shared.launch_gsq(M, N)
+        with torch.cuda.stream(ss):
+            self.shared.launch_probs(M, N, chunks)  # chunked: g_k^2 per landed chunk in here
+            ev_p.record(ss)
+            if gs is not None:
+                ss.wait_stream(gs)
             ev_g.record(ss)
         return ev_p, ev_g, ss
 

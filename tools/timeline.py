@@ -24,7 +24,8 @@ seeds = lambda: [seeds_from_rngs(m, [workloads.sample_rng(2, cb)], len(sizes)) f
 group.run(Md, Nd, seeds())
 start = torch.zeros(1, dtype=torch.int64, device="cuda")
 end = torch.zeros(1, dtype=torch.int64, device="cuda")
-for p in pipes:
+sh = group.shared  # the shared statistics stage (norms, probabilities, g_k once per step)
+for p in pipes + ([sh] if sh is not None else []):
     p.stamps = (torch.zeros(256, dtype=torch.int64, device="cuda"), [])
 lib = _lib.load()
 # capture: a stamp at the start (before the fork) and one after the join
@@ -34,14 +35,20 @@ side.wait_stream(torch.cuda.current_stream())
 with torch.cuda.stream(side):
     group._launch_all(Md, Nd)
 torch.cuda.current_stream().wait_stream(side)
-for p in pipes:
+for p in pipes + ([sh] if sh is not None else []):
     p.stamps[1].clear()
 streams = group._branch_streams()
+group._active(True)
 with torch.cuda.graph(g):
     cap = torch.cuda.current_stream()
     lib.bmm_timestamp(start.data_ptr(), _lib.stream_ptr())
+    evs = None
+    if sh is not None:
+        *evs, ss = group._fork_stats(cap, Md, Nd)
+        streams.append(ss)
     for s, p in zip(streams, pipes):
         s.wait_stream(cap)
+        group._member_wait(s, p, evs)
         with torch.cuda.stream(s):
             p.launch(Md, Nd)
     for jg in group._jgroups:
@@ -64,7 +71,12 @@ for r in range(reps):
     torch.cuda.synchronize()
     t0 = int(start.item())
     rows.append((t0, int(end.item()), [(p.stamps[1], p.stamps[0][:len(p.stamps[1])].cpu().numpy() - t0) for p in pipes]))
+group._active(False)
 t0, t1, br = rows[-1]
+if sh is not None:
+    names, ts = sh.stamps[1], sh.stamps[0][:len(sh.stamps[1])].cpu().numpy() - t0
+    print("shared  stats   done at " + f"{ts[-1] / 1e3:7.1f} us | " +
+          " ".join(f"{nm.replace('bmm_', '')}:{t / 1e3:.0f}" for nm, t in zip(names, ts)))
 print(f"step (stamp to stamp): {(t1 - t0) / 1e3:.1f} us  (reps: {[round((b - a) / 1e3, 1) for a, b, _ in rows]})")
 for (cb, W, meth), (names, ts) in zip(runs, br):
     prev = 0
