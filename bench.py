@@ -1487,12 +1487,14 @@ def run_cfg4(args):
                            "achieved": norm_bytes / (norms_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                            "frac": norm_bytes / (norms_ms * 1e-3) / 1e9 / hbm_peak, "algorithmic_bytes": norm_bytes,
                            "colsq_ms": cs_ms, "rowsq_ms": rs_ms, "ms": norms_ms,
-                           "traffic": tr.get("norms"), "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+                           "traffic": tr.get("norms"), "traffic_src": tr.get("src"),
+                           "peak_source": "MEASURED_PEAKS.json hbm_gbs (a copy: read + write)"},
         "roofline_gram": {"bound": "tensor", "kernel": "segsq_gram_kernel (OPL g_k^2 = <M^k'M^k, N_k N_k'>, DMMA)",
                           "ms": gram_ms, "flops": gram_flops,
                           "f64_tflops": gram_flops / (gram_ms * 1e-3) / 1e12,
                           "hbm_gbs": norm_bytes / (gram_ms * 1e-3) / 1e9,
-                          "note": "reads M and N once (34.4 GB): bound by max(HBM, DMMA)"},
+                          "note": "reads M and N once (34.4 GB): bound by max(HBM, DMMA)",
+                          "traffic": tr.get("gram")},
         "roofline_gather": {"bound": "hbm", "kernel": "gather_a_split_kernel + gather_bt_split_kernel (K4)",
                             "ms": gather_ms, "algorithmic_bytes": gather_bytes,
                             "achieved": sum(gather_bytes) / (sum(gather_ms) * 1e-3) / 1e9, "peak": hbm_peak,
