@@ -1479,15 +1479,12 @@ def run_cfg4(args):
                                                P(sh.gsq), st))
     gather_ms, gemm_ms, kexec, kdist = [], [], [], []
     for pipe in group.pipes:
-        W = pipe.W
-        gather_ms.append(timed(lambda: lib.bmm_gather_f32split_dk(
-            1, P(Md), n, 0, P(Nd), p, 0, m, p, P(pipe.k_column), P(pipe.k_scale), W, W, P(pipe.k_count), 1,
-            P(pipe.a_hi), P(pipe.a_x), P(pipe.b_hi), P(pipe.b_x), st)))
-        gemm_ms.append(timed(lambda: lib.bmm_gemm_f32split_dk(P(pipe.a_hi), P(pipe.a_x), P(pipe.b_hi), P(pipe.b_x),
-                                                              m, p, W, P(pipe.k_count), 1, P(pipe.CD), p, m * p, st)))
+        gather_ms.append(timed(lambda: pipe.split_gather(Md, Nd, st)))
+        gemm_ms.append(timed(lambda: pipe.split_gemm(st)))
         kd = int(pipe.k_count[0].item())
         kdist.append(kd)
-        kexec.append((kd + 31) // 32 * 32)
+        step = 64 if pipe.f16 else 32
+        kexec.append((kd + step - 1) // step * step)
 
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peak.get("hbm_gbs", 6538.6))
@@ -1496,8 +1493,13 @@ def run_cfg4(args):
     traffic = json.loads((ROOT / "profiles" / "traffic.json").read_text()) \
         if (ROOT / "profiles" / "traffic.json").exists() else {}
     norm_bytes = 4 * (m * n + n * p)
-    useful = [2.0 * m * p * k for k in kexec]  # over the distinct drawn columns (padded to 32)
-    executed = [2 * u for u in useful]          # one TF32 K=8 + one BF16 K=16 MMA (equal cycles) per 8 K
+    useful = [2.0 * m * p * k for k in kexec]  # over the distinct drawn columns (padded to the K step)
+    f16 = all(q.f16 for q in group.pipes)
+    # executed tensor work: fp16 split = 3 kind::f16 MMAs (K=16) per 16 K, at the dense fp16/bf16 rate;
+    # tf32 split = one TF32 K=8 + one BF16 K=16 MMA (equal cycles) per 8 K, at the dense TF32 rate
+    executed = [3 * u for u in useful] if f16 else [2 * u for u in useful]
+    if f16:
+        tf32_burst, tf32_sust = 2 * tf32_burst, 2 * tf32_sust  # dense fp16 = MEASURED bf16 rates
     gemm_tot = sum(gemm_ms)
     gemm_ach = sum(executed) / (gemm_tot * 1e-3) / 1e12
     gather_bytes = [4 * (m + p) * kd + 8 * (m + p) * ke for kd, ke in zip(kdist, kexec)]
@@ -1514,14 +1516,19 @@ def run_cfg4(args):
                    "step": "one shared norm pass + block probabilities + Gram g_k, then three approximate products",
                    "distinct_columns": kdist, "l2": "inputs 34.4 GB >> 126 MB L2 (no flush needed)"},
         "gpu_launches": int(group.graph_launches),
-        "roofline": {"bound": "tensor", "kernel": "gemm_f32split_kernel (tcgen05 kind::tf32 h*h + kind::f16 "
-                                                  "cross terms, 128x128 tiles, TMA SWIZZLE_128B)",
+        "roofline": {"bound": "tensor",
+                     "kernel": ("gemm_f16split_2sm_kernel (tcgen05.mma.cta_group::2 kind::f16: fp16 h.h + [h|l].[l|h] "
+                                "pairs, 256x256 tiles per CTA pair, TMA SWIZZLE_128B)") if f16 else
+                               "gemm_f32split_2sm_kernel (tcgen05.mma.cta_group::2 kind::tf32 h.h + kind::f16 pairs)",
                      "achieved": gemm_ach, "peak": tf32_sust, "unit": "TFLOP/s", "frac": gemm_ach / tf32_sust,
                      "frac_of_burst": gemm_ach / tf32_burst,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained / 2 (dense TF32 issues at half the "
-                                    "BF16 rate; sustained: the kernel runs inside a ~0.2 s step)",
-                     "algorithmic": "executed = 2 x 2*m*p*k per launch, k = distinct drawn columns padded to 32 "
-                                    "(one TF32 K8 and one BF16 K16 MMA per 8 k)",
+                     "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (dense fp16 = bf16 rate)" if f16 else
+                                     "MEASURED_PEAKS.json bf16_tflops_sustained / 2 (dense TF32)") +
+                                    "; sustained: the kernel runs inside a ~0.2 s step",
+                     "algorithmic": ("executed = 3 x 2*m*p*k per launch, k = distinct drawn columns padded to 64 "
+                                     "(three kind::f16 K16 MMAs per 16 k)") if f16 else
+                                    ("executed = 2 x 2*m*p*k per launch, k = distinct drawn columns padded to 32 "
+                                     "(one TF32 K8 and one BF16 K16 MMA per 8 k)"),
                      "useful_fp32_tflops": sum(useful) / (gemm_tot * 1e-3) / 1e12,
                      "launch_ms": gemm_ms, "share_of_step": gemm_tot / ms_step,
                      "traffic": tr.get("gemm_f32split"), "traffic_src": tr.get("src")},

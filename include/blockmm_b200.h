@@ -428,6 +428,30 @@ int bmm_gather_f32split(int dtype, const void* M, int64_t ldm, int64_t strideM,
 int bmm_gemm_f32split(const float* a_hi, const void* a_x, const float* b_hi, const void* b_x,
                       int64_t m, int64_t nc, int64_t k, int64_t batch,
                       float* out, int64_t ldo, int64_t strideO, void* stream);
+/* F16 split for the CTA-pair contraction (config 4 sizes): C.D for float32 data
+ * (estimators.py:175) with every sketch value x = h + l, h = fp16(y), l = fp16(y - h),
+ * y = x * 2^(kexp[t] - gshift[b]) for C and 2^(-kexp[t] - gshift[b]) for D (exact
+ * powers of two: the balanced exponents keep both operands inside fp16's range).
+ * bmm_balance_f16: kexp from the norm pass (colsq/rowsq, n_stride per problem)
+ *   and the sketch scales, gshift per problem so that |y| < 2^15; 0 past k_dev.
+ * bmm_gather_f16split_dk: a_h (fp16, rows x W), a_x (fp16 pairs [h|l] per 8
+ *   columns, rows x 2W), b_h / b_x for D^T with pairs [l|h]; columns zero-padded
+ *   to a multiple of 64 past k_dev (the contraction's K step).  Buffers of the
+ *   float32 split (a_hi/a_x/b_hi/b_x) are large enough.
+ * bmm_gemm_f16split_dk: out[b] = 2^(2 gshift[b]) * (a . b^T) on CTA pairs
+ *   (tcgen05.mma.cta_group::2, 256 x 256 tiles), 3 kind::f16 MMAs per 16 K.    */
+int bmm_balance_f16(const double* colsq, const double* rowsq, int64_t n_stride, const int64_t* column,
+                    const double* scale, int64_t w, int64_t w_stride, const int64_t* k_dev, int64_t batch,
+                    int32_t* kexp, int32_t* gshift, void* stream);
+int bmm_gather_f16split_dk(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
+                           int64_t ldn, int64_t strideN, int64_t m, int64_t p, const int64_t* column,
+                           const double* scale, const int32_t* kexp, const int32_t* gshift, int64_t W,
+                           int64_t w_stride, const int64_t* w_dev, int64_t batch, void* a_h, void* a_x,
+                           void* b_h, void* b_x, void* stream);
+int bmm_gemm_f16split_dk(const void* a_h, const void* a_x, const void* b_h, const void* b_x, int64_t m,
+                         int64_t nc, int64_t k_max, const int64_t* k_dev, const int32_t* gshift,
+                         int64_t batch, float* out, int64_t ldo, int64_t strideO, void* stream);
+
 /* Compressed-sketch variants (bmm_compress_sketch): the gather writes and the
  * contraction reads only the first ceil(count[b] / 32) * 32 sketch columns of
  * problem b (the compression zero-pads the scales past the count).          */

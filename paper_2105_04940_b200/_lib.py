@@ -104,6 +104,10 @@ SIGNATURES = {
     "bmm_gather_f32split_dk": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _P, _I64,
                                     _P, _P, _P, _P, _P]),
     "bmm_gemm_f32split_dk": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P]),
+    "bmm_balance_f16": (_I, [_P, _P, _I64, _P, _P, _I64, _I64, _P, _I64, _P, _P, _P]),
+    "bmm_gather_f16split_dk": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _P,
+                                    _I64, _P, _P, _P, _P, _P]),
+    "bmm_gemm_f16split_dk": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _I64, _P, _I64, _I64, _P]),
     "bmm_gemm_f32split": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _I64, _P]),
     "bmm_timestamp": (_I, [_P, _P]),
     "bmm_gemm_f32split_gather": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _P, _I64,

@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 #include <type_traits>
@@ -501,6 +502,232 @@ __global__ void __launch_bounds__(32 * P_WARPS, 1) gemm_f32split_2sm_kernel(
   }
 }
 
+// ---- F16 split, CTA pairs (round 2): C (fp16 h, [h|l] pairs) . D^T (fp16 h,
+// [l|h] pairs), operands scaled by the balanced exponents and the problem's
+// shift (bmm_balance_f16).  Per 16 K-elements: one kind::f16 MMA for h.h (K=16)
+// and two for the cross terms on pairs (K=16 over 8 elements each) -- three
+// tensor instructions where the TF32 form needs four -- and 6 operand bytes per
+// element instead of 8.  Stage = 64 K: A_h (1 SWIZZLE_128B tile of 128 rows x
+// 64 fp16), A_x (2 tiles: pairs of elements 0-31 and 32-63), B_h, B_x likewise:
+// 96 KB per CTA, 2 stages; accumulators promoted every 128 K as above.
+// power of two 2^k as a float (|k| <= 126)
+__device__ __forceinline__ float pow2f(int k) { return __int_as_float((127 + k) << 23); }
+
+constexpr int H_BK = 64;
+constexpr int H_TILE = 128 * 128;  // 16 KB
+constexpr int H_STAGES = 2;
+constexpr int H_STAGE = 6 * H_TILE;
+constexpr int H_SMEM = H_STAGES * H_STAGE + 1024 + 256;
+constexpr int H_CHUNK = 2;  // stages per promotion chunk (128 K)
+
+template <int M_, int N_>
+constexpr uint32_t idesc_f16_mn() {  // kind::f16, A/B F16, D F32, K-major
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N_ >> 3) << 17) | ((uint32_t)(M_ >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(32 * P_WARPS, 1) gemm_f16split_2sm_kernel(
+    const __grid_constant__ CUtensorMap tm_ah, const __grid_constant__ CUtensorMap tm_ax,
+    const __grid_constant__ CUtensorMap tm_bh, const __grid_constant__ CUtensorMap tm_bx, int64_t m, int64_t nc,
+    int64_t k, float* __restrict__ out, int64_t ldo, int64_t strideO, const int64_t* __restrict__ kdev,
+    const int32_t* __restrict__ gshift) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + H_STAGES * H_STAGE);
+  uint64_t* empty = full + H_STAGES;
+  uint64_t* acc_full = empty + H_STAGES;   // [2]
+  uint64_t* acc_empty = acc_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = blockIdx.z;
+  uint32_t rank;
+  asm("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  constexpr int GROUP_M = 8;
+  int tile_m, tile_n;
+  {
+    const int tm = gridDim.y, tn = gridDim.x / 2;
+    const int lin = blockIdx.y * tn + blockIdx.x / 2;
+    const int group = lin / (GROUP_M * tn);
+    const int first_m = group * GROUP_M;
+    const int gsz = min(tm - first_m, GROUP_M);
+    tile_m = first_m + (lin % (GROUP_M * tn)) % gsz;
+    tile_n = (lin % (GROUP_M * tn)) / gsz;
+  }
+  if (kdev != nullptr) {
+    const int64_t kd = ((kdev[b] + H_BK - 1) / H_BK) * H_BK;
+    k = kd < k ? kd : k;
+  }
+  const int a_row0 = (int)(b * m + (int64_t)tile_m * 256 + 128 * rank);
+  const int b_row0 = (int)(b * nc + (int64_t)tile_n * 256 + 128 * rank);
+  const int ktiles = (int)((k + H_BK - 1) / H_BK);
+  const int nchunks = (ktiles + H_CHUNK - 1) / H_CHUNK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < H_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&acc_full[q], 1);
+      mbar_init(&acc_empty[q], 2 * P_DRAIN);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_ah)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_ax)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_bh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_bx)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t full0 = cluster_addr(&full[0], 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % H_STAGES;
+        if (kt >= H_STAGES) mbar_wait(&empty[s], ((kt / H_STAGES) - 1) & 1);
+        uint8_t* st = smem + s * H_STAGE;
+        if (rank == 0) mbar_expect_tx(&full[s], 2 * H_STAGE);
+        const uint32_t fb = full0 + (uint32_t)(s * sizeof(uint64_t));
+        const int kc = kt * H_BK;
+        tma_load_2d_2sm(st + 0 * H_TILE, &tm_ah, fb, kc, a_row0);
+        tma_load_2d_2sm(st + 1 * H_TILE, &tm_ax, fb, 2 * kc, a_row0);
+        tma_load_2d_2sm(st + 2 * H_TILE, &tm_ax, fb, 2 * kc + H_BK, a_row0);
+        tma_load_2d_2sm(st + 3 * H_TILE, &tm_bh, fb, kc, b_row0);
+        tma_load_2d_2sm(st + 4 * H_TILE, &tm_bx, fb, 2 * kc, b_row0);
+        tma_load_2d_2sm(st + 5 * H_TILE, &tm_bx, fb, 2 * kc + H_BK, b_row0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_f16_mn<256, 256>();
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % H_STAGES;
+        const int chunk = kt / H_CHUNK, q = chunk & 1;
+        const bool first = (kt % H_CHUNK) == 0;
+        if (first && chunk >= 2) mbar_wait(&acc_empty[q], ((chunk >> 1) - 1) & 1);
+        mbar_wait(&full[s], (kt / H_STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t base = su32(smem + s * H_STAGE);
+        const uint32_t acc = tmem + (uint32_t)(q * 256);
+#pragma unroll
+        for (int kk = 0; kk < H_BK / 16; ++kk) {
+          // h.h over elements 16kk .. 16kk+15 (32 bytes of the 128-byte swizzle row)
+          umma2_bf16(acc, umma_desc_sw128(base + 0 * H_TILE + kk * 32), umma_desc_sw128(base + 3 * H_TILE + kk * 32),
+                     idesc, !(first && kk == 0));
+#pragma unroll
+          for (int g = 2 * kk; g < 2 * kk + 2; ++g) {  // pair groups of 8 elements: h_x.l_y + l_x.h_y
+            const uint32_t off = (uint32_t)((g >> 2) * H_TILE + (g & 3) * 32);
+            umma2_bf16(acc, umma_desc_sw128(base + 1 * H_TILE + off), umma_desc_sw128(base + 4 * H_TILE + off),
+                       idesc, 1);
+          }
+        }
+        umma2_commit_mc(&empty[s]);
+        if ((kt % H_CHUNK) == H_CHUNK - 1 || kt == ktiles - 1) umma2_commit_mc(&acc_full[q]);
+      }
+    }
+  } else {
+    constexpr int DC = 128;
+    const int quarter = warp & 3;
+    const int half = (warp - 2) / 4;
+    const uint32_t ae0 = cluster_addr(&acc_empty[0], 0);
+    float sum[DC];
+#pragma unroll
+    for (int c = 0; c < DC; ++c) sum[c] = 0.f;
+    for (int chunk = 0; chunk < nchunks; ++chunk) {
+      const int q = chunk & 1;
+      mbar_wait(&acc_full[q], (chunk >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < DC; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(q * 256 + half * DC + c), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum[c + j] += __uint_as_float(v[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(
+                         ae0 + (uint32_t)(q * sizeof(uint64_t)))
+                     : "memory");
+    }
+    const float unscale = pow2f(2 * gshift[b]);  // undo 2^-G on both operands (exact)
+    const int64_t row = (int64_t)tile_m * 256 + 128 * rank + quarter * 32 + lane;
+    if (row < m) {
+      float* orow = out + b * strideO + row * ldo;
+      const int64_t col0 = (int64_t)tile_n * 256 + half * DC;
+      const bool vec = (col0 + DC <= nc) && (ldo % 4) == 0 && ((reinterpret_cast<uintptr_t>(orow + col0) & 15) == 0);
+      if (vec) {
+        float4* o4 = reinterpret_cast<float4*>(orow + col0);
+#pragma unroll
+        for (int j = 0; j < DC / 4; ++j)
+          o4[j] = make_float4(sum[4 * j] * unscale, sum[4 * j + 1] * unscale, sum[4 * j + 2] * unscale,
+                              sum[4 * j + 3] * unscale);
+      } else {
+#pragma unroll
+        for (int j = 0; j < DC; ++j)
+          if (col0 + j < nc) orow[col0 + j] = sum[j] * unscale;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+  }
+}
+
+// balanced exponents and the problem's shift for the F16 split: kexp[t] =
+// round(log2(||N_i|| / ||M_i||) / 2) (i = column[t]), gshift[b] such that every
+// scaled operand |C[h,t]| 2^(kexp - G), |D[t,f]| 2^(-kexp - G) < 2^15 -- bounded by
+// the column / row norms from the norm pass times the sketch scale.
+__global__ void __launch_bounds__(256) f16_balance_kernel(const double* __restrict__ colsq,
+                                                          const double* __restrict__ rowsq, int64_t n_stride,
+                                                          const int64_t* __restrict__ column,
+                                                          const double* __restrict__ scale, int64_t w,
+                                                          int64_t w_stride, const int64_t* __restrict__ kdev,
+                                                          int32_t* __restrict__ kexp, int32_t* __restrict__ gshift) {
+  __shared__ int red[8];
+  const int64_t b = blockIdx.x;
+  const int64_t kd = kdev != nullptr ? min(kdev[b], w) : w;
+  int emax = -100000;
+  for (int64_t t = threadIdx.x; t < w; t += blockDim.x) {
+    int32_t e = 0;
+    if (t < kd) {
+      const int64_t i = column[b * w_stride + t];
+      const double c = colsq[b * n_stride + i], r = rowsq[b * n_stride + i], sc = fabs(scale[b * w_stride + t]);
+      if (c > 0.0 && r > 0.0 && sc > 0.0 && c < 1e300 && r < 1e300 && sc < 1e300) {
+        const int d = ilogb(r) - ilogb(c);
+        e = (int32_t)((d >= 0 ? d + 2 : d - 2) / 4);
+        e = max(-60, min(60, e));
+        const double bc = ldexp(sqrt(c) * sc, e), bd = ldexp(sqrt(r) * sc, -e);
+        emax = max(emax, ilogb(fmax(bc, bd)) + 1);
+      }
+    }
+    kexp[b * w_stride + t] = e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = emax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int v = red[0];
+    for (int j = 1; j < (int)(blockDim.x >> 5); ++j) v = max(v, red[j]);
+    gshift[b] = v <= -100000 ? 0 : max(-60, min(60, v - 15));
+  }
+}
+
 // ---- split gather (K4 for the float32 path)
 
 // position of element t inside its row of bf16 pairs: group t/8 holds 16 bf16
@@ -529,60 +756,97 @@ __device__ __forceinline__ void split_rna(float x, float& hi, float& lo) {
 // are loaded once per thread, and every row's stores are coalesced.
 constexpr int A_ROWS = 32;
 
-template <typename T>
+// F16 (round 2, the CTA-pair contraction): x = h + l with h = fp16_rn(y),
+// l = fp16_rn(y - h), y = x * 2^(kexp[t] - gshift) -- the sketch column scaled by the
+// norm-balanced exponent (C column up, D row down by the same power of two) and the
+// problem's shift that keeps |y| < 2^15 (bmm_balance_f16); both exact.  Two fp16
+// halves carry 22 bits (the tf32 + bf16 form: 21) and one kind::f16 MMA of K = 16
+// does the work of two kind::tf32 MMAs of K = 8 for the leading products.
+__device__ __forceinline__ void split_f16(float y, float& hi, float& lo) {
+  const __half h = __float2half_rn(y);
+  hi = __half2float(h);
+  lo = __half2float(__float2half_rn(y - hi));
+}
+
+template <typename T, bool F16 = false>
 __global__ void __launch_bounds__(256) gather_a_split_kernel(const T* __restrict__ M, int64_t ldm, int64_t strideM,
                                                              int64_t m, const int64_t* __restrict__ column,
                                                              const double* __restrict__ scale, int64_t W,
                                                              int64_t w_stride, float* __restrict__ ahi,
                                                              __nv_bfloat16* __restrict__ ax,
-                                                             const int64_t* __restrict__ wdev) {
+                                                             const int64_t* __restrict__ wdev,
+                                                             const int32_t* __restrict__ kexp = nullptr,
+                                                             const int32_t* __restrict__ gshift = nullptr) {
+  constexpr int KPAD = F16 ? 64 : 32;  // the contraction's K step
   const int64_t b = blockIdx.z;
   const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
   const int64_t h0 = (int64_t)blockIdx.y * A_ROWS;
   if (t >= W) return;
-  if (wdev != nullptr && t >= ((wdev[b] + 31) / 32) * 32) return;  // past the GEMM's K of a compressed sketch
+  if (wdev != nullptr && t >= ((wdev[b] + KPAD - 1) / KPAD) * KPAD) return;  // past the GEMM's K
   const int64_t col = column[b * w_stride + t];
   const double sc = scale[b * w_stride + t];
   const T* src = M + b * strideM + col;
   const int64_t h1 = min(m, h0 + A_ROWS);
-  float* oh = ahi + (b * m) * W + t;
-  __nv_bfloat16* ox = ax + (b * m) * 2 * W + pair_pos(t);
   const float scf = (float)sc;
+  if constexpr (F16) {
+    const float f2 = pow2f(kexp[b * w_stride + t] - gshift[b]);
+    __half* oh = reinterpret_cast<__half*>(ahi) + (b * m) * W + t;
+    __half* ox = reinterpret_cast<__half*>(ax) + (b * m) * 2 * W + pair_pos(t);
 #pragma unroll 8
-  for (int64_t h = h0; h < h1; ++h) {
-    float hi, lo;
-    if constexpr (sizeof(T) == 4) {
-      split_rna(__fmul_rn(__ldg(src + h * ldm), scf), hi, lo);  // float32 inputs: no float64 conversions
-    } else {
-      split_tf32(__dmul_rn(ld_d(src + h * ldm), sc), hi, lo);
+    for (int64_t h = h0; h < h1; ++h) {
+      float x;
+      if constexpr (sizeof(T) == 4) x = __fmul_rn(__ldg(src + h * ldm), scf);
+      else x = (float)__dmul_rn(ld_d(src + h * ldm), sc);
+      float hi, lo;
+      split_f16(__fmul_rn(x, f2), hi, lo);
+      oh[h * W] = __float2half_rn(hi);
+      ox[h * 2 * W] = __float2half_rn(hi);  // [h_x | l_x]
+      ox[h * 2 * W + 8] = __float2half_rn(lo);
     }
-    oh[h * W] = hi;
-    ox[h * 2 * W] = __float2bfloat16_rn(hi);      // [h_x | l_x]
-    ox[h * 2 * W + 8] = __float2bfloat16_rn(lo);
+  } else {
+    float* oh = ahi + (b * m) * W + t;
+    __nv_bfloat16* ox = ax + (b * m) * 2 * W + pair_pos(t);
+#pragma unroll 8
+    for (int64_t h = h0; h < h1; ++h) {
+      float hi, lo;
+      if constexpr (sizeof(T) == 4) {
+        split_rna(__fmul_rn(__ldg(src + h * ldm), scf), hi, lo);  // float32 inputs: no float64 conversions
+      } else {
+        split_tf32(__dmul_rn(ld_d(src + h * ldm), sc), hi, lo);
+      }
+      oh[h * W] = hi;
+      ox[h * 2 * W] = __float2bfloat16_rn(hi);      // [h_x | l_x]
+      ox[h * 2 * W + 8] = __float2bfloat16_rn(lo);
+    }
   }
 }
 
 // b_hi / b_x for rows of D^T (D = N[column, :] * scale[:, None]): a CTA stages
 // a 32 (t) x 128 (f) tile through shared memory -- 512-byte coalesced row
 // reads of N, coalesced writes of the transposed operand.
-template <typename T>
+template <typename T, bool F16 = false>
 __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restrict__ N, int64_t ldn, int64_t strideN,
                                                               int64_t p, const int64_t* __restrict__ column,
                                                               const double* __restrict__ scale, int64_t W,
                                                               int64_t w_stride, float* __restrict__ bhi,
                                                               __nv_bfloat16* __restrict__ bx,
-                                                              const int64_t* __restrict__ wdev) {
+                                                              const int64_t* __restrict__ wdev,
+                                                              const int32_t* __restrict__ kexp = nullptr,
+                                                              const int32_t* __restrict__ gshift = nullptr) {
+  constexpr int KPAD = F16 ? 64 : 32;
   __shared__ float sh[32][129], sl[32][129];
   __shared__ int64_t scol[32];
   __shared__ double sscale[32];
+  __shared__ float sf2[32];
   const int64_t b = blockIdx.z;
   const int64_t t0 = (int64_t)blockIdx.x * 32, f0 = (int64_t)blockIdx.y * 128;
-  if (wdev != nullptr && t0 >= ((wdev[b] + 31) / 32) * 32) return;  // whole CTA past the compressed K
+  if (wdev != nullptr && t0 >= ((wdev[b] + KPAD - 1) / KPAD) * KPAD) return;  // whole CTA past the compressed K
   const int tid = threadIdx.x;
   if (tid < 32) {
     const int64_t t = t0 + tid;
     scol[tid] = t < W ? column[b * w_stride + t] : 0;
     sscale[tid] = t < W ? scale[b * w_stride + t] : 0.0;
+    if constexpr (F16) sf2[tid] = t < W ? pow2f(-kexp[b * w_stride + t] - gshift[b]) : 0.f;
   }
   __syncthreads();
   // reads: 32 lanes x 4 consecutive f per row (16-byte loads when the rows allow),
@@ -612,8 +876,15 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
     for (int e = 0; e < 4; ++e) {
       float hi = 0.f, lo = 0.f;
       if (t0 + i < W && f0 + fq + e < p) {
-        if constexpr (sizeof(T) == 4) split_rna(__fmul_rn((float)v[r][e], (float)sscale[i]), hi, lo);
-        else split_tf32(__dmul_rn(v[r][e], sscale[i]), hi, lo);
+        if constexpr (F16) {
+          const float x = sizeof(T) == 4 ? __fmul_rn((float)v[r][e], (float)sscale[i])
+                                         : (float)__dmul_rn((double)v[r][e], sscale[i]);
+          split_f16(__fmul_rn(x, sf2[i]), hi, lo);
+        } else if constexpr (sizeof(T) == 4) {
+          split_rna(__fmul_rn((float)v[r][e], (float)sscale[i]), hi, lo);
+        } else {
+          split_tf32(__dmul_rn(v[r][e], sscale[i]), hi, lo);
+        }
       }
       sh[i][fq + e] = hi;
       sl[i][fq + e] = lo;
@@ -631,12 +902,20 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
     const int64_t f = f0 + i;
     if (f < p) {
       const int64_t row = b * p + f;
-      if (t < W) bhi[row * W + t] = sh[tx][i];
+      if constexpr (F16) {
+        if (t < W) reinterpret_cast<__half*>(bhi)[row * W + t] = __float2half_rn(sh[tx][i]);
+      } else {
+        if (t < W) bhi[row * W + t] = sh[tx][i];
+      }
       if (t0 + tl < W) {
         const float a = is_h ? sh[tl][i] : sl[tl][i];
         const float c = is_h ? sh[tl + 1][i] : sl[tl + 1][i];
-        *reinterpret_cast<__nv_bfloat162*>(bx + row * 2 * W + 2 * t0 + 2 * tx) =
-            __halves2bfloat162(__float2bfloat16_rn(a), __float2bfloat16_rn(c));
+        if constexpr (F16)
+          *reinterpret_cast<__half2*>(reinterpret_cast<__half*>(bx) + row * 2 * W + 2 * t0 + 2 * tx) =
+              __halves2half2(__float2half_rn(a), __float2half_rn(c));
+        else
+          *reinterpret_cast<__nv_bfloat162*>(bx + row * 2 * W + 2 * t0 + 2 * tx) =
+              __halves2bfloat162(__float2bfloat16_rn(a), __float2bfloat16_rn(c));
       }
     }
   }
@@ -1120,6 +1399,108 @@ static int gemm_split_impl(const float* a_hi, const void* a_x, const float* b_hi
                                                                          ldo, strideO, k_dev);
   }
   BMM_CHECK_LAUNCH("gemm_f32split_kernel");
+  return BMM_OK;
+}
+
+static int make_map_f16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols) {
+  auto enc = get_encode();
+  BMM_REQUIRE(enc != nullptr, BMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)H_BK, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BMM_REQUIRE(r == CUDA_SUCCESS, BMM_E_CUDA, "cuTensorMapEncodeTiled (f16) failed (%d)", (int)r);
+  return BMM_OK;
+}
+
+extern "C" int bmm_balance_f16(const double* colsq, const double* rowsq, int64_t n_stride, const int64_t* column,
+                               const double* scale, int64_t w, int64_t w_stride, const int64_t* k_dev, int64_t batch,
+                               int32_t* kexp, int32_t* gshift, void* stream) {
+  BMM_REQUIRE(colsq && rowsq && column && scale && kexp && gshift && w >= 1 && batch >= 1 && w_stride >= w,
+              BMM_E_ARG, "bmm_balance_f16: bad arguments");
+  f16_balance_kernel<<<(unsigned)batch, 256, 0, as_stream(stream)>>>(colsq, rowsq, n_stride, column, scale, w,
+                                                                      w_stride, k_dev, kexp, gshift);
+  BMM_CHECK_LAUNCH("f16_balance_kernel");
+  return BMM_OK;
+}
+
+extern "C" int bmm_gather_f16split_dk(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
+                                      int64_t ldn, int64_t strideN, int64_t m, int64_t p, const int64_t* column,
+                                      const double* scale, const int32_t* kexp, const int32_t* gshift, int64_t W,
+                                      int64_t w_stride, const int64_t* w_dev, int64_t batch, void* a_h, void* a_x,
+                                      void* b_h, void* b_x, void* stream) {
+  BMM_REQUIRE(m >= 1 && p >= 1 && W >= 1 && batch >= 1, BMM_E_ARG, "bmm_gather_f16split_dk: bad shape");
+  BMM_REQUIRE(W % 8 == 0, BMM_E_UNSUPPORTED, "bmm_gather_f16split_dk: W must be a multiple of 8");
+  BMM_REQUIRE(kexp && gshift && column && scale, BMM_E_ARG, "bmm_gather_f16split_dk: null pointer");
+  BMM_REQUIRE(batch <= 65535 && ceil_div(m, A_ROWS) <= 65535, BMM_E_UNSUPPORTED,
+              "bmm_gather_f16split_dk: grid too large");
+  cudaStream_t st = as_stream(stream);
+  dim3 agrid((unsigned)ceil_div(W, 256), (unsigned)ceil_div(m, A_ROWS), (unsigned)batch);
+  dim3 tgrid((unsigned)ceil_div(W, 32), (unsigned)ceil_div(p, 128), (unsigned)batch);
+  float* ah = (float*)a_h;
+  float* bh = (float*)b_h;
+  __nv_bfloat16* ax = (__nv_bfloat16*)a_x;
+  __nv_bfloat16* bx = (__nv_bfloat16*)b_x;
+  if (dtype == BMM_F32) {
+    gather_a_split_kernel<float, true><<<agrid, 256, 0, st>>>((const float*)M, ldm, strideM, m, column, scale, W,
+                                                              w_stride, ah, ax, w_dev, kexp, gshift);
+    BMM_CHECK_LAUNCH("gather_a_split_kernel<f16>");
+    gather_bt_split_kernel<float, true><<<tgrid, 256, 0, st>>>((const float*)N, ldn, strideN, p, column, scale, W,
+                                                               w_stride, bh, bx, w_dev, kexp, gshift);
+  } else if (dtype == BMM_F64) {
+    gather_a_split_kernel<double, true><<<agrid, 256, 0, st>>>((const double*)M, ldm, strideM, m, column, scale, W,
+                                                               w_stride, ah, ax, w_dev, kexp, gshift);
+    BMM_CHECK_LAUNCH("gather_a_split_kernel<f16>");
+    gather_bt_split_kernel<double, true><<<tgrid, 256, 0, st>>>((const double*)N, ldn, strideN, p, column, scale,
+                                                                W, w_stride, bh, bx, w_dev, kexp, gshift);
+  } else {
+    set_error("bmm_gather_f16split_dk: unknown dtype %d", dtype);
+    return BMM_E_ARG;
+  }
+  BMM_CHECK_LAUNCH("gather_bt_split_kernel<f16>");
+  return BMM_OK;
+}
+
+extern "C" int bmm_gemm_f16split_dk(const void* a_h, const void* a_x, const void* b_h, const void* b_x, int64_t m,
+                                    int64_t nc, int64_t k_max, const int64_t* k_dev, const int32_t* gshift,
+                                    int64_t batch, float* out, int64_t ldo, int64_t strideO, void* stream) {
+  BMM_REQUIRE(m >= 1 && nc >= 1 && k_max >= 1 && batch >= 1 && gshift != nullptr, BMM_E_ARG,
+              "bmm_gemm_f16split_dk: bad shape");
+  BMM_REQUIRE(k_max % 8 == 0, BMM_E_UNSUPPORTED, "bmm_gemm_f16split_dk: k must be a multiple of 8");
+  BMM_REQUIRE(batch * m < (1LL << 31) && batch * nc < (1LL << 31) && batch <= 65535, BMM_E_UNSUPPORTED,
+              "bmm_gemm_f16split_dk: problem too large for 32-bit TMA coordinates");
+  CUtensorMap ma_h, ma_x, mb_h, mb_x;
+  int rc;
+  if ((rc = make_map_f16(&ma_h, a_h, batch * m, k_max)) != BMM_OK) return rc;
+  if ((rc = make_map_f16(&ma_x, a_x, batch * m, 2 * k_max)) != BMM_OK) return rc;
+  if ((rc = make_map_f16(&mb_h, b_h, batch * nc, k_max)) != BMM_OK) return rc;
+  if ((rc = make_map_f16(&mb_x, b_x, batch * nc, 2 * k_max)) != BMM_OK) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_f16split_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, H_SMEM);
+    attr = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(2 * ceil_div(nc, 256)), (unsigned)ceil_div(m, 256), (unsigned)batch);
+  lc.blockDim = dim3(32 * P_WARPS, 1, 1);
+  lc.dynamicSmemBytes = H_SMEM;
+  lc.stream = as_stream(stream);
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = 2;
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = 1;
+  lc.attrs = la;
+  lc.numAttrs = 1;
+  if (cudaLaunchKernelEx(&lc, gemm_f16split_2sm_kernel, ma_h, ma_x, mb_h, mb_x, m, nc, k_max, out, ldo, strideO,
+                         k_dev, gshift) != cudaSuccess) {
+    set_error("bmm_gemm_f16split_dk: cluster launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return BMM_E_CUDA;
+  }
+  BMM_CHECK_LAUNCH("gemm_f16split_2sm_kernel");
   return BMM_OK;
 }
 

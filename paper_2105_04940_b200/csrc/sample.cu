@@ -437,8 +437,8 @@ __global__ void __launch_bounds__(kCompactThreads) sketch_compact_kernel(
     }
     pos += __popc(mk);
   }
-  // zero padding up to the next multiple of 32 (the float32 contraction's K step)
-  const int64_t pad_end = min(W, ((total + 31) / 32) * 32);
+  // zero padding up to the next multiple of 64 (the float32 contractions' K steps: 32, 64)
+  const int64_t pad_end = min(W, ((total + 63) / 64) * 64);
   for (int64_t u = total + tid; u < pad_end; u += kCompactThreads) {
     oc[u] = 0;
     os[u] = 0.0;

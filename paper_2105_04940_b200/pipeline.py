@@ -211,6 +211,13 @@ class SketchPipeline:
         # small float32 outputs (at most 4 x 4 tiles of 128): gather inside the contraction
         # (bmm_gemm_f32split_gather); large ones would re-gather A once per column tile
         self.fused = self.tf32 and self.compress and f32_fused(self.m, self.p)
+        # large float32 outputs: the fp16 split on CTA pairs (3 tensor instructions per 16 K
+        # instead of 4; BMM_F16=0 keeps the tf32 + bf16 split)
+        self.f16 = (self.tf32 and self.compress and not self.fused and self.m >= 256 and self.p >= 512
+                    and os.environ.get("BMM_F16", "1") != "0")
+        if self.f16:
+            self.kexp = torch.zeros(B * W, dtype=torch.int32, device=dev)
+            self.gshift = torch.zeros(B, dtype=torch.int32, device=dev)
         if self.tf32:
             f32 = dict(dtype=torch.float32, device=dev)
             if not self.fused:
@@ -468,12 +475,9 @@ class SketchPipeline:
             self._c("bmm_gemm_f32split_gather", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
                     P(self.k_scale), W, W, P(self.k_count), B, P(self.CD), p, m * p, st)
         elif self.tf32 and self.compress:
-            # float32 inputs: split gather + tcgen05 TF32 / BF16-cross-term contraction
-            self._c("bmm_gather_f32split_dk", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
-                    P(self.k_scale), W, W, P(self.k_count), B, P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x),
-                    st)
-            self._c("bmm_gemm_f32split_dk", P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), m, p, W,
-                    P(self.k_count), B, P(self.CD), p, m * p, st)
+            # float32 inputs: split gather + tcgen05 contraction (fp16 or tf32 + bf16 split)
+            self.split_gather(M, N, st)
+            self.split_gemm(st)
         elif self.tf32:
             self._c("bmm_gather_f32split", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column), P(self.scale), W, W,
                     B, P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), st)
@@ -482,6 +486,36 @@ class SketchPipeline:
         else:
             self.contract(M, N, st)
         return self._result()
+
+    def split_gather(self, M, N, st=None):
+        """The float32 path's split gather of the compressed sketch (K4)."""
+        B, m, n, p, W = self.B, self.m, self.n, self.p, self.W
+        st = _lib.stream_ptr() if st is None else st
+        dt = _lib.matrix_dtype(M)
+        ldm, ldn = M.stride(-2), N.stride(-2)
+        P = lambda t: t.data_ptr()  # noqa: E731
+        if self.f16:
+            self._c("bmm_balance_f16", P(self.colsq), P(self.rowsq), n, P(self.k_column), P(self.k_scale), W, W,
+                    P(self.k_count), B, P(self.kexp), P(self.gshift), st)
+            self._c("bmm_gather_f16split_dk", dt, P(M), ldm, m * n, P(N), ldn, n * p, m, p, P(self.k_column),
+                    P(self.k_scale), P(self.kexp), P(self.gshift), W, W, P(self.k_count), B, P(self.a_hi),
+                    P(self.a_x), P(self.b_hi), P(self.b_x), st)
+        else:
+            self._c("bmm_gather_f32split_dk", dt, P(M), ldm, m * n, P(N), ldn, n * p, m, p, P(self.k_column),
+                    P(self.k_scale), W, W, P(self.k_count), B, P(self.a_hi), P(self.a_x), P(self.b_hi),
+                    P(self.b_x), st)
+
+    def split_gemm(self, st=None):
+        """The float32 path's tcgen05 contraction of the split operands (K6)."""
+        B, m, p, W = self.B, self.m, self.p, self.W
+        st = _lib.stream_ptr() if st is None else st
+        P = lambda t: t.data_ptr()  # noqa: E731
+        if self.f16:
+            self._c("bmm_gemm_f16split_dk", P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), m, p, W,
+                    P(self.k_count), P(self.gshift), B, P(self.CD), p, m * p, st)
+        else:
+            self._c("bmm_gemm_f32split_dk", P(self.a_hi), P(self.a_x), P(self.b_hi), P(self.b_x), m, p, W,
+                    P(self.k_count), B, P(self.CD), p, m * p, st)
 
     def contract(self, M, N, st=None):
         """C @ D of the current sketch on the float64 path (gather + DMMA GEMM, or

@@ -136,3 +136,52 @@ def test_fused_gather_gemm(B, m, n, p, W):
         e_fused = ((out.double() - full).norm() / full.norm()).item()
         e_two = ((two.double() - full).norm() / full.norm()).item()
         assert e_fused < 1e-5 and e_two < 1e-5, (e_fused, e_two)
+
+
+@pytest.mark.parametrize("B,m,p,n,W,spread", [(1, 256, 512, 3000, 1024, 1.0), (2, 300, 520, 2000, 2048, 4.0),
+                                              (1, 512, 768, 5000, 4096, 8.0), (1, 256, 1024, 999, 32768, 2.0)])
+def test_f16_split_pair_contraction(B, m, p, n, W, spread):
+    """The fp16 split on CTA pairs (bmm_balance_f16 + bmm_gather_f16split_dk +
+    bmm_gemm_f16split_dk) on compressed sketches: distinct counts not a multiple
+    of 64, a zero column, lognormal column / row scales of wide spread (the
+    balanced exponents and the shift must keep both operands in fp16 range),
+    partial pair tiles and batches -- against float64 of the same float32 sketch
+    (C = fl32(M * s), D = fl32(N * s)) within 1e-5."""
+    g = torch.Generator(device="cuda").manual_seed(B * 7 + m + p + W)
+    M = torch.randn((B, m, n), generator=g, device="cuda") * torch.exp(spread * torch.randn((B, 1, n), generator=g, device="cuda"))
+    N = torch.randn((B, n, p), generator=g, device="cuda") * torch.exp(spread * torch.randn((B, n, 1), generator=g, device="cuda"))
+    M[:, :, 3] = 0.0  # a zero column of M
+    colsq = (M.double() ** 2).sum(1).reshape(-1)
+    rowsq = (N.double() ** 2).sum(2).reshape(-1)
+    cnt = [min(W, n, 1000 + 37 * b + (W // 3)) for b in range(B)]
+    col = torch.zeros((B, W), dtype=torch.int64, device="cuda")
+    sc = torch.zeros((B, W), dtype=torch.float64, device="cuda")
+    for b in range(B):
+        c = torch.sort(torch.randperm(n, generator=g, device="cuda")[:cnt[b]]).values
+        col[b, :cnt[b]] = c
+        sc[b, :cnt[b]] = torch.rand(cnt[b], generator=g, device="cuda", dtype=torch.float64) * 50 + 0.01
+    kd = torch.as_tensor(cnt, dtype=torch.int64, device="cuda")
+    kexp = torch.zeros((B, W), dtype=torch.int32, device="cuda")
+    gsh = torch.zeros(B, dtype=torch.int32, device="cuda")
+    st = _lib.stream_ptr()
+    _lib.call("bmm_balance_f16", colsq.data_ptr(), rowsq.data_ptr(), n, col.data_ptr(), sc.data_ptr(), W, W,
+              kd.data_ptr(), B, kexp.data_ptr(), gsh.data_ptr(), st)
+    ah = torch.full((B * m * W,), float("nan"), dtype=torch.float32, device="cuda")  # garbage past the K step
+    ax = torch.full_like(ah, float("nan"))
+    bh = torch.full((B * p * W,), float("nan"), dtype=torch.float32, device="cuda")
+    bx = torch.full_like(bh, float("nan"))
+    _lib.call("bmm_gather_f16split_dk", _lib.BMM_F32, M.data_ptr(), n, m * n, N.data_ptr(), p, n * p, m, p,
+              col.data_ptr(), sc.data_ptr(), kexp.data_ptr(), gsh.data_ptr(), W, W, kd.data_ptr(), B,
+              ah.data_ptr(), ax.data_ptr(), bh.data_ptr(), bx.data_ptr(), st)
+    out = torch.empty((B, m, p), dtype=torch.float32, device="cuda")
+    _lib.call("bmm_gemm_f16split_dk", ah.data_ptr(), ax.data_ptr(), bh.data_ptr(), bx.data_ptr(), m, p, W,
+              kd.data_ptr(), gsh.data_ptr(), B, out.data_ptr(), p, m * p, st)
+    torch.cuda.synchronize()
+    for b in range(B):
+        c, s = col[b, :cnt[b]], sc[b, :cnt[b]]
+        C = (M[b][:, c] * s.float()).double()          # the float32 sketch values
+        D = (N[b][c, :] * s.float()[:, None]).double()
+        ref = C @ D
+        err = ((out[b].double() - ref).norm() / ref.norm()).item()
+        assert err < 1e-5, (b, err)
+        assert torch.isfinite(out[b]).all()
