@@ -1048,23 +1048,22 @@ def run_device(args):
 
     norms_ms = timed(lambda: lib.bmm_norms(1, P(Md), m, n, n, m * n, P(Nd), p, p, n * p, B, 0, P(pipe.colsq),
                                            P(pipe.rowsq), st))
-    gather_ms = timed(lambda: lib.bmm_gather_f32split_dk(1, P(Md), n, m * n, P(Nd), p, n * p, m, p,
-                                                       P(pipe.k_column), P(pipe.k_scale), W, W, P(pipe.k_count), B,
-                                                       P(pipe.a_hi), P(pipe.a_x), P(pipe.b_hi), P(pipe.b_x), st))
-    gemm_ms = timed(lambda: lib.bmm_gemm_f32split_dk(P(pipe.a_hi), P(pipe.a_x), P(pipe.b_hi), P(pipe.b_x), m, p, W,
-                                                   P(pipe.k_count), B, P(pipe.CD), p, m * p, st))
+    gather_ms = timed(lambda: pipe.split_gather(Md, Nd, st))
+    gemm_ms = timed(lambda: pipe.split_gemm(st))
     kcounts = pipe.k_count.cpu().numpy()
-    k_exec = int((((kcounts + 31) // 32) * 32).sum())  # columns the compressed contraction runs over
+    kstep = 64 if pipe.f16 else 32
+    k_exec = int((((kcounts + kstep - 1) // kstep) * kstep).sum())  # columns the compressed contraction runs over
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peak.get("hbm_gbs", 6650.0))
-    tf32_peak = float(peak.get("bf16_tflops", 1590.0)) / 2  # dense TF32 issues at half the BF16 rate
+    tf32_peak = float(peak.get("bf16_tflops", 1590.0)) / (1 if pipe.f16 else 2)  # dense fp16 / TF32 rate
     norm_bytes = 4 * B * (m * n + n * p)
     useful = 2.0 * m * p * k_exec  # over the distinct drawn columns (compressed sketch, padded to 32)
-    executed = 2 * useful  # one TF32 K=8 MMA + one BF16 K=16 MMA (same cycles) per 8 K-elements
+    # fp16 split: three kind::f16 K=16 MMAs per 16 K; tf32 split: one TF32 K=8 + one BF16 K=16 per 8 K
+    executed = (3 if pipe.f16 else 2) * useful
     # the split gather: reads the sampled elements of M and N, writes the split operands
     # (8 bytes per element: tf32 hi in a float32 container + the bf16 pair word)
     k_distinct = int(kcounts.sum())
-    split_bytes = 8 * (m + p) * k_exec
+    split_bytes = (6 if pipe.f16 else 8) * (m + p) * k_exec
     gather_bytes = 4 * (m + p) * k_distinct + split_bytes
     roof_gather = {"bound": "hbm", "kernel": "gather_a_split_kernel + gather_bt_split_kernel (K4, float32 split)",
                    "achieved": gather_bytes / (gather_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",

@@ -213,7 +213,7 @@ class SketchPipeline:
         self.fused = self.tf32 and self.compress and f32_fused(self.m, self.p)
         # large float32 outputs: the fp16 split on CTA pairs (3 tensor instructions per 16 K
         # instead of 4; BMM_F16=0 keeps the tf32 + bf16 split)
-        self.f16 = (self.tf32 and self.compress and not self.fused and self.m >= 256 and self.p >= 512
+        self.f16 = (self.tf32 and self.compress and not self.fused and self.m >= 256 and self.p >= 256
                     and os.environ.get("BMM_F16", "1") != "0")
         if self.f16:
             self.kexp = torch.zeros(B * W, dtype=torch.int32, device=dev)
