@@ -518,13 +518,14 @@ constexpr int H_TILE = 128 * 128;  // 16 KB
 constexpr int H_STAGES = 2;
 constexpr int H_STAGE = 6 * H_TILE;
 constexpr int H_SMEM = H_STAGES * H_STAGE + 1024 + 256;
-constexpr int H_CHUNK = 2;  // stages per promotion chunk (128 K)
+constexpr int H_CHUNK_DEFAULT = 2;  // stages per promotion chunk (128 K)
 
 template <int M_, int N_>
 constexpr uint32_t idesc_f16_mn() {  // kind::f16, A/B F16, D F32, K-major
   return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N_ >> 3) << 17) | ((uint32_t)(M_ >> 4) << 24);
 }
 
+template <int H_CHUNK>
 __global__ void __launch_bounds__(32 * P_WARPS, 1) gemm_f16split_2sm_kernel(
     const __grid_constant__ CUtensorMap tm_ah, const __grid_constant__ CUtensorMap tm_ax,
     const __grid_constant__ CUtensorMap tm_bh, const __grid_constant__ CUtensorMap tm_bx, int64_t m, int64_t nc,
@@ -1478,9 +1479,17 @@ extern "C" int bmm_gemm_f16split_dk(const void* a_h, const void* a_x, const void
   if ((rc = make_map_f16(&ma_x, a_x, batch * m, 2 * k_max)) != BMM_OK) return rc;
   if ((rc = make_map_f16(&mb_h, b_h, batch * nc, k_max)) != BMM_OK) return rc;
   if ((rc = make_map_f16(&mb_x, b_x, batch * nc, 2 * k_max)) != BMM_OK) return rc;
+  // promotion chunk: 128 K (default) or 256 K (BMM_F16_CHUNK=4: half the TMEM drain traffic)
+  static const int chunk = [] {
+    const char* e = getenv("BMM_F16_CHUNK");
+    return e ? atoi(e) : H_CHUNK_DEFAULT;
+  }();
+  auto kern = chunk == 4 ? gemm_f16split_2sm_kernel<4> : gemm_f16split_2sm_kernel<H_CHUNK_DEFAULT>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_f16split_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, H_SMEM);
+    cudaFuncSetAttribute(gemm_f16split_2sm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, H_SMEM);
+    cudaFuncSetAttribute(gemm_f16split_2sm_kernel<H_CHUNK_DEFAULT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         H_SMEM);
     attr = true;
   }
   cudaLaunchConfig_t lc = {};
@@ -1495,8 +1504,8 @@ extern "C" int bmm_gemm_f16split_dk(const void* a_h, const void* a_x, const void
   la[0].val.clusterDim.z = 1;
   lc.attrs = la;
   lc.numAttrs = 1;
-  if (cudaLaunchKernelEx(&lc, gemm_f16split_2sm_kernel, ma_h, ma_x, mb_h, mb_x, m, nc, k_max, out, ldo, strideO,
-                         k_dev, gshift) != cudaSuccess) {
+  if (cudaLaunchKernelEx(&lc, kern, ma_h, ma_x, mb_h, mb_x, m, nc, k_max, out, ldo, strideO, k_dev, gshift) !=
+      cudaSuccess) {
     set_error("bmm_gemm_f16split_dk: cluster launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     return BMM_E_CUDA;
   }
