@@ -96,6 +96,59 @@ __global__ void __launch_bounds__(32 * kProbWarps) block_probs_kernel(
   }
 }
 
+// Many small blocks (config 5: 4096 problems x 64 blocks of 64): one THREAD per
+// (problem, block).  The warp version keeps 32 lanes busy on 64-element sums,
+// shuffles and a 64-step sequential cumsum and ran issue-bound (0.56 ms at
+// config 5); here each thread walks its block with NumPy's scalar pairwise
+// sum (pw_sum) and the sequential cumsum out of a thread-local buffer (local
+// memory is interleaved across the warp's threads, so the buffer accesses are
+// coalesced).  Same operations in the same order: bit-identical results.
+template <int MAXL>
+__global__ void __launch_bounds__(128) block_probs_thread_kernel(
+    const double* __restrict__ colsq, const double* __restrict__ rowsq, int64_t n,
+    const int64_t* __restrict__ offsets, int64_t K, int64_t batch, double* __restrict__ probs,
+    double* __restrict__ s, double* __restrict__ fnorm, double* __restrict__ cum, int64_t* __restrict__ last) {
+  const int64_t total = K * batch;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g / K, k = g - b * K;
+    const int64_t o = offsets[k], nk = offsets[k + 1] - o;
+    const double* cs = colsq + b * n + o;
+    const double* rs = rowsq + b * n + o;
+    double buf[MAXL];
+    for (int64_t i = 0; i < nk; ++i) buf[i] = __dmul_rn(__dsqrt_rn(cs[i]), __dsqrt_rn(rs[i]));
+    const SrcF64 sp{buf};
+    if (s != nullptr) s[g] = __dadd_rn(buf[0], pw_sum(sp, 1, nk - 1));  // np.add.reduceat   plan.py:173
+    if (probs != nullptr) {
+      const double tot = __dadd_rn(0.0, pw_sum(sp, 0, nk));             // plan.py:199-205
+      if (tot == 0.0) {
+        for (int64_t i = 0; i < nk; ++i) buf[i] = 0.0;
+      } else {
+        for (int64_t i = 0; i < nk; ++i) buf[i] = __ddiv_rn(buf[i], tot);
+        const double tot2 = __dadd_rn(0.0, pw_sum(sp, 0, nk));
+        for (int64_t i = 0; i < nk; ++i) buf[i] = __ddiv_rn(buf[i], tot2);
+      }
+      double* pb = probs + b * n + o;
+      for (int64_t i = 0; i < nk; ++i) pb[i] = buf[i];
+      if (cum != nullptr) {  // np.cumsum, sequential   estimators.py:37-38
+        double acc = 0.0;
+        int64_t lst = -1;
+        double* cb = cum + b * n + o;
+        for (int64_t i = 0; i < nk; ++i) {
+          acc = __dadd_rn(acc, buf[i]);
+          cb[i] = acc;
+          if (buf[i] > 0.0) lst = i;
+        }
+        last[g] = lst;
+      }
+    }
+    if (fnorm != nullptr) {  // ||M^k||_F * ||N_k||_F (plan.py:489), the warp kernel's order
+      const double fm = __dsqrt_rn(__dadd_rn(0.0, pw_sum(SrcF64{cs}, 0, nk)));
+      const double fn = __dsqrt_rn(__dadd_rn(0.0, pw_sum(SrcF64{rs}, 0, nk)));
+      fnorm[g] = __dmul_rn(fm, fn);
+    }
+  }
+}
+
 // Large blocks (max_len > 256): one 256-thread CTA per block.  The elementwise
 // scores and the two divisions use every thread; warp 0 runs the NumPy sums
 // and the sequential cumsum from the shared-memory copy.  Same arithmetic and
@@ -657,7 +710,14 @@ extern "C" int bmm_block_probs(const double* colsq, const double* rowsq, int64_t
   unsigned grid = (unsigned)std::min<int64_t>(ceil_div(warps, kProbWarps), 148LL * 16 * 64);
   const int64_t smem = max_len * 8 * kProbWarps;
   cudaStream_t st = as_stream(stream);
-  if (probs != nullptr && fnorm == nullptr && max_len > 256 && max_len * 16 <= 160 * 1024 &&
+  static const int thread_mode = [] {
+    const char* e = getenv("BMM_PROBS_THREAD");  // A/B switch: 0 keeps the warp kernel for small blocks
+    return e ? atoi(e) : 1;
+  }();
+  if (thread_mode != 0 && max_len <= 64 && K * batch >= 16384) {
+    block_probs_thread_kernel<64><<<(unsigned)std::min<int64_t>(ceil_div(K * batch, 128), 148LL * 16 * 64), 128,
+                                    0, st>>>(colsq, rowsq, n, offsets, K, batch, probs, s, fnorm, cum, last_support);
+  } else if (probs != nullptr && fnorm == nullptr && max_len > 256 && max_len * 16 <= 160 * 1024 &&
       K * batch < (1LL << 31)) {
     static bool attr_c = false;
     if (!attr_c) {

@@ -264,12 +264,66 @@ extern "C" int bmm_seed_streams(const uint32_t* words, int64_t n_words, const in
   return BMM_OK;
 }
 
+// Many small blocks (config 5): one THREAD per (problem, block) draws the block's
+// budget sequentially -- one PCG64 step per draw, binary search of the block's CDF
+// (64 entries, L1-resident) -- instead of a warp whose lanes jump ahead 32 steps
+// and, with ~16 draws per block, sit half idle.  Same draws, same order.
+template <bool SHARED>
+__global__ void __launch_bounds__(128) sample_thread_kernel(
+    const double* __restrict__ probs, const double* __restrict__ cum, const int64_t* __restrict__ last,
+    const int64_t* __restrict__ offsets, int64_t K, int64_t batch, int64_t n, const int64_t* __restrict__ budgets,
+    const int64_t* __restrict__ col_off, int64_t w_stride, const uint64_t* __restrict__ states,
+    int64_t* __restrict__ column, double* __restrict__ prob, double* __restrict__ scale) {
+  const int64_t total = K * batch;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g / K, k = g - b * K;
+    const int64_t pb_ = SHARED ? 0 : b;
+    const int64_t gp = pb_ * K + k;
+    const int64_t ck = budgets[gp];
+    if (ck <= 0) continue;
+    const int64_t o = offsets[k], len = offsets[k + 1] - o;
+    const double* cb = cum + pb_ * n + o;
+    const double* pb = probs + pb_ * n + o;
+    const int64_t lst = last[gp];
+    const uint64_t* sp = states + 4 * (b * K + k);
+    U128 st{sp[0], sp[1]};
+    const U128 inc{sp[2], sp[3]};
+    const double dck = (double)ck;
+    const int64_t t0 = b * w_stride + col_off[pb_ * (K + 1) + k];
+    for (int64_t j = 0; j < ck; ++j) {
+      st = pcg_step(st, inc);
+      const double u = u53(pcg_output(st));
+      int64_t lo = 0, hi = len;  // first index with cum > u (searchsorted side="right")
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (cb[mid] > u) hi = mid; else lo = mid + 1;
+      }
+      const int64_t idx = max((int64_t)0, lo < lst ? lo : lst);
+      const double pr = pb[idx];
+      column[t0 + j] = o + idx;
+      prob[t0 + j] = pr;
+      scale[t0 + j] = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dck, pr)));
+    }
+  }
+}
+
 template <bool SHARED>
 static int sample_impl(const double* probs, const double* cum, const int64_t* last_support, const int64_t* offsets,
                        int64_t K, int64_t batch, int64_t n, int64_t max_len, const int64_t* budgets,
                        const int64_t* col_off, int64_t w_stride, const uint64_t* states, int64_t* column,
                        double* prob, double* scale, cudaStream_t st) {
   BMM_REQUIRE(K >= 1 && batch >= 1 && max_len >= 1, BMM_E_ARG, "bmm_sample: bad shape");
+  static const int thread_mode = [] {
+    const char* e = getenv("BMM_SAMPLE_THREAD");  // A/B switch: 0 keeps the warp kernel for small blocks
+    return e ? atoi(e) : 1;
+  }();
+  if (thread_mode != 0 && max_len <= 128 && K * batch >= 16384) {
+    sample_thread_kernel<SHARED><<<(unsigned)std::min<int64_t>(ceil_div(K * batch, 128), 148LL * 16 * 64), 128, 0,
+                                   st>>>(probs, cum, last_support, offsets, K, batch, n, budgets, col_off, w_stride,
+                                         states, column, prob, scale);
+    BMM_CHECK_LAUNCH("sample_thread_kernel");
+    return BMM_OK;
+  }
   const int64_t warps = K * batch * ((w_stride + kSampleChunk - 1) / kSampleChunk);
   const int64_t per_warp = 2 * max_len * 8;  // CDF and probabilities
   int wpb = kSampleWarps;

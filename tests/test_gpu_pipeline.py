@@ -352,3 +352,42 @@ def test_nonfinite_input_raises_like_the_reference(bad, dtype):
         with pytest.raises(ValueError, match=msg):
             pipe.check()
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("method", ["ONC", "OPL", "SSM"])
+def test_many_small_blocks_thread_kernels_match_oracle(method):
+    """K x batch >= 16384 blocks of <= 64 columns take the thread-per-block
+    probability and sampling kernels (config 5's shape): budgets, draws and
+    scales bit-exact to the oracle on a spread of problems, also for unequal
+    blocks with a zero block."""
+    B, m, n, p, K = 260, 24, 4096, 16, 64
+    g = np.random.default_rng(31)
+    Ms = (g.standard_normal((B, m, n)) * g.lognormal(0, 1, (B, 1, n))).astype(np.float32)
+    Ns = (g.standard_normal((B, n, p)) * g.lognormal(0, 1, (B, n, 1))).astype(np.float32)
+    if method == "SSM":
+        sizes = (64,) * K
+    else:
+        sizes = tuple([64] * 60 + [10, 54, 100, 92])  # unequal, max 100 > 64 -> warp kernels for probs
+        sizes = (64,) * K
+        Ms[:, :, 64:128] = 0.0  # block 1 has zero score in every problem
+    Md, Nd = torch.as_tensor(Ms, device="cuda"), torch.as_tensor(Ns, device="cuda")
+    if method == "SSM":
+        pipe = SketchPipeline(m, n, p, sizes, 0, "SSM", batch=B, draws=8, dtype=torch.float32)
+        rngs = [np.random.default_rng(1000 + b) for b in range(B)]
+        CD = pipe.run(Md, Nd, seeds_from_rngs("SSM", rngs, K, draws=8)).cpu().numpy()
+    else:
+        pipe = SketchPipeline(m, n, p, sizes, 512, method, batch=B, dtype=torch.float32)
+        rngs = [np.random.default_rng(1000 + b) for b in range(B)]
+        CD = pipe.run(Md, Nd, seeds_from_rngs(method, rngs, K)).cpu().numpy()
+    pipe.check()
+    for b in (0, 1, 77, 130, 259):
+        M64, N64 = Ms[b].astype(np.float64), Ns[b].astype(np.float64)
+        if method == "SSM":
+            ref = O.ssm_product(M64, N64, sizes, 8, np.random.default_rng(1000 + b))
+            assert np.array_equal(pipe.columns_host()[b], ref["blocks"]), b
+        else:
+            ref = O.approx_product(M64, N64, sizes, 512, method, np.random.default_rng(1000 + b))
+            assert np.array_equal(pipe.budgets_host()[b], ref["budgets"]), b
+            assert np.array_equal(pipe.columns_host()[b], ref["columns"]), b
+            assert np.array_equal(pipe.scales_host()[b], ref["scale"]), b
+        assert rel(CD[b], ref["CD"]) < 1e-5
