@@ -358,17 +358,13 @@ def test_nonfinite_input_raises_like_the_reference(bad, dtype):
 def test_many_small_blocks_thread_kernels_match_oracle(method):
     """K x batch >= 16384 blocks of <= 64 columns take the thread-per-block
     probability and sampling kernels (config 5's shape): budgets, draws and
-    scales bit-exact to the oracle on a spread of problems, also for unequal
-    blocks with a zero block."""
+    scales bit-exact to the oracle on a spread of problems, with a zero block."""
     B, m, n, p, K = 260, 24, 4096, 16, 64
     g = np.random.default_rng(31)
     Ms = (g.standard_normal((B, m, n)) * g.lognormal(0, 1, (B, 1, n))).astype(np.float32)
     Ns = (g.standard_normal((B, n, p)) * g.lognormal(0, 1, (B, n, 1))).astype(np.float32)
-    if method == "SSM":
-        sizes = (64,) * K
-    else:
-        sizes = tuple([64] * 60 + [10, 54, 100, 92])  # unequal, max 100 > 64 -> warp kernels for probs
-        sizes = (64,) * K
+    sizes = (64,) * K
+    if method != "SSM":
         Ms[:, :, 64:128] = 0.0  # block 1 has zero score in every problem
     Md, Nd = torch.as_tensor(Ms, device="cuda"), torch.as_tensor(Ns, device="cuda")
     if method == "SSM":
