@@ -1578,9 +1578,46 @@ def run_cfg4(args):
         ref = [o.cpu() for o in group.run(Md, Nd, cfg4_seeds(K))]
         if not all(torch.equal(a, b) for a, b in zip(ref, outs_h)):
             raise RuntimeError("cfg4 end-to-end products differ from the resident run")
-        line["e2e"] = {"value": float(np.mean(e2e)), "unit": "ms/step", "h2d_bytes_per_step": norm_bytes,
-                       "d2h_bytes_per_step": 3 * 4 * m * p,
-                       "api": "PipelineGroup.capture_host/run_host: pinned host M, N -> pinned host products"}
+        latency = float(np.mean(e2e))
+        # steady state: two copies of the step (device inputs, sketch buffers, graph) alternate on
+        # two streams, so step i+1's host->device transfer overlaps step i's contractions -- every
+        # step still copies its 34 GB of inputs in and its three products out
+        pipelined, pipe_note = None, None
+        try:
+            Md2, Nd2 = torch.empty_like(Md), torch.empty_like(Nd)
+            group2 = cfg4_group(torch, m, n, p, sizes)
+            outs_h2 = [torch.empty((m, p), dtype=torch.float32).pin_memory() for _ in CFG4_RUNS]
+            group2.capture_host(Md2, Nd2, M_pin, N_pin, outs_h2, cfg4_seeds(K), n_chunks=8)
+            lanes = [(group, torch.cuda.Stream()), (group2, torch.cuda.Stream())]
+            for g_, s_ in lanes:  # warm
+                with torch.cuda.stream(s_):
+                    g_.run_host(cfg4_seeds(K))
+            torch.cuda.synchronize()
+            ksteps = max(4, args.steps)
+            t0 = time.perf_counter()
+            for it in range(ksteps):
+                g_, s_ = lanes[it % 2]
+                seeds = cfg4_seeds(K)
+                with torch.cuda.stream(s_):
+                    g_.run_host(seeds)
+            torch.cuda.synchronize()
+            pipelined = (time.perf_counter() - t0) * 1e3 / ksteps
+            if not all(torch.equal(a, b) for a, b in zip(ref, outs_h2)):
+                raise RuntimeError("cfg4 pipelined end-to-end products differ from the resident run")
+            del group2, Md2, Nd2, outs_h2
+        except torch.cuda.OutOfMemoryError as e:  # pragma: no cover
+            pipe_note = f"pipelined run skipped: {e}"
+        torch.cuda.empty_cache()
+        line["e2e"] = {"value": pipelined if pipelined is not None else latency, "unit": "ms/step",
+                       "h2d_bytes_per_step": norm_bytes, "d2h_bytes_per_step": 3 * 4 * m * p,
+                       "latency_ms": latency,
+                       "api": "PipelineGroup.capture_host/run_host: pinned host M, N -> pinned host products "
+                              "(one graph per step: chunked H2D with the shared norm pass and Gram g_k behind it)",
+                       "mode": ("steady state of consecutive steps, two step instances alternating on two streams "
+                                "(transfer of step i+1 overlaps the work of step i); latency_ms: one step alone")
+                       if pipelined is not None else "one step at a time"}
+        if pipe_note:
+            line["e2e"]["note"] = pipe_note
         del M_pin, N_pin, outs_h
     else:
         line["e2e"] = {"value": None, "unit": "ms/step", "h2d_bytes_per_step": norm_bytes,

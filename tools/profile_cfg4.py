@@ -27,9 +27,8 @@ W = q.W
 torch.cuda.cudart().cudaProfilerStart()
 lib.bmm_norms(1, P(Md), m, n, n, 0, P(Nd), p, p, 0, 1, 0, P(sh.colsq), P(sh.rowsq), st)
 lib.bmm_segsq_gram(1, P(Md), n, 0, P(Nd), p, 0, m, p, P(sh.offsets), K, 0, 1, P(sh.gsq), st)
-lib.bmm_gather_f32split_dk(1, P(Md), n, 0, P(Nd), p, 0, m, p, P(q.k_column), P(q.k_scale), W, W, P(q.k_count), 1,
-                           P(q.a_hi), P(q.a_x), P(q.b_hi), P(q.b_x), st)
-lib.bmm_gemm_f32split_dk(P(q.a_hi), P(q.a_x), P(q.b_hi), P(q.b_x), m, p, W, P(q.k_count), 1, P(q.CD), p, m * p, st)
+q.split_gather(Md, Nd, st)   # fp16 split (balance + gather) for these sizes
+q.split_gemm(st)              # gemm_f16split_2sm_kernel
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStop()
 print("profiled kernels done")
