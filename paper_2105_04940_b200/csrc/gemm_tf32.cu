@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(32 * P_WARPS, 1) gemm_f16split_2sm_kernel(
     const __grid_constant__ CUtensorMap tm_ah, const __grid_constant__ CUtensorMap tm_ax,
     const __grid_constant__ CUtensorMap tm_bh, const __grid_constant__ CUtensorMap tm_bx, int64_t m, int64_t nc,
     int64_t k, float* __restrict__ out, int64_t ldo, int64_t strideO, const int64_t* __restrict__ kdev,
-    const int32_t* __restrict__ gshift) {
+    const int32_t* __restrict__ gshift, int group_m) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + H_STAGES * H_STAGE);
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(32 * P_WARPS, 1) gemm_f16split_2sm_kernel(
   const int64_t b = blockIdx.z;
   uint32_t rank;
   asm("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
-  constexpr int GROUP_M = 8;
+  const int GROUP_M = group_m;  // grouped rasterisation over 256 x 256 pair tiles (default 8)
   int tile_m, tile_n;
   {
     const int tm = gridDim.y, tn = gridDim.x / 2;
@@ -1504,8 +1504,13 @@ extern "C" int bmm_gemm_f16split_dk(const void* a_h, const void* a_x, const void
   la[0].val.clusterDim.z = 1;
   lc.attrs = la;
   lc.numAttrs = 1;
-  if (cudaLaunchKernelEx(&lc, kern, ma_h, ma_x, mb_h, mb_x, m, nc, k_max, out, ldo, strideO, k_dev, gshift) !=
-      cudaSuccess) {
+  static const int group_m = [] {
+    const char* e = getenv("BMM_F16_GROUP_M");  // A/B switch: pair-tile rows per raster group
+    const int v = e ? atoi(e) : 8;
+    return v >= 1 ? v : 8;
+  }();
+  if (cudaLaunchKernelEx(&lc, kern, ma_h, ma_x, mb_h, mb_x, m, nc, k_max, out, ldo, strideO, k_dev, gshift,
+                         group_m) != cudaSuccess) {
     set_error("bmm_gemm_f16split_dk: cluster launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     return BMM_E_CUDA;
   }
