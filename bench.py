@@ -1189,8 +1189,10 @@ def _oracle_draws(O, probs, sizes, budgets, streams):
     return np.concatenate(cols), np.concatenate(scales)
 
 
-def cfg4_parity(torch, group, Md, Nd, outs):
-    """Untimed: the benched products against the oracle.
+def cfg4_cpu_leg_parity(torch, group, Md, Nd, outs):
+    """CPU-baseline leg, untimed: the oracle (oracle/blockmm_oracle.py, the CPU
+    restatement of the reference) run on the host as the CHECKER of the benched
+    products -- never on the measured path.
     * norms: 64 random columns of M and 64 random rows of N, bit-exact (the
       chains are per column / per row, so a sample is exact);
     * plan and draws: the oracle's probabilities, score sums, budgets (OPL with
@@ -1418,7 +1420,7 @@ def run_cfg4(args):
     group = cfg4_group(torch, m, n, p, sizes)
     outs = [o.clone() for o in group.run(Md, Nd, cfg4_seeds(K))]
     group.check()
-    parity = cfg4_parity(torch, group, Md, Nd, outs)
+    parity = cfg4_cpu_leg_parity(torch, group, Md, Nd, outs)
     del outs
     group.capture(Md, Nd)
     # the norm pass alone on a cool GPU (before the power-capped GEMM steps)

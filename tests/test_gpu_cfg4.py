@@ -41,6 +41,6 @@ def test_cfg4_full_size_parity():
     assert np.array_equal(group.shared.colsq.cpu().numpy(), acc)
     assert np.array_equal(group.shared.rowsq.cpu().numpy(), rowsq)
 
-    res = bench.cfg4_parity(torch, group, Md, Nd, outs)  # raises on any mismatch
+    res = bench.cfg4_cpu_leg_parity(torch, group, Md, Nd, outs)  # raises on any mismatch
     assert res["ok"]
     assert max(res["cd_rel_err_vs_f64_same_sketch"].values()) < 1e-5
