@@ -717,10 +717,14 @@ class PipelineGroup:
             # same time, and each width's GEMM can start while the other widths still plan
             m, p, dev = p0.m, p0.p, p0.C.device
             f64 = dict(dtype=torch.float64, device=dev)
+            # BMM_JOINT_BY=method pools each method's members instead (pool width = the
+            # widest member; per-member inner lengths are read on the device anyway)
+            by = os.environ.get("BMM_JOINT_BY", "width")
             by_w = {}
             for i, q in enumerate(self.pipes):
-                by_w.setdefault(q.W, []).append(i)
-            for Wj, idx in by_w.items():
+                by_w.setdefault(q.method if by == "method" else q.W, []).append(i)
+            for key, idx in by_w.items():
+                Wj = max(self.pipes[i].W for i in idx)
                 G = len(idx)
                 jg = dict(idx=idx, W=Wj, C=torch.zeros((G, m, Wj), **f64), D=torch.zeros((G, Wj, p), **f64),
                           k=torch.zeros(G, dtype=torch.int64, device=dev), CD=torch.empty((G, m, p), **f64),
