@@ -561,7 +561,7 @@ def kernel_times(torch, bm, pipes, runs, Md, Nd, cfg, K, flush, group=None):
     out["gemm_engine"] = [getattr(pipe, "gemm_engine", "dmma") for pipe in pipes]
     for (cb, W, meth, c0), pipe, kd in zip(runs, pipes, out["gemm_k"]):
         if hasattr(pipe, "C"):
-            Wc = W
+            Wc = pipe._joint or W  # pooled operands (joint group) have the pool's row stride
             C, D = pipe.C.view(m, Wc)[:, :kd], pipe.D.view(Wc, p)[:kd]
         else:  # the i8 engine gathers inside its split: build C, D for the cuBLAS reference point
             col, sc = (pipe.k_column, pipe.k_scale) if pipe.compress else (pipe.column, pipe.scale)
