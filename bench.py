@@ -1766,8 +1766,9 @@ def main():
         return run_mc(args)
     if args.impl == "reference":
         return run_reference_cfg4(args) if args.workload == "cfg4" else run_reference(args)
-    if args.workload == "cfg4" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        return run_cfg4_sharded(args)
+    if args.workload == "cfg4" and (int(os.environ.get("WORLD_SIZE", "1")) > 1 or
+                                    os.environ.get("BMM_FORCE_SHARDED") == "1"):
+        return run_cfg4_sharded(args)  # (BMM_FORCE_SHARDED=1: the sharded path at world 1, for testing)
     if args.workload == "cfg4":
         return run_cfg4(args)
     if args.workload == "cfg5":
