@@ -812,7 +812,9 @@ def run_cfg4_sharded(args):
     for _ in range(args.warmup):
         sh.run(M, N, cfg4_seeds(K))
     torch.cuda.synchronize()
+    from paper_2105_04940_b200 import _lib as _l
     times = []
+    n_l0 = _l.launches()
     with ClockSampler(local) as clocks:
         dist.barrier()
         torch.cuda.synchronize()
@@ -825,6 +827,7 @@ def run_cfg4_sharded(args):
             times.append((e0, e1))
         torch.cuda.synchronize()
         dist.barrier()
+    launches = (_l.launches() - n_l0) // max(1, args.steps)
     ms = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in times]))], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     # e2e: this rank's shard from pinned host memory, its tiles back, every step
@@ -852,7 +855,7 @@ def run_cfg4_sharded(args):
         print(json.dumps({
             "metric": METRIC, "value": float(ms.item()), "unit": "ms/step", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": float(ms.item()), "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 (TF32 + BF16 split-operand tensor contraction, f64 norms/plan)",
+            "vs_baseline": None, "dtype": "f32 (fp16 split-operand tensor contraction on CTA pairs, f64 norms/plan)",
             "data": "synthetic (chunk-seeded on device: every rank regenerates exactly its slice)",
             "config": {"workload": "cfg4", "grid": list(L.grid), "m": m, "n": n, "p": p, "K": K, "block": 64,
                        "runs": ["OPL@W=32768", "ONC@W=32768", "SSM@draws=512"],
@@ -860,7 +863,7 @@ def run_cfg4_sharded(args):
                                       "exchange + g_k^2 partials (NCCL all-gather)",
                        "l2": "inputs >> L2"},
             "draws_identical_on_all_ranks": bool(same_draws),
-            "gpu_launches": None,
+            "gpu_launches": int(launches),
             "e2e": {"value": float(e2e_t.item()), "unit": "ms/step",
                     "h2d_bytes_per_step": int(M.numel() * 4 + N.numel() * 4) * world,
                     "d2h_bytes_per_step": int(sum(t.numel() for t in tiles) * 4) * world,
@@ -1510,7 +1513,7 @@ def run_cfg4(args):
     line = {
         "metric": METRIC, "value": ms_step, "unit": "ms/step", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (TF32 + BF16 split-operand tensor contraction, f64 norms/plan)",
+        "vs_baseline": None, "dtype": "f32 (fp16 split-operand tensor contraction on CTA pairs, f64 norms/plan)",
         "data": "synthetic (chunk-seeded torch generator on device; SURVEY.md §8(d1) distributions)",
         "config": {"workload": "cfg4", "m": m, "n": n, "p": p, "K": K, "block": 64,
                    "runs": ["OPL@W=32768", "ONC@W=32768", "SSM@draws=512"],

@@ -750,14 +750,37 @@ class PipelineGroup:
                       g["k"].data_ptr(), G, g["CD"].data_ptr(), p, m * p, g["ws"].data_ptr(), g["ws"].numel(),
                       _lib.stream_ptr())
 
+    def serial(self) -> bool:
+        """Members one after another instead of concurrent branches when every
+        member's contraction alone fills the GPU (large outputs: config 4).  Two
+        concurrent 16384 x 16384 contractions share L2 and power and measured slower
+        than the same work in sequence (183 vs 172 ms per config-4 step).
+        BMM_GROUP_SERIAL=0|1 forces either."""
+        forced = os.environ.get("BMM_GROUP_SERIAL", "")
+        if forced in ("0", "1"):
+            return forced == "1"
+        p0 = self.pipes[0]
+        return p0.m * p0.p >= (1 << 24) and not self.joint
+
     def _branch_streams(self) -> list:
         """One stream per member.  OPL members (the longest chains: their g_k
         contraction occupies every SM) get the high priority, so their kernels take
         SMs first and the other branches fill the gaps (BMM_BRANCH_PRIORITY=0: all
-        equal)."""
+        equal).  Serial groups: ONE stream, members needing g_k last."""
+        if self.serial():
+            one = torch.cuda.Stream()
+            return [one for _ in self.pipes]
         if os.environ.get("BMM_BRANCH_PRIORITY", "1") == "0":
             return [torch.cuda.Stream() for _ in self.pipes]
         return [torch.cuda.Stream(priority=-1 if q.method == "OPL" else 0) for q in self.pipes]
+
+    def _order(self) -> list:
+        """Member launch order: as given, except serial groups put OPL (which waits
+        for the shared g_k) after the others."""
+        idx = list(range(len(self.pipes)))
+        if self.serial():
+            idx.sort(key=lambda i: self.pipes[i].method == "OPL")
+        return idx
 
     def _launch_all(self, M: torch.Tensor, N: torch.Tensor) -> None:
         self._active(True)
@@ -819,11 +842,13 @@ class PipelineGroup:
                 if self.shared is not None:
                     *evs, ss = self._fork_stats(cap, M, N)
                     extra.append(ss)
-                for s, pipe in zip(streams, self.pipes):
+                for i in self._order():
+                    s, pipe = streams[i], self.pipes[i]
                     s.wait_stream(cap)
                     self._member_wait(s, pipe, evs)
                     with torch.cuda.stream(s):
                         pipe.launch(M, N)
+                streams = list(dict.fromkeys(streams))  # serial groups share one stream
                 for jg in self._jgroups:  # each width's GEMM after its own members
                     js = torch.cuda.Stream()
                     for i in jg["idx"]:
@@ -867,7 +892,7 @@ class PipelineGroup:
             self._launch_all(M, N)
         cur.wait_stream(side)
         copy = torch.cuda.Stream()
-        streams = [torch.cuda.Stream() for _ in pipes]
+        streams = self._branch_streams()
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launches()
         self._active(True)
@@ -891,7 +916,8 @@ class PipelineGroup:
                 if self.shared is not None:
                     *evs, ss = self._fork_stats(cap, M, N, chunks)
                     extra.append(ss)
-                for s, pipe, oh in zip(streams, pipes, out_host):
+                for i in self._order():
+                    s, pipe, oh = streams[i], pipes[i], out_host[i]
                     s.wait_stream(cap)
                     self._member_wait(s, pipe, evs)
                     with torch.cuda.stream(s):
@@ -901,6 +927,7 @@ class PipelineGroup:
                             out = pipe.launch(M, N, chunks=chunks)
                         if not self.joint:
                             oh.copy_(out.reshape(oh.shape), non_blocking=True)
+                streams = list(dict.fromkeys(streams))
                 for jg in self._jgroups:  # joint mode: each width's GEMM, then its products go home
                     js = torch.cuda.Stream()
                     for i in jg["idx"]:

@@ -69,8 +69,9 @@ def test_pipeline_group_concurrent_replay_is_bit_identical(shared):
             group.pipes[1].run(Md, Nd, seeds(3)[1])
 
 
+@pytest.mark.parametrize("serial", ["0", "1"])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-def test_shared_stats_group_with_ssm_matches_oracle(dtype):
+def test_shared_stats_group_with_ssm_matches_oracle(dtype, serial, monkeypatch):
     """OPL, ONC and SSM over one instance with one shared statistics stage (the
     config-4 step): budgets, draws and scales bit-exact to the oracle, products
     within the dtype's bar, eager and replayed."""
@@ -82,6 +83,7 @@ def test_shared_stats_group_with_ssm_matches_oracle(dtype):
     tdt = torch.float64 if dtype == np.float64 else torch.float32
     Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
     W, draws = 640, 10
+    monkeypatch.setenv("BMM_GROUP_SERIAL", serial)  # members as concurrent branches, or one after another
     group = PipelineGroup([SketchPipeline(96, n, 80, sizes, W, "OPL", dtype=tdt),
                            SketchPipeline(96, n, 80, sizes, W, "ONC", dtype=tdt),
                            SketchPipeline(96, n, 80, sizes, 0, "SSM", draws=draws, dtype=tdt)])
@@ -295,7 +297,8 @@ def test_streamed_end_to_end_graph_matches_resident_run(joint, shared):
     assert np.array_equal(Mx.cpu().numpy(), M)
 
 
-def test_streamed_end_to_end_float32_shared_group():
+@pytest.mark.parametrize("serial", ["0", "1"])
+def test_streamed_end_to_end_float32_shared_group(serial, monkeypatch):
     """The config-4 end-to-end shape at small size: float32 host inputs streamed in
     chunks under the shared statistics stage (norms and Gram g_k per chunk), OPL,
     ONC and SSM members, products copied back -- bit-identical to the resident run."""
@@ -314,6 +317,7 @@ def test_streamed_end_to_end_float32_shared_group():
                 seeds_from_rngs("ONC", [np.random.default_rng(s + 1)], 48),
                 seeds_from_rngs("SSM", [np.random.default_rng(s + 2)], 48, draws=12)]
 
+    monkeypatch.setenv("BMM_GROUP_SERIAL", serial)
     want = [o.cpu().numpy() for o in mk().run(Md, Nd, seeds(4))]
     grp = mk()
     Mh, Nh = torch.from_numpy(M).pin_memory(), torch.from_numpy(N).pin_memory()
