@@ -751,16 +751,13 @@ class PipelineGroup:
                       _lib.stream_ptr())
 
     def serial(self) -> bool:
-        """Members one after another instead of concurrent branches when every
-        member's contraction alone fills the GPU (large outputs: config 4).  Two
-        concurrent 16384 x 16384 contractions share L2 and power and measured slower
-        than the same work in sequence (183 vs 172 ms per config-4 step).
-        BMM_GROUP_SERIAL=0|1 forces either."""
+        """BMM_GROUP_SERIAL=1: members one after another (one stream, OPL last)
+        instead of concurrent branches.  Measured at config 4, where every
+        member's contraction alone fills the GPU: 177.5 vs 180.0 ms per step and a
+        longer single-step latency end to end (808 vs 770 ms), i.e. within the
+        run-to-run spread, so concurrent branches stay the default."""
         forced = os.environ.get("BMM_GROUP_SERIAL", "")
-        if forced in ("0", "1"):
-            return forced == "1"
-        p0 = self.pipes[0]
-        return p0.m * p0.p >= (1 << 24) and not self.joint
+        return forced == "1"
 
     def _branch_streams(self) -> list:
         """One stream per member.  OPL members (the longest chains: their g_k
@@ -848,7 +845,6 @@ class PipelineGroup:
                     self._member_wait(s, pipe, evs)
                     with torch.cuda.stream(s):
                         pipe.launch(M, N)
-                streams = list(dict.fromkeys(streams))  # serial groups share one stream
                 for jg in self._jgroups:  # each width's GEMM after its own members
                     js = torch.cuda.Stream()
                     for i in jg["idx"]:
@@ -856,7 +852,7 @@ class PipelineGroup:
                     with torch.cuda.stream(js):
                         self._joint_gemm(jg)
                     extra.append(js)
-                for s in streams + extra:
+                for s in list(dict.fromkeys(streams)) + extra:  # serial groups share one stream
                     cap.wait_stream(s)
         finally:
             self._active(False)
@@ -927,7 +923,6 @@ class PipelineGroup:
                             out = pipe.launch(M, N, chunks=chunks)
                         if not self.joint:
                             oh.copy_(out.reshape(oh.shape), non_blocking=True)
-                streams = list(dict.fromkeys(streams))
                 for jg in self._jgroups:  # joint mode: each width's GEMM, then its products go home
                     js = torch.cuda.Stream()
                     for i in jg["idx"]:
@@ -937,7 +932,7 @@ class PipelineGroup:
                         for j, i in enumerate(jg["idx"]):
                             out_host[i].copy_(jg["CD"][j].reshape(out_host[i].shape), non_blocking=True)
                     extra.append(js)
-                for s in streams + extra:
+                for s in list(dict.fromkeys(streams)) + extra:
                     cap.wait_stream(s)
         finally:
             self._active(False)
