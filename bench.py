@@ -293,7 +293,9 @@ def run_ours(args):
         same = (torch.equal(o, h) if group.joint == host_group.joint
                 else bool(((o - h).norm() <= 1e-13 * o.norm()).item()))
         if not same:
-            raise RuntimeError("streamed end-to-end products differ from the resident run")
+            raise RuntimeError("streamed end-to-end products differ from the resident run: rel "
+                               f"{float((o - h).norm() / o.norm()):.3e}, finite {bool(torch.isfinite(o).all())} "
+                               f"{bool(torch.isfinite(h).all())}, joint {group.joint}/{host_group.joint}")
     latency_ms = float(np.mean(e2e))
     # steady state: a second instance of the streamed graph alternates with the first on two
     # streams, so one step's host->device transfer overlaps the previous step's work; every

@@ -801,7 +801,7 @@ class PipelineGroup:
         ss.wait_stream(cap)
         ev_p, ev_g = torch.cuda.Event(), torch.cuda.Event()
         gs = None
-        if chunks is None and self.shared.needs_gsq:
+        if chunks is None and self.shared.needs_gsq and os.environ.get("BMM_GSQ_FORK", "1") != "0":
             gs = torch.cuda.Stream(priority=-1)
             gs.wait_stream(cap)
             with torch.cuda.stream(gs):
