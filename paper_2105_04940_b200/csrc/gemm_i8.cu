@@ -51,7 +51,12 @@ constexpr int OZ_A_PLANE = OZ_BM * OZ_BK;            // 4 KB
 constexpr int OZ_B_PLANE = OZ_BN * OZ_BK;            // 2 KB
 constexpr int OZ_STAGE = OZ_S * (OZ_A_PLANE + OZ_B_PLANE);  // 48 KB
 constexpr int OZ_STAGES = 4;
-constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE + 1024 + 1024;
+// stages (1024-aligned inside the allocation: up to 1023 bytes of padding), then the
+// barriers (256 B), wcol [2][64] and red[] doubles: 1344 bytes past the stages.  (Round 2:
+// this was + 1024 + 1024, so with an unaligned base the epilogue's red[] landed past the
+// CTA's allocation -- in a co-resident CTA's shared memory: the colsq ring of a concurrent
+// norm pass got corrupted; tools/stress_group.py found it.)
+constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE + 1024 + 2048;
 constexpr int OZ_EPI_WARPS = 8;    // two per TMEM lane quarter, 32 columns each
 constexpr int OZ_EPI_COLS = OZ_BN / (OZ_EPI_WARPS / 4);
 constexpr int OZ_THREADS = 64 + 32 * OZ_EPI_WARPS;  // warp 0 TMA, warp 1 MMA, then the epilogue warps

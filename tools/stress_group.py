@@ -24,6 +24,11 @@ seeds = lambda: [seeds_from_rngs(meth, [workloads.sample_rng(cfg, cb)], K) for c
 g = PipelineGroup([SketchPipeline(m, n, p, sizes, W, meth, c0=c0) for _, W, meth, c0 in runs])
 ref = [o.cpu().clone() for o in g.run(Md, Nd, seeds())]
 refb = [q.budgets_host().copy() for q in g.pipes]
+refc = [q.columns_host().copy() for q in g.pipes]
+refs = [q.scales_host().copy() for q in g.pipes]
+refn = [(q.colsq.cpu().clone(), q.rowsq.cpu().clone(), q.probs.cpu().clone(), q.cum.cpu().clone()) for q in g.pipes]
+refk = [q.k_column.cpu().clone() for q in g.pipes]
+refst = [q.states.cpu().clone() for q in g.pipes]
 g.capture(Md, Nd)
 bad = 0
 for r in range(reps):
@@ -31,9 +36,23 @@ for r in range(reps):
     for i, (a, b) in enumerate(zip(ref, out)):
         if not torch.equal(a, b):
             bad += 1
-            same_b = np.array_equal(refb[i], g.pipes[i].budgets_host())
+            q = g.pipes[i]
+            same_b = np.array_equal(refb[i], q.budgets_host())
+            same_c = np.array_equal(refc[i], q.columns_host())
+            same_s = np.array_equal(refs[i], q.scales_host())
+            nn = [torch.equal(x, y.cpu()) for x, y in zip(refn[i], (q.colsq, q.rowsq, q.probs, q.cum))]
+            same_k = torch.equal(refk[i], q.k_column.cpu())
+            same_st = torch.equal(refst[i], q.states.cpu())
+            if not nn[0]:
+                d = (refn[i][0] - q.colsq.cpu()).abs()
+                bad_idx = torch.nonzero(d).flatten()
+                rel = (d / refn[i][0].abs().clamp_min(1e-300))[bad_idx]
+                print(f"   colsq differs at {bad_idx.numel()} of {d.numel()} columns: first {bad_idx[:8].tolist()} "
+                      f"last {bad_idx[-4:].tolist()} rel max {float(rel.max()):.3e} min {float(rel.min()):.3e}",
+                      flush=True)
             print(f"resident replay {r} product {i} ({runs[i][2]} W={runs[i][1]}): rel "
-                  f"{float((a - b).norm() / a.norm()):.3e} budgets same {same_b}", flush=True)
+                  f"{float((a - b).norm() / a.norm()):.3e} budgets {same_b} cols {same_c} scales {same_s} "
+                  f"norms/probs/cum {nn} kcol {same_k} states {same_st}", flush=True)
 print(f"resident: {bad} mismatches in {reps} replays", flush=True)
 hg = PipelineGroup([SketchPipeline(m, n, p, sizes, W, meth, c0=c0) for _, W, meth, c0 in runs], joint=False)
 M_pin, N_pin = torch.from_numpy(M_h).pin_memory(), torch.from_numpy(N_h).pin_memory()
