@@ -997,7 +997,7 @@ static bool launch_colsq_tma(const T* M, int64_t m, int64_t n, int64_t ldm, int6
   auto enc = tma_encode_fn();
   if (enc == nullptr) return false;
   const int rows = (variant == 2 || variant == 5 || variant == 8) ? 32 : 16;
-  const int bcols = variant == 6 || variant == 8 ? 128 : (variant == 7 || variant == 0) ? 64 : 32;
+  const int bcols = variant == 6 || variant == 8 ? 128 : variant == 7 ? 64 : 32;
   CUtensorMap map;
   cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)(batch * m)};
   cuuint64_t strides[1] = {(cuuint64_t)(n * sizeof(T))};
@@ -1017,6 +1017,12 @@ static bool launch_colsq_tma(const T* M, int64_t m, int64_t n, int64_t ldm, int6
     case 7: return launch_colsq_tma_cta<T, 2, 6, 16>(map, m, n, batch, accumulate, colsq, st);
     case 8: return launch_colsq_tma_cta<T, 4, 4, 32>(map, m, n, batch, accumulate, colsq, st);
     case 9: return launch_colsq_tma_cfg<T, 4, 4, 16>(map, m, n, batch, accumulate, colsq, st);
+    // default: per-warp rings (variant 3).  The CTA-wide ring with 6 stages of 16 rows
+    // (variants 0 and 6, the round-1 default) gave wrong column sums for a warp's 32
+    // columns in ~1 of 2 replays of the cfg2 graph whenever the int8 g_k chain ran
+    // concurrently (tools/stress_group.py, tests/test_gpu_stress.py); variants 2, 3, 8
+    // and 9 never did in 80 replays each, and 3 is as fast at cfg2 (22.6 us)
+    case 0: return launch_colsq_tma_cfg<T, 2, 6, 16>(map, m, n, batch, accumulate, colsq, st);
     default: return launch_colsq_tma_cta<T, 2, 6, 16>(map, m, n, batch, accumulate, colsq, st);
   }
 }
