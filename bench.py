@@ -859,14 +859,26 @@ def run_cfg4_sharded(args):
     launches = (_l.launches() - n_l0) // max(1, args.steps)
     ms = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in times]))], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    # e2e: this rank's shard from pinned host memory, its tiles back, every step
-    M_pin = torch.empty(M.shape, dtype=M.dtype).pin_memory()
-    N_pin = torch.empty(N.shape, dtype=N.dtype).pin_memory()
-    M_pin.copy_(M)
-    N_pin.copy_(N)
-    outs = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in tiles]
+    # e2e: this rank's shard from pinned host memory, its tiles back, every step (skipped
+    # when the node's RAM cannot pin every rank's shard)
+    import psutil
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    need = (M.numel() + N.numel() + sum(t.numel() for t in tiles)) * 4 * local_world
+    can = torch.tensor([1.0 if psutil.virtual_memory().available > need + (16 << 30) else 0.0], device="cuda")
+    dist.all_reduce(can, op=dist.ReduceOp.MIN)
+    if can.item() < 1.0:
+        e2e_line = {"value": None, "unit": "ms/step", "skipped": "host RAM too small to pin every rank's shard"}
+        ms_e2e = None
+    else:
+        e2e_line = None
+    M_pin = torch.empty(M.shape, dtype=M.dtype).pin_memory() if e2e_line is None else None
+    N_pin = torch.empty(N.shape, dtype=N.dtype).pin_memory() if e2e_line is None else None
+    if e2e_line is None:
+        M_pin.copy_(M)
+        N_pin.copy_(N)
+    outs = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in tiles] if e2e_line is None else []
     e2e = []
-    for it in range(1 + args.steps):
+    for it in range(1 + args.steps if e2e_line is None else 0):
         seeds = cfg4_seeds(K)
         dist.barrier()
         torch.cuda.synchronize()
@@ -878,7 +890,7 @@ def run_cfg4_sharded(args):
         torch.cuda.synchronize()
         if it >= 1:
             e2e.append((time.perf_counter() - t0) * 1e3)
-    e2e_t = torch.tensor([float(np.mean(e2e))], device="cuda")
+    e2e_t = torch.tensor([float(np.mean(e2e)) if e2e else 0.0], device="cuda")
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     if rank == 0:
         print(json.dumps({
@@ -893,7 +905,8 @@ def run_cfg4_sharded(args):
                        "l2": "inputs >> L2"},
             "draws_identical_on_all_ranks": bool(same_draws),
             "gpu_launches": int(launches),
-            "e2e": {"value": float(e2e_t.item()), "unit": "ms/step",
+            "e2e": e2e_line if e2e_line is not None else
+                   {"value": float(e2e_t.item()), "unit": "ms/step",
                     "h2d_bytes_per_step": int(M.numel() * 4 + N.numel() * 4) * world,
                     "d2h_bytes_per_step": int(sum(t.numel() for t in tiles) * 4) * world,
                     "api": "ShardedApproxProduct.run on each rank's shard copied from pinned host memory"},
