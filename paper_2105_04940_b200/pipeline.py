@@ -767,9 +767,13 @@ class PipelineGroup:
         if self.serial():
             one = torch.cuda.Stream()
             return [one for _ in self.pipes]
-        if os.environ.get("BMM_BRANCH_PRIORITY", "1") == "0":
+        mode = os.environ.get("BMM_BRANCH_PRIORITY", "2")
+        if mode == "0":
             return [torch.cuda.Stream() for _ in self.pipes]
-        return [torch.cuda.Stream(priority=-1 if q.method == "OPL" else 0) for q in self.pipes]
+        # "2" (default): the two-step members too -- with the statistics shared, their
+        # pilot chains (pilot plan, draws, pilot norms, main plan) are the longest
+        hi = ("OPL",) if mode == "1" else ("OPL", "ONU", "ONMCNR")
+        return [torch.cuda.Stream(priority=-1 if q.method in hi else 0) for q in self.pipes]
 
     def _order(self) -> list:
         """Member launch order: as given, except serial groups put OPL (which waits
