@@ -1665,6 +1665,30 @@ def run_cfg4(args):
                        if pipelined is not None else "one step at a time"}
         if pipe_note:
             line["e2e"]["note"] = pipe_note
+        # the drop-in API on host (numpy) arrays for one ONC product, as a reference user
+        # calls it: allocate_by_score_sums + estimate_product (uploads M and N on each call,
+        # float64 C and D and the product back as the reference's records)
+        try:
+            import paper_2105_04940_b200 as bm
+            Mh, Nh = M_pin.numpy(), N_pin.numpy()
+            part = bm.BlockPartition(sizes)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            plan = bm.allocate_by_score_sums(Mh, Nh, part, 32768)
+            t1 = time.perf_counter()
+            pair, CDh, log = bm.estimate_product(Mh, Nh, plan, workloads.sample_rng(4, 1))
+            t2 = time.perf_counter()
+            ok = np.array_equal(log.column, group.pipes[1].columns_host()[0])
+            line["e2e_dropin_api"] = {
+                "value": (t2 - t0) * 1e3, "unit": "ms per ONC product", "plan_ms": (t1 - t0) * 1e3,
+                "estimate_ms": (t2 - t1) * 1e3, "draws_equal_pipeline": bool(ok),
+                "api": "allocate_by_score_sums(M, N, part, 32768) + estimate_product(M, N, plan, rng) on numpy "
+                       "float32 arrays (views of pinned buffers here); returns float64 C, D (4.3 GB each), the "
+                       "product and the sample log to the host, C @ D on the DMMA engine as the reference's float64"}
+            del pair, CDh, log, plan
+        except (RuntimeError, torch.cuda.OutOfMemoryError) as e:  # pragma: no cover
+            line["e2e_dropin_api"] = {"value": None, "skipped": str(e)[:200]}
+        torch.cuda.empty_cache()
         del M_pin, N_pin, outs_h
     else:
         line["e2e"] = {"value": None, "unit": "ms/step", "h2d_bytes_per_step": norm_bytes,
