@@ -978,6 +978,35 @@ def cfg5_cpu_baseline(pipe, CD, Md, Nd, sizes, W, keys, sample=16):
     return cb, par
 
 
+def cfg_traffic(key):
+    """DRAM bytes per launch of a kernel from one committed `ncu --set full`
+    capture (profiles/traffic.json; null when that kernel was not captured)."""
+    path = ROOT / "profiles" / "traffic.json"
+    if not path.exists():
+        return None
+    ent = json.loads(path.read_text()).get(key)
+    return None if ent is None else ent.get("bytes_per_launch")
+
+
+def sketch_numeric_err(pipe, Md, Nd, CD, nb):
+    """Numeric error of the float32 contraction alone: ||CD - C.D||_F / ||C.D||_F
+    over the first nb problems, C.D in float64 from the same compressed sketch
+    (the estimator's own error is the rel_err_* fields)."""
+    import torch
+    cols = pipe.k_column.view(pipe.B, pipe.W)[:nb]
+    sc = pipe.k_scale.view(pipe.B, pipe.W)[:nb]
+    cnt = pipe.k_count[:nb].cpu().tolist()
+    num = den = 0.0
+    for b in range(nb):
+        c, s = cols[b, :cnt[b]], sc[b, :cnt[b]]
+        C = Md[b][:, c].double() * s
+        D = Nd[b][c, :].double() * s[:, None]
+        ex = C @ D
+        num += float(((CD.view(pipe.B, pipe.m, pipe.p)[b].double() - ex) ** 2).sum())
+        den += float((ex ** 2).sum())
+    return {"value": float(np.sqrt(num / den)), "problems": nb, "bar": 1e-5}
+
+
 def run_device(args):
     """cfg5: 4096 independent problems (per-problem seeds).  Under torchrun the
     problems are split over the ranks (no collective; weak in data, the whole
@@ -1093,24 +1122,44 @@ def run_device(args):
 
     norms_ms = timed(lambda: lib.bmm_norms(1, P(Md), m, n, n, m * n, P(Nd), p, p, n * p, B, 0, P(pipe.colsq),
                                            P(pipe.rowsq), st))
-    gather_ms = timed(lambda: pipe.split_gather(Md, Nd, st))
-    gemm_ms = timed(lambda: pipe.split_gemm(st))
+    if pipe.fused16:  # config 5: gather + fp16 split + contraction in one kernel (plus the exponent balance)
+        fused_ms = timed(lambda: pipe.fused_f16(Md, Nd, st))
+        gather_ms = gemm_ms = None
+    else:
+        gather_ms = timed(lambda: pipe.split_gather(Md, Nd, st))
+        gemm_ms = timed(lambda: pipe.split_gemm(st))
+        fused_ms = None
     kcounts = pipe.k_count.cpu().numpy()
-    kstep = 64 if pipe.f16 else 32
+    kstep = 64 if pipe.f16 else 32  # the contraction's K step (fused fp16 kernel: 32)
     k_exec = int((((kcounts + kstep - 1) // kstep) * kstep).sum())  # columns the compressed contraction runs over
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peak.get("hbm_gbs", 6650.0))
-    tf32_peak = float(peak.get("bf16_tflops", 1590.0)) / (1 if pipe.f16 else 2)  # dense fp16 / TF32 rate
+    tf32_peak = float(peak.get("bf16_tflops", 1590.0)) / (1 if (pipe.f16 or pipe.fused16) else 2)  # fp16 / TF32
     norm_bytes = 4 * B * (m * n + n * p)
     useful = 2.0 * m * p * k_exec  # over the distinct drawn columns (compressed sketch, padded to 32)
     # fp16 split: three kind::f16 K=16 MMAs per 16 K; tf32 split: one TF32 K=8 + one BF16 K=16 per 8 K
-    executed = (3 if pipe.f16 else 2) * useful
+    executed = (3 if (pipe.f16 or pipe.fused16) else 2) * useful
     # the split gather: reads the sampled elements of M and N, writes the split operands
     # (8 bytes per element: tf32 hi in a float32 container + the bf16 pair word)
     k_distinct = int(kcounts.sum())
     split_bytes = (6 if pipe.f16 else 8) * (m + p) * k_exec
     gather_bytes = 4 * (m + p) * k_distinct + split_bytes
-    roof_gather = {"bound": "hbm", "kernel": "gather_a_split_kernel + gather_bt_split_kernel (K4, float32 split)",
+    if fused_ms is not None:
+        # one kernel: reads the sampled elements of M and N once, writes the products
+        fused_bytes = 4 * (m + p) * k_distinct + 4 * B * m * p
+        roof_fused = {"bound": "hbm", "kernel": "gemm_f16split_gather_kernel (gather + fp16 split + tcgen05 "
+                                                "kind::f16 contraction, one CTA per problem)",
+                      "achieved": fused_bytes / (fused_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": fused_bytes / (fused_ms * 1e-3) / 1e9 / hbm_peak,
+                      "algorithmic": "4 B per sampled element of C and D (m + p per distinct drawn column) + 4 B "
+                                     "per product element written",
+                      "algorithmic_bytes": fused_bytes, "traffic": cfg_traffic("cfg5_fused"),
+                      "traffic_note": "M is streamed by TMA in 16-column slabs that hold a drawn column (680 "
+                                      "distinct of 4096 touch ~95% of them, as per-element gathers would in "
+                                      "DRAM bursts): DRAM reads exceed the sampled bytes (profiles/traffic.json)",
+                      "tensor_tflops_executed": executed / (fused_ms * 1e-3) / 1e12,
+                      "tensor_frac": executed / (fused_ms * 1e-3) / 1e12 / tf32_peak}
+    roof_gather = None if fused_ms is not None else {"bound": "hbm", "kernel": "gather_a_split_kernel + gather_bt_split_kernel (K4, float32 split)",
                    "achieved": gather_bytes / (gather_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                    "frac": gather_bytes / (gather_ms * 1e-3) / 1e9 / hbm_peak,
                    "algorithmic": "4 B per sampled element of C and D read + 8 B per split-operand element written "
@@ -1151,31 +1200,37 @@ def run_device(args):
     line = {
         "metric": METRIC, "value": ms_step, "unit": "ms/step", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (TF32 + BF16 split-operand tensor, f64 plan)",
+        "vs_baseline": None, "dtype": ("f32 (fp16 h + l split, kind::f16 tensor, f64 plan)" if (pipe.f16 or pipe.fused16)
+                                       else "f32 (TF32 + BF16 split-operand tensor, f64 plan)"),
         "data": "synthetic (seeded torch generator on device, SURVEY.md §8(d) distributions)",
         "config": {"workload": name, "batch": 4096, "batch_per_gpu": B, "m": m, "n": n, "p": p, "K": K, "W": W, "method": "ONC",
                    "distinct_columns_mean": float(kcounts.mean()),
                    "l2": f"inputs {norm_bytes / 1e9:.1f} GB >> L2"},
         "gpu_launches": int(pipe.graph_launches),
-        "roofline": roof_gather if gather_ms > max(gemm_ms, norms_ms) else
-                    {"bound": "tensor", "kernel": "gemm_f32split_kernel (tcgen05 kind::tf32 + kind::f16 cross terms)",
-                     "achieved": executed / (gemm_ms * 1e-3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
-                     "frac": executed / (gemm_ms * 1e-3) / 1e12 / tf32_peak,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 rate)",
-                     "useful_fp32_tflops": useful / (gemm_ms * 1e-3) / 1e12, "traffic": None},
         "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norm_bytes / (norms_ms * 1e-3) / 1e9,
                            "peak": hbm_peak, "unit": "GB/s", "frac": norm_bytes / (norms_ms * 1e-3) / 1e9 / hbm_peak,
-                           "algorithmic_bytes": norm_bytes},
-        "roofline_gemm": {"bound": "tensor", "kernel": "gemm_f32split_kernel (tcgen05 kind::tf32 + kind::f16 cross terms)",
-                          "achieved": executed / (gemm_ms * 1e-3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
-                          "frac": executed / (gemm_ms * 1e-3) / 1e12 / tf32_peak,
-                          "operand_bytes": split_bytes, "operand_gbs": split_bytes / (gemm_ms * 1e-3) / 1e9},
-        "roofline_gather": roof_gather,
-        "kernel_ms": {"norms_ms": norms_ms, "gather_f32split_ms": gather_ms, "gemm_f32split_ms": gemm_ms},
+                           "algorithmic_bytes": norm_bytes, "traffic": cfg_traffic("cfg5_norms")},
         "rel_err_reference_metric": float(np.sqrt(err_sq / ref_sq)),
         "rel_err_baseline_metric": float(np.sqrt(err_sq) / fro), "error_scope": scope,
+        "numeric_err_vs_f64_sketch": sketch_numeric_err(pipe, Md, Nd, CD, min(B, 16)),
         "clocks": clocks.summary(),
     }
+    if fused_ms is not None:
+        line["roofline_fused"] = roof_fused
+        line["kernel_ms"] = {"norms_ms": norms_ms, "gather_gemm_f16split_fused_ms": fused_ms}
+        dom = max((norms_ms, line["roofline_norms"]), (fused_ms, roof_fused), key=lambda x: x[0])[1]
+    else:
+        line["roofline_gemm"] = {"bound": "tensor", "kernel": "gemm_f16split_2sm_kernel" if pipe.f16 else
+                                 "gemm_f32split_kernel (tcgen05 kind::tf32 + kind::f16 cross terms)",
+                                 "achieved": executed / (gemm_ms * 1e-3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
+                                 "frac": executed / (gemm_ms * 1e-3) / 1e12 / tf32_peak,
+                                 "operand_bytes": split_bytes, "operand_gbs": split_bytes / (gemm_ms * 1e-3) / 1e9,
+                                 "traffic": None}
+        line["roofline_gather"] = roof_gather
+        line["kernel_ms"] = {"norms_ms": norms_ms, "gather_split_ms": gather_ms, "gemm_split_ms": gemm_ms}
+        dom = max((norms_ms, line["roofline_norms"]), (gather_ms, roof_gather), (gemm_ms, line["roofline_gemm"]),
+                  key=lambda x: x[0])[1]
+    line["roofline"] = dict(dom, dominant="the largest of the kernel_ms entries")
     line["e2e"] = {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": int(norm_bytes),
                    "d2h_bytes_per_step": int(B * m * p * 4),
                    "api": "SketchPipeline.run on 8 sub-batches: pinned host M, N -> device -> pinned host products"}

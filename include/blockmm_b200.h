@@ -476,6 +476,21 @@ int bmm_gemm_f32split_gather(int dtype, const void* M, int64_t ldm, int64_t stri
                              const int64_t* w_dev, int64_t batch, float* out, int64_t ldo,
                              int64_t strideO, void* stream);
 
+/* The fp16-split form of the same fusion (round 2, config 5): one CTA per
+ * 256 x 256 output tile, every element of C and D gathered once per tile,
+ * scaled by 2^(kexp[t] - gshift[b]) (C) and 2^(-kexp[t] - gshift[b]) (D) from
+ * bmm_balance_f16, split into fp16 h + l and contracted as h.h + h.l + l.h
+ * (kind::f16) into an unpromoted TMEM accumulator; out[b] = 2^(2 gshift[b])
+ * (C[b] @ D[b]).  The accumulator's truncation error grows with K (~4.5e-9 per
+ * sketch column): the pipeline uses it for W <= 1024.  M is streamed by TMA
+ * (16-column slabs holding a drawn column): its rows must be 16-byte aligned
+ * (ldm, strideM multiples of 4).  dtype BMM_F32 only.                          */
+int bmm_gemm_f16split_gather(int dtype, const void* M, int64_t ldm, int64_t strideM,
+                             const void* N, int64_t ldn, int64_t strideN, int64_t m, int64_t n, int64_t p,
+                             const int64_t* column, const double* scale, const int32_t* kexp,
+                             const int32_t* gshift, int64_t W, int64_t w_stride, const int64_t* w_dev,
+                             int64_t batch, float* out, int64_t ldo, int64_t strideO, void* stream);
+
 /* Diagnostics: the device clock (%globaltimer, ns) written to out[0] by a
  * one-thread kernel on `stream` (graph-capturable; tools/timeline.py).        */
 int bmm_timestamp(unsigned long long* out, void* stream);

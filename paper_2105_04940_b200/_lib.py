@@ -112,6 +112,8 @@ SIGNATURES = {
     "bmm_timestamp": (_I, [_P, _P]),
     "bmm_gemm_f32split_gather": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _P, _I64,
                                       _P, _I64, _I64, _P]),
+    "bmm_gemm_f16split_gather": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64,
+                                      _P, _I64, _P, _I64, _I64, _P]),
 }
 
 _lib = None

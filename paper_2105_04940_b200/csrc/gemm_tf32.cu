@@ -1220,6 +1220,354 @@ __global__ void __launch_bounds__(32 * FG_WARPS, 1) gemm_f32split_gather_kernel(
   }
 }
 
+// ---- fused fp16-split gather + contraction, one CTA per 256 x 256 output tile
+// (round 2, config 5: 4096 problems of 256 x 4096 x 256)
+//
+// The two-kernel form writes the split operands (6 bytes per sketch element)
+// and reads them back: at config 5 that is ~18 GB of the step's ~75 GB of HBM
+// traffic.  Here the sketch is gathered straight into the shared-memory stages
+// the tensor core reads, and one CTA owns a whole 256 x 256 output, so every
+// element of C and D is gathered exactly once (the round-1 fused kernel used
+// 128 x 128 tiles: four CTAs per config-5 problem, each element gathered twice).
+//
+// All global reads are TMA, so the bytes in flight are bounded by shared memory,
+// not registers (per-thread loads of the drawn columns of M, one stage ahead in
+// registers, made a first version long-scoreboard bound at 7.7 ms; 3.5 ms now):
+//   * C: M is streamed in SWIZZLE_64B slabs of 256 rows x 16 columns, only the
+//     slabs that hold a drawn column (680 distinct of 4096 at config 5 touch
+//     ~95% of them -- what per-element gathers fetch from DRAM anyway), 5 deep;
+//   * D: each drawn row of N (256 output columns, 1 KB) is one TMA box, 3
+//     stages of 16 rows deep.
+//   warp 0       tcgen05.mma issuer: per stage (16 K) and row half, h.h, h.l and
+//                l.h (three kind::f16 MMAs, M=128, N=256) into that half's TMEM
+//                accumulator (2 x 256 columns: the whole TMEM)
+//   warps 1-8    C converters: thread = tile row; each drawn column is picked
+//                out of its slab, scaled by scale * 2^(kexp - G), split into
+//                fp16 h + l, stored as the row's [h(16) | l(16)] SWIZZLE_64B
+//                operand line; then the drain (TMEM -> 2^(2G) -> global)
+//   warps 9-16   D^T converters: thread = output column; the stage's 16 rows of
+//                N are read across (conflict-free), scaled, split, stored as the
+//                column's operand line (the transpose happens here)
+//   warp 17      TMA issuer for the slabs of M (a ballot over 32 sketch columns
+//                finds where a new slab starts)
+//   warp 18      TMA issuer for the drawn rows of N
+// Accumulation is not promoted (the TMEM holds no second accumulator pair):
+// the tensor core's truncating float32 accumulate adds ~4.5e-9 relative error
+// per K element in this form, so plan.f16_fused selects the kernel for sketch
+// widths W <= 1024 only (<= 5e-6; config 5 measures 2.4e-6, the bar is 1e-5).
+constexpr int GF_BK = 16;                            // sketch columns per operand stage
+constexpr int GF_TILE = 256 * 64;                    // 16 KB: 256 operand rows x 64 B ([h(16) | l(16)] fp16)
+constexpr int GF_STAGE = 2 * GF_TILE;                // A, B
+constexpr int GF_STAGES = 3;
+constexpr int GF_SLAB_COLS = 16;
+constexpr int GF_SLAB = 256 * GF_SLAB_COLS * 4;      // 16 KB: 256 rows x 64 B of M (SWIZZLE_64B)
+constexpr int GF_SLABS = 5;
+constexpr int GF_BROW = 256 * 4;                     // one row of N: 256 output columns, float32
+constexpr int GF_BRAW = GF_BK * GF_BROW;             // 16 KB: a stage's 16 rows of N
+constexpr int GF_BRAWS = 3;
+constexpr int GF_WARPS = 19;
+constexpr int GF_SMEM = GF_STAGES * GF_STAGE + GF_SLABS * GF_SLAB + GF_BRAWS * GF_BRAW + 1024 + 256;
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_64B (64-byte rows, 8-row groups 512 B apart)
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;           // leading byte offset (unused: K fits one swizzle row)
+  d |= (uint64_t)(512 >> 4) << 32;  // stride byte offset: 8 rows x 64 B
+  d |= (uint64_t)1 << 46;           // Blackwell descriptor version
+  d |= (uint64_t)4 << 61;           // SWIZZLE_64B
+  return d;
+}
+
+// byte offset of 16-byte chunk q (0..3) of row r in a SWIZZLE_64B tile of 64-byte rows
+__device__ __forceinline__ uint32_t sw64(int r, int q) {
+  return (uint32_t)(r * 64 + ((q ^ ((r >> 1) & 3)) << 4));
+}
+
+__device__ __forceinline__ void split_pair(float y0, float y1, uint32_t& hw, uint32_t& lw) {
+  const __half2 h = __floats2half2_rn(y0, y1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(y0 - hf.x, y1 - hf.y);
+  hw = *reinterpret_cast<const uint32_t*>(&h);
+  lw = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+__device__ __forceinline__ void tma_load_3d_gf(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n"
+      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(32 * GF_WARPS, 1) gemm_f16split_gather_kernel(
+    const __grid_constant__ CUtensorMap tm_M, const __grid_constant__ CUtensorMap tm_N, int64_t m, int64_t nc,
+    const int64_t* __restrict__ column, const double* __restrict__ scale, const int32_t* __restrict__ kexp,
+    const int32_t* __restrict__ gshift, int64_t W, int64_t w_stride, const int64_t* __restrict__ count,
+    float* __restrict__ out, int64_t ldo, int64_t strideO) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* slabs = smem + GF_STAGES * GF_STAGE;
+  uint8_t* braw = slabs + GF_SLABS * GF_SLAB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(braw + GF_BRAWS * GF_BRAW);
+  uint64_t* empty = full + GF_STAGES;
+  uint64_t* slab_full = empty + GF_STAGES;
+  uint64_t* slab_empty = slab_full + GF_SLABS;
+  uint64_t* braw_full = slab_empty + GF_SLABS;
+  uint64_t* braw_empty = braw_full + GF_BRAWS;
+  uint64_t* acc_full = braw_empty + GF_BRAWS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = blockIdx.z;
+  const int64_t row0 = (int64_t)blockIdx.y * 256, col0 = (int64_t)blockIdx.x * 256;
+  int64_t cnt = W;
+  if (count != nullptr) cnt = count[b] < W ? count[b] : W;
+  const int ktiles = (int)((cnt + GF_BK - 1) / GF_BK);
+  const int G = gshift[b];
+  const int64_t* colp = column + b * w_stride;
+  const double* scp = scale + b * w_stride;
+  const int32_t* kxp = kexp + b * w_stride;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GF_STAGES; ++s) {
+      mbar_init(&full[s], 16);  // one arrive per converter warp (8 C + 8 D^T), after its stores
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < GF_SLABS; ++s) {
+      mbar_init(&slab_full[s], 1);
+      mbar_init(&slab_empty[s], 8);
+    }
+    for (int s = 0; s < GF_BRAWS; ++s) {
+      mbar_init(&braw_full[s], 1);
+      mbar_init(&braw_empty[s], 8);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_M)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_N)) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- MMA issuer: per stage (16 K) and row half: h.h, h.l, l.h
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16_mn<128, 256>();
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % GF_STAGES;
+        mbar_wait(&full[s], (kt / GF_STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t a = su32(smem + s * GF_STAGE), bb = a + GF_TILE;
+        const uint64_t bh = umma_desc_sw64(bb), bl = umma_desc_sw64(bb + 32);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t ah = a + h * (GF_TILE / 2);
+          const uint32_t acc = tmem + (uint32_t)(h * 256);
+          umma_bf16(acc, umma_desc_sw64(ah), bh, idesc, kt > 0);
+          umma_bf16(acc, umma_desc_sw64(ah), bl, idesc, 1);
+          umma_bf16(acc, umma_desc_sw64(ah + 32), bh, idesc, 1);
+        }
+        umma_commit(&empty[s]);
+      }
+      if (ktiles > 0) umma_commit(acc_full);
+    }
+  } else if (warp == 17) {
+    // ---- TMA issuer for C: the slabs of M (16 columns x 256 rows) holding a drawn
+    // column, in order; 32 sketch columns scanned at a time (ballot of slab changes)
+    int64_t prev = -1;
+    int j = 0;
+    for (int64_t g = 0; g < cnt; g += 32) {
+      const int64_t t = g + lane;
+      const int64_t slab = t < cnt ? (__ldg(colp + t) >> 4) : (int64_t)-1;
+      int64_t before = __shfl_up_sync(0xffffffffu, slab, 1);
+      if (lane == 0) before = prev;
+      uint32_t fresh = __ballot_sync(0xffffffffu, t < cnt && slab != before);
+      prev = __shfl_sync(0xffffffffu, slab, 31);
+      while (fresh) {
+        const int src = __ffs(fresh) - 1;
+        fresh &= fresh - 1;
+        const int64_t c = __shfl_sync(0xffffffffu, slab, src);
+        if (lane == 0) {
+          const int s = j % GF_SLABS;
+          if (j >= GF_SLABS) mbar_wait(&slab_empty[s], ((j / GF_SLABS) - 1) & 1);
+          mbar_expect_tx(&slab_full[s], GF_SLAB);
+          tma_load_3d_gf(slabs + s * GF_SLAB, &tm_M, &slab_full[s], (int)(c * GF_SLAB_COLS), (int)row0, (int)b);
+        }
+        ++j;
+      }
+    }
+  } else if (warp == 18) {
+    // ---- TMA issuer for D: each stage's 16 drawn rows of N (256 output columns each)
+    if (lane == 0) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % GF_BRAWS;
+        if (kt >= GF_BRAWS) mbar_wait(&braw_empty[s], ((kt / GF_BRAWS) - 1) & 1);
+        const int nval = (int)min((int64_t)GF_BK, cnt - (int64_t)kt * GF_BK);
+        mbar_expect_tx(&braw_full[s], nval * GF_BROW);
+        for (int i = 0; i < nval; ++i)
+          tma_load_3d_gf(braw + s * GF_BRAW + i * GF_BROW, &tm_N, &braw_full[s], (int)col0,
+                         (int)__ldg(colp + (int64_t)kt * GF_BK + i), (int)b);
+      }
+    }
+  } else if (warp <= 8) {
+    // ---- C converters: thread = tile row r, one stage (16 sketch columns) per iteration,
+    // unrolled.  Lane i < 16 holds sketch column 16 kt + i: its byte in an unswizzled slab
+    // row and its factor scale * 2^(kexp - G) (exact: a power of two); a ballot marks where
+    // a new slab starts.  Pairs of columns are split with one packed conversion each way;
+    // a stage's row goes out as four 16-byte stores ([h(8)] [h(8)] [l(8)] [l(8)]).
+    const int r = (warp - 1) * 32 + lane;
+    const uint32_t sbase = su32(smem);
+    const uint32_t rslab = su32(slabs) + (uint32_t)(r * 64);
+    const uint32_t rsw16 = (uint32_t)(((r >> 1) & 3) << 4);  // SWIZZLE_64B: chunk ^= (r >> 1) & 3
+    int j = -1;
+    uint32_t sl = 0;
+    int64_t carry = -1;  // the slab of the previous stage's last column
+    auto meta = [&](int kt, int64_t& c_, float& f_) {  // lane's sketch column of stage kt (lanes < 16)
+      const int64_t t = (int64_t)kt * GF_BK + lane;
+      const bool ok = lane < GF_BK && t < cnt;
+      c_ = ok ? __ldg(colp + t) : (int64_t)-1;
+      f_ = ok ? __fmul_rn((float)__ldg(scp + t), pow2f(__ldg(kxp + t) - G)) : 0.f;
+    };
+    int64_t ncol;
+    float nfac;
+    meta(0, ncol, nfac);
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int64_t t = (int64_t)kt * GF_BK + lane;
+      const bool ok = lane < GF_BK && t < cnt;
+      const int64_t col = ncol;
+      const float fac = nfac;
+      meta(kt + 1, ncol, nfac);  // one stage ahead
+      const int64_t slab = col >> 4;
+      int64_t before = __shfl_up_sync(0xffffffffu, slab, 1);
+      if (lane == 0) before = carry;
+      const uint32_t fresh = __ballot_sync(0xffffffffu, ok && slab != before);
+      const int nval = (int)min((int64_t)GF_BK, cnt - (int64_t)kt * GF_BK);
+      carry = __shfl_sync(0xffffffffu, slab, nval - 1);
+      const uint32_t q4 = (uint32_t)(col & 15) * 4;
+      if (kt >= GF_STAGES) mbar_wait(&empty[kt % GF_STAGES], ((kt / GF_STAGES) - 1) & 1);
+      const uint32_t st = sbase + (uint32_t)((kt % GF_STAGES) * GF_STAGE);
+      uint32_t hw[8], lw[8];
+#pragma unroll
+      for (int i = 0; i < GF_BK; i += 2) {
+        float y[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int tt = i + u;
+          if ((fresh >> tt) & 1u) {  // warp-uniform: the next slab
+            if (j >= 0) {
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&slab_empty[j % GF_SLABS]);
+            }
+            ++j;
+            mbar_wait(&slab_full[j % GF_SLABS], (j / GF_SLABS) & 1);
+            sl = rslab + (uint32_t)((j % GF_SLABS) * GF_SLAB);
+          }
+          const uint32_t o = __shfl_sync(0xffffffffu, q4, tt) ^ rsw16;
+          const float f = __shfl_sync(0xffffffffu, fac, tt);
+          y[u] = tt < nval ? __fmul_rn(lds_f32(sl + o), f) : 0.f;
+        }
+        split_pair(y[0], y[1], hw[i >> 1], lw[i >> 1]);
+      }
+      sts128s(st + sw64(r, 0), hw[0], hw[1], hw[2], hw[3]);
+      sts128s(st + sw64(r, 1), hw[4], hw[5], hw[6], hw[7]);
+      sts128s(st + sw64(r, 2), lw[0], lw[1], lw[2], lw[3]);
+      sts128s(st + sw64(r, 3), lw[4], lw[5], lw[6], lw[7]);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[kt % GF_STAGES]);
+    }
+    if (j >= 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&slab_empty[j % GF_SLABS]);
+    }
+    // ---- drain: warp w reads TMEM lanes 32 (w % 4), row half (w - 1) / 4, all 256 columns
+    const int quarter = warp & 3, half = (warp - 1) >> 2;
+    if (ktiles > 0) {
+      mbar_wait(acc_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    }
+    const float unscale = pow2f(2 * G);
+    const int64_t row = row0 + half * 128 + quarter * 32 + lane;
+    float* orow = out + b * strideO + (row < m ? row : 0) * ldo;
+    const bool vec = (col0 + 256 <= nc) && (ldo % 4) == 0 && ((reinterpret_cast<uintptr_t>(orow + col0) & 15) == 0);
+#pragma unroll 1
+    for (int cc = 0; cc < 256; cc += 32) {
+      uint32_t v[32];
+      if (ktiles > 0) {
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 256 + cc), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) v[jj] = 0u;
+      }
+      if (row < m) {
+        if (vec) {
+          float4* o4 = reinterpret_cast<float4*>(orow + col0 + cc);
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            o4[jj] = make_float4(__uint_as_float(v[4 * jj]) * unscale, __uint_as_float(v[4 * jj + 1]) * unscale,
+                                 __uint_as_float(v[4 * jj + 2]) * unscale, __uint_as_float(v[4 * jj + 3]) * unscale);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            if (col0 + cc + jj < nc) orow[col0 + cc + jj] = __uint_as_float(v[jj]) * unscale;
+        }
+      }
+    }
+  } else {
+    // ---- D^T converters (warps 9-16): thread = output column f of the tile; the stage's
+    // 16 rows of N arrive by TMA (a 1 KB row each), are scaled, split and stored as the
+    // thread's operand row [h(16) | l(16)]
+    const int fl = (warp - 9) * 32 + lane;
+    const uint32_t sbase = su32(smem);
+    auto meta = [&](int kt) {  // lane's factor scale * 2^(-kexp - G) of stage kt (lanes < 16)
+      const int64_t t = (int64_t)kt * GF_BK + lane;
+      const bool ok = lane < GF_BK && t < cnt;
+      return ok ? __fmul_rn((float)__ldg(scp + t), pow2f(-__ldg(kxp + t) - G)) : 0.f;
+    };
+    float nfac = meta(0);
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const float fac = nfac;
+      nfac = meta(kt + 1);  // one stage ahead
+      const int nval = (int)min((int64_t)GF_BK, cnt - (int64_t)kt * GF_BK);
+      const int sr = kt % GF_BRAWS;
+      mbar_wait(&braw_full[sr], (kt / GF_BRAWS) & 1);
+      const uint32_t raw = su32(braw + sr * GF_BRAW) + 4u * fl;
+      float y[GF_BK];
+#pragma unroll
+      for (int i = 0; i < GF_BK; ++i)
+        y[i] = i < nval ? __fmul_rn(lds_f32(raw + i * GF_BROW), __shfl_sync(0xffffffffu, fac, i)) : 0.f;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&braw_empty[sr]);
+      uint32_t hw[8], lw[8];
+#pragma unroll
+      for (int i = 0; i < GF_BK; i += 2) split_pair(y[i], y[i + 1], hw[i >> 1], lw[i >> 1]);
+      if (kt >= GF_STAGES) mbar_wait(&empty[kt % GF_STAGES], ((kt / GF_STAGES) - 1) & 1);
+      const uint32_t bt = sbase + (uint32_t)((kt % GF_STAGES) * GF_STAGE) + GF_TILE;
+      sts128s(bt + sw64(fl, 0), hw[0], hw[1], hw[2], hw[3]);
+      sts128s(bt + sw64(fl, 1), hw[4], hw[5], hw[6], hw[7]);
+      sts128s(bt + sw64(fl, 2), lw[0], lw[1], lw[2], lw[3]);
+      sts128s(bt + sw64(fl, 3), lw[4], lw[5], lw[6], lw[7]);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[kt % GF_STAGES]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+  }
+}
+
 // ---- host side
 
 static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int box_rows = T_BM) {
@@ -1549,5 +1897,62 @@ extern "C" int bmm_gemm_f32split_gather(int dtype, const void* M, int64_t ldm, i
       (const float*)M, ldm, strideM, (const float*)N, ldn, strideN, m, p, column, scale, W, w_stride, w_dev, out, ldo,
       strideO);
   BMM_CHECK_LAUNCH("gemm_f32split_gather_kernel");
+  return BMM_OK;
+}
+
+extern "C" int bmm_gemm_f16split_gather(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
+                                        int64_t ldn, int64_t strideN, int64_t m, int64_t n, int64_t p,
+                                        const int64_t* column, const double* scale, const int32_t* kexp,
+                                        const int32_t* gshift, int64_t W, int64_t w_stride, const int64_t* w_dev,
+                                        int64_t batch, float* out, int64_t ldo, int64_t strideO, void* stream) {
+  BMM_REQUIRE(m >= 1 && n >= 1 && p >= 1 && W >= 1 && batch >= 1, BMM_E_ARG, "bmm_gemm_f16split_gather: bad shape");
+  BMM_REQUIRE(kexp != nullptr && gshift != nullptr, BMM_E_ARG, "bmm_gemm_f16split_gather: kexp / gshift is NULL");
+  BMM_REQUIRE(dtype == BMM_F32, BMM_E_UNSUPPORTED, "bmm_gemm_f16split_gather: float32 inputs only");
+  BMM_REQUIRE(batch <= 65535 && ceil_div(m, 256) <= 65535 && n < (1LL << 31), BMM_E_UNSUPPORTED,
+              "bmm_gemm_f16split_gather: grid too large");
+  BMM_REQUIRE(ldm % 4 == 0 && (batch == 1 || strideM % 4 == 0) && (reinterpret_cast<uintptr_t>(M) & 15) == 0,
+              BMM_E_UNSUPPORTED, "bmm_gemm_f16split_gather: M rows must be 16-byte aligned (TMA)");
+  auto enc = get_encode();
+  BMM_REQUIRE(enc != nullptr, BMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  // M as [batch][m][n] float32: boxes of 16 columns x 256 rows of one problem, SWIZZLE_64B
+  CUtensorMap tm;
+  cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)m, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)ldm * 4, (cuuint64_t)(batch == 1 ? ldm * m : strideM) * 4};
+  cuuint32_t box[3] = {(cuuint32_t)GF_SLAB_COLS, 256, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(M), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BMM_REQUIRE(r == CUDA_SUCCESS, BMM_E_CUDA, "bmm_gemm_f16split_gather: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  BMM_REQUIRE(ldn % 4 == 0 && (batch == 1 || strideN % 4 == 0) && (reinterpret_cast<uintptr_t>(N) & 15) == 0,
+              BMM_E_UNSUPPORTED, "bmm_gemm_f16split_gather: N rows must be 16-byte aligned (TMA)");
+  // N as [batch][n][p] float32: one drawn row (256 output columns of the tile) per box
+  CUtensorMap tn;
+  cuuint64_t ndims[3] = {(cuuint64_t)p, (cuuint64_t)n, (cuuint64_t)batch};
+  cuuint64_t nstrides[2] = {(cuuint64_t)ldn * 4, (cuuint64_t)(batch == 1 ? ldn * n : strideN) * 4};
+  cuuint32_t nbox[3] = {256, 1, 1};
+  r = enc(&tn, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(N), ndims, nstrides, nbox, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BMM_REQUIRE(r == CUDA_SUCCESS, BMM_E_CUDA, "bmm_gemm_f16split_gather: cuTensorMapEncodeTiled (N) failed (%d)", (int)r);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(gemm_f16split_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GF_SMEM);
+  BMM_REQUIRE(attr == cudaSuccess, BMM_E_CUDA, "bmm_gemm_f16split_gather: %d bytes of shared memory: %s", GF_SMEM,
+              cudaGetErrorString(attr));
+  dim3 grid((unsigned)ceil_div(p, 256), (unsigned)ceil_div(m, 256), (unsigned)batch);
+  gemm_f16split_gather_kernel<<<grid, 32 * GF_WARPS, GF_SMEM, as_stream(stream)>>>(
+      tm, tn, m, p, column, scale, kexp, gshift, W, w_stride, w_dev, out, ldo, strideO);
+  {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cudaFuncAttributes fa = {};
+      cudaFuncGetAttributes(&fa, gemm_f16split_gather_kernel);
+      set_error("gemm_f16split_gather_kernel: launch failed: %s (regs %d, max threads %d, static smem %zu, "
+                "max dynamic %d, requested %d x %d threads)", cudaGetErrorString(e), fa.numRegs,
+                fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, GF_SMEM, 32 * GF_WARPS);
+      return BMM_E_CUDA;
+    }
+    count_launch();
+  }
   return BMM_OK;
 }

@@ -27,7 +27,7 @@ import torch
 
 from . import _lib
 from . import rng as _rng
-from .plan import PILOT_GRAM_MAX, f32_fused, gemm_engine, raise_status, segsq_engine
+from .plan import PILOT_GRAM_MAX, f16_fused, f32_fused, gemm_engine, raise_status, segsq_engine
 
 METHODS = ("OPL", "ONC", "UU", "ONU", "ONMCNR", "SSM")
 
@@ -211,16 +211,20 @@ class SketchPipeline:
         # small float32 outputs (at most 4 x 4 tiles of 128): gather inside the contraction
         # (bmm_gemm_f32split_gather); large ones would re-gather A once per column tile
         self.fused = self.tf32 and self.compress and f32_fused(self.m, self.p)
+        # outputs of one 256 x 256 tile at W <= 1024 (config 5): the fp16-split gather and
+        # contraction in one kernel, no split operands in HBM
+        self.fused16 = (self.tf32 and self.compress and not self.fused and self.n % 4 == 0 and self.p % 4 == 0
+                        and f16_fused(self.m, self.p, W))  # (TMA streams rows of M and N)
         # large float32 outputs: the fp16 split on CTA pairs (3 tensor instructions per 16 K
         # instead of 4; BMM_F16=0 keeps the tf32 + bf16 split)
-        self.f16 = (self.tf32 and self.compress and not self.fused and self.m >= 256 and self.p >= 256
-                    and os.environ.get("BMM_F16", "1") != "0")
-        if self.f16:
+        self.f16 = (self.tf32 and self.compress and not self.fused and not self.fused16 and self.m >= 256
+                    and self.p >= 256 and os.environ.get("BMM_F16", "1") != "0")
+        if self.f16 or self.fused16:
             self.kexp = torch.zeros(B * W, dtype=torch.int32, device=dev)
             self.gshift = torch.zeros(B, dtype=torch.int32, device=dev)
         if self.tf32:
             f32 = dict(dtype=torch.float32, device=dev)
-            if not self.fused:
+            if not (self.fused or self.fused16):
                 self.a_hi = torch.empty(B * self.m * W, **f32)
                 self.a_x = torch.empty(B * self.m * W, **f32)
                 self.b_hi = torch.empty(B * self.p * W, **f32)
@@ -474,6 +478,8 @@ class SketchPipeline:
             # float32 inputs: the split gather runs inside the tcgen05 contraction's producer warps
             self._c("bmm_gemm_f32split_gather", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
                     P(self.k_scale), W, W, P(self.k_count), B, P(self.CD), p, m * p, st)
+        elif self.fused16:
+            self.fused_f16(M, N, st)
         elif self.tf32 and self.compress:
             # float32 inputs: split gather + tcgen05 contraction (fp16 or tf32 + bf16 split)
             self.split_gather(M, N, st)
@@ -486,6 +492,18 @@ class SketchPipeline:
         else:
             self.contract(M, N, st)
         return self._result()
+
+    def fused_f16(self, M, N, st=None):
+        """Balanced exponents, then the fp16-split gather + contraction in one
+        kernel (K4 + K6 fused, bmm_gemm_f16split_gather)."""
+        B, m, n, p, W = self.B, self.m, self.n, self.p, self.W
+        st = _lib.stream_ptr() if st is None else st
+        P = lambda t: t.data_ptr()  # noqa: E731
+        self._c("bmm_balance_f16", P(self.colsq), P(self.rowsq), n, P(self.k_column), P(self.k_scale), W, W,
+                P(self.k_count), B, P(self.kexp), P(self.gshift), st)
+        self._c("bmm_gemm_f16split_gather", _lib.matrix_dtype(M), P(M), M.stride(-2), m * n, P(N), N.stride(-2),
+                n * p, m, n, p, P(self.k_column), P(self.k_scale), P(self.kexp), P(self.gshift), W, W, P(self.k_count),
+                B, P(self.CD), p, m * p, st)
 
     def split_gather(self, M, N, st=None):
         """The float32 path's split gather of the compressed sketch (K4)."""

@@ -257,6 +257,19 @@ def f32_fused(m: int, p: int) -> bool:
     return m <= 128 and p <= 128
 
 
+def f16_fused(m: int, p: int, W: int) -> bool:
+    """float32 compressed sketches with outputs of at most one 256 x 256 tile
+    (config 5): gather, fp16 split and contraction in one kernel
+    (bmm_gemm_f16split_gather: every sketch element gathered once, no split
+    operands in HBM).  Its accumulator is not promoted, so only for W <= 1024
+    (error <= ~5e-6).  Single 128 x 128 tiles keep bmm_gemm_f32split_gather;
+    BMM_F16_FUSED=0|1 forces the choice."""
+    forced = os.environ.get("BMM_F16_FUSED", "")
+    if forced in ("0", "1"):
+        return forced == "1" and W <= 1024
+    return m <= 256 and p <= 256 and not (m <= 128 and p <= 128) and W <= 1024
+
+
 def segsq(A: torch.Tensor, B: torch.Tensor, seg: torch.Tensor, nseg: int) -> torch.Tensor:
     if A.dtype != torch.float64:
         A = A.to(torch.float64)

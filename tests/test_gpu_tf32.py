@@ -185,3 +185,64 @@ def test_f16_split_pair_contraction(B, m, p, n, W, spread):
         err = ((out[b].double() - ref).norm() / ref.norm()).item()
         assert err < 1e-5, (b, err)
         assert torch.isfinite(out[b]).all()
+
+
+@pytest.mark.parametrize("B,m,p,n,W,spread,zero", [
+    (3, 256, 256, 4096, 1024, 0.5, False),   # config-5 shape
+    (2, 200, 252, 2048, 512, 2.0, False),    # ragged rows / columns inside one tile
+    (2, 300, 140, 1500, 1000, 1.0, False),   # two row tiles, one column tile
+    (2, 256, 256, 1024, 96, 0.5, True),      # a problem with no drawn column (count 0)
+])
+def test_f16_split_fused_gather(B, m, p, n, W, spread, zero):
+    """bmm_gemm_f16split_gather (gather + fp16 split + contraction in one kernel,
+    one CTA per 256 x 256 tile): distinct counts not a multiple of 32, a zero
+    column, wide column / row scales, ragged tiles and an empty sketch -- against
+    float64 of the same float32 sketch within 1e-5."""
+    g = torch.Generator(device="cuda").manual_seed(B * 11 + m + p + W)
+    M = torch.randn((B, m, n), generator=g, device="cuda") * torch.exp(spread * torch.randn((B, 1, n), generator=g, device="cuda"))
+    N = torch.randn((B, n, p), generator=g, device="cuda") * torch.exp(spread * torch.randn((B, n, 1), generator=g, device="cuda"))
+    M[:, :, 3] = 0.0
+    colsq = (M.double() ** 2).sum(1).reshape(-1)
+    rowsq = (N.double() ** 2).sum(2).reshape(-1)
+    cnt = [min(W, n, (W * 2) // 3 + 37 * b + 5) for b in range(B)]
+    if zero:
+        cnt[0] = 0
+    col = torch.zeros((B, W), dtype=torch.int64, device="cuda")
+    sc = torch.zeros((B, W), dtype=torch.float64, device="cuda")
+    for b in range(B):
+        c = torch.sort(torch.randperm(n, generator=g, device="cuda")[:cnt[b]]).values
+        col[b, :cnt[b]] = c
+        sc[b, :cnt[b]] = torch.rand(cnt[b], generator=g, device="cuda", dtype=torch.float64) * 50 + 0.01
+    kd = torch.as_tensor(cnt, dtype=torch.int64, device="cuda")
+    kexp = torch.zeros((B, W), dtype=torch.int32, device="cuda")
+    gsh = torch.zeros(B, dtype=torch.int32, device="cuda")
+    st = _lib.stream_ptr()
+    _lib.call("bmm_balance_f16", colsq.data_ptr(), rowsq.data_ptr(), n, col.data_ptr(), sc.data_ptr(), W, W,
+              kd.data_ptr(), B, kexp.data_ptr(), gsh.data_ptr(), st)
+    out = torch.full((B, m, p), float("nan"), dtype=torch.float32, device="cuda")
+    _lib.call("bmm_gemm_f16split_gather", _lib.BMM_F32, M.data_ptr(), n, m * n, N.data_ptr(), p, n * p, m, n, p,
+              col.data_ptr(), sc.data_ptr(), kexp.data_ptr(), gsh.data_ptr(), W, W, kd.data_ptr(), B,
+              out.data_ptr(), p, m * p, st)
+    torch.cuda.synchronize()
+    for b in range(B):
+        assert torch.isfinite(out[b]).all(), b
+        if cnt[b] == 0:
+            assert (out[b] == 0).all()
+            continue
+        c, s = col[b, :cnt[b]], sc[b, :cnt[b]]
+        C = (M[b][:, c] * s.float()).double()
+        D = (N[b][c, :] * s.float()[:, None]).double()
+        ref = C @ D
+        err = ((out[b].double() - ref).norm() / ref.norm()).item()
+        assert err < 1e-5, (b, err)
+    # rows of N that TMA cannot address (p % 4 != 0) are refused, not misread
+    if p % 8 == 4:
+        with pytest.raises(RuntimeError, match="16-byte aligned"):
+            _lib.call("bmm_gemm_f16split_gather", _lib.BMM_F32, M.data_ptr(), n, m * n, N.data_ptr(), p - 2,
+                      n * p, m, n, p - 2, col.data_ptr(), sc.data_ptr(), kexp.data_ptr(), gsh.data_ptr(), W, W,
+                      kd.data_ptr(), B, out.data_ptr(), p, m * p, st)
+    # the float32 path's dtype check: float64 inputs are refused, not misread
+    with pytest.raises(RuntimeError):
+        _lib.call("bmm_gemm_f16split_gather", _lib.BMM_F64, M.data_ptr(), n, m * n, N.data_ptr(), p, n * p, m, n, p,
+                  col.data_ptr(), sc.data_ptr(), kexp.data_ptr(), gsh.data_ptr(), W, W, kd.data_ptr(), B,
+                  out.data_ptr(), p, m * p, st)
