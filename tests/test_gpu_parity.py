@@ -401,3 +401,38 @@ def test_fused_gather_kernels_match_materialised_sketch():
               W, seg.data_ptr(), 4, 0, 1, g_out.data_ptr(), ws.data_ptr(), ws.numel(), st)
     np.testing.assert_allclose(g_out.cpu().numpy(), g_ref.cpu().numpy(), rtol=1e-13)
     assert g_ref[1].item() == 0.0
+
+
+# ---------------------------------------------------------------- OPL weights
+
+@pytest.mark.parametrize("case", ["cfg1", "unequal", "rank1"])
+def test_optimal_size_weights_and_real_budgets(case):
+    """optimal_size_weights = sqrt(max(s^2 - g^2, 0)) and real_optimal_budgets =
+    c w / sum(w) (reference plan.py:350-370) against the oracle's s (exact order)
+    and g (BLAS order: tolerance-level, 1e-12); the rank-1 case has g_k = s_k in
+    exact arithmetic (radicand at the rounding slack, clamped to ~0)."""
+    g = np.random.default_rng(77)
+    if case == "cfg1":
+        M, N = g.standard_normal((60, 1000)), g.standard_normal((1000, 50))
+        sizes = (100,) * 10
+    elif case == "unequal":
+        M = g.standard_normal((40, 700)) * g.lognormal(0, 1.5, 700)
+        N = g.standard_normal((700, 30)) * g.lognormal(0, 1.5, (700, 1))
+        sizes = (1, 99, 300, 50, 250)
+    else:  # every block's product M^k N_k is a sum of rank-1 terms u v^T: g_k = s_k
+        u, v = g.standard_normal(20), g.standard_normal(30)
+        a, b = g.lognormal(0, 1, 200), g.lognormal(0, 1, 200)
+        M, N = np.outer(u, a), np.outer(b, v)
+        sizes = (50,) * 4
+    part = bm.BlockPartition(sizes)
+    cs, rs = O.colsq(M), O.rowsq(N)
+    _, s = O.block_stats(cs, rs, sizes)
+    gsq = O.block_product_sq(M, N, sizes)
+    w_ref = np.sqrt(np.maximum(s ** 2 - gsq, 0.0))
+    w = bm.optimal_size_weights(M, N, part)
+    if case == "rank1":
+        assert np.all(w <= 1e-6 * s) and np.all(w_ref <= 1e-6 * s)
+        return
+    assert rel(w, w_ref) < 1e-12
+    r = bm.real_optimal_budgets(M, N, part, 40)
+    assert abs(r.sum() - 40) < 1e-9 and rel(r, 40 * w_ref / w_ref.sum()) < 1e-12

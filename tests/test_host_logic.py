@@ -100,3 +100,67 @@ def test_seeds_from_keys_matches_generators(method):
     assert np.array_equal(a.main.words, b.main.words) and np.array_equal(a.main.first, b.main.first)
     if method == "ONU":
         assert np.array_equal(a.pilot.words, b.pilot.words) and np.array_equal(a.pilot.first, b.pilot.first)
+
+
+# ---------------------------------------------------------------- matrix helpers
+
+def test_as_matrix_coerces_and_validates():
+    """as_matrix (reference matrix.py:21-32): float64, C-ordered, 2-D, finite."""
+    from paper_2105_04940_b200.matrix import as_matrix
+    a = as_matrix([[1, 2], [3, 4]])
+    assert a.dtype == np.float64 and a.flags.c_contiguous and a.shape == (2, 2)
+    f = np.asfortranarray(np.arange(6, dtype=np.float32).reshape(2, 3))
+    b = as_matrix(f)
+    assert b.flags.c_contiguous and b.dtype == np.float64 and np.array_equal(b, f)
+    c = np.ones((3, 4))
+    assert as_matrix(c) is c or np.shares_memory(as_matrix(c), c)  # already conforming: no copy
+    with pytest.raises(ValueError, match="2-D"):
+        as_matrix(np.ones(3))
+    with pytest.raises(ValueError, match="2-D"):
+        as_matrix(np.ones((2, 2, 2)))
+    for bad in (np.nan, np.inf, -np.inf):
+        x = np.ones((2, 2))
+        x[1, 0] = bad
+        with pytest.raises(ValueError, match="NaN or Inf"):
+            as_matrix(x)
+
+
+def test_block_partition_contract():
+    """BlockPartition (reference matrix.py:35-79): sizes, equal(), offsets, block_slice."""
+    p = BlockPartition((3, 1, 4))
+    assert p.num_blocks == 3 and p.total == 8
+    assert list(p.offsets) == [0, 3, 4, 8] and p.offsets.dtype == np.int64
+    assert p.block_slice(2) == slice(4, 8)
+    with pytest.raises(IndexError):
+        p.block_slice(3)
+    with pytest.raises(IndexError):
+        p.block_slice(-1)
+    assert BlockPartition.equal(12, 4).sizes == (3, 3, 3, 3)
+    with pytest.raises(ValueError):
+        BlockPartition.equal(10, 4)
+    with pytest.raises(ValueError):
+        BlockPartition(())
+    with pytest.raises(ValueError):
+        BlockPartition((2, 0, 1))
+    with pytest.raises(ValueError, match="partition covers"):
+        p.check_length(9)
+
+
+def test_block_view_zero_copy():
+    """block_view (reference matrix.py:82-95): views, never copies; axis and length checks."""
+    from paper_2105_04940_b200.matrix import block_view
+    part = BlockPartition((2, 3, 1))
+    M = np.arange(4 * 6, dtype=np.float64).reshape(4, 6)
+    N = np.arange(6 * 5, dtype=np.float64).reshape(6, 5)
+    v = block_view(M, part, 1, "columns")
+    assert v.shape == (4, 3) and np.shares_memory(v, M) and np.array_equal(v, M[:, 2:5])
+    w = block_view(N, part, 2, "rows")
+    assert w.shape == (1, 5) and np.shares_memory(w, N) and np.array_equal(w, N[5:6])
+    v[0, 0] = -1.0  # a view: writes show through
+    assert M[0, 2] == -1.0
+    with pytest.raises(ValueError, match="axis"):
+        block_view(M, part, 0, "diagonal")
+    with pytest.raises(ValueError, match="partition covers"):
+        block_view(N, part, 0, "columns")
+    with pytest.raises(IndexError):
+        block_view(M, part, 3)
