@@ -491,6 +491,30 @@ int bmm_gemm_f16split_gather(int dtype, const void* M, int64_t ldm, int64_t stri
                              const int32_t* gshift, int64_t W, int64_t w_stride, const int64_t* w_dev,
                              int64_t batch, float* out, int64_t ldo, int64_t strideO, void* stream);
 
+/* ---------------------------------------------------------------- exchanges over NCCL
+ * The cross-rank steps of the sharded product (distributed.py; SURVEY §8(b2)
+ * optional ncclComm_t variants, §8(e1) C1-C3), enqueued on the caller's stream.
+ * NCCL is resolved at run time (libnccl.so.2, the process's own copy when one
+ * is loaded); without it these return BMM_E_UNSUPPORTED.  `comm` is an
+ * ncclComm_t (opaque here: no NCCL types in the ABI).
+ * bmm_nccl_version: NCCL's version code, 0 when unavailable.
+ * bmm_nccl_unique_id: ncclGetUniqueId into id_out (128 bytes); rank 0 makes
+ *   it, the caller broadcasts it (torch.distributed does it in distributed.py).
+ * bmm_nccl_comm_init / _destroy: ncclCommInitRank / ncclCommDestroy.
+ * bmm_all_gather_f64_nccl: dst (nranks x len) = every rank's src, rank order
+ *   (C1: the colsq chain hand-offs and the rowsq subtree partials).
+ * bmm_exchange_sum_nccl: out = ((p_0 + p_1) + p_2) + ... over the ranks'
+ *   partials (C2: g_k^2 and pilot^2 over output tiles; C3: error sums) --
+ *   an all-gather into ws (nranks x len) and a fixed rank-order sum, so every
+ *   rank holds identical bits (replaces distributed.exchange_sum).            */
+int bmm_nccl_version(void);
+int bmm_nccl_unique_id(void* id_out);
+int bmm_nccl_comm_init(void** comm_out, int nranks, const void* id, int rank);
+int bmm_nccl_comm_destroy(void* comm);
+int bmm_all_gather_f64_nccl(void* comm, const double* src, int64_t len, double* dst, void* stream);
+int bmm_exchange_sum_nccl(void* comm, int nranks, const double* partial, int64_t len, double* ws,
+                          double* out, void* stream);
+
 /* Diagnostics: the device clock (%globaltimer, ns) written to out[0] by a
  * one-thread kernel on `stream` (graph-capturable; tools/timeline.py).        */
 int bmm_timestamp(unsigned long long* out, void* stream);

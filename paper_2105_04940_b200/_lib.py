@@ -112,6 +112,12 @@ SIGNATURES = {
     "bmm_timestamp": (_I, [_P, _P]),
     "bmm_gemm_f32split_gather": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I64, _P, _I64,
                                       _P, _I64, _I64, _P]),
+    "bmm_nccl_version": (_I, []),
+    "bmm_nccl_unique_id": (_I, [_P]),
+    "bmm_nccl_comm_init": (_I, [_P, _I, _P, _I]),
+    "bmm_nccl_comm_destroy": (_I, [_P]),
+    "bmm_all_gather_f64_nccl": (_I, [_P, _P, _I64, _P, _P]),
+    "bmm_exchange_sum_nccl": (_I, [_P, _I, _P, _I64, _P, _P, _P]),
     "bmm_gemm_f16split_gather": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64,
                                       _P, _I64, _P, _I64, _I64, _P]),
 }

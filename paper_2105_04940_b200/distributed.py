@@ -169,6 +169,61 @@ def exchange_sum(partial: torch.Tensor, group=None) -> torch.Tensor:
     return acc
 
 
+class NcclComm:
+    """An NCCL communicator owned by the C-ABI (bmm_nccl_comm_init), for the
+    exchanges enqueued on the current stream as C-ABI calls
+    (bmm_all_gather_f64_nccl / bmm_exchange_sum_nccl: SURVEY §8(b2) optional
+    ncclComm_t variants).  Built over a torch.distributed group, which only
+    carries the unique id from rank 0; world 1 needs no group."""
+
+    def __init__(self, group=None):
+        import ctypes
+        self.world = _world(group)
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        uid = np.zeros(128, dtype=np.uint8)
+        if self.rank == 0:
+            _lib.call("bmm_nccl_unique_id", uid.ctypes.data)
+        if self.world > 1:
+            box = [uid.tobytes()]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            uid = np.frombuffer(box[0], dtype=np.uint8).copy()
+        ptr = ctypes.c_void_p()
+        _lib.call("bmm_nccl_comm_init", ctypes.addressof(ptr), self.world, uid.ctypes.data, self.rank)
+        self.comm = ptr.value
+        self._ws = None
+
+    def all_gather(self, buf: torch.Tensor) -> torch.Tensor:
+        """(world, len) gathered copy of every rank's float64 `buf`."""
+        src = buf.contiguous()
+        out = torch.empty((self.world,) + tuple(src.shape), dtype=torch.float64, device=src.device)
+        _lib.call("bmm_all_gather_f64_nccl", self.comm, src.data_ptr(), src.numel(), out.data_ptr(),
+                  _lib.stream_ptr())
+        return out
+
+    def exchange_sum(self, buf: torch.Tensor) -> torch.Tensor:
+        """The rank-ordered sum of every rank's float64 `buf` (= exchange_sum)."""
+        src = buf.contiguous()
+        n = src.numel()
+        if self._ws is None or self._ws.numel() < self.world * n:
+            self._ws = torch.empty(self.world * n, dtype=torch.float64, device=src.device)
+        out = torch.empty_like(src)
+        _lib.call("bmm_exchange_sum_nccl", self.comm, self.world, src.data_ptr(), n, self._ws.data_ptr(),
+                  out.data_ptr(), _lib.stream_ptr())
+        return out
+
+    def close(self) -> None:
+        if self.comm:
+            _lib.call("bmm_nccl_comm_destroy", self.comm)
+            self.comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
+
+
 def _kernel_colsq(Mslab: torch.Tensor, acc: torch.Tensor, accumulate: bool) -> None:
     rows, cols = Mslab.shape
     if rows == 0 or cols == 0:
@@ -195,6 +250,12 @@ class ShardExchange:
     group: object = None
     colsq_fn: object = field(default=_kernel_colsq)
     rowsq_fn: object = field(default=_kernel_rowsq)
+    comm: object = None  # NcclComm: the exchanges as C-ABI calls on its communicator
+
+    def _gather(self, buf: torch.Tensor) -> torch.Tensor:
+        if self.comm is not None:
+            return self.comm.all_gather(buf)
+        return _all_gather(buf, self.group)
 
     def norms(self, M_local: torch.Tensor, N_local: torch.Tensor, colsq: torch.Tensor, rowsq: torch.Tensor) -> None:
         """Full-length colsq and rowsq (bit-identical to one device when the
@@ -215,7 +276,7 @@ class ShardExchange:
         for j in range(gr):
             if a == j:
                 self.colsq_fn(M_local[:, c0:c1], acc[:c1 - c0], j > 0)
-            g = _all_gather(buf if j == 0 else acc, self.group)
+            g = self._gather(buf if j == 0 else acc)
             if j == 0:
                 gathered0 = g
             if j + 1 < gr:  # the next row group continues the chains of the same column slab
@@ -230,7 +291,10 @@ class ShardExchange:
 
     def sum_(self, t: torch.Tensor) -> None:
         """In place: the rank-ordered sum of every rank's partial `t`."""
-        t.copy_(exchange_sum(t, self.group))
+        if self.comm is not None:
+            t.copy_(self.comm.exchange_sum(t))
+        else:
+            t.copy_(exchange_sum(t, self.group))
 
 
 def exchange_sum_list(parts: list):
@@ -249,15 +313,17 @@ class ShardedApproxProduct:
     for each member.  Buffers are allocated once (construction), the kernels
     are those of the single-GPU pipeline.
 
-    runs: [(method, c)] (SSM: c = number of whole-block draws); c0 for two-step."""
+    runs: [(method, c)] (SSM: c = number of whole-block draws); c0 for two-step.
+    comm: an NcclComm -- the exchanges then run as C-ABI NCCL calls on the
+    current stream instead of torch.distributed collectives."""
 
     def __init__(self, layout: ShardLayout, sizes, runs, *, dtype=torch.float32, c0: int = 0, cap: bool = True,
-                 group=None):
+                 group=None, comm: NcclComm | None = None):
         from .pipeline import PipelineGroup, SketchPipeline
         self.L, self.sizes, self.runs = layout, tuple(int(s) for s in sizes), [(str(mt), int(c)) for mt, c in runs]
         if sum(self.sizes) != layout.n:
             raise ValueError("partition does not cover n")
-        self.exchange = ShardExchange(layout, group)
+        self.exchange = ShardExchange(layout, group, comm=comm)
         r0, r1 = layout.rows
         b0, b1 = layout.cols
         self.ma, self.pb = r1 - r0, b1 - b0

@@ -99,3 +99,34 @@ def test_sharded_world_matches_single_gpu(world, dtype):
     for r in res:
         for j, pipe in enumerate([q for q in grp.pipes if q.method != "SSM"]):
             assert np.array_equal(r["budgets"][j], pipe.budgets_host()[0])
+
+
+def test_nccl_comm_exchanges_world1(monkeypatch):
+    """The C-ABI NCCL exchanges (bmm_nccl_comm_init, bmm_all_gather_f64_nccl,
+    bmm_exchange_sum_nccl) on a one-rank communicator -- this box has one GPU,
+    and NCCL refuses two ranks on one device -- and the sharded product run
+    through them (the collective runs even at world 1) against the single-GPU
+    PipelineGroup, bit for bit."""
+    from paper_2105_04940_b200 import _lib
+    from paper_2105_04940_b200.distributed import NcclComm, ShardLayout, ShardedApproxProduct
+    from paper_2105_04940_b200.pipeline import PipelineGroup, SketchPipeline
+    assert _lib.load().bmm_nccl_version() >= 22000
+    comm = NcclComm()
+    x = torch.randn(1000, dtype=torch.float64, device="cuda")
+    g = comm.all_gather(x)
+    assert g.shape == (1, 1000) and torch.equal(g[0], x)
+    assert torch.equal(comm.exchange_sum(x), x)
+    M, N, sizes = _instance(np.float32)
+    m, n, p = M.shape[0], M.shape[1], N.shape[1]
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    grp = PipelineGroup([SketchPipeline(m, n, p, sizes, 0, "SSM", draws=c, dtype=torch.float32) if meth == "SSM" else
+                         SketchPipeline(m, n, p, sizes, c, meth, c0=256, dtype=torch.float32) for meth, c in RUNS])
+    want = [o.cpu().numpy() for o in grp.run(Md, Nd, _seeds(len(sizes)))]
+    monkeypatch.setenv("BMM_EXCHANGE_WORLD1", "1")
+    sh = ShardedApproxProduct(ShardLayout(1, 0, m, n, p), sizes, RUNS, dtype=torch.float32, c0=256, comm=comm)
+    got = [t.cpu().numpy() for t in sh.run(Md, Nd, _seeds(len(sizes)))]
+    sh.check()
+    for i, (meth, _) in enumerate(RUNS):
+        assert np.array_equal(sh.pipes[i].columns_host(), grp.pipes[i].columns_host()), meth
+        assert np.array_equal(got[i], want[i]), meth
+    comm.close()
