@@ -814,6 +814,18 @@ class PipelineGroup:
         finally:
             self._active(False)
 
+    def _fork_gsq(self) -> bool:
+        """g_k^2 beside the norm pass on its own stream?  Small instances (config 2:
+        the two fill the GPU together) gain; at config 4 both are full-GPU kernels
+        and the interleaved CTAs cost more than they overlap (tools/timeline.py
+        cfg4: statistics done at 40.7 ms forked vs 38.8 ms in sequence).
+        BMM_GSQ_FORK=0|1 forces either."""
+        forced = os.environ.get("BMM_GSQ_FORK", "")
+        if forced in ("0", "1"):
+            return forced == "1"
+        sh = self.shared
+        return sh.B * sh.m * sh.n < (1 << 30)
+
     def _fork_stats(self, cap, M, N, chunks=None):
         """Enqueue the shared statistics on their own streams (forked from `cap`):
         the norm pass and block probabilities on one, OPL's g_k^2 (which needs only
@@ -823,7 +835,7 @@ class PipelineGroup:
         ss.wait_stream(cap)
         ev_p, ev_g = torch.cuda.Event(), torch.cuda.Event()
         gs = None
-        if chunks is None and self.shared.needs_gsq and os.environ.get("BMM_GSQ_FORK", "1") != "0":
+        if chunks is None and self.shared.needs_gsq and self._fork_gsq():
             gs = torch.cuda.Stream(priority=-1)
             gs.wait_stream(cap)
             with torch.cuda.stream(gs):
@@ -833,6 +845,8 @@ class PipelineGroup:
             ev_p.record(ss)
             if gs is not None:
                 ss.wait_stream(gs)
+            elif chunks is None and self.shared.needs_gsq:  # not forked: after the probabilities
+                self.shared.launch_gsq(M, N)
             ev_g.record(ss)
         return ev_p, ev_g, ss
 

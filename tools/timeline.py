@@ -1,8 +1,9 @@
-"""Where the config-2 sweep step spends its time inside ONE graph replay: every
+"""Where a PipelineGroup step spends its time inside ONE graph replay: every
 pipeline of the group records a device clock stamp (bmm_timestamp, %globaltimer)
 after each of its C-ABI calls, the group graph is captured with the stamps and
 replayed; prints per branch the end time of every stage relative to the step start.
-Usage: python tools/timeline.py [reps]"""
+Usage: python tools/timeline.py [reps] [cfg2|cfg4]   (cfg2: the nine-product sweep;
+cfg4: the default bench step -- shared stats + OPL, ONC, SSM at full size)"""
 import sys
 from pathlib import Path
 
@@ -15,12 +16,21 @@ from paper_2105_04940_b200 import _lib  # noqa: E402
 from paper_2105_04940_b200.pipeline import PipelineGroup, SketchPipeline, seeds_from_rngs  # noqa: E402
 
 torch.cuda.set_device(0)
-M, N, sizes = workloads.cfg2()
-Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
-runs = [(cb, W, m) for cb, W in zip((10, 20, 40), (4000, 8000, 16000)) for m in ("OPL", "ONC", "ONMCNR")]
-pipes = [SketchPipeline(500, 20000, 500, sizes, W, m, c0=500) for _, W, m in runs]
-group = PipelineGroup(pipes)
-seeds = lambda: [seeds_from_rngs(m, [workloads.sample_rng(2, cb)], len(sizes)) for cb, W, m in runs]  # noqa: E731
+WORKLOAD = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
+if WORKLOAD == "cfg4":
+    import bench  # noqa: E402
+    Md, Nd, sizes, _ = bench.device_data(torch, "cfg4")
+    group = bench.cfg4_group(torch, Md.shape[0], Md.shape[1], Nd.shape[1], sizes)
+    pipes = group.pipes
+    runs = [(rep, w, meth) for meth, w, rep in bench.CFG4_RUNS]
+    seeds = lambda: bench.cfg4_seeds(len(sizes))  # noqa: E731
+else:
+    M, N, sizes = workloads.cfg2()
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    runs = [(cb, W, m) for cb, W in zip((10, 20, 40), (4000, 8000, 16000)) for m in ("OPL", "ONC", "ONMCNR")]
+    pipes = [SketchPipeline(500, 20000, 500, sizes, W, m, c0=500) for _, W, m in runs]
+    group = PipelineGroup(pipes)
+    seeds = lambda: [seeds_from_rngs(m, [workloads.sample_rng(2, cb)], len(sizes)) for cb, W, m in runs]  # noqa: E731
 group.run(Md, Nd, seeds())
 start = torch.zeros(1, dtype=torch.int64, device="cuda")
 end = torch.zeros(1, dtype=torch.int64, device="cuda")
