@@ -69,12 +69,14 @@ def test_pipeline_group_concurrent_replay_is_bit_identical(shared):
             group.pipes[1].run(Md, Nd, seeds(3)[1])
 
 
-@pytest.mark.parametrize("serial", ["0", "1"])
+@pytest.mark.parametrize("serial,fork", [("0", "1"), ("1", "1"), ("0", "0")])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-def test_shared_stats_group_with_ssm_matches_oracle(dtype, serial, monkeypatch):
+def test_shared_stats_group_with_ssm_matches_oracle(dtype, serial, fork, monkeypatch):
     """OPL, ONC and SSM over one instance with one shared statistics stage (the
     config-4 step): budgets, draws and scales bit-exact to the oracle, products
-    within the dtype's bar, eager and replayed."""
+    within the dtype's bar, eager and replayed -- with g_k^2 forked beside the
+    norm pass or after it (BMM_GSQ_FORK), and after the instance changes in
+    place between replays (every statistic recomputed, none stale)."""
     g = np.random.default_rng(44)
     sizes = (64,) * 40
     n = sum(sizes)
@@ -84,6 +86,7 @@ def test_shared_stats_group_with_ssm_matches_oracle(dtype, serial, monkeypatch):
     Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
     W, draws = 640, 10
     monkeypatch.setenv("BMM_GROUP_SERIAL", serial)  # members as concurrent branches, or one after another
+    monkeypatch.setenv("BMM_GSQ_FORK", fork)
     group = PipelineGroup([SketchPipeline(96, n, 80, sizes, W, "OPL", dtype=tdt),
                            SketchPipeline(96, n, 80, sizes, W, "ONC", dtype=tdt),
                            SketchPipeline(96, n, 80, sizes, 0, "SSM", draws=draws, dtype=tdt)])
@@ -93,6 +96,11 @@ def test_shared_stats_group_with_ssm_matches_oracle(dtype, serial, monkeypatch):
     for rep, s in enumerate((5, 6, 7)):
         if rep == 1:
             group.capture(Md, Nd)
+        if rep == 2:  # new data in the captured buffers: block 0 and 7 of M rescaled
+            for k, f in ((0, 3.0), (7, 0.25)):
+                M[:, 64 * k:64 * (k + 1)] = (M[:, 64 * k:64 * (k + 1)] * f).astype(dtype)
+            Md.copy_(torch.as_tensor(M, device="cuda"))
+            M64 = M.astype(np.float64)
         rngs = [np.random.default_rng(s + i) for i in range(3)]
         sd = [seeds_from_rngs("OPL", [rngs[0]], 40), seeds_from_rngs("ONC", [rngs[1]], 40),
               seeds_from_rngs("SSM", [rngs[2]], 40, draws=draws)]
