@@ -375,6 +375,18 @@ int bmm_segsq_gram(int dtype, const void* A, int64_t lda, int64_t strideA,
                    const void* B, int64_t ldb, int64_t strideB,
                    int64_t m, int64_t nc, const int64_t* seg, int64_t nseg, int64_t seg_stride,
                    int64_t batch, double* gsq, void* stream);
+/* The same, with the norm pass fused in (round 2): the segments must tile the
+ * inner dimension (seg[0] = 0, seg[nseg] = n), and the kernel that reads each
+ * segment's columns of A and rows of B once also writes colsq[b*n_stride + i]
+ * (column_norms^2, NumPy's sequential order over the m rows, matrix.py:107-109)
+ * and rowsq[b*n_stride + i] (row_norms^2, NumPy's pairwise tree over the nc
+ * columns, matrix.py:112-114) -- bit-identical to bmm_norms.  nc must be
+ * 128 * 2^k (the tree is then perfect: 128-element leaves paired in order).  */
+int bmm_segsq_gram_norms(int dtype, const void* A, int64_t lda, int64_t strideA,
+                         const void* B, int64_t ldb, int64_t strideB,
+                         int64_t m, int64_t nc, const int64_t* seg, int64_t nseg, int64_t seg_stride,
+                         int64_t batch, double* gsq, double* colsq, double* rowsq, int64_t n_stride,
+                         void* stream);
 
 /* ---------------------------------------------------------------- exact variance analytics
  * (analysis.py:57-116)

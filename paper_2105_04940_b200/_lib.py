@@ -89,6 +89,8 @@ SIGNATURES = {
     "bmm_segsq_gram_max_len": (_I64, []),
     "bmm_expand_blocks": (_I, [_P, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _I64, _P]),
     "bmm_segsq_gram": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P, _P]),
+    "bmm_segsq_gram_norms": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P, _P, _P,
+                                  _I64, _P]),
     "bmm_variance_workspace": (_I64, [_I64, _I64, _I64, _I64]),
     "bmm_elementwise_variance": (_I, [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _P, _P, _P, _I64,
                                       _P, _P, _I64, _P]),

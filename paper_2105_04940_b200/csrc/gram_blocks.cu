@@ -25,6 +25,8 @@
 // shuffle tree.  Parity with the reference is to rounding (~1e-15 relative,
 // as for the DMMA / int8 segmented GEMMs it replaces); g^2 is clamped at 0 (the
 // reference's norm is >= 0 by construction).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace bmm {
@@ -132,12 +134,65 @@ __device__ __forceinline__ void load_stage(T* stage, const T* __restrict__ base,
   }
 }
 
+// acc + x*x with NumPy's rounding (as norms.cu add_sq: one rounding for float32
+// data, where the square is exact; the square then the sum for float64)
+template <typename T>
+__device__ __forceinline__ double gb_add_sq(double acc, double x) {
+  if constexpr (sizeof(T) == 4) return __fma_rn(x, x, acc);
+  else return __dadd_rn(acc, __dmul_rn(x, x));
+}
+
+// The norm pass fused into the Gram's stream (NORMS): the CTA already reads its
+// block's m x L columns of M and L x p rows of N once, in order, so thread a < L
+// also runs
+//   M side: column a's sequential chain over the rows (NumPy's column_norms,
+//           matrix.py:107-109), 32 rows per stage;
+//   N side: row a's pairwise tree (matrix.py:112-114) for p = 128 * 2^k: NumPy's
+//           leaves are the 128-element runs (8 interleaved accumulators, then
+//           ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))), 4 stages each, and the leaves
+//           pair in order (a binary counter of pending subtrees).
+// Same operations in the same order as norms.cu: bit-identical colsq / rowsq.
+constexpr int TREE_LEVELS = 24;
+
+template <typename T>
+struct RowTree {
+  double r[8];
+  double pend[TREE_LEVELS];
+  int64_t leaves = 0;
+  __device__ __forceinline__ void stage(const T* row, int x0) {  // 32 elements of the row, x0 = stage start
+    if ((x0 & 127) == 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = 0.0;
+    }
+#pragma unroll
+    for (int x = 0; x < KX; ++x) r[x & 7] = gb_add_sq<T>(r[x & 7], (double)row[x]);
+    if ((x0 & 127) == 96) {  // the leaf is complete
+      double v = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      int l = 0;
+      for (; (leaves >> l) & 1; ++l) v = __dadd_rn(pend[l], v);  // left sibling + right
+      pend[l] = v;
+      ++leaves;
+    }
+  }
+  __device__ __forceinline__ double root() const {  // leaves = 2^k: one pending subtree
+    int l = 0;
+    while (!((leaves >> l) & 1)) ++l;
+    return pend[l];
+  }
+};
+
 // One side's Gram (36 upper tiles) over `len` contraction positions, summed
 // over the CTA's warps in a fixed order; the result is left in warp 0's acc.
-template <typename T, bool MSIDE>
+// NORMS: also the side's squared norms of the block (see RowTree) into nrm[0..Lj).
+template <typename T, bool MSIDE, bool NORMS = false>
 __device__ __forceinline__ void gram_side(double (&acc)[NTILE][2], T* ring, double* red, const T* __restrict__ base,
-                                          int64_t ld, int64_t col0, int Lj, int64_t len, bool vec) {
+                                          int64_t ld, int64_t col0, int Lj, int64_t len, bool vec,
+                                          double* __restrict__ nrm = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double chain = 0.0;     // M side: column threadIdx.x's sequential sum
+  RowTree<T> tree;        // N side: row threadIdx.x's pairwise tree
+  const bool owner = NORMS && (int)threadIdx.x < Lj;
 #pragma unroll
   for (int q = 0; q < NTILE; ++q) acc[q][0] = acc[q][1] = 0.0;
   const int64_t nst = (len + KX - 1) / KX;
@@ -156,6 +211,14 @@ __device__ __forceinline__ void gram_side(double (&acc)[NTILE][2], T* ring, doub
       commit();
     }
     const T* stg = ring + (i % STAGES) * SE;
+    if (owner) {
+      if (MSIDE) {
+#pragma unroll
+        for (int x = 0; x < KX; ++x) chain = gb_add_sq<T>(chain, (double)stg[x * SM + threadIdx.x]);
+      } else {
+        tree.stage(stg + threadIdx.x * SN, (int)(i * KX));
+      }
+    }
 #pragma unroll
     for (int kk = 0; kk < KX / 4 / WARPS; ++kk) {
       const int s = warp + kk * WARPS;  // k-step within the stage
@@ -172,6 +235,7 @@ __device__ __forceinline__ void gram_side(double (&acc)[NTILE][2], T* ring, doub
         for (int u = t; u < NT; ++u, ++q) dmma(acc[q], f[t], f[u]);
     }
   }
+  if (owner) nrm[threadIdx.x] = MSIDE ? chain : tree.root();
   wait_group<0>();
   __syncthreads();  // the ring is free: reuse it (red) for the cross-warp sum
   // fixed order: (w0 + w2) + (w1 + w3)
@@ -211,11 +275,12 @@ __device__ __forceinline__ void gram_side(double (&acc)[NTILE][2], T* ring, doub
   __syncthreads();
 }
 
-template <typename T>
+template <typename T, int SIDES>
 __global__ void __launch_bounds__(THREADS, 2)
     block_gram_kernel(const T* __restrict__ M, int64_t ldm, int64_t strideM, const T* __restrict__ N, int64_t ldn,
                       int64_t strideN, int64_t m, int64_t p, const int64_t* __restrict__ seg, int64_t nseg,
-                      int64_t seg_stride, double* __restrict__ gsq) {
+                      int64_t seg_stride, double* __restrict__ gsq, double* __restrict__ colsq,
+                      double* __restrict__ rowsq, int64_t n_stride) {
   extern __shared__ __align__(128) unsigned char smem[];
   T* ring = reinterpret_cast<T*>(smem);
   double* red = reinterpret_cast<double*>(smem);
@@ -235,7 +300,8 @@ __global__ void __launch_bounds__(THREADS, 2)
   const bool vecM = ((reinterpret_cast<uintptr_t>(Mb) & 15) == 0) && (ldm % VE == 0) && (o % VE == 0);
   const bool vecN = ((reinterpret_cast<uintptr_t>(Nb) & 15) == 0) && (ldn % VE == 0);
   double acc[NTILE][2];
-  gram_side<T, true>(acc, ring, red, Mb, ldm, o, Lj, m, vecM);
+  gram_side<T, true, (SIDES & 1) != 0>(acc, ring, red, Mb, ldm, o, Lj, m, vecM,
+                                       (SIDES & 1) ? colsq + b * n_stride + o : nullptr);
   if (warp == 0) {
 #pragma unroll
     for (int q = 0; q < NTILE; ++q) {
@@ -244,7 +310,8 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
   }
   // (gram_side begins with cp.async into the ring only; gm is a separate region)
-  gram_side<T, false>(acc, ring, red, Nb, ldn, o, Lj, p, vecN);
+  gram_side<T, false, (SIDES & 2) != 0>(acc, ring, red, Nb, ldn, o, Lj, p, vecN,
+                                        (SIDES & 2) ? rowsq + b * n_stride + o : nullptr);
   if (warp == 0) {
     double t = 0.0;
     int q = 0;
@@ -268,19 +335,20 @@ __global__ void __launch_bounds__(THREADS, 2)
 
 using namespace bmm;
 
-template <typename T>
+template <typename T, int SIDES>
 static int block_gram_launch(const void* M, int64_t ldm, int64_t strideM, const void* N, int64_t ldn,
                              int64_t strideN, int64_t m, int64_t nc, const int64_t* seg, int64_t nseg,
-                             int64_t seg_stride, int64_t batch, double* gsq, cudaStream_t st) {
+                             int64_t seg_stride, int64_t batch, double* gsq, double* colsq, double* rowsq,
+                             int64_t n_stride, cudaStream_t st) {
   constexpr int smem = gb::smem_bytes<T>();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gb::block_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(gb::block_gram_kernel<T, SIDES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   dim3 grid((unsigned)nseg, (unsigned)batch);
-  gb::block_gram_kernel<T><<<grid, gb::THREADS, smem, st>>>((const T*)M, ldm, strideM, (const T*)N, ldn, strideN, m,
-                                                             nc, seg, nseg, seg_stride, gsq);
+  gb::block_gram_kernel<T, SIDES><<<grid, gb::THREADS, smem, st>>>(
+      (const T*)M, ldm, strideM, (const T*)N, ldn, strideN, m, nc, seg, nseg, seg_stride, gsq, colsq, rowsq, n_stride);
   BMM_CHECK_LAUNCH("block_gram_kernel");
   return BMM_OK;
 }
@@ -296,9 +364,43 @@ extern "C" int bmm_segsq_gram(int dtype, const void* M, int64_t ldm, int64_t str
   BMM_REQUIRE(nseg < (1LL << 31) && batch <= 65535, BMM_E_UNSUPPORTED, "bmm_segsq_gram: grid too large");
   cudaStream_t st = as_stream(stream);
   if (dtype == BMM_F64)
-    return block_gram_launch<double>(M, ldm, strideM, N, ldn, strideN, m, nc, seg, nseg, seg_stride, batch, gsq, st);
+    return block_gram_launch<double, 0>(M, ldm, strideM, N, ldn, strideN, m, nc, seg, nseg, seg_stride, batch,
+                                            gsq, nullptr, nullptr, 0, st);
   if (dtype == BMM_F32)
-    return block_gram_launch<float>(M, ldm, strideM, N, ldn, strideN, m, nc, seg, nseg, seg_stride, batch, gsq, st);
+    return block_gram_launch<float, 0>(M, ldm, strideM, N, ldn, strideN, m, nc, seg, nseg, seg_stride, batch,
+                                           gsq, nullptr, nullptr, 0, st);
   set_error("bmm_segsq_gram: unknown dtype %d", dtype);
+  return BMM_E_ARG;
+}
+
+extern "C" int bmm_segsq_gram_norms(int dtype, const void* M, int64_t ldm, int64_t strideM, const void* N,
+                                    int64_t ldn, int64_t strideN, int64_t m, int64_t nc, const int64_t* seg,
+                                    int64_t nseg, int64_t seg_stride, int64_t batch, double* gsq, double* colsq,
+                                    double* rowsq, int64_t n_stride, void* stream) {
+  BMM_REQUIRE(m >= 1 && nc >= 1 && nseg >= 1 && batch >= 1, BMM_E_ARG, "bmm_segsq_gram_norms: bad shape");
+  BMM_REQUIRE(M != nullptr && N != nullptr && seg != nullptr && gsq != nullptr && colsq != nullptr &&
+                  rowsq != nullptr, BMM_E_ARG, "bmm_segsq_gram_norms: null pointer");
+  BMM_REQUIRE(nseg < (1LL << 31) && batch <= 65535, BMM_E_UNSUPPORTED, "bmm_segsq_gram_norms: grid too large");
+  BMM_REQUIRE(nc >= 128 && (nc & (nc - 1)) == 0, BMM_E_UNSUPPORTED,
+              "bmm_segsq_gram_norms: p must be 128 * 2^k (NumPy's row tree is then perfect)");
+  cudaStream_t st = as_stream(stream);
+  // A/B (tools/gram_norms_probe.py): BMM_GRAM_NORMS_SIDES=1 fuses only colsq (rowsq untouched)
+  static const int sides = [] {
+    const char* e = getenv("BMM_GRAM_NORMS_SIDES");
+    return e ? atoi(e) : 3;
+  }();
+#define BMM_GN(TT, S) \
+  return block_gram_launch<TT, S>(M, ldm, strideM, N, ldn, strideN, m, nc, seg, nseg, seg_stride, batch, gsq, colsq, \
+                                  rowsq, n_stride, st)
+  if (dtype == BMM_F64) {
+    if (sides == 1) BMM_GN(double, 1);
+    BMM_GN(double, 3);
+  }
+  if (dtype == BMM_F32) {
+    if (sides == 1) BMM_GN(float, 1);
+    BMM_GN(float, 3);
+  }
+#undef BMM_GN
+  set_error("bmm_segsq_gram_norms: unknown dtype %d", dtype);
   return BMM_E_ARG;
 }

@@ -98,6 +98,20 @@ def seeds_from_keys(method: str, entropy: int, key_prefix: tuple, keys, K: int) 
     return CallSeeds(main=StreamSeeds(np.ascontiguousarray(words), zeros))
 
 
+def _fused_stats(obj, M: torch.Tensor) -> bool:
+    """Norm pass inside OPL's Gram-form g_k^2 kernel (bmm_segsq_gram_norms)?  Needs
+    the Gram engine, p = 128 * 2^k (NumPy's row tree is perfect), one device (no
+    exchange).  Opt-in (BMM_FUSED_STATS=1): bit-identical, but the norm chains sit
+    on the DMMA warps' critical path -- config 4, cool GPU: 24.3 ms fused against
+    5.3 + 18.8 ms separate; inside the power-capped step 46.5 against 38.8 ms
+    (tools/gram_norms_probe.py, tools/timeline.py cfg4)."""
+    if os.environ.get("BMM_FUSED_STATS", "0") != "1" or getattr(obj, "exchange", None) is not None:
+        return False
+    p = obj.p
+    return (getattr(obj, "seg_engine", None) == "gram" and p >= 128 and (p & (p - 1)) == 0
+            and M.dtype in (torch.float32, torch.float64))
+
+
 def _stats_launch(obj, M: torch.Tensor, N: torch.Tensor, chunks, *, probs: bool, gsq: bool) -> bool:
     """Per-instance statistics of `obj` (a SketchPipeline or a group's SharedStats):
     the norm pass (K1), optionally the optimal probabilities / score sums / main
@@ -110,7 +124,13 @@ def _stats_launch(obj, M: torch.Tensor, N: torch.Tensor, chunks, *, probs: bool,
     ldm, ldn = M.stride(-2), N.stride(-2)
     P = lambda t: t.data_ptr()  # noqa: E731
     seg_done = False
-    if getattr(obj, "exchange", None) is not None:
+    if gsq and chunks is None and _fused_stats(obj, M):
+        # OPL's Gram kernel reads every column of M and row of N once anyway: the norm
+        # pass rides along (bit-identical colsq / rowsq, gram_blocks.cu RowTree)
+        obj._c("bmm_segsq_gram_norms", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(obj.offsets), K, 0, B, P(obj.gsq),
+               P(obj.colsq), P(obj.rowsq), n, st)
+        seg_done = True
+    elif getattr(obj, "exchange", None) is not None:
         # one rank of a sharded product: exact cross-rank norm pass (distributed.ShardExchange)
         if B != 1 or chunks is not None:
             raise ValueError("sharded pipelines run one problem, without chunked transfer")
@@ -672,6 +692,7 @@ class SharedStats:
         self.needs_gsq = bool(opl)
         src = next((q for q in pipes if q.method not in ("SSM", "UU")), p0)
         self.probs, self.s, self.cum, self.last = src.probs, src.s, src.cum, src.last
+        self.seg_engine = None
         if opl:
             self.gsq, self.seg_engine, self.ws_seg = opl[0].gsq, opl[0].seg_engine, opl[0].ws_seg
         for q in pipes:
@@ -683,8 +704,13 @@ class SharedStats:
             q.shared = self
 
     def launch_probs(self, M: torch.Tensor, N: torch.Tensor, chunks=None) -> bool:
-        """Norm pass (+ g_k^2 per chunk when chunked) and the block probabilities."""
+        """Norm pass (+ g_k^2 per chunk when chunked, or with the norms fused into
+        the Gram kernel) and the block probabilities.  True when g_k^2 is done."""
         return _stats_launch(self, M, N, chunks, probs=self.needs_probs, gsq=self.needs_gsq)
+
+    def fused(self, M: torch.Tensor) -> bool:
+        """g_k^2 and the norm pass in one kernel (launch_probs does both)."""
+        return self.needs_gsq and _fused_stats(self, M)
 
     def launch_gsq(self, M: torch.Tensor, N: torch.Tensor) -> None:
         if self.needs_gsq:
@@ -805,8 +831,8 @@ class PipelineGroup:
         self._active(True)
         try:
             if self.shared is not None:
-                self.shared.launch_probs(M, N)
-                self.shared.launch_gsq(M, N)
+                if not self.shared.launch_probs(M, N):
+                    self.shared.launch_gsq(M, N)
             for pipe in self.pipes:
                 pipe.launch(M, N)
             if self.joint:
@@ -835,7 +861,8 @@ class PipelineGroup:
         ss.wait_stream(cap)
         ev_p, ev_g = torch.cuda.Event(), torch.cuda.Event()
         gs = None
-        if chunks is None and self.shared.needs_gsq and self._fork_gsq():
+        fused = chunks is None and self.shared.fused(M)
+        if chunks is None and self.shared.needs_gsq and not fused and self._fork_gsq():
             gs = torch.cuda.Stream(priority=-1)
             gs.wait_stream(cap)
             with torch.cuda.stream(gs):
@@ -845,7 +872,7 @@ class PipelineGroup:
             ev_p.record(ss)
             if gs is not None:
                 ss.wait_stream(gs)
-            elif chunks is None and self.shared.needs_gsq:  # not forked: after the probabilities
+            elif chunks is None and self.shared.needs_gsq and not fused:  # not forked: after the probabilities
                 self.shared.launch_gsq(M, N)
             ev_g.record(ss)
         return ev_p, ev_g, ss

@@ -161,3 +161,69 @@ def test_ssm_pipeline_batched(dtype, graph):
         assert rel(CD[b], ref["CD"]) < tol
         # the caller's generator is left where the reference leaves it
         assert rngs[b].random() == ref_rng.random()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("m,p,sizes,batch", [(300, 128, (64,) * 10, 1), (129, 1024, (1, 63, 64, 17, 40), 1),
+                                             (64, 16384, (64,) * 3, 1), (100, 256, (32,) * 8, 3)])
+def test_gram_norms_fused_bit_exact(dtype, m, p, sizes, batch):
+    """bmm_segsq_gram_norms: g_k^2 as bmm_segsq_gram, and the norm pass riding in
+    the same read of M and N -- colsq (sequential over the rows) and rowsq
+    (NumPy's pairwise tree, p = 128 * 2^k) bit-identical to the oracle's NumPy
+    order; ragged segments, rows not a multiple of the 32-row stage, batches."""
+    g = np.random.default_rng(m + p + len(sizes))
+    n = sum(sizes)
+    M = (g.standard_normal((batch, m, n)) * g.lognormal(0, 2, (batch, 1, n))).astype(dtype)
+    N = (g.standard_normal((batch, n, p)) * g.lognormal(0, 2, (batch, n, 1))).astype(dtype)
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    K = len(sizes)
+    off = torch.as_tensor(O.offsets_of(sizes), device="cuda")
+    gsq = torch.full((batch * K,), -1.0, dtype=torch.float64, device="cuda")
+    cs = torch.full((batch * n,), -1.0, dtype=torch.float64, device="cuda")
+    rs = torch.full((batch * n,), -1.0, dtype=torch.float64, device="cuda")
+    _lib.call("bmm_segsq_gram_norms", _lib.matrix_dtype(Md), Md.data_ptr(), n, m * n, Nd.data_ptr(), p, n * p, m, p,
+              off.data_ptr(), K, 0, batch, gsq.data_ptr(), cs.data_ptr(), rs.data_ptr(), n, _lib.stream_ptr())
+    ref = gram(M if batch > 1 else M[0], N if batch > 1 else N[0], sizes, batch)
+    assert np.array_equal(gsq.view(batch, K).cpu().numpy(), ref)  # the Gram part: the unfused kernel's bits
+    for b in range(batch):
+        M64, N64 = M[b].astype(np.float64), N[b].astype(np.float64)
+        assert np.array_equal(cs[b * n:(b + 1) * n].cpu().numpy(), O.colsq(M64)), b
+        assert np.array_equal(rs[b * n:(b + 1) * n].cpu().numpy(), O.rowsq(N64)), b
+    with pytest.raises(RuntimeError, match="128"):
+        _lib.call("bmm_segsq_gram_norms", _lib.matrix_dtype(Md), Md.data_ptr(), n, m * n, Nd.data_ptr(), p, n * p,
+                  m, p - 1, off.data_ptr(), K, 0, batch, gsq.data_ptr(), cs.data_ptr(), rs.data_ptr(), n,
+                  _lib.stream_ptr())
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_opl_group_with_fused_stats(fused, monkeypatch):
+    """The config-4 step's shared statistics with the norm pass fused into the
+    Gram kernel (opt-in, BMM_FUSED_STATS=1) or separate: identical budgets,
+    draws and products."""
+    from paper_2105_04940_b200.pipeline import PipelineGroup
+    monkeypatch.setenv("BMM_FUSED_STATS", fused)
+    g = np.random.default_rng(5)
+    sizes = (64,) * 32
+    n = sum(sizes)
+    M = (g.standard_normal((200, n)) * np.repeat(g.uniform(0.1, 10, 32), 64)).astype(np.float32)
+    N = (g.standard_normal((n, 256)) * np.repeat(g.uniform(0.1, 10, 32), 64)[:, None]).astype(np.float32)
+    Md, Nd = torch.as_tensor(M, device="cuda"), torch.as_tensor(N, device="cuda")
+    group = PipelineGroup([SketchPipeline(200, n, 256, sizes, 512, "OPL", dtype=torch.float32),
+                           SketchPipeline(200, n, 256, sizes, 512, "ONC", dtype=torch.float32)])
+    assert group.shared.fused(Md) == (fused == "1")
+    group.run(Md, Nd, [seeds_from_rngs("OPL", [np.random.default_rng(1)], 32),
+                       seeds_from_rngs("ONC", [np.random.default_rng(2)], 32)])
+    group.capture(Md, Nd)
+    for s in (3, 4):
+        sd = [seeds_from_rngs("OPL", [np.random.default_rng(s)], 32),
+              seeds_from_rngs("ONC", [np.random.default_rng(s + 9)], 32)]
+        outs = [o.cpu().numpy() for o in group.run(Md, Nd, sd)]
+        group.check()
+        M64, N64 = M.astype(np.float64), N.astype(np.float64)
+        assert np.array_equal(group.shared.colsq.cpu().numpy(), O.colsq(M64))
+        assert np.array_equal(group.shared.rowsq.cpu().numpy(), O.rowsq(N64))
+        for i, meth in enumerate(("OPL", "ONC")):
+            ref = O.approx_product(M64, N64, sizes, 512, meth, np.random.default_rng(s + 9 * i))
+            assert np.array_equal(group.pipes[i].budgets_host()[0], ref["budgets"]), meth
+            assert np.array_equal(group.pipes[i].columns_host()[0], ref["columns"]), meth
+            assert rel(outs[i], ref["CD"]) < 1e-5, meth
