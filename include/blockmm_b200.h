@@ -551,6 +551,19 @@ int bmm_gen_instance(int heavy, int dtype, int64_t m, int64_t n, int64_t p,
                      double scale_left, double rho_left, double scale_right, double rho_right,
                      double location, void* M, int64_t ldm, void* N, int64_t ldn, void* stream);
 
+/* The same instances from the REFERENCE's own variates (datagen.py:70-71, 104-106):
+ * Z (dim x count, row-major float64, device) holds rng.standard_normal((dim, count)) as the
+ * reference draws it -- numpy's ziggurat/gamma variates are third-party libm-dependent
+ * arithmetic, so the caller's Generator produces them and the generator state advances
+ * exactly as in the reference -- and this entry replaces the Cholesky product L @ Z by the
+ * AR(1) recursion: out[i, j] (transpose_out = 0: M, dim = m, count = n) or out[j, i]
+ * (transpose_out = 1: N = ascontiguousarray((L @ Z).T), dim = p, count = n).  w_opt (count
+ * chi-square(1) draws, device) selects the heavy-tailed form location + x / sqrt(w[j]) in the
+ * reference's operation order.  dtype of out: BMM_F64 or BMM_F32 (rounded once).           */
+int bmm_ar1_transform(int dtype, const double* Z, int64_t dim, int64_t count, int64_t ldz,
+                      int transpose_out, double scale, double rho, const double* w_opt,
+                      double location, void* out, int64_t ldo, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

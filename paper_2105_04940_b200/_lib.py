@@ -98,6 +98,8 @@ SIGNATURES = {
     "bmm_gen_instance": (_I, [_I, _I, _I64, _I64, _I64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double,
                               ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, _P, _I64, _P,
                               _I64, _P]),
+    "bmm_ar1_transform": (_I, [_I, _P, _I64, _I64, _I64, _I, ctypes.c_double, ctypes.c_double, _P, ctypes.c_double,
+                               _P, _I64, _P]),
     "bmm_sqdiff_workspace": (_I64, [_I64, _I64, _I64]),
     "bmm_sqdiff": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P]),
     "bmm_pairwise_sum": (_I, [_P, _I64, _I64, _I64, _P, _P]),

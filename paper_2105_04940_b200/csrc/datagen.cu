@@ -139,6 +139,73 @@ static int gen_impl(int heavy, int64_t m, int64_t n, int64_t p, uint64_t seed_hi
   return BMM_OK;
 }
 
+
+// ---- the reference's own variates (datagen.py:70-71, 104-106) -------------------------------
+// Z (dim x count, row-major float64) holds rng.standard_normal((dim, count)) exactly as the
+// reference draws it; vector j is column j of Z.  out = L @ Z by the AR(1) recursion (no
+// transpose: out[i, j], M's layout) or its transpose (out[j, i], N's layout: the reference's
+// ascontiguousarray((L @ Z).T)).  w != NULL: the heavy-tailed form loc + x / sqrt(w[j]) with
+// the reference's operation order (a division by the square root, then the location).
+template <typename T>
+__global__ void __launch_bounds__(256) ar1_cols_kernel(const double* __restrict__ Z, int64_t dim, int64_t count,
+                                                       int64_t ldz, double sqrt_s, double rho, double innov,
+                                                       const double* __restrict__ w, double loc,
+                                                       T* __restrict__ out, int64_t ldo) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < count;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double sw = w ? sqrt(w[j]) : 1.0;
+    double x = 0.0;
+    for (int64_t i = 0; i < dim; ++i) {
+      const double z = Z[i * ldz + j];
+      x = (i == 0) ? sqrt_s * z : fma(rho, x, innov * z);
+      put(out + i * ldo + j, w ? loc + x / sw : x);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) ar1_rows_kernel(const double* __restrict__ Z, int64_t dim, int64_t count,
+                                                       int64_t ldz, double sqrt_s, double rho, double innov,
+                                                       const double* __restrict__ w, double loc,
+                                                       T* __restrict__ out, int64_t ldo) {
+  __shared__ double tile[4][32][33];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  for (int64_t row0 = ((int64_t)blockIdx.x * 4 + wp) * 32; row0 < count; row0 += (int64_t)gridDim.x * 4 * 32) {
+    const int64_t j = row0 + lane;
+    const bool live = j < count;
+    const double sw = (w && live) ? sqrt(w[j]) : 1.0;
+    double x = 0.0;
+    for (int64_t f0 = 0; f0 < dim; f0 += 32) {
+      const int cnt = (int)min((int64_t)32, dim - f0);
+      for (int f = 0; f < cnt; ++f) {
+        const double z = live ? Z[(f0 + f) * ldz + j] : 0.0;
+        x = (f0 + f == 0) ? sqrt_s * z : fma(rho, x, innov * z);
+        tile[wp][lane][f] = w ? loc + x / sw : x;
+      }
+      __syncwarp();
+      for (int r = 0; r < 32 && row0 + r < count; ++r)
+        if (lane < cnt) put(out + (row0 + r) * ldo + f0 + lane, tile[wp][r][lane]);
+      __syncwarp();
+    }
+  }
+}
+
+template <typename T>
+static int ar1_impl(const double* Z, int64_t dim, int64_t count, int64_t ldz, int transpose_out, double scale,
+                    double rho, const double* w, double loc, T* out, int64_t ldo, cudaStream_t st) {
+  const double sqrt_s = sqrt(scale), innov = sqrt(scale * (1.0 - rho * rho));
+  if (!transpose_out) {
+    ar1_cols_kernel<T><<<grid_for(count, 256, 8, 4), 256, 0, st>>>(Z, dim, count, ldz, sqrt_s, rho, innov, w, loc,
+                                                                  out, ldo);
+    BMM_CHECK_LAUNCH("ar1_cols_kernel");
+  } else {
+    ar1_rows_kernel<T><<<grid_for(ceil_div(count, 32) * 32, 128, 8, 4), 128, 0, st>>>(Z, dim, count, ldz, sqrt_s,
+                                                                                      rho, innov, w, loc, out, ldo);
+    BMM_CHECK_LAUNCH("ar1_rows_kernel");
+  }
+  return BMM_OK;
+}
+
 }  // namespace bmm
 
 using namespace bmm;
@@ -158,5 +225,20 @@ extern "C" int bmm_gen_instance(int heavy, int dtype, int64_t m, int64_t n, int6
     return gen_impl<float>(heavy, m, n, p, seed_hi, seed_lo, scale_left, rho_left, scale_right, rho_right, location,
                            (float*)M, ldm, (float*)N, ldn, st);
   set_error("bmm_gen_instance: unknown dtype %d", dtype);
+  return BMM_E_ARG;
+}
+
+extern "C" int bmm_ar1_transform(int dtype, const double* Z, int64_t dim, int64_t count, int64_t ldz,
+                                 int transpose_out, double scale, double rho, const double* w_opt, double location,
+                                 void* out, int64_t ldo, void* stream) {
+  BMM_REQUIRE(dim >= 1 && count >= 1 && ldz >= count, BMM_E_ARG, "bmm_ar1_transform: bad dimensions");
+  BMM_REQUIRE(ldo >= (transpose_out ? dim : count), BMM_E_ARG, "bmm_ar1_transform: bad output stride");
+  BMM_REQUIRE(scale > 0 && rho > -1 && rho < 1, BMM_E_ARG, "bmm_ar1_transform: bad covariance parameters");
+  cudaStream_t st = as_stream(stream);
+  if (dtype == BMM_F64)
+    return ar1_impl<double>(Z, dim, count, ldz, transpose_out, scale, rho, w_opt, location, (double*)out, ldo, st);
+  if (dtype == BMM_F32)
+    return ar1_impl<float>(Z, dim, count, ldz, transpose_out, scale, rho, w_opt, location, (float*)out, ldo, st);
+  set_error("bmm_ar1_transform: unknown dtype %d", dtype);
   return BMM_E_ARG;
 }

@@ -9,11 +9,24 @@ and multiplies by a Cholesky factor; here ``bmm_gen_instance`` generates every
 vector in HBM by the equivalent AR(1) recursion (csrc/datagen.cu), so an
 instance costs one write of M and N and no host->device copy.
 
-Deliberate difference: the random streams are this library's (PCG64 per
-vector + Box-Muller), seeded from four 32-bit words drawn from ``rng``; the
-instance is a deterministic function of (dims, rng state) like the
-reference's, distribution-identical but not bit-identical to numpy's ziggurat
-draws, and ``rng`` advances by those draws only.
+Two stream modes:
+
+* ``stream="numpy"`` (default, the drop-in): the variates are the reference's
+  own -- ``rng.standard_normal`` / ``rng.chisquare`` called on the caller's
+  Generator in the reference's order and shapes (datagen.py:70-71, 104-106), so
+  the instance is the same pure function of (dims, rng state) and ``rng`` is
+  left in exactly the reference's state.  numpy's ziggurat and gamma samplers
+  are third-party arithmetic whose values depend on the host libm (log1p, pow),
+  so they are not restated on the device; the variates are uploaded and
+  ``bmm_ar1_transform`` replaces the Cholesky products ``L @ Z`` -- the only
+  O(dim^2) work, 8 s of the reference's time at 1000 x 100000 -- by the
+  recursion.  Entries agree with the reference's to BLAS rounding (1e-13 of the
+  vector's norm; tests/golden/datagen.npz), the heavy-tailed division and
+  location are applied in the reference's operation order.
+* ``stream="device"``: this library's streams (PCG64 per vector + Box-Muller,
+  seeded from four 32-bit words drawn from ``rng``), generated in HBM with no
+  host traffic: distribution-identical, deterministic per seed, not the
+  reference's values; ``rng`` advances by those four draws only.
 """
 from __future__ import annotations
 
@@ -58,13 +71,48 @@ def _specs(m: int, p: int, cov_left, cov_right):
     return cov_left, cov_right
 
 
+def _chi_square_1(rng: np.random.Generator, n: int) -> np.ndarray:
+    """datagen.py:75-80: chi-square(1) draws, zeros redrawn -- the caller's Generator,
+    the reference's call sequence."""
+    w = rng.chisquare(1.0, n)
+    while (w == 0.0).any():
+        zeros = w == 0.0
+        w[zeros] = rng.chisquare(1.0, int(zeros.sum()))
+    return w
+
+
+def _ar1(Z: np.ndarray, spec: CovarianceSpec, w, loc: float, transpose: bool, tdt) -> torch.Tensor:
+    """L @ Z (datagen.py:70-71) on the device: Z is (dim, count); returns (dim, count) or its
+    transpose (count, dim), heavy-tailed when w is given."""
+    dim, count = Z.shape
+    Zd = _lib.f64(Z)
+    wd = _lib.f64(w) if w is not None else None
+    out = torch.empty((count, dim) if transpose else (dim, count), dtype=tdt, device=_lib.device())
+    _lib.call("bmm_ar1_transform", _lib.matrix_dtype(out), _lib.ptr(Zd), dim, count, count, int(transpose),
+              float(spec.scale), float(spec.rho), _lib.ptr(wd), float(loc), _lib.ptr(out), out.shape[1],
+              _lib.stream_ptr())
+    return out
+
+
 def _generate(heavy: bool, m: int, n: int, p: int, rng: np.random.Generator, cov_left, cov_right, loc: float,
-              device: bool, dtype):
+              device: bool, dtype, stream: str = "numpy"):
     if min(m, n, p) < 1:
         raise ValueError("dimensions must be >= 1")
+    if stream not in ("numpy", "device"):
+        raise ValueError("stream must be 'numpy' or 'device'")
     cl, cr = _specs(m, p, cov_left, cov_right)
     tdt = torch.float32 if np.dtype(dtype) == np.float32 else torch.float64
     dev = _lib.device()
+    if stream == "numpy":
+        # the reference's draw order: Z_left, (w_left), Z_right, (w_right)
+        Z = rng.standard_normal((m, n))
+        w = _chi_square_1(rng, n) if heavy else None
+        M = _ar1(Z, cl, w, loc, False, tdt)
+        Z = rng.standard_normal((p, n))
+        w = _chi_square_1(rng, n) if heavy else None
+        N = _ar1(Z, cr, w, loc, True, tdt)
+        del Z
+        return (M, N) if device else (_lib.host(M), _lib.host(N))
     w = rng.integers(0, 2 ** 32, size=4, dtype=np.uint64)
     seed_lo = int(w[0]) | (int(w[1]) << 32)
     seed_hi = int(w[2]) | (int(w[3]) << 32)
@@ -80,18 +128,20 @@ def _generate(heavy: bool, m: int, n: int, p: int, rng: np.random.Generator, cov
 
 def gen_normal_instance(m: int, n: int, p: int, rng: np.random.Generator,
                         cov_left: Optional[CovarianceSpec] = None, cov_right: Optional[CovarianceSpec] = None,
-                        *, device: bool = False, dtype=np.float64):
+                        *, device: bool = False, dtype=np.float64, stream: str = "numpy"):
     """M (m x n) with i.i.d. N(0, Sigma_left) columns, N (n x p) with i.i.d.
     N(0, Sigma_right) rows (datagen.py:55-72).  device=True keeps them in HBM."""
-    return _generate(False, m, n, p, rng, cov_left, cov_right, 0.0, device, dtype)
+    return _generate(False, m, n, p, rng, cov_left, cov_right, 0.0, device, dtype, stream)
 
 
 def gen_heavy_tail_instance(m: int, n: int, p: int, rng: np.random.Generator,
                             cov_left: Optional[CovarianceSpec] = None, cov_right: Optional[CovarianceSpec] = None,
-                            location: str = "ones", *, device: bool = False, dtype=np.float64):
+                            location: str = "ones", *, device: bool = False, dtype=np.float64,
+                            stream: str = "numpy"):
     """location + z / sqrt(chi^2(1)) columns / rows (datagen.py:84-110)."""
     if min(m, n, p) < 1:
         raise ValueError("dimensions must be >= 1")
     if location not in ("ones", "zero"):
         raise ValueError("location must be 'ones' or 'zero'")
-    return _generate(True, m, n, p, rng, cov_left, cov_right, 1.0 if location == "ones" else 0.0, device, dtype)
+    return _generate(True, m, n, p, rng, cov_left, cov_right, 1.0 if location == "ones" else 0.0, device, dtype,
+                     stream)

@@ -71,16 +71,33 @@ def spawn_words(rng, count: int) -> tuple[np.ndarray, int]:
 
 
 def advance_spawn_counter(ss: np.random.SeedSequence, count: int) -> None:
-    """``ss.spawn(count)`` without materialising the children when possible."""
+    """``ss.spawn(count)`` for its side effect on the parent (``n_children_spawned += count``,
+    which is all the reference's ``rng.spawn(K)`` leaves behind on the caller's generator).
+
+    The public call is the contract; the pickle-state shortcut only skips building ``count``
+    child objects and is taken only when the state tuple has the layout this numpy writes
+    (entropy, n_children_spawned, pool, pool_size, spawn_key) and the counter reads back as
+    expected -- otherwise the parent is put back as it was and ``spawn`` runs."""
     if count <= 0:
         return
-    try:
-        st = ss.__reduce__()[2]  # (entropy, n_children_spawned, pool, pool_size, spawn_key)
-        ss.__setstate_cython__((st[0], st[1] + count, st[2], st[3], st[4]))
-        if ss.n_children_spawned == st[1] + count:
-            return
-    except Exception:  # pragma: no cover - numpy internals changed; fall back to the public call
-        pass
+    before = ss.n_children_spawned
+    if count >= 64:  # small counts: the public call costs microseconds
+        st = None
+        try:
+            st = ss.__reduce__()[2]
+            if isinstance(st, tuple) and len(st) == 5 and st[1] == before:
+                ss.__setstate_cython__((st[0], before + count, st[2], st[3], st[4]))
+                if ss.n_children_spawned == before + count and ss.__reduce__()[2][2:] == st[2:]:
+                    return
+                ss.__setstate_cython__(st)
+        except Exception:  # numpy internals changed: undo if possible, then the public call
+            try:
+                if st is not None and ss.n_children_spawned != before:
+                    ss.__setstate_cython__(st)
+            except Exception:
+                pass
+    if ss.n_children_spawned != before:
+        raise RuntimeError("SeedSequence spawn counter could not be restored; refusing to continue")
     ss.spawn(count)
 
 
