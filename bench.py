@@ -1033,6 +1033,15 @@ def run_device(args):
     W = 1024 if name == "cfg5" else 32768
     pipe = SketchPipeline(m, n, p, sizes, W, "ONC", batch=B, dtype=torch.float32)
     keys = np.arange(lo, hi)
+    # the batch in waves on several streams of the one graph: a wave's latency-bound planning
+    # kernels run beside another wave's HBM-bound norm pass / gather-contraction
+    # (tools/cfg5_waves_probe.py; BMM_CFG5_WAVES=0 keeps one batch)
+    wv = os.environ.get("BMM_CFG5_WAVES", "1024,4")
+    waves = tuple(int(x) for x in wv.split(",")) if wv not in ("", "0") else None
+    if waves is not None and B > waves[0]:
+        pipe.set_waves(*waves)
+    else:
+        waves = None
 
     def seeds():
         return seeds_from_keys("ONC", workloads.ROOT, (cfg, 1), keys, K)
@@ -1205,7 +1214,8 @@ def run_device(args):
         "data": "synthetic (seeded torch generator on device, SURVEY.md §8(d) distributions)",
         "config": {"workload": name, "batch": 4096, "batch_per_gpu": B, "m": m, "n": n, "p": p, "K": K, "W": W, "method": "ONC",
                    "distinct_columns_mean": float(kcounts.mean()),
-                   "l2": f"inputs {norm_bytes / 1e9:.1f} GB >> L2"},
+                   "l2": f"inputs {norm_bytes / 1e9:.1f} GB >> L2",
+                   "waves": (f"{waves[0]} problems per wave on {waves[1]} streams of one graph" if waves else "one batch")},
         "gpu_launches": int(pipe.graph_launches),
         "roofline_norms": {"bound": "hbm", "kernel": "colsq/rowsq (K1)", "achieved": norm_bytes / (norms_ms * 1e-3) / 1e9,
                            "peak": hbm_peak, "unit": "GB/s", "frac": norm_bytes / (norms_ms * 1e-3) / 1e9 / hbm_peak,

@@ -30,6 +30,7 @@
 
 #include "common.cuh"
 #include "tcgen05.cuh"
+#include "balance.cuh"
 
 namespace bmm {
 
@@ -689,44 +690,17 @@ __global__ void __launch_bounds__(32 * P_WARPS, 1) gemm_f16split_2sm_kernel(
   }
 }
 
-// balanced exponents and the problem's shift for the F16 split: kexp[t] =
-// round(log2(||N_i|| / ||M_i||) / 2) (i = column[t]), gshift[b] such that every
-// scaled operand |C[h,t]| 2^(kexp - G), |D[t,f]| 2^(-kexp - G) < 2^15 -- bounded by
-// the column / row norms from the norm pass times the sketch scale.
+// balanced exponents and the problem's shift for the F16 split (balance.cuh)
 __global__ void __launch_bounds__(256) f16_balance_kernel(const double* __restrict__ colsq,
                                                           const double* __restrict__ rowsq, int64_t n_stride,
                                                           const int64_t* __restrict__ column,
                                                           const double* __restrict__ scale, int64_t w,
                                                           int64_t w_stride, const int64_t* __restrict__ kdev,
                                                           int32_t* __restrict__ kexp, int32_t* __restrict__ gshift) {
-  __shared__ int red[8];
   const int64_t b = blockIdx.x;
   const int64_t kd = kdev != nullptr ? min(kdev[b], w) : w;
-  int emax = -100000;
-  for (int64_t t = threadIdx.x; t < w; t += blockDim.x) {
-    int32_t e = 0;
-    if (t < kd) {
-      const int64_t i = column[b * w_stride + t];
-      const double c = colsq[b * n_stride + i], r = rowsq[b * n_stride + i], sc = fabs(scale[b * w_stride + t]);
-      if (c > 0.0 && r > 0.0 && sc > 0.0 && c < 1e300 && r < 1e300 && sc < 1e300) {
-        const int d = ilogb(r) - ilogb(c);
-        e = (int32_t)((d >= 0 ? d + 2 : d - 2) / 4);
-        e = max(-60, min(60, e));
-        const double bc = ldexp(sqrt(c) * sc, e), bd = ldexp(sqrt(r) * sc, -e);
-        emax = max(emax, ilogb(fmax(bc, bd)) + 1);
-      }
-    }
-    kexp[b * w_stride + t] = e;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = emax;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int v = red[0];
-    for (int j = 1; j < (int)(blockDim.x >> 5); ++j) v = max(v, red[j]);
-    gshift[b] = v <= -100000 ? 0 : max(-60, min(60, v - 15));
-  }
+  f16_balance_body(colsq + b * n_stride, rowsq + b * n_stride, column + b * w_stride, scale + b * w_stride, w, kd,
+                   kexp + b * w_stride, gshift + b);
 }
 
 // ---- split gather (K4 for the float32 path)

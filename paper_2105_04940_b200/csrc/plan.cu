@@ -368,25 +368,18 @@ __device__ void bitonic_sort(uint64_t* key, int32_t* pos, int64_t n) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
-    int rule, const double* __restrict__ s, const double* __restrict__ aux,
-    const int64_t* __restrict__ sizes, const int64_t* __restrict__ caps_in,
-    const uint8_t* __restrict__ floors_in, int64_t K, const int64_t* __restrict__ c_arr, int cap,
-    int64_t* budgets, int64_t* col_off, int32_t* status, int64_t* diag, int32_t* notes,
-    char* ws_base, int use_smem) {
-  // working set in shared memory when it fits (every fixpoint phase then
-  // costs shared- rather than L2-latency round trips); global otherwise
-  extern __shared__ __align__(16) char dyn_ws[];
+// integerize + the allocators' weights for ONE problem, run by every thread of the CTA
+// (budgets_kernel: one CTA per problem; plan_small_kernel: a stage of the fused plan).
+// sb / ab: the problem's K score sums / auxiliary values (global or shared memory).
+__device__ void budgets_body(int rule, const double* sb, const double* ab, const int64_t* __restrict__ sizes,
+                             const int64_t* caps_b, const uint8_t* floors_b, int64_t K, int64_t c, int cap,
+                             int64_t* budgets_b, int64_t* col_off_b, int32_t* status_b, int64_t* diag_b,
+                             int32_t* notes_b, BudgetWs ws) {
   __shared__ int64_t red[32];
   __shared__ int64_t sh_scalar[4];
   __shared__ double sh_S;
-  const int64_t b = blockIdx.x;
   const int tid = threadIdx.x;
   const int NT = blockDim.x;
-  BudgetWs ws = carve_ws(use_smem ? dyn_ws : ws_base + b * budget_ws_bytes(K), K);
-  const int64_t c = c_arr[b];
-  const double* sb = s ? s + b * K : nullptr;
-  const double* ab = aux ? aux + b * K : nullptr;
   // chunked ownership keeps compaction in ascending block order
   const int64_t per = (K + NT - 1) / NT;
   const int64_t k_lo = tid * per, k_hi = min(K, k_lo + per);
@@ -395,22 +388,22 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
     int64_t run = 0;
     for (int64_t k = k_lo; k < k_hi; ++k) {
       const int64_t v = (sb == nullptr || sb[k] > 0.0) ? c : 0;
-      budgets[b * K + k] = v;
+      budgets_b[k] = v;
       run += v;
     }
-    if (col_off != nullptr) {
+    if (col_off_b != nullptr) {
       int64_t tot = 0;
       int64_t before = block_exclusive_scan(run, red, &tot);
       for (int64_t k = k_lo; k < k_hi; ++k) {
-        col_off[b * (K + 1) + k] = before;
-        before += budgets[b * K + k];
+        col_off_b[k] = before;
+        before += budgets_b[k];
       }
-      if (tid == 0) col_off[b * (K + 1) + K] = tot;
+      if (tid == 0) col_off_b[K] = tot;
     }
     if (tid == 0) {
-      if (status) status[b] = BMM_ST_OK;
-      if (diag) diag[b] = 0;
-      if (notes) notes[b] = 0;
+      if (status_b) *status_b = BMM_ST_OK;
+      if (diag_b) *diag_b = 0;
+      if (notes_b) *notes_b = 0;
     }
     return;
   }
@@ -430,8 +423,8 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
       mn = 1;
     } else if (rule == BMM_RULE_EXPLICIT) {
       w = ab[k];
-      capk = caps_in ? caps_in[b * K + k] : c;
-      mn = floors_in ? (floors_in[b * K + k] != 0) : (w > 0.0);
+      capk = caps_b ? caps_b[k] : c;
+      mn = floors_b ? (floors_b[k] != 0) : (w > 0.0);
       if (!(isfinite(w)) || w < 0.0) local_err = max(local_err, 100 + BMM_ST_BAD_WEIGHT);
     } else {
       if (sk > 0.0) any_pos_s = 1;
@@ -661,7 +654,7 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
     else if (ws.capped[k]) v = ws.maxs[k];
     else if (ws.floored[k]) v = ws.mins[k];
     else v = ws.base[pos++];
-    budgets[b * K + k] = v;
+    budgets_b[k] = v;
     ws.maxs[k] = v;  // reuse for the prefix below
     run += v;
     if (scored && (v == 0) != !(sb[k] > 0.0)) first_bad = min(first_bad, k);
@@ -679,20 +672,38 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
     __syncthreads();
     if (fb < K) { st = BMM_ST_PLAN_MISMATCH; dg = fb; }
   }
-  if (col_off != nullptr) {
+  if (col_off_b != nullptr) {
     int64_t tot = 0;
     int64_t before = block_exclusive_scan(run, red, &tot);
     for (int64_t k = k_lo; k < k_hi; ++k) {
-      col_off[b * (K + 1) + k] = before;
+      col_off_b[k] = before;
       before += ws.maxs[k];
     }
-    if (tid == 0) col_off[b * (K + 1) + K] = tot;
+    if (tid == 0) col_off_b[K] = tot;
   }
   if (tid == 0) {
-    if (status) status[b] = st;
-    if (diag) diag[b] = dg;
-    if (notes) notes[b] = note;
+    if (status_b) *status_b = st;
+    if (diag_b) *diag_b = dg;
+    if (notes_b) *notes_b = note;
   }
+}
+
+
+__global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
+    int rule, const double* __restrict__ s, const double* __restrict__ aux,
+    const int64_t* __restrict__ sizes, const int64_t* __restrict__ caps_in,
+    const uint8_t* __restrict__ floors_in, int64_t K, const int64_t* __restrict__ c_arr, int cap,
+    int64_t* budgets, int64_t* col_off, int32_t* status, int64_t* diag, int32_t* notes,
+    char* ws_base, int use_smem) {
+  // working set in shared memory when it fits (every fixpoint phase then
+  // costs shared- rather than L2-latency round trips); global otherwise
+  extern __shared__ __align__(16) char dyn_ws[];
+  const int64_t b = blockIdx.x;
+  BudgetWs ws = carve_ws(use_smem ? dyn_ws : ws_base + b * budget_ws_bytes(K), K);
+  budgets_body(rule, s ? s + b * K : nullptr, aux ? aux + b * K : nullptr, sizes, caps_in ? caps_in + b * K : nullptr,
+               floors_in ? floors_in + b * K : nullptr, K, c_arr[b], cap, budgets + b * K,
+               col_off ? col_off + b * (K + 1) : nullptr, status ? status + b : nullptr, diag ? diag + b : nullptr,
+               notes ? notes + b : nullptr, ws);
 }
 
 }  // namespace bmm
