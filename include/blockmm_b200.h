@@ -527,6 +527,27 @@ int bmm_all_gather_f64_nccl(void* comm, const double* src, int64_t len, double* 
 int bmm_exchange_sum_nccl(void* comm, int nranks, const double* partial, int64_t len, double* ws,
                           double* out, void* stream);
 
+/* The whole plan of MANY SMALL problems, one CTA per problem (config 5: 4096 problems of
+ * n = 4096, K = 64): bmm_block_probs + bmm_budgets (ONC / OPL rules) + bmm_seed_streams +
+ * bmm_sample + bmm_compress_sketch + bmm_balance_f16 in one launch, with the probabilities
+ * and the CDF held in shared memory (plan.py:165-206, 242-421; estimators.py:34-44, 78,
+ * 141).  Same device functions in the same order as the separate entries: every output is
+ * bit-identical to theirs.  cum, last_support, diag, notes, states and (kexp, gshift) are
+ * optional (NULL).  Needs bmm_plan_small_smem(n, K, W) <= 200 KiB and n, W < 65536;
+ * BMM_E_UNSUPPORTED otherwise (callers then use the separate entries).                     */
+int64_t bmm_plan_small_smem(int64_t n, int64_t K, int64_t W);
+/* diagnostics: later launches write 16 SM-clock stamps per problem (stage boundaries) to
+ * `stamps` (batch x 16, device); NULL switches it off (tools/plan_small_probe.py)          */
+int bmm_plan_small_debug(long long* stamps);
+int bmm_plan_small(int rule, const double* colsq, const double* rowsq, int64_t n,
+                   const int64_t* offsets, const int64_t* sizes, int64_t K, int64_t batch,
+                   const double* aux, const int64_t* c, int cap, const uint32_t* words,
+                   int64_t n_words, const int64_t* first_child, int64_t W, double* probs, double* s,
+                   double* cum, int64_t* last_support, int64_t* budgets, int64_t* col_off,
+                   int32_t* status, int64_t* diag, int32_t* notes, uint64_t* states,
+                   int64_t* column, double* prob, double* scale, int64_t* k_column,
+                   double* k_scale, int64_t* k_count, int32_t* kexp, int32_t* gshift, void* stream);
+
 /* Diagnostics: the device clock (%globaltimer, ns) written to out[0] by a
  * one-thread kernel on `stream` (graph-capturable; tools/timeline.py).        */
 int bmm_timestamp(unsigned long long* out, void* stream);

@@ -100,6 +100,9 @@ SIGNATURES = {
                               _I64, _P]),
     "bmm_ar1_transform": (_I, [_I, _P, _I64, _I64, _I64, _I, ctypes.c_double, ctypes.c_double, _P, ctypes.c_double,
                                _P, _I64, _P]),
+    "bmm_plan_small_smem": (_I64, [_I64, _I64, _I64]),
+    "bmm_plan_small_debug": (_I, [_P]),
+    "bmm_plan_small": (_I, [_I, _P, _P, _I64, _P, _P, _I64, _I64, _P, _P, _I, _P, _I64, _P, _I64] + [_P] * 18 + [_P]),
     "bmm_sqdiff_workspace": (_I64, [_I64, _I64, _I64]),
     "bmm_sqdiff": (_I, [_I, _P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P]),
     "bmm_pairwise_sum": (_I, [_P, _I64, _I64, _I64, _P, _P]),

@@ -14,6 +14,7 @@ __device__ __forceinline__ void f16_balance_body(const double* __restrict__ cols
                                                  int32_t* kexp, int32_t* gshift) {
   __shared__ int red[32];
   int emax = -100000;
+#pragma unroll 4
   for (int64_t t = threadIdx.x; t < w; t += blockDim.x) {
     int32_t e = 0;
     if (t < kd) {

@@ -9,6 +9,8 @@
 // given bit-identical norms.
 #include "common.cuh"
 #include "pairwise.cuh"
+#include "rng.cuh"
+#include "balance.cuh"
 
 namespace bmm {
 
@@ -706,6 +708,373 @@ __global__ void __launch_bounds__(kBudgetThreads) budgets_kernel(
                notes ? notes + b : nullptr, ws);
 }
 
+
+// ---- K2 + K3 for many small problems (config 5: 4096 problems of n = 4096, K = 64): the
+// whole plan of ONE problem in ONE CTA -- scores, block probabilities, score sums, CDF
+// (plan.py:165-206, estimators.py:37-38), budgets (budgets_body), child streams
+// (estimators.py:141), the draws (estimators.py:34-44,78), the compressed sketch
+// (bmm_compress_sketch) and the fp16 split's balanced exponents (bmm_balance_f16) -- with the
+// probabilities and the CDF held in shared memory instead of making a round trip through HBM
+// between seven launches.  Every value comes from the same device functions in the same
+// order as the separate kernels, so budgets, draws and scales are bit-identical to them
+// (tests/test_gpu_pipeline.py::test_plan_small_matches_separate_kernels).
+struct PlanSmallArgs {
+  int rule, cap;
+  const double* colsq;
+  const double* rowsq;
+  int64_t n;
+  const int64_t* offsets;
+  const int64_t* sizes;
+  int64_t K;
+  const double* aux;  // OPL: g_k^2 (batch x K)
+  const int64_t* c_arr;
+  const uint32_t* words;
+  int64_t n_words;
+  const int64_t* first_child;
+  int64_t W;  // sketch width (= row stride of the draw arrays)
+  double* probs;
+  double* s;
+  double* cum;     // optional
+  int64_t* last;   // optional
+  int64_t* budgets;
+  int64_t* col_off;
+  int32_t* status;
+  int64_t* diag;
+  int32_t* notes;
+  uint64_t* states;  // optional
+  int64_t* column;
+  double* prob;
+  double* scale;
+  int64_t* k_column;
+  double* k_scale;
+  int64_t* k_count;
+  int32_t* kexp;    // optional (with gshift): balanced exponents of the compressed sketch
+  int32_t* gshift;
+  long long* dbg;   // optional: 16 clock64 stamps per problem (tools/plan_small_probe.py)
+};
+
+constexpr int kPlanThreads = 128;
+
+__host__ __device__ inline int64_t plan_small_smem(int64_t n, int64_t K, int64_t W) {
+  int64_t b = 0;
+  b += align_up(8 * (n + K), 16);          // padded scores -> probabilities -> CDF (in place)
+  b += align_up(8 * K, 16);                // score sums
+  b += 2 * align_up(8 * (K + 1), 16);      // offsets, first sketch column of each block
+  b += 2 * align_up(8 * K, 16);            // budgets, last support index
+  b += align_up(32 * K, 16);               // child PCG64 states
+  b += align_up(4 * ((n + 1) / 2), 16);    // draw counts per column (16-bit fields)
+  b += align_up(2 * W, 16);                // drawn column of every sketch slot, then the distinct list
+  b += 256 + budget_ws_bytes(K);           // integerize working set
+  return b;
+}
+
+// NumPy's pairwise sum of buf[start, start + n) for n <= 128 (one leaf, pairwise.cuh) by an
+// aligned group of 8 lanes: lane j runs accumulator r_j, the xor butterfly combines them as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), the group's first lane adds the n % 8 tail; every lane
+// of the group gets the sum.  `gmask` = the group's 8 lanes (other groups may diverge).
+__device__ __forceinline__ double group8_pw_sum(const double* buf, int64_t start, int64_t n, int j, unsigned gmask,
+                                                int lane0) {
+  double r = 0.0;
+  if (n < 8) {
+    if (j == 0)
+      for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, buf[start + i]);
+  } else {
+    r = warp_leaf8(SrcF64{buf}, start, n, j);
+    r = __dadd_rn(r, __shfl_xor_sync(gmask, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(gmask, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(gmask, r, 4));
+    if (j == 0)
+      for (int64_t i = n - (n % 8); i < n; ++i) r = __dadd_rn(r, buf[start + i]);
+  }
+  return __shfl_sync(gmask, r, lane0);
+}
+
+// buf[i] /= d for this lane's elements i = j, j + 8, ...; 4 independent divisions per step
+__device__ __forceinline__ void group8_divide(double* buf, int64_t nk, int j, double d) {
+  for (int64_t i0 = j; i0 < nk; i0 += 32) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = (i0 + 8 * u < nk) ? buf[i0 + 8 * u] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ddiv_rn(v[u], d);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + 8 * u < nk) buf[i0 + 8 * u] = v[u];
+  }
+}
+
+__global__ void __launch_bounds__(kPlanThreads, 4) plan_small_kernel(const PlanSmallArgs a) {
+  extern __shared__ __align__(16) char dyn_plan[];
+  __shared__ int64_t red[32];
+  const int64_t b = blockIdx.x, n = a.n, K = a.K, W = a.W;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
+  char* q = dyn_plan;
+  auto take = [&](int64_t bytes) { char* r = q; q += align_up(bytes, 16); return r; };
+  // block k's scores, then probabilities, then CDF at sc[offsets[k] + k ...] (the pad spreads the banks)
+  double* sc = (double*)take(8 * (n + K));
+  double* ss = (double*)take(8 * K);
+  int64_t* s_off = (int64_t*)take(8 * (K + 1));
+  int64_t* s_col = (int64_t*)take(8 * (K + 1));
+  int64_t* s_bud = (int64_t*)take(8 * K);
+  int64_t* s_last = (int64_t*)take(8 * K);
+  uint64_t* s_state = (uint64_t*)take(32 * K);
+  uint32_t* cnt = (uint32_t*)take(4 * ((n + 1) / 2));
+  uint16_t* s_draw = (uint16_t*)take(2 * W);
+  q = (char*)(((uintptr_t)q + 255) & ~(uintptr_t)255);
+  BudgetWs ws = carve_ws(q, K);
+  auto stamp = [&](int i) {
+    if (a.dbg != nullptr && tid == 0) a.dbg[b * 16 + i] = clock64();
+  };
+  stamp(0);
+  for (int64_t k = tid; k <= K; k += NT) s_off[k] = a.offsets[k];
+  for (int64_t j = tid; j < (n + 1) / 2; j += NT) cnt[j] = 0u;
+  __syncthreads();
+  const double* cs = a.colsq + b * n;
+  const double* rs = a.rowsq + b * n;
+  double* probs_b = a.probs + b * n;
+  // ---- a group of 8 lanes per block: scores (plan.py:167), score sum (:173), the two
+  // normalisations (:199-205), then the CDF in place (np.cumsum, estimators.py:37-38)
+  {
+    const int j = lane & 7, grp = tid >> 3, ngrp = NT >> 3;
+    const unsigned gmask = 0xffu << (lane & 24);
+    const int lane0 = lane & 24;
+    for (int64_t k = grp; k < K; k += ngrp) {
+      const int64_t o = s_off[k], nk = s_off[k + 1] - o;
+      double* buf = sc + o + k;
+      // 4 elements per step, loads first: independent square roots overlap their latencies
+      for (int64_t i0 = j; i0 < nk; i0 += 32) {
+        double c4[4], r4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = i0 + 8 * u;
+          c4[u] = i < nk ? cs[o + i] : 0.0;
+          r4[u] = i < nk ? rs[o + i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c4[u] = __dmul_rn(__dsqrt_rn(c4[u]), __dsqrt_rn(r4[u]));
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + 8 * u < nk) buf[i0 + 8 * u] = c4[u];
+      }
+      __syncwarp(gmask);
+      if (k == 0) stamp(8);
+      const double rest = group8_pw_sum(buf, 1, nk - 1, j, gmask, lane0);
+      const double tot = __dadd_rn(0.0, group8_pw_sum(buf, 0, nk, j, gmask, lane0));
+      if (j == 0) {
+        const double sk = __dadd_rn(buf[0], rest);
+        ss[k] = sk;
+        a.s[b * K + k] = sk;
+      }
+      __syncwarp(gmask);
+      if (k == 0) stamp(9);
+      if (tot == 0.0) {
+        for (int64_t i = j; i < nk; i += 8) buf[i] = 0.0;
+      } else {
+        group8_divide(buf, nk, j, tot);
+        __syncwarp(gmask);
+        const double tot2 = __dadd_rn(0.0, group8_pw_sum(buf, 0, nk, j, gmask, lane0));
+        __syncwarp(gmask);
+        group8_divide(buf, nk, j, tot2);
+      }
+      __syncwarp(gmask);
+      if (k == 0) stamp(10);
+      for (int64_t i = j; i < nk; i += 8) probs_b[o + i] = buf[i];
+      __syncwarp(gmask);
+      if (k == 0) stamp(11);
+      if (j == 0) {
+        double acc = 0.0;
+        int64_t lst = -1;
+        for (int64_t i = 0; i < nk; ++i) {
+          const double x = buf[i];
+          acc = __dadd_rn(acc, x);
+          buf[i] = acc;
+          if (x > 0.0) lst = i;
+        }
+        s_last[k] = lst;
+        if (a.last != nullptr) a.last[b * K + k] = lst;
+      }
+      if (k == 0) stamp(12);
+    }
+    if (tid == 0) stamp(13);
+  }
+  __syncthreads();
+  stamp(1);
+  if (a.cum != nullptr) {
+    for (int64_t k = warp; k < K; k += nwarps) {
+      const int64_t o = s_off[k], nk = s_off[k + 1] - o;
+      for (int64_t i = lane; i < nk; i += 32) a.cum[b * n + o + i] = sc[o + k + i];
+    }
+  }
+  stamp(2);
+  // ---- budgets                                                     plan.py:242-421
+  budgets_body(a.rule, ss, a.aux ? a.aux + b * K : nullptr, a.sizes, nullptr, nullptr, K, a.c_arr[b], a.cap,
+               a.budgets + b * K, a.col_off + b * (K + 1), a.status + b, a.diag ? a.diag + b : nullptr,
+               a.notes ? a.notes + b : nullptr, ws);
+  __syncthreads();
+  stamp(3);
+  for (int64_t k = tid; k <= K; k += NT) {
+    s_col[k] = a.col_off[b * (K + 1) + k];
+    if (k < K) s_bud[k] = a.budgets[b * K + k];
+  }
+  // ---- child streams                                               estimators.py:141
+  for (int64_t k = tid; k < K; k += NT) {
+    U128 st, inc;
+    seed_pcg64(a.words + b * a.n_words, a.n_words, (uint64_t)(a.first_child[b] + k), st, inc);
+    s_state[4 * k] = st.hi;
+    s_state[4 * k + 1] = st.lo;
+    s_state[4 * k + 2] = inc.hi;
+    s_state[4 * k + 3] = inc.lo;
+    if (a.states != nullptr) {
+      uint64_t* o = a.states + 4 * (b * K + k);
+      o[0] = st.hi; o[1] = st.lo; o[2] = inc.hi; o[3] = inc.lo;
+    }
+  }
+  __syncthreads();
+  stamp(4);
+  // ---- draws: L threads per block, thread `sub` takes draws sub, sub + L, ... of the block's
+  // stream (PCG64 jump-ahead), inverse CDF by binary search        estimators.py:34-44,78
+  {
+    const int64_t L = K >= NT ? 1 : NT / K;
+    for (int64_t unit = tid; unit < K * L; unit += NT) {
+      const int64_t k = unit / L, sub = unit - k * L;
+      const int64_t ck = s_bud[k];
+      if (ck <= sub) continue;
+      const int64_t o = s_off[k], len = s_off[k + 1] - o, lst = s_last[k];
+      const double* cb = sc + o + k;
+      U128 st{s_state[4 * k], s_state[4 * k + 1]};
+      const U128 inc{s_state[4 * k + 2], s_state[4 * k + 3]};
+      U128 am, ap, jm{0, 1}, jp{0, 0};
+      pcg_jump((uint64_t)(sub + 1), inc, am, ap);
+      st = add128(mul128(st, am), ap);  // the state draw `sub` reads
+      if (L > 1) pcg_jump((uint64_t)L, inc, jm, jp);
+      const int64_t t0 = s_col[k];
+      for (int64_t j = sub; j < ck; j += L) {
+        const double u = u53(pcg_output(st));
+        int64_t lo = 0, hi = len;  // first index with cum > u (searchsorted side="right")
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (cb[mid] > u) hi = mid; else lo = mid + 1;
+        }
+        const int64_t idx = max((int64_t)0, lo < lst ? lo : lst);
+        const int64_t col = o + idx;
+        a.column[b * W + t0 + j] = col;
+        s_draw[t0 + j] = (uint16_t)col;
+        atomicAdd(&cnt[col >> 1], 1u << (16 * (int)(col & 1)));
+        st = (L > 1) ? add128(mul128(st, jm), jp) : pcg_step(st, inc);
+      }
+    }
+  }
+  __syncthreads();
+  // the drawn columns' probabilities and scales 1 / sqrt(c_k p_i) (estimators.py:78), four
+  // sketch slots per step so the probability loads (L2) and the square roots overlap
+  {
+    auto block_of_slot = [&](int64_t t) {  // the last k with s_col[k] <= t (empty blocks skipped)
+      int64_t lo = 0, hi = K;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (s_col[mid] <= t) lo = mid; else hi = mid;
+      }
+      return lo;
+    };
+    const int64_t drawn = s_col[K];
+    for (int64_t t0 = tid; t0 < drawn; t0 += 4 * NT) {
+      double pr[4], dck[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t t = t0 + u * NT;
+        pr[u] = t < drawn ? probs_b[s_draw[t]] : 1.0;
+        dck[u] = t < drawn ? (double)s_bud[block_of_slot(t)] : 1.0;
+      }
+      double sv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sv[u] = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dck[u], pr[u])));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t t = t0 + u * NT;
+        if (t < drawn) {
+          a.prob[b * W + t] = pr[u];
+          a.scale[b * W + t] = sv[u];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  stamp(5);
+  // ---- compressed sketch: the distinct drawn columns in column order with scale
+  // s_i sqrt(c_i) (sketch_count_kernel + sketch_compact_kernel): warp w owns a contiguous
+  // range of columns, 32 at a time; ballots count and place the drawn ones
+  int64_t total = 0;
+  {
+    const int64_t per = (((n + nwarps - 1) / nwarps + 31) / 32) * 32;
+    const int64_t lo = min(n, (int64_t)warp * per), hi = min(n, lo + per);
+    auto count_of = [&](int64_t j) { return (cnt[j >> 1] >> (16 * (int)(j & 1))) & 0xffffu; };
+    int64_t mine = 0;
+    for (int64_t j0 = lo; j0 < hi; j0 += 32) {
+      const int64_t j = j0 + lane;
+      mine += __popc(__ballot_sync(0xffffffffu, j < hi && count_of(j) != 0u));
+    }
+    if (lane == 0) red[warp] = mine;
+    __syncthreads();
+    int64_t pos = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      if (w < warp) pos += red[w];
+      total += red[w];
+    }
+    int64_t* oc = a.k_column + b * W;
+    double* os = a.k_scale + b * W;
+    const unsigned below = (1u << lane) - 1u;
+    __syncthreads();  // s_draw: every slot's column has been read above; now the distinct list
+    for (int64_t j0 = lo; j0 < hi; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const unsigned mk = __ballot_sync(0xffffffffu, j < hi && count_of(j) != 0u);
+      if ((mk >> lane) & 1u) {
+        const int64_t qpos = pos + __popc(mk & below);
+        oc[qpos] = j;
+        s_draw[qpos] = (uint16_t)j;
+      }
+      pos += __popc(mk);
+    }
+    __syncthreads();
+    // scales s_i sqrt(c_i), four distinct columns per step
+    for (int64_t q0 = tid; q0 < total; q0 += 4 * NT) {
+      double pr[4], dck[4], dc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t qq = q0 + u * NT;
+        const int64_t j = qq < total ? (int64_t)s_draw[qq] : 0;
+        pr[u] = qq < total ? probs_b[j] : 1.0;
+        int64_t kl = 0, kh = K;  // block of column j: the last k with offsets[k] <= j
+        while (kh - kl > 1) {
+          const int64_t mid = (kl + kh) >> 1;
+          if (s_off[mid] <= j) kl = mid; else kh = mid;
+        }
+        dck[u] = qq < total ? (double)s_bud[kl] : 1.0;
+        dc[u] = qq < total ? (double)count_of(j) : 1.0;
+      }
+      double sv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        sv[u] = __dmul_rn(__ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dck[u], pr[u]))), __dsqrt_rn(dc[u]));
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + u * NT < total) os[q0 + u * NT] = sv[u];
+    }
+    // zero padding up to the next multiple of 64 (the float32 contractions' K steps)
+    const int64_t pad_end = min(W, ((total + 63) / 64) * 64);
+    for (int64_t u = total + tid; u < pad_end; u += NT) {
+      oc[u] = 0;
+      os[u] = 0.0;
+    }
+    if (tid == 0) a.k_count[b] = total;
+  }
+  stamp(6);
+  if (a.kexp != nullptr) {
+    __syncthreads();  // the compressed sketch of this CTA, written above
+    f16_balance_body(cs, rs, a.k_column + b * W, a.k_scale + b * W, W, min(total, W), a.kexp + b * W, a.gshift + b);
+  }
+  stamp(7);
+}
+
 }  // namespace bmm
 
 using namespace bmm;
@@ -799,5 +1168,48 @@ extern "C" int bmm_budgets(int rule, const double* s, const double* aux, const i
   budgets_kernel<<<(unsigned)batch, nt, smem ? (size_t)bytes : 0, as_stream(stream)>>>(
       rule, s, aux, sizes, caps, floors, K, c, cap, budgets, col_off, status, diag, notes, (char*)ws, smem ? 1 : 0);
   BMM_CHECK_LAUNCH("budgets_kernel");
+  return BMM_OK;
+}
+
+extern "C" int64_t bmm_plan_small_smem(int64_t n, int64_t K, int64_t W) { return plan_small_smem(n, K, W); }
+
+static long long* g_plan_dbg = nullptr;
+// diagnostics: 16 SM-clock stamps per problem (stage boundaries) written by the next launches
+extern "C" int bmm_plan_small_debug(long long* stamps) {
+  g_plan_dbg = stamps;
+  return BMM_OK;
+}
+
+extern "C" int bmm_plan_small(int rule, const double* colsq, const double* rowsq, int64_t n, const int64_t* offsets,
+                              const int64_t* sizes, int64_t K, int64_t batch, const double* aux, const int64_t* c,
+                              int cap, const uint32_t* words, int64_t n_words, const int64_t* first_child, int64_t W,
+                              double* probs, double* s, double* cum, int64_t* last_support, int64_t* budgets,
+                              int64_t* col_off, int32_t* status, int64_t* diag, int32_t* notes, uint64_t* states,
+                              int64_t* column, double* prob, double* scale, int64_t* k_column, double* k_scale,
+                              int64_t* k_count, int32_t* kexp, int32_t* gshift, void* stream) {
+  BMM_REQUIRE(n >= 1 && K >= 1 && K <= n && batch >= 1 && W >= 1, BMM_E_ARG, "bmm_plan_small: bad shape");
+  BMM_REQUIRE(rule == BMM_RULE_ONC || rule == BMM_RULE_OPL, BMM_E_UNSUPPORTED,
+              "bmm_plan_small: score-sum (ONC) and optimal (OPL) sizes only");
+  BMM_REQUIRE(rule != BMM_RULE_OPL || aux != nullptr, BMM_E_ARG, "bmm_plan_small: OPL needs g_k^2");
+  BMM_REQUIRE(W < 65536 && n < 65536, BMM_E_UNSUPPORTED,
+              "bmm_plan_small: W and n must be below 65536 (16-bit draw counts and column lists)");
+  BMM_REQUIRE(colsq && rowsq && offsets && sizes && c && words && first_child && probs && s && budgets && col_off && status &&
+                  column && prob && scale && k_column && k_scale && k_count,
+              BMM_E_ARG, "bmm_plan_small: null pointer");
+  BMM_REQUIRE((kexp == nullptr) == (gshift == nullptr), BMM_E_ARG, "bmm_plan_small: kexp and gshift go together");
+  BMM_REQUIRE(n_words >= 4, BMM_E_ARG, "bmm_plan_small: need >= 4 entropy words (padded run entropy)");
+  const int64_t smem = plan_small_smem(n, K, W);
+  BMM_REQUIRE(smem <= 200 * 1024, BMM_E_UNSUPPORTED, "bmm_plan_small: problem too large for one CTA (%lld bytes)",
+              (long long)smem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(plan_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  PlanSmallArgs a{rule, cap, colsq, rowsq, n, offsets, sizes, K, aux, c, words, n_words, first_child, W,
+                  probs, s, cum, last_support, budgets, col_off, status, diag, notes, states, column, prob, scale,
+                  k_column, k_scale, k_count, kexp, gshift, g_plan_dbg};
+  plan_small_kernel<<<(unsigned)batch, kPlanThreads, (size_t)smem, as_stream(stream)>>>(a);
+  BMM_CHECK_LAUNCH("plan_small_kernel");
   return BMM_OK;
 }

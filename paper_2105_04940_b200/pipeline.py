@@ -243,6 +243,12 @@ class SketchPipeline:
         if self.f16 or self.fused16:
             self.kexp = torch.zeros(B * W, dtype=torch.int32, device=dev)
             self.gshift = torch.zeros(B, dtype=torch.int32, device=dev)
+        # many small problems (config 5): probabilities, budgets, child streams, draws, the
+        # compressed sketch and the balanced exponents in ONE launch, one CTA per problem
+        # (bmm_plan_small; BMM_PLAN_SMALL=0 keeps the separate kernels)
+        self.plan_small = (method in ("ONC", "OPL") and self.compress and B >= 256 and self.max_len <= 128
+                           and W < 65536 and n_ < 65536 and self.lib.bmm_plan_small_smem(n_, K, W) <= 200 * 1024
+                           and os.environ.get("BMM_PLAN_SMALL", "1") != "0")
         if self.tf32:
             f32 = dict(dtype=torch.float32, device=dev)
             if not (self.fused or self.fused16):
@@ -427,7 +433,7 @@ class SketchPipeline:
         if self._waves is not None and chunks is None and self.B > self._waves[0]:
             return self._launch_waves(M, N)
         if self.shared is None:
-            seg_done = _stats_launch(self, M, N, chunks, probs=self.method != "SSM",
+            seg_done = _stats_launch(self, M, N, chunks, probs=self.method != "SSM" and not self._plan_small_now(),
                                      gsq=self.method == "OPL")
             if self.method == "OPL" and not seg_done:
                 self._segsq(M, N, _lib.matrix_dtype(M), 0, self.K, self.B, _lib.stream_ptr())
@@ -443,7 +449,7 @@ class SketchPipeline:
         gather-contraction runs, another wave's latency-bound planning kernels (block
         probabilities, budgets, draws, compaction) fill the gaps.  Every wave is this
         pipeline's own launch sequence on a slice of its buffers, so the results are
-        bit-identical to the single-batch run (config 5: 4 x 1024 problems, 10.1 -> 9.3 ms)."""
+        bit-identical to the single-batch run (config 5: 4 x 1024 problems, 9.7 -> 9.2 ms)."""
         if per_wave < 1 or streams < 1:
             raise ValueError("per_wave and streams must be >= 1")
         if not (self.fused16 or self.fused) or self.method in ("ONU", "ONMCNR") or self.shared is not None or (
@@ -469,7 +475,13 @@ class SketchPipeline:
             v._seedbuf = {k: tuple(t[a:b] for t in ts) for k, ts in self._seedbuf.items()}
             views.append((a, b, v))
         self._wave_views = views
-        self._wave_streams = [torch.cuda.Stream() for _ in range(S)]
+        # equal priorities by default.  BMM_WAVE_PRIO=1 puts earlier waves on higher-priority
+        # streams (a software pipeline over the waves): measured slower at config 5, 9.84 against
+        # 9.60 ms (profiles/r2aw_waves_priorities.txt)
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+        if os.environ.get("BMM_WAVE_PRIO", "0") != "1":
+            hi = lo = 0
+        self._wave_streams = [torch.cuda.Stream(priority=max(hi, lo - (S - 1 - i))) for i in range(S)]
 
     def _launch_waves(self, M: torch.Tensor, N: torch.Tensor) -> torch.Tensor:
         if self._wave_views is None:
@@ -477,6 +489,10 @@ class SketchPipeline:
         Mb = M.view(self.B, self.m, self.n)
         Nb = N.view(self.B, self.n, self.p)
         cur = torch.cuda.current_stream()
+        # (an explicit two-stream pipeline -- norm passes and contractions back to back on one
+        # stream, each wave's plan on a side stream between them -- measured slower, 10.3 against
+        # 9.6 ms at config 5: the HBM-bound kernels fill every SM, so a plan cannot run beside
+        # them and only delays its own contraction; profiles/r2ax_waves_pipelined.txt)
         for st in self._wave_streams:
             st.wait_stream(cur)
         for w, (a, b, v) in enumerate(self._wave_views):
@@ -502,6 +518,9 @@ class SketchPipeline:
         ldm, ldn = M.stride(-2), N.stride(-2)
         if self.method == "OPL":
             aux = self.gsq
+        if self._plan_small_now():
+            self._plan_small_call(st)
+            return self._contract_sketch(M, N, dt, st, planned=True)
         if self.method in ("ONU", "ONMCNR"):
             p0 = self.p0 if self.method == "ONU" else self.probs
             s_for_pilot = None if self.method == "ONU" else self.s
@@ -542,13 +561,34 @@ class SketchPipeline:
                 P(self.col_off), W, P(self.states), P(self.column), P(self.prob), P(self.scale), st)
         return self._contract_sketch(M, N, dt, st)
 
-    def _contract_sketch(self, M, N, dt, st):
-        """Compress the drawn sketch (column, scale) and contract it: C @ D."""
+    def _plan_small_call(self, st) -> None:
+        """The whole plan of every problem of the batch in one launch (bmm_plan_small)."""
+        B, n, K, W = self.B, self.n, self.K, self.W
+        P = lambda t: t.data_ptr()  # noqa: E731
+        rule = _lib.RULE_ONC if self.method == "ONC" else _lib.RULE_OPL
+        aux = self.gsq if self.method == "OPL" else None
+        words, first = self._seedbuf["main"]
+        bal = self.f16 or self.fused16
+        self._c("bmm_plan_small", rule, P(self.colsq), P(self.rowsq), n, P(self.offsets), P(self.sizes_d), K, B,
+                P(aux) if aux is not None else None, P(self.c_arr), int(self.cap), words.data_ptr(), words.shape[1],
+                first.data_ptr(), W, P(self.probs), P(self.s), None, P(self.last), P(self.budgets),
+                P(self.col_off), P(self.status), P(self.diag), P(self.notes), P(self.states), P(self.column),
+                P(self.prob), P(self.scale), P(self.k_column), P(self.k_scale), P(self.k_count),
+                P(self.kexp) if bal else None, P(self.gshift) if bal else None, st)
+
+    def _plan_small_now(self) -> bool:
+        """bmm_plan_small replaces the separate planning kernels: own statistics (no group's
+        shared stage or exchange feeding probabilities from elsewhere)."""
+        return self.plan_small and self.shared is None and self.exchange is None
+
+    def _contract_sketch(self, M, N, dt, st, planned: bool = False):
+        """Compress the drawn sketch (column, scale) and contract it: C @ D.
+        planned: bmm_plan_small already compressed it and balanced the exponents."""
         B, m, n, p, W = self.B, self.m, self.n, self.p, self.W
         sM, sN = m * n, n * p
         ldm, ldn = M.stride(-2), N.stride(-2)
         P = lambda t: t.data_ptr()  # noqa: E731
-        if self.compress:
+        if self.compress and not planned:
             # duplicates of a column share its scale: contract the distinct columns only
             self._c("bmm_compress_sketch", P(self.column), P(self.scale), W, W, n, B, P(self.ws_cmp),
                     self.ws_cmp.numel(), P(self.k_column), P(self.k_scale), P(self.k_count), st)
@@ -557,10 +597,10 @@ class SketchPipeline:
             self._c("bmm_gemm_f32split_gather", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.k_column),
                     P(self.k_scale), W, W, P(self.k_count), B, P(self.CD), p, m * p, st)
         elif self.fused16:
-            self.fused_f16(M, N, st)
+            self.fused_f16(M, N, st, balance=not planned)
         elif self.tf32 and self.compress:
             # float32 inputs: split gather + tcgen05 contraction (fp16 or tf32 + bf16 split)
-            self.split_gather(M, N, st)
+            self.split_gather(M, N, st, balance=not planned)
             self.split_gemm(st)
         elif self.tf32:
             self._c("bmm_gather_f32split", dt, P(M), ldm, sM, P(N), ldn, sN, m, p, P(self.column), P(self.scale), W, W,
@@ -571,19 +611,20 @@ class SketchPipeline:
             self.contract(M, N, st)
         return self._result()
 
-    def fused_f16(self, M, N, st=None):
+    def fused_f16(self, M, N, st=None, balance: bool = True):
         """Balanced exponents, then the fp16-split gather + contraction in one
         kernel (K4 + K6 fused, bmm_gemm_f16split_gather)."""
         B, m, n, p, W = self.B, self.m, self.n, self.p, self.W
         st = _lib.stream_ptr() if st is None else st
         P = lambda t: t.data_ptr()  # noqa: E731
-        self._c("bmm_balance_f16", P(self.colsq), P(self.rowsq), n, P(self.k_column), P(self.k_scale), W, W,
-                P(self.k_count), B, P(self.kexp), P(self.gshift), st)
+        if balance:
+            self._c("bmm_balance_f16", P(self.colsq), P(self.rowsq), n, P(self.k_column), P(self.k_scale), W, W,
+                    P(self.k_count), B, P(self.kexp), P(self.gshift), st)
         self._c("bmm_gemm_f16split_gather", _lib.matrix_dtype(M), P(M), M.stride(-2), m * n, P(N), N.stride(-2),
                 n * p, m, n, p, P(self.k_column), P(self.k_scale), P(self.kexp), P(self.gshift), W, W, P(self.k_count),
                 B, P(self.CD), p, m * p, st)
 
-    def split_gather(self, M, N, st=None):
+    def split_gather(self, M, N, st=None, balance: bool = True):
         """The float32 path's split gather of the compressed sketch (K4)."""
         B, m, n, p, W = self.B, self.m, self.n, self.p, self.W
         st = _lib.stream_ptr() if st is None else st
@@ -591,8 +632,9 @@ class SketchPipeline:
         ldm, ldn = M.stride(-2), N.stride(-2)
         P = lambda t: t.data_ptr()  # noqa: E731
         if self.f16:
-            self._c("bmm_balance_f16", P(self.colsq), P(self.rowsq), n, P(self.k_column), P(self.k_scale), W, W,
-                    P(self.k_count), B, P(self.kexp), P(self.gshift), st)
+            if balance:
+                self._c("bmm_balance_f16", P(self.colsq), P(self.rowsq), n, P(self.k_column), P(self.k_scale), W, W,
+                        P(self.k_count), B, P(self.kexp), P(self.gshift), st)
             self._c("bmm_gather_f16split_dk", dt, P(M), ldm, m * n, P(N), ldn, n * p, m, p, P(self.k_column),
                     P(self.k_scale), P(self.kexp), P(self.gshift), W, W, P(self.k_count), B, P(self.a_hi),
                     P(self.a_x), P(self.b_hi), P(self.b_x), st)

@@ -439,3 +439,73 @@ def test_waves_bit_identical_to_single_batch(method):
             assert np.array_equal(ref.budgets_host(), wav.budgets_host())
     with pytest.raises(ValueError, match="waves"):
         SketchPipeline(40, 512, 40, (64,) * 8, 128, "ONC", batch=4).set_waves(2, 2)
+
+
+@pytest.mark.parametrize("method,dtype", [("ONC", "f32"), ("OPL", "f32"), ("ONC", "f64"), ("OPL", "f64")])
+def test_plan_small_matches_separate_kernels(method, dtype, monkeypatch):
+    """bmm_plan_small (probabilities, budgets, child streams, draws, compressed sketch and
+    balanced exponents of a problem in one CTA) against the separate kernels: every plan
+    output bit-identical, unequal blocks, a zero-score block, an all-zero problem (its
+    status raises the reference's error), and the oracle on a few problems."""
+    B, m, n, p = 300, 24, 1000, 16
+    sizes = (64, 1, 100, 35, 128, 64, 8, 90, 64, 64, 64, 31, 97, 64, 62, 64)
+    assert sum(sizes) == n
+    K = len(sizes)
+    g = np.random.default_rng(5)
+    npdt = np.float32 if dtype == "f32" else np.float64
+    Ms = (g.standard_normal((B, m, n)) * g.lognormal(0, 1, (B, 1, n))).astype(npdt)
+    Ns = (g.standard_normal((B, n, p)) * g.lognormal(0, 1, (B, n, 1))).astype(npdt)
+    Ms[:, :, 65:165] = 0.0  # block 2 has zero score in every problem
+    Ms[7] = 0.0             # problem 7: nothing to sample
+    Md, Nd = torch.as_tensor(Ms, device="cuda"), torch.as_tensor(Ns, device="cuda")
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    W = 256
+    fused = SketchPipeline(m, n, p, sizes, W, method, batch=B, dtype=tdt)
+    assert fused.plan_small
+    waved = None
+    if dtype == "f32" and fused.fused and method == "ONC":  # the two-stream pipeline over waves (norms | plan | contraction)
+        waved = SketchPipeline(m, n, p, sizes, W, method, batch=B, dtype=tdt)
+        waved.set_waves(128, 2)
+    monkeypatch.setenv("BMM_PLAN_SMALL", "0")
+    sep = SketchPipeline(m, n, p, sizes, W, method, batch=B, dtype=tdt)
+    assert not sep.plan_small
+    for base in (1000, 5000):
+        rngs = lambda: [np.random.default_rng(base + b) for b in range(B)]  # noqa: E731
+        CDf = fused.run(Md, Nd, seeds_from_rngs(method, rngs(), K)).clone()
+        CDs = sep.run(Md, Nd, seeds_from_rngs(method, rngs(), K)).clone()
+        for name in ("s", "probs", "last", "budgets", "col_off", "status", "diag", "notes", "states"):
+            a, b_ = getattr(fused, name), getattr(sep, name)
+            assert torch.equal(a, b_), (name, base)
+        st = fused.status.cpu().numpy()
+        assert st[7] != 0 and (np.delete(st, 7) == 0).all()
+        kc = fused.k_count.cpu().numpy()
+        ok = np.flatnonzero(st == 0)
+        assert np.array_equal(kc[ok], sep.k_count.cpu().numpy()[ok]) and kc[7] == 0
+        for name in ("column", "prob", "scale"):  # a failed plan draws nothing: its rows are not written
+            a, b_ = getattr(fused, name).view(B, W), getattr(sep, name).view(B, W)
+            assert torch.equal(a[ok], b_[ok]), (name, base)
+        for b in ok[:40]:
+            pad = min(W, (kc[b] + 63) // 64 * 64)
+            sl = slice(b * W, b * W + pad)
+            assert torch.equal(fused.k_column[sl], sep.k_column[sl]) and torch.equal(fused.k_scale[sl], sep.k_scale[sl])
+            if hasattr(fused, "gshift"):
+                assert torch.equal(fused.kexp[b * W:b * W + kc[b]], sep.kexp[b * W:b * W + kc[b]])
+        if hasattr(fused, "gshift"):
+            assert torch.equal(fused.gshift[ok], sep.gshift[ok])
+        okt = torch.as_tensor(ok, device="cuda")
+        assert torch.equal(CDf.view(B, m, p)[okt], CDs.view(B, m, p)[okt])
+        if waved is not None:
+            if base == 5000:
+                waved.capture(Md, Nd)
+            CDw = waved.run(Md, Nd, seeds_from_rngs(method, rngs(), K)).clone()
+            assert torch.equal(CDw.view(B, m, p)[okt], CDf.view(B, m, p)[okt])
+            assert torch.equal(waved.column.view(B, W)[okt], fused.column.view(B, W)[okt])
+            assert torch.equal(waved.budgets, fused.budgets) and torch.equal(waved.status, fused.status)
+    with pytest.raises(ValueError):
+        fused.check()
+    for b in (0, 150, 299):
+        ref = O.approx_product(Ms[b].astype(np.float64), Ns[b].astype(np.float64), sizes, W, method,
+                               np.random.default_rng(5000 + b))
+        assert np.array_equal(fused.budgets_host()[b], ref["budgets"]), b
+        assert np.array_equal(fused.columns_host()[b], ref["columns"]), b
+        assert np.array_equal(fused.scales_host()[b], ref["scale"]), b
