@@ -266,6 +266,18 @@ int bmm_gemm_f64_gather(const double* M, int64_t ldm, int64_t strideM,
                         double* out, int64_t ldo, int64_t strideO,
                         void* ws, int64_t ws_bytes, void* stream);
 
+/* K9, the fused error epilogue (SURVEY.md §8 b2 `err_sq_out_opt`; relative_error,
+ * analysis.py:318-325, as coverage_check uses it, analysis.py:343-380): C @ D as bmm_gemm_f64
+ * with err_sq[b] = || ref_b - A_b B_b ||_F^2 taken from the accumulator tiles (or the ordered
+ * split-K reduction), ref_b = ref + b * strideR (strideR = 0: one exact product for every
+ * replication).  out_opt == NULL: the product is never written to HBM.  Deterministic (fixed
+ * thread, warp and tile order).                                                            */
+int64_t bmm_gemm_f64_err_workspace(int64_t m, int64_t nc, int64_t k, int64_t batch);
+int bmm_gemm_f64_err(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                     int64_t strideB, int64_t m, int64_t nc, int64_t k, int64_t batch,
+                     const double* ref, int64_t ldr, int64_t strideR, double* out_opt, int64_t ldo,
+                     int64_t strideO, double* err_sq, void* ws, int64_t ws_bytes, void* stream);
+
 /* bmm_gemm_f64 with the inner length read from the device (k_dev[b] <= k_max,
  * e.g. bmm_compress_sketch's count): the split-K plan is re-made on the device
  * for the actual length, so a shorter K costs proportionally less.  Workspace:

@@ -216,6 +216,18 @@ __device__ __forceinline__ void mainloop(const TileArgs& ta, int64_t kbeg, int64
   __syncthreads();
 }
 
+// K9 -- fused error epilogue (SURVEY.md §8 b2 `err_sq_out_opt`; relative_error,
+// analysis.py:318-325): with a reference product `ref` (the exact M @ N) the tile's
+// sum of (ref - acc)^2 is taken straight from the accumulator registers (or, under
+// split-K, in the ordered split reduction) and written as one partial per tile; the
+// product itself need not be stored.  Fixed thread / warp / tile order: deterministic.
+struct ErrEpi {
+  const double* ref = nullptr;  // batch stride strideR (0: one reference for every problem)
+  int64_t ldr = 0, strideR = 0;
+  double* part = nullptr;       // batch x parts partial sums
+  int write_out = 1;
+};
+
 // split-K plan for an inner length known only on the device (compressed sketch):
 // the host rule of plan_split (>= 4 k-tiles per split) capped at the launched splits
 __device__ __forceinline__ void device_split(int64_t k, int64_t smax, int bk, int64_t& splits, int64_t& kchunk) {
@@ -236,7 +248,8 @@ __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __re
                                                               int64_t strideO, double* __restrict__ part,
                                                               const int64_t* __restrict__ col,
                                                               const double* __restrict__ scale, int64_t w_stride,
-                                                              const int64_t* __restrict__ kdev = nullptr) {
+                                                              const int64_t* __restrict__ kdev = nullptr,
+                                                              const ErrEpi err = ErrEpi{}) {
   extern __shared__ __align__(16) double smem[];
   const int64_t z = blockIdx.z;
   const int64_t b = z / splits, sp = z - b * splits;
@@ -263,6 +276,34 @@ __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __re
   if (kbeg < kend) mainloop<C, V16, G, SQ>(ta, kbeg, kend, smem, acc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N, g = lane >> 2, t = lane & 3;
+  if constexpr (!G && !SQ) {
+    if (err.ref != nullptr && splits == 1) {
+      // sum of (ref - acc)^2 over the tile: thread order, warp butterfly, warps in order
+      const double* rb = err.ref + b * err.strideR;
+      double se = 0.0;
+#pragma unroll
+      for (int mi = 0; mi < C::FM; ++mi) {
+        const int64_t r = ta.m0 + wm * C::WM + mi * 8 + g;
+#pragma unroll
+        for (int ni = 0; ni < C::FN; ++ni) {
+          const int64_t c0 = ta.n0 + wn * C::WN + ni * 8 + 2 * t;
+          if (r < m && c0 < nc) { const double d = rb[r * err.ldr + c0] - acc[mi][ni][0]; se = fma(d, d, se); }
+          if (r < m && c0 + 1 < nc) { const double d = rb[r * err.ldr + c0 + 1] - acc[mi][ni][1]; se = fma(d, d, se); }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+      if (lane == 0) smem[warp] = se;  // the mainloop's stages are drained (its closing barrier)
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int w = 0; w < C::THREADS / 32; ++w) a += smem[w];
+        const int64_t tiles = (int64_t)gridDim.x * gridDim.y;
+        err.part[b * tiles + (int64_t)blockIdx.y * gridDim.x + blockIdx.x] = a;
+      }
+      if (!err.write_out) return;
+    }
+  }
   double* dst;
   int64_t ld;
   if (splits == 1) { dst = out + b * strideO; ld = ldo; }
@@ -277,6 +318,49 @@ __global__ void __launch_bounds__(C::THREADS) gemm_f64_kernel(const double* __re
       if (c0 < nc) dst[r * ld + c0] = acc[mi][ni][0];
       if (c0 + 1 < nc) dst[r * ld + c0 + 1] = acc[mi][ni][1];
     }
+  }
+}
+
+// split-K form of the error epilogue: CTA c of problem b sums its chunk of elements over the
+// splits in split order, squares the difference to the reference and writes one partial
+constexpr int ERR_THREADS = 256;
+__global__ void __launch_bounds__(ERR_THREADS) splitk_reduce_err_kernel(
+    const double* __restrict__ part, int64_t splits, int64_t m, int64_t nc, int64_t parts, double* __restrict__ out,
+    int64_t ldo, int64_t strideO, const ErrEpi err) {
+  __shared__ double red[ERR_THREADS / 32];
+  const int64_t b = blockIdx.y, c = blockIdx.x;
+  const int64_t per = m * nc;
+  const int64_t chunk = (per + parts - 1) / parts;
+  const int64_t e0 = c * chunk, e1 = min(per, e0 + chunk);
+  const double* rb = err.ref + b * err.strideR;
+  double se = 0.0;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += ERR_THREADS) {
+    const double* p = part + b * splits * per + e;
+    double acc = p[0];
+    for (int64_t s = 1; s < splits; ++s) acc = __dadd_rn(acc, p[s * per]);
+    const int64_t r = e / nc, col = e - r * nc;
+    if (err.write_out) out[b * strideO + r * ldo + col] = acc;
+    const double d = rb[r * err.ldr + col] - acc;
+    se = fma(d, d, se);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = se;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int w = 0; w < ERR_THREADS / 32; ++w) a += red[w];
+    err.part[b * parts + c] = a;
+  }
+}
+
+__global__ void err_final_kernel(const double* __restrict__ part, int64_t parts, int64_t batch,
+                                 double* __restrict__ err_sq) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int64_t c = 0; c < parts; ++c) a += part[b * parts + c];
+    err_sq[b] = a;
   }
 }
 
@@ -628,7 +712,7 @@ static void launch_gemm(bool v16, dim3 grid, cudaStream_t st, const double* A, i
                         const double* B, int64_t ldb, int64_t strideB, int64_t m, int64_t nc, int64_t k,
                         const SplitPlan& sp, double* out, int64_t ldo, int64_t strideO, double* part,
                         const int64_t* col = nullptr, const double* scale = nullptr, int64_t w_stride = 0,
-                        const int64_t* kdev = nullptr) {
+                        const int64_t* kdev = nullptr, const ErrEpi err = ErrEpi{}) {
   if (col != nullptr) {
     static bool attr = false;
     if (!attr) {
@@ -649,11 +733,11 @@ static void launch_gemm(bool v16, dim3 grid, cudaStream_t st, const double* A, i
   if (v16)
     gemm_f64_kernel<C, true><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k, sp.splits,
                                                                sp.kchunk, out, ldo, strideO, part, nullptr, nullptr, 0,
-                                                               kdev);
+                                                               kdev, err);
   else
     gemm_f64_kernel<C, false><<<grid, C::THREADS, C::SMEM, st>>>(A, lda, strideA, B, ldb, strideB, m, nc, k, sp.splits,
                                                                 sp.kchunk, out, ldo, strideO, part, nullptr, nullptr, 0,
-                                                                kdev);
+                                                                kdev, err);
 }
 
 template <class C>
@@ -715,7 +799,8 @@ extern "C" int64_t bmm_gemm_f64_workspace(int64_t m, int64_t nc, int64_t k, int6
 static int gemm_impl(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb, int64_t strideB,
                      int64_t m, int64_t nc, int64_t k, int64_t batch, double* out, int64_t ldo, int64_t strideO,
                      void* ws, int64_t ws_bytes, cudaStream_t st, const int64_t* col, const double* scale,
-                     int64_t w_stride, const int64_t* kdev = nullptr) {
+                     int64_t w_stride, const int64_t* kdev = nullptr, ErrEpi err = ErrEpi{},
+                     double* err_sq = nullptr) {
   if (m == 0 || nc == 0) return BMM_OK;
   if (k == 0) {
     for (int64_t b = 0; b < batch; ++b)
@@ -728,7 +813,14 @@ static int gemm_impl(const double* A, int64_t lda, int64_t strideA, const double
   const int variant = pick_variant(m, nc);
   const VariantInfo vi = variant_info(variant);
   SplitPlan sp = plan_split(vi, m, nc, k, batch);
-  const int64_t need = sp.splits > 1 ? sp.splits * batch * m * nc * 8 : 0;
+  int64_t need = sp.splits > 1 ? sp.splits * batch * m * nc * 8 : 0;
+  int64_t err_parts = 0;
+  if (err.ref != nullptr) {
+    // one partial per tile (fused epilogue) or per reduction CTA (split-K), after the split partials
+    err_parts = sp.splits > 1 ? sq_parts(m, nc, batch) : ceil_div(m, vi.BM) * ceil_div(nc, vi.BN);
+    err.part = (double*)((char*)ws + need);
+    need += batch * err_parts * 8;
+  }
   BMM_REQUIRE(ws_bytes >= need && (need == 0 || ws != nullptr), BMM_E_ARG,
               "bmm_gemm_f64: workspace too small (%lld < %lld)", (long long)ws_bytes, (long long)need);
   BMM_REQUIRE(ceil_div(m, vi.BM) <= 65535, BMM_E_UNSUPPORTED, "bmm_gemm_f64: m too large");
@@ -739,7 +831,7 @@ static int gemm_impl(const double* A, int64_t lda, int64_t strideA, const double
   double* part = (double*)ws;
 #define BMM_GEMM_CASE(V)                                                                                       \
   launch_gemm<V>(v16, grid, st, A, lda, strideA, B, ldb, strideB, m, nc, k, sp, out, ldo, strideO, part, col, \
-                 scale, w_stride, kdev)
+                 scale, w_stride, kdev, err)
   switch (variant) {
     case 1: BMM_GEMM_CASE(DV1); break;
     case 2: BMM_GEMM_CASE(DV2); break;
@@ -752,12 +844,43 @@ static int gemm_impl(const double* A, int64_t lda, int64_t strideA, const double
   }
 #undef BMM_GEMM_CASE
   BMM_CHECK_LAUNCH("gemm_f64_kernel");
-  if (sp.splits > 1) {
+  if (sp.splits > 1 && err.ref != nullptr) {
+    dim3 rgrid((unsigned)err_parts, (unsigned)batch);
+    splitk_reduce_err_kernel<<<rgrid, ERR_THREADS, 0, st>>>((const double*)ws, sp.splits, m, nc, err_parts, out, ldo,
+                                                            strideO, err);
+    BMM_CHECK_LAUNCH("splitk_reduce_err_kernel");
+  } else if (sp.splits > 1) {
     splitk_reduce_kernel<<<grid_for(m * nc * batch, 256), 256, 0, st>>>((const double*)ws, sp.splits, m, nc,
                                                                         batch, out, ldo, strideO, kdev, vi.BK);
     BMM_CHECK_LAUNCH("splitk_reduce_kernel");
   }
+  if (err.ref != nullptr) {
+    err_final_kernel<<<grid_for(batch, 128), 128, 0, st>>>(err.part, err_parts, batch, err_sq);
+    BMM_CHECK_LAUNCH("err_final_kernel");
+  }
   return BMM_OK;
+}
+
+extern "C" int64_t bmm_gemm_f64_err_workspace(int64_t m, int64_t nc, int64_t k, int64_t batch) {
+  const VariantInfo vi = variant_info(pick_variant(m, nc));
+  SplitPlan sp = plan_split(vi, m, nc, k, batch);
+  const int64_t parts = sp.splits > 1 ? sq_parts(m, nc, batch) : ceil_div(m, vi.BM) * ceil_div(nc, vi.BN);
+  return (sp.splits > 1 ? sp.splits * batch * m * nc * 8 : 0) + batch * parts * 8 + 256;
+}
+
+extern "C" int bmm_gemm_f64_err(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                                int64_t strideB, int64_t m, int64_t nc, int64_t k, int64_t batch, const double* ref,
+                                int64_t ldr, int64_t strideR, double* out_opt, int64_t ldo, int64_t strideO,
+                                double* err_sq, void* ws, int64_t ws_bytes, void* stream) {
+  BMM_REQUIRE(m >= 1 && nc >= 1 && k >= 1 && batch >= 1, BMM_E_ARG, "bmm_gemm_f64_err: bad shape");
+  BMM_REQUIRE(ref != nullptr && err_sq != nullptr && ldr >= nc, BMM_E_ARG, "bmm_gemm_f64_err: reference and output required");
+  ErrEpi err;
+  err.ref = ref;
+  err.ldr = ldr;
+  err.strideR = strideR;
+  err.write_out = out_opt != nullptr ? 1 : 0;
+  return gemm_impl(A, lda, strideA, B, ldb, strideB, m, nc, k, batch, out_opt, ldo, strideO, ws, ws_bytes,
+                   as_stream(stream), nullptr, nullptr, 0, nullptr, err, err_sq);
 }
 
 extern "C" int bmm_gemm_f64(const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,

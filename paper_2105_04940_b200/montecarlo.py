@@ -141,9 +141,9 @@ class ReplicationEngine:
         CD = torch.empty(R * m * p, dtype=torch.float64, device=dev)
         first_d = torch.zeros(R, dtype=torch.int64, device=dev)
         lib = _lib.load()
-        ws_g = _lib.workspace(lib.bmm_gemm_f64_workspace(m, p, W, R))
-        ws_e = _lib.workspace(lib.bmm_sqdiff_workspace(m, p, R))
-        err = torch.empty(2 * R, dtype=torch.float64, device=dev)
+        ws_g = _lib.workspace(max(lib.bmm_gemm_f64_workspace(m, p, W, R), lib.bmm_gemm_f64_err_workspace(m, p, W, R)))
+        err = torch.empty(R, dtype=torch.float64, device=dev)
+        need_cd = entry is not None  # the products themselves are only read for the entry diagnostic
         exact = self.exact if sq_errors else None
         dt = _lib.matrix_dtype(inst.M)
         st = _lib.stream_ptr()
@@ -159,12 +159,15 @@ class ReplicationEngine:
             _lib.call("bmm_gather", dt, _lib.BMM_F64, _lib.ptr(inst.M), inst.M.stride(0), 0, _lib.ptr(inst.N),
                       inst.N.stride(0), 0, m, p, _lib.ptr(column), _lib.ptr(scale), W, W, Rc, _lib.ptr(C), W, m * W,
                       _lib.ptr(D), p, W * p, st)
-            _lib.call("bmm_gemm_f64", _lib.ptr(C), W, m * W, _lib.ptr(D), p, W * p, m, p, W, Rc, _lib.ptr(CD), p,
-                      m * p, _lib.ptr(ws_g), ws_g.numel(), st)
             if sq_errors:
-                _lib.call("bmm_sqdiff", _lib.BMM_F64, _lib.ptr(CD), p, m * p, _lib.ptr(exact), p, 0, m, p, Rc,
-                          _lib.ptr(err), _lib.ptr(ws_e), ws_e.numel(), st)
-                out["sq_error"][r0:r0 + Rc] = err[0:2 * Rc:2]
+                # K9: ||C_r D_r - MN||_F^2 in the contraction's epilogue; C_r D_r stays on chip
+                _lib.call("bmm_gemm_f64_err", _lib.ptr(C), W, m * W, _lib.ptr(D), p, W * p, m, p, W, Rc,
+                          _lib.ptr(exact), exact.stride(0), 0, _lib.ptr(CD) if need_cd else None, p, m * p,
+                          _lib.ptr(err), _lib.ptr(ws_g), ws_g.numel(), st)
+                out["sq_error"][r0:r0 + Rc] = err[:Rc]
+            else:
+                _lib.call("bmm_gemm_f64", _lib.ptr(C), W, m * W, _lib.ptr(D), p, W * p, m, p, W, Rc, _lib.ptr(CD), p,
+                          m * p, _lib.ptr(ws_g), ws_g.numel(), st)
             if entry is not None:
                 out["entry"][r0:r0 + Rc] = CD.view(R, m, p)[:Rc, h, f]
             if keep_columns:

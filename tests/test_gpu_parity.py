@@ -369,6 +369,42 @@ def test_block_scores_and_relative_error():
     assert abs(bm.relative_error(Bm, A) - np.sqrt(e) / np.sqrt(r)) < 1e-14
 
 
+@pytest.mark.parametrize("m,k,n,batch,shared_ref", [(200, 2000, 200, 7, True), (40, 64, 40, 33, False),
+                                                    (65, 17, 63, 3, True), (130, 30000, 257, 1, False),
+                                                    (500, 4001, 500, 2, True)])
+def test_fused_error_epilogue(m, k, n, batch, shared_ref):
+    """K9 (bmm_gemm_f64_err): ||ref - A B||_F^2 from the contraction's epilogue (single-pass
+    tiles and split-K), with and without writing the product -- against NumPy (1e-12) and the
+    plain contraction (the written product is bit-identical, the error sums equal)."""
+    import torch
+    from paper_2105_04940_b200 import _lib
+    g = np.random.default_rng(m + k + n + batch)
+    A, B = g.standard_normal((batch, m, k)), g.standard_normal((batch, k, n))
+    exact = A @ B
+    ref = (exact[0] if shared_ref else exact) + 1e-3 * g.standard_normal((m, n) if shared_ref else (batch, m, n))
+    want = np.array([np.sum(((ref if shared_ref else ref[b]) - exact[b]) ** 2) for b in range(batch)])
+    Ad, Bd, Rd = _lib.f64(A), _lib.f64(B), _lib.f64(ref)
+    lib = _lib.load()
+    ws = _lib.workspace(max(lib.bmm_gemm_f64_err_workspace(m, n, k, batch), lib.bmm_gemm_f64_workspace(m, n, k, batch)))
+    plain = torch.empty((batch, m, n), dtype=torch.float64, device="cuda")
+    _lib.call("bmm_gemm_f64", _lib.ptr(Ad), k, m * k, _lib.ptr(Bd), n, k * n, m, n, k, batch, _lib.ptr(plain), n, m * n,
+              _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    errs = []
+    for write in (True, False):
+        out = torch.full((batch, m, n), -7.0, dtype=torch.float64, device="cuda")
+        err = torch.empty(batch, dtype=torch.float64, device="cuda")
+        _lib.call("bmm_gemm_f64_err", _lib.ptr(Ad), k, m * k, _lib.ptr(Bd), n, k * n, m, n, k, batch, _lib.ptr(Rd), n,
+                  0 if shared_ref else m * n, _lib.ptr(out) if write else None, n, m * n, _lib.ptr(err), _lib.ptr(ws),
+                  ws.numel(), _lib.stream_ptr())
+        if write:
+            assert torch.equal(out, plain)
+        else:
+            assert bool((out == -7.0).all())  # the product is never stored
+        errs.append(err.cpu().numpy())
+        np.testing.assert_allclose(errs[-1], want, rtol=1e-9)
+    assert np.array_equal(errs[0], errs[1])
+
+
 def test_fused_gather_kernels_match_materialised_sketch():
     """bmm_gemm_f64_gather / bmm_segsq_f64_gather == gather + GEMM / segsq (float64 rounding level)."""
     import torch
