@@ -203,7 +203,7 @@ def to_device(x, dtype=None) -> torch.Tensor:
             t = t.to(dev, non_blocking=True)
     else:
         a = np.asarray(x)
-        t = torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=False)
+        t = _upload(np.ascontiguousarray(a))
     if dtype is not None and t.dtype != dtype:
         t = t.to(dtype)
     if not t.is_contiguous():
@@ -239,8 +239,97 @@ def f64(values) -> torch.Tensor:
     return torch.as_tensor(np.ascontiguousarray(values, dtype=np.float64), device=device())
 
 
+# ---- large host <-> device transfers of the drop-in API (numpy in, numpy out): pageable
+# memory moves through two pinned staging buffers, the PCIe copy of one chunk overlapping the
+# host-side memcpy of the other (4 threads; first-touch page faults of a fresh result array
+# are what bound a plain `.cpu()`: config 4's C and D, 4.3 GB each).  Measured on the B200 box
+# (tools/host_copy_probe.py, profiles/r2be_host_copy_probe.txt): plain copies are as fast up to
+# 32 MB and fall to 2.2 GB/s (D2H) / 11 GB/s (H2D) from 64 MB on; staged 23 / 41 GB/s at 4.3 GB.
+_BIG = 48 << 20
+_CHUNK = 64 << 20
+_stage = None
+
+
+def _staging():
+    global _stage
+    if _stage is None:
+        from concurrent.futures import ThreadPoolExecutor
+        workers = max(2, min(8, (os.cpu_count() or 4) // 2))
+        _stage = {"pin": [torch.empty(_CHUNK, dtype=torch.uint8).pin_memory() for _ in range(2)],
+                  "stream": torch.cuda.Stream(), "pool": ThreadPoolExecutor(max_workers=workers), "workers": workers}
+    return _stage
+
+
+def _par_copy(pool, dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[:] = src (flat uint8 views) on the pool's threads (numpy releases the GIL)."""
+    n = dst.size
+    parts = _stage["workers"]
+    step = max(1, -(-n // parts))
+    futs = [pool.submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, n, step)]
+    for f in futs:
+        f.result()
+
+
 def host(t: torch.Tensor) -> np.ndarray:
-    return t.detach().cpu().numpy()
+    t = t.detach()
+    nbytes = t.numel() * t.element_size()
+    if t.device.type != "cuda" or nbytes < _BIG or not t.is_contiguous():
+        return t.cpu().numpy()
+    sg = _staging()
+    out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    dst = out.reshape(-1).view(np.uint8)
+    src = t.reshape(-1).view(torch.uint8)
+    cs = sg["stream"]
+    cs.wait_stream(torch.cuda.current_stream())
+    pend = None  # (event, offset, length, buffer index) of the chunk in flight
+    for i, off in enumerate(range(0, nbytes, _CHUNK)):
+        ln = min(_CHUNK, nbytes - off)
+        buf = sg["pin"][i & 1]
+        with torch.cuda.stream(cs):
+            buf[:ln].copy_(src[off:off + ln], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        if pend is not None:
+            pev, poff, pln, pi = pend
+            pev.synchronize()
+            _par_copy(sg["pool"], dst[poff:poff + pln], sg["pin"][pi].numpy()[:pln])
+        pend = (ev, off, ln, i & 1)
+    pev, poff, pln, pi = pend
+    pev.synchronize()
+    _par_copy(sg["pool"], dst[poff:poff + pln], sg["pin"][pi].numpy()[:pln])
+    return out
+
+
+def _upload(a: np.ndarray) -> torch.Tensor:
+    """Contiguous numpy array -> CUDA tensor; large pageable arrays through the staging buffers."""
+    dev = device()
+    nbytes = a.nbytes
+    th = torch.from_numpy(a)
+    if nbytes < _BIG or th.is_pinned():
+        return th.to(dev, non_blocking=False)
+    sg = _staging()
+    out = torch.empty(a.shape, dtype=th.dtype, device=dev)
+    dst = out.reshape(-1).view(torch.uint8)
+    src = a.reshape(-1).view(np.uint8)
+    cs = sg["stream"]
+    cs.wait_stream(torch.cuda.current_stream())
+    evs = [None, None]
+    for i, off in enumerate(range(0, nbytes, _CHUNK)):
+        ln = min(_CHUNK, nbytes - off)
+        if evs[i & 1] is not None:
+            evs[i & 1].synchronize()  # the buffer's previous chunk has left for the device
+        buf = sg["pin"][i & 1]
+        _par_copy(sg["pool"], buf.numpy()[:ln], src[off:off + ln])
+        with torch.cuda.stream(cs):
+            dst[off:off + ln].copy_(buf[:ln], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        evs[i & 1] = ev
+    torch.cuda.current_stream().wait_stream(cs)
+    for ev in evs:
+        if ev is not None:
+            ev.synchronize()
+    return out
 
 
 def want_numpy(*xs) -> bool:

@@ -966,7 +966,7 @@ __device__ __forceinline__ void sts128(uint8_t* p, uint32_t a, uint32_t b, uint3
   *reinterpret_cast<uint4*>(p) = make_uint4(a, b, c, d);
 }
 
-__global__ void __maxnreg__(152) gemm_f32split_gather_kernel(
+__global__ void __launch_bounds__(32 * FG_WARPS, 1) gemm_f32split_gather_kernel(
     const float* __restrict__ M, int64_t ldm, int64_t strideM, const float* __restrict__ N, int64_t ldn,
     int64_t strideN, int64_t m, int64_t nc, const int64_t* __restrict__ column, const double* __restrict__ scale,
     int64_t W, int64_t w_stride, const int64_t* __restrict__ count, float* __restrict__ out, int64_t ldo,

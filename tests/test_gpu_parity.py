@@ -472,3 +472,24 @@ def test_optimal_size_weights_and_real_budgets(case):
     assert rel(w, w_ref) < 1e-12
     r = bm.real_optimal_budgets(M, N, part, 40)
     assert abs(r.sum() - 40) < 1e-9 and rel(r, 40 * w_ref / w_ref.sum()) < 1e-12
+
+
+def test_staged_host_transfers_round_trip(monkeypatch):
+    """Large numpy <-> device transfers of the drop-in API go through two pinned staging
+    buffers with a threaded memcpy (_lib._upload / _lib.host): exact round trips for sizes
+    that are not multiples of the chunk, every dtype the API moves."""
+    import torch
+    from paper_2105_04940_b200 import _lib
+    monkeypatch.setattr(_lib, "_BIG", 1 << 20)
+    monkeypatch.setattr(_lib, "_CHUNK", 300_000)
+    g = np.random.default_rng(9)
+    for shape, dt in (((1031, 517), np.float64), ((777, 1213), np.float32), ((400_003,), np.int64)):
+        a = (g.standard_normal(shape) * 1000).astype(dt)
+        d = _lib.to_device(a)
+        assert d.is_cuda and tuple(d.shape) == shape and np.array_equal(d.cpu().numpy(), a)
+        back = _lib.host(d)
+        assert back.dtype == a.dtype and back.shape == a.shape and np.array_equal(back, a)
+    small = g.standard_normal((10, 10))
+    assert np.array_equal(_lib.host(_lib.to_device(small)), small)
+    pinned = torch.from_numpy(g.standard_normal((600, 600))).pin_memory()
+    assert torch.equal(_lib.to_device(pinned.numpy()).cpu(), pinned)
