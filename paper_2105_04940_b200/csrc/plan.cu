@@ -881,22 +881,26 @@ __global__ void __launch_bounds__(kPlanThreads, 4) plan_small_kernel(const PlanS
       for (int64_t i = j; i < nk; i += 8) probs_b[o + i] = buf[i];
       __syncwarp(gmask);
       if (k == 0) stamp(11);
-      if (j == 0) {
-        double acc = 0.0;
-        int64_t lst = -1;
-        for (int64_t i = 0; i < nk; ++i) {
-          const double x = buf[i];
-          acc = __dadd_rn(acc, x);
-          buf[i] = acc;
-          if (x > 0.0) lst = i;
-        }
-        s_last[k] = lst;
-        if (a.last != nullptr) a.last[b * K + k] = lst;
-      }
-      if (k == 0) stamp(12);
     }
-    if (tid == 0) stamp(13);
+    if (tid == 0) stamp(12);
   }
+  __syncthreads();
+  // the CDF in place, one lane per block: np.cumsum is a sequential chain (estimators.py:37-38)
+  for (int64_t k = tid; k < K; k += NT) {
+    const int64_t o = s_off[k], nk = s_off[k + 1] - o;
+    double* buf = sc + o + k;
+    double acc = 0.0;
+    int64_t lst = -1;
+    for (int64_t i = 0; i < nk; ++i) {
+      const double x = buf[i];
+      acc = __dadd_rn(acc, x);
+      buf[i] = acc;
+      if (x > 0.0) lst = i;
+    }
+    s_last[k] = lst;
+    if (a.last != nullptr) a.last[b * K + k] = lst;
+  }
+  if (tid == 0) stamp(13);
   __syncthreads();
   stamp(1);
   if (a.cum != nullptr) {
@@ -931,42 +935,11 @@ __global__ void __launch_bounds__(kPlanThreads, 4) plan_small_kernel(const PlanS
   }
   __syncthreads();
   stamp(4);
-  // ---- draws: L threads per block, thread `sub` takes draws sub, sub + L, ... of the block's
-  // stream (PCG64 jump-ahead), inverse CDF by binary search        estimators.py:34-44,78
-  {
-    const int64_t L = K >= NT ? 1 : NT / K;
-    for (int64_t unit = tid; unit < K * L; unit += NT) {
-      const int64_t k = unit / L, sub = unit - k * L;
-      const int64_t ck = s_bud[k];
-      if (ck <= sub) continue;
-      const int64_t o = s_off[k], len = s_off[k + 1] - o, lst = s_last[k];
-      const double* cb = sc + o + k;
-      U128 st{s_state[4 * k], s_state[4 * k + 1]};
-      const U128 inc{s_state[4 * k + 2], s_state[4 * k + 3]};
-      U128 am, ap, jm{0, 1}, jp{0, 0};
-      pcg_jump((uint64_t)(sub + 1), inc, am, ap);
-      st = add128(mul128(st, am), ap);  // the state draw `sub` reads
-      if (L > 1) pcg_jump((uint64_t)L, inc, jm, jp);
-      const int64_t t0 = s_col[k];
-      for (int64_t j = sub; j < ck; j += L) {
-        const double u = u53(pcg_output(st));
-        int64_t lo = 0, hi = len;  // first index with cum > u (searchsorted side="right")
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (cb[mid] > u) hi = mid; else lo = mid + 1;
-        }
-        const int64_t idx = max((int64_t)0, lo < lst ? lo : lst);
-        const int64_t col = o + idx;
-        a.column[b * W + t0 + j] = col;
-        s_draw[t0 + j] = (uint16_t)col;
-        atomicAdd(&cnt[col >> 1], 1u << (16 * (int)(col & 1)));
-        st = (L > 1) ? add128(mul128(st, jm), jp) : pcg_step(st, inc);
-      }
-    }
-  }
-  __syncthreads();
-  // the drawn columns' probabilities and scales 1 / sqrt(c_k p_i) (estimators.py:78), four
-  // sketch slots per step so the probability loads (L2) and the square roots overlap
+  // ---- draws, flat over the sketch slots: slot t is draw j = t - s_col[k] of block k; its
+  // stream state is j + 1 steps ahead of the child's seed (pcg_ahead: two 128-bit multiplies
+  // from the jump table), inverse CDF by binary search, scale 1 / sqrt(c_k p_i)
+  // (estimators.py:34-44, 78).  Four slots per step: their searches, probability loads (L2)
+  // and square roots overlap.
   {
     auto block_of_slot = [&](int64_t t) {  // the last k with s_col[k] <= t (empty blocks skipped)
       int64_t lo = 0, hi = K;
@@ -978,20 +951,40 @@ __global__ void __launch_bounds__(kPlanThreads, 4) plan_small_kernel(const PlanS
     };
     const int64_t drawn = s_col[K];
     for (int64_t t0 = tid; t0 < drawn; t0 += 4 * NT) {
-      double pr[4], dck[4];
+      int64_t col[4];
+      double dck[4], pr[4], sv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t t = t0 + u * NT;
-        pr[u] = t < drawn ? probs_b[s_draw[t]] : 1.0;
-        dck[u] = t < drawn ? (double)s_bud[block_of_slot(t)] : 1.0;
+        col[u] = 0;
+        dck[u] = 1.0;
+        if (t < drawn) {
+          const int64_t k = block_of_slot(t);
+          const int64_t o = s_off[k], len = s_off[k + 1] - o, lst = s_last[k];
+          const double* cb = sc + o + k;
+          const U128 st = pcg_ahead(U128{s_state[4 * k], s_state[4 * k + 1]},
+                                    U128{s_state[4 * k + 2], s_state[4 * k + 3]}, (uint64_t)(t - s_col[k] + 1));
+          const double uu = u53(pcg_output(st));
+          int64_t lo = 0, hi = len;  // first index with cum > u (searchsorted side="right")
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (cb[mid] > uu) hi = mid; else lo = mid + 1;
+          }
+          const int64_t idx = max((int64_t)0, lo < lst ? lo : lst);
+          col[u] = o + idx;
+          dck[u] = (double)s_bud[k];
+          atomicAdd(&cnt[col[u] >> 1], 1u << (16 * (int)(col[u] & 1)));
+        }
       }
-      double sv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) pr[u] = (t0 + u * NT < drawn) ? probs_b[col[u]] : 1.0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) sv[u] = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dck[u], pr[u])));
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t t = t0 + u * NT;
         if (t < drawn) {
+          a.column[b * W + t] = col[u];
           a.prob[b * W + t] = pr[u];
           a.scale[b * W + t] = sv[u];
         }

@@ -63,6 +63,55 @@ __device__ __forceinline__ void pcg_jump(uint64_t delta, U128 inc, U128& am, U12
   ap = acc_p;
 }
 
+// ---- PCG64 jump table: the state i steps ahead is a^i * s + inc * S_i (mod 2^128) with
+// S_i = 1 + a + ... + a^(i-1) independent of the stream, so a draw's state costs two 128-bit
+// multiplies instead of pcg_jump's O(log i) loop.  Constant-initialised at compile time.
+struct U128c {
+  uint64_t hi, lo;
+};
+
+constexpr U128c mul128c(U128c a, U128c b) {
+  const uint64_t a0 = a.lo & 0xffffffffULL, a1 = a.lo >> 32, b0 = b.lo & 0xffffffffULL, b1 = b.lo >> 32;
+  const uint64_t p00 = a0 * b0, p01 = a0 * b1, p10 = a1 * b0, p11 = a1 * b1;
+  const uint64_t mid = (p00 >> 32) + (p01 & 0xffffffffULL) + (p10 & 0xffffffffULL);
+  const uint64_t lo = (p00 & 0xffffffffULL) | (mid << 32);
+  const uint64_t hi = p11 + (p01 >> 32) + (p10 >> 32) + (mid >> 32) + a.lo * b.hi + a.hi * b.lo;
+  return U128c{hi, lo};
+}
+
+constexpr int kPcgTable = 1024;
+
+struct PcgTable {
+  uint64_t v[kPcgTable + 1][4];  // a^i (hi, lo), S_i (hi, lo)
+  constexpr PcgTable() : v{} {
+    const U128c a{0x2360ED051FC65DA4ULL, 0x4385DF649FCCF645ULL};
+    U128c am{0, 1}, S{0, 0};
+    for (int i = 0; i <= kPcgTable; ++i) {
+      v[i][0] = am.hi;
+      v[i][1] = am.lo;
+      v[i][2] = S.hi;
+      v[i][3] = S.lo;
+      S = mul128c(S, a);
+      S.lo += 1;
+      if (S.lo == 0) S.hi += 1;
+      am = mul128c(am, a);
+    }
+  }
+};
+
+__device__ constexpr PcgTable kPcgAhead{};
+
+// the state `steps` >= 0 ahead of `state` on the stream with increment `inc`
+__device__ __forceinline__ U128 pcg_ahead(U128 state, U128 inc, uint64_t steps) {
+  if (steps <= (uint64_t)kPcgTable) {
+    const uint64_t* e = kPcgAhead.v[steps];
+    return add128(mul128(state, U128{e[0], e[1]}), mul128(inc, U128{e[2], e[3]}));
+  }
+  U128 am, ap;
+  pcg_jump(steps, inc, am, ap);
+  return add128(mul128(state, am), ap);
+}
+
 // ---- SeedSequence (pool_size 4)
 constexpr uint32_t kInitA = 0x43b0d7e5u, kMultA = 0x931e8875u;
 constexpr uint32_t kInitB = 0x8b51f9ddu, kMultB = 0x58f38dedu;

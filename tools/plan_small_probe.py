@@ -44,7 +44,7 @@ def main():
     for i in range(7):
         print(f"{names[i]:18s} median {np.median(d[:, i]):9.0f} clk   p90 {np.percentile(d[:, i], 90):9.0f}")
     # inside the first stage, block 0's group: stamps 8..13 after the stage's start (stamp 0)
-    fine = ["setup+loads+scores", "two sums", "normalise x2 + sum", "probs write", "cdf chain", "other rounds"]
+    fine = ["setup+loads+scores", "two sums", "normalise x2 + sum", "probs write", "other rounds", "cdf chains"]
     prev = t[:, 0]
     for i, nm in zip(range(8, 14), fine):
         print(f"  {nm:18s} median {np.median(t[:, i] - prev):9.0f} clk")
