@@ -503,21 +503,20 @@ __global__ void __launch_bounds__(32 * P_WARPS, 1) gemm_f32split_2sm_kernel(
   }
 }
 
-// ---- F16 split, CTA pairs (round 2): C (fp16 h, [h|l] pairs) . D^T (fp16 h,
-// [l|h] pairs), operands scaled by the balanced exponents and the problem's
-// shift (bmm_balance_f16).  Per 16 K-elements: one kind::f16 MMA for h.h (K=16)
-// and two for the cross terms on pairs (K=16 over 8 elements each) -- three
-// tensor instructions where the TF32 form needs four -- and 6 operand bytes per
-// element instead of 8.  Stage = 64 K: A_h (1 SWIZZLE_128B tile of 128 rows x
-// 64 fp16), A_x (2 tiles: pairs of elements 0-31 and 32-63), B_h, B_x likewise:
-// 96 KB per CTA, 2 stages; accumulators promoted every 128 K as above.
+// ---- F16 split, CTA pairs (round 2): C = h + l (two fp16 arrays) . D^T = h' + l',
+// operands scaled by the balanced exponents and the problem's shift
+// (bmm_balance_f16).  Per 16 K-elements three kind::f16 MMAs, h.h' + h.l' + l.h'
+// (the TF32 form needs four tensor instructions) on 4 operand bytes per element
+// (8 there; 6 in the first version, which kept the cross terms as [h|l].[l|h]
+// pair tiles).  Stage = 64 K: A_h, A_l, B_h, B_l, one SWIZZLE_128B tile of 128 rows
+// x 64 fp16 each: 64 KB per CTA, 3 stages; accumulators promoted every 128 K.
 // power of two 2^k as a float (|k| <= 126)
 __device__ __forceinline__ float pow2f(int k) { return __int_as_float((127 + k) << 23); }
 
 constexpr int H_BK = 64;
 constexpr int H_TILE = 128 * 128;  // 16 KB
-constexpr int H_STAGES = 2;
-constexpr int H_STAGE = 6 * H_TILE;
+constexpr int H_STAGES = 3;
+constexpr int H_STAGE = 4 * H_TILE;  // A_h, A_l, B_h, B_l
 constexpr int H_SMEM = H_STAGES * H_STAGE + 1024 + 256;
 constexpr int H_CHUNK_DEFAULT = 2;  // stages per promotion chunk (128 K)
 
@@ -601,11 +600,9 @@ __global__ void __launch_bounds__(32 * P_WARPS, 1) gemm_f16split_2sm_kernel(
         const uint32_t fb = full0 + (uint32_t)(s * sizeof(uint64_t));
         const int kc = kt * H_BK;
         tma_load_2d_2sm(st + 0 * H_TILE, &tm_ah, fb, kc, a_row0);
-        tma_load_2d_2sm(st + 1 * H_TILE, &tm_ax, fb, 2 * kc, a_row0);
-        tma_load_2d_2sm(st + 2 * H_TILE, &tm_ax, fb, 2 * kc + H_BK, a_row0);
-        tma_load_2d_2sm(st + 3 * H_TILE, &tm_bh, fb, kc, b_row0);
-        tma_load_2d_2sm(st + 4 * H_TILE, &tm_bx, fb, 2 * kc, b_row0);
-        tma_load_2d_2sm(st + 5 * H_TILE, &tm_bx, fb, 2 * kc + H_BK, b_row0);
+        tma_load_2d_2sm(st + 1 * H_TILE, &tm_ax, fb, kc, a_row0);  // A_l
+        tma_load_2d_2sm(st + 2 * H_TILE, &tm_bh, fb, kc, b_row0);
+        tma_load_2d_2sm(st + 3 * H_TILE, &tm_bx, fb, kc, b_row0);  // B_l
       }
     }
   } else if (warp == 1) {
@@ -622,15 +619,14 @@ __global__ void __launch_bounds__(32 * P_WARPS, 1) gemm_f16split_2sm_kernel(
         const uint32_t acc = tmem + (uint32_t)(q * 256);
 #pragma unroll
         for (int kk = 0; kk < H_BK / 16; ++kk) {
-          // h.h over elements 16kk .. 16kk+15 (32 bytes of the 128-byte swizzle row)
-          umma2_bf16(acc, umma_desc_sw128(base + 0 * H_TILE + kk * 32), umma_desc_sw128(base + 3 * H_TILE + kk * 32),
-                     idesc, !(first && kk == 0));
-#pragma unroll
-          for (int g = 2 * kk; g < 2 * kk + 2; ++g) {  // pair groups of 8 elements: h_x.l_y + l_x.h_y
-            const uint32_t off = (uint32_t)((g >> 2) * H_TILE + (g & 3) * 32);
-            umma2_bf16(acc, umma_desc_sw128(base + 1 * H_TILE + off), umma_desc_sw128(base + 4 * H_TILE + off),
-                       idesc, 1);
-          }
+          // elements 16kk .. 16kk+15 (32 bytes of the 128-byte swizzle row): h.h' + h.l' + l.h'
+          const uint64_t dah = umma_desc_sw128(base + 0 * H_TILE + kk * 32);
+          const uint64_t dal = umma_desc_sw128(base + 1 * H_TILE + kk * 32);
+          const uint64_t dbh = umma_desc_sw128(base + 2 * H_TILE + kk * 32);
+          const uint64_t dbl = umma_desc_sw128(base + 3 * H_TILE + kk * 32);
+          umma2_bf16(acc, dah, dbh, idesc, !(first && kk == 0));
+          umma2_bf16(acc, dah, dbl, idesc, 1);
+          umma2_bf16(acc, dal, dbh, idesc, 1);
         }
         umma2_commit_mc(&empty[s]);
         if ((kt % H_CHUNK) == H_CHUNK - 1 || kt == ktiles - 1) umma2_commit_mc(&acc_full[q]);
@@ -766,7 +762,7 @@ __global__ void __launch_bounds__(256) gather_a_split_kernel(const T* __restrict
   if constexpr (F16) {
     const float f2 = pow2f(kexp[b * w_stride + t] - gshift[b]);
     __half* oh = reinterpret_cast<__half*>(ahi) + (b * m) * W + t;
-    __half* ox = reinterpret_cast<__half*>(ax) + (b * m) * 2 * W + pair_pos(t);
+    __half* ol = reinterpret_cast<__half*>(ax) + (b * m) * W + t;  // the low halves, same layout
 #pragma unroll 8
     for (int64_t h = h0; h < h1; ++h) {
       float x;
@@ -775,8 +771,7 @@ __global__ void __launch_bounds__(256) gather_a_split_kernel(const T* __restrict
       float hi, lo;
       split_f16(__fmul_rn(x, f2), hi, lo);
       oh[h * W] = __float2half_rn(hi);
-      ox[h * 2 * W] = __float2half_rn(hi);  // [h_x | l_x]
-      ox[h * 2 * W + 8] = __float2half_rn(lo);
+      ol[h * W] = __float2half_rn(lo);
     }
   } else {
     float* oh = ahi + (b * m) * W + t;
@@ -878,7 +873,11 @@ __global__ void __launch_bounds__(256) gather_bt_split_kernel(const T* __restric
     if (f < p) {
       const int64_t row = b * p + f;
       if constexpr (F16) {
-        if (t < W) reinterpret_cast<__half*>(bhi)[row * W + t] = __float2half_rn(sh[tx][i]);
+        if (t < W) {
+          reinterpret_cast<__half*>(bhi)[row * W + t] = __float2half_rn(sh[tx][i]);
+          reinterpret_cast<__half*>(bx)[row * W + t] = __float2half_rn(sl[tx][i]);  // the low halves
+        }
+        continue;
       } else {
         if (t < W) bhi[row * W + t] = sh[tx][i];
       }
@@ -1798,9 +1797,9 @@ extern "C" int bmm_gemm_f16split_dk(const void* a_h, const void* a_x, const void
   CUtensorMap ma_h, ma_x, mb_h, mb_x;
   int rc;
   if ((rc = make_map_f16(&ma_h, a_h, batch * m, k_max)) != BMM_OK) return rc;
-  if ((rc = make_map_f16(&ma_x, a_x, batch * m, 2 * k_max)) != BMM_OK) return rc;
+  if ((rc = make_map_f16(&ma_x, a_x, batch * m, k_max)) != BMM_OK) return rc;
   if ((rc = make_map_f16(&mb_h, b_h, batch * nc, k_max)) != BMM_OK) return rc;
-  if ((rc = make_map_f16(&mb_x, b_x, batch * nc, 2 * k_max)) != BMM_OK) return rc;
+  if ((rc = make_map_f16(&mb_x, b_x, batch * nc, k_max)) != BMM_OK) return rc;
   // promotion chunk: 128 K (default) or 256 K (BMM_F16_CHUNK=4: half the TMEM drain traffic)
   static const int chunk = [] {
     const char* e = getenv("BMM_F16_CHUNK");

@@ -1,0 +1,10 @@
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_tf32.py tests/test_gpu_cfg4.py tests/test_gpu_sharded.py -x -q -m gpu > gpurun_out/bh_pytest.log 2>&1; echo "pytest rc=$?"
+tail -5 gpurun_out/bh_pytest.log
+timeout 1500 python bench.py > gpurun_out/bh_bench_cfg4.json 2> gpurun_out/bh_bench_cfg4.err; echo "bench rc=$?"
+tail -3 gpurun_out/bh_bench_cfg4.err
+python - <<'PY'
+import json
+d=json.loads(open('gpurun_out/bh_bench_cfg4.json').read().strip().splitlines()[-1])
+print(d['value'], d['kernel_ms'], d['clocks'], d['parity'].get('cd_rel_err_vs_f64_same_sketch'), d['e2e']['value'])
+PY
