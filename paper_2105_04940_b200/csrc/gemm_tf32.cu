@@ -1800,10 +1800,10 @@ extern "C" int bmm_gemm_f16split_dk(const void* a_h, const void* a_x, const void
   if ((rc = make_map_f16(&ma_x, a_x, batch * m, k_max)) != BMM_OK) return rc;
   if ((rc = make_map_f16(&mb_h, b_h, batch * nc, k_max)) != BMM_OK) return rc;
   if ((rc = make_map_f16(&mb_x, b_x, batch * nc, k_max)) != BMM_OK) return rc;
-  // promotion chunk: 128 K (default) or 256 K (BMM_F16_CHUNK=4: half the TMEM drain traffic)
+  // promotion chunk: 256 K (default: half the TMEM drain traffic) or 128 K (BMM_F16_CHUNK=2)
   static const int chunk = [] {
     const char* e = getenv("BMM_F16_CHUNK");
-    return e ? atoi(e) : H_CHUNK_DEFAULT;
+    return e ? atoi(e) : 4;  // 256 K per promotion: 35.0 vs 36.2 ms at config 4, error 1.0e-6 vs 6.1e-7
   }();
   auto kern = chunk == 4 ? gemm_f16split_2sm_kernel<4> : gemm_f16split_2sm_kernel<H_CHUNK_DEFAULT>;
   static bool attr = false;
@@ -1827,8 +1827,8 @@ extern "C" int bmm_gemm_f16split_dk(const void* a_h, const void* a_x, const void
   lc.numAttrs = 1;
   static const int group_m = [] {
     const char* e = getenv("BMM_F16_GROUP_M");  // A/B switch: pair-tile rows per raster group
-    const int v = e ? atoi(e) : 8;
-    return v >= 1 ? v : 8;
+    const int v = e ? atoi(e) : 4;  // config 4 (profiles/r2bj_gemm_sweep.txt): 4 -> 36.2 ms, 8 -> 39, 16 -> 41
+    return v >= 1 ? v : 4;
   }();
   if (cudaLaunchKernelEx(&lc, kern, ma_h, ma_x, mb_h, mb_x, m, nc, k_max, out, ldo, strideO, k_dev, gshift,
                          group_m) != cudaSuccess) {
