@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from pathlib import Path
 
 import numpy as np
@@ -248,6 +249,7 @@ def f64(values) -> torch.Tensor:
 _BIG = 48 << 20
 _CHUNK = 64 << 20
 _stage = None
+_stage_lock = threading.Lock()  # one staged transfer at a time: the two pinned buffers are shared
 
 
 def _staging():
@@ -275,6 +277,11 @@ def host(t: torch.Tensor) -> np.ndarray:
     nbytes = t.numel() * t.element_size()
     if t.device.type != "cuda" or nbytes < _BIG or not t.is_contiguous():
         return t.cpu().numpy()
+    with _stage_lock:
+        return _host_staged(t, nbytes)
+
+
+def _host_staged(t: torch.Tensor, nbytes: int) -> np.ndarray:
     sg = _staging()
     out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
     dst = out.reshape(-1).view(np.uint8)
@@ -307,6 +314,11 @@ def _upload(a: np.ndarray) -> torch.Tensor:
     th = torch.from_numpy(a)
     if nbytes < _BIG or th.is_pinned():
         return th.to(dev, non_blocking=False)
+    with _stage_lock:
+        return _upload_staged(a, th, dev, nbytes)
+
+
+def _upload_staged(a: np.ndarray, th: torch.Tensor, dev, nbytes: int) -> torch.Tensor:
     sg = _staging()
     out = torch.empty(a.shape, dtype=th.dtype, device=dev)
     dst = out.reshape(-1).view(torch.uint8)
