@@ -458,12 +458,13 @@ int bmm_gemm_f32split(const float* a_hi, const void* a_x, const float* b_hi, con
  * powers of two: the balanced exponents keep both operands inside fp16's range).
  * bmm_balance_f16: kexp from the norm pass (colsq/rowsq, n_stride per problem)
  *   and the sketch scales, gshift per problem so that |y| < 2^15; 0 past k_dev.
- * bmm_gather_f16split_dk: a_h (fp16, rows x W), a_x (fp16 pairs [h|l] per 8
- *   columns, rows x 2W), b_h / b_x for D^T with pairs [l|h]; columns zero-padded
- *   to a multiple of 64 past k_dev (the contraction's K step).  Buffers of the
- *   float32 split (a_hi/a_x/b_hi/b_x) are large enough.
+ * bmm_gather_f16split_dk: a_h and a_x = the high and the low fp16 halves of C
+ *   (rows x W each), b_h / b_x likewise for D^T; columns zero-padded to a multiple
+ *   of 64 past k_dev (the contraction's K step).  4 operand bytes per sketch
+ *   element; buffers of the float32 split (a_hi/a_x/b_hi/b_x) are large enough.
  * bmm_gemm_f16split_dk: out[b] = 2^(2 gshift[b]) * (a . b^T) on CTA pairs
- *   (tcgen05.mma.cta_group::2, 256 x 256 tiles), 3 kind::f16 MMAs per 16 K.    */
+ *   (tcgen05.mma.cta_group::2, 256 x 256 tiles), per 16 K the three kind::f16
+ *   MMAs h.h' + h.l' + l.h'.                                                   */
 int bmm_balance_f16(const double* colsq, const double* rowsq, int64_t n_stride, const int64_t* column,
                     const double* scale, int64_t w, int64_t w_stride, const int64_t* k_dev, int64_t batch,
                     int32_t* kexp, int32_t* gshift, void* stream);
