@@ -32,5 +32,5 @@ for i in range(6):
     evs[i + 1].record()
 torch.cuda.synchronize()
 ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(6)]
-print(f"GROUP_M={os.environ.get('BMM_F16_GROUP_M', '8')} CHUNK={os.environ.get('BMM_F16_CHUNK', '2')}: "
+print(f"GROUP_M={os.environ.get('BMM_F16_GROUP_M', '4')} CHUNK={os.environ.get('BMM_F16_CHUNK', '4')}: "
       f"{' '.join(f'{x:.2f}' for x in ms)} ms", flush=True)
