@@ -164,3 +164,25 @@ def test_block_view_zero_copy():
         block_view(N, part, 0, "columns")
     with pytest.raises(IndexError):
         block_view(M, part, 3)
+
+
+@pytest.mark.parametrize("count", [1, 5, 50, 64, 4096])
+def test_advance_spawn_counter_equals_public_spawn(count):
+    """rng.spawn(K)'s only lasting effect on the caller's generator is the parent's child
+    counter (estimators.py:141,207; plan.py:456): the shortcut leaves the SeedSequence in the
+    state the public call leaves it in -- same counter, entropy, key and pool, same next
+    children -- for the first spawn and for a later one."""
+    from paper_2105_04940_b200.rng import advance_spawn_counter
+    a = np.random.SeedSequence(210504940, spawn_key=(2, 1, 7))
+    b = np.random.SeedSequence(210504940, spawn_key=(2, 1, 7))
+    for _ in range(2):
+        advance_spawn_counter(a, count)
+        b.spawn(count)
+        assert a.n_children_spawned == b.n_children_spawned
+        assert a.entropy == b.entropy and a.spawn_key == b.spawn_key and a.pool_size == b.pool_size
+        assert np.array_equal(a.pool, b.pool)
+        ca, cb = a.spawn(2), b.spawn(2)
+        for x, y in zip(ca, cb):
+            assert x.spawn_key == y.spawn_key and np.array_equal(x.generate_state(4), y.generate_state(4))
+    advance_spawn_counter(a, 0)
+    assert a.n_children_spawned == b.n_children_spawned
