@@ -4,6 +4,15 @@ pkg/tests -- against THIS package, with the module name ``blockmm`` aliased to
 ``paper_2105_04940_b200`` (and blockmm.matrix / .plan / .estimators to its
 modules).  Needs a GPU (the package has no CPU fallback).
 
+With ``--next`` the gate also runs the reference's tests of the SURVEY §8(f) rows:
+test_datagen.py (f3, f4: the default stream="numpy" reproduces the reference's
+instances) and the in-scope part of test_analysis.py (f1, f2: exact variance,
+expected squared error, relative_error, Clopper-Pearson, coverage counting, the
+normality diagnostic).  test_analysis.py also imports the closed-form bounds and
+the analytics CSV, which are OUT of scope: the runner
+gives those names placeholders that raise when called, so the module imports, and
+deselects the tests of the OUT functions by name (listed in OUT_TESTS).
+
 The reference's tests are not part of this repository.  To run the gate on the
 GPU box, stage them next to the repo first (a git-ignored directory that
 travels with gpurun):
@@ -28,17 +37,55 @@ def alias():
         sys.modules[f"blockmm.{sub}"] = importlib.import_module(f"paper_2105_04940_b200.{sub}")
 
 
+# names test_analysis.py imports that are OUT of scope here (closed-form bounds, analytics CSV)
+OUT_NAMES = ("AnalyticsRow", "BoundInputs", "bound_inputs_for_plan", "bounds_optimal_allocation",
+             "bounds_pilot_allocation", "bounds_score_allocation", "cancellation_stats", "write_analytics_csv")
+# ... and the tests that exercise them
+OUT_TESTS = ("cancellation", "test_bound", "test_bounds", "test_score_bound", "test_pilot_bound",
+             "closed_form_bound", "analytics_csv")
+
+
+def _out_of_scope(name):
+    def stub(*a, **k):
+        raise NotImplementedError(f"{name} is out of scope (SURVEY.md §2 / Appendix C)")
+    stub.__name__ = name
+    return stub
+
+
+def alias_next():
+    pkg = sys.modules["blockmm"]
+    added = []
+    for name in OUT_NAMES:
+        if not hasattr(pkg, name):
+            setattr(pkg, name, _out_of_scope(name))
+            added.append(name)
+    ana = sys.modules["blockmm.analysis"]
+    mc = importlib.import_module("paper_2105_04940_b200.montecarlo")
+    if not hasattr(ana, "_clopper_pearson"):
+        ana._clopper_pearson = mc.clopper_pearson  # analysis.py:328-340 lives in montecarlo.py here
+    if not hasattr(ana, "ANALYTICS_HEADER"):
+        ana.ANALYTICS_HEADER = ()
+    return added
+
+
 def main(argv):
-    stage = Path(argv[1] if len(argv) > 1 else ROOT / "conformance_stage").resolve()
-    files = [str(stage / f) for f in ("test_matrix.py", "test_plan.py", "test_estimators.py")]
+    args = [a for a in argv[1:] if not a.startswith("--")]
+    nxt = "--next" in argv
+    stage = Path(args[0] if args else ROOT / "conformance_stage").resolve()
+    names = ["test_matrix.py", "test_plan.py", "test_estimators.py"] + (["test_datagen.py", "test_analysis.py"] if nxt else [])
+    files = [str(stage / f) for f in names]
     missing = [f for f in files if not Path(f).exists()]
     if missing:
         print(f"reference tests not staged: {missing}")
         return 2
     alias()
+    extra = []
+    if nxt:
+        alias_next()
+        extra = ["-k", " and ".join(f"not {t}" for t in OUT_TESTS)]
     sys.path.insert(0, str(stage))
     return pytest.main([*files, "-q", "-rA", "-p", "no:cacheprovider", "--rootdir", str(stage),
-                        "-o", "addopts=", "--tb=short"])
+                        "-o", "addopts=", "--tb=short", *extra])
 
 
 if __name__ == "__main__":
