@@ -546,15 +546,16 @@ int bmm_exchange_sum_nccl(void* comm, int nranks, const double* partial, int64_t
  * and the CDF held in shared memory (plan.py:165-206, 242-421; estimators.py:34-44, 78,
  * 141).  Same device functions in the same order as the separate entries: every output is
  * bit-identical to theirs.  cum, last_support, diag, notes, states and (kexp, gshift) are
- * optional (NULL).  Needs bmm_plan_small_smem(n, K, W) <= 200 KiB and n, W < 65536;
- * BMM_E_UNSUPPORTED otherwise (callers then use the separate entries).                     */
+ * optional (NULL).  Needs blocks of at most 128 columns (max_len: one leaf of NumPy's pairwise
+ * sum per block), bmm_plan_small_smem(n, K, W) <= 200 KiB and n, W < 65536; BMM_E_UNSUPPORTED
+ * otherwise (callers then use the separate entries).                                        */
 int64_t bmm_plan_small_smem(int64_t n, int64_t K, int64_t W);
 /* diagnostics: later launches write 16 SM-clock stamps per problem (stage boundaries) to
  * `stamps` (batch x 16, device); NULL switches it off (tools/plan_small_probe.py)          */
 int bmm_plan_small_debug(long long* stamps);
 int bmm_plan_small(int rule, const double* colsq, const double* rowsq, int64_t n,
                    const int64_t* offsets, const int64_t* sizes, int64_t K, int64_t batch,
-                   const double* aux, const int64_t* c, int cap, const uint32_t* words,
+                   int64_t max_len, const double* aux, const int64_t* c, int cap, const uint32_t* words,
                    int64_t n_words, const int64_t* first_child, int64_t W, double* probs, double* s,
                    double* cum, int64_t* last_support, int64_t* budgets, int64_t* col_off,
                    int32_t* status, int64_t* diag, int32_t* notes, uint64_t* states,

@@ -103,7 +103,7 @@ SIGNATURES = {
                                _P, _I64, _P]),
     "bmm_plan_small_smem": (_I64, [_I64, _I64, _I64]),
     "bmm_plan_small_debug": (_I, [_P]),
-    "bmm_plan_small": (_I, [_I, _P, _P, _I64, _P, _P, _I64, _I64, _P, _P, _I, _P, _I64, _P, _I64] + [_P] * 18 + [_P]),
+    "bmm_plan_small": (_I, [_I, _P, _P, _I64, _P, _P, _I64, _I64, _I64, _P, _P, _I, _P, _I64, _P, _I64] + [_P] * 18 + [_P]),
     "bmm_gemm_f64_err_workspace": (_I64, [_I64, _I64, _I64, _I64]),
     "bmm_gemm_f64_err": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64,
                               _P, _P, _I64, _P]),

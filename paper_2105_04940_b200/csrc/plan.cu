@@ -1174,13 +1174,17 @@ extern "C" int bmm_plan_small_debug(long long* stamps) {
 }
 
 extern "C" int bmm_plan_small(int rule, const double* colsq, const double* rowsq, int64_t n, const int64_t* offsets,
-                              const int64_t* sizes, int64_t K, int64_t batch, const double* aux, const int64_t* c,
+                              const int64_t* sizes, int64_t K, int64_t batch, int64_t max_len, const double* aux,
+                              const int64_t* c,
                               int cap, const uint32_t* words, int64_t n_words, const int64_t* first_child, int64_t W,
                               double* probs, double* s, double* cum, int64_t* last_support, int64_t* budgets,
                               int64_t* col_off, int32_t* status, int64_t* diag, int32_t* notes, uint64_t* states,
                               int64_t* column, double* prob, double* scale, int64_t* k_column, double* k_scale,
                               int64_t* k_count, int32_t* kexp, int32_t* gshift, void* stream) {
-  BMM_REQUIRE(n >= 1 && K >= 1 && K <= n && batch >= 1 && W >= 1, BMM_E_ARG, "bmm_plan_small: bad shape");
+  BMM_REQUIRE(n >= 1 && K >= 1 && K <= n && batch >= 1 && W >= 1 && max_len >= 1, BMM_E_ARG,
+              "bmm_plan_small: bad shape");
+  BMM_REQUIRE(max_len <= 128, BMM_E_UNSUPPORTED,
+              "bmm_plan_small: blocks of at most 128 columns (one leaf of NumPy's pairwise sum per block)");
   BMM_REQUIRE(rule == BMM_RULE_ONC || rule == BMM_RULE_OPL, BMM_E_UNSUPPORTED,
               "bmm_plan_small: score-sum (ONC) and optimal (OPL) sizes only");
   BMM_REQUIRE(rule != BMM_RULE_OPL || aux != nullptr, BMM_E_ARG, "bmm_plan_small: OPL needs g_k^2");

@@ -570,7 +570,7 @@ class SketchPipeline:
         words, first = self._seedbuf["main"]
         bal = self.f16 or self.fused16
         self._c("bmm_plan_small", rule, P(self.colsq), P(self.rowsq), n, P(self.offsets), P(self.sizes_d), K, B,
-                P(aux) if aux is not None else None, P(self.c_arr), int(self.cap), words.data_ptr(), words.shape[1],
+                self.max_len, P(aux) if aux is not None else None, P(self.c_arr), int(self.cap), words.data_ptr(), words.shape[1],
                 first.data_ptr(), W, P(self.probs), P(self.s), None, P(self.last), P(self.budgets),
                 P(self.col_off), P(self.status), P(self.diag), P(self.notes), P(self.states), P(self.column),
                 P(self.prob), P(self.scale), P(self.k_column), P(self.k_scale), P(self.k_count),
