@@ -72,12 +72,15 @@ def _specs(m: int, p: int, cov_left, cov_right):
 
 
 def _chi_square_1(rng: np.random.Generator, n: int) -> np.ndarray:
-    """datagen.py:75-80: chi-square(1) draws, zeros redrawn -- the caller's Generator,
-    the reference's call sequence."""
+    """n chi-square(1) draws from the caller's Generator with exact zeros redrawn, in the
+    reference's call sequence (datagen.py:75-80: one more ``chisquare(1, #zeros)`` call per
+    round, the new values filling the zero positions in ascending order), so the generator
+    ends in the reference's state."""
     w = rng.chisquare(1.0, n)
-    while (w == 0.0).any():
-        zeros = w == 0.0
-        w[zeros] = rng.chisquare(1.0, int(zeros.sum()))
+    bad = np.flatnonzero(w == 0.0)
+    while bad.size:
+        w[bad] = rng.chisquare(1.0, bad.size)
+        bad = bad[w[bad] == 0.0]
     return w
 
 
