@@ -1643,14 +1643,16 @@ def run_cfg4(args):
                      "useful_fp32_tflops": sum(useful) / (gemm_tot * 1e-3) / 1e12,
                      "launch_ms": gemm_ms, "share_of_step": gemm_tot / ms_step,
                      "traffic": tr.get("gemm_f32split"), "traffic_src": tr.get("src")},
-        "roofline_norms": {"bound": "hbm", "kernel": "colsq_vec_kernel + rowsq_tma_kernel (K1)",
+        "roofline_norms": {"bound": "hbm", "kernel": "colsq_wide_kernel + rowsq_tma_kernel (K1)",
                            "achieved": norm_bytes / (norms_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                            "frac": norm_bytes / (norms_ms * 1e-3) / 1e9 / hbm_peak, "algorithmic_bytes": norm_bytes,
                            "colsq_ms": cs_ms, "rowsq_ms": rs_ms, "ms": norms_ms,
                            "ms_cool": norms_cool_ms,
                            "frac_cool": norm_bytes / (norms_cool_ms * 1e-3) / 1e9 / hbm_peak,
-                           "note": "ms / frac: timed after the step runs (SM clock power-capped by the GEMMs, "
-                                   "where the float64 chains' issue rate limits it); ms_cool: before them",
+                           "note": "ms / frac: timed right after the step's contractions (SM clock power-capped: "
+                                   "the kernels' TMA rings stream ~29 B per clock per SM, the HBM peak only at full "
+                                   "clock; DESIGN.md section 8); ms_cool: before them, after the data generation; on "
+                                   "a rested GPU 5.1-5.3 ms = 0.99 (tools/cfg4_norms_probe.py)",
                            "traffic": tr.get("norms"), "traffic_src": tr.get("src"),
                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (a copy: read + write)"},
         "roofline_gram": {"bound": "tensor", "kernel": "segsq_gram_kernel (OPL g_k^2 = <M^k'M^k, N_k N_k'>, DMMA)",
