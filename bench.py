@@ -1035,8 +1035,10 @@ def run_device(args):
     keys = np.arange(lo, hi)
     # the batch in waves on several streams of the one graph: a wave's latency-bound planning
     # kernels run beside another wave's HBM-bound norm pass / gather-contraction
-    # (tools/cfg5_waves_probe.py; BMM_CFG5_WAVES=0 keeps one batch)
-    wv = os.environ.get("BMM_CFG5_WAVES", "1024,4")
+    # (tools/cfg5_waves_probe.py; BMM_CFG5_WAVES=0 keeps one batch).  With the one-launch plan the
+    # waves cost little, and more of them overlap better: 256 x 16 streams 8.91-8.92 ms, 512 x 8
+    # 8.94-8.98, 1024 x 4 8.98-9.02, 128 x 32 9.12, one batch 9.67 (profiles/r2by_waves_plan_small.txt)
+    wv = os.environ.get("BMM_CFG5_WAVES", "256,16")
     waves = tuple(int(x) for x in wv.split(",")) if wv not in ("", "0") else None
     if waves is not None and B > waves[0]:
         pipe.set_waves(*waves)
